@@ -1,0 +1,137 @@
+/*
+ * runlab_gpu.h -- C ABI of the B200 (sm_100a) labeling/analysis path.
+ *
+ * Drop-in boundary for the reference's C++ entry points (paths relative to
+ * /root/reference/proj/include/runlab/):
+ *
+ *   rl_label()          replaces  label_image        labeling.hpp:336-339
+ *                        and      timed_label_image  labeling.hpp:343-348 (phase_ms below)
+ *                        and the filled image of     binarize_labels    labeling.hpp:354-360
+ *                        (as used by `runlab fill`, tools/runlab.cpp:128-137)
+ *   rl_label_device()   the same pipeline on device-resident batches (no host copies)
+ *   rl_result fields    feed components/holes/adjacency_tree/euler_number
+ *                                                    analysis.hpp:23-79
+ *
+ * POD types only (no C++/torch types), so the reference (namespace runlab) and this
+ * library can be linked into one test binary without an ODR clash.  The C++ drop-in
+ * header include/runlab/gpu_labeling.hpp rebuilds runlab::LabelingResult from it.
+ *
+ * Canonical numbering: every component (foreground or background) gets the rank of its
+ * raster-first pixel; id 0 is the exterior background.  This equals the ascending order
+ * of the reference's root labels (tables.hpp:68-76) and the oracle's ids
+ * (oracle.hpp:20-23).
+ */
+#ifndef RUNLAB_GPU_H
+#define RUNLAB_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes (mapped to the reference's exception types by the C++ drop-in). */
+#define RL_OK 0
+#define RL_EINVAL 1    /* std::invalid_argument (labeling.hpp:271-273) */
+#define RL_ELOGIC 2    /* std::logic_error */
+#define RL_EOVERFLOW 3 /* std::overflow_error (features.hpp:37-39) */
+#define RL_ECUDA 4     /* std::runtime_error */
+#define RL_ENOMEM 5    /* std::bad_alloc */
+#define RL_EINTERNAL 6 /* std::runtime_error (invariant violated on device) */
+
+/* types.hpp:18-21 */
+#define RL_FG8_BG4 0
+#define RL_FG4_BG8 1
+
+/* labeling.hpp:20-27 LabelingConfig */
+typedef struct rl_config {
+    int32_t connectivity; /* RL_FG8_BG4 (default) or RL_FG4_BG8 */
+    int32_t fill_holes;
+    int32_t compute_features;
+    int32_t relabel;
+    int32_t densify_labels;
+    int32_t compute_euler;
+} rl_config;
+
+/* features.hpp:14-25 FeatureAccumulator (40 bytes; empty = s 0, bbox INT32_MAX/MIN) */
+typedef struct rl_features {
+    int64_t s, sx, sy;
+    int32_t row_min, row_max, col_min, col_max;
+} rl_features;
+
+/* One pre-fill component (48 bytes). */
+typedef struct rl_component {
+    rl_features f;
+    uint32_t parent; /* canonical id of the surrounding component; UINT32_MAX for id 0 */
+    uint32_t flags;  /* bit 0: foreground */
+} rl_component;
+
+/* Per-phase device times of the last call (CUDA events), cf. StepTimes labeling.hpp:253-259. */
+typedef struct rl_times {
+    float analyze_ms;  /* K1a tile scan: segments + tile union-find + border tables */
+    float merge_ms;    /* cross-tile union, closure, canonical ids, tree, fill fold */
+    float emit_ms;     /* K1b second tile pass: records, filled image, labels */
+    float total_ms;
+} rl_times;
+
+/* Result of one call over n_images images of identical size, library-allocated
+ * (free with rl_result_free).  Per-image arrays are concatenated; image i owns
+ * [comp_offset[i], comp_offset[i+1]) of comps/top/filled and pixels
+ * [i*w*h, (i+1)*w*h) of filled_image/labels. */
+typedef struct rl_result {
+    int32_t width, height, n_images;
+    int64_t* n_components; /* [n_images] C_pre, exterior included */
+    int64_t* n_fg;         /* [n_images] foreground components, pre-fill */
+    int64_t* n_holes;      /* [n_images] holes, pre-fill */
+    int64_t* euler;        /* [n_images] n_fg - n_holes */
+    int64_t* n_survivors;  /* [n_images] C_post: components left after hole filling */
+    int64_t* comp_offset;  /* [n_images + 1] */
+    rl_component* comps;   /* pre-fill records, canonical order */
+    uint32_t* top;         /* post-fill root (depth-1 ancestor) of every component */
+    rl_features* filled;   /* post-fill features; meaningful where top[i] == i */
+    uint8_t* filled_image; /* hole-filled image (binarize_labels after fill) */
+    uint32_t* labels;      /* per-pixel label image when cfg.relabel, else NULL */
+    rl_times times;
+} rl_result;
+
+typedef struct rl_ctx rl_ctx;
+
+/* One context = one device + one CUDA stream + workspace. One context per host thread. */
+rl_ctx* rl_create(int device);
+void rl_destroy(rl_ctx* ctx);
+const char* rl_last_error(const rl_ctx* ctx);
+
+/* Host-buffer entry point (the drop-in): copies the images in, runs the pipeline, copies
+ * every requested output back.  pixels: n_images * height * width bytes, values 0/1. */
+int rl_label(rl_ctx* ctx, const uint8_t* pixels, int32_t width, int32_t height,
+             int32_t n_images, const rl_config* cfg, rl_result* out);
+void rl_result_free(rl_result* r);
+
+/* Device-resident entry point: d_pixels is a device pointer; the pipeline is enqueued on
+ * the context stream and outputs stay in the context's device buffers (see rl_device_*).
+ * Returns after enqueueing; call rl_sync() before reading.  If a capacity estimate was
+ * exceeded the call re-runs internally after growing (host sync in that case only). */
+int rl_label_device(rl_ctx* ctx, const uint8_t* d_pixels, int32_t width, int32_t height,
+                    int32_t n_images, const rl_config* cfg);
+int rl_sync(rl_ctx* ctx);
+/* Copies the results of the last rl_label_device() to host memory (like rl_label). */
+int rl_fetch(rl_ctx* ctx, rl_result* out);
+/* Device views of the last call's outputs (valid until the next call). */
+void* rl_device_filled_image(rl_ctx* ctx);
+void* rl_device_labels(rl_ctx* ctx);
+void* rl_device_comps(rl_ctx* ctx);
+/* Stream the context enqueues on (cudaStream_t). */
+void* rl_stream(rl_ctx* ctx);
+/* Bind the context to an external stream (e.g. torch's current stream); NULL = own. */
+int rl_set_stream(rl_ctx* ctx, void* stream);
+/* Number of kernel launches the last pipeline enqueued. */
+int rl_last_launch_count(const rl_ctx* ctx);
+
+/* Tile geometry used by the kernels (for DESIGN/roofline bookkeeping). */
+void rl_tile_shape(int32_t* tile_h, int32_t* tile_w);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

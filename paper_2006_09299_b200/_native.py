@@ -1,0 +1,89 @@
+"""ctypes binding of the C ABI in ``include/runlab_gpu.h`` (``librunlab_gpu.so``).
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc, sm_100a).  There is no
+CPU fallback: if the library or a GPU is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librunlab_gpu.so")
+
+RL_OK, RL_EINVAL, RL_ELOGIC, RL_EOVERFLOW, RL_ECUDA, RL_ENOMEM, RL_EINTERNAL = range(7)
+
+EXPORTED_SYMBOLS = (
+    "rl_create", "rl_destroy", "rl_last_error", "rl_label", "rl_result_free", "rl_label_device",
+    "rl_sync", "rl_fetch", "rl_device_filled_image", "rl_device_labels", "rl_device_comps",
+    "rl_stream", "rl_set_stream", "rl_last_launch_count", "rl_tile_shape",
+)
+
+FEATURE_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),
+                          ("row_max", "<i4"), ("col_min", "<i4"), ("col_max", "<i4")])
+COMPONENT_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),
+                            ("row_max", "<i4"), ("col_min", "<i4"), ("col_max", "<i4"),
+                            ("parent", "<u4"), ("flags", "<u4")])
+
+
+class RlConfig(C.Structure):
+    _fields_ = [("connectivity", C.c_int32), ("fill_holes", C.c_int32),
+                ("compute_features", C.c_int32), ("relabel", C.c_int32),
+                ("densify_labels", C.c_int32), ("compute_euler", C.c_int32)]
+
+
+class RlTimes(C.Structure):
+    _fields_ = [("analyze_ms", C.c_float), ("merge_ms", C.c_float), ("emit_ms", C.c_float),
+                ("total_ms", C.c_float)]
+
+
+class RlResult(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("n_images", C.c_int32),
+                ("n_components", C.c_void_p), ("n_fg", C.c_void_p), ("n_holes", C.c_void_p),
+                ("euler", C.c_void_p), ("n_survivors", C.c_void_p), ("comp_offset", C.c_void_p),
+                ("comps", C.c_void_p), ("top", C.c_void_p), ("filled", C.c_void_p),
+                ("filled_image", C.c_void_p), ("labels", C.c_void_p), ("times", RlTimes)]
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load librunlab_gpu.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() first "
+                           "(the CUDA path has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    L.rl_create.restype = C.c_void_p
+    L.rl_create.argtypes = [C.c_int]
+    L.rl_destroy.argtypes = [C.c_void_p]
+    L.rl_last_error.restype = C.c_char_p
+    L.rl_last_error.argtypes = [C.c_void_p]
+    L.rl_label.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                           C.POINTER(RlConfig), C.POINTER(RlResult)]
+    L.rl_result_free.argtypes = [C.POINTER(RlResult)]
+    L.rl_label_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                  C.POINTER(RlConfig)]
+    L.rl_sync.argtypes = [C.c_void_p]
+    L.rl_fetch.argtypes = [C.c_void_p, C.POINTER(RlResult)]
+    for name in ("rl_device_filled_image", "rl_device_labels", "rl_device_comps", "rl_stream"):
+        getattr(L, name).restype = C.c_void_p
+        getattr(L, name).argtypes = [C.c_void_p]
+    L.rl_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+    L.rl_last_launch_count.argtypes = [C.c_void_p]
+    L.rl_tile_shape.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    _lib = L
+    return L
+
+
+def copy_out(ptr: int, dtype, n: int) -> np.ndarray:
+    dtype = np.dtype(dtype)
+    if n == 0 or not ptr:
+        return np.zeros(n, dtype=dtype)
+    buf = (C.c_char * (n * dtype.itemsize)).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype).copy()

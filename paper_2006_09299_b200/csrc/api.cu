@@ -1,0 +1,477 @@
+// api.cu -- host orchestration and the extern "C" ABI (include/runlab_gpu.h).
+//
+// One rl_ctx = one device, one stream, a grow-only device workspace and events.  A call
+// enqueues the whole pipeline (kernels.cu) on the context stream with no host sync in the
+// middle; capacity estimates for border nodes and components are checked on device and,
+// if exceeded, the call is re-run once after growing (the counters say by how much).
+//
+// Reference boundary: runlab::label_image / timed_label_image (labeling.hpp:336-348) and
+// binarize_labels (labeling.hpp:354-360); error mapping per labeling.hpp:271-273.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+#include "runlab_gpu.h"
+
+namespace rlg {
+size_t analyze_smem();
+size_t emit_smem();
+cudaError_t configure_kernels();
+void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s);
+void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
+void launch_resolve(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
+void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
+void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
+void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
+void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s);
+void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
+                       cudaStream_t s, int sms);
+void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, const uint64_t* cbase,
+                  cudaStream_t s, int sms);
+}  // namespace rlg
+
+using namespace rlg;
+
+namespace {
+
+// per-image summary gathered on device after a run: [0] comp base (canonical offset),
+// [1] C_pre, [2] n_fg, [3] C_post
+__global__ void k_summary(Geo g, Ws ws, uint64_t* cbase, int64_t* summ) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > g.B) return;
+    const int64_t idx = (int64_t)b * g.H * g.ntx;
+    const uint64_t base = (uint64_t)ws.off[idx] + (uint64_t)b;
+    cbase[b] = base;
+    if (b < g.B) {
+        const uint64_t next = (uint64_t)ws.off[idx + (int64_t)g.H * g.ntx] + (uint64_t)b + 1u;
+        summ[4 * b + 0] = (int64_t)base;
+        summ[4 * b + 1] = (int64_t)(next - base);
+        summ[4 * b + 2] = (int64_t)ws.img_fg[b];
+        summ[4 * b + 3] = (int64_t)ws.img_surv[b];
+    } else {
+        summ[4 * b + 0] = (int64_t)base;  // total components
+        summ[4 * b + 1] = (int64_t)ws.counters[0];
+        summ[4 * b + 2] = (int64_t)ws.counters[1];
+        summ[4 * b + 3] = 0;
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct rl_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // workspace
+    DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
+    DevBuf cnt, off, counters, img_fg, img_surv, comps, top, filled, filled_img, labels, pix;
+    DevBuf cub_tmp, cbase, summ, rank, flag;
+    uint32_t cap_nodes = 0;
+    uint64_t cap_comps = 0;
+    // pinned host mirror of the summary
+    int64_t* h_summ = nullptr;
+    size_t h_summ_n = 0;
+    // last call
+    Geo geo{};
+    Ws ws{};
+    rl_config cfg{};
+    const uint8_t* last_pix = nullptr;
+    int launches = 0;
+    bool have_result = false;
+};
+
+namespace {
+
+int set_err(rl_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_fail(rl_ctx* c, cudaError_t e, const char* what) {
+    return set_err(c, RL_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool ensure(DevBuf& b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return true;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    const size_t want = bytes + bytes / 8;  // some headroom against regrowth
+    if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    b.bytes = want;
+    return true;
+}
+
+template <class T>
+T* P(DevBuf& b) {
+    return static_cast<T*>(b.p);
+}
+
+int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cfg) {
+    if (!ctx) return RL_EINVAL;
+    if (!cfg) return set_err(ctx, RL_EINVAL, "null config");
+    if (w < 1 || h < 1 || n < 1) return set_err(ctx, RL_EINVAL, "image must be at least 1x1 and n_images >= 1");
+    if (cfg->densify_labels && !cfg->relabel)
+        return set_err(ctx, RL_EINVAL, "label_image: densify_labels requires relabel");
+    if (cfg->connectivity != RL_FG8_BG4 && cfg->connectivity != RL_FG4_BG8)
+        return set_err(ctx, RL_EINVAL, "unknown connectivity");
+    // int64 feature sums: Sx <= P * W must stay below 2^63 (features.hpp:37-39)
+    const double P = (double)w * (double)h;
+    if (P * (double)std::max(w, h) >= 9.2e18) return set_err(ctx, RL_EOVERFLOW, "feature accumulator overflow");
+    if (P * n >= 4.0e9 * 64) return set_err(ctx, RL_EINVAL, "batch too large");
+    if ((double)n * h * ((w + TW - 1) / TW) >= 4.0e9) return set_err(ctx, RL_EINVAL, "batch too large");
+    return RL_OK;
+}
+
+// (Re)build geometry, grow the workspace, enqueue the pipeline.
+int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg) {
+    Geo g{};
+    g.W = W;
+    g.H = H;
+    g.B = B;
+    g.ntx = (W + TW - 1) / TW;
+    g.nty = (H + TH - 1) / TH;
+    g.tpi = g.ntx * g.nty;
+    const int64_t ntiles = (int64_t)g.tpi * B;
+    if (ntiles >= (1ll << 31)) return set_err(ctx, RL_EINVAL, "too many tiles");
+    g.ntiles = (int32_t)ntiles;
+    g.flip = cfg->connectivity == RL_FG4_BG8 ? 1 : 0;
+    g.P = (int64_t)W * H;
+    g.vec_ok = ((W % 16) == 0 && (reinterpret_cast<uintptr_t>(dpix) % 16) == 0) ? 1 : 0;
+    g.label_mode = cfg->relabel ? (cfg->fill_holes ? 2 : 1) : 0;
+
+    const int64_t ncnt = (int64_t)B * H * g.ntx + 1;
+    if (ctx->cap_nodes == 0) ctx->cap_nodes = (uint32_t)std::min<int64_t>(std::max<int64_t>(ntiles * 96, 4096), 0xF0000000ll);
+    if (ctx->cap_comps == 0) ctx->cap_comps = (uint64_t)std::max<int64_t>(g.P * B / 16, 4096);
+    const uint64_t nn = (uint64_t)B + ctx->cap_nodes;
+    bool ok = ensure(ctx->bits, (size_t)ntiles * NW * 4) && ensure(ctx->tbase, (size_t)ntiles * 4) &&
+              ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->perim, (size_t)ntiles * PERIM * 2) &&
+              ensure(ctx->uf, nn * 4) && ensure(ctx->nkey, nn * 8) && ensure(ctx->nmin, nn * 8) &&
+              ensure(ctx->nacc, nn * sizeof(Acc)) && ensure(ctx->nrec, nn * sizeof(NodeRec)) &&
+              ensure(ctx->nrep, nn) && ensure(ctx->nrootcid, nn * 4) && ensure(ctx->nparent, nn * 4) &&
+              ensure(ctx->nanccid, nn * 4) && ensure(ctx->cnt, (size_t)ncnt * 4) &&
+              ensure(ctx->off, (size_t)ncnt * 4) && ensure(ctx->counters, 64) &&
+              ensure(ctx->img_fg, (size_t)B * 4) && ensure(ctx->img_surv, (size_t)B * 4) &&
+              ensure(ctx->comps, ctx->cap_comps * sizeof(rl_component)) &&
+              ensure(ctx->top, ctx->cap_comps * 4) && ensure(ctx->filled, ctx->cap_comps * sizeof(Acc)) &&
+              ensure(ctx->filled_img, (size_t)(g.P * B)) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
+              ensure(ctx->summ, (size_t)(B + 1) * 32);
+    if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)(g.P * B) * 4);
+    if (!ok) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)ncnt);
+    size_t tmp2 = 0;
+    if (cfg->densify_labels && cfg->fill_holes)
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp2, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                      (int)std::min<uint64_t>(ctx->cap_comps + 1, 0x7FFFFFFF));
+    if (!ensure(ctx->cub_tmp, std::max(tmp, tmp2))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+
+    Ws ws{};
+    ws.bits = P<uint32_t>(ctx->bits);
+    ws.tbase = P<uint32_t>(ctx->tbase);
+    ws.tnb = P<uint32_t>(ctx->tnb);
+    ws.perim = P<uint16_t>(ctx->perim);
+    ws.uf = P<uint32_t>(ctx->uf);
+    ws.nkey = P<uint64_t>(ctx->nkey);
+    ws.nmin = P<uint64_t>(ctx->nmin);
+    ws.nacc = P<Acc>(ctx->nacc);
+    ws.nrec = P<NodeRec>(ctx->nrec);
+    ws.nrep = P<uint8_t>(ctx->nrep);
+    ws.nrootcid = P<uint32_t>(ctx->nrootcid);
+    ws.nparent = P<uint32_t>(ctx->nparent);
+    ws.nanccid = P<uint32_t>(ctx->nanccid);
+    ws.cnt = P<uint32_t>(ctx->cnt);
+    ws.off = P<uint32_t>(ctx->off);
+    ws.counters = P<uint32_t>(ctx->counters);
+    ws.img_fg = P<uint32_t>(ctx->img_fg);
+    ws.img_surv = P<uint32_t>(ctx->img_surv);
+    ws.cap_nodes = ctx->cap_nodes;
+    ws.cap_comps = ctx->cap_comps;
+    ws.comps = P<rl_component>(ctx->comps);
+    ws.top = P<uint32_t>(ctx->top);
+    ws.filled = P<Acc>(ctx->filled);
+    ws.filled_img = P<uint8_t>(ctx->filled_img);
+    ws.labels = g.label_mode ? P<uint32_t>(ctx->labels) : nullptr;
+
+    cudaStream_t s = ctx->stream;
+    int launches = 0;
+    cudaMemsetAsync(ws.counters, 0, 64, s);
+    cudaMemsetAsync(ws.img_fg, 0, (size_t)B * 4, s);
+    cudaMemsetAsync(ws.img_surv, 0, (size_t)B * 4, s);
+    cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
+    cudaEventRecord(ctx->ev[0], s);
+    launch_analyze(dpix, g, ws, s);
+    ++launches;
+    cudaEventRecord(ctx->ev[1], s);
+    launch_seams(g, ws, s, ctx->sms);
+    launches += (g.nty > 1) + (g.ntx > 1);
+    const int64_t hint = (int64_t)ctx->cap_nodes;
+    launch_resolve(g, ws, s, ctx->sms, hint);
+    launch_reps(g, ws, s, ctx->sms, hint);
+    cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ws.cnt, ws.off, (int)ncnt, s);
+    launch_cids(g, ws, s, ctx->sms);
+    launch_tree(g, ws, s, ctx->sms, hint);
+    launches += 2 + 1 + 1 + 3;
+    cudaEventRecord(ctx->ev[2], s);
+    launch_emit(g, ws, s);
+    ++launches;
+    k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));
+    ++launches;
+    if (cfg->densify_labels && cfg->fill_holes && g.label_mode) {
+        // densified post-fill ids: rank of each survivor inside its image (labeling.hpp:231-236)
+        // total components is bounded by cap_comps; flags over [0, cap) are computed for the
+        // prefix that is in use (the remap only reads ranks of survivors).
+        const uint64_t total = ctx->cap_comps;
+        if (!ensure(ctx->rank, (total + 1) * 4) || !ensure(ctx->flag, (total + 1) * 4))
+            return set_err(ctx, RL_ENOMEM, "device allocation failed");
+        launch_surv_flags(ws.top, P<uint64_t>(ctx->cbase), B, total, P<uint32_t>(ctx->flag), s, ctx->sms);
+        size_t t2 = ctx->cub_tmp.bytes;
+        cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t2, P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank),
+                                      (int)std::min<uint64_t>(total + 1, 0x7FFFFFFF), s);
+        launch_remap(ws.labels, g.P, B, P<uint32_t>(ctx->rank), P<uint64_t>(ctx->cbase), s, ctx->sms);
+        launches += 3;
+    }
+    cudaEventRecord(ctx->ev[3], s);
+    const size_t sn = (size_t)(B + 1) * 4;
+    if (ctx->h_summ_n < sn) {
+        if (ctx->h_summ) cudaFreeHost(ctx->h_summ);
+        ctx->h_summ = nullptr;
+        if (cudaMallocHost(&ctx->h_summ, sn * 8) != cudaSuccess) return set_err(ctx, RL_ENOMEM, "pinned alloc failed");
+        ctx->h_summ_n = sn;
+    }
+    cudaMemcpyAsync(ctx->h_summ, ctx->summ.p, sn * 8, cudaMemcpyDeviceToHost, s);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "launch");
+    ctx->geo = g;
+    ctx->ws = ws;
+    ctx->cfg = *cfg;
+    ctx->last_pix = dpix;
+    ctx->launches = launches;
+    ctx->have_result = true;
+    return RL_OK;
+}
+
+// Wait for the last enqueue; on capacity overflow grow and re-run (synchronously).
+int finish(rl_ctx* ctx) {
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "pipeline");
+        const int B = ctx->geo.B;
+        const int64_t* tail = ctx->h_summ + 4 * B;
+        const uint64_t total_comps = (uint64_t)tail[0];
+        const uint64_t nodes = (uint64_t)tail[1];
+        const uint32_t errs = (uint32_t)tail[2];
+        bool grow = false;
+        if (errs & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (tree reference)");
+        if (errs & ERR_NODE_CAP) {
+            ctx->cap_nodes = (uint32_t)std::min<uint64_t>(nodes + nodes / 4 + 1024, 0xF0000000ull);
+            grow = true;
+        } else if (total_comps > ctx->cap_comps) {
+            ctx->cap_comps = total_comps + total_comps / 8 + 1024;
+            grow = true;
+        }
+        if (!grow) return RL_OK;
+        const rl_config cfg = ctx->cfg;
+        const int rc = enqueue(ctx, ctx->last_pix, ctx->geo.W, ctx->geo.H, ctx->geo.B, &cfg);
+        if (rc) return rc;
+    }
+    return set_err(ctx, RL_EINTERNAL, "capacity did not converge");
+}
+
+void fill_times(rl_ctx* ctx, rl_times* t) {
+    float a = 0, m = 0, e = 0, tot = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&m, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&e, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[3]);
+    t->analyze_ms = a;
+    t->merge_ms = m;
+    t->emit_ms = e;
+    t->total_ms = tot;
+}
+
+int fetch(rl_ctx* ctx, rl_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    const Geo& g = ctx->geo;
+    const int B = g.B;
+    out->width = g.W;
+    out->height = g.H;
+    out->n_images = B;
+    const int64_t* s = ctx->h_summ;
+    const uint64_t total = (uint64_t)s[4 * B];
+    out->n_components = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->n_fg = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->n_holes = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->euler = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->n_survivors = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->comp_offset = (int64_t*)std::malloc(sizeof(int64_t) * (B + 1));
+    out->comps = (rl_component*)std::malloc(sizeof(rl_component) * std::max<uint64_t>(total, 1));
+    out->top = (uint32_t*)std::malloc(sizeof(uint32_t) * std::max<uint64_t>(total, 1));
+    out->filled = (rl_features*)std::malloc(sizeof(rl_features) * std::max<uint64_t>(total, 1));
+    const size_t npx = (size_t)(g.P * B);
+    out->filled_image = (uint8_t*)std::malloc(npx);
+    if (g.label_mode) out->labels = (uint32_t*)std::malloc(npx * 4);
+    if (!out->n_components || !out->n_fg || !out->n_holes || !out->euler || !out->n_survivors ||
+        !out->comp_offset || !out->comps || !out->top || !out->filled || !out->filled_image ||
+        (g.label_mode && !out->labels)) {
+        rl_result_free(out);
+        return set_err(ctx, RL_ENOMEM, "host allocation failed");
+    }
+    for (int b = 0; b < B; ++b) {
+        out->comp_offset[b] = s[4 * b + 0];
+        out->n_components[b] = s[4 * b + 1];
+        out->n_fg[b] = s[4 * b + 2];
+        out->n_holes[b] = s[4 * b + 1] - 1 - s[4 * b + 2];
+        out->euler[b] = out->n_fg[b] - out->n_holes[b];
+        out->n_survivors[b] = s[4 * b + 3];
+    }
+    out->comp_offset[B] = (int64_t)total;
+    cudaStream_t st = ctx->stream;
+    cudaMemcpyAsync(out->comps, ctx->ws.comps, sizeof(rl_component) * total, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(out->top, ctx->ws.top, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(out->filled, ctx->ws.filled, sizeof(rl_features) * total, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
+    if (g.label_mode) cudaMemcpyAsync(out->labels, ctx->ws.labels, npx * 4, cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        rl_result_free(out);
+        return cuda_fail(ctx, e, "fetch");
+    }
+    fill_times(ctx, &out->times);
+    return RL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rl_ctx* rl_create(int device) {
+    rl_ctx* c = new (std::nothrow) rl_ctx();
+    if (!c) return nullptr;
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return nullptr;
+    }
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (configure_kernels() != cudaSuccess || cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return nullptr;
+    }
+    c->stream = c->own_stream;
+    for (auto& e : c->ev) cudaEventCreate(&e);
+    return c;
+}
+
+void rl_destroy(rl_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    DevBuf* bufs[] = {&c->bits, &c->tbase, &c->tnb, &c->perim, &c->uf, &c->nkey, &c->nmin, &c->nacc,
+                      &c->nrec, &c->nrep, &c->nrootcid, &c->nparent, &c->nanccid, &c->cnt, &c->off,
+                      &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
+                      &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
+                      &c->rank, &c->flag};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (c->h_summ) cudaFreeHost(c->h_summ);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+const char* rl_last_error(const rl_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int rl_label_device(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg) {
+    const int rc = check_args(ctx, w, h, n, cfg);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    return enqueue(ctx, d_pixels, w, h, n, cfg);
+}
+
+int rl_sync(rl_ctx* ctx) {
+    if (!ctx || !ctx->have_result) return set_err(ctx, RL_ELOGIC, "no pipeline enqueued");
+    cudaSetDevice(ctx->device);
+    return finish(ctx);
+}
+
+int rl_fetch(rl_ctx* ctx, rl_result* out) {
+    if (!out) return RL_EINVAL;
+    const int rc = rl_sync(ctx);
+    if (rc) return rc;
+    return fetch(ctx, out);
+}
+
+int rl_label(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+             rl_result* out) {
+    if (!out) return RL_EINVAL;
+    std::memset(out, 0, sizeof(*out));
+    int rc = check_args(ctx, w, h, n, cfg);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    const size_t npx = (size_t)w * h * n;
+    if (!ensure(ctx->pix, npx)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    cudaError_t e = cudaMemcpyAsync(ctx->pix.p, pixels, npx, cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "copy in");
+    rc = enqueue(ctx, P<uint8_t>(ctx->pix), w, h, n, cfg);
+    if (rc) return rc;
+    rc = finish(ctx);
+    if (rc) return rc;
+    return fetch(ctx, out);
+}
+
+void rl_result_free(rl_result* r) {
+    if (!r) return;
+    std::free(r->n_components);
+    std::free(r->n_fg);
+    std::free(r->n_holes);
+    std::free(r->euler);
+    std::free(r->n_survivors);
+    std::free(r->comp_offset);
+    std::free(r->comps);
+    std::free(r->top);
+    std::free(r->filled);
+    std::free(r->filled_image);
+    std::free(r->labels);
+    std::memset(r, 0, sizeof(*r));
+}
+
+void* rl_device_filled_image(rl_ctx* c) { return c ? c->ws.filled_img : nullptr; }
+void* rl_device_labels(rl_ctx* c) { return c ? c->ws.labels : nullptr; }
+void* rl_device_comps(rl_ctx* c) { return c ? c->ws.comps : nullptr; }
+void* rl_stream(rl_ctx* c) { return c ? (void*)c->stream : nullptr; }
+int rl_set_stream(rl_ctx* c, void* stream) {
+    if (!c) return RL_EINVAL;
+    c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+    return RL_OK;
+}
+int rl_last_launch_count(const rl_ctx* c) { return c ? c->launches : 0; }
+void rl_tile_shape(int32_t* th, int32_t* tw) {
+    if (th) *th = TH;
+    if (tw) *tw = TW;
+}
+
+}  // extern "C"

@@ -1,0 +1,220 @@
+// common.cuh -- tile geometry, workspace layout and small device helpers shared by the
+// kernels of the sm_100a labeling/analysis path.  See DESIGN.md for the data layout.
+#pragma once
+
+#include <cstdint>
+
+#include "runlab_gpu.h"
+
+namespace rlg {
+
+// ---- tile geometry -------------------------------------------------------------------
+// One CTA owns one TH x TW tile.  Pixels are bit-packed: one 32-bit word = 32 pixels of a
+// row, bit j = column 32*w + j.  One thread per word.
+constexpr int TH = 32;                 // tile rows
+constexpr int TW = 256;                // tile columns
+constexpr int WPR = TW / 32;           // words per tile row
+constexpr int NW = TH * WPR;           // words per tile
+constexpr int NT = NW;                 // threads per CTA (one word each)
+constexpr int NWARPS = NT / 32;
+constexpr int MAXRUNS = TH * TW;       // runs per tile <= pixels
+constexpr int MAXLC = MAXRUNS;         // tile-local components <= runs
+constexpr int PERIM = 2 * TW + 2 * TH; // perimeter label slots: top, bottom, left, right
+constexpr int NBMAX = PERIM;           // border components per tile <= perimeter pixels
+constexpr int FCH = 512;               // interior-feature accumulator chunk (K1b)
+constexpr uint32_t TAG = 0x80000000u;  // run-parent slot holds a tile-component index
+constexpr uint16_t PERIM_NONE = 0xFFFF;
+
+static_assert(MAXRUNS <= 32768, "local ids must fit 15 bits");
+static_assert(TW == 256, "lcpos packs the column in 8 bits");
+
+// Error bits in counters[1]
+constexpr uint32_t ERR_NODE_CAP = 1u;
+constexpr uint32_t ERR_COMP_CAP = 2u;
+constexpr uint32_t ERR_INTERNAL = 4u;
+
+// Global feature accumulator: exactly rl_features (40 B).
+using Acc = rl_features;
+
+// Border-component node record written by the analyze pass (immutable afterwards).
+struct NodeRec {
+    uint32_t tile;       // global tile index
+    uint16_t fr, fc;     // tile-local first pixel
+    uint16_t ibefore;    // interior components of the same tile row that precede it
+    uint16_t left;       // left reference: border index (kind 0) or tile row (kind 1)
+    uint8_t leftkind;    // 0 same tile, 1 left neighbour tile, 2 exterior frame, 3 none
+    uint8_t fg;          // foreground?
+    uint16_t pad;
+};
+static_assert(sizeof(NodeRec) == 16, "NodeRec layout");
+
+struct Geo {
+    int32_t W, H, B;     // image width, height, batch
+    int32_t ntx, nty;    // tiles per row / column
+    int32_t tpi;         // tiles per image
+    int32_t ntiles;
+    int32_t flip;        // 1 for fg4_bg8
+    int64_t P;           // pixels per image
+    int32_t vec_ok;      // 16-B vector pixel I/O allowed
+    int32_t label_mode;  // 0 none, 1 pre-fill canonical id, 2 post-fill root id
+};
+
+struct Ws {
+    // tile tables
+    uint32_t* bits;      // [ntiles*NW] packed 8-connected-value bits
+    uint32_t* tbase;     // [ntiles] first node of the tile (add B)
+    uint32_t* tnb;       // [ntiles] border components of the tile
+    uint16_t* perim;     // [ntiles*PERIM] (value << 15) | border index
+    // node tables: node b < B is image b's exterior, nodes B.. are border components
+    uint32_t* uf;        // union-find parent
+    uint64_t* nkey;      // first pixel raster index within the image
+    uint64_t* nmin;      // min key over the class (valid at roots)
+    Acc* nacc;           // own features, then class features at roots
+    NodeRec* nrec;
+    uint8_t* nrep;       // node holds its component's first pixel
+    uint32_t* nrootcid;  // canonical id (valid at roots)
+    uint32_t* nparent;   // root node of the surrounding component (valid at roots)
+    uint32_t* nanccid;   // canonical id of the post-fill root (valid at roots)
+    // canonical numbering
+    uint32_t* cnt;       // [B*H*ntx + 1] roots whose first pixel is in (image,row,tile col)
+    uint32_t* off;       // exclusive scan of cnt
+    uint32_t* counters;  // [0] nodes used, [1] error bits
+    uint32_t* img_fg;    // [B] foreground components
+    uint32_t* img_surv;  // [B] post-fill components (exterior included)
+    uint32_t cap_nodes;
+    uint64_t cap_comps;
+    // outputs
+    rl_component* comps;
+    uint32_t* top;
+    Acc* filled;
+    uint8_t* filled_img;
+    uint32_t* labels;
+};
+
+struct TileGeom {
+    int32_t t, b, ty, tx, x0, y0, tw, th;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(const Geo& g, int32_t t) {
+    TileGeom tg;
+    tg.t = t;
+    tg.b = t / g.tpi;
+    const int32_t rem = t - tg.b * g.tpi;
+    tg.ty = rem / g.ntx;
+    tg.tx = rem - tg.ty * g.ntx;
+    tg.x0 = tg.tx * TW;
+    tg.y0 = tg.ty * TH;
+    tg.tw = min(TW, g.W - tg.x0);
+    tg.th = min(TH, g.H - tg.y0);
+    return tg;
+}
+
+// valid-pixel mask of word w (column 32w..32w+31) of tile row r
+__device__ __forceinline__ uint32_t valid_mask(const TileGeom& tg, int r, int w) {
+    if (r >= tg.th) return 0u;
+    const int vc = tg.tw - 32 * w;
+    if (vc >= 32) return 0xFFFFFFFFu;
+    if (vc <= 0) return 0u;
+    return (1u << vc) - 1u;
+}
+
+// Block-wide exclusive scan over NT threads; `wsum` is __shared__ int[NWARPS + 1].
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += n;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int s = lane < NWARPS ? wsum[lane] : 0;
+        int si = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xFFFFFFFFu, si, o);
+            if (lane >= o) si += n;
+        }
+        if (lane < NWARPS) wsum[lane] = si - s;
+        if (lane == NWARPS - 1) wsum[NWARPS] = si;
+    }
+    __syncthreads();
+    total = wsum[NWARPS];
+    const int r = wsum[warp] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ int block_reduce_sum(int v, int* wsum) {
+    int t;
+    block_excl_scan(v, wsum, t);
+    return t;
+}
+
+// 4 mask bits -> 4 bytes of 0/1 (bit k -> byte k)
+__device__ __forceinline__ uint32_t nibble_to_bytes(uint32_t n) {
+    return ((n & 1u)) | ((n & 2u) << 7) | ((n & 4u) << 14) | ((n & 8u) << 21);
+}
+
+// 16 pixel bytes (values 0/1) -> 16 mask bits
+__device__ __forceinline__ uint32_t pack16(uint4 v) {
+    // each byte is 0 or 1: byte i lands on bit 24+i of the product, without carries
+    const uint32_t m = 0x01020408u;
+    const uint32_t a = ((v.x * m) >> 24) & 0xFu;
+    const uint32_t b = ((v.y * m) >> 24) & 0xFu;
+    const uint32_t c = ((v.z * m) >> 24) & 0xFu;
+    const uint32_t d = ((v.w * m) >> 24) & 0xFu;
+    return a | (b << 4) | (c << 8) | (d << 12);
+}
+
+__device__ __forceinline__ void acc_atomic_fold(Acc* dst, const Acc& f) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&dst->s), static_cast<unsigned long long>(f.s));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&dst->sx), static_cast<unsigned long long>(f.sx));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&dst->sy), static_cast<unsigned long long>(f.sy));
+    atomicMin(&dst->row_min, f.row_min);
+    atomicMax(&dst->row_max, f.row_max);
+    atomicMin(&dst->col_min, f.col_min);
+    atomicMax(&dst->col_max, f.col_max);
+}
+
+__device__ __forceinline__ Acc acc_empty() {
+    Acc a;
+    a.s = a.sx = a.sy = 0;
+    a.row_min = 0x7FFFFFFF;
+    a.row_max = (int32_t)0x80000000;
+    a.col_min = 0x7FFFFFFF;
+    a.col_max = (int32_t)0x80000000;
+    return a;
+}
+
+// ---- global union-find (lock-free; min-index linking, path halving) -------------------
+__device__ __forceinline__ uint32_t gfind(uint32_t* uf, uint32_t a) {
+    for (;;) {
+        const uint32_t p = __ldcg(uf + a);
+        if (p == a) return a;
+        const uint32_t gp = __ldcg(uf + p);
+        if (gp == p) return p;
+        __stcg(uf + a, gp);
+        a = gp;
+    }
+}
+
+__device__ __forceinline__ void gunion(uint32_t* uf, uint32_t a, uint32_t b) {
+    for (;;) {
+        a = gfind(uf, a);
+        b = gfind(uf, b);
+        if (a == b) return;
+        if (a < b) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        const uint32_t old = atomicMin(uf + a, b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+}  // namespace rlg

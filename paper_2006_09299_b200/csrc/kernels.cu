@@ -1,0 +1,808 @@
+// kernels.cu -- the sm_100a kernels of the labeling/analysis path.
+//
+//   K1a analyze  (per tile)  pixels -> packed bits, tile CCL, border-component nodes,
+//                            perimeter labels, interior-component counts per row
+//   M1  seams    (per seam pixel) lock-free union of border components across tile seams
+//   M2  resolve  (per node)  flatten, fold node features / first-pixel keys into roots
+//   M3  reps     (per node)  which node holds its component's first pixel; row counts
+//   --  scan     (CUB)       exclusive scan of per-(image,row,tile-col) root counts
+//   M4  cids     (per tile)  canonical ids of border components
+//   M5  parents  (per node)  adjacency parent, pre-fill records of border components
+//   M6  tops     (per node)  depth-1 ancestor (hole-fill target), post-fill init
+//   M7  fold     (per node)  fold non-surviving border components into their survivor
+//   K1b emit     (per tile)  tile CCL again from packed bits; interior-component records,
+//                            tree, fill fold, hole-filled image, optional label image
+//
+// Reference (paths relative to /root/reference/proj/include/runlab/): labeling.hpp:81-217
+// (Alg. 1-3 + fill), :224-250 (Alg. 4), :354-360 (binarize_labels), features.hpp:33-66.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "tile_ccl.cuh"
+
+namespace rlg {
+
+// ---------------------------------------------------------------------------------------
+// K1a: analyze
+// ---------------------------------------------------------------------------------------
+struct AnalyzeSmem {
+    CclSmem c;
+    // border-component accumulators (tile-local coordinates)
+    uint32_t bs[NBMAX], bsx[NBMAX], bsy[NBMAX];
+    int32_t brmax[NBMAX], bcmin[NBMAX], bcmax[NBMAX];
+    uint8_t bimg[NBMAX];  // touches the image border
+    uint32_t base;
+};
+
+__global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    AnalyzeSmem& A = *reinterpret_cast<AnalyzeSmem*>(smem_raw);
+    CclSmem& S = A.c;
+    const TileGeom tg = tile_geom(g, blockIdx.x);
+    const int tid = threadIdx.x;
+    const int r = tid / WPR, w = tid % WPR;
+
+    // ---- load 32 pixels (bytes) of this thread's word and pack them to bits
+    const uint32_t vm = valid_mask(tg, r, w);
+    uint32_t bits = 0;
+    if (vm) {
+        const uint8_t* src = pix + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
+        if (g.vec_ok && vm == 0xFFFFFFFFu) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+            const uint4 v0 = __ldcs(s4), v1 = __ldcs(s4 + 1);
+            bits = pack16(v0) | (pack16(v1) << 16);
+        } else {
+            const int n = 32 - __clz(vm);
+            for (int j = 0; j < n; ++j) bits |= (uint32_t)(src[j] & 1u) << j;
+        }
+    }
+    const uint32_t x = (bits ^ (g.flip ? 0xFFFFFFFFu : 0u)) & vm;
+    S.x[tid] = x;
+    S.vm[tid] = vm;
+    ws.bits[(int64_t)tg.t * NW + tid] = x;
+    if (tid < NBMAX) {
+        A.bs[tid] = A.bsx[tid] = A.bsy[tid] = 0;
+        A.brmax[tid] = -1;
+        A.bcmin[tid] = 0x7FFFFFFF;
+        A.bcmax[tid] = -1;
+        A.bimg[tid] = 0;
+    }
+    for (int i = tid + NT; i < NBMAX; i += NT) {
+        A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
+        A.brmax[i] = -1;
+        A.bcmin[i] = 0x7FFFFFFF;
+        A.bcmax[i] = -1;
+        A.bimg[i] = 0;
+    }
+    if (tg.tx == 0 && tg.ty == 0 && tid == 0) {
+        // exterior node of image b
+        const uint32_t e = (uint32_t)tg.b;
+        ws.uf[e] = e;
+        ws.nacc[e] = acc_empty();
+        ws.nmin[e] = ~0ull;
+        ws.nrootcid[e] = 0;
+        ws.nparent[e] = e;
+        ws.nanccid[e] = 0;
+        ws.nrep[e] = 0;
+    }
+    __syncthreads();
+
+    ccl_tile(S, tg);
+
+    const int nlc = S.nlc, nb = S.nb;
+    if (tid == 0) {
+        const uint32_t base = atomicAdd(&ws.counters[0], (uint32_t)nb);
+        A.base = base;
+        if ((uint64_t)base + nb > ws.cap_nodes) atomicOr(&ws.counters[1], ERR_NODE_CAP);
+        ws.tbase[tg.t] = base;
+        ws.tnb[tg.t] = (uint32_t)nb;
+    }
+
+    // ---- border-component features and image-border contact (run pieces)
+    const bool top_img = tg.ty == 0, bot_img = (tg.y0 + tg.th == g.H);
+    const bool left_img = tg.tx == 0, right_img = (tg.x0 + tg.tw == g.W);
+    for_each_piece(S, tid, [&](int ri, int j0, int j1) {
+        const uint32_t lc = lc_of_run(S, ri);
+        if (!lc_is_border(S, lc)) return;
+        const int bi = S.lcb[lc];
+        const int c0 = 32 * w + j0, c1 = 32 * w + j1;  // [c0, c1) tile-local
+        const uint32_t n = (uint32_t)(c1 - c0);
+        atomicAdd(&A.bs[bi], n);
+        atomicAdd(&A.bsx[bi], n * (uint32_t)(c0 + c1 - 1) / 2u);
+        atomicAdd(&A.bsy[bi], n * (uint32_t)r);
+        atomicMax(&A.brmax[bi], r);
+        atomicMin(&A.bcmin[bi], c0);
+        atomicMax(&A.bcmax[bi], c1 - 1);
+        if ((top_img && r == 0) || (bot_img && r == tg.th - 1) || (left_img && c0 == 0) ||
+            (right_img && c1 == tg.tw))
+            A.bimg[bi] = 1;
+    });
+    __syncthreads();
+
+    // ---- border-component nodes
+    const uint32_t base = A.base;
+    const bool node_ok = (uint64_t)base + nb <= ws.cap_nodes;
+    const int flip = g.flip;
+    for (int i = tid; i < nb && node_ok; i += NT) {
+        const int lc = S.blc[i];
+        const int fr = S.lcpos[lc] >> 8, fc = S.lcpos[lc] & 0xFF;
+        const uint32_t fg = xbit(S, fr, fc) ^ (uint32_t)flip;
+        NodeRec rec;
+        rec.tile = (uint32_t)tg.t;
+        rec.fr = (uint16_t)fr;
+        rec.fc = (uint16_t)fc;
+        rec.ibefore = (uint16_t)((lc - S.rowlc[fr]) - (i - S.rowbx[fr]));
+        rec.fg = (uint8_t)fg;
+        rec.pad = 0;
+        if (fc > 0) {
+            const uint32_t l2 = lc_at(S, fr, fc - 1);
+            if (lc_is_border(S, l2)) {
+                rec.leftkind = 0;
+                rec.left = S.lcb[l2];
+            } else {
+                rec.leftkind = 3;
+                rec.left = 0;
+            }
+        } else if (tg.x0 == 0) {
+            rec.leftkind = 2;
+            rec.left = 0;
+        } else {
+            rec.leftkind = 1;
+            rec.left = (uint16_t)fr;
+        }
+        const uint32_t node = (uint32_t)g.B + base + (uint32_t)i;
+        const uint64_t key = (uint64_t)(tg.y0 + fr) * (uint64_t)g.W + (uint64_t)(tg.x0 + fc);
+        Acc f;
+        const int64_t s = A.bs[i];
+        f.s = s;
+        f.sx = (int64_t)A.bsx[i] + s * tg.x0;
+        f.sy = (int64_t)A.bsy[i] + s * tg.y0;
+        f.row_min = tg.y0 + fr;
+        f.row_max = tg.y0 + A.brmax[i];
+        f.col_min = tg.x0 + A.bcmin[i];
+        f.col_max = tg.x0 + A.bcmax[i];
+        ws.nrec[node] = rec;
+        ws.nkey[node] = key;
+        ws.nmin[node] = key;
+        ws.nacc[node] = f;
+        // border background touching the image frame is the exterior (App. A R3)
+        ws.uf[node] = (!fg && A.bimg[i]) ? (uint32_t)tg.b : node;
+    }
+
+    // ---- perimeter labels: (value << 15) | border index
+    for (int q = tid; q < PERIM; q += NT) {
+        int pr, pc;
+        if (q < TW) { pr = 0; pc = q; }
+        else if (q < 2 * TW) { pr = tg.th - 1; pc = q - TW; }
+        else if (q < 2 * TW + TH) { pr = q - 2 * TW; pc = 0; }
+        else { pr = q - 2 * TW - TH; pc = tg.tw - 1; }
+        uint16_t v = PERIM_NONE;
+        if (pr >= 0 && pr < tg.th && pc >= 0 && pc < tg.tw) {
+            const uint32_t lc = lc_at(S, pr, pc);
+            const uint32_t val = xbit(S, pr, pc) ^ (uint32_t)flip;
+            v = (uint16_t)((val << 15) | (S.lcb[lc] & 0x7FFF));
+        }
+        ws.perim[(int64_t)tg.t * PERIM + q] = v;
+    }
+
+    // ---- interior components per row, foreground interior components
+    if (tid < tg.th) {
+        const int nl = S.rowlc[tid + 1] - S.rowlc[tid];
+        const int nbr = S.rowbx[tid + 1] - S.rowbx[tid];
+        ws.cnt[((int64_t)tg.b * g.H + tg.y0 + tid) * g.ntx + tg.tx] = (uint32_t)(nl - nbr);
+    }
+    int nfg = 0;
+    for (int l = tid; l < nlc; l += NT) {
+        if (lc_is_border(S, l)) continue;
+        const int fr = S.lcpos[l] >> 8, fc = S.lcpos[l] & 0xFF;
+        nfg += (int)(xbit(S, fr, fc) ^ (uint32_t)flip);
+    }
+    nfg = block_reduce_sum(nfg, S.wsum);
+    if (tid == 0 && nfg) atomicAdd(&ws.img_fg[tg.b], (uint32_t)nfg);
+}
+
+// ---------------------------------------------------------------------------------------
+// M1: union across tile seams
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t node_of(const Ws& ws, const Geo& g, int64_t t, uint16_t lab) {
+    return (uint32_t)g.B + ws.tbase[t] + (lab & 0x7FFFu);
+}
+
+// horizontal seams: between band s and s+1, one thread per image column
+__global__ void k_seam_h(Geo g, Ws ws) {
+    if (ws.counters[1]) return;
+    const int64_t nseam = (int64_t)g.B * (g.nty - 1) * g.W;
+    const uint32_t v8 = g.flip ? 0u : 1u;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseam;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t x = (int32_t)(i % g.W);
+        const int64_t bs = i / g.W;
+        const int32_t s = (int32_t)(bs % (g.nty - 1));
+        const int32_t b = (int32_t)(bs / (g.nty - 1));
+        const int32_t tx = x / TW, c = x % TW;
+        const int64_t tu = ((int64_t)b * g.nty + s) * g.ntx + tx, tl = tu + g.ntx;
+        const uint16_t lu = ws.perim[tu * PERIM + TW + c], ld = ws.perim[tl * PERIM + c];
+        const uint32_t vu = lu >> 15, vd = ld >> 15;
+        uint16_t lul = PERIM_NONE, ldl = PERIM_NONE;
+        int64_t tul = tu, tll = tl;
+        if (x > 0) {
+            const int32_t cl = (x - 1) % TW;
+            if (c == 0) {
+                tul = tu - 1;
+                tll = tl - 1;
+            }
+            lul = ws.perim[tul * PERIM + TW + cl];
+            ldl = ws.perim[tll * PERIM + cl];
+        }
+        if (vu == vd) {
+            const bool same = (c > 0) && lul == lu && ldl == ld;
+            if (!same) gunion(ws.uf, node_of(ws, g, tu, lu), node_of(ws, g, tl, ld));
+        }
+        if (x > 0) {
+            const uint32_t vul = lul >> 15, vdl = ldl >> 15;
+            if (vul == v8 && vd == v8 && vu != v8 && vdl != v8)
+                gunion(ws.uf, node_of(ws, g, tul, lul), node_of(ws, g, tl, ld));
+            if (vu == v8 && vdl == v8 && vul != v8 && vd != v8)
+                gunion(ws.uf, node_of(ws, g, tu, lu), node_of(ws, g, tll, ldl));
+        }
+    }
+}
+
+// vertical seams: between tile column s-1 and s, one thread per tile row
+__global__ void k_seam_v(Geo g, Ws ws) {
+    if (ws.counters[1]) return;
+    const int64_t nseam = (int64_t)g.B * g.nty * (g.ntx - 1) * TH;
+    const uint32_t v8 = g.flip ? 0u : 1u;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseam;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = (int32_t)(i % TH);
+        int64_t q = i / TH;
+        const int32_t s = 1 + (int32_t)(q % (g.ntx - 1));
+        q /= (g.ntx - 1);
+        const int32_t ty = (int32_t)(q % g.nty);
+        const int32_t b = (int32_t)(q / g.nty);
+        const int32_t th = min(TH, g.H - ty * TH);
+        if (r >= th) continue;
+        const int64_t tR = ((int64_t)b * g.nty + ty) * g.ntx + s, tL = tR - 1;
+        const uint16_t* pL = ws.perim + tL * PERIM + 2 * TW + TH;  // right column of left tile
+        const uint16_t* pR = ws.perim + tR * PERIM + 2 * TW;       // left column of right tile
+        const uint16_t lL = pL[r], lR = pR[r];
+        const uint32_t vL = lL >> 15, vR = lR >> 15;
+        if (vL == vR) {
+            const bool same = r > 0 && pL[r - 1] == lL && pR[r - 1] == lR;
+            if (!same) gunion(ws.uf, node_of(ws, g, tL, lL), node_of(ws, g, tR, lR));
+        }
+        if (r + 1 < th) {
+            const uint16_t lL1 = pL[r + 1], lR1 = pR[r + 1];
+            const uint32_t vL1 = lL1 >> 15, vR1 = lR1 >> 15;
+            if (vL == v8 && vR1 == v8 && vR != v8 && vL1 != v8)
+                gunion(ws.uf, node_of(ws, g, tL, lL), node_of(ws, g, tR, lR1));
+            if (vL1 == v8 && vR == v8 && vL != v8 && vR1 != v8)
+                gunion(ws.uf, node_of(ws, g, tL, lL1), node_of(ws, g, tR, lR));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// M2..M7: node passes
+// ---------------------------------------------------------------------------------------
+#define NODE_LOOP(n)                                                                   \
+    const uint32_t nused_ = min(ws.counters[0], ws.cap_nodes);                         \
+    for (uint32_t n = (uint32_t)g.B + blockIdx.x * blockDim.x + threadIdx.x;           \
+         n < (uint32_t)g.B + nused_; n += gridDim.x * blockDim.x)
+
+__global__ void k_resolve(Geo g, Ws ws) {
+    if (ws.counters[1]) return;
+    NODE_LOOP(n) {
+        const uint32_t root = gfind(ws.uf, n);
+        if (root != n) {
+            __stcg(ws.uf + n, root);
+            acc_atomic_fold(ws.nacc + root, ws.nacc[n]);
+            atomicMin(reinterpret_cast<unsigned long long*>(ws.nmin + root),
+                      static_cast<unsigned long long>(ws.nkey[n]));
+        }
+    }
+}
+
+__device__ __forceinline__ void tile_of(const Geo& g, uint32_t t, int32_t& b, int32_t& ty, int32_t& tx) {
+    b = (int32_t)(t / (uint32_t)g.tpi);
+    const int32_t rem = (int32_t)(t - (uint32_t)b * g.tpi);
+    ty = rem / g.ntx;
+    tx = rem - ty * g.ntx;
+}
+
+__global__ void k_reps(Geo g, Ws ws) {
+    if (ws.counters[1]) return;
+    NODE_LOOP(n) {
+        const uint32_t root = ws.uf[n];
+        const bool rep = root >= (uint32_t)g.B && ws.nkey[n] == ws.nmin[root];
+        ws.nrep[n] = rep ? 1 : 0;
+        if (rep) {
+            const NodeRec rec = ws.nrec[n];
+            int32_t b, ty, tx;
+            tile_of(g, rec.tile, b, ty, tx);
+            atomicAdd(&ws.cnt[((int64_t)b * g.H + ty * TH + rec.fr) * g.ntx + tx], 1u);
+            if (rec.fg) atomicAdd(&ws.img_fg[b], 1u);
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t comp_base(const Geo& g, const Ws& ws, int32_t b) {
+    return (uint64_t)ws.off[(int64_t)b * g.H * g.ntx] + (uint64_t)b;
+}
+
+__device__ __forceinline__ bool comps_fit(const Geo& g, const Ws& ws) {
+    return (uint64_t)ws.off[(int64_t)g.B * g.H * g.ntx] + (uint64_t)g.B <= ws.cap_comps;
+}
+
+// one thread per tile: canonical ids of the tile's border representatives
+__global__ void k_cids(Geo g, Ws ws) {
+    if (ws.counters[1]) return;
+    for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < g.ntiles; t += gridDim.x * blockDim.x) {
+        int32_t b, ty, tx;
+        tile_of(g, (uint32_t)t, b, ty, tx);
+        const uint32_t nb = ws.tnb[t];
+        const uint32_t n0 = (uint32_t)g.B + ws.tbase[t];
+        const int64_t img0 = (int64_t)b * g.H * g.ntx;
+        const uint32_t offimg = ws.off[img0];
+        int cur_row = -1, reps = 0;
+        for (uint32_t i = 0; i < nb; ++i) {
+            const uint32_t n = n0 + i;
+            const NodeRec rec = ws.nrec[n];
+            if (rec.fr != cur_row) {
+                cur_row = rec.fr;
+                reps = 0;
+            }
+            if (!ws.nrep[n]) continue;
+            const uint32_t cid = 1u + (ws.off[img0 + (int64_t)(ty * TH + rec.fr) * g.ntx + tx] - offimg) +
+                                 rec.ibefore + (uint32_t)reps;
+            ++reps;
+            ws.nrootcid[ws.uf[n]] = cid;
+        }
+    }
+}
+
+__global__ void k_parents(Geo g, Ws ws) {
+    if (ws.counters[1] || !comps_fit(g, ws)) return;
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid < g.B) {  // exterior records
+        const uint64_t cb = comp_base(g, ws, gid);
+        rl_component c;
+        c.f = ws.nacc[gid];
+        c.parent = 0xFFFFFFFFu;
+        c.flags = 0;
+        ws.comps[cb] = c;
+    }
+    NODE_LOOP(n) {
+        if (!ws.nrep[n]) continue;
+        const uint32_t root = ws.uf[n];
+        const NodeRec rec = ws.nrec[n];
+        int32_t b, ty, tx;
+        tile_of(g, rec.tile, b, ty, tx);
+        uint32_t proot;
+        if (rec.leftkind == 0) {
+            proot = ws.uf[(uint32_t)g.B + ws.tbase[rec.tile] + rec.left];
+        } else if (rec.leftkind == 1) {
+            const uint32_t tl = rec.tile - 1;
+            const uint16_t lab = ws.perim[(int64_t)tl * PERIM + 2 * TW + TH + rec.left];
+            proot = ws.uf[(uint32_t)g.B + ws.tbase[tl] + (lab & 0x7FFFu)];
+        } else if (rec.leftkind == 2) {
+            proot = (uint32_t)b;
+        } else {
+            atomicOr(&ws.counters[1], ERR_INTERNAL);
+            continue;
+        }
+        ws.nparent[root] = proot;
+        const uint32_t cid = ws.nrootcid[root];
+        rl_component c;
+        c.f = ws.nacc[root];
+        c.parent = ws.nrootcid[proot];
+        c.flags = rec.fg;
+        ws.comps[comp_base(g, ws, b) + cid] = c;
+    }
+}
+
+__global__ void k_tops(Geo g, Ws ws) {
+    if (ws.counters[1] || !comps_fit(g, ws)) return;
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid < g.B) {
+        const uint64_t cb = comp_base(g, ws, gid);
+        ws.top[cb] = 0;
+        ws.filled[cb] = ws.nacc[gid];
+        atomicAdd(&ws.img_surv[gid], 1u);
+    }
+    NODE_LOOP(n) {
+        if (!ws.nrep[n]) continue;
+        const uint32_t root = ws.uf[n];
+        uint32_t cur = root;
+        for (;;) {
+            const uint32_t p = ws.nparent[cur];
+            if (p < (uint32_t)g.B) break;
+            cur = p;
+        }
+        const uint32_t anc = ws.nrootcid[cur];
+        ws.nanccid[root] = anc;
+        const NodeRec rec = ws.nrec[n];
+        int32_t b, ty, tx;
+        tile_of(g, rec.tile, b, ty, tx);
+        const uint64_t cb = comp_base(g, ws, b);
+        const uint32_t cid = ws.nrootcid[root];
+        ws.top[cb + cid] = anc;
+        if (cur == root) {
+            ws.filled[cb + cid] = ws.nacc[root];
+            atomicAdd(&ws.img_surv[b], 1u);
+        }
+    }
+}
+
+__global__ void k_fold(Geo g, Ws ws) {
+    if (ws.counters[1] || !comps_fit(g, ws)) return;
+    NODE_LOOP(n) {
+        if (!ws.nrep[n]) continue;
+        const uint32_t root = ws.uf[n];
+        const uint32_t anc = ws.nanccid[root];
+        const uint32_t cid = ws.nrootcid[root];
+        if (anc == cid) continue;
+        int32_t b, ty, tx;
+        tile_of(g, ws.nrec[n].tile, b, ty, tx);
+        acc_atomic_fold(ws.filled + comp_base(g, ws, b) + anc, ws.nacc[root]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1b: emit
+// ---------------------------------------------------------------------------------------
+struct EmitSmem {
+    CclSmem c;
+    // interior-feature chunk accumulators (tile-local coordinates)
+    uint32_t fs[FCH], fsx[FCH], fsy[FCH];
+    int32_t frmax[FCH], fcmin[FCH], fcmax[FCH];
+    // border components of this tile
+    uint32_t bcid[NBMAX];   // canonical id of the component
+    uint32_t banc[NBMAX];   // canonical id of its post-fill root
+    uint8_t bflag[NBMAX];   // bit0 representative, bit1 exterior
+    uint16_t repx[NBMAX + 1];  // exclusive prefix of representative flags over border index
+    // fold of interior components into border-derived survivors, keyed by border index
+    uint32_t ps[NBMAX], psx[NBMAX], psy[NBMAX];
+    int32_t prmin[NBMAX], prmax[NBMAX], pcmin[NBMAX], pcmax[NBMAX];
+    uint32_t rowoff[TH];    // canonical id offset of each tile row (relative to the image)
+    uint64_t cb;
+};
+
+// canonical id of tile component lc (any kind)
+__device__ __forceinline__ uint32_t comp_cid(const EmitSmem& E, uint32_t lc) {
+    const CclSmem& S = E.c;
+    const uint16_t lb = S.lcb[lc];
+    if (!(lb & 0x8000u)) return E.bcid[lb];
+    const int r = S.lcpos[lc] >> 8;
+    const int bp = lb & 0x7FFF;                  // border components before lc
+    const int rb0 = S.rowbx[r];
+    const int nonrep_before = (bp - rb0) - (E.repx[bp] - E.repx[rb0]);
+    return 1u + E.rowoff[r] + (uint32_t)((int)lc - S.rowlc[r] - nonrep_before);
+}
+
+// Walk the tree inside the tile: returns the post-fill root's canonical id of interior
+// component lc; `end` = border index where the walk left the tile interior, or -1 when lc's
+// chain reached the exterior (then `surv` is the interior survivor).
+__device__ __forceinline__ uint32_t interior_top(const EmitSmem& E, uint32_t lc, int& end, uint32_t& surv) {
+    const CclSmem& S = E.c;
+    uint32_t cur = lc;
+    for (;;) {
+        const int r = S.lcpos[cur] >> 8, c = S.lcpos[cur] & 0xFF;
+        const uint32_t p = lc_at(S, r, c - 1);  // interior: c >= 1
+        const uint16_t pb = S.lcb[p];
+        if (!(pb & 0x8000u)) {
+            if (E.bflag[pb] & 2u) {  // parent is the exterior: cur survives
+                end = -1;
+                surv = cur;
+                return comp_cid(E, cur);
+            }
+            end = pb;
+            surv = 0;
+            return E.banc[pb];
+        }
+        cur = p;
+    }
+}
+
+__global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    EmitSmem& E = *reinterpret_cast<EmitSmem*>(smem_raw);
+    CclSmem& S = E.c;
+    if (ws.counters[1] || !comps_fit(g, ws)) return;
+    const TileGeom tg = tile_geom(g, blockIdx.x);
+    const int tid = threadIdx.x;
+    const int r = tid / WPR, w = tid % WPR;
+    const uint32_t vm = valid_mask(tg, r, w);
+    S.x[tid] = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
+    S.vm[tid] = vm;
+    const int64_t img0 = (int64_t)tg.b * g.H * g.ntx;
+    const uint32_t offimg = ws.off[img0];
+    if (tid < TH && tid < tg.th)
+        E.rowoff[tid] = ws.off[img0 + (int64_t)(tg.y0 + tid) * g.ntx + tg.tx] - offimg;
+    if (tid == 0) E.cb = (uint64_t)offimg + (uint64_t)tg.b;
+    __syncthreads();
+
+    ccl_tile(S, tg);
+
+    const int nlc = S.nlc, nb = S.nb;
+    const uint64_t cb = E.cb;
+    const uint32_t nbase = (uint32_t)g.B + ws.tbase[tg.t];
+    for (int i = tid; i < nb; i += NT) {
+        const uint32_t node = nbase + (uint32_t)i;
+        const uint32_t root = ws.uf[node];
+        const bool ext = root < (uint32_t)g.B;
+        E.bcid[i] = ws.nrootcid[root];
+        E.banc[i] = ext ? 0u : ws.nanccid[root];
+        E.bflag[i] = (uint8_t)((ws.nrep[node] ? 1u : 0u) | (ext ? 2u : 0u));
+        E.ps[i] = E.psx[i] = E.psy[i] = 0;
+        E.prmin[i] = 0x7FFFFFFF;
+        E.prmax[i] = -1;
+        E.pcmin[i] = 0x7FFFFFFF;
+        E.pcmax[i] = -1;
+    }
+    __syncthreads();
+    if (tid == 0) {  // tiny serial prefix (nb <= NBMAX)
+        uint16_t acc = 0;
+        for (int i = 0; i < nb; ++i) {
+            E.repx[i] = acc;
+            acc += E.bflag[i] & 1u;
+        }
+        E.repx[nb] = acc;
+    }
+    __syncthreads();
+
+    // ---- interior components, in chunks of FCH tile components
+    const int flip = g.flip;
+    int nsurv = 0;
+    for (int l0 = 0; l0 < nlc; l0 += FCH) {
+        const int l1 = min(l0 + FCH, nlc);
+        for (int i = tid; i < FCH; i += NT) {
+            E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
+            E.frmax[i] = -1;
+            E.fcmin[i] = 0x7FFFFFFF;
+            E.fcmax[i] = -1;
+        }
+        __syncthreads();
+        for_each_piece(S, tid, [&](int ri, int j0, int j1) {
+            const uint32_t lc = lc_of_run(S, ri);
+            if ((int)lc < l0 || (int)lc >= l1 || lc_is_border(S, lc)) return;
+            const int k = (int)lc - l0;
+            const int c0 = 32 * w + j0, c1 = 32 * w + j1;
+            const uint32_t n = (uint32_t)(c1 - c0);
+            atomicAdd(&E.fs[k], n);
+            atomicAdd(&E.fsx[k], n * (uint32_t)(c0 + c1 - 1) / 2u);
+            atomicAdd(&E.fsy[k], n * (uint32_t)r);
+            atomicMax(&E.frmax[k], r);
+            atomicMin(&E.fcmin[k], c0);
+            atomicMax(&E.fcmax[k], c1 - 1);
+        });
+        __syncthreads();
+        // pre-fill records, post-fill roots, survivor init
+        for (int lc = l0 + tid; lc < l1; lc += NT) {
+            if (lc_is_border(S, lc)) continue;
+            const int k = lc - l0;
+            const int fr = S.lcpos[lc] >> 8, fc = S.lcpos[lc] & 0xFF;
+            const uint32_t cid = comp_cid(E, (uint32_t)lc);
+            const uint32_t pcid = comp_cid(E, lc_at(S, fr, fc - 1));
+            int end;
+            uint32_t surv;
+            const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
+            const int64_t s = E.fs[k];
+            rl_component c;
+            c.f.s = s;
+            c.f.sx = (int64_t)E.fsx[k] + s * tg.x0;
+            c.f.sy = (int64_t)E.fsy[k] + s * tg.y0;
+            c.f.row_min = tg.y0 + fr;
+            c.f.row_max = tg.y0 + E.frmax[k];
+            c.f.col_min = tg.x0 + E.fcmin[k];
+            c.f.col_max = tg.x0 + E.fcmax[k];
+            c.parent = pcid;
+            c.flags = xbit(S, fr, fc) ^ (uint32_t)flip;
+            ws.comps[cb + cid] = c;
+            ws.top[cb + cid] = anc;
+            if (anc == cid) {
+                ws.filled[cb + cid] = c.f;
+                ++nsurv;
+            }
+        }
+        __syncthreads();
+        // fold non-survivors into their post-fill root
+        for (int lc = l0 + tid; lc < l1; lc += NT) {
+            if (lc_is_border(S, lc)) continue;
+            const int k = lc - l0;
+            int end;
+            uint32_t surv;
+            const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
+            const uint32_t cid = comp_cid(E, (uint32_t)lc);
+            if (anc == cid) continue;
+            const int fr = S.lcpos[lc] >> 8;
+            if (end >= 0) {
+                atomicAdd(&E.ps[end], E.fs[k]);
+                atomicAdd(&E.psx[end], E.fsx[k]);
+                atomicAdd(&E.psy[end], E.fsy[k]);
+                atomicMin(&E.prmin[end], fr);
+                atomicMax(&E.prmax[end], E.frmax[k]);
+                atomicMin(&E.pcmin[end], E.fcmin[k]);
+                atomicMax(&E.pcmax[end], E.fcmax[k]);
+            } else {
+                Acc f;
+                const int64_t s = E.fs[k];
+                f.s = s;
+                f.sx = (int64_t)E.fsx[k] + s * tg.x0;
+                f.sy = (int64_t)E.fsy[k] + s * tg.y0;
+                f.row_min = tg.y0 + fr;
+                f.row_max = tg.y0 + E.frmax[k];
+                f.col_min = tg.x0 + E.fcmin[k];
+                f.col_max = tg.x0 + E.fcmax[k];
+                acc_atomic_fold(ws.filled + cb + anc, f);
+            }
+        }
+        __syncthreads();
+    }
+    // flush border-keyed folds (the survivors were initialised by k_tops)
+    for (int i = tid; i < nb; i += NT) {
+        if (!E.ps[i]) continue;
+        Acc f;
+        const int64_t s = E.ps[i];
+        f.s = s;
+        f.sx = (int64_t)E.psx[i] + s * tg.x0;
+        f.sy = (int64_t)E.psy[i] + s * tg.y0;
+        f.row_min = tg.y0 + E.prmin[i];
+        f.row_max = tg.y0 + E.prmax[i];
+        f.col_min = tg.x0 + E.pcmin[i];
+        f.col_max = tg.x0 + E.pcmax[i];
+        acc_atomic_fold(ws.filled + cb + E.banc[i], f);
+    }
+    nsurv = block_reduce_sum(nsurv, S.wsum);
+    if (tid == 0 && nsurv) atomicAdd(&ws.img_surv[tg.b], (uint32_t)nsurv);
+
+    // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
+    if (vm) {
+        uint32_t ext = 0;
+        for_each_piece(S, tid, [&](int ri, int j0, int j1) {
+            const uint32_t lc = lc_of_run(S, ri);
+            const uint16_t lb = S.lcb[lc];
+            if (!(lb & 0x8000u) && (E.bflag[lb] & 2u)) {
+                const uint32_t m = (j1 >= 32 ? 0xFFFFFFFFu : ((1u << j1) - 1u)) & ~((1u << j0) - 1u);
+                ext |= m;
+            }
+        });
+        const uint32_t fillbits = vm & ~ext;
+        uint8_t* dst = ws.filled_img + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
+        if (g.vec_ok && vm == 0xFFFFFFFFu) {
+            uint4 o0, o1;
+            o0.x = nibble_to_bytes(fillbits & 0xF);
+            o0.y = nibble_to_bytes((fillbits >> 4) & 0xF);
+            o0.z = nibble_to_bytes((fillbits >> 8) & 0xF);
+            o0.w = nibble_to_bytes((fillbits >> 12) & 0xF);
+            o1.x = nibble_to_bytes((fillbits >> 16) & 0xF);
+            o1.y = nibble_to_bytes((fillbits >> 20) & 0xF);
+            o1.z = nibble_to_bytes((fillbits >> 24) & 0xF);
+            o1.w = nibble_to_bytes((fillbits >> 28) & 0xF);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            __stcs(d4, o0);
+            __stcs(d4 + 1, o1);
+        } else {
+            const int n = 32 - __clz(vm);
+            for (int j = 0; j < n; ++j) dst[j] = (uint8_t)((fillbits >> j) & 1u);
+        }
+        // ---- optional label image (Alg. 4 relabel, canonical ids)
+        if (g.label_mode) {
+            uint32_t* ldst = ws.labels + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
+            for_each_piece(S, tid, [&](int ri, int j0, int j1) {
+                const uint32_t lc = lc_of_run(S, ri);
+                uint32_t v = comp_cid(E, lc);
+                if (g.label_mode == 2) {
+                    const uint16_t lb = S.lcb[lc];
+                    if (!(lb & 0x8000u)) {
+                        v = (E.bflag[lb] & 2u) ? 0u : E.banc[lb];
+                    } else {
+                        int end;
+                        uint32_t surv;
+                        v = interior_top(E, lc, end, surv);
+                    }
+                }
+                for (int j = j0; j < j1; ++j) ldst[j] = v;
+            });
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// densified post-fill label image (labeling.hpp:231-236 with fill): rank of the survivor
+// ---------------------------------------------------------------------------------------
+__global__ void k_surv_flags(const uint32_t* top, uint64_t n, uint32_t* flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        flag[i] = top[i] == (uint32_t)i ? 1u : 0u;  // caller offsets per image below
+}
+
+__global__ void k_remap_labels(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank,
+                               const uint64_t* cbase) {
+    const int64_t total = P * B;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / P;
+        const uint64_t cb = cbase[b];
+        labels[i] = rank[cb + labels[i]] - rank[cb];
+    }
+}
+
+__global__ void k_surv_flags_img(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total,
+                                 uint32_t* flag) {
+    // flag[i] = 1 iff component i (global index) is a post-fill root of its image
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        // binary search the image
+        int32_t lo = 0, hi = B - 1;
+        while (lo < hi) {
+            const int32_t mid = (lo + hi + 1) / 2;
+            if (cbase[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        flag[i] = top[i] == (uint32_t)(i - cbase[lo]) ? 1u : 0u;
+    }
+}
+
+}  // namespace rlg
+
+// ---------------------------------------------------------------------------------------
+// launch wrappers (called from api.cu)
+// ---------------------------------------------------------------------------------------
+namespace rlg {
+
+size_t analyze_smem() { return sizeof(AnalyzeSmem); }
+size_t emit_smem() { return sizeof(EmitSmem); }
+
+cudaError_t configure_kernels() {
+    cudaError_t e = cudaFuncSetAttribute(k_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(AnalyzeSmem));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem));
+}
+
+static int grid_for(int64_t n, int block, int maxgrid) {
+    int64_t gr = (n + block - 1) / block;
+    if (gr < 1) gr = 1;
+    if (gr > maxgrid) gr = maxgrid;
+    return (int)gr;
+}
+
+void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
+    k_analyze<<<g.ntiles, NT, sizeof(AnalyzeSmem), s>>>(pix, g, ws);
+}
+void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
+    if (g.nty > 1) {
+        const int64_t n = (int64_t)g.B * (g.nty - 1) * g.W;
+        k_seam_h<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(g, ws);
+    }
+    if (g.ntx > 1) {
+        const int64_t n = (int64_t)g.B * g.nty * (g.ntx - 1) * TH;
+        k_seam_v<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(g, ws);
+    }
+}
+void launch_resolve(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
+    k_resolve<<<grid_for(nodes_hint, 256, sms * 8), 256, 0, s>>>(g, ws);
+}
+void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
+    k_reps<<<grid_for(nodes_hint, 256, sms * 8), 256, 0, s>>>(g, ws);
+}
+void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
+    k_cids<<<grid_for(g.ntiles, 128, sms * 8), 128, 0, s>>>(g, ws);
+}
+void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
+    const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;
+    k_parents<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
+    k_tops<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
+    k_fold<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
+}
+void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s) {
+    k_emit<<<g.ntiles, NT, sizeof(EmitSmem), s>>>(g, ws);
+}
+void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
+                       cudaStream_t s, int sms) {
+    k_surv_flags_img<<<grid_for((int64_t)total, 256, sms * 8), 256, 0, s>>>(top, cbase, B, total, flag);
+}
+void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, const uint64_t* cbase,
+                  cudaStream_t s, int sms) {
+    k_remap_labels<<<grid_for(P * B, 256, sms * 16), 256, 0, s>>>(labels, P, B, rank, cbase);
+}
+
+}  // namespace rlg

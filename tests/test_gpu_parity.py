@@ -1,0 +1,73 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle, bit-exact.
+
+Corpus modelled on the reference's acceptance corpus (acceptance.cpp:61-153: sizes 1x1..64x64,
+g in {1,2,4,8}, d in 0..1, both connectivities) plus multi-tile images that exercise the
+cross-tile merge (tile = 32 x 256), ragged widths (scalar I/O path), batches, and the
+structured nesting generator of config 3.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2006_09299_b200 import LabelingConfig
+from tests.parity_util import compare_image
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [(1, 1), (1, 7), (7, 1), (2, 2), (3, 5), (8, 8), (13, 9), (16, 16), (29, 23), (31, 33),
+         (47, 61), (64, 64), (64, 1)]
+
+
+def _check_batch(labeler, imgs, conn, where):
+    cfg = LabelingConfig(connectivity=conn, relabel=True)
+    res = labeler.label_batch(imgs, cfg)
+    for i in range(imgs.shape[0]):
+        ref = O.label_canonical(imgs[i], conn, want_labels=True)
+        compare_image(res.image(i), ref, f"{where} #{i}")
+
+
+@pytest.mark.parametrize("conn", [0, 1])
+@pytest.mark.parametrize("w,h", SIZES)
+def test_acceptance_corpus(labeler, conn, w, h):
+    imgs = []
+    for g in (1, 2, 4, 8):
+        if g > min(w, h):
+            continue
+        for d in (0.0, 0.1, 0.3, 0.5, 0.7, 0.9, 1.0):
+            for seed in (1, 2):
+                imgs.append(O.generate(w, h, d, g, seed * 1000 + g))
+    _check_batch(labeler, np.stack(imgs), conn, f"{w}x{h} conn{conn}")
+
+
+@pytest.mark.parametrize("conn", [0, 1])
+@pytest.mark.parametrize("w,h,d,g", [
+    (300, 70, 0.5, 1), (300, 70, 0.45, 2), (513, 97, 0.5, 1), (257, 33, 0.6, 1),
+    (256, 32, 0.5, 1), (512, 64, 0.55, 3), (1000, 333, 0.5, 2), (777, 129, 0.4, 1),
+    (1024, 1024, 0.5, 1), (640, 480, 0.3, 4), (640, 480, 0.75, 1)])
+def test_multi_tile(labeler, conn, w, h, d, g):
+    img = O.generate(w, h, d, g, 7 + w + h)
+    _check_batch(labeler, img[None], conn, f"{w}x{h} d{d} g{g}")
+
+
+def test_batch_mixed(labeler):
+    imgs = np.stack([O.generate(520, 96, d, g, 100 + i)
+                     for i, (d, g) in enumerate([(0.1, 1), (0.5, 1), (0.9, 2), (0.5, 8), (0.0, 1), (1.0, 1)])])
+    _check_batch(labeler, imgs, 0, "batch")
+
+
+def test_nested_rings(labeler):
+    img = O.generate_rings(512, 512, 64, 3, 0.02)
+    _check_batch(labeler, img[None], 0, "rings")
+    img = O.generate_rings(512, 512, 64, 5, 0.0)
+    _check_batch(labeler, img[None], 0, "rings-clean")
+
+
+def test_cfg2_cells(labeler):
+    """A few full-size 2048^2 cells of BASELINE config 2."""
+    imgs = np.stack([O.generate(2048, 2048, d, g, 1) for d, g in [(0.5, 1), (0.75, 1), (0.5, 4), (0.35, 16)]])
+    res = labeler.label_batch(imgs, LabelingConfig())
+    for i in range(imgs.shape[0]):
+        ref = O.label_canonical(imgs[i], 0)
+        compare_image(res.image(i), ref, f"cfg2 #{i}")
