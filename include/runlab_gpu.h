@@ -39,6 +39,7 @@ extern "C" {
 #define RL_ECUDA 4     /* std::runtime_error */
 #define RL_ENOMEM 5    /* std::bad_alloc */
 #define RL_EINTERNAL 6 /* std::runtime_error (invariant violated on device) */
+#define RL_ENOSPC 7    /* caller-provided output buffer too small (see comps_needed) */
 
 /* types.hpp:18-21 */
 #define RL_FG8_BG4 0
@@ -125,6 +126,38 @@ void* rl_device_comps(rl_ctx* ctx);
 void* rl_stream(rl_ctx* ctx);
 /* Bind the context to an external stream (e.g. torch's current stream); NULL = own. */
 int rl_set_stream(rl_ctx* ctx, void* stream);
+/* Caller-owned host outputs for rl_label_into (pinned memory makes the copies fast). */
+typedef struct rl_host_outputs {
+    uint8_t* filled_image;  /* [n*h*w] or NULL */
+    uint32_t* labels;       /* [n*h*w] or NULL (requires cfg.relabel) */
+    rl_component* comps;    /* [comp_capacity] or NULL */
+    uint32_t* top;          /* [comp_capacity] or NULL */
+    rl_features* filled;    /* [comp_capacity] or NULL */
+    int64_t comp_capacity;
+    int64_t* summary;       /* [n*5] C_pre, n_fg, n_holes, euler, C_post per image, or NULL */
+    int64_t* comp_offset;   /* [n+1] or NULL */
+    int64_t comps_needed;   /* out: total components of the batch */
+    int64_t h2d_bytes;      /* out: bytes copied host->device */
+    int64_t d2h_bytes;      /* out: bytes copied device->host */
+} rl_host_outputs;
+
+/* Host-buffer entry point with caller-owned outputs: H2D copy of the pixels, pipeline, D2H
+ * copy of every non-NULL output, one stream sync.  RL_ENOSPC if comp_capacity is too small
+ * (comps_needed tells the size; the non-component outputs are still filled). */
+int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t width, int32_t height,
+                  int32_t n_images, const rl_config* cfg, rl_host_outputs* out);
+
+/* Per-phase device times of the call `back` calls ago (0 = last; back < 64). */
+int rl_phase_times(const rl_ctx* ctx, int back, rl_times* out);
+
+/* Device-side input generators (BASELINE configs), bit-identical to the reference's
+ * generate() (generator.hpp:46-83).  stream: cudaStream_t or NULL; d_out: w*h bytes. */
+int rl_generate(void* stream, uint8_t* d_out, int32_t w, int32_t h, double density, int32_t g,
+                uint64_t seed);
+int rl_generate_rings(void* stream, uint8_t* d_out, int32_t w, int32_t h, int32_t tile,
+                      uint64_t seed, double salt);
+void rl_cfg4_params(uint64_t i, double* density, int32_t* g);
+
 /* Number of kernel launches the last pipeline enqueued. */
 int rl_last_launch_count(const rl_ctx* ctx);
 

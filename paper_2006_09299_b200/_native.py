@@ -18,7 +18,8 @@ RL_OK, RL_EINVAL, RL_ELOGIC, RL_EOVERFLOW, RL_ECUDA, RL_ENOMEM, RL_EINTERNAL = r
 EXPORTED_SYMBOLS = (
     "rl_create", "rl_destroy", "rl_last_error", "rl_label", "rl_result_free", "rl_label_device",
     "rl_sync", "rl_fetch", "rl_device_filled_image", "rl_device_labels", "rl_device_comps",
-    "rl_stream", "rl_set_stream", "rl_last_launch_count", "rl_tile_shape",
+    "rl_stream", "rl_set_stream", "rl_last_launch_count", "rl_tile_shape", "rl_label_into",
+    "rl_phase_times", "rl_generate", "rl_generate_rings", "rl_cfg4_params",
 )
 
 FEATURE_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),
@@ -45,6 +46,13 @@ class RlResult(C.Structure):
                 ("euler", C.c_void_p), ("n_survivors", C.c_void_p), ("comp_offset", C.c_void_p),
                 ("comps", C.c_void_p), ("top", C.c_void_p), ("filled", C.c_void_p),
                 ("filled_image", C.c_void_p), ("labels", C.c_void_p), ("times", RlTimes)]
+
+
+class RlHostOutputs(C.Structure):
+    _fields_ = [("filled_image", C.c_void_p), ("labels", C.c_void_p), ("comps", C.c_void_p),
+                ("top", C.c_void_p), ("filled", C.c_void_p), ("comp_capacity", C.c_int64),
+                ("summary", C.c_void_p), ("comp_offset", C.c_void_p), ("comps_needed", C.c_int64),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 _lib = None
@@ -77,6 +85,14 @@ def load() -> C.CDLL:
     L.rl_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     L.rl_last_launch_count.argtypes = [C.c_void_p]
     L.rl_tile_shape.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.rl_label_into.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                C.POINTER(RlConfig), C.POINTER(RlHostOutputs)]
+    L.rl_phase_times.argtypes = [C.c_void_p, C.c_int, C.POINTER(RlTimes)]
+    L.rl_generate.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_int32,
+                              C.c_uint64]
+    L.rl_generate_rings.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_uint64, C.c_double]
+    L.rl_cfg4_params.argtypes = [C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
     _lib = L
     return L
 

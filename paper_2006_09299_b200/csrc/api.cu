@@ -77,7 +77,10 @@ struct rl_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     std::string err;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // events of the current call
+    static constexpr int RING = 64;
+    cudaEvent_t ring[RING][4] = {};
+    int64_t calls = 0;
     // workspace
     DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
     DevBuf cnt, off, counters, img_fg, img_surv, comps, top, filled, filled_img, labels, pix;
@@ -94,6 +97,7 @@ struct rl_ctx {
     const uint8_t* last_pix = nullptr;
     int launches = 0;
     bool have_result = false;
+    bool reran = false;  // finish() had to grow a capacity and re-run
 };
 
 namespace {
@@ -214,6 +218,14 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     ws.labels = g.label_mode ? P<uint32_t>(ctx->labels) : nullptr;
 
     cudaStream_t s = ctx->stream;
+    {
+        const int slot = (int)(ctx->calls % rl_ctx::RING);
+        for (int k = 0; k < 4; ++k) {
+            if (!ctx->ring[slot][k]) cudaEventCreate(&ctx->ring[slot][k]);
+            ctx->ev[k] = ctx->ring[slot][k];
+        }
+        ++ctx->calls;
+    }
     int launches = 0;
     cudaMemsetAsync(ws.counters, 0, 64, s);
     cudaMemsetAsync(ws.img_fg, 0, (size_t)B * 4, s);
@@ -273,6 +285,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
 
 // Wait for the last enqueue; on capacity overflow grow and re-run (synchronously).
 int finish(rl_ctx* ctx) {
+    ctx->reran = false;
     for (int attempt = 0; attempt < 4; ++attempt) {
         const cudaError_t e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pipeline");
@@ -291,6 +304,7 @@ int finish(rl_ctx* ctx) {
             grow = true;
         }
         if (!grow) return RL_OK;
+        ctx->reran = true;
         const rl_config cfg = ctx->cfg;
         const int rc = enqueue(ctx, ctx->last_pix, ctx->geo.W, ctx->geo.H, ctx->geo.B, &cfg);
         if (rc) return rc;
@@ -381,7 +395,6 @@ rl_ctx* rl_create(int device) {
         return nullptr;
     }
     c->stream = c->own_stream;
-    for (auto& e : c->ev) cudaEventCreate(&e);
     return c;
 }
 
@@ -397,8 +410,9 @@ void rl_destroy(rl_ctx* c) {
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_summ) cudaFreeHost(c->h_summ);
-    for (auto& e : c->ev)
-        if (e) cudaEventDestroy(e);
+    for (auto& slot : c->ring)
+        for (auto& e : slot)
+            if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -441,6 +455,99 @@ int rl_label(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n
     rc = finish(ctx);
     if (rc) return rc;
     return fetch(ctx, out);
+}
+
+int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+                  rl_host_outputs* out) {
+    if (!out) return RL_EINVAL;
+    out->comps_needed = 0;
+    out->h2d_bytes = out->d2h_bytes = 0;
+    int rc = check_args(ctx, w, h, n, cfg);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    const size_t npx = (size_t)w * h * n;
+    if (!ensure(ctx->pix, npx)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    cudaStream_t st = ctx->stream;
+    cudaError_t e = cudaMemcpyAsync(ctx->pix.p, pixels, npx, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "copy in");
+    out->h2d_bytes = (int64_t)npx;
+    rc = enqueue(ctx, P<uint8_t>(ctx->pix), w, h, n, cfg);
+    if (rc) return rc;
+    // outputs whose size does not depend on the result go out on the same stream
+    int64_t d2h = 0;
+    if (out->filled_image) {
+        cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
+        d2h += (int64_t)npx;
+    }
+    if (out->labels && ctx->geo.label_mode) {
+        cudaMemcpyAsync(out->labels, ctx->ws.labels, npx * 4, cudaMemcpyDeviceToHost, st);
+        d2h += (int64_t)npx * 4;
+    }
+    rc = finish(ctx);  // syncs; reruns (and recopies above outputs' sources) on overflow
+    if (rc) return rc;
+    if (ctx->reran) {
+        // a capacity grew and the pipeline re-ran after the copies above: copy again
+        if (out->filled_image)
+            cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
+        if (out->labels && ctx->geo.label_mode)
+            cudaMemcpyAsync(out->labels, ctx->ws.labels, npx * 4, cudaMemcpyDeviceToHost, st);
+    }
+    const int B = ctx->geo.B;
+    const int64_t* s = ctx->h_summ;
+    const int64_t total = s[4 * B];
+    out->comps_needed = total;
+    d2h += (int64_t)(B + 1) * 32;
+    if (out->summary)
+        for (int b = 0; b < B; ++b) {
+            const int64_t cp = s[4 * b + 1], fg = s[4 * b + 2];
+            out->summary[5 * b + 0] = cp;
+            out->summary[5 * b + 1] = fg;
+            out->summary[5 * b + 2] = cp - 1 - fg;
+            out->summary[5 * b + 3] = fg - (cp - 1 - fg);
+            out->summary[5 * b + 4] = s[4 * b + 3];
+        }
+    if (out->comp_offset) {
+        for (int b = 0; b < B; ++b) out->comp_offset[b] = s[4 * b];
+        out->comp_offset[B] = total;
+    }
+    const bool want_comps = out->comps || out->top || out->filled;
+    if (want_comps && total > out->comp_capacity) {
+        out->d2h_bytes = d2h;
+        return set_err(ctx, RL_ENOSPC, "component buffers too small");
+    }
+    if (out->comps) {
+        cudaMemcpyAsync(out->comps, ctx->ws.comps, sizeof(rl_component) * total, cudaMemcpyDeviceToHost, st);
+        d2h += (int64_t)sizeof(rl_component) * total;
+    }
+    if (out->top) {
+        cudaMemcpyAsync(out->top, ctx->ws.top, 4 * total, cudaMemcpyDeviceToHost, st);
+        d2h += 4 * total;
+    }
+    if (out->filled) {
+        cudaMemcpyAsync(out->filled, ctx->ws.filled, sizeof(rl_features) * total, cudaMemcpyDeviceToHost, st);
+        d2h += (int64_t)sizeof(rl_features) * total;
+    }
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "copy out");
+    out->d2h_bytes = d2h;
+    return RL_OK;
+}
+
+int rl_phase_times(const rl_ctx* ctx, int back, rl_times* out) {
+    if (!ctx || !out || back < 0 || back >= rl_ctx::RING || back >= ctx->calls) return RL_EINVAL;
+    const int slot = (int)((ctx->calls - 1 - back) % rl_ctx::RING);
+    cudaEvent_t const* ev = ctx->ring[slot];
+    float a = 0, m = 0, e = 0, t = 0;
+    if (cudaEventElapsedTime(&a, ev[0], ev[1]) != cudaSuccess || cudaEventElapsedTime(&m, ev[1], ev[2]) != cudaSuccess ||
+        cudaEventElapsedTime(&e, ev[2], ev[3]) != cudaSuccess || cudaEventElapsedTime(&t, ev[0], ev[3]) != cudaSuccess) {
+        cudaGetLastError();
+        return RL_ECUDA;
+    }
+    out->analyze_ms = a;
+    out->merge_ms = m;
+    out->emit_ms = e;
+    out->total_ms = t;
+    return RL_OK;
 }
 
 void rl_result_free(rl_result* r) {

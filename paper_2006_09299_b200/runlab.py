@@ -226,6 +226,26 @@ class Labeler:
         finally:
             self._L.rl_result_free(C.byref(res))
 
+    def label_into(self, pixels_ptr: int, w: int, h: int, n: int, config: LabelingConfig,
+                   outs: N.RlHostOutputs) -> N.RlHostOutputs:
+        """rl_label_into: host pixels in, caller-owned host outputs (the e2e entry point)."""
+        cfg = config.to_c()
+        rc = self._L.rl_label_into(self._ctx, C.c_void_p(pixels_ptr), w, h, n, C.byref(cfg),
+                                   C.byref(outs))
+        if rc != N.RL_OK:
+            _raise(rc, self._err())
+        return outs
+
+    def phase_times(self, back: int = 0) -> StepTimes:
+        t = N.RlTimes()
+        rc = self._L.rl_phase_times(self._ctx, back, C.byref(t))
+        if rc != N.RL_OK:
+            _raise(rc, "phase times unavailable")
+        return StepTimes(t.analyze_ms, t.merge_ms, t.emit_ms, t.total_ms)
+
+    def stream(self) -> int:
+        return int(self._L.rl_stream(self._ctx) or 0)
+
     def launch_count(self) -> int:
         return int(self._L.rl_last_launch_count(self._ctx))
 
@@ -381,3 +401,36 @@ def euler_number(res: LabelingResult) -> int:
     if res.euler is None:
         raise LogicError("euler_number: labeling ran without compute_euler")
     return int(res.euler)
+
+
+# ---------------------------------------------------------------------------------------
+# device-side input generators (generator.hpp:46-83 and the BASELINE configs)
+# ---------------------------------------------------------------------------------------
+def generate_device(d_ptr: int, w: int, h: int, density: float, g: int, seed: int,
+                    stream: int | None = None) -> None:
+    """generate() on the device into w*h bytes at d_ptr (bit-identical to the reference)."""
+    rc = N.load().rl_generate(C.c_void_p(stream or 0), C.c_void_p(d_ptr), w, h, float(density), g,
+                              seed & (2**64 - 1))
+    if rc != N.RL_OK:
+        _raise(rc, "generate: invalid spec" if rc == N.RL_EINVAL else "generate failed")
+
+
+def generate_rings_device(d_ptr: int, w: int, h: int, tile: int = 64, seed: int = 3,
+                          salt: float = 0.02, stream: int | None = None) -> None:
+    """Config-3 nested-ring image on the device."""
+    rc = N.load().rl_generate_rings(C.c_void_p(stream or 0), C.c_void_p(d_ptr), w, h, tile, seed,
+                                    float(salt))
+    if rc != N.RL_OK:
+        _raise(rc, "generate_rings failed")
+
+
+def cfg4_params(i: int) -> tuple[float, int]:
+    d = C.c_double()
+    g = C.c_int32()
+    N.load().rl_cfg4_params(i, C.byref(d), C.byref(g))
+    return d.value, g.value
+
+
+def cfg2_cells() -> list[tuple[float, int]]:
+    """BASELINE config 2: density k/20 (k = 0..20) x granularity {1,2,4,8,16}."""
+    return [(k / 20.0, g) for k in range(21) for g in (1, 2, 4, 8, 16)]
