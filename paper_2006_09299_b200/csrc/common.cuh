@@ -22,7 +22,7 @@ constexpr int MAXLC = MAXRUNS;         // tile-local components <= runs
 constexpr int PERIM = 2 * TW + 2 * TH; // perimeter label slots: top, bottom, left, right
 constexpr int NBMAX = PERIM;           // border components per tile <= perimeter pixels
 constexpr int FCH = 512;               // interior-feature accumulator chunk (K1b)
-constexpr uint32_t TAG = 0x80000000u;  // run-parent slot holds a tile-component index
+constexpr uint32_t TAG16 = 0x8000u;    // run-parent slot holds a tile-component index
 constexpr uint16_t PERIM_NONE = 0xFFFF;
 
 static_assert(MAXRUNS <= 32768, "local ids must fit 15 bits");
@@ -32,6 +32,7 @@ static_assert(TW == 256, "lcpos packs the column in 8 bits");
 constexpr uint32_t ERR_NODE_CAP = 1u;
 constexpr uint32_t ERR_COMP_CAP = 2u;
 constexpr uint32_t ERR_INTERNAL = 4u;
+// counters[2]: tiles deferred to the full-capacity kernels (overflow list length)
 
 // Global feature accumulator: exactly rl_features (40 B).
 using Acc = rl_features;
@@ -78,7 +79,8 @@ struct Ws {
     // canonical numbering
     uint32_t* cnt;       // [B*H*ntx + 1] roots whose first pixel is in (image,row,tile col)
     uint32_t* off;       // exclusive scan of cnt
-    uint32_t* counters;  // [0] nodes used, [1] error bits
+    uint32_t* counters;  // [0] nodes used, [1] error bits, [2] deferred tiles
+    uint32_t* ovf;       // [ntiles] deferred (run-heavy) tiles
     uint32_t* img_fg;    // [B] foreground components
     uint32_t* img_surv;  // [B] post-fill components (exterior included)
     uint32_t cap_nodes;
@@ -102,6 +104,20 @@ __device__ __forceinline__ TileGeom tile_geom(const Geo& g, int32_t t) {
     const int32_t rem = t - tg.b * g.tpi;
     tg.ty = rem / g.ntx;
     tg.tx = rem - tg.ty * g.ntx;
+    tg.x0 = tg.tx * TW;
+    tg.y0 = tg.ty * TH;
+    tg.tw = min(TW, g.W - tg.x0);
+    tg.th = min(TH, g.H - tg.y0);
+    return tg;
+}
+
+// tile of a CTA launched on the (ntx, nty, B) grid: no integer division
+__device__ __forceinline__ TileGeom tile_geom_grid(const Geo& g) {
+    TileGeom tg;
+    tg.tx = blockIdx.x;
+    tg.ty = blockIdx.y;
+    tg.b = blockIdx.z;
+    tg.t = (tg.b * g.nty + tg.ty) * g.ntx + tg.tx;
     tg.x0 = tg.tx * TW;
     tg.y0 = tg.ty * TH;
     tg.tw = min(TW, g.W - tg.x0);

@@ -25,8 +25,9 @@ namespace rlg {
 // ---------------------------------------------------------------------------------------
 // K1a: analyze
 // ---------------------------------------------------------------------------------------
+template <int MR>
 struct AnalyzeSmem {
-    CclSmem c;
+    CclSmem<MR> c;
     // border-component accumulators (tile-local coordinates)
     uint32_t bs[NBMAX], bsx[NBMAX], bsy[NBMAX];
     int32_t brmax[NBMAX], bcmin[NBMAX], bcmax[NBMAX];
@@ -34,11 +35,12 @@ struct AnalyzeSmem {
     uint32_t base;
 };
 
-__global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    AnalyzeSmem& A = *reinterpret_cast<AnalyzeSmem*>(smem_raw);
-    CclSmem& S = A.c;
-    const TileGeom tg = tile_geom(g, blockIdx.x);
+// Returns false when the tile exceeds the MR run capacity (then nothing was written for
+// it except the packed bits; the caller queues it for the full-capacity kernel).
+template <int MR>
+__device__ __forceinline__ bool analyze_tile(AnalyzeSmem<MR>& A, const uint8_t* __restrict__ pix, const Geo& g,
+                                             const Ws& ws, const TileGeom& tg) {
+    CclSmem<MR>& S = A.c;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
 
@@ -60,14 +62,7 @@ __global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix,
     S.x[tid] = x;
     S.vm[tid] = vm;
     ws.bits[(int64_t)tg.t * NW + tid] = x;
-    if (tid < NBMAX) {
-        A.bs[tid] = A.bsx[tid] = A.bsy[tid] = 0;
-        A.brmax[tid] = -1;
-        A.bcmin[tid] = 0x7FFFFFFF;
-        A.bcmax[tid] = -1;
-        A.bimg[tid] = 0;
-    }
-    for (int i = tid + NT; i < NBMAX; i += NT) {
+    for (int i = tid; i < NBMAX; i += NT) {
         A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
         A.brmax[i] = -1;
         A.bcmin[i] = 0x7FFFFFFF;
@@ -87,9 +82,9 @@ __global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix,
     }
     __syncthreads();
 
-    ccl_tile(S, tg);
+    if (!ccl_tile(S, tg)) return false;
 
-    const int nlc = S.nlc, nb = S.nb;
+    const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
     if (tid == 0) {
         const uint32_t base = atomicAdd(&ws.counters[0], (uint32_t)nb);
         A.base = base;
@@ -98,25 +93,25 @@ __global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix,
         ws.tnb[tg.t] = (uint32_t)nb;
     }
 
-    // ---- border-component features and image-border contact (run pieces)
+    // ---- border-component features and image-border contact (one lane per run)
     const bool top_img = tg.ty == 0, bot_img = (tg.y0 + tg.th == g.H);
     const bool left_img = tg.tx == 0, right_img = (tg.x0 + tg.tw == g.W);
-    for_each_piece(S, tid, [&](int ri, int j0, int j1) {
-        const uint32_t lc = lc_of_run(S, ri);
-        if (!lc_is_border(S, lc)) return;
+    for (int i = tid; i < nruns; i += NT) {
+        const uint32_t lc = lc_of_run(S, i);
+        if (!lc_is_border(S, lc)) continue;
         const int bi = S.lcb[lc];
-        const int c0 = 32 * w + j0, c1 = 32 * w + j1;  // [c0, c1) tile-local
+        const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
         const uint32_t n = (uint32_t)(c1 - c0);
         atomicAdd(&A.bs[bi], n);
         atomicAdd(&A.bsx[bi], n * (uint32_t)(c0 + c1 - 1) / 2u);
-        atomicAdd(&A.bsy[bi], n * (uint32_t)r);
-        atomicMax(&A.brmax[bi], r);
+        atomicAdd(&A.bsy[bi], n * (uint32_t)rr);
+        atomicMax(&A.brmax[bi], rr);
         atomicMin(&A.bcmin[bi], c0);
         atomicMax(&A.bcmax[bi], c1 - 1);
-        if ((top_img && r == 0) || (bot_img && r == tg.th - 1) || (left_img && c0 == 0) ||
+        if ((top_img && rr == 0) || (bot_img && rr == tg.th - 1) || (left_img && c0 == 0) ||
             (right_img && c1 == tg.tw))
             A.bimg[bi] = 1;
-    });
+    }
     __syncthreads();
 
     // ---- border-component nodes
@@ -125,7 +120,7 @@ __global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix,
     const int flip = g.flip;
     for (int i = tid; i < nb && node_ok; i += NT) {
         const int lc = S.blc[i];
-        const int fr = S.lcpos[lc] >> 8, fc = S.lcpos[lc] & 0xFF;
+        const int fr = lc_row(S, lc), fc = lc_col(S, lc);
         const uint32_t fg = xbit(S, fr, fc) ^ (uint32_t)flip;
         NodeRec rec;
         rec.tile = (uint32_t)tg.t;
@@ -194,11 +189,32 @@ __global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix,
     int nfg = 0;
     for (int l = tid; l < nlc; l += NT) {
         if (lc_is_border(S, l)) continue;
-        const int fr = S.lcpos[l] >> 8, fc = S.lcpos[l] & 0xFF;
-        nfg += (int)(xbit(S, fr, fc) ^ (uint32_t)flip);
+        nfg += (int)(xbit(S, lc_row(S, l), lc_col(S, l)) ^ (uint32_t)flip);
     }
     nfg = block_reduce_sum(nfg, S.wsum);
     if (tid == 0 && nfg) atomicAdd(&ws.img_fg[tg.b], (uint32_t)nfg);
+    return true;
+}
+
+// fast variant: one CTA per tile on the (ntx, nty, B) grid; run-heavy tiles are deferred
+__global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& A = *reinterpret_cast<AnalyzeSmem<MR_FAST>*>(smem_raw);
+    const TileGeom tg = tile_geom_grid(g);
+    if (!analyze_tile(A, pix, g, ws, tg) && threadIdx.x == 0)
+        ws.ovf[atomicAdd(&ws.counters[2], 1u)] = (uint32_t)tg.t;
+}
+
+// full-capacity variant over the deferred tiles (one run per pixel fits)
+__global__ void __launch_bounds__(NT) k_analyze_full(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& A = *reinterpret_cast<AnalyzeSmem<MAXRUNS>*>(smem_raw);
+    const uint32_t n = ws.counters[2];
+    for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+        const TileGeom tg = tile_geom(g, (int32_t)ws.ovf[k]);
+        analyze_tile(A, pix, g, ws, tg);
+        __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -452,8 +468,11 @@ __global__ void k_fold(Geo g, Ws ws) {
 // ---------------------------------------------------------------------------------------
 // K1b: emit
 // ---------------------------------------------------------------------------------------
+constexpr int FOLD_SLOTS = 64;  // distinct border fold targets per tile kept in smem
+
+template <int MR>
 struct EmitSmem {
-    CclSmem c;
+    CclSmem<MR> c;
     // interior-feature chunk accumulators (tile-local coordinates)
     uint32_t fs[FCH], fsx[FCH], fsy[FCH];
     int32_t frmax[FCH], fcmin[FCH], fcmax[FCH];
@@ -462,19 +481,23 @@ struct EmitSmem {
     uint32_t banc[NBMAX];   // canonical id of its post-fill root
     uint8_t bflag[NBMAX];   // bit0 representative, bit1 exterior
     uint16_t repx[NBMAX + 1];  // exclusive prefix of representative flags over border index
-    // fold of interior components into border-derived survivors, keyed by border index
-    uint32_t ps[NBMAX], psx[NBMAX], psy[NBMAX];
-    int32_t prmin[NBMAX], prmax[NBMAX], pcmin[NBMAX], pcmax[NBMAX];
+    // fold of interior components into border-derived survivors: small open-addressing
+    // table keyed by border index (overflow goes straight to global atomics)
+    uint16_t pkey[FOLD_SLOTS];
+    uint32_t ps[FOLD_SLOTS], psx[FOLD_SLOTS], psy[FOLD_SLOTS];
+    int32_t prmin[FOLD_SLOTS], prmax[FOLD_SLOTS], pcmin[FOLD_SLOTS], pcmax[FOLD_SLOTS];
+    uint32_t ext[NW];       // exterior-pixel masks of the tile words
     uint32_t rowoff[TH];    // canonical id offset of each tile row (relative to the image)
     uint64_t cb;
 };
 
 // canonical id of tile component lc (any kind)
-__device__ __forceinline__ uint32_t comp_cid(const EmitSmem& E, uint32_t lc) {
-    const CclSmem& S = E.c;
+template <class ES>
+__device__ __forceinline__ uint32_t comp_cid(const ES& E, uint32_t lc) {
+    const auto& S = E.c;
     const uint16_t lb = S.lcb[lc];
     if (!(lb & 0x8000u)) return E.bcid[lb];
-    const int r = S.lcpos[lc] >> 8;
+    const int r = lc_row(S, lc);
     const int bp = lb & 0x7FFF;                  // border components before lc
     const int rb0 = S.rowbx[r];
     const int nonrep_before = (bp - rb0) - (E.repx[bp] - E.repx[rb0]);
@@ -484,12 +507,12 @@ __device__ __forceinline__ uint32_t comp_cid(const EmitSmem& E, uint32_t lc) {
 // Walk the tree inside the tile: returns the post-fill root's canonical id of interior
 // component lc; `end` = border index where the walk left the tile interior, or -1 when lc's
 // chain reached the exterior (then `surv` is the interior survivor).
-__device__ __forceinline__ uint32_t interior_top(const EmitSmem& E, uint32_t lc, int& end, uint32_t& surv) {
-    const CclSmem& S = E.c;
+template <class ES>
+__device__ __forceinline__ uint32_t interior_top(const ES& E, uint32_t lc, int& end, uint32_t& surv) {
+    const auto& S = E.c;
     uint32_t cur = lc;
     for (;;) {
-        const int r = S.lcpos[cur] >> 8, c = S.lcpos[cur] & 0xFF;
-        const uint32_t p = lc_at(S, r, c - 1);  // interior: c >= 1
+        const uint32_t p = lc_at(S, lc_row(S, cur), lc_col(S, cur) - 1);  // interior: col >= 1
         const uint16_t pb = S.lcb[p];
         if (!(pb & 0x8000u)) {
             if (E.bflag[pb] & 2u) {  // parent is the exterior: cur survives
@@ -505,27 +528,49 @@ __device__ __forceinline__ uint32_t interior_top(const EmitSmem& E, uint32_t lc,
     }
 }
 
-__global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    EmitSmem& E = *reinterpret_cast<EmitSmem*>(smem_raw);
-    CclSmem& S = E.c;
-    if (ws.counters[1] || !comps_fit(g, ws)) return;
-    const TileGeom tg = tile_geom(g, blockIdx.x);
+// slot of border index `key` in the fold table, or -1 when the table is full
+template <class ES>
+__device__ __forceinline__ int fold_slot(ES& E, uint32_t key) {
+    uint32_t h = (key * 2654435761u) >> 26;  // 6 bits
+    for (int probe = 0; probe < FOLD_SLOTS; ++probe, h = (h + 1) & (FOLD_SLOTS - 1)) {
+        const unsigned short cur = E.pkey[h];
+        if (cur == key) return (int)h;
+        if (cur == 0xFFFF) {
+            const unsigned short prev = atomicCAS(reinterpret_cast<unsigned short*>(&E.pkey[h]),
+                                                  (unsigned short)0xFFFF, (unsigned short)key);
+            if (prev == 0xFFFF || prev == key) return (int)h;
+        }
+    }
+    return -1;
+}
+
+template <int MR>
+__device__ __forceinline__ bool emit_tile(EmitSmem<MR>& E, const Geo& g, const Ws& ws, const TileGeom& tg) {
+    CclSmem<MR>& S = E.c;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
     const uint32_t vm = valid_mask(tg, r, w);
     S.x[tid] = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
     S.vm[tid] = vm;
+    E.ext[tid] = 0;
     const int64_t img0 = (int64_t)tg.b * g.H * g.ntx;
     const uint32_t offimg = ws.off[img0];
     if (tid < TH && tid < tg.th)
         E.rowoff[tid] = ws.off[img0 + (int64_t)(tg.y0 + tid) * g.ntx + tg.tx] - offimg;
     if (tid == 0) E.cb = (uint64_t)offimg + (uint64_t)tg.b;
+    if (tid < FOLD_SLOTS) {
+        E.pkey[tid] = 0xFFFF;
+        E.ps[tid] = E.psx[tid] = E.psy[tid] = 0;
+        E.prmin[tid] = 0x7FFFFFFF;
+        E.prmax[tid] = -1;
+        E.pcmin[tid] = 0x7FFFFFFF;
+        E.pcmax[tid] = -1;
+    }
     __syncthreads();
 
-    ccl_tile(S, tg);
+    if (!ccl_tile(S, tg)) return false;
 
-    const int nlc = S.nlc, nb = S.nb;
+    const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
     const uint64_t cb = E.cb;
     const uint32_t nbase = (uint32_t)g.B + ws.tbase[tg.t];
     for (int i = tid; i < nb; i += NT) {
@@ -535,22 +580,36 @@ __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
         E.bcid[i] = ws.nrootcid[root];
         E.banc[i] = ext ? 0u : ws.nanccid[root];
         E.bflag[i] = (uint8_t)((ws.nrep[node] ? 1u : 0u) | (ext ? 2u : 0u));
-        E.ps[i] = E.psx[i] = E.psy[i] = 0;
-        E.prmin[i] = 0x7FFFFFFF;
-        E.prmax[i] = -1;
-        E.pcmin[i] = 0x7FFFFFFF;
-        E.pcmax[i] = -1;
     }
     __syncthreads();
-    if (tid == 0) {  // tiny serial prefix (nb <= NBMAX)
-        uint16_t acc = 0;
-        for (int i = 0; i < nb; ++i) {
-            E.repx[i] = acc;
-            acc += E.bflag[i] & 1u;
+    if (tid < 32) {  // warp prefix of representative flags over border index
+        int carry = 0;
+        for (int i0 = 0; i0 <= nb; i0 += 32) {
+            const int i = i0 + tid;
+            const int f = (i < nb) ? (E.bflag[i] & 1) : 0;
+            int incl = f;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int n = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (tid >= o) incl += n;
+            }
+            if (i <= nb) E.repx[i] = (uint16_t)(carry + incl - f);
+            carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
-        E.repx[nb] = acc;
     }
     __syncthreads();
+
+    // ---- exterior pixels (for the hole-filled image), one lane per run
+    for (int i = tid; i < nruns; i += NT) {
+        const uint16_t lb = S.lcb[lc_of_run(S, i)];
+        if ((lb & 0x8000u) || !(E.bflag[lb] & 2u)) continue;
+        const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
+        for (int wd = c0 >> 5; wd <= ((c1 - 1) >> 5); ++wd) {
+            const int lo = max(c0 - 32 * wd, 0), hi = min(c1 - 32 * wd, 32);
+            const uint32_t m = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+            atomicOr(&E.ext[rr * WPR + wd], m);
+        }
+    }
 
     // ---- interior components, in chunks of FCH tile components
     const int flip = g.flip;
@@ -564,25 +623,25 @@ __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
             E.fcmax[i] = -1;
         }
         __syncthreads();
-        for_each_piece(S, tid, [&](int ri, int j0, int j1) {
-            const uint32_t lc = lc_of_run(S, ri);
-            if ((int)lc < l0 || (int)lc >= l1 || lc_is_border(S, lc)) return;
+        for (int i = tid; i < nruns; i += NT) {
+            const uint32_t lc = lc_of_run(S, i);
+            if ((int)lc < l0 || (int)lc >= l1 || lc_is_border(S, lc)) continue;
             const int k = (int)lc - l0;
-            const int c0 = 32 * w + j0, c1 = 32 * w + j1;
+            const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
             const uint32_t n = (uint32_t)(c1 - c0);
             atomicAdd(&E.fs[k], n);
             atomicAdd(&E.fsx[k], n * (uint32_t)(c0 + c1 - 1) / 2u);
-            atomicAdd(&E.fsy[k], n * (uint32_t)r);
-            atomicMax(&E.frmax[k], r);
+            atomicAdd(&E.fsy[k], n * (uint32_t)rr);
+            atomicMax(&E.frmax[k], rr);
             atomicMin(&E.fcmin[k], c0);
             atomicMax(&E.fcmax[k], c1 - 1);
-        });
+        }
         __syncthreads();
         // pre-fill records, post-fill roots, survivor init
         for (int lc = l0 + tid; lc < l1; lc += NT) {
             if (lc_is_border(S, lc)) continue;
             const int k = lc - l0;
-            const int fr = S.lcpos[lc] >> 8, fc = S.lcpos[lc] & 0xFF;
+            const int fr = lc_row(S, lc), fc = lc_col(S, lc);
             const uint32_t cid = comp_cid(E, (uint32_t)lc);
             const uint32_t pcid = comp_cid(E, lc_at(S, fr, fc - 1));
             int end;
@@ -616,15 +675,16 @@ __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
             const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
             const uint32_t cid = comp_cid(E, (uint32_t)lc);
             if (anc == cid) continue;
-            const int fr = S.lcpos[lc] >> 8;
-            if (end >= 0) {
-                atomicAdd(&E.ps[end], E.fs[k]);
-                atomicAdd(&E.psx[end], E.fsx[k]);
-                atomicAdd(&E.psy[end], E.fsy[k]);
-                atomicMin(&E.prmin[end], fr);
-                atomicMax(&E.prmax[end], E.frmax[k]);
-                atomicMin(&E.pcmin[end], E.fcmin[k]);
-                atomicMax(&E.pcmax[end], E.fcmax[k]);
+            const int fr = lc_row(S, lc);
+            const int slot = end >= 0 ? fold_slot(E, (uint32_t)end) : -1;
+            if (slot >= 0) {
+                atomicAdd(&E.ps[slot], E.fs[k]);
+                atomicAdd(&E.psx[slot], E.fsx[k]);
+                atomicAdd(&E.psy[slot], E.fsy[k]);
+                atomicMin(&E.prmin[slot], fr);
+                atomicMax(&E.prmax[slot], E.frmax[k]);
+                atomicMin(&E.pcmin[slot], E.fcmin[k]);
+                atomicMax(&E.pcmax[slot], E.fcmax[k]);
             } else {
                 Acc f;
                 const int64_t s = E.fs[k];
@@ -641,8 +701,8 @@ __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
         __syncthreads();
     }
     // flush border-keyed folds (the survivors were initialised by k_tops)
-    for (int i = tid; i < nb; i += NT) {
-        if (!E.ps[i]) continue;
+    for (int i = tid; i < FOLD_SLOTS; i += NT) {
+        if (E.pkey[i] == 0xFFFF || !E.ps[i]) continue;
         Acc f;
         const int64_t s = E.ps[i];
         f.s = s;
@@ -652,23 +712,14 @@ __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
         f.row_max = tg.y0 + E.prmax[i];
         f.col_min = tg.x0 + E.pcmin[i];
         f.col_max = tg.x0 + E.pcmax[i];
-        acc_atomic_fold(ws.filled + cb + E.banc[i], f);
+        acc_atomic_fold(ws.filled + cb + E.banc[E.pkey[i]], f);
     }
-    nsurv = block_reduce_sum(nsurv, S.wsum);
+    nsurv = block_reduce_sum(nsurv, S.wsum);  // also orders the ext-mask atomics before use
     if (tid == 0 && nsurv) atomicAdd(&ws.img_surv[tg.b], (uint32_t)nsurv);
 
     // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
     if (vm) {
-        uint32_t ext = 0;
-        for_each_piece(S, tid, [&](int ri, int j0, int j1) {
-            const uint32_t lc = lc_of_run(S, ri);
-            const uint16_t lb = S.lcb[lc];
-            if (!(lb & 0x8000u) && (E.bflag[lb] & 2u)) {
-                const uint32_t m = (j1 >= 32 ? 0xFFFFFFFFu : ((1u << j1) - 1u)) & ~((1u << j0) - 1u);
-                ext |= m;
-            }
-        });
-        const uint32_t fillbits = vm & ~ext;
+        const uint32_t fillbits = vm & ~E.ext[tid];
         uint8_t* dst = ws.filled_img + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
         if (g.vec_ok && vm == 0xFFFFFFFFu) {
             uint4 o0, o1;
@@ -687,25 +738,45 @@ __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
             const int n = 32 - __clz(vm);
             for (int j = 0; j < n; ++j) dst[j] = (uint8_t)((fillbits >> j) & 1u);
         }
-        // ---- optional label image (Alg. 4 relabel, canonical ids)
-        if (g.label_mode) {
-            uint32_t* ldst = ws.labels + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
-            for_each_piece(S, tid, [&](int ri, int j0, int j1) {
-                const uint32_t lc = lc_of_run(S, ri);
-                uint32_t v = comp_cid(E, lc);
-                if (g.label_mode == 2) {
-                    const uint16_t lb = S.lcb[lc];
-                    if (!(lb & 0x8000u)) {
-                        v = (E.bflag[lb] & 2u) ? 0u : E.banc[lb];
-                    } else {
-                        int end;
-                        uint32_t surv;
-                        v = interior_top(E, lc, end, surv);
-                    }
+    }
+    // ---- optional label image (Alg. 4 relabel, canonical ids), one lane per run
+    if (g.label_mode) {
+        for (int i = tid; i < nruns; i += NT) {
+            const uint32_t lc = lc_of_run(S, i);
+            uint32_t v = comp_cid(E, lc);
+            if (g.label_mode == 2) {
+                const uint16_t lb = S.lcb[lc];
+                if (!(lb & 0x8000u)) {
+                    v = (E.bflag[lb] & 2u) ? 0u : E.banc[lb];
+                } else {
+                    int end;
+                    uint32_t surv;
+                    v = interior_top(E, lc, end, surv);
                 }
-                for (int j = j0; j < j1; ++j) ldst[j] = v;
-            });
+            }
+            const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
+            uint32_t* ldst = ws.labels + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + rr) * g.W + tg.x0;
+            for (int j = c0; j < c1; ++j) ldst[j] = v;
         }
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ws.counters[1] || !comps_fit(g, ws)) return;
+    auto& E = *reinterpret_cast<EmitSmem<MR_FAST>*>(smem_raw);
+    emit_tile(E, g, ws, tile_geom_grid(g));  // run-heavy tiles: k_emit_full
+}
+
+__global__ void __launch_bounds__(NT) k_emit_full(Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ws.counters[1] || !comps_fit(g, ws)) return;
+    auto& E = *reinterpret_cast<EmitSmem<MAXRUNS>*>(smem_raw);
+    const uint32_t n = ws.counters[2];
+    for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+        emit_tile(E, g, ws, tile_geom(g, (int32_t)ws.ovf[k]));
+        __syncthreads();
     }
 }
 
@@ -748,14 +819,21 @@ __global__ void k_surv_flags_img(const uint32_t* top, const uint64_t* cbase, int
 // ---------------------------------------------------------------------------------------
 namespace rlg {
 
-size_t analyze_smem() { return sizeof(AnalyzeSmem); }
-size_t emit_smem() { return sizeof(EmitSmem); }
+size_t analyze_smem() { return sizeof(AnalyzeSmem<MR_FAST>); }
+size_t emit_smem() { return sizeof(EmitSmem<MR_FAST>); }
 
 cudaError_t configure_kernels() {
     cudaError_t e = cudaFuncSetAttribute(k_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(AnalyzeSmem));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem));
+                                         (int)sizeof(AnalyzeSmem<MR_FAST>));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_analyze_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(AnalyzeSmem<MAXRUNS>));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem<MR_FAST>));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_emit_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(EmitSmem<MAXRUNS>));
+    return e;
 }
 
 static int grid_for(int64_t n, int block, int maxgrid) {
@@ -766,7 +844,9 @@ static int grid_for(int64_t n, int block, int maxgrid) {
 }
 
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
-    k_analyze<<<g.ntiles, NT, sizeof(AnalyzeSmem), s>>>(pix, g, ws);
+    k_analyze<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(AnalyzeSmem<MR_FAST>), s>>>(pix, g, ws);
+    // deferred run-heavy tiles (the grid loops over the device-side list; usually empty)
+    k_analyze_full<<<148, NT, sizeof(AnalyzeSmem<MAXRUNS>), s>>>(pix, g, ws);
 }
 void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
     if (g.nty > 1) {
@@ -794,7 +874,8 @@ void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
     k_fold<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
 }
 void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s) {
-    k_emit<<<g.ntiles, NT, sizeof(EmitSmem), s>>>(g, ws);
+    k_emit<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(EmitSmem<MR_FAST>), s>>>(g, ws);
+    k_emit_full<<<148, NT, sizeof(EmitSmem<MAXRUNS>), s>>>(g, ws);
 }
 void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
                        cudaStream_t s, int sms) {

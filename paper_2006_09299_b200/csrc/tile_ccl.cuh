@@ -11,55 +11,87 @@
 //    raster-order index inside the tile, so every root is its component's raster-first run
 //    and tile-local component ids come out in raster order of first pixel (App. A R4).
 //
-// B200 formulation: one thread per 32-pixel word; run starts come from `x ^ (x << 1)`
-// bit algebra; every overlap of two runs contributes exactly one union event, found with
-// bit masks (vertical contact at the first overlapping column, i.e. at a run start of
-// either row; plus diagonal-only contacts for the 8-connected value); union-find is
-// lock-free (atomicMin linking, path halving) on a shared-memory parent array.
+// B200 formulation (one thread per 32-pixel word, one warp = 32/WPR tile rows):
+//  * run starts are bit algebra on the packed row (`x & ~(x << 1 | carry)`), run indices a
+//    block scan of popcounts; the run list (`runpos`) then drives every per-run phase with
+//    all lanes busy (no per-lane loops of data-dependent length);
+//  * every overlap of two runs contributes exactly one union event, found with bit masks
+//    (vertical contact at the first overlapping column, i.e. at a run start of either row,
+//    plus diagonal-only contacts for the 8-connected value).  Each warp compacts its events
+//    into a shared queue and resolves them lane-parallel;
+//  * union-find is lock-free on a shared-memory parent array (atomicMin linking toward the
+//    smaller run index, path halving).
 #pragma once
 
 #include "common.cuh"
 
 namespace rlg {
 
+constexpr int EVCAP = 32 * (32 / WPR) * WPR;  // events per warp <= one per pixel of its rows
+
+// MR = run capacity of the shared-memory tables.  The fast variant is sized for realistic
+// inputs (<= MR_FAST runs per tile, > 0.62 runs/pixel never happens for random images);
+// tiles beyond it are re-run by the full-capacity variant (MAXRUNS = one run per pixel).
+constexpr int MR_FAST = 5120;
+
+template <int MR>
 struct CclSmem {
+    static constexpr int kRuns = MR;
     uint32_t x[NW];            // 8-connected-value bits (pixel value XOR flip), 0 where invalid
     uint32_t vm[NW];           // valid-pixel masks
     uint32_t st[NW];           // run-start masks
     uint16_t rbase[NW + 1];    // first run index of each word
-    uint16_t lbase[NW + 1];    // first tile-component index among the word's root runs
-    uint16_t rowlc[TH + 1];    // first tile-component index of each row
+    uint16_t rowlc[TH + 1];    // first tile component of each row
     uint16_t rowbx[TH + 1];    // border components before each row start
-    uint32_t par[MAXRUNS];     // union-find parent; afterwards TAG | component of each run
-    uint16_t lcpos[MAXLC];     // first pixel (row << 8) | col of each tile component
-    uint16_t lcb[MAXLC];       // border index, or 0x8000 | (border components before it)
+    uint16_t runpos[MR];       // (row << 8) | col of each run start, raster order
+    uint16_t par[MR];          // union-find parent; afterwards TAG | component of each run
+    union {
+        struct {
+            uint16_t lcrun[MR];     // root (first) run of each tile component
+            uint16_t lcb[MR];       // border index, or 0x8000 | (border components before it)
+        };
+        uint16_t evq[NWARPS][EVCAP];  // union-event queues (dead before lcrun/lcb are written)
+    };
     uint16_t blc[NBMAX];       // border index -> tile component
     int wsum[NWARPS + 1];
     int nruns, nlc, nb;
 };
 
-__device__ __forceinline__ int run_at(const CclSmem& S, int word, int bit) {
+template <class SM>
+__device__ __forceinline__ int run_at(const SM& S, int word, int bit) {
     return (int)S.rbase[word] + __popc(S.st[word] & (0xFFFFFFFFu >> (31 - bit))) - 1;
 }
 
 // run of the pixel left of (word, bit); the caller guarantees it exists
-__device__ __forceinline__ int run_left(const CclSmem& S, int word, int bit) {
+template <class SM>
+__device__ __forceinline__ int run_left(const SM& S, int word, int bit) {
     return bit > 0 ? run_at(S, word, bit - 1) : (int)S.rbase[word] - 1;
 }
 
-__device__ __forceinline__ uint32_t sfind(volatile uint32_t* par, uint32_t a) {
+__device__ __forceinline__ uint32_t sfind(volatile uint16_t* par, uint32_t a) {
     for (;;) {
         const uint32_t p = par[a];
         if (p == a) return a;
         const uint32_t gp = par[p];
         if (gp == p) return p;
-        par[a] = gp;
+        par[a] = (uint16_t)gp;
         a = gp;
     }
 }
 
-__device__ __forceinline__ void sunion(uint32_t* par, uint32_t a, uint32_t b) {
-    volatile uint32_t* vp = par;
+// 16-bit atomic min (CAS loop; unions that actually link are rare), returns the old value
+__device__ __forceinline__ uint32_t atomic_min_u16(uint16_t* addr, uint32_t v) {
+    unsigned short old = *reinterpret_cast<volatile unsigned short*>(addr);
+    while (old > v) {
+        const unsigned short prev = atomicCAS(reinterpret_cast<unsigned short*>(addr), old, (unsigned short)v);
+        if (prev == old) break;
+        old = prev;
+    }
+    return old;
+}
+
+__device__ __forceinline__ void sunion(uint16_t* par, uint32_t a, uint32_t b) {
+    volatile uint16_t* vp = par;
     for (;;) {
         a = sfind(vp, a);
         b = sfind(vp, b);
@@ -69,63 +101,71 @@ __device__ __forceinline__ void sunion(uint32_t* par, uint32_t a, uint32_t b) {
             a = b;
             b = t;
         }
-        const uint32_t old = atomicMin(par + a, b);
+        const uint32_t old = atomic_min_u16(par + a, b);
         if (old == a) return;
         a = old;
     }
 }
 
-__device__ __forceinline__ uint32_t lc_of_run(const CclSmem& S, int run) {
-    return S.par[run] & ~TAG;
+template <class SM>
+__device__ __forceinline__ uint32_t lc_of_run(const SM& S, int run) {
+    return S.par[run] & 0x7FFFu;
 }
 
-__device__ __forceinline__ bool lc_is_border(const CclSmem& S, uint32_t lc) {
+template <class SM>
+__device__ __forceinline__ bool lc_is_border(const SM& S, uint32_t lc) {
     return (S.lcb[lc] & 0x8000u) == 0;
 }
 
 // tile component of pixel (r, c); pixel must be valid
-__device__ __forceinline__ uint32_t lc_at(const CclSmem& S, int r, int c) {
+template <class SM>
+__device__ __forceinline__ uint32_t lc_at(const SM& S, int r, int c) {
     return lc_of_run(S, run_at(S, r * WPR + (c >> 5), c & 31));
 }
 
 // pixel value in "8-connected value" space at (r, c)
-__device__ __forceinline__ uint32_t xbit(const CclSmem& S, int r, int c) {
+template <class SM>
+__device__ __forceinline__ uint32_t xbit(const SM& S, int r, int c) {
     return (S.x[r * WPR + (c >> 5)] >> (c & 31)) & 1u;
 }
 
-// Visit the run pieces of the calling thread's word: f(run, j0, j1) for [j0, j1) in word
-// bit coordinates.  Runs that started in an earlier word continue at bit 0.
-template <class F>
-__device__ __forceinline__ void for_each_piece(const CclSmem& S, int word, F&& f) {
-    const uint32_t vm = S.vm[word];
-    if (!vm) return;
-    const int vend = 32 - __clz(vm);
-    uint32_t rem = S.st[word];
-    int ri = (rem & 1u) ? (int)S.rbase[word] : (int)S.rbase[word] - 1;
-    if (rem & 1u) rem &= rem - 1u;
-    int cur = 0;
-    for (;;) {
-        const int nxt = rem ? __ffs(rem) - 1 : vend;
-        f(ri, cur, nxt);
-        if (!rem) break;
-        rem &= rem - 1u;
-        cur = nxt;
-        ++ri;
+template <class SM>
+__device__ __forceinline__ int run_row(const SM& S, int i) { return S.runpos[i] >> 8; }
+template <class SM>
+__device__ __forceinline__ int run_col(const SM& S, int i) { return S.runpos[i] & 0xFF; }
+
+// exclusive end column of run i
+template <class SM>
+__device__ __forceinline__ int run_end(const SM& S, int i, int tw) {
+    if (i + 1 < S.nruns) {
+        const uint16_t q = S.runpos[i + 1];
+        if ((q >> 8) == (S.runpos[i] >> 8)) return q & 0xFF;
     }
+    return tw;
 }
 
+template <class SM>
+__device__ __forceinline__ int lc_row(const SM& S, uint32_t lc) { return run_row(S, S.lcrun[lc]); }
+template <class SM>
+__device__ __forceinline__ int lc_col(const SM& S, uint32_t lc) { return run_col(S, S.lcrun[lc]); }
+
 // Full tile labeling.  Pre: S.x / S.vm filled for all NW words and a __syncthreads().
-// Post (all synced): S.par[run] = TAG | component, S.lcpos, S.lcb (border flags
+// Post (all synced): S.par[run] = TAG | component, S.runpos, S.lcrun, S.lcb (border flags
 // compacted to border indices), S.blc, S.rowlc, S.rowbx, S.nruns, S.nlc, S.nb.
-__device__ void ccl_tile(CclSmem& S, const TileGeom& tg) {
+// Returns false (uniformly) when the tile has more runs than the tables hold.
+template <int MR>
+__device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const int r = tid / WPR, w = tid % WPR;
     const uint32_t x = S.x[tid], vm = S.vm[tid];
     const uint32_t nx = ~x;
+    // left neighbour word of the same row is lane - 1 (rows never straddle a warp)
+    const uint32_t xl = __shfl_up_sync(0xFFFFFFFFu, x, 1);
+    const uint32_t vml = __shfl_up_sync(0xFFFFFFFFu, vm, 1);
     uint32_t c1 = 0, c0 = 0;
     if (w > 0) {
-        const uint32_t xl = S.x[tid - 1];
-        const uint32_t lv = S.vm[tid - 1] >> 31;
+        const uint32_t lv = vml >> 31;
         c1 = (xl >> 31) & lv;
         c0 = ((~xl) >> 31) & lv;
     }
@@ -133,44 +173,91 @@ __device__ void ccl_tile(CclSmem& S, const TileGeom& tg) {
     const uint32_t s0 = nx & ~((nx << 1) | c0) & vm;
     const uint32_t st = s1 | s0;
     S.st[tid] = st;
-    const int nr = __popc(st);
     int total;
-    const int rb = block_excl_scan(nr, S.wsum, total);  // contains __syncthreads
+    const int rb = block_excl_scan(__popc(st), S.wsum, total);  // contains __syncthreads
+    if (total > MR) return false;
     S.rbase[tid] = (uint16_t)rb;
     if (tid == 0) {
         S.rbase[NW] = (uint16_t)total;
         S.nruns = total;
     }
-    for (int k = 0; k < nr; ++k) S.par[rb + k] = (uint32_t)(rb + k);
-    __syncthreads();
-
-    // ---- union events with the row above (Alg. 2's overlap test, one event per pair)
+    {
+        uint32_t m = st;
+        int i = rb;
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1u;
+            S.runpos[i] = (uint16_t)((r << 8) | (32 * w + j));
+            S.par[i] = (uint16_t)i;
+            ++i;
+        }
+    }
+    // ---- union events with the row above (Alg. 2's overlap test, one event per pair),
+    // compacted into the warp's queue: entry = (word << 7) | (type << 5) | bit
+    uint32_t ev = 0, d1 = 0, d2 = 0;
     if (r >= 1 && vm) {
         const int ta = tid - WPR;
-        const uint32_t a = S.x[ta], vma = S.vm[ta], sta = S.st[ta];
-        uint32_t ca1 = 0;
-        if (w > 0) ca1 = (S.x[ta - 1] >> 31) & (S.vm[ta - 1] >> 31);
-        const uint32_t both = vm & vma;
+        const uint32_t a = S.x[ta], vma = S.vm[ta];
+        // above row's starts/carry are recomputed locally (no dependency on other warps)
+        uint32_t ca1 = 0, ca0 = 0;
+        if (w > 0) {
+            const uint32_t al = S.x[ta - 1], lva = S.vm[ta - 1] >> 31;
+            ca1 = (al >> 31) & lva;
+            ca0 = ((~al) >> 31) & lva;
+        }
         const uint32_t na = ~a;
-        uint32_t ev = ((x & a & (s1 | (sta & a))) | (nx & na & (s0 | (sta & na)))) & both;
+        const uint32_t sa1 = a & ~((a << 1) | ca1) & vma;
+        const uint32_t sa0 = na & ~((na << 1) | ca0) & vma;
+        const uint32_t both = vm & vma;
+        ev = ((x & a & (s1 | sa1)) | (nx & na & (s0 | sa0))) & both;
+        const uint32_t xl1 = (x << 1) | c1, al1 = (a << 1) | ca1;
+        d1 = x & al1 & ~xl1 & na & both;  // (r, j) ~ (r-1, j-1)
+        d2 = xl1 & a & nx & ~al1 & both;  // (r, j-1) ~ (r-1, j)
+    }
+    const int nev = __popc(ev) + __popc(d1) + __popc(d2);
+    int incl = nev;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += n;
+    }
+    const int wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    {
+        uint16_t* q = S.evq[warp] + (incl - nev);
+        const uint16_t wbase = (uint16_t)(tid << 7);
         while (ev) {
             const int j = __ffs(ev) - 1;
             ev &= ev - 1u;
-            sunion(S.par, (uint32_t)run_at(S, tid, j), (uint32_t)run_at(S, ta, j));
+            *q++ = (uint16_t)(wbase | j);
         }
-        const uint32_t xl1 = (x << 1) | c1, al1 = (a << 1) | ca1;
-        uint32_t d1 = x & al1 & ~xl1 & na & both;  // (r, j) ~ (r-1, j-1)
         while (d1) {
             const int j = __ffs(d1) - 1;
             d1 &= d1 - 1u;
-            sunion(S.par, (uint32_t)run_at(S, tid, j), (uint32_t)run_left(S, ta, j));
+            *q++ = (uint16_t)(wbase | (1 << 5) | j);
         }
-        uint32_t d2 = xl1 & a & nx & ~al1 & both;  // (r, j-1) ~ (r-1, j)
         while (d2) {
             const int j = __ffs(d2) - 1;
             d2 &= d2 - 1u;
-            sunion(S.par, (uint32_t)run_left(S, tid, j), (uint32_t)run_at(S, ta, j));
+            *q++ = (uint16_t)(wbase | (2 << 5) | j);
         }
+    }
+    __syncthreads();  // runpos/par/st/rbase of all words ready
+    for (int k = lane; k < wtot; k += 32) {
+        const uint32_t e = S.evq[warp][k];
+        const int word = (int)(e >> 7), type = (int)((e >> 5) & 3u), j = (int)(e & 31u);
+        const int wa = word - WPR;
+        uint32_t ra, rb2;
+        if (type == 0) {
+            ra = (uint32_t)run_at(S, word, j);
+            rb2 = (uint32_t)run_at(S, wa, j);
+        } else if (type == 1) {
+            ra = (uint32_t)run_at(S, word, j);
+            rb2 = (uint32_t)run_left(S, wa, j);
+        } else {
+            ra = (uint32_t)run_left(S, word, j);
+            rb2 = (uint32_t)run_at(S, wa, j);
+        }
+        sunion(S.par, ra, rb2);
     }
     __syncthreads();
 
@@ -178,58 +265,57 @@ __device__ void ccl_tile(CclSmem& S, const TileGeom& tg) {
     const int nruns = S.nruns;
     for (int i = tid; i < nruns; i += NT) {
         uint32_t p = S.par[i];
-        while (true) {
+        for (;;) {
             const uint32_t q = S.par[p];
             if (q == p) break;
             p = q;
         }
-        S.par[i] = p;
+        S.par[i] = (uint16_t)p;
     }
     __syncthreads();
 
-    // ---- tile components = root runs, numbered in raster order
+    // ---- tile components = root runs, numbered in raster order (contiguous run chunks)
+    const int per = (nruns + NT - 1) / NT;
+    const int i0 = min(tid * per, nruns), i1 = min(i0 + per, nruns);
     int nroots = 0;
-    for (int k = 0; k < nr; ++k) nroots += (S.par[rb + k] == (uint32_t)(rb + k));
+    for (int i = i0; i < i1; ++i) nroots += (S.par[i] == (uint32_t)i);
     int nlc;
-    const int lb = block_excl_scan(nroots, S.wsum, nlc);
-    S.lbase[tid] = (uint16_t)lb;
-    if (tid == 0) {
-        S.lbase[NW] = (uint16_t)nlc;
-        S.nlc = nlc;
-    }
-    {
-        uint32_t m = st;
-        int k = 0, lc = lb;
-        while (m) {
-            const int j = __ffs(m) - 1;
-            m &= m - 1u;
-            const int ri = rb + k++;
-            if (S.par[ri] == (uint32_t)ri) {
-                S.lcpos[lc] = (uint16_t)((r << 8) | (32 * w + j));
-                S.lcb[lc] = 0;
-                S.par[ri] = TAG | (uint32_t)lc;
-                ++lc;
-            }
+    int lc = block_excl_scan(nroots, S.wsum, nlc);
+    for (int i = i0; i < i1; ++i) {
+        if (S.par[i] == (uint32_t)i) {
+            S.lcrun[lc] = (uint16_t)i;
+            S.lcb[lc] = 0;
+            S.par[i] = (uint16_t)(TAG16 | lc);
+            ++lc;
         }
     }
+    if (tid == 0) S.nlc = nlc;
     __syncthreads();
-    for (int k = 0; k < nr; ++k) {
-        const uint32_t p = S.par[rb + k];
-        if (!(p & TAG)) S.par[rb + k] = S.par[p];
+    for (int i = tid; i < nruns; i += NT) {
+        const uint32_t p = S.par[i];
+        if (!(p & TAG16)) S.par[i] = S.par[p];
     }
-    if (tid <= TH) S.rowlc[tid] = tid < TH ? S.lbase[tid * WPR] : (uint16_t)nlc;
+    if (tid <= TH) {  // first component of each row: binary search over the raster-ordered roots
+        int lo = 0, hi = nlc;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (lc_row(S, (uint32_t)mid) < tid) lo = mid + 1; else hi = mid;
+        }
+        S.rowlc[tid] = (uint16_t)lo;
+    }
     __syncthreads();
 
     // ---- components touching the tile border (plain stores of 1: race-free)
-    for_each_piece(S, tid, [&](int ri, int j0, int j1) {
-        if (r == 0 || r == tg.th - 1 || (w == 0 && j0 == 0) || (32 * w + j1 == tg.tw))
-            S.lcb[lc_of_run(S, ri)] = 1;
-    });
+    for (int i = tid; i < nruns; i += NT) {
+        const int rr = run_row(S, i), c0 = run_col(S, i);
+        if (rr == 0 || rr == tg.th - 1 || c0 == 0 || run_end(S, i, tg.tw) == tg.tw)
+            S.lcb[lc_of_run(S, i)] = 1;
+    }
     __syncthreads();
 
     // ---- compact border components to border indices (raster order)
-    const int per = (nlc + NT - 1) / NT;
-    const int l0 = min(tid * per, nlc), l1 = min(l0 + per, nlc);
+    const int perl = (nlc + NT - 1) / NT;
+    const int l0 = min(tid * perl, nlc), l1 = min(l0 + perl, nlc);
     int cnt = 0;
     for (int l = l0; l < l1; ++l) cnt += S.lcb[l];
     int nb;
@@ -249,6 +335,7 @@ __device__ void ccl_tile(CclSmem& S, const TileGeom& tg) {
         S.rowbx[tid] = l < nlc ? (uint16_t)(S.lcb[l] & 0x7FFF) : (uint16_t)nb;
     }
     __syncthreads();
+    return true;
 }
 
 }  // namespace rlg

@@ -71,3 +71,25 @@ def test_cfg2_cells(labeler):
     for i in range(imgs.shape[0]):
         ref = O.label_canonical(imgs[i], 0)
         compare_image(res.image(i), ref, f"cfg2 #{i}")
+
+
+def _patterns(w, h):
+    yy, xx = np.mgrid[0:h, 0:w]
+    return {
+        "checker": ((xx + yy) % 2).astype(np.uint8),          # one run per pixel: full-capacity path
+        "vstripes": (xx % 2).astype(np.uint8),
+        "hstripes": (yy % 2).astype(np.uint8),
+        "dots": ((xx % 2 == 0) & (yy % 2 == 0)).astype(np.uint8),
+        "diag": (((xx - yy) % 3) == 0).astype(np.uint8),
+        "rings": (np.minimum(np.minimum(xx, yy), np.minimum(w - 1 - xx, h - 1 - yy)) % 2).astype(np.uint8),
+    }
+
+
+@pytest.mark.parametrize("conn", [0, 1])
+def test_adversarial_patterns(labeler, conn):
+    """Run-dense tiles (more runs than the fast tables hold) go through the full-capacity
+    kernels; mixed batches exercise both paths in one call."""
+    for (w, h) in [(256, 32), (300, 70), (1024, 96), (33, 17)]:
+        pats = _patterns(w, h)
+        imgs = np.stack(list(pats.values()) + [O.generate(w, h, 0.5, 1, 5)])
+        _check_batch(labeler, imgs, conn, f"patterns {w}x{h}")

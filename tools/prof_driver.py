@@ -1,0 +1,71 @@
+#!/usr/bin/env python
+"""Small driver for ncu / per-cell timing: labels a device-generated batch and prints the
+per-phase device times.
+
+  python tools/prof_driver.py --cells 0.5:1,0.5:4 --copies 8 --iters 3
+  python tools/prof_driver.py --sweep        # per-cell phase times over the config-2 sweep
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cells", default="0.5:1")
+    ap.add_argument("--copies", type=int, default=8)
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--size", type=int, default=2048)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--conn", type=int, default=0)
+    args = ap.parse_args()
+
+    import torch
+    from paper_2006_09299_b200 import Connectivity, Labeler, LabelingConfig
+    from paper_2006_09299_b200.runlab import cfg2_cells, generate_device
+
+    lab = Labeler(0)
+    cfg = LabelingConfig(connectivity=Connectivity(args.conn), compute_features=True,
+                         compute_euler=True, fill_holes=True)
+    S = args.size
+
+    def run(cells, copies, iters):
+        B = len(cells) * copies
+        imgs = torch.empty((B, S, S), dtype=torch.uint8, device="cuda")
+        for i in range(B):
+            d, g = cells[i % len(cells)]
+            generate_device(imgs[i].data_ptr(), S, S, d, g, 1 + i // len(cells))
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(iters):
+            lab.label_device(imgs.data_ptr(), S, S, B, cfg)
+            lab.sync()
+            ts.append(lab.phase_times(0))
+        t = ts[-1]
+        return B, t
+
+    if args.sweep:
+        out = []
+        for (d, g) in cfg2_cells():
+            B, t = run([(d, g)], args.copies, 2)
+            gpx = B * S * S / (t.total_ms / 1e3) / 1e9
+            out.append({"d": d, "g": g, "analyze": t.analyze_ms / B, "merge": t.merge_ms / B,
+                        "emit": t.emit_ms / B, "total": t.total_ms / B, "gpx": gpx})
+            print(json.dumps(out[-1]), flush=True)
+        return
+    cells = [tuple(float(v) if i == 0 else int(v) for i, v in enumerate(c.split(":")))
+             for c in args.cells.split(",")]
+    B, t = run(cells, args.copies, args.iters)
+    print(json.dumps({"images": B, "analyze_ms": t.analyze_ms, "merge_ms": t.merge_ms,
+                      "emit_ms": t.emit_ms, "total_ms": t.total_ms,
+                      "gpx": B * S * S / (t.total_ms / 1e3) / 1e9}))
+
+
+if __name__ == "__main__":
+    main()
