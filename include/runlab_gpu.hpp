@@ -1,0 +1,327 @@
+// runlab_gpu.hpp -- C++ drop-in for the reference's labeling/analysis entry points,
+// running on the B200 through the C ABI of include/runlab_gpu.h (librunlab_gpu.so).
+//
+// A reference user switches `#include "runlab/runlab.hpp"` to `#include "runlab_gpu.hpp"`
+// and links -lrunlab_gpu; the names below keep the reference's signatures and semantics
+// (paths relative to /root/reference/proj/include/runlab/):
+//
+//   label_t, no_label, Connectivity          types.hpp:10-21
+//   BinaryImage, LabelImage                  image.hpp:14-67
+//   FeatureAccumulator, FeatureTable         features.hpp:14-30
+//   EquivalenceTable, AdjacencyTable         tables.hpp:37-108 (result-side accessors)
+//   LabelingConfig, LabelingResult           labeling.hpp:20-50
+//   StepTimes, label_image, timed_label_image, binarize_labels   labeling.hpp:253-360
+//   ComponentRecord, components, holes, ComponentTree, adjacency_tree, euler_number
+//                                            analysis.hpp:13-79
+//
+// Label values are canonical ids: the rank of each component's raster-first pixel, exterior
+// 0 -- i.e. the reference's root labels renumbered in ascending order (its provisional
+// labels are an artefact of the sequential scan).  With fill_holes, T[e] is e's post-fill
+// root (its depth-1 ancestor).  Errors map as in the reference: std::invalid_argument,
+// std::logic_error, std::overflow_error; device failures throw std::runtime_error.
+#pragma once
+
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "runlab_gpu.h"
+
+namespace runlab {
+
+using label_t = std::uint32_t;
+inline constexpr label_t no_label = std::numeric_limits<label_t>::max();
+
+enum class Connectivity : std::uint8_t { fg8_bg4, fg4_bg8 };
+
+struct BinaryImage {
+    std::int32_t width = 0;
+    std::int32_t height = 0;
+    std::vector<std::uint8_t> pixels;  // row-major, 0 = background, 1 = foreground
+
+    BinaryImage() = default;
+    BinaryImage(std::int32_t w, std::int32_t h)
+        : width(w), height(h), pixels(static_cast<std::size_t>(w) * static_cast<std::size_t>(h), 0) {}
+    std::int64_t pixel_count() const { return static_cast<std::int64_t>(width) * height; }
+    std::uint8_t operator()(std::int32_t r, std::int32_t c) const { return pixels[static_cast<std::size_t>(r) * width + c]; }
+    std::uint8_t& operator()(std::int32_t r, std::int32_t c) { return pixels[static_cast<std::size_t>(r) * width + c]; }
+    bool operator==(const BinaryImage&) const = default;
+};
+
+struct LabelImage {
+    std::int32_t width = 0;
+    std::int32_t height = 0;
+    std::vector<label_t> labels;
+
+    LabelImage() = default;
+    LabelImage(std::int32_t w, std::int32_t h)
+        : width(w), height(h), labels(static_cast<std::size_t>(w) * static_cast<std::size_t>(h), 0) {}
+    label_t operator()(std::int32_t r, std::int32_t c) const { return labels[static_cast<std::size_t>(r) * width + c]; }
+    bool operator==(const LabelImage&) const = default;
+};
+
+struct FeatureAccumulator {
+    std::int64_t s = 0, sx = 0, sy = 0;
+    std::int32_t row_min = std::numeric_limits<std::int32_t>::max();
+    std::int32_t row_max = std::numeric_limits<std::int32_t>::min();
+    std::int32_t col_min = std::numeric_limits<std::int32_t>::max();
+    std::int32_t col_max = std::numeric_limits<std::int32_t>::min();
+    bool empty() const { return s == 0; }
+    bool operator==(const FeatureAccumulator&) const = default;
+};
+using FeatureTable = std::vector<FeatureAccumulator>;
+
+// Result-side equivalence table: parent and parity per label (no scan-time mutators).
+class EquivalenceTable {
+public:
+    EquivalenceTable() = default;
+    EquivalenceTable(std::vector<label_t> parent, std::vector<std::uint8_t> fg)
+        : t_(std::move(parent)), fg_(std::move(fg)) {}
+    label_t size() const { return static_cast<label_t>(t_.size()); }
+    bool is_foreground(label_t e) const { return fg_[e] != 0; }
+    label_t parent(label_t e) const { return t_[e]; }
+    bool is_root(label_t e) const { return t_[e] == e; }
+    label_t find(label_t e) const {
+        while (t_[e] != e) e = t_[e];
+        return e;
+    }
+
+private:
+    std::vector<label_t> t_;
+    std::vector<std::uint8_t> fg_;
+};
+
+class AdjacencyTable {
+public:
+    AdjacencyTable() = default;
+    explicit AdjacencyTable(std::vector<label_t> i) : i_(std::move(i)) {}
+    label_t size() const { return static_cast<label_t>(i_.size()); }
+    label_t operator[](label_t e) const { return i_[e]; }
+
+private:
+    std::vector<label_t> i_;
+};
+
+struct LabelingConfig {
+    Connectivity connectivity = Connectivity::fg8_bg4;
+    bool fill_holes = false;
+    bool compute_features = false;
+    bool relabel = false;
+    bool densify_labels = false;
+    bool compute_euler = false;
+};
+
+struct LabelingResult {
+    std::int32_t width = 0;
+    std::int32_t height = 0;
+    LabelingConfig config;
+    EquivalenceTable equivalences;
+    AdjacencyTable adjacency;
+    std::optional<FeatureTable> features;
+    std::optional<LabelImage> labels;
+    std::optional<std::int64_t> fg_count;
+    std::optional<std::int64_t> hole_count;
+    std::optional<std::int64_t> euler;
+
+    std::vector<label_t> roots() const {
+        std::vector<label_t> out;
+        for (label_t e = 0; e < equivalences.size(); ++e)
+            if (equivalences.is_root(e)) out.push_back(e);
+        return out;
+    }
+};
+
+// Device phase times (ms, CUDA events), cf. labeling.hpp:253-259.
+struct StepTimes {
+    double encode_ns = 0;   // tile analysis pass (segments + tile union-find)
+    double unify_ns = 0;    // cross-tile merge, canonical ids, tree, fill fold
+    double closure_ns = 0;  // emit pass (records, filled image)
+    double relabel_ns = 0;
+    double total_ns = 0;
+};
+
+namespace gpu {
+
+// One C-ABI context per thread (SPEC: single-threaded per call, distinct images may be
+// labeled concurrently).
+class Context {
+public:
+    explicit Context(int device = 0) : ctx_(rl_create(device), &rl_destroy) {
+        if (!ctx_) throw std::runtime_error("runlab_gpu: no usable CUDA device");
+    }
+    rl_ctx* get() const { return ctx_.get(); }
+
+private:
+    std::unique_ptr<rl_ctx, void (*)(rl_ctx*)> ctx_;
+};
+
+inline Context& thread_context() {
+    thread_local Context ctx(0);
+    return ctx;
+}
+
+[[noreturn]] inline void raise(int code, rl_ctx* ctx) {
+    const std::string msg = rl_last_error(ctx);
+    switch (code) {
+        case RL_EINVAL: throw std::invalid_argument(msg);
+        case RL_ELOGIC: throw std::logic_error(msg);
+        case RL_EOVERFLOW: throw std::overflow_error(msg);
+        case RL_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error(msg);
+    }
+}
+
+inline FeatureAccumulator to_acc(const rl_features& f) {
+    FeatureAccumulator a;
+    a.s = f.s;
+    a.sx = f.sx;
+    a.sy = f.sy;
+    a.row_min = f.row_min;
+    a.row_max = f.row_max;
+    a.col_min = f.col_min;
+    a.col_max = f.col_max;
+    return a;
+}
+
+inline LabelingResult run(const BinaryImage& image, const LabelingConfig& config, StepTimes* times) {
+    if (config.densify_labels && !config.relabel)
+        throw std::invalid_argument("label_image: densify_labels requires relabel");
+    rl_ctx* ctx = thread_context().get();
+    rl_config c{};
+    c.connectivity = config.connectivity == Connectivity::fg4_bg8 ? RL_FG4_BG8 : RL_FG8_BG4;
+    c.fill_holes = config.fill_holes;
+    c.compute_features = config.compute_features;
+    c.relabel = config.relabel;
+    c.densify_labels = config.densify_labels;
+    c.compute_euler = config.compute_euler;
+    rl_result r{};
+    const int rc = rl_label(ctx, image.pixels.data(), image.width, image.height, 1, &c, &r);
+    if (rc != RL_OK) raise(rc, ctx);
+    struct Free {
+        rl_result* r;
+        ~Free() { rl_result_free(r); }
+    } guard{&r};
+
+    const std::int64_t n = r.n_components[0];
+    std::vector<label_t> t(static_cast<std::size_t>(n)), adj(static_cast<std::size_t>(n));
+    std::vector<std::uint8_t> fg(static_cast<std::size_t>(n));
+    for (std::int64_t e = 0; e < n; ++e) {
+        t[e] = config.fill_holes ? r.top[e] : static_cast<label_t>(e);
+        adj[e] = e == 0 ? no_label : r.comps[e].parent;
+        fg[e] = static_cast<std::uint8_t>(r.comps[e].flags & 1u);
+    }
+    LabelingResult res;
+    res.width = image.width;
+    res.height = image.height;
+    res.config = config;
+    if (config.compute_features) {
+        FeatureTable ft(static_cast<std::size_t>(n));
+        for (std::int64_t e = 0; e < n; ++e)
+            ft[e] = to_acc((config.fill_holes && r.top[e] == e) ? r.filled[e] : r.comps[e].f);
+        res.features = std::move(ft);
+    }
+    if (config.relabel) {
+        LabelImage li(image.width, image.height);
+        std::copy(r.labels, r.labels + li.labels.size(), li.labels.begin());
+        res.labels = std::move(li);
+    }
+    if (config.compute_euler) {
+        res.fg_count = r.n_fg[0];
+        res.hole_count = r.n_holes[0];
+        res.euler = r.euler[0];
+    }
+    res.equivalences = EquivalenceTable(std::move(t), std::move(fg));
+    res.adjacency = AdjacencyTable(std::move(adj));
+    if (times) {
+        times->encode_ns = r.times.analyze_ms * 1e6;
+        times->unify_ns = r.times.merge_ms * 1e6;
+        times->closure_ns = r.times.emit_ms * 1e6;
+        times->relabel_ns = 0;
+        times->total_ns = r.times.total_ms * 1e6;
+    }
+    return res;
+}
+
+}  // namespace gpu
+
+// labeling.hpp:336-339
+inline LabelingResult label_image(const BinaryImage& image, const LabelingConfig& config = {}) {
+    return gpu::run(image, config, nullptr);
+}
+
+// labeling.hpp:343-348
+inline LabelingResult timed_label_image(const BinaryImage& image, const LabelingConfig& config, StepTimes& times) {
+    times = {};
+    return gpu::run(image, config, &times);
+}
+
+// labeling.hpp:354-360: foreground iff the label's parity is foreground
+inline BinaryImage binarize_labels(const LabelImage& li, const EquivalenceTable& eq) {
+    BinaryImage out(li.width, li.height);
+    for (std::size_t i = 0; i < li.labels.size(); ++i) out.pixels[i] = eq.is_foreground(li.labels[i]) ? 1 : 0;
+    return out;
+}
+
+// ---- analysis.hpp:13-79 projections over the result tables
+struct ComponentRecord {
+    label_t root = 0;
+    bool foreground = false;
+    label_t parent_root = no_label;
+    std::int32_t depth = 0;
+    FeatureAccumulator features;
+};
+
+inline std::vector<ComponentRecord> components(const LabelingResult& res) {
+    const EquivalenceTable& eq = res.equivalences;
+    std::vector<ComponentRecord> out;
+    std::vector<std::int32_t> depth(eq.size(), 0);
+    for (label_t e = 0; e < eq.size(); ++e) {
+        if (!eq.is_root(e)) continue;
+        ComponentRecord rec;
+        rec.root = e;
+        rec.foreground = eq.is_foreground(e);
+        if (e != 0) {
+            rec.parent_root = res.adjacency[e];
+            depth[e] = depth[rec.parent_root] + 1;
+        }
+        rec.depth = depth[e];
+        if (res.features) rec.features = (*res.features)[e];
+        out.push_back(rec);
+    }
+    return out;
+}
+
+inline std::vector<ComponentRecord> holes(const LabelingResult& res) {
+    if (res.config.fill_holes) throw std::logic_error("holes: result was computed with hole filling");
+    std::vector<ComponentRecord> out;
+    for (ComponentRecord& rec : components(res))
+        if (!rec.foreground && rec.root != 0) out.push_back(rec);
+    return out;
+}
+
+struct ComponentTree {
+    std::vector<ComponentRecord> nodes;
+    std::vector<std::vector<std::size_t>> children;
+};
+
+inline ComponentTree adjacency_tree(const LabelingResult& res) {
+    ComponentTree tree;
+    tree.nodes = components(res);
+    tree.children.resize(tree.nodes.size());
+    std::vector<std::size_t> index(res.equivalences.size(), 0);
+    for (std::size_t i = 0; i < tree.nodes.size(); ++i) index[tree.nodes[i].root] = i;
+    for (std::size_t i = 1; i < tree.nodes.size(); ++i)
+        tree.children[index[tree.nodes[i].parent_root]].push_back(i);
+    return tree;
+}
+
+inline std::int64_t euler_number(const LabelingResult& res) {
+    if (!res.euler) throw std::logic_error("euler_number: labeling ran without compute_euler");
+    return *res.euler;
+}
+
+}  // namespace runlab

@@ -1,0 +1,131 @@
+// dropin_test.cpp -- the reference's own known-answer tests, restated against the C++
+// drop-in (include/runlab_gpu.hpp) running on the GPU.  Each check cites the reference test
+// it mirrors (paths relative to /root/reference/proj/tests/).  Exit code = failures.
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "runlab_gpu.hpp"
+
+using namespace runlab;
+
+static int failures = 0;
+
+#define CHECK(cond)                                                            \
+    do {                                                                       \
+        if (!(cond)) {                                                         \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+            ++failures;                                                        \
+        }                                                                      \
+    } while (0)
+
+static BinaryImage make_image(const std::vector<std::string>& rows) {
+    BinaryImage img(static_cast<std::int32_t>(rows[0].size()), static_cast<std::int32_t>(rows.size()));
+    for (std::int32_t r = 0; r < img.height; ++r)
+        for (std::int32_t c = 0; c < img.width; ++c) img(r, c) = rows[r][c] == '1' ? 1 : 0;
+    return img;
+}
+
+static LabelingConfig full_config() {
+    LabelingConfig cfg;
+    cfg.compute_features = true;
+    cfg.compute_euler = true;
+    cfg.relabel = true;
+    return cfg;
+}
+
+int main() {
+    const BinaryImage fig = make_image({"011111111111110", "010000010000010", "010111010111010",
+                                        "010101000101010", "010101111101010", "010100000001000",
+                                        "011111111111110"});
+    // test_labeling.cpp:107-134 "golden example: end-to-end result" (roots 0,1,6 -> 0,1,2)
+    {
+        const LabelingResult res = label_image(fig, full_config());
+        CHECK(*res.fg_count == 1);
+        CHECK(*res.hole_count == 1);
+        CHECK(*res.euler == 0);
+        CHECK((res.roots() == std::vector<label_t>{0, 1, 2}));
+        CHECK(res.adjacency[2] == 1 && res.adjacency[1] == 0);
+        const FeatureAccumulator& fg = (*res.features)[1];
+        CHECK(fg.s == 56 && fg.row_min == 0 && fg.row_max == 6 && fg.col_min == 1 && fg.col_max == 13);
+        const FeatureAccumulator& hole = (*res.features)[2];
+        CHECK(hole.s == 11 && hole.row_min == 3 && hole.row_max == 5 && hole.col_min == 4 && hole.col_max == 10);
+        CHECK((*res.features)[0].s == 38);
+        std::vector<label_t> row3(res.labels->labels.begin() + 45, res.labels->labels.begin() + 60);
+        CHECK((row3 == std::vector<label_t>{0, 1, 0, 1, 2, 1, 0, 0, 0, 1, 2, 1, 0, 1, 0}));
+        // analysis.hpp projections
+        CHECK(holes(res).size() == 1);
+        CHECK(adjacency_tree(res).children[0].size() == 1);
+        CHECK(euler_number(res) == 0);
+    }
+    // test_labeling.cpp:136-148 "golden example: hole filled end-to-end"
+    {
+        LabelingConfig cfg = full_config();
+        cfg.fill_holes = true;
+        const LabelingResult res = label_image(fig, cfg);
+        CHECK((res.roots() == std::vector<label_t>{0, 1}));
+        CHECK((*res.features)[1].s == 67);
+        CHECK(*res.euler == 0);
+        std::vector<label_t> row3(res.labels->labels.begin() + 45, res.labels->labels.begin() + 60);
+        CHECK((row3 == std::vector<label_t>{0, 1, 0, 1, 1, 1, 0, 0, 0, 1, 1, 1, 0, 1, 0}));
+        const BinaryImage filled = binarize_labels(*res.labels, res.equivalences);
+        CHECK(filled(3, 4) == 1 && filled(3, 2) == 0);
+        bool threw = false;
+        try {
+            holes(res);
+        } catch (const std::logic_error&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    // test_labeling.cpp:178-190 ring-hole-dot collapses; test_analysis.cpp:103-110 depth 3
+    {
+        const BinaryImage rhd = make_image({"0000000", "0111110", "0100010", "0101010", "0100010", "0111110", "0000000"});
+        LabelingConfig cfg = full_config();
+        const ComponentTree tree = adjacency_tree(label_image(rhd, cfg));
+        CHECK(tree.nodes.size() == 4 && tree.nodes[3].depth == 3);
+        cfg.fill_holes = true;
+        const LabelingResult res = label_image(rhd, cfg);
+        CHECK((res.roots() == std::vector<label_t>{0, 1}));
+        CHECK((*res.features)[1].s == 25);
+    }
+    // test_labeling.cpp:192-203 misuse
+    {
+        LabelingConfig bad;
+        bad.densify_labels = true;
+        bool threw = false;
+        try {
+            label_image(make_image({"0"}), bad);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+        bool threw2 = false;
+        try {
+            euler_number(label_image(make_image({"1"}), {}));
+        } catch (const std::logic_error&) {
+            threw2 = true;
+        }
+        CHECK(threw2);
+    }
+    // test_labeling.cpp:217-230 diagonal pair depends on the convention
+    {
+        const BinaryImage img = make_image({"10", "01"});
+        LabelingConfig cfg;
+        cfg.compute_euler = true;
+        CHECK(*label_image(img, cfg).euler == 1);
+        cfg.connectivity = Connectivity::fg4_bg8;
+        const LabelingResult res = label_image(img, cfg);
+        CHECK(*res.fg_count == 2 && *res.euler == 2);
+    }
+    // timed_label_image gives identical results (test_bench.cpp:31-60)
+    {
+        StepTimes t;
+        const LabelingResult a = timed_label_image(fig, full_config(), t);
+        const LabelingResult b = label_image(fig, full_config());
+        CHECK(*a.labels == *b.labels && t.total_ns > 0);
+    }
+    std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
+    return failures;
+}

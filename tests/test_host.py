@@ -1,0 +1,141 @@
+"""CPU tests of the host side: the C-ABI library loads and exports every symbol the header
+declares (no compute without a GPU), the Python mirror's argument checking and host-side
+projections, the C++ drop-in compiles, and the multi-rank plumbing under gloo."""
+from __future__ import annotations
+
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols() -> list[str]:
+    src = open(os.path.join(ROOT, "include", "runlab_gpu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rl_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2006_09299_b200 import _native
+    lib = _native.load()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(_native.EXPORTED_SYMBOLS) <= set(syms)
+
+
+def test_library_is_sm100a():
+    lib = os.path.join(ROOT, "paper_2006_09299_b200", "librunlab_gpu.so")
+    out = subprocess.run(["cuobjdump", "--list-elf", lib], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_tile_shape_query():
+    import ctypes as C
+    from paper_2006_09299_b200 import _native
+    th, tw = C.c_int32(), C.c_int32()
+    _native.load().rl_tile_shape(C.byref(th), C.byref(tw))
+    assert (th.value, tw.value) == (32, 256)
+
+
+def test_cfg4_params_host_side():
+    from oracle import oracle as O
+    from paper_2006_09299_b200.runlab import cfg2_cells, cfg4_params
+    assert [cfg4_params(i) for i in range(32)] == [O.cfg4_params(i) for i in range(32)]
+    cells = cfg2_cells()
+    assert len(cells) == 105 and cells[0] == (0.0, 1) and cells[-1] == (1.0, 16)
+
+
+def test_config_errors_raise_before_device():
+    from paper_2006_09299_b200 import LabelingConfig, label_image
+    with pytest.raises(ValueError):
+        label_image(np.zeros((1, 1), np.uint8), LabelingConfig(densify_labels=True))
+    with pytest.raises(ValueError):
+        label_image(np.zeros((0, 3), np.uint8), LabelingConfig())
+
+
+def _fig3_result(fill: bool):
+    """A LabelingResult as the GPU returns it for Fig. 3 (canonical ids), built by hand."""
+    from paper_2006_09299_b200 import runlab as R
+    from paper_2006_09299_b200._native import FEATURE_DTYPE
+    t = np.array([0, 1, 1] if fill else [0, 1, 2], dtype=np.uint32)
+    feats = np.zeros(3, dtype=FEATURE_DTYPE)
+    feats["s"] = [38, 67 if fill else 56, 11]
+    return R.LabelingResult(width=15, height=7, config=R.LabelingConfig(fill_holes=fill, compute_euler=True),
+                            equivalences=R.EquivalenceTable(t=t, parity=np.array([0, 1, 0], np.uint8)),
+                            adjacency=np.array([R.NO_LABEL, 0, 1], np.uint32), features=feats,
+                            fg_count=1, hole_count=1, euler=0)
+
+
+def test_analysis_projections_host_side():
+    from paper_2006_09299_b200 import runlab as R
+    res = _fig3_result(False)
+    comps = R.components(res)
+    assert [c.root for c in comps] == [0, 1, 2] and [c.depth for c in comps] == [0, 1, 2]
+    assert [h.root for h in R.holes(res)] == [2]
+    tree = R.adjacency_tree(res)
+    assert tree.children == [[1], [2], []]
+    assert R.euler_number(res) == 0
+    filled = _fig3_result(True)
+    assert filled.roots() == [0, 1]
+    with pytest.raises(R.LogicError):
+        R.holes(filled)
+    res.euler = None
+    with pytest.raises(R.LogicError):
+        R.euler_number(res)
+    labels = np.array([[0, 1, 2, 1]], np.uint32)
+    assert list(R.binarize_labels(labels, res.equivalences)[0]) == [0, 1, 0, 1]
+
+
+def test_cpp_dropin_header_compiles():
+    out = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"),
+                          os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp")],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+
+
+def test_shard_range():
+    from paper_2006_09299_b200.distributed import shard_range
+    for n in (0, 1, 7, 105, 4096):
+        for world in (1, 2, 3, 8):
+            parts = [shard_range(n, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            sizes = [hi - lo for lo, hi in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_2006_09299_b200.distributed import max_over_ranks, shard_range, sum_over_ranks
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    lo, hi = shard_range(105, rank, world)
+    t = max_over_ranks(1.0 + rank)
+    n = sum_over_ranks(hi - lo)
+    dist.destroy_process_group()
+    q.put((rank, t, n))
+
+
+def test_multirank_reductions_gloo():
+    """world_size-2 gloo run of the bench's N>1 plumbing: shard, max-time, sum."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = sorted(q.get(timeout=10) for _ in procs)
+    assert [r[1] for r in res] == [2.0, 2.0]
+    assert [r[2] for r in res] == [105, 105]
