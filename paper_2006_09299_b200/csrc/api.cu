@@ -60,7 +60,7 @@ __global__ void k_summary(Geo g, Ws ws, uint64_t* cbase, int64_t* summ) {
         summ[4 * b + 0] = (int64_t)base;  // total components
         summ[4 * b + 1] = (int64_t)ws.counters[0];
         summ[4 * b + 2] = (int64_t)ws.counters[1];
-        summ[4 * b + 3] = 0;
+        summ[4 * b + 3] = (int64_t)*ws.rused;
     }
 }
 
@@ -84,9 +84,10 @@ struct rl_ctx {
     // workspace
     DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
     DevBuf cnt, off, counters, img_fg, img_surv, comps, top, filled, filled_img, labels, pix;
-    DevBuf cub_tmp, cbase, summ, rank, flag, ovf;
+    DevBuf cub_tmp, cbase, summ, rank, flag, ovf, thdr, tmap, rstore, rused;
     uint32_t cap_nodes = 0;
     uint64_t cap_comps = 0;
+    uint64_t cap_rstore = 0;
     // pinned host mirror of the summary
     int64_t* h_summ = nullptr;
     size_t h_summ_n = 0;
@@ -167,9 +168,10 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     const int64_t ncnt = (int64_t)B * H * g.ntx + 1;
     if (ctx->cap_nodes == 0) ctx->cap_nodes = (uint32_t)std::min<int64_t>(std::max<int64_t>(ntiles * 96, 4096), 0xF0000000ll);
     if (ctx->cap_comps == 0) ctx->cap_comps = (uint64_t)std::max<int64_t>(g.P * B / 16, 4096);
+    if (ctx->cap_rstore == 0) ctx->cap_rstore = (uint64_t)std::max<int64_t>(g.P * B * 3 / 10 + ntiles * 64, 1 << 16);
     const uint64_t nn = (uint64_t)B + ctx->cap_nodes;
     bool ok = ensure(ctx->bits, (size_t)ntiles * NW * 4) && ensure(ctx->tbase, (size_t)ntiles * 4) &&
-              ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->ovf, (size_t)ntiles * 4) && ensure(ctx->perim, (size_t)ntiles * PERIM * 2) &&
+              ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->ovf, (size_t)ntiles * 4) && ensure(ctx->thdr, (size_t)ntiles * THDR * 2) && ensure(ctx->tmap, (size_t)ntiles * 8) && ensure(ctx->rstore, ctx->cap_rstore * 2) && ensure(ctx->rused, 64) && ensure(ctx->perim, (size_t)ntiles * PERIM * 2) &&
               ensure(ctx->uf, nn * 4) && ensure(ctx->nkey, nn * 8) && ensure(ctx->nmin, nn * 8) &&
               ensure(ctx->nacc, nn * sizeof(Acc)) && ensure(ctx->nrec, nn * sizeof(NodeRec)) &&
               ensure(ctx->nrep, nn) && ensure(ctx->nrootcid, nn * 4) && ensure(ctx->nparent, nn * 4) &&
@@ -195,6 +197,11 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     ws.tbase = P<uint32_t>(ctx->tbase);
     ws.tnb = P<uint32_t>(ctx->tnb);
     ws.ovf = P<uint32_t>(ctx->ovf);
+    ws.thdr = P<uint16_t>(ctx->thdr);
+    ws.tmap = P<uint64_t>(ctx->tmap);
+    ws.rstore = P<uint16_t>(ctx->rstore);
+    ws.rused = P<unsigned long long>(ctx->rused);
+    ws.cap_rstore = ctx->cap_rstore;
     ws.perim = P<uint16_t>(ctx->perim);
     ws.uf = P<uint32_t>(ctx->uf);
     ws.nkey = P<uint64_t>(ctx->nkey);
@@ -229,6 +236,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     }
     int launches = 0;
     cudaMemsetAsync(ws.counters, 0, 64, s);
+    cudaMemsetAsync(ws.rused, 0, 8, s);
     cudaMemsetAsync(ws.img_fg, 0, (size_t)B * 4, s);
     cudaMemsetAsync(ws.img_surv, 0, (size_t)B * 4, s);
     cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
@@ -295,10 +303,13 @@ int finish(rl_ctx* ctx) {
         const uint64_t total_comps = (uint64_t)tail[0];
         const uint64_t nodes = (uint64_t)tail[1];
         const uint32_t errs = (uint32_t)tail[2];
+        const uint64_t rused = (uint64_t)tail[3];
         bool grow = false;
         if (errs & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (tree reference)");
-        if (errs & ERR_NODE_CAP) {
-            ctx->cap_nodes = (uint32_t)std::min<uint64_t>(nodes + nodes / 4 + 1024, 0xF0000000ull);
+        if (errs & (ERR_NODE_CAP | ERR_RSTORE_CAP)) {
+            if (errs & ERR_NODE_CAP)
+                ctx->cap_nodes = (uint32_t)std::min<uint64_t>(nodes + nodes / 4 + 1024, 0xF0000000ull);
+            if (errs & ERR_RSTORE_CAP) ctx->cap_rstore = rused + rused / 8 + 4096;
             grow = true;
         } else if (total_comps > ctx->cap_comps) {
             ctx->cap_comps = total_comps + total_comps / 8 + 1024;
@@ -407,7 +418,7 @@ void rl_destroy(rl_ctx* c) {
                       &c->nrec, &c->nrep, &c->nrootcid, &c->nparent, &c->nanccid, &c->cnt, &c->off,
                       &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
-                      &c->rank, &c->flag, &c->ovf};
+                      &c->rank, &c->flag, &c->ovf, &c->thdr, &c->tmap, &c->rstore, &c->rused};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_summ) cudaFreeHost(c->h_summ);

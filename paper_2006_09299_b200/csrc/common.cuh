@@ -32,6 +32,8 @@ static_assert(TW == 256, "lcpos packs the column in 8 bits");
 constexpr uint32_t ERR_NODE_CAP = 1u;
 constexpr uint32_t ERR_COMP_CAP = 2u;
 constexpr uint32_t ERR_INTERNAL = 4u;
+constexpr uint32_t ERR_RSTORE_CAP = 8u;
+constexpr int THDR = 4 + 2 * (TH + 1);  // u16 slots of a tile-map header
 // counters[2]: tiles deferred to the full-capacity kernels (overflow list length)
 
 // Global feature accumulator: exactly rl_features (40 B).
@@ -81,6 +83,13 @@ struct Ws {
     uint32_t* off;       // exclusive scan of cnt
     uint32_t* counters;  // [0] nodes used, [1] error bits, [2] deferred tiles
     uint32_t* ovf;       // [ntiles] deferred (run-heavy) tiles
+    // tile component maps stored by the analyze pass for the emit pass
+    uint16_t* thdr;      // [ntiles*THDR] nruns, nlc, nb, -, rowlc[TH+1], rowbx[TH+1]
+    uint64_t* tmap;      // [ntiles] offset of the tile's map in rstore (u16 units)
+    uint16_t* rstore;    // per tile: component of each run, first run and border index of
+                         // each component
+    unsigned long long* rused;  // rstore elements allocated
+    uint64_t cap_rstore;
     uint32_t* img_fg;    // [B] foreground components
     uint32_t* img_surv;  // [B] post-fill components (exterior included)
     uint32_t cap_nodes;

@@ -33,6 +33,7 @@ struct AnalyzeSmem {
     int32_t brmax[NBMAX], bcmin[NBMAX], bcmax[NBMAX];
     uint8_t bimg[NBMAX];  // touches the image border
     uint32_t base;
+    unsigned long long moff;
 };
 
 // Returns false when the tile exceeds the MR run capacity (then nothing was written for
@@ -91,6 +92,38 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<MR>& A, const uint8_t* 
         if ((uint64_t)base + nb > ws.cap_nodes) atomicOr(&ws.counters[1], ERR_NODE_CAP);
         ws.tbase[tg.t] = base;
         ws.tnb[tg.t] = (uint32_t)nb;
+        const unsigned long long need = (unsigned long long)nruns + 2ull * (unsigned long long)nlc;
+        const unsigned long long off = atomicAdd(ws.rused, need);
+        A.moff = off;
+        if (off + need > ws.cap_rstore) atomicOr(&ws.counters[1], ERR_RSTORE_CAP);
+        ws.tmap[tg.t] = off;
+    }
+    // ---- tile header (run/component counts, row tables) for the emit pass
+    {
+        uint16_t* hdr = ws.thdr + (int64_t)tg.t * THDR;
+        if (tid == 0) {
+            hdr[0] = (uint16_t)nruns;
+            hdr[1] = (uint16_t)nlc;
+            hdr[2] = (uint16_t)nb;
+            hdr[3] = 0;
+        }
+        if (tid <= TH) {
+            hdr[4 + tid] = S.rowlc[tid];
+            hdr[4 + TH + 1 + tid] = S.rowbx[tid];
+        }
+    }
+    __syncthreads();
+    // ---- component map: component of every run, first run and border index of every component
+    {
+        const unsigned long long off = A.moff;
+        if (off + (unsigned long long)nruns + 2ull * nlc <= ws.cap_rstore) {
+            uint16_t* dst = ws.rstore + off;
+            for (int i = tid; i < nruns; i += NT) dst[i] = (uint16_t)lc_of_run(S, i);
+            for (int l = tid; l < nlc; l += NT) {
+                dst[nruns + l] = S.lcrun[l];
+                dst[nruns + nlc + l] = S.lcb[l];
+            }
+        }
     }
 
     // ---- border-component features and image-border contact (one lane per run)
@@ -566,9 +599,30 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<MR>& E, const Geo& g, const W
         E.pcmin[tid] = 0x7FFFFFFF;
         E.pcmax[tid] = -1;
     }
+    const uint16_t* hdr = ws.thdr + (int64_t)tg.t * THDR;
+    if (tid == 0) {
+        S.nlc = hdr[1];
+        S.nb = hdr[2];
+    }
+    if (tid <= TH) {
+        S.rowlc[tid] = hdr[4 + tid];
+        S.rowbx[tid] = hdr[4 + TH + 1 + tid];
+    }
     __syncthreads();
 
-    if (!ccl_tile(S, tg)) return false;
+    // runs again from the packed bits (cheap); the component map comes from the analyze pass
+    WordBits wb;
+    if (!tile_runs<false>(S, wb)) return false;
+    {
+        const int nr = wb.nruns, nl = S.nlc;
+        const uint16_t* src = ws.rstore + ws.tmap[tg.t];
+        for (int i = tid; i < nr; i += NT) S.par[i] = src[i];
+        for (int l = tid; l < nl; l += NT) {
+            S.lcrun[l] = src[nr + l];
+            S.lcb[l] = src[nr + nl + l];
+        }
+    }
+    __syncthreads();
 
     const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
     const uint64_t cb = E.cb;

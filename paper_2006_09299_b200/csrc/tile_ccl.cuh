@@ -153,45 +153,64 @@ __device__ __forceinline__ int lc_col(const SM& S, uint32_t lc) { return run_col
 // Post (all synced): S.par[run] = TAG | component, S.runpos, S.lcrun, S.lcb (border flags
 // compacted to border indices), S.blc, S.rowlc, S.rowbx, S.nruns, S.nlc, S.nb.
 // Returns false (uniformly) when the tile has more runs than the tables hold.
-template <int MR>
-__device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
+// Per-thread word state shared by the run and union phases.
+struct WordBits {
+    uint32_t x, nx, vm, c1, s1, s0, st;
+    int nruns;
+};
+
+// Runs of the tile: start masks, raster-order run indices (block scan), run positions and
+// identity parents.  Returns false (uniformly) when the tile has more runs than MR.
+template <bool INIT_PAR = true, int MR>
+__device__ __forceinline__ bool tile_runs(CclSmem<MR>& S, WordBits& wb) {
     const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
     const int r = tid / WPR, w = tid % WPR;
-    const uint32_t x = S.x[tid], vm = S.vm[tid];
-    const uint32_t nx = ~x;
+    wb.x = S.x[tid];
+    wb.vm = S.vm[tid];
+    wb.nx = ~wb.x;
     // left neighbour word of the same row is lane - 1 (rows never straddle a warp)
-    const uint32_t xl = __shfl_up_sync(0xFFFFFFFFu, x, 1);
-    const uint32_t vml = __shfl_up_sync(0xFFFFFFFFu, vm, 1);
+    const uint32_t xl = __shfl_up_sync(0xFFFFFFFFu, wb.x, 1);
+    const uint32_t vml = __shfl_up_sync(0xFFFFFFFFu, wb.vm, 1);
     uint32_t c1 = 0, c0 = 0;
     if (w > 0) {
         const uint32_t lv = vml >> 31;
         c1 = (xl >> 31) & lv;
         c0 = ((~xl) >> 31) & lv;
     }
-    const uint32_t s1 = x & ~((x << 1) | c1) & vm;
-    const uint32_t s0 = nx & ~((nx << 1) | c0) & vm;
-    const uint32_t st = s1 | s0;
-    S.st[tid] = st;
+    wb.c1 = c1;
+    wb.s1 = wb.x & ~((wb.x << 1) | c1) & wb.vm;
+    wb.s0 = wb.nx & ~((wb.nx << 1) | c0) & wb.vm;
+    wb.st = wb.s1 | wb.s0;
+    S.st[tid] = wb.st;
     int total;
-    const int rb = block_excl_scan(__popc(st), S.wsum, total);  // contains __syncthreads
+    const int rb = block_excl_scan(__popc(wb.st), S.wsum, total);  // contains __syncthreads
+    wb.nruns = total;
     if (total > MR) return false;
     S.rbase[tid] = (uint16_t)rb;
     if (tid == 0) {
         S.rbase[NW] = (uint16_t)total;
         S.nruns = total;
     }
-    {
-        uint32_t m = st;
-        int i = rb;
-        while (m) {
-            const int j = __ffs(m) - 1;
-            m &= m - 1u;
-            S.runpos[i] = (uint16_t)((r << 8) | (32 * w + j));
-            S.par[i] = (uint16_t)i;
-            ++i;
-        }
+    uint32_t m = wb.st;
+    int i = rb;
+    while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1u;
+        S.runpos[i] = (uint16_t)((r << 8) | (32 * w + j));
+        if (INIT_PAR) S.par[i] = (uint16_t)i;
+        ++i;
     }
+    return true;
+}
+
+template <int MR>
+__device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int r = tid / WPR, w = tid % WPR;
+    WordBits wb;
+    if (!tile_runs(S, wb)) return false;
+    const uint32_t x = wb.x, nx = wb.nx, vm = wb.vm, c1 = wb.c1, s1 = wb.s1, s0 = wb.s0;
     // ---- union events with the row above (Alg. 2's overlap test, one event per pair),
     // compacted into the warp's queue: entry = (word << 7) | (type << 5) | bit
     uint32_t ev = 0, d1 = 0, d2 = 0;
@@ -261,18 +280,24 @@ __device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
     }
     __syncthreads();
 
-    // ---- flatten (roots are final now)
+    // ---- flatten (roots are final now): a short walk, then pointer jumping until every run
+    // points at its root (vertical stacks of runs form chains as long as the tile is tall)
     const int nruns = S.nruns;
-    for (int i = tid; i < nruns; i += NT) {
-        uint32_t p = S.par[i];
-        for (;;) {
-            const uint32_t q = S.par[p];
-            if (q == p) break;
-            p = q;
+    for (int round = 0;; ++round) {
+        int changed = 0;
+        for (int i = tid; i < nruns; i += NT) {
+            uint32_t p = S.par[i];
+            const uint32_t p0 = p;
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t q = S.par[p];
+                if (q == p) break;
+                p = q;
+            }
+            if (p != p0) S.par[i] = (uint16_t)p;
+            changed |= (S.par[p] != p);
         }
-        S.par[i] = (uint16_t)p;
+        if (!__syncthreads_or(changed)) break;
     }
-    __syncthreads();
 
     // ---- tile components = root runs, numbered in raster order (contiguous run chunks)
     const int per = (nruns + NT - 1) / NT;
@@ -282,6 +307,8 @@ __device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
     int nlc;
     int lc = block_excl_scan(nroots, S.wsum, nlc);
     for (int i = i0; i < i1; ++i) {
+        const int rr = run_row(S, i);
+        if (S.rbase[rr * WPR] == i) S.rowlc[rr] = (uint16_t)lc;  // first run of its row
         if (S.par[i] == (uint32_t)i) {
             S.lcrun[lc] = (uint16_t)i;
             S.lcb[lc] = 0;
@@ -290,26 +317,18 @@ __device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
         }
     }
     if (tid == 0) S.nlc = nlc;
+    if (tid >= tg.th && tid <= TH) S.rowlc[tid] = (uint16_t)nlc;  // rows without pixels
     __syncthreads();
+    // resolve non-root runs; mark components touching the tile border (plain stores of 1)
     for (int i = tid; i < nruns; i += NT) {
-        const uint32_t p = S.par[i];
-        if (!(p & TAG16)) S.par[i] = S.par[p];
-    }
-    if (tid <= TH) {  // first component of each row: binary search over the raster-ordered roots
-        int lo = 0, hi = nlc;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (lc_row(S, (uint32_t)mid) < tid) lo = mid + 1; else hi = mid;
+        uint32_t p = S.par[i];
+        if (!(p & TAG16)) {
+            p = S.par[p];
+            S.par[i] = (uint16_t)p;
         }
-        S.rowlc[tid] = (uint16_t)lo;
-    }
-    __syncthreads();
-
-    // ---- components touching the tile border (plain stores of 1: race-free)
-    for (int i = tid; i < nruns; i += NT) {
         const int rr = run_row(S, i), c0 = run_col(S, i);
         if (rr == 0 || rr == tg.th - 1 || c0 == 0 || run_end(S, i, tg.tw) == tg.tw)
-            S.lcb[lc_of_run(S, i)] = 1;
+            S.lcb[p & 0x7FFFu] = 1;
     }
     __syncthreads();
 
