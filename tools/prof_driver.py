@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--size", type=int, default=2048)
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--conn", type=int, default=0)
+    ap.add_argument("--cfg2", action="store_true", help="the exact 105-image bench batch")
     args = ap.parse_args()
 
     import torch
@@ -40,7 +41,7 @@ def main():
         imgs = torch.empty((B, S, S), dtype=torch.uint8, device="cuda")
         for i in range(B):
             d, g = cells[i % len(cells)]
-            generate_device(imgs[i].data_ptr(), S, S, d, g, 1 + i // len(cells))
+            generate_device(imgs[i].data_ptr(), S, S, d, g, 1 if args.cfg2 else 1 + i // len(cells))
         torch.cuda.synchronize()
         ts = []
         for _ in range(iters):
@@ -61,6 +62,9 @@ def main():
         return
     cells = [tuple(float(v) if i == 0 else int(v) for i, v in enumerate(c.split(":")))
              for c in args.cells.split(",")]
+    if args.cfg2:
+        cells = cfg2_cells()
+        args.copies = 1
     B, t = run(cells, args.copies, args.iters)
     print(json.dumps({"images": B, "analyze_ms": t.analyze_ms, "merge_ms": t.merge_ms,
                       "emit_ms": t.emit_ms, "total_ms": t.total_ms,
