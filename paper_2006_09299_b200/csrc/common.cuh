@@ -214,15 +214,85 @@ __device__ __forceinline__ Acc acc_empty() {
     return a;
 }
 
+// ---- block-level aggregation of feature folds ------------------------------------------
+// Many nodes fold into few hot targets (the percolating component of an image has a node
+// in every tile).  A block first reduces its folds in a shared open-addressing table keyed
+// by the target, then flushes one global atomic fold per distinct target.
+constexpr uint32_t FT_EMPTY = 0xFFFFFFFFu;
+
+template <int SLOTS>
+struct FoldTable {
+    uint32_t key[SLOTS];
+    unsigned long long s[SLOTS], sx[SLOTS], sy[SLOTS], kmin[SLOTS];
+    int32_t rmin[SLOTS], rmax[SLOTS], cmin[SLOTS], cmax[SLOTS];
+
+    __device__ void init() {
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+            key[i] = FT_EMPTY;
+            s[i] = sx[i] = sy[i] = 0;
+            kmin[i] = ~0ull;
+            rmin[i] = cmin[i] = 0x7FFFFFFF;
+            rmax[i] = cmax[i] = (int32_t)0x80000000;
+        }
+    }
+    // false when the table is full (the caller folds straight into global memory)
+    __device__ bool add(uint32_t k, const Acc& f, unsigned long long km) {
+        uint32_t h = (k * 2654435761u) & (SLOTS - 1);
+        for (int probe = 0; probe < 32; ++probe, h = (h + 1) & (SLOTS - 1)) {
+            uint32_t cur = key[h];
+            if (cur == FT_EMPTY) cur = atomicCAS(&key[h], FT_EMPTY, k), cur = (cur == FT_EMPTY) ? k : cur;
+            if (cur != k) continue;
+            atomicAdd(&s[h], (unsigned long long)f.s);
+            atomicAdd(&sx[h], (unsigned long long)f.sx);
+            atomicAdd(&sy[h], (unsigned long long)f.sy);
+            atomicMin(&rmin[h], f.row_min);
+            atomicMax(&rmax[h], f.row_max);
+            atomicMin(&cmin[h], f.col_min);
+            atomicMax(&cmax[h], f.col_max);
+            if (km != ~0ull) atomicMin(&kmin[h], km);
+            return true;
+        }
+        return false;
+    }
+    template <class Dst, class KeyDst>
+    __device__ void flush(Dst&& dst, KeyDst&& kdst) {
+        for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+            if (key[i] == FT_EMPTY) continue;
+            Acc f;
+            f.s = (int64_t)s[i];
+            f.sx = (int64_t)sx[i];
+            f.sy = (int64_t)sy[i];
+            f.row_min = rmin[i];
+            f.row_max = rmax[i];
+            f.col_min = cmin[i];
+            f.col_max = cmax[i];
+            acc_atomic_fold(dst(key[i]), f);
+            if (kmin[i] != ~0ull) atomicMin(kdst(key[i]), kmin[i]);
+        }
+    }
+};
+
 // ---- global union-find (lock-free; min-index linking, path halving) -------------------
+// Plain (L1-cacheable) reads are safe: parents only ever decrease, so a stale value is
+// still an ancestor, and the linking atomicMin returns the true old value.
 __device__ __forceinline__ uint32_t gfind(uint32_t* uf, uint32_t a) {
     for (;;) {
-        const uint32_t p = __ldcg(uf + a);
+        const uint32_t p = uf[a];
         if (p == a) return a;
-        const uint32_t gp = __ldcg(uf + p);
+        const uint32_t gp = uf[p];
         if (gp == p) return p;
-        __stcg(uf + a, gp);
+        uf[a] = gp;
         a = gp;
+    }
+}
+
+// Read-only find for the flattening pass: every thread then writes only its own node, so
+// no concurrent path-halving store can overwrite a node's final root with an ancestor.
+__device__ __forceinline__ uint32_t gfind_ro(const uint32_t* uf, uint32_t a) {
+    for (;;) {
+        const uint32_t p = uf[a];
+        if (p == a) return a;
+        a = p;
     }
 }
 

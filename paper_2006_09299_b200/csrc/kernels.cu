@@ -340,17 +340,37 @@ __global__ void k_seam_v(Geo g, Ws ws) {
     for (uint32_t n = (uint32_t)g.B + blockIdx.x * blockDim.x + threadIdx.x;           \
          n < (uint32_t)g.B + nused_; n += gridDim.x * blockDim.x)
 
-__global__ void k_resolve(Geo g, Ws ws) {
+// contiguous node range of this block (nodes are tile-major, so a component's nodes from
+// neighbouring tiles land in the same block and aggregate in its fold table)
+#define NODE_CHUNK(n)                                                                   \
+    const uint32_t nused_ = min(ws.counters[0], ws.cap_nodes);                          \
+    const uint32_t chunk_ = (nused_ + gridDim.x - 1) / gridDim.x;                       \
+    const uint32_t lo_ = (uint32_t)g.B + min(nused_, blockIdx.x * chunk_);              \
+    const uint32_t hi_ = (uint32_t)g.B + min(nused_, (blockIdx.x + 1) * chunk_);        \
+    for (uint32_t n = lo_ + threadIdx.x; n < hi_; n += blockDim.x)
+
+constexpr int FT_SLOTS = 512;
+
+__global__ void __launch_bounds__(256) k_resolve(Geo g, Ws ws) {
+    __shared__ FoldTable<FT_SLOTS> T;
     if (ws.counters[1]) return;
-    NODE_LOOP(n) {
-        const uint32_t root = gfind(ws.uf, n);
+    T.init();
+    __syncthreads();
+    NODE_CHUNK(n) {
+        const uint32_t root = gfind_ro(ws.uf, n);
         if (root != n) {
-            __stcg(ws.uf + n, root);
-            acc_atomic_fold(ws.nacc + root, ws.nacc[n]);
-            atomicMin(reinterpret_cast<unsigned long long*>(ws.nmin + root),
-                      static_cast<unsigned long long>(ws.nkey[n]));
+            ws.uf[n] = root;
+            const Acc f = ws.nacc[n];
+            const unsigned long long key = ws.nkey[n];
+            if (!T.add(root, f, key)) {
+                acc_atomic_fold(ws.nacc + root, f);
+                atomicMin(reinterpret_cast<unsigned long long*>(ws.nmin + root), key);
+            }
         }
     }
+    __syncthreads();
+    T.flush([&](uint32_t k) { return ws.nacc + k; },
+            [&](uint32_t k) { return reinterpret_cast<unsigned long long*>(ws.nmin + k); });
 }
 
 __device__ __forceinline__ void tile_of(const Geo& g, uint32_t t, int32_t& b, int32_t& ty, int32_t& tx) {
@@ -362,16 +382,30 @@ __device__ __forceinline__ void tile_of(const Geo& g, uint32_t t, int32_t& b, in
 
 __global__ void k_reps(Geo g, Ws ws) {
     if (ws.counters[1]) return;
-    NODE_LOOP(n) {
-        const uint32_t root = ws.uf[n];
-        const bool rep = root >= (uint32_t)g.B && ws.nkey[n] == ws.nmin[root];
-        ws.nrep[n] = rep ? 1 : 0;
-        if (rep) {
-            const NodeRec rec = ws.nrec[n];
-            int32_t b, ty, tx;
-            tile_of(g, rec.tile, b, ty, tx);
-            atomicAdd(&ws.cnt[((int64_t)b * g.H + ty * TH + rec.fr) * g.ntx + tx], 1u);
-            if (rec.fg) atomicAdd(&ws.img_fg[b], 1u);
+    const uint32_t nused = min(ws.counters[0], ws.cap_nodes);
+    // whole warps iterate together so the per-image foreground count aggregates per warp
+    for (uint32_t base = (uint32_t)g.B + (blockIdx.x * blockDim.x + threadIdx.x) - (threadIdx.x & 31u);
+         base < (uint32_t)g.B + nused; base += gridDim.x * blockDim.x) {
+        const uint32_t n = base + (threadIdx.x & 31u);
+        bool fgrep = false;
+        int32_t b = -1;
+        if (n < (uint32_t)g.B + nused) {
+            const uint32_t root = ws.uf[n];
+            const bool rep = root >= (uint32_t)g.B && ws.nkey[n] == ws.nmin[root];
+            ws.nrep[n] = rep ? 1 : 0;
+            if (rep) {
+                const NodeRec rec = ws.nrec[n];
+                int32_t ty, tx;
+                tile_of(g, rec.tile, b, ty, tx);
+                atomicAdd(&ws.cnt[((int64_t)b * g.H + ty * TH + rec.fr) * g.ntx + tx], 1u);
+                fgrep = rec.fg != 0;
+            }
+        }
+        const uint32_t fgmask = __ballot_sync(0xFFFFFFFFu, fgrep);
+        if (fgmask) {
+            const uint32_t same = __match_any_sync(0xFFFFFFFFu, fgrep ? b : -1);
+            if (fgrep && (__ffs(same & fgmask) - 1) == (int)(threadIdx.x & 31u))
+                atomicAdd(&ws.img_fg[b], (uint32_t)__popc(same & fgmask));
         }
     }
 }
@@ -384,29 +418,44 @@ __device__ __forceinline__ bool comps_fit(const Geo& g, const Ws& ws) {
     return (uint64_t)ws.off[(int64_t)g.B * g.H * g.ntx] + (uint64_t)g.B <= ws.cap_comps;
 }
 
-// one thread per tile: canonical ids of the tile's border representatives
+// one warp per tile: canonical ids of the tile's border representatives.  The tile's border
+// components are in raster order of first pixel, so "representatives before me in my row"
+// is a prefix count inside the run of equal rows (match_any) plus a carry across chunks.
 __global__ void k_cids(Geo g, Ws ws) {
     if (ws.counters[1]) return;
-    for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < g.ntiles; t += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < g.ntiles; t += warps) {
         int32_t b, ty, tx;
         tile_of(g, (uint32_t)t, b, ty, tx);
         const uint32_t nb = ws.tnb[t];
         const uint32_t n0 = (uint32_t)g.B + ws.tbase[t];
         const int64_t img0 = (int64_t)b * g.H * g.ntx;
         const uint32_t offimg = ws.off[img0];
-        int cur_row = -1, reps = 0;
-        for (uint32_t i = 0; i < nb; ++i) {
+        int carry_row = -1, carry = 0;
+        for (uint32_t i0 = 0; i0 < nb; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool valid = i < nb;
             const uint32_t n = n0 + i;
-            const NodeRec rec = ws.nrec[n];
-            if (rec.fr != cur_row) {
-                cur_row = rec.fr;
-                reps = 0;
+            const int row = valid ? (int)ws.nrec[n].fr : 0x10000 + lane;
+            const bool rep = valid && ws.nrep[n];
+            const uint32_t repmask = __ballot_sync(0xFFFFFFFFu, rep);
+            const uint32_t same = __match_any_sync(0xFFFFFFFFu, row);
+            const uint32_t below = (1u << lane) - 1u;
+            int before = __popc(repmask & same & below);
+            if (row == carry_row) before += carry;
+            if (rep) {
+                const NodeRec rec = ws.nrec[n];
+                const uint32_t cid = 1u + (ws.off[img0 + (int64_t)(ty * TH + rec.fr) * g.ntx + tx] - offimg) +
+                                     rec.ibefore + (uint32_t)before;
+                ws.nrootcid[ws.uf[n]] = cid;
             }
-            if (!ws.nrep[n]) continue;
-            const uint32_t cid = 1u + (ws.off[img0 + (int64_t)(ty * TH + rec.fr) * g.ntx + tx] - offimg) +
-                                 rec.ibefore + (uint32_t)reps;
-            ++reps;
-            ws.nrootcid[ws.uf[n]] = cid;
+            // carry for the next chunk: reps of the chunk's last row (continuing rows only)
+            const int last_row = __shfl_sync(0xFFFFFFFFu, row, 31);
+            const uint32_t last_same = __shfl_sync(0xFFFFFFFFu, same, 31);
+            const int cnt_last = __popc(repmask & last_same);
+            carry = (last_row == carry_row ? carry : 0) + cnt_last;
+            carry_row = last_row;
         }
     }
 }
@@ -479,14 +528,20 @@ __global__ void k_tops(Geo g, Ws ws) {
         ws.top[cb + cid] = anc;
         if (cur == root) {
             ws.filled[cb + cid] = ws.nacc[root];
-            atomicAdd(&ws.img_surv[b], 1u);
+            // warp-aggregated survivor count (same image for most lanes)
+            const uint32_t active = __activemask();
+            const uint32_t same = __match_any_sync(active, b);
+            if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u)) atomicAdd(&ws.img_surv[b], (uint32_t)__popc(same));
         }
     }
 }
 
-__global__ void k_fold(Geo g, Ws ws) {
+__global__ void __launch_bounds__(256) k_fold(Geo g, Ws ws) {
+    __shared__ FoldTable<FT_SLOTS> T;
     if (ws.counters[1] || !comps_fit(g, ws)) return;
-    NODE_LOOP(n) {
+    T.init();
+    __syncthreads();
+    NODE_CHUNK(n) {
         if (!ws.nrep[n]) continue;
         const uint32_t root = ws.uf[n];
         const uint32_t anc = ws.nanccid[root];
@@ -494,8 +549,13 @@ __global__ void k_fold(Geo g, Ws ws) {
         if (anc == cid) continue;
         int32_t b, ty, tx;
         tile_of(g, ws.nrec[n].tile, b, ty, tx);
-        acc_atomic_fold(ws.filled + comp_base(g, ws, b) + anc, ws.nacc[root]);
+        const uint32_t dst = (uint32_t)(comp_base(g, ws, b) + anc);  // < 2^32 components
+        const Acc f = ws.nacc[root];
+        if (!T.add(dst, f, ~0ull)) acc_atomic_fold(ws.filled + dst, f);
     }
+    __syncthreads();
+    T.flush([&](uint32_t k) { return ws.filled + k; },
+            [&](uint32_t) { return static_cast<unsigned long long*>(nullptr); });
 }
 
 // ---------------------------------------------------------------------------------------
@@ -919,7 +979,7 @@ void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
     k_reps<<<grid_for(nodes_hint, 256, sms * 8), 256, 0, s>>>(g, ws);
 }
 void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
-    k_cids<<<grid_for(g.ntiles, 128, sms * 8), 128, 0, s>>>(g, ws);
+    k_cids<<<grid_for((int64_t)g.ntiles * 32, 256, sms * 16), 256, 0, s>>>(g, ws);
 }
 void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
     const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;
