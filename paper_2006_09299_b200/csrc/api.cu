@@ -84,7 +84,7 @@ struct rl_ctx {
     // workspace
     DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
     DevBuf cnt, off, counters, img_fg, img_surv, comps, top, filled, filled_img, labels, pix;
-    DevBuf cub_tmp, cbase, summ, rank, flag, ovf, thdr, tmap, rstore, rused;
+    DevBuf cub_tmp, cbase, summ, rank, flag, ovf, ovf2, thdr, tmap, rstore, rused;
     uint32_t cap_nodes = 0;
     uint64_t cap_comps = 0;
     uint64_t cap_rstore = 0;
@@ -171,7 +171,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     if (ctx->cap_rstore == 0) ctx->cap_rstore = (uint64_t)std::max<int64_t>(g.P * B * 3 / 10 + ntiles * 64, 1 << 16);
     const uint64_t nn = (uint64_t)B + ctx->cap_nodes;
     bool ok = ensure(ctx->bits, (size_t)ntiles * NW * 4) && ensure(ctx->tbase, (size_t)ntiles * 4) &&
-              ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->ovf, (size_t)ntiles * 4) && ensure(ctx->thdr, (size_t)ntiles * THDR * 2) && ensure(ctx->tmap, (size_t)ntiles * 8) && ensure(ctx->rstore, ctx->cap_rstore * 2) && ensure(ctx->rused, 64) && ensure(ctx->perim, (size_t)ntiles * PERIM * 2) &&
+              ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->ovf, (size_t)ntiles * 4) && ensure(ctx->ovf2, (size_t)ntiles * 4) && ensure(ctx->thdr, (size_t)ntiles * THDR * 2) && ensure(ctx->tmap, (size_t)ntiles * 8) && ensure(ctx->rstore, ctx->cap_rstore * 2) && ensure(ctx->rused, 64) && ensure(ctx->perim, (size_t)ntiles * PERIM * 2) &&
               ensure(ctx->uf, nn * 4) && ensure(ctx->nkey, nn * 8) && ensure(ctx->nmin, nn * 8) &&
               ensure(ctx->nacc, nn * sizeof(Acc)) && ensure(ctx->nrec, nn * sizeof(NodeRec)) &&
               ensure(ctx->nrep, nn) && ensure(ctx->nrootcid, nn * 4) && ensure(ctx->nparent, nn * 4) &&
@@ -197,6 +197,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     ws.tbase = P<uint32_t>(ctx->tbase);
     ws.tnb = P<uint32_t>(ctx->tnb);
     ws.ovf = P<uint32_t>(ctx->ovf);
+    ws.ovf2 = P<uint32_t>(ctx->ovf2);
     ws.thdr = P<uint16_t>(ctx->thdr);
     ws.tmap = P<uint64_t>(ctx->tmap);
     ws.rstore = P<uint16_t>(ctx->rstore);
@@ -242,7 +243,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
     cudaEventRecord(ctx->ev[0], s);
     launch_analyze(dpix, g, ws, s);
-    launches += 2;
+    launches += 3;
     cudaEventRecord(ctx->ev[1], s);
     launch_seams(g, ws, s, ctx->sms);
     launches += (g.nty > 1) + (g.ntx > 1);
@@ -255,7 +256,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launches += 2 + 1 + 1 + 3;
     cudaEventRecord(ctx->ev[2], s);
     launch_emit(g, ws, s);
-    launches += 2;
+    launches += 3;
     k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));
     ++launches;
     if (cfg->densify_labels && cfg->fill_holes && g.label_mode) {
@@ -418,7 +419,7 @@ void rl_destroy(rl_ctx* c) {
                       &c->nrec, &c->nrep, &c->nrootcid, &c->nparent, &c->nanccid, &c->cnt, &c->off,
                       &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
-                      &c->rank, &c->flag, &c->ovf, &c->thdr, &c->tmap, &c->rstore, &c->rused};
+                      &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_summ) cudaFreeHost(c->h_summ);

@@ -82,7 +82,8 @@ struct Ws {
     uint32_t* cnt;       // [B*H*ntx + 1] roots whose first pixel is in (image,row,tile col)
     uint32_t* off;       // exclusive scan of cnt
     uint32_t* counters;  // [0] nodes used, [1] error bits, [2] deferred tiles
-    uint32_t* ovf;       // [ntiles] deferred (run-heavy) tiles
+    uint32_t* ovf;       // [ntiles] tiles deferred from class S to M (counters[2])
+    uint32_t* ovf2;      // [ntiles] tiles deferred from class M to F (counters[4])
     // tile component maps stored by the analyze pass for the emit pass
     uint16_t* thdr;      // [ntiles*THDR] nruns, nlc, nb, -, rowlc[TH+1], rowbx[TH+1]
     uint64_t* tmap;      // [ntiles] offset of the tile's map in rstore (u16 units)

@@ -25,23 +25,23 @@ namespace rlg {
 // ---------------------------------------------------------------------------------------
 // K1a: analyze
 // ---------------------------------------------------------------------------------------
-template <int MR>
+template <class C>
 struct AnalyzeSmem {
-    CclSmem<MR> c;
+    CclSmem<C> c;
     // border-component accumulators (tile-local coordinates)
-    uint32_t bs[NBMAX], bsx[NBMAX], bsy[NBMAX];
-    int32_t brmax[NBMAX], bcmin[NBMAX], bcmax[NBMAX];
-    uint8_t bimg[NBMAX];  // touches the image border
+    uint32_t bs[C::NBC], bsx[C::NBC], bsy[C::NBC];
+    int32_t brmax[C::NBC], bcmin[C::NBC], bcmax[C::NBC];
+    uint8_t bimg[C::NBC];  // touches the image border
     uint32_t base;
     unsigned long long moff;
 };
 
-// Returns false when the tile exceeds the MR run capacity (then nothing was written for
-// it except the packed bits; the caller queues it for the full-capacity kernel).
-template <int MR>
-__device__ __forceinline__ bool analyze_tile(AnalyzeSmem<MR>& A, const uint8_t* __restrict__ pix, const Geo& g,
+// Returns false when the tile exceeds the capacity class C (then nothing was written for it
+// except the packed bits; the caller defers it to the next class).
+template <class C>
+__device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* __restrict__ pix, const Geo& g,
                                              const Ws& ws, const TileGeom& tg) {
-    CclSmem<MR>& S = A.c;
+    CclSmem<C>& S = A.c;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
 
@@ -63,7 +63,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<MR>& A, const uint8_t* 
     S.x[tid] = x;
     S.vm[tid] = vm;
     ws.bits[(int64_t)tg.t * NW + tid] = x;
-    for (int i = tid; i < NBMAX; i += NT) {
+    for (int i = tid; i < C::NBC; i += NT) {
         A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
         A.brmax[i] = -1;
         A.bcmin[i] = 0x7FFFFFFF;
@@ -229,22 +229,35 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<MR>& A, const uint8_t* 
     return true;
 }
 
-// fast variant: one CTA per tile on the (ntx, nty, B) grid; run-heavy tiles are deferred
+// class S: one CTA per tile on the (ntx, nty, B) grid; heavier tiles go to list A
 __global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto& A = *reinterpret_cast<AnalyzeSmem<MR_FAST>*>(smem_raw);
+    auto& A = *reinterpret_cast<AnalyzeSmem<CapS>*>(smem_raw);
     const TileGeom tg = tile_geom_grid(g);
     if (!analyze_tile(A, pix, g, ws, tg) && threadIdx.x == 0)
         ws.ovf[atomicAdd(&ws.counters[2], 1u)] = (uint32_t)tg.t;
 }
 
-// full-capacity variant over the deferred tiles (one run per pixel fits)
-__global__ void __launch_bounds__(NT) k_analyze_full(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+// class M over list A; heavier tiles go to list B
+__global__ void __launch_bounds__(NT) k_analyze_m(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto& A = *reinterpret_cast<AnalyzeSmem<MAXRUNS>*>(smem_raw);
+    auto& A = *reinterpret_cast<AnalyzeSmem<CapM>*>(smem_raw);
     const uint32_t n = ws.counters[2];
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
         const TileGeom tg = tile_geom(g, (int32_t)ws.ovf[k]);
+        if (!analyze_tile(A, pix, g, ws, tg) && threadIdx.x == 0)
+            ws.ovf2[atomicAdd(&ws.counters[4], 1u)] = (uint32_t)tg.t;
+        __syncthreads();
+    }
+}
+
+// class F over list B (one run per pixel fits)
+__global__ void __launch_bounds__(NT) k_analyze_full(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& A = *reinterpret_cast<AnalyzeSmem<CapF>*>(smem_raw);
+    const uint32_t n = ws.counters[4];
+    for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+        const TileGeom tg = tile_geom(g, (int32_t)ws.ovf2[k]);
         analyze_tile(A, pix, g, ws, tg);
         __syncthreads();
     }
@@ -563,17 +576,17 @@ __global__ void __launch_bounds__(256) k_fold(Geo g, Ws ws) {
 // ---------------------------------------------------------------------------------------
 constexpr int FOLD_SLOTS = 64;  // distinct border fold targets per tile kept in smem
 
-template <int MR>
+template <class C>
 struct EmitSmem {
-    CclSmem<MR> c;
+    CclSmem<C> c;
     // interior-feature chunk accumulators (tile-local coordinates)
     uint32_t fs[FCH], fsx[FCH], fsy[FCH];
     int32_t frmax[FCH], fcmin[FCH], fcmax[FCH];
     // border components of this tile
-    uint32_t bcid[NBMAX];   // canonical id of the component
-    uint32_t banc[NBMAX];   // canonical id of its post-fill root
-    uint8_t bflag[NBMAX];   // bit0 representative, bit1 exterior
-    uint16_t repx[NBMAX + 1];  // exclusive prefix of representative flags over border index
+    uint32_t bcid[C::NBC];   // canonical id of the component
+    uint32_t banc[C::NBC];   // canonical id of its post-fill root
+    uint8_t bflag[C::NBC];   // bit0 representative, bit1 exterior
+    uint16_t repx[C::NBC + 1];  // exclusive prefix of representative flags over border index
     // fold of interior components into border-derived survivors: small open-addressing
     // table keyed by border index (overflow goes straight to global atomics)
     uint16_t pkey[FOLD_SLOTS];
@@ -637,11 +650,16 @@ __device__ __forceinline__ int fold_slot(ES& E, uint32_t key) {
     return -1;
 }
 
-template <int MR>
-__device__ __forceinline__ bool emit_tile(EmitSmem<MR>& E, const Geo& g, const Ws& ws, const TileGeom& tg) {
-    CclSmem<MR>& S = E.c;
+// Emits a tile iff it belongs to capacity class C (the class its analyze pass used).
+template <class C>
+__device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws& ws, const TileGeom& tg) {
+    CclSmem<C>& S = E.c;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
+    {
+        const uint16_t* h = ws.thdr + (int64_t)tg.t * THDR;
+        if ((int)h[0] > C::MR || (int)h[2] > C::NBC) return false;  // a larger class owns it
+    }
     const uint32_t vm = valid_mask(tg, r, w);
     S.x[tid] = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
     S.vm[tid] = vm;
@@ -876,20 +894,32 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<MR>& E, const Geo& g, const W
     return true;
 }
 
+// class S on the full grid (tiles of larger classes are skipped), M over list A, F over list B
 __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ws.counters[1] || !comps_fit(g, ws)) return;
-    auto& E = *reinterpret_cast<EmitSmem<MR_FAST>*>(smem_raw);
-    emit_tile(E, g, ws, tile_geom_grid(g));  // run-heavy tiles: k_emit_full
+    auto& E = *reinterpret_cast<EmitSmem<CapS>*>(smem_raw);
+    emit_tile(E, g, ws, tile_geom_grid(g));
+}
+
+__global__ void __launch_bounds__(NT) k_emit_m(Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ws.counters[1] || !comps_fit(g, ws)) return;
+    auto& E = *reinterpret_cast<EmitSmem<CapM>*>(smem_raw);
+    const uint32_t n = ws.counters[2];
+    for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+        emit_tile(E, g, ws, tile_geom(g, (int32_t)ws.ovf[k]));
+        __syncthreads();
+    }
 }
 
 __global__ void __launch_bounds__(NT) k_emit_full(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ws.counters[1] || !comps_fit(g, ws)) return;
-    auto& E = *reinterpret_cast<EmitSmem<MAXRUNS>*>(smem_raw);
-    const uint32_t n = ws.counters[2];
+    auto& E = *reinterpret_cast<EmitSmem<CapF>*>(smem_raw);
+    const uint32_t n = ws.counters[4];
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
-        emit_tile(E, g, ws, tile_geom(g, (int32_t)ws.ovf[k]));
+        emit_tile(E, g, ws, tile_geom(g, (int32_t)ws.ovf2[k]));
         __syncthreads();
     }
 }
@@ -933,20 +963,21 @@ __global__ void k_surv_flags_img(const uint32_t* top, const uint64_t* cbase, int
 // ---------------------------------------------------------------------------------------
 namespace rlg {
 
-size_t analyze_smem() { return sizeof(AnalyzeSmem<MR_FAST>); }
-size_t emit_smem() { return sizeof(EmitSmem<MR_FAST>); }
+size_t analyze_smem() { return sizeof(AnalyzeSmem<CapS>); }
+size_t emit_smem() { return sizeof(EmitSmem<CapS>); }
+
+template <class K>
+static cudaError_t set_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 
 cudaError_t configure_kernels() {
-    cudaError_t e = cudaFuncSetAttribute(k_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(AnalyzeSmem<MR_FAST>));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_analyze_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(AnalyzeSmem<MAXRUNS>));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem<MR_FAST>));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_emit_full, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(EmitSmem<MAXRUNS>));
+    cudaError_t e = set_smem(k_analyze, sizeof(AnalyzeSmem<CapS>));
+    if (e == cudaSuccess) e = set_smem(k_analyze_m, sizeof(AnalyzeSmem<CapM>));
+    if (e == cudaSuccess) e = set_smem(k_analyze_full, sizeof(AnalyzeSmem<CapF>));
+    if (e == cudaSuccess) e = set_smem(k_emit, sizeof(EmitSmem<CapS>));
+    if (e == cudaSuccess) e = set_smem(k_emit_m, sizeof(EmitSmem<CapM>));
+    if (e == cudaSuccess) e = set_smem(k_emit_full, sizeof(EmitSmem<CapF>));
     return e;
 }
 
@@ -958,9 +989,10 @@ static int grid_for(int64_t n, int block, int maxgrid) {
 }
 
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
-    k_analyze<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(AnalyzeSmem<MR_FAST>), s>>>(pix, g, ws);
-    // deferred run-heavy tiles (the grid loops over the device-side list; usually empty)
-    k_analyze_full<<<148, NT, sizeof(AnalyzeSmem<MAXRUNS>), s>>>(pix, g, ws);
+    k_analyze<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
+    // deferred heavier tiles: the grids loop over device-side lists (no host sync)
+    k_analyze_m<<<148 * 3, NT, sizeof(AnalyzeSmem<CapM>), s>>>(pix, g, ws);
+    k_analyze_full<<<148, NT, sizeof(AnalyzeSmem<CapF>), s>>>(pix, g, ws);
 }
 void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
     if (g.nty > 1) {
@@ -988,8 +1020,9 @@ void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
     k_fold<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
 }
 void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s) {
-    k_emit<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(EmitSmem<MR_FAST>), s>>>(g, ws);
-    k_emit_full<<<148, NT, sizeof(EmitSmem<MAXRUNS>), s>>>(g, ws);
+    k_emit<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(EmitSmem<CapS>), s>>>(g, ws);
+    k_emit_m<<<148 * 3, NT, sizeof(EmitSmem<CapM>), s>>>(g, ws);
+    k_emit_full<<<148, NT, sizeof(EmitSmem<CapF>), s>>>(g, ws);
 }
 void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
                        cudaStream_t s, int sms) {

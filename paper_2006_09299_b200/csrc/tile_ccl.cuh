@@ -27,16 +27,26 @@
 
 namespace rlg {
 
-constexpr int EVCAP = 32 * (32 / WPR) * WPR;  // events per warp <= one per pixel of its rows
+// Capacity classes of the shared-memory tables.  A tile is tried in the small class first
+// (most tiles: >= 8 CTAs per SM), and deferred through device-side lists to the larger ones
+// when it holds more runs / border components than fit:
+//   S: <= 1536 runs (0.19 runs/pixel), <= 256 border components;
+//   M: <= 5120 runs (0.62 runs/pixel, covers any random image), all border components;
+//   F: one run per pixel (checkerboards and other adversarial inputs).
+// EVC = union-event queue per warp; longer queues are processed in rounds.
+template <int MR_, int NBC_, int EVC_>
+struct Cap {
+    static constexpr int MR = MR_;
+    static constexpr int NBC = NBC_;
+    static constexpr int EVC = EVC_;
+};
+using CapS = Cap<1536, 256, 192>;
+using CapM = Cap<5120, NBMAX, 1024>;
+using CapF = Cap<MAXRUNS, NBMAX, 1024>;
 
-// MR = run capacity of the shared-memory tables.  The fast variant is sized for realistic
-// inputs (<= MR_FAST runs per tile, > 0.62 runs/pixel never happens for random images);
-// tiles beyond it are re-run by the full-capacity variant (MAXRUNS = one run per pixel).
-constexpr int MR_FAST = 5120;
-
-template <int MR>
+template <class C>
 struct CclSmem {
-    static constexpr int kRuns = MR;
+    static constexpr int MR = C::MR;
     uint32_t x[NW];            // 8-connected-value bits (pixel value XOR flip), 0 where invalid
     uint32_t vm[NW];           // valid-pixel masks
     uint32_t st[NW];           // run-start masks
@@ -50,9 +60,9 @@ struct CclSmem {
             uint16_t lcrun[MR];     // root (first) run of each tile component
             uint16_t lcb[MR];       // border index, or 0x8000 | (border components before it)
         };
-        uint16_t evq[NWARPS][EVCAP];  // union-event queues (dead before lcrun/lcb are written)
+        uint16_t evq[NWARPS][C::EVC];  // union-event queues (dead before lcrun/lcb are written)
     };
-    uint16_t blc[NBMAX];       // border index -> tile component
+    uint16_t blc[C::NBC];      // border index -> tile component
     int wsum[NWARPS + 1];
     int nruns, nlc, nb;
 };
@@ -161,8 +171,9 @@ struct WordBits {
 
 // Runs of the tile: start masks, raster-order run indices (block scan), run positions and
 // identity parents.  Returns false (uniformly) when the tile has more runs than MR.
-template <bool INIT_PAR = true, int MR>
-__device__ __forceinline__ bool tile_runs(CclSmem<MR>& S, WordBits& wb) {
+template <bool INIT_PAR = true, class C>
+__device__ __forceinline__ bool tile_runs(CclSmem<C>& S, WordBits& wb) {
+    constexpr int MR = C::MR;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
     wb.x = S.x[tid];
@@ -203,8 +214,8 @@ __device__ __forceinline__ bool tile_runs(CclSmem<MR>& S, WordBits& wb) {
     return true;
 }
 
-template <int MR>
-__device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
+template <class C>
+__device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int r = tid / WPR, w = tid % WPR;
@@ -233,6 +244,41 @@ __device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
         d1 = x & al1 & ~xl1 & na & both;  // (r, j) ~ (r-1, j-1)
         d2 = xl1 & a & nx & ~al1 & both;  // (r, j-1) ~ (r-1, j)
     }
+    __syncthreads();  // run bases of every word are visible (the init below reads the row above)
+    // ---- first contact: a run starting in this word takes the first run it touches in the
+    // row above as its initial parent (cf. Alg. 2's `era[er] = find(above)`), and that contact
+    // is not queued.  Contacts are ordered by column: the up-left diagonal at the run start
+    // (d1), vertical contacts (ev), the up-right diagonal past the run end (d2, stored at the
+    // next column).  Vertical stacks of equal runs (rows of a g x g block) need no union at all.
+    if (r >= 1 && vm) {
+        const int ta = tid - WPR;
+        const uint32_t contacts = d1 | ev | (d2 >> 1);
+        uint32_t m = wb.st;
+        int k = S.rbase[tid];
+        while (m) {
+            const int s = __ffs(m) - 1;
+            m &= m - 1u;
+            const uint32_t upto = m ? ((1u << (__ffs(m) - 1)) - 1u) : 0xFFFFFFFFu;
+            const uint32_t cseg = contacts & upto & ~((1u << s) - 1u);
+            if (cseg) {
+                const int j = __ffs(cseg) - 1;
+                const uint32_t bit = 1u << j;
+                int above;
+                if (d1 & bit) {
+                    above = run_left(S, ta, j);
+                    d1 &= ~bit;
+                } else if (ev & bit) {
+                    above = run_at(S, ta, j);
+                    ev &= ~bit;
+                } else {
+                    above = run_at(S, ta, j + 1);
+                    d2 &= ~(bit << 1);
+                }
+                S.par[k] = (uint16_t)above;
+            }
+            ++k;
+        }
+    }
     const int nev = __popc(ev) + __popc(d1) + __popc(d2);
     int incl = nev;
 #pragma unroll
@@ -241,42 +287,41 @@ __device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
         if (lane >= o) incl += n;
     }
     const int wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    {
-        uint16_t* q = S.evq[warp] + (incl - nev);
-        const uint16_t wbase = (uint16_t)(tid << 7);
-        while (ev) {
-            const int j = __ffs(ev) - 1;
-            ev &= ev - 1u;
-            *q++ = (uint16_t)(wbase | j);
+    const int my0 = incl - nev;  // offset of this lane's first event in the warp's sequence
+    __syncthreads();             // first-contact parents of every word are in place
+    // compact the warp's events into its queue (in rounds of EVC) and resolve them lane-parallel
+    for (int done = 0; done < wtot; done += C::EVC) {
+        if (nev && my0 < done + C::EVC && my0 + nev > done) {
+            int o = my0;
+            const uint16_t wbase = (uint16_t)(tid << 7);
+            auto put = [&](uint32_t code) {
+                if (o >= done && o < done + C::EVC) S.evq[warp][o - done] = (uint16_t)code;
+                ++o;
+            };
+            for (uint32_t e = ev; e; e &= e - 1u) put(wbase | (__ffs(e) - 1));
+            for (uint32_t e = d1; e; e &= e - 1u) put(wbase | (1u << 5) | (__ffs(e) - 1));
+            for (uint32_t e = d2; e; e &= e - 1u) put(wbase | (2u << 5) | (__ffs(e) - 1));
         }
-        while (d1) {
-            const int j = __ffs(d1) - 1;
-            d1 &= d1 - 1u;
-            *q++ = (uint16_t)(wbase | (1 << 5) | j);
+        __syncwarp();
+        const int cnt = min(C::EVC, wtot - done);
+        for (int k = lane; k < cnt; k += 32) {
+            const uint32_t e = S.evq[warp][k];
+            const int word = (int)(e >> 7), type = (int)((e >> 5) & 3u), j = (int)(e & 31u);
+            const int wa = word - WPR;
+            uint32_t ra, rb2;
+            if (type == 0) {
+                ra = (uint32_t)run_at(S, word, j);
+                rb2 = (uint32_t)run_at(S, wa, j);
+            } else if (type == 1) {
+                ra = (uint32_t)run_at(S, word, j);
+                rb2 = (uint32_t)run_left(S, wa, j);
+            } else {
+                ra = (uint32_t)run_left(S, word, j);
+                rb2 = (uint32_t)run_at(S, wa, j);
+            }
+            sunion(S.par, ra, rb2);
         }
-        while (d2) {
-            const int j = __ffs(d2) - 1;
-            d2 &= d2 - 1u;
-            *q++ = (uint16_t)(wbase | (2 << 5) | j);
-        }
-    }
-    __syncthreads();  // runpos/par/st/rbase of all words ready
-    for (int k = lane; k < wtot; k += 32) {
-        const uint32_t e = S.evq[warp][k];
-        const int word = (int)(e >> 7), type = (int)((e >> 5) & 3u), j = (int)(e & 31u);
-        const int wa = word - WPR;
-        uint32_t ra, rb2;
-        if (type == 0) {
-            ra = (uint32_t)run_at(S, word, j);
-            rb2 = (uint32_t)run_at(S, wa, j);
-        } else if (type == 1) {
-            ra = (uint32_t)run_at(S, word, j);
-            rb2 = (uint32_t)run_left(S, wa, j);
-        } else {
-            ra = (uint32_t)run_left(S, word, j);
-            rb2 = (uint32_t)run_at(S, wa, j);
-        }
-        sunion(S.par, ra, rb2);
+        __syncwarp();
     }
     __syncthreads();
 
@@ -339,6 +384,7 @@ __device__ bool ccl_tile(CclSmem<MR>& S, const TileGeom& tg) {
     for (int l = l0; l < l1; ++l) cnt += S.lcb[l];
     int nb;
     int bx = block_excl_scan(cnt, S.wsum, nb);
+    if (nb > C::NBC) return false;  // more border components than this class holds
     for (int l = l0; l < l1; ++l) {
         if (S.lcb[l]) {
             S.blc[bx] = (uint16_t)l;
