@@ -11,7 +11,7 @@ namespace rlg {
 // ---- tile geometry -------------------------------------------------------------------
 // One CTA owns one TH x TW tile.  Pixels are bit-packed: one 32-bit word = 32 pixels of a
 // row, bit j = column 32*w + j.  One thread per word.
-constexpr int TH = 32;                 // tile rows
+constexpr int TH = 32;                 // tile rows (64 was measured slower: longer CTA critical path)
 constexpr int TW = 256;                // tile columns
 constexpr int WPR = TW / 32;           // words per tile row
 constexpr int NW = TH * WPR;           // words per tile
@@ -21,7 +21,7 @@ constexpr int MAXRUNS = TH * TW;       // runs per tile <= pixels
 constexpr int MAXLC = MAXRUNS;         // tile-local components <= runs
 constexpr int PERIM = 2 * TW + 2 * TH; // perimeter label slots: top, bottom, left, right
 constexpr int NBMAX = PERIM;           // border components per tile <= perimeter pixels
-constexpr int FCH = 512;               // interior-feature accumulator chunk (K1b)
+
 constexpr uint32_t TAG16 = 0x8000u;    // run-parent slot holds a tile-component index
 constexpr uint16_t PERIM_NONE = 0xFFFF;
 

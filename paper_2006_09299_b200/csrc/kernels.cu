@@ -580,8 +580,8 @@ template <class C>
 struct EmitSmem {
     CclSmem<C> c;
     // interior-feature chunk accumulators (tile-local coordinates)
-    uint32_t fs[FCH], fsx[FCH], fsy[FCH];
-    int32_t frmax[FCH], fcmin[FCH], fcmax[FCH];
+    uint32_t fs[C::FCH], fsx[C::FCH], fsy[C::FCH];
+    int32_t frmax[C::FCH], fcmin[C::FCH], fcmax[C::FCH];
     // border components of this tile
     uint32_t bcid[C::NBC];   // canonical id of the component
     uint32_t banc[C::NBC];   // canonical id of its post-fill root
@@ -743,12 +743,12 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         }
     }
 
-    // ---- interior components, in chunks of FCH tile components
+    // ---- interior components, in chunks of C::FCH tile components
     const int flip = g.flip;
     int nsurv = 0;
-    for (int l0 = 0; l0 < nlc; l0 += FCH) {
-        const int l1 = min(l0 + FCH, nlc);
-        for (int i = tid; i < FCH; i += NT) {
+    for (int l0 = 0; l0 < nlc; l0 += C::FCH) {
+        const int l1 = min(l0 + C::FCH, nlc);
+        for (int i = tid; i < C::FCH; i += NT) {
             E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
             E.frmax[i] = -1;
             E.fcmin[i] = 0x7FFFFFFF;

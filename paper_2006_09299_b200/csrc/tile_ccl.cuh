@@ -30,19 +30,20 @@ namespace rlg {
 // Capacity classes of the shared-memory tables.  A tile is tried in the small class first
 // (most tiles: >= 8 CTAs per SM), and deferred through device-side lists to the larger ones
 // when it holds more runs / border components than fit:
-//   S: <= 1536 runs (0.19 runs/pixel), <= 256 border components;
-//   M: <= 5120 runs (0.62 runs/pixel, covers any random image), all border components;
+//   S: <= MAXRUNS * 3/16 runs (0.19 runs/pixel), <= NBMAX/2 border components;
+//   M: <= MAXRUNS * 5/8 runs (0.62 runs/pixel, covers any random image), all border components;
 //   F: one run per pixel (checkerboards and other adversarial inputs).
 // EVC = union-event queue per warp; longer queues are processed in rounds.
-template <int MR_, int NBC_, int EVC_>
+template <int MR_, int NBC_, int EVC_, int FCH_>
 struct Cap {
     static constexpr int MR = MR_;
     static constexpr int NBC = NBC_;
     static constexpr int EVC = EVC_;
+    static constexpr int FCH = FCH_;  // interior-feature accumulator chunk (emit pass)
 };
-using CapS = Cap<1536, 256, 192>;
-using CapM = Cap<5120, NBMAX, 1024>;
-using CapF = Cap<MAXRUNS, NBMAX, 1024>;
+using CapS = Cap<MAXRUNS * 3 / 16, NBMAX / 2, 192, 512>;
+using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 320>;
+using CapF = Cap<MAXRUNS, NBMAX, 1024, 320>;
 
 template <class C>
 struct CclSmem {
