@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librunlab_gpu.so")
+LIB_PATH = os.environ.get("RUNLAB_GPU_LIB", os.path.join(HERE, "librunlab_gpu.so"))
 
 RL_OK, RL_EINVAL, RL_ELOGIC, RL_EOVERFLOW, RL_ECUDA, RL_ENOMEM, RL_EINTERNAL = range(7)
 

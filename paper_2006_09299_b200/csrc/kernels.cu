@@ -44,6 +44,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     CclSmem<C>& S = A.c;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
+    RL_PHASE(tg.t, 0);
 
     // ---- load 32 pixels (bytes) of this thread's word and pack them to bits
     const uint32_t vm = valid_mask(tg, r, w);
@@ -83,15 +84,19 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     }
     __syncthreads();
 
+    RL_PHASE(tg.t, 1);
     if (!ccl_tile(S, tg)) return false;
 
     const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
+    // the two allocations are issued by different warps so their latencies overlap
     if (tid == 0) {
         const uint32_t base = atomicAdd(&ws.counters[0], (uint32_t)nb);
         A.base = base;
         if ((uint64_t)base + nb > ws.cap_nodes) atomicOr(&ws.counters[1], ERR_NODE_CAP);
         ws.tbase[tg.t] = base;
         ws.tnb[tg.t] = (uint32_t)nb;
+    }
+    if (tid == 32) {
         const unsigned long long need = (unsigned long long)nruns + 2ull * (unsigned long long)nlc;
         const unsigned long long off = atomicAdd(ws.rused, need);
         A.moff = off;
@@ -126,27 +131,70 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         }
     }
 
+    RL_PHASE(tg.t, 9);
     // ---- border-component features and image-border contact (one lane per run)
     const bool top_img = tg.ty == 0, bot_img = (tg.y0 + tg.th == g.H);
     const bool left_img = tg.tx == 0, right_img = (tg.x0 + tg.tw == g.W);
-    for (int i = tid; i < nruns; i += NT) {
-        const uint32_t lc = lc_of_run(S, i);
-        if (!lc_is_border(S, lc)) continue;
-        const int bi = S.lcb[lc];
-        const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
-        const uint32_t n = (uint32_t)(c1 - c0);
-        atomicAdd(&A.bs[bi], n);
-        atomicAdd(&A.bsx[bi], n * (uint32_t)(c0 + c1 - 1) / 2u);
-        atomicAdd(&A.bsy[bi], n * (uint32_t)rr);
-        atomicMax(&A.brmax[bi], rr);
-        atomicMin(&A.bcmin[bi], c0);
-        atomicMax(&A.bcmax[bi], c1 - 1);
-        if ((top_img && rr == 0) || (bot_img && rr == tg.th - 1) || (left_img && c0 == 0) ||
-            (right_img && c1 == tg.tw))
-            A.bimg[bi] = 1;
+    // Runs of one large border component (the percolating one) would all hit the same shared
+    // accumulators.  Per warp iteration, the component of the first border run is the candidate:
+    // its lanes reduce in registers (REDUX) and one lane does the atomics; the other lanes
+    // accumulate directly.
+    constexpr int U = 4;  // loads of U iterations are issued together (latency hiding)
+    for (int j0 = 0; j0 < nruns; j0 += U * NT) {
+      uint16_t lbv[U], rpv[U], nxv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+          const int i = j0 + u * NT + tid;
+          const bool ok = i < nruns;
+          const uint32_t lc = ok ? lc_of_run(S, i) : 0u;
+          rpv[u] = ok ? S.runpos[i] : 0;
+          nxv[u] = (i + 1 < nruns) ? S.runpos[i + 1] : 0xFFFF;
+          lbv[u] = ok ? S.lcb[lc] : 0x8000;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int bi = -1, rr = 0, c0 = 0x7FFFFFFF, cl = -1;
+        uint32_t n = 0, sx = 0, sy = 0, img = 0;
+        if (!(lbv[u] & 0x8000u)) {
+            bi = lbv[u];
+            rr = rpv[u] >> 8;
+            c0 = rpv[u] & 0xFF;
+            const int c1 = ((nxv[u] >> 8) == rr) ? (nxv[u] & 0xFF) : tg.tw;
+            n = (uint32_t)(c1 - c0);
+            sx = n * (uint32_t)(c0 + c1 - 1) / 2u;
+            sy = n * (uint32_t)rr;
+            cl = c1 - 1;
+            img = ((top_img && rr == 0) || (bot_img && rr == tg.th - 1) || (left_img && c0 == 0) ||
+                   (right_img && c1 == tg.tw)) ? 1u : 0u;
+        }
+        const uint32_t valid = __ballot_sync(0xFFFFFFFFu, bi >= 0);
+        if (!valid) continue;
+        const int cand = __shfl_sync(0xFFFFFFFFu, bi, __ffs(valid) - 1);
+        const uint32_t grp = __ballot_sync(0xFFFFFFFFu, bi == cand);
+        if (bi == cand) {
+            n = __reduce_add_sync(grp, n);
+            sx = __reduce_add_sync(grp, sx);
+            sy = __reduce_add_sync(grp, sy);
+            rr = __reduce_max_sync(grp, rr);
+            c0 = __reduce_min_sync(grp, c0);
+            cl = __reduce_max_sync(grp, cl);
+            img = __reduce_or_sync(grp, img);
+            if ((int)(tid & 31) != __ffs(grp) - 1) bi = -1;  // the leader commits the group
+        }
+        if (bi >= 0) {
+            atomicAdd(&A.bs[bi], n);
+            atomicAdd(&A.bsx[bi], sx);
+            atomicAdd(&A.bsy[bi], sy);
+            atomicMax(&A.brmax[bi], rr);
+            atomicMin(&A.bcmin[bi], c0);
+            atomicMax(&A.bcmax[bi], cl);
+            if (img) A.bimg[bi] = 1;
+        }
+      }
     }
     __syncthreads();
 
+    RL_PHASE(tg.t, 10);
     // ---- border-component nodes
     const uint32_t base = A.base;
     const bool node_ok = (uint64_t)base + nb <= ws.cap_nodes;
@@ -224,7 +272,9 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         if (lc_is_border(S, l)) continue;
         nfg += (int)(xbit(S, lc_row(S, l), lc_col(S, l)) ^ (uint32_t)flip);
     }
+    RL_PHASE(tg.t, 11);
     nfg = block_reduce_sum(nfg, S.wsum);
+    RL_PHASE(tg.t, 12);
     if (tid == 0 && nfg) atomicAdd(&ws.img_fg[tg.b], (uint32_t)nfg);
     return true;
 }
@@ -1034,3 +1084,12 @@ void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, 
 }
 
 }  // namespace rlg
+
+#ifdef RL_PHASE_PROF
+// profiling builds only: where the tile kernels stamp their phases
+extern "C" int rl_debug_phase_buffer(void* dptr, int n_tiles) {
+    unsigned long long* p = static_cast<unsigned long long*>(dptr);
+    if (cudaMemcpyToSymbol(rlg::g_phase_buf, &p, sizeof(p)) != cudaSuccess) return 4;
+    return cudaMemcpyToSymbol(rlg::g_phase_n, &n_tiles, sizeof(int)) == cudaSuccess ? 0 : 4;
+}
+#endif

@@ -27,6 +27,22 @@
 
 namespace rlg {
 
+// Optional per-phase clock64() stamps of each tile CTA (profiling builds only:
+// -DRL_PHASE_PROF; tools/phase_prof.py).  Slot 16*tile + k holds the stamp of phase k.
+#ifdef RL_PHASE_PROF
+__device__ unsigned long long* g_phase_buf = nullptr;
+__device__ int g_phase_n = 0;
+#define RL_PHASE(tile, k)                                                         \
+    do {                                                                          \
+        if (threadIdx.x == 0 && g_phase_buf && (tile) < g_phase_n)               \
+            g_phase_buf[16ull * (unsigned)(tile) + (k)] = clock64();              \
+    } while (0)
+#else
+#define RL_PHASE(tile, k) \
+    do {                  \
+    } while (0)
+#endif
+
 // Capacity classes of the shared-memory tables.  A tile is tried in the small class first
 // (most tiles: >= 8 CTAs per SM), and deferred through device-side lists to the larger ones
 // when it holds more runs / border components than fit:
@@ -222,6 +238,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     const int r = tid / WPR, w = tid % WPR;
     WordBits wb;
     if (!tile_runs(S, wb)) return false;
+    RL_PHASE(tg.t, 2);
     const uint32_t x = wb.x, nx = wb.nx, vm = wb.vm, c1 = wb.c1, s1 = wb.s1, s0 = wb.s0;
     // ---- union events with the row above (Alg. 2's overlap test, one event per pair),
     // compacted into the warp's queue: entry = (word << 7) | (type << 5) | bit
@@ -290,6 +307,25 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     const int wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
     const int my0 = incl - nev;  // offset of this lane's first event in the warp's sequence
     __syncthreads();             // first-contact parents of every word are in place
+    // The first-contact forest links every run to one in the row above, so a vertical stack
+    // of runs is a chain as tall as the stack.  Pointer jumping flattens it (log2 of the tile
+    // height rounds) so that the finds of the union phase are short.
+    {
+        const int nr = S.nruns;
+        for (;;) {
+            int changed = 0;
+            for (int i = tid; i < nr; i += NT) {
+                const uint32_t p = S.par[i];
+                const uint32_t gp = S.par[p];
+                if (gp != p) {
+                    S.par[i] = (uint16_t)gp;
+                    changed = 1;
+                }
+            }
+            if (!__syncthreads_or(changed)) break;
+        }
+    }
+    RL_PHASE(tg.t, 3);
     // compact the warp's events into its queue (in rounds of EVC) and resolve them lane-parallel
     for (int done = 0; done < wtot; done += C::EVC) {
         if (nev && my0 < done + C::EVC && my0 + nev > done) {
@@ -325,6 +361,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
         __syncwarp();
     }
     __syncthreads();
+    RL_PHASE(tg.t, 4);
 
     // ---- flatten (roots are final now): a short walk, then pointer jumping until every run
     // points at its root (vertical stacks of runs form chains as long as the tile is tall)
@@ -344,6 +381,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
         }
         if (!__syncthreads_or(changed)) break;
     }
+    RL_PHASE(tg.t, 5);
 
     // ---- tile components = root runs, numbered in raster order (contiguous run chunks)
     const int per = (nruns + NT - 1) / NT;
@@ -365,6 +403,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     if (tid == 0) S.nlc = nlc;
     if (tid >= tg.th && tid <= TH) S.rowlc[tid] = (uint16_t)nlc;  // rows without pixels
     __syncthreads();
+    RL_PHASE(tg.t, 6);
     // resolve non-root runs; mark components touching the tile border (plain stores of 1)
     for (int i = tid; i < nruns; i += NT) {
         uint32_t p = S.par[i];
@@ -377,6 +416,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
             S.lcb[p & 0x7FFFu] = 1;
     }
     __syncthreads();
+    RL_PHASE(tg.t, 7);
 
     // ---- compact border components to border indices (raster order)
     const int perl = (nlc + NT - 1) / NT;
@@ -401,6 +441,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
         S.rowbx[tid] = l < nlc ? (uint16_t)(S.lcb[l] & 0x7FFF) : (uint16_t)nb;
     }
     __syncthreads();
+    RL_PHASE(tg.t, 8);
     return true;
 }
 

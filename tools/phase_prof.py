@@ -1,0 +1,61 @@
+#!/usr/bin/env python
+"""Per-phase latency of the analyze-pass tile CTAs (clock64 stamps of a profiling build).
+
+Build here:  nvcc ... -DRL_PHASE_PROF -o paper_2006_09299_b200/librunlab_gpu_prof.so
+Run on GPU:  python tools/phase_prof.py --cells 0.5:1 --copies 4
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("RUNLAB_GPU_LIB", os.path.join(ROOT, "paper_2006_09299_b200", "librunlab_gpu_prof.so"))
+
+NAMES = ["start", "load+init", "runs(scan)", "events+first-contact", "union", "flatten", "lc-assign",
+         "relabel+flags", "border-compact", "header+map", "border-features", "nodes+perim+cnt", "fg-reduce"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cells", default="0.5:1")
+    ap.add_argument("--copies", type=int, default=4)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    from paper_2006_09299_b200 import Labeler, LabelingConfig, _native
+    from paper_2006_09299_b200.runlab import generate_device
+
+    L = _native.load()
+    L.rl_debug_phase_buffer.argtypes = [C.c_void_p, C.c_int]
+    cells = [tuple(float(v) if i == 0 else int(v) for i, v in enumerate(c.split(":"))) for c in args.cells.split(",")]
+    S = 2048
+    B = len(cells) * args.copies
+    imgs = torch.empty((B, S, S), dtype=torch.uint8, device="cuda")
+    for i in range(B):
+        d, g = cells[i % len(cells)]
+        generate_device(imgs[i].data_ptr(), S, S, d, g, 1 + i)
+    ntiles = B * (S // 32) * (S // 256)
+    buf = torch.zeros(ntiles * 16, dtype=torch.int64, device="cuda")
+    lab = Labeler(0)
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    lab.label_device(imgs.data_ptr(), S, S, B, cfg)
+    lab.sync()
+    assert L.rl_debug_phase_buffer(C.c_void_p(buf.data_ptr()), ntiles) == 0
+    buf.zero_()
+    lab.label_device(imgs.data_ptr(), S, S, B, cfg)
+    lab.sync()
+    st = buf.view(ntiles, 16).cpu().numpy().astype(np.float64)
+    ok = (st[:, :13] > 0).all(axis=1)
+    d = np.diff(st[ok, :13], axis=1)
+    print(f"tiles with complete stamps: {ok.sum()} / {ntiles}; mean CTA latency "
+          f"{(st[ok, 12] - st[ok, 0]).mean():.0f} cycles")
+    for k in range(12):
+        print(f"  {NAMES[k + 1]:22s} {d[:, k].mean():9.0f} cycles  (p90 {np.percentile(d[:, k], 90):9.0f})")
+
+
+if __name__ == "__main__":
+    main()
