@@ -1,23 +1,23 @@
 #!/usr/bin/env python
 """Benchmark: full FG/BG connected-component labeling + analysis (features, Euler number,
-adjacency tree, hole filling) on B200, BASELINE config 2.
+adjacency tree, hole filling) on B200.
 
-One step = one pass of the whole pipeline over the config-2 sweep: 105 images of 2048 x 2048,
-density k/20 (k = 0..20) x granularity {1, 2, 4, 8, 16}, seed 1, generated on the device with
-the reference's generator (bit-identical; tests/test_gpu_generate.py).  Inputs stay resident in
-HBM (440 MB > 126 MB L2, so no L2 flush is needed between steps).
+Default workload = BASELINE config 2 (the config the metric is quoted on): one step labels the
+whole sweep of 105 images of 2048 x 2048, density k/20 (k = 0..20) x granularity
+{1, 2, 4, 8, 16}, seed 1.  Inputs are generated on the device with the reference's generator
+(bit-identical: tests/test_gpu_generate.py) and stay resident in HBM (440 MB > 126 MB L2, so
+no L2 flush is needed between steps).  `--config cfg1|cfg3|cfg4|cfg5` runs the other BASELINE
+configs (cfg4 shards its 4096 images across ranks; the others run one replica per rank).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfgX]
 
-Under torchrun each rank labels its own copy of the sweep (weak scaling, no collective on
-the data path); time = max over ranks of the CUDA-event time; value = all ranks' pixels / time.
-``--impl reference`` times the reference's own CPU path (oracle/_ref, compiled from the
-unmodified reference headers) on the host cores, rank 0 only.
+Under torchrun each rank times its own work with CUDA events; time = max over ranks; value =
+all ranks' pixels / time.  `--impl reference` times the reference's own CPU path
+(oracle/_ref, compiled from the unmodified reference headers) on the host cores, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
 import os
 import statistics
@@ -31,20 +31,99 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Gpixel/s full FG/BG CCA (features+Euler+tree+hole fill); % of HBM roofline"
-W_IMG, H_IMG = 2048, 2048
+
+
+# ------------------------------------------------------------------------------ workloads
+class Workload:
+    """A BASELINE config: image shape, per-image generator specs, sharding."""
+
+    def __init__(self, name: str):
+        from paper_2006_09299_b200.runlab import cfg2_cells, cfg4_params
+        self.name = name
+        if name == "cfg1":
+            self.W = self.H = 1024
+            self.specs = [("gen", 0.5, 1, 1)]
+            self.desc = "cfg1: 1 x 1024x1024, Bernoulli(0.5), g=1, seed 1"
+            self.shard = False
+        elif name == "cfg2":
+            self.W = self.H = 2048
+            self.specs = [("gen", d, g, 1) for d, g in cfg2_cells()]
+            self.desc = "cfg2: 105 x 2048x2048, density k/20 (k=0..20) x granularity {1,2,4,8,16}, seed 1"
+            self.shard = False
+        elif name == "cfg3":
+            self.W = self.H = 4096
+            self.specs = [("rings", 64, 3, 0.02)]
+            self.desc = "cfg3: 1 x 4096x4096 nested rings (64x64 blocks, k<=16 rings, 2% salt), seed 3"
+            self.shard = False
+        elif name == "cfg4":
+            self.W, self.H = 1920, 1080
+            self.specs = [("gen",) + cfg4_params(i) + (i,) for i in range(4096)]
+            self.desc = "cfg4: 4096 x 1920x1080, density U[0.1,0.9], granularity U{1..8}, seed i"
+            self.shard = True
+        elif name == "cfg5":
+            self.W = self.H = 32768
+            self.specs = [("gen", 0.45, 4, 5)]
+            self.desc = "cfg5: 1 x 32768x32768 (1 Gpixel), Bernoulli(0.45), g=4, seed 5"
+            self.shard = False
+        else:
+            raise SystemExit(f"unknown config {name}")
+
+    def local_specs(self, rank: int, world: int):
+        if not self.shard:
+            return self.specs
+        from paper_2006_09299_b200.distributed import shard_range
+        lo, hi = shard_range(len(self.specs), rank, world)
+        return self.specs[lo:hi]
+
+    def make_device(self, specs):
+        import torch
+        from paper_2006_09299_b200.runlab import generate_device, generate_rings_device
+        imgs = torch.empty((len(specs), self.H, self.W), dtype=torch.uint8, device="cuda")
+        for i, s in enumerate(specs):
+            if s[0] == "gen":
+                generate_device(imgs[i].data_ptr(), self.W, self.H, s[1], s[2], s[3])
+            else:
+                generate_rings_device(imgs[i].data_ptr(), self.W, self.H, s[1], s[2], s[3])
+        torch.cuda.synchronize()
+        return imgs
+
+    def make_host(self, specs) -> np.ndarray:
+        """Same inputs on the host via the oracle's generators (CPU legs only)."""
+        from oracle import oracle as O
+        out = np.empty((len(specs), self.H, self.W), dtype=np.uint8)
+        for i, s in enumerate(specs):
+            out[i] = (O.generate(self.W, self.H, s[1], s[2], s[3]) if s[0] == "gen"
+                      else O.generate_rings(self.W, self.H, s[1], s[2], s[3]))
+        return out
+
+    def cpu_sample(self):
+        """Bounded sample for the CPU baseline (about 5-30 s of single-core work)."""
+        if self.name == "cfg2":
+            return self.specs[::5], "21 of the 105 config-2 images (every 5th cell)"
+        if self.name == "cfg4":
+            return self.specs[:64], "the first 64 of the 4096 config-4 images"
+        if self.name == "cfg5":
+            return None, "1 Gpixel image too large for a bounded sample; see BASELINE.md (3.0 s, 1 core)"
+        return self.specs, "the full workload"
 
 
 def measured_peaks() -> tuple[float, str]:
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def cells():
-    return [(k / 20.0, g) for k in range(21) for g in (1, 2, 4, 8, 16)]
+def profiled_traffic(config: str, kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu capture of this workload."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel), os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -58,7 +137,6 @@ class ClockSampler:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
-        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -96,7 +174,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------------------------ reference arm
+# ------------------------------------------------------------------------------ CPU side
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -115,20 +193,13 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def reference_images(idx: list[int]) -> np.ndarray:
-    """Config-2 inputs on the host via the oracle's generator (bench's CPU legs only)."""
-    from oracle import oracle as O
-    cs = cells()
-    return np.stack([O.generate(W_IMG, H_IMG, cs[i][0], cs[i][1], 1) for i in idx])
-
-
 def time_reference(imgs: np.ndarray, threads: int) -> float:
     from oracle import oracle as O
     secs, _ = O.ref_time_batch(imgs, 0, threads)
     return secs
 
 
-def run_reference_arm(args, rank: int) -> None:
+def run_reference_arm(args, wl: Workload, rank: int) -> None:
     """--impl reference: the reference's own CPU path, all host threads, rank 0 only."""
     if rank != 0:
         return
@@ -137,27 +208,28 @@ def run_reference_arm(args, rank: int) -> None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_runlab.so not built"}))
         return
     threads = cpu_threads()
-    idx = list(range(len(cells())))
-    imgs = reference_images(idx)
-    px = imgs.shape[0] * W_IMG * H_IMG
+    specs = wl.specs if wl.name != "cfg4" else wl.specs[:512]
+    imgs = wl.make_host(specs)
+    px = imgs.shape[0] * wl.W * wl.H
     for _ in range(args.warmup):
         time_reference(imgs, threads)
     times = [time_reference(imgs, threads) for _ in range(args.steps)]
     t = sum(times) / len(times)
     value = px / t / 1e9
-    sample = f"full config-2 sweep ({imgs.shape[0]} images of {W_IMG}x{H_IMG}) per step, one image per thread"
-    line = {
+    sample = (f"{imgs.shape[0]} images of {wl.W}x{wl.H} per step"
+              + (" (first 512 of 4096)" if wl.name == "cfg4" else " (the full workload)")
+              + ", one image per thread")
+    print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpixel/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (reference generator, seed 1)",
-        "config": {"workload": "cfg2: 105 x 2048x2048, d=k/20 x g in {1,2,4,8,16}, fg8_bg4",
+        "data": "synthetic (reference generator)",
+        "config": {"workload": wl.desc + ", fg8_bg4",
                    "path": "label_image(features,euler) + label_image(fill,features,relabel) + binarize_labels"},
         "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": threads, "kind": "reference",
                          "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
+    }))
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -167,44 +239,42 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = Workload(args.config)
 
     if args.impl == "reference":
-        run_reference_arm(args, rank)
+        run_reference_arm(args, wl, rank)
         return
+    args.warmup = max(args.warmup, 3)
 
     import torch
     import torch.distributed as dist
 
     from paper_2006_09299_b200 import Labeler, LabelingConfig
     from paper_2006_09299_b200 import _native as N
-    from paper_2006_09299_b200.runlab import generate_device
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    cs = cells()
-    B = len(cs)
-    P = W_IMG * H_IMG
-    imgs = torch.empty((B, H_IMG, W_IMG), dtype=torch.uint8, device="cuda")
-    for i, (d, g) in enumerate(cs):
-        generate_device(imgs[i].data_ptr(), W_IMG, H_IMG, d, g, 1)
-    torch.cuda.synchronize()
+    specs = wl.local_specs(rank, world)
+    B = len(specs)
+    P = wl.W * wl.H
+    imgs = wl.make_device(specs)
 
     lab = Labeler(local)
     cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
     stream = torch.cuda.ExternalStream(lab.stream())
 
     def step():
-        lab.label_device(imgs.data_ptr(), W_IMG, H_IMG, B, cfg)
+        lab.label_device(imgs.data_ptr(), wl.W, wl.H, B, cfg)
 
     for _ in range(args.warmup):
         step()
@@ -212,7 +282,7 @@ def main() -> None:
 
     clocks = ClockSampler(local)
     clocks.start()
-    t_busy = time.time() + 0.3  # put the GPU under load before the timed region
+    t_busy = time.time() + 0.3  # the GPU is under load before the timed region
     while time.time() < t_busy:
         step()
         lab.sync()
@@ -233,8 +303,7 @@ def main() -> None:
     launches_per_step = lab.launch_count()
     if world > 1:
         dist.barrier()
-    # keep the same load a little longer so the clock sampler brackets the timed region
-    t_busy = time.time() + 0.3
+    t_busy = time.time() + 0.3  # same load a little longer: the sampler brackets the region
     while time.time() < t_busy:
         step()
         lab.sync()
@@ -245,7 +314,6 @@ def main() -> None:
         t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-
     ana = statistics.mean(p.analyze_ms for p in phases)
     mer = statistics.mean(p.merge_ms for p in phases)
     emi = statistics.mean(p.emit_ms for p in phases)
@@ -255,18 +323,24 @@ def main() -> None:
     c_pre = int(res.n_components.sum())
     c_post = int(res.n_survivors.sum())
     px = B * P
+    total_px = px
+    if world > 1:
+        t = torch.tensor([px], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        total_px = int(t.item())
     bytes_alg = 2 * px + 48 * c_pre + 40 * c_post
     peak, peak_src = measured_peaks()
     pipe_gbs = bytes_alg / (ms_step / 1e3) / 1e9
-    dom = max((("analyze", ana, px), ("emit", emi, px + 48 * c_pre + 40 * c_post)), key=lambda x: x[1])
+    dom = max((("k_analyze", ana, px), ("k_emit", emi, px + 48 * c_pre + 40 * c_post)), key=lambda x: x[1])
     dom_gbs = dom[2] / (dom[1] / 1e3) / 1e9
+    traffic, traffic_src = profiled_traffic(args.config, dom[0])
 
     # ---- e2e: the host-buffer C-ABI call (pinned host in/out, copies inside the timed region)
     e2e = None
     if args.e2e_steps > 0:
-        h_in = torch.empty((B, H_IMG, W_IMG), dtype=torch.uint8, pin_memory=True)
+        h_in = torch.empty((B, wl.H, wl.W), dtype=torch.uint8, pin_memory=True)
         h_in.copy_(imgs.cpu())
-        h_fill = torch.empty((B, H_IMG, W_IMG), dtype=torch.uint8, pin_memory=True)
+        h_fill = torch.empty((B, wl.H, wl.W), dtype=torch.uint8, pin_memory=True)
         cap = c_pre + 1024
         h_comps = torch.empty(cap * 48, dtype=torch.uint8, pin_memory=True)
         h_top = torch.empty(cap * 4, dtype=torch.uint8, pin_memory=True)
@@ -275,19 +349,19 @@ def main() -> None:
         h_off = torch.empty(B + 1, dtype=torch.int64, pin_memory=True)
         outs = N.RlHostOutputs(h_fill.data_ptr(), None, h_comps.data_ptr(), h_top.data_ptr(),
                                h_filled.data_ptr(), cap, h_summ.data_ptr(), h_off.data_ptr(), 0, 0, 0)
-        lab.label_into(h_in.data_ptr(), W_IMG, H_IMG, B, cfg, outs)  # warm
+        lab.label_into(h_in.data_ptr(), wl.W, wl.H, B, cfg, outs)  # warm
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            lab.label_into(h_in.data_ptr(), W_IMG, H_IMG, B, cfg, outs)
+            lab.label_into(h_in.data_ptr(), wl.W, wl.H, B, cfg, outs)
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         if world > 1:
             t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         assert np.array_equal(h_summ.numpy().reshape(B, 5)[:, 0], res.n_components), "e2e result mismatch"
-        e2e = {"value": world * px / e2e_s / 1e9, "unit": "Gpixel/s",
+        e2e = {"value": total_px / e2e_s / 1e9, "unit": "Gpixel/s",
                "h2d_bytes_per_step": int(outs.h2d_bytes), "d2h_bytes_per_step": int(outs.d2h_bytes),
                "ms_per_step": e2e_s * 1e3,
                "api": "rl_label_into (pinned host pixels in; filled image, component records, "
@@ -298,33 +372,37 @@ def main() -> None:
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O
-            if O.ref_available():
-                idx = list(range(0, B, 5))  # 21 of the 105 cells, every granularity and density
-                h_imgs = reference_images(idx)
+            sample_specs, sample_desc = wl.cpu_sample()
+            if O.ref_available() and sample_specs is not None:
+                h_imgs = wl.make_host(sample_specs)
                 threads = cpu_threads()
                 secs = time_reference(h_imgs, threads)
                 cpu = {"value": h_imgs.shape[0] * P / secs / 1e9, "unit": "Gpixel/s", "cores": threads,
                        "kind": "reference",
-                       "sample": f"{len(idx)} of the 105 config-2 images (every 5th cell), one image per "
-                                 f"thread, same-outputs path (2x label_image + binarize_labels)",
+                       "sample": f"{sample_desc}, one image per thread, same-outputs path "
+                                 "(2x label_image + binarize_labels)",
                        "cpu": cpu_model(), "seconds": secs}
+            elif sample_specs is None:
+                cpu = {"value": None, "unit": "Gpixel/s", "cores": 0, "kind": "reference", "sample": sample_desc}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "Gpixel/s", "cores": 0, "kind": "reference",
                    "sample": f"failed: {exc}"}
 
     if rank == 0:
+        scaling = "strong" if (wl.shard and world > 1) else "weak"
         line = {
-            "metric": METRIC, "value": world * px / (ms_step / 1e3) / 1e9, "unit": "Gpixel/s",
+            "metric": METRIC, "value": total_px / (ms_step / 1e3) / 1e9, "unit": "Gpixel/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (reference generator on device, seed 1)",
-            "config": {"workload": "cfg2: 105 x 2048x2048, density k/20 (k=0..20) x granularity {1,2,4,8,16}, "
-                                   "fg8_bg4, features+Euler+tree+hole fill",
-                       "images_per_gpu": B, "pixels_per_gpu": px, "l2": "inputs 440 MB > L2, no flush",
-                       "parallelism": f"batch sharding x{world} (replica per rank)"},
-            "roofline": {"bound": "hbm", "kernel": f"k_{dom[0]}", "achieved": dom_gbs, "peak": peak,
-                         "unit": "GB/s", "frac": dom_gbs / peak, "traffic": None,
-                         "peak_source": peak_src,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (reference generator on device)",
+            "config": {"workload": wl.desc + ", fg8_bg4, features+Euler+tree+hole fill",
+                       "images_per_gpu": B, "pixels_per_gpu": px,
+                       "l2": "inputs > L2 (no flush)" if px > 126e6 else "inputs fit L2 (cfg1/cfg3 are launch-bound single images)",
+                       "parallelism": (f"batch sharded by image x{world}" if wl.shard and world > 1
+                                       else f"replica per rank x{world}")},
+            "roofline": {"bound": "hbm", "kernel": dom[0] + " (+ deferred-class launches)", "achieved": dom_gbs,
+                         "peak": peak, "unit": "GB/s", "frac": dom_gbs / peak, "traffic": traffic,
+                         "traffic_source": traffic_src, "peak_source": peak_src,
                          "alg_bytes_per_launch": dom[2], "avg_launch_ms": dom[1],
                          "pipeline": {"alg_bytes_per_step": bytes_alg, "achieved": pipe_gbs,
                                       "frac": pipe_gbs / peak, "c_pre": c_pre, "c_post": c_post,

@@ -167,7 +167,8 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
 
     const int64_t ncnt = (int64_t)B * H * g.ntx + 1;
     if (ctx->cap_nodes == 0) ctx->cap_nodes = (uint32_t)std::min<int64_t>(std::max<int64_t>(ntiles * 96, 4096), 0xF0000000ll);
-    if (ctx->cap_comps == 0) ctx->cap_comps = (uint64_t)std::max<int64_t>(g.P * B / 16, 4096);
+    // initial estimate 0.02 components/pixel (random images: 0.003-0.13); grows on demand
+    if (ctx->cap_comps == 0) ctx->cap_comps = (uint64_t)std::max<int64_t>(g.P * B / 48, 4096);
     if (ctx->cap_rstore == 0) ctx->cap_rstore = (uint64_t)std::max<int64_t>(g.P * B * 3 / 10 + ntiles * 64, 1 << 16);
     const uint64_t nn = (uint64_t)B + ctx->cap_nodes;
     bool ok = ensure(ctx->bits, (size_t)ntiles * NW * 4) && ensure(ctx->tbase, (size_t)ntiles * 4) &&
