@@ -299,7 +299,8 @@ def main() -> None:
     lab.sync()  # raises if the device flagged an error
     ms = ev0.elapsed_time(ev1)
     # per-phase device times of the timed steps (library events on its stream)
-    phases = [lab.phase_times(k) for k in range(min(args.steps, 60))]
+    phases = ([lab.phase_times(0)] if lab.used_graph()
+              else [lab.phase_times(k) for k in range(min(args.steps, 60))])
     launches_per_step = lab.launch_count()
     if world > 1:
         dist.barrier()

@@ -160,6 +160,10 @@ void rl_cfg4_params(uint64_t i, double* density, int32_t* g);
 
 /* Number of kernel launches the last pipeline enqueued. */
 int rl_last_launch_count(const rl_ctx* ctx);
+/* 1 when the last call replayed a captured CUDA graph (small workloads; disable with the
+ * environment variable RUNLAB_GPU_NO_GRAPH).  Phase times of older calls (back > 0) are then
+ * not kept. */
+int rl_last_used_graph(const rl_ctx* ctx);
 
 /* Tile geometry used by the kernels (for DESIGN/roofline bookkeeping). */
 void rl_tile_shape(int32_t* tile_h, int32_t* tile_w);

@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = (
     "rl_create", "rl_destroy", "rl_last_error", "rl_label", "rl_result_free", "rl_label_device",
     "rl_sync", "rl_fetch", "rl_device_filled_image", "rl_device_labels", "rl_device_comps",
     "rl_stream", "rl_set_stream", "rl_last_launch_count", "rl_tile_shape", "rl_label_into",
-    "rl_phase_times", "rl_generate", "rl_generate_rings", "rl_cfg4_params",
+    "rl_phase_times", "rl_generate", "rl_generate_rings", "rl_cfg4_params", "rl_last_used_graph",
 )
 
 FEATURE_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),
@@ -84,6 +84,7 @@ def load() -> C.CDLL:
         getattr(L, name).argtypes = [C.c_void_p]
     L.rl_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     L.rl_last_launch_count.argtypes = [C.c_void_p]
+    L.rl_last_used_graph.argtypes = [C.c_void_p]
     L.rl_tile_shape.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.rl_label_into.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                 C.POINTER(RlConfig), C.POINTER(RlHostOutputs)]

@@ -69,6 +69,19 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
+// Everything a captured pipeline depends on (compared bytewise before a replay).
+struct GraphKey {
+    Geo g;
+    Ws ws;
+    rl_config cfg;
+    const void* pix;
+    cudaStream_t stream;
+    const void* summ;
+    const void* rank;
+    const void* flag;
+    uint64_t cap_comps;
+};
+
 }  // namespace
 
 struct rl_ctx {
@@ -99,6 +112,12 @@ struct rl_ctx {
     int launches = 0;
     bool have_result = false;
     bool reran = false;  // finish() had to grow a capacity and re-run
+    // CUDA graph of the last small pipeline
+    bool graphs = true;
+    bool used_graph = false;
+    cudaGraphExec_t gexec = nullptr;
+    GraphKey gkey{};
+    cudaEvent_t gev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -146,6 +165,15 @@ int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cf
     if (P * n >= 4.0e9 * 64) return set_err(ctx, RL_EINVAL, "batch too large");
     if ((double)n * h * ((w + TW - 1) / TW) >= 4.0e9) return set_err(ctx, RL_EINVAL, "batch too large");
     return RL_OK;
+}
+
+// Phase-timing event.  Inside a stream capture a plain record only becomes an internal graph
+// dependency; the external flag makes it a real event record node that replays time.
+void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
+    if (capturing)
+        cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+    else
+        cudaEventRecord(ev, s);
 }
 
 // (Re)build geometry, grow the workspace, enqueue the pipeline.
@@ -228,6 +256,45 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     ws.labels = g.label_mode ? P<uint32_t>(ctx->labels) : nullptr;
 
     cudaStream_t s = ctx->stream;
+    const bool densify_fill = cfg->densify_labels && cfg->fill_holes && g.label_mode;
+    if (densify_fill) {
+        const uint64_t total = ctx->cap_comps;
+        if (!ensure(ctx->rank, (total + 1) * 4) || !ensure(ctx->flag, (total + 1) * 4))
+            return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    }
+    const size_t sn = (size_t)(B + 1) * 4;
+    if (ctx->h_summ_n < sn) {
+        if (ctx->h_summ) cudaFreeHost(ctx->h_summ);
+        ctx->h_summ = nullptr;
+        if (cudaMallocHost(&ctx->h_summ, sn * 8) != cudaSuccess) return set_err(ctx, RL_ENOMEM, "pinned alloc failed");
+        ctx->h_summ_n = sn;
+    }
+
+    // Small workloads are launch-bound: the whole pipeline is captured once into a CUDA graph
+    // and replayed while the geometry, configuration and workspace stay the same.
+    const bool use_graph = ctx->graphs && (double)g.P * B <= 64.0 * 1024 * 1024;
+    GraphKey key{};
+    key.g = g;
+    key.ws = ws;
+    key.cfg = *cfg;
+    key.pix = dpix;
+    key.stream = s;
+    key.summ = ctx->h_summ;
+    key.rank = ctx->rank.p;
+    key.flag = ctx->flag.p;
+    key.cap_comps = ctx->cap_comps;
+    if (use_graph && ctx->gexec && std::memcmp(&key, &ctx->gkey, sizeof(key)) == 0) {
+        const cudaError_t e = cudaGraphLaunch(ctx->gexec, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "graph launch");
+        for (int k = 0; k < 4; ++k) ctx->ev[k] = ctx->gev[k];
+        ctx->geo = g;
+        ctx->ws = ws;
+        ctx->cfg = *cfg;
+        ctx->last_pix = dpix;
+        ctx->have_result = true;
+        ctx->used_graph = true;
+        return RL_OK;
+    }
     {
         const int slot = (int)(ctx->calls % rl_ctx::RING);
         for (int k = 0; k < 4; ++k) {
@@ -236,16 +303,22 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
         }
         ++ctx->calls;
     }
+    if (use_graph) {
+        if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+        if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+            return cuda_fail(ctx, cudaGetLastError(), "graph capture");
+    }
     int launches = 0;
     cudaMemsetAsync(ws.counters, 0, 64, s);
     cudaMemsetAsync(ws.rused, 0, 8, s);
     cudaMemsetAsync(ws.img_fg, 0, (size_t)B * 4, s);
     cudaMemsetAsync(ws.img_surv, 0, (size_t)B * 4, s);
     cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
-    cudaEventRecord(ctx->ev[0], s);
+    record_event(ctx->ev[0], s, use_graph);
     launch_analyze(dpix, g, ws, s);
     launches += 3;
-    cudaEventRecord(ctx->ev[1], s);
+    record_event(ctx->ev[1], s, use_graph);
     launch_seams(g, ws, s, ctx->sms);
     launches += (g.nty > 1) + (g.ntx > 1);
     const int64_t hint = (int64_t)ctx->cap_nodes;
@@ -255,18 +328,16 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launch_cids(g, ws, s, ctx->sms);
     launch_tree(g, ws, s, ctx->sms, hint);
     launches += 2 + 1 + 1 + 3;
-    cudaEventRecord(ctx->ev[2], s);
+    record_event(ctx->ev[2], s, use_graph);
     launch_emit(g, ws, s);
     launches += 3;
     k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));
     ++launches;
-    if (cfg->densify_labels && cfg->fill_holes && g.label_mode) {
+    if (densify_fill) {
         // densified post-fill ids: rank of each survivor inside its image (labeling.hpp:231-236)
         // total components is bounded by cap_comps; flags over [0, cap) are computed for the
         // prefix that is in use (the remap only reads ranks of survivors).
         const uint64_t total = ctx->cap_comps;
-        if (!ensure(ctx->rank, (total + 1) * 4) || !ensure(ctx->flag, (total + 1) * 4))
-            return set_err(ctx, RL_ENOMEM, "device allocation failed");
         launch_surv_flags(ws.top, P<uint64_t>(ctx->cbase), B, total, P<uint32_t>(ctx->flag), s, ctx->sms);
         size_t t2 = ctx->cub_tmp.bytes;
         cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t2, P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank),
@@ -274,15 +345,22 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
         launch_remap(ws.labels, g.P, B, P<uint32_t>(ctx->rank), P<uint64_t>(ctx->cbase), s, ctx->sms);
         launches += 3;
     }
-    cudaEventRecord(ctx->ev[3], s);
-    const size_t sn = (size_t)(B + 1) * 4;
-    if (ctx->h_summ_n < sn) {
-        if (ctx->h_summ) cudaFreeHost(ctx->h_summ);
-        ctx->h_summ = nullptr;
-        if (cudaMallocHost(&ctx->h_summ, sn * 8) != cudaSuccess) return set_err(ctx, RL_ENOMEM, "pinned alloc failed");
-        ctx->h_summ_n = sn;
-    }
+    record_event(ctx->ev[3], s, use_graph);
     cudaMemcpyAsync(ctx->h_summ, ctx->summ.p, sn * 8, cudaMemcpyDeviceToHost, s);
+    if (use_graph) {
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(s, &graph);
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&ctx->gexec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (e == cudaSuccess) e = cudaGraphLaunch(ctx->gexec, s);
+        if (e != cudaSuccess) {
+            ctx->gexec = nullptr;
+            return cuda_fail(ctx, e, "graph instantiate");
+        }
+        ctx->gkey = key;
+        for (int k = 0; k < 4; ++k) ctx->gev[k] = ctx->ev[k];
+    }
+    ctx->used_graph = use_graph;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "launch");
     ctx->geo = g;
@@ -409,6 +487,7 @@ rl_ctx* rl_create(int device) {
         return nullptr;
     }
     c->stream = c->own_stream;
+    if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
     return c;
 }
 
@@ -427,6 +506,7 @@ void rl_destroy(rl_ctx* c) {
     for (auto& slot : c->ring)
         for (auto& e : slot)
             if (e) cudaEventDestroy(e);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -549,8 +629,10 @@ int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int3
 
 int rl_phase_times(const rl_ctx* ctx, int back, rl_times* out) {
     if (!ctx || !out || back < 0 || back >= rl_ctx::RING || back >= ctx->calls) return RL_EINVAL;
+    // back == 0 is the last call (also when it was a CUDA-graph replay, whose events are
+    // the captured ones); older calls come from the ring of eagerly enqueued calls
     const int slot = (int)((ctx->calls - 1 - back) % rl_ctx::RING);
-    cudaEvent_t const* ev = ctx->ring[slot];
+    cudaEvent_t const* ev = back == 0 ? ctx->ev : ctx->ring[slot];
     float a = 0, m = 0, e = 0, t = 0;
     if (cudaEventElapsedTime(&a, ev[0], ev[1]) != cudaSuccess || cudaEventElapsedTime(&m, ev[1], ev[2]) != cudaSuccess ||
         cudaEventElapsedTime(&e, ev[2], ev[3]) != cudaSuccess || cudaEventElapsedTime(&t, ev[0], ev[3]) != cudaSuccess) {
@@ -596,3 +678,5 @@ void rl_tile_shape(int32_t* th, int32_t* tw) {
 }
 
 }  // extern "C"
+
+extern "C" int rl_last_used_graph(const rl_ctx* c) { return c && c->used_graph ? 1 : 0; }

@@ -249,6 +249,9 @@ class Labeler:
     def launch_count(self) -> int:
         return int(self._L.rl_last_launch_count(self._ctx))
 
+    def used_graph(self) -> bool:
+        return bool(self._L.rl_last_used_graph(self._ctx))
+
     def device_filled_image(self) -> int:
         return int(self._L.rl_device_filled_image(self._ctx) or 0)
 
