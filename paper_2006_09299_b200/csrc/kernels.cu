@@ -739,6 +739,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     __syncthreads();
 
     // runs again from the packed bits (cheap); the component map comes from the analyze pass
+    RL_PHASE(tg.t, 16);
     WordBits wb;
     if (!tile_runs<false>(S, wb)) return false;
     {
@@ -752,6 +753,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     }
     __syncthreads();
 
+    RL_PHASE(tg.t, 17);
     const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
     const uint64_t cb = E.cb;
     const uint32_t nbase = (uint32_t)g.B + ws.tbase[tg.t];
@@ -780,23 +782,13 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         }
     }
     __syncthreads();
+    RL_PHASE(tg.t, 18);
 
-    // ---- exterior pixels (for the hole-filled image), one lane per run
-    for (int i = tid; i < nruns; i += NT) {
-        const uint16_t lb = S.lcb[lc_of_run(S, i)];
-        if ((lb & 0x8000u) || !(E.bflag[lb] & 2u)) continue;
-        const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
-        for (int wd = c0 >> 5; wd <= ((c1 - 1) >> 5); ++wd) {
-            const int lo = max(c0 - 32 * wd, 0), hi = min(c1 - 32 * wd, 32);
-            const uint32_t m = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
-            atomicOr(&E.ext[rr * WPR + wd], m);
-        }
-    }
-
-    // ---- interior components, in chunks of C::FCH tile components
+    // ---- interior components, in chunks of C::FCH tile components.  The first chunk's run
+    // pass also marks exterior pixels (for the hole-filled image).
     const int flip = g.flip;
     int nsurv = 0;
-    for (int l0 = 0; l0 < nlc; l0 += C::FCH) {
+    for (int l0 = 0; l0 < max(nlc, 1); l0 += C::FCH) {
         const int l1 = min(l0 + C::FCH, nlc);
         for (int i = tid; i < C::FCH; i += NT) {
             E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
@@ -805,9 +797,22 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             E.fcmax[i] = -1;
         }
         __syncthreads();
-        for (int i = tid; i < nruns; i += NT) {
+        RL_PHASE(tg.t, 19);
+        // a component's runs never precede its first (root) run
+        const int ifirst = (l0 == 0 || l0 >= nlc) ? 0 : S.lcrun[l0];
+        for (int i = ifirst + tid; i < nruns; i += NT) {
             const uint32_t lc = lc_of_run(S, i);
-            if ((int)lc < l0 || (int)lc >= l1 || lc_is_border(S, lc)) continue;
+            const uint16_t lb = S.lcb[lc];
+            if (l0 == 0 && !(lb & 0x8000u) && (E.bflag[lb] & 2u)) {
+                const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
+                for (int wd = c0 >> 5; wd <= ((c1 - 1) >> 5); ++wd) {
+                    const int lo = max(c0 - 32 * wd, 0), hi = min(c1 - 32 * wd, 32);
+                    const uint32_t m = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+                    atomicOr(&E.ext[rr * WPR + wd], m);
+                }
+                continue;
+            }
+            if ((int)lc < l0 || (int)lc >= l1 || !(lb & 0x8000u)) continue;
             const int k = (int)lc - l0;
             const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
             const uint32_t n = (uint32_t)(c1 - c0);
@@ -819,6 +824,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             atomicMax(&E.fcmax[k], c1 - 1);
         }
         __syncthreads();
+        RL_PHASE(tg.t, 20);
         // pre-fill records, post-fill roots, survivor init
         for (int lc = l0 + tid; lc < l1; lc += NT) {
             if (lc_is_border(S, lc)) continue;
@@ -848,6 +854,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             }
         }
         __syncthreads();
+        RL_PHASE(tg.t, 21);
         // fold non-survivors into their post-fill root
         for (int lc = l0 + tid; lc < l1; lc += NT) {
             if (lc_is_border(S, lc)) continue;
@@ -881,6 +888,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             }
         }
         __syncthreads();
+        RL_PHASE(tg.t, 22);
     }
     // flush border-keyed folds (the survivors were initialised by k_tops)
     for (int i = tid; i < FOLD_SLOTS; i += NT) {
@@ -898,6 +906,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     }
     nsurv = block_reduce_sum(nsurv, S.wsum);  // also orders the ext-mask atomics before use
     if (tid == 0 && nsurv) atomicAdd(&ws.img_surv[tg.b], (uint32_t)nsurv);
+    RL_PHASE(tg.t, 23);
 
     // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
     if (vm) {
@@ -941,6 +950,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             for (int j = c0; j < c1; ++j) ldst[j] = v;
         }
     }
+    RL_PHASE(tg.t, 24);
     return true;
 }
 

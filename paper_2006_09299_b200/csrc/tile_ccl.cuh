@@ -28,14 +28,15 @@
 namespace rlg {
 
 // Optional per-phase clock64() stamps of each tile CTA (profiling builds only:
-// -DRL_PHASE_PROF; tools/phase_prof.py).  Slot 16*tile + k holds the stamp of phase k.
+// -DRL_PHASE_PROF; tools/phase_prof.py).  Slot 32*tile + k holds the stamp of phase k
+// (analyze pass 0..12, emit pass 16..24).
 #ifdef RL_PHASE_PROF
 __device__ unsigned long long* g_phase_buf = nullptr;
 __device__ int g_phase_n = 0;
 #define RL_PHASE(tile, k)                                                         \
     do {                                                                          \
         if (threadIdx.x == 0 && g_phase_buf && (tile) < g_phase_n)               \
-            g_phase_buf[16ull * (unsigned)(tile) + (k)] = clock64();              \
+            g_phase_buf[32ull * (unsigned)(tile) + (k)] = clock64();              \
     } while (0)
 #else
 #define RL_PHASE(tile, k) \
@@ -58,7 +59,7 @@ struct Cap {
     static constexpr int FCH = FCH_;  // interior-feature accumulator chunk (emit pass)
 };
 using CapS = Cap<MAXRUNS * 3 / 16, NBMAX / 2, 192, 512>;
-using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 320>;
+using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 640>;
 using CapF = Cap<MAXRUNS, NBMAX, 1024, 320>;
 
 template <class C>

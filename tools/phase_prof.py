@@ -39,7 +39,7 @@ def main():
         d, g = cells[i % len(cells)]
         generate_device(imgs[i].data_ptr(), S, S, d, g, 1 + i)
     ntiles = B * (S // 32) * (S // 256)
-    buf = torch.zeros(ntiles * 16, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(ntiles * 32, dtype=torch.int64, device="cuda")
     lab = Labeler(0)
     cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
     lab.label_device(imgs.data_ptr(), S, S, B, cfg)
@@ -48,13 +48,20 @@ def main():
     buf.zero_()
     lab.label_device(imgs.data_ptr(), S, S, B, cfg)
     lab.sync()
-    st = buf.view(ntiles, 16).cpu().numpy().astype(np.float64)
+    st = buf.view(ntiles, 32).cpu().numpy().astype(np.float64)
     ok = (st[:, :13] > 0).all(axis=1)
     d = np.diff(st[ok, :13], axis=1)
-    print(f"tiles with complete stamps: {ok.sum()} / {ntiles}; mean CTA latency "
+    print(f"analyze: tiles with complete stamps: {ok.sum()} / {ntiles}; mean CTA latency "
           f"{(st[ok, 12] - st[ok, 0]).mean():.0f} cycles")
     for k in range(12):
         print(f"  {NAMES[k + 1]:22s} {d[:, k].mean():9.0f} cycles  (p90 {np.percentile(d[:, k], 90):9.0f})")
+    ok = (st[:, 16:25] > 0).all(axis=1)
+    d = np.diff(st[ok, 16:25], axis=1)
+    print(f"emit: tiles with complete stamps: {ok.sum()} / {ntiles}; mean CTA latency "
+          f"{(st[ok, 24] - st[ok, 16]).mean():.0f} cycles (chunk phases: last chunk)")
+    for k, name in enumerate(["runs+map", "border-info+repx", "ext-mask", "features", "records",
+                              "fold", "flush+reduce", "filled-image"]):
+        print(f"  {name:22s} {d[:, k].mean():9.0f} cycles  (p90 {np.percentile(d[:, k], 90):9.0f})")
 
 
 if __name__ == "__main__":
