@@ -958,14 +958,14 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
 __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ws.counters[1] || !comps_fit(g, ws)) return;
-    auto& E = *reinterpret_cast<EmitSmem<CapS>*>(smem_raw);
+    auto& E = *reinterpret_cast<EmitSmem<CapSE>*>(smem_raw);
     emit_tile(E, g, ws, tile_geom_grid(g));
 }
 
 __global__ void __launch_bounds__(NT) k_emit_m(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ws.counters[1] || !comps_fit(g, ws)) return;
-    auto& E = *reinterpret_cast<EmitSmem<CapM>*>(smem_raw);
+    auto& E = *reinterpret_cast<EmitSmem<CapME>*>(smem_raw);
     const uint32_t n = ws.counters[2];
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
         emit_tile(E, g, ws, tile_geom(g, (int32_t)ws.ovf[k]));
@@ -976,7 +976,7 @@ __global__ void __launch_bounds__(NT) k_emit_m(Geo g, Ws ws) {
 __global__ void __launch_bounds__(NT) k_emit_full(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ws.counters[1] || !comps_fit(g, ws)) return;
-    auto& E = *reinterpret_cast<EmitSmem<CapF>*>(smem_raw);
+    auto& E = *reinterpret_cast<EmitSmem<CapFE>*>(smem_raw);
     const uint32_t n = ws.counters[4];
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
         emit_tile(E, g, ws, tile_geom(g, (int32_t)ws.ovf2[k]));
@@ -1024,7 +1024,7 @@ __global__ void k_surv_flags_img(const uint32_t* top, const uint64_t* cbase, int
 namespace rlg {
 
 size_t analyze_smem() { return sizeof(AnalyzeSmem<CapS>); }
-size_t emit_smem() { return sizeof(EmitSmem<CapS>); }
+size_t emit_smem() { return sizeof(EmitSmem<CapSE>); }
 
 template <class K>
 static cudaError_t set_smem(K kernel, size_t bytes) {
@@ -1035,9 +1035,9 @@ cudaError_t configure_kernels() {
     cudaError_t e = set_smem(k_analyze, sizeof(AnalyzeSmem<CapS>));
     if (e == cudaSuccess) e = set_smem(k_analyze_m, sizeof(AnalyzeSmem<CapM>));
     if (e == cudaSuccess) e = set_smem(k_analyze_full, sizeof(AnalyzeSmem<CapF>));
-    if (e == cudaSuccess) e = set_smem(k_emit, sizeof(EmitSmem<CapS>));
-    if (e == cudaSuccess) e = set_smem(k_emit_m, sizeof(EmitSmem<CapM>));
-    if (e == cudaSuccess) e = set_smem(k_emit_full, sizeof(EmitSmem<CapF>));
+    if (e == cudaSuccess) e = set_smem(k_emit, sizeof(EmitSmem<CapSE>));
+    if (e == cudaSuccess) e = set_smem(k_emit_m, sizeof(EmitSmem<CapME>));
+    if (e == cudaSuccess) e = set_smem(k_emit_full, sizeof(EmitSmem<CapFE>));
     return e;
 }
 
@@ -1080,9 +1080,9 @@ void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
     k_fold<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
 }
 void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s) {
-    k_emit<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(EmitSmem<CapS>), s>>>(g, ws);
-    k_emit_m<<<148 * 3, NT, sizeof(EmitSmem<CapM>), s>>>(g, ws);
-    k_emit_full<<<148, NT, sizeof(EmitSmem<CapF>), s>>>(g, ws);
+    k_emit<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(EmitSmem<CapSE>), s>>>(g, ws);
+    k_emit_m<<<148 * 3, NT, sizeof(EmitSmem<CapME>), s>>>(g, ws);
+    k_emit_full<<<148, NT, sizeof(EmitSmem<CapFE>), s>>>(g, ws);
 }
 void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
                        cudaStream_t s, int sms) {

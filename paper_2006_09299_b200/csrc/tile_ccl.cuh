@@ -51,16 +51,22 @@ __device__ int g_phase_n = 0;
 //   M: <= MAXRUNS * 5/8 runs (0.62 runs/pixel, covers any random image), all border components;
 //   F: one run per pixel (checkerboards and other adversarial inputs).
 // EVC = union-event queue per warp; longer queues are processed in rounds.
-template <int MR_, int NBC_, int EVC_, int FCH_>
+template <int MR_, int NBC_, int EVC_, int FCH_, class PT_>
 struct Cap {
     static constexpr int MR = MR_;
     static constexpr int NBC = NBC_;
     static constexpr int EVC = EVC_;
     static constexpr int FCH = FCH_;  // interior-feature accumulator chunk (emit pass)
+    using PT = PT_;                   // run-parent type: 32-bit for native atomicMin unions
 };
-using CapS = Cap<MAXRUNS * 3 / 16, NBMAX / 2, 192, 512>;
-using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 640>;
-using CapF = Cap<MAXRUNS, NBMAX, 1024, 320>;
+// analyze pass (union-find: 32-bit parents)
+using CapS = Cap<MAXRUNS * 3 / 16, NBMAX / 2, 192, 512, uint32_t>;
+using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 384, uint32_t>;
+using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t>;
+// emit pass: same classes, no unions (16-bit component map, larger feature chunks)
+using CapSE = Cap<CapS::MR, CapS::NBC, 192, 512, uint16_t>;
+using CapME = Cap<CapM::MR, CapM::NBC, 1024, 640, uint16_t>;
+using CapFE = Cap<CapF::MR, CapF::NBC, 1024, 320, uint16_t>;
 
 template <class C>
 struct CclSmem {
@@ -72,7 +78,7 @@ struct CclSmem {
     uint16_t rowlc[TH + 1];    // first tile component of each row
     uint16_t rowbx[TH + 1];    // border components before each row start
     uint16_t runpos[MR];       // (row << 8) | col of each run start, raster order
-    uint16_t par[MR];          // union-find parent; afterwards TAG | component of each run
+    typename C::PT par[MR];    // union-find parent; then TAG | component of each run
     union {
         struct {
             uint16_t lcrun[MR];     // root (first) run of each tile component
@@ -96,30 +102,19 @@ __device__ __forceinline__ int run_left(const SM& S, int word, int bit) {
     return bit > 0 ? run_at(S, word, bit - 1) : (int)S.rbase[word] - 1;
 }
 
-__device__ __forceinline__ uint32_t sfind(volatile uint16_t* par, uint32_t a) {
+__device__ __forceinline__ uint32_t sfind(volatile uint32_t* par, uint32_t a) {
     for (;;) {
         const uint32_t p = par[a];
         if (p == a) return a;
         const uint32_t gp = par[p];
         if (gp == p) return p;
-        par[a] = (uint16_t)gp;
+        par[a] = gp;
         a = gp;
     }
 }
 
-// 16-bit atomic min (CAS loop; unions that actually link are rare), returns the old value
-__device__ __forceinline__ uint32_t atomic_min_u16(uint16_t* addr, uint32_t v) {
-    unsigned short old = *reinterpret_cast<volatile unsigned short*>(addr);
-    while (old > v) {
-        const unsigned short prev = atomicCAS(reinterpret_cast<unsigned short*>(addr), old, (unsigned short)v);
-        if (prev == old) break;
-        old = prev;
-    }
-    return old;
-}
-
-__device__ __forceinline__ void sunion(uint16_t* par, uint32_t a, uint32_t b) {
-    volatile uint16_t* vp = par;
+__device__ __forceinline__ void sunion(uint32_t* par, uint32_t a, uint32_t b) {
+    volatile uint32_t* vp = par;
     for (;;) {
         a = sfind(vp, a);
         b = sfind(vp, b);
@@ -129,7 +124,7 @@ __device__ __forceinline__ void sunion(uint16_t* par, uint32_t a, uint32_t b) {
             a = b;
             b = t;
         }
-        const uint32_t old = atomic_min_u16(par + a, b);
+        const uint32_t old = atomicMin(par + a, b);
         if (old == a) return;
         a = old;
     }
