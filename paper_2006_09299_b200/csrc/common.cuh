@@ -144,8 +144,10 @@ __device__ __forceinline__ uint32_t valid_mask(const TileGeom& tg, int r, int w)
     return (1u << vc) - 1u;
 }
 
-// Block-wide exclusive scan over NT threads; `wsum` is __shared__ int[NWARPS + 1].
+// Block-wide exclusive scan over BT threads; `wsum` is __shared__ int[BT / 32 + 1].
+template <int BT = NT>
 __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
+    constexpr int NWP = BT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int incl = v;
 #pragma unroll
@@ -156,26 +158,27 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        const int s = lane < NWARPS ? wsum[lane] : 0;
+        const int s = lane < NWP ? wsum[lane] : 0;
         int si = s;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int n = __shfl_up_sync(0xFFFFFFFFu, si, o);
             if (lane >= o) si += n;
         }
-        if (lane < NWARPS) wsum[lane] = si - s;
-        if (lane == NWARPS - 1) wsum[NWARPS] = si;
+        if (lane < NWP) wsum[lane] = si - s;
+        if (lane == NWP - 1) wsum[NWP] = si;
     }
     __syncthreads();
-    total = wsum[NWARPS];
+    total = wsum[NWP];
     const int r = wsum[warp] + incl - v;
     __syncthreads();
     return r;
 }
 
+template <int BT = NT>
 __device__ __forceinline__ int block_reduce_sum(int v, int* wsum) {
     int t;
-    block_excl_scan(v, wsum, t);
+    block_excl_scan<BT>(v, wsum, t);
     return t;
 }
 

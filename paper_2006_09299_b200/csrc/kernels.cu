@@ -44,10 +44,12 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     CclSmem<C>& S = A.c;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
+    constexpr int BT = C::BT;
+    const bool word = BT == NW || tid < NW;
     RL_PHASE(tg.t, 0);
 
     // ---- load 32 pixels (bytes) of this thread's word and pack them to bits
-    const uint32_t vm = valid_mask(tg, r, w);
+    const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;
     uint32_t bits = 0;
     if (vm) {
         const uint8_t* src = pix + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
@@ -61,10 +63,12 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         }
     }
     const uint32_t x = (bits ^ (g.flip ? 0xFFFFFFFFu : 0u)) & vm;
-    S.x[tid] = x;
-    S.vm[tid] = vm;
-    ws.bits[(int64_t)tg.t * NW + tid] = x;
-    for (int i = tid; i < C::NBC; i += NT) {
+    if (word) {
+        S.x[tid] = x;
+        S.vm[tid] = vm;
+        ws.bits[(int64_t)tg.t * NW + tid] = x;
+    }
+    for (int i = tid; i < C::NBC; i += BT) {
         A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
         A.brmax[i] = -1;
         A.bcmin[i] = 0x7FFFFFFF;
@@ -123,8 +127,8 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         const unsigned long long off = A.moff;
         if (off + (unsigned long long)nruns + 2ull * nlc <= ws.cap_rstore) {
             uint16_t* dst = ws.rstore + off;
-            for (int i = tid; i < nruns; i += NT) dst[i] = (uint16_t)lc_of_run(S, i);
-            for (int l = tid; l < nlc; l += NT) {
+            for (int i = tid; i < nruns; i += BT) dst[i] = (uint16_t)lc_of_run(S, i);
+            for (int l = tid; l < nlc; l += BT) {
                 dst[nruns + l] = S.lcrun[l];
                 dst[nruns + nlc + l] = S.lcb[l];
             }
@@ -140,11 +144,11 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     // its lanes reduce in registers (REDUX) and one lane does the atomics; the other lanes
     // accumulate directly.
     constexpr int U = 4;  // loads of U iterations are issued together (latency hiding)
-    for (int j0 = 0; j0 < nruns; j0 += U * NT) {
+    for (int j0 = 0; j0 < nruns; j0 += U * BT) {
       uint16_t lbv[U], rpv[U], nxv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-          const int i = j0 + u * NT + tid;
+          const int i = j0 + u * BT + tid;
           const bool ok = i < nruns;
           const uint32_t lc = ok ? lc_of_run(S, i) : 0u;
           rpv[u] = ok ? S.runpos[i] : 0;
@@ -199,7 +203,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     const uint32_t base = A.base;
     const bool node_ok = (uint64_t)base + nb <= ws.cap_nodes;
     const int flip = g.flip;
-    for (int i = tid; i < nb && node_ok; i += NT) {
+    for (int i = tid; i < nb && node_ok; i += BT) {
         const int lc = S.blc[i];
         const int fr = lc_row(S, lc), fc = lc_col(S, lc);
         const uint32_t fg = xbit(S, fr, fc) ^ (uint32_t)flip;
@@ -246,7 +250,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     }
 
     // ---- perimeter labels: (value << 15) | border index
-    for (int q = tid; q < PERIM; q += NT) {
+    for (int q = tid; q < PERIM; q += BT) {
         int pr, pc;
         if (q < TW) { pr = 0; pc = q; }
         else if (q < 2 * TW) { pr = tg.th - 1; pc = q - TW; }
@@ -268,12 +272,12 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         ws.cnt[((int64_t)tg.b * g.H + tg.y0 + tid) * g.ntx + tg.tx] = (uint32_t)(nl - nbr);
     }
     int nfg = 0;
-    for (int l = tid; l < nlc; l += NT) {
+    for (int l = tid; l < nlc; l += BT) {
         if (lc_is_border(S, l)) continue;
         nfg += (int)(xbit(S, lc_row(S, l), lc_col(S, l)) ^ (uint32_t)flip);
     }
     RL_PHASE(tg.t, 11);
-    nfg = block_reduce_sum(nfg, S.wsum);
+    nfg = block_reduce_sum<BT>(nfg, S.wsum);
     RL_PHASE(tg.t, 12);
     if (tid == 0 && nfg) atomicAdd(&ws.img_fg[tg.b], (uint32_t)nfg);
     return true;
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix,
 }
 
 // class M over list A; heavier tiles go to list B
-__global__ void __launch_bounds__(NT) k_analyze_m(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+__global__ void __launch_bounds__(CapM::BT) k_analyze_m(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& A = *reinterpret_cast<AnalyzeSmem<CapM>*>(smem_raw);
     const uint32_t n = ws.counters[2];
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(NT) k_analyze_m(const uint8_t* __restrict__ pi
 }
 
 // class F over list B (one run per pixel fits)
-__global__ void __launch_bounds__(NT) k_analyze_full(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+__global__ void __launch_bounds__(CapF::BT) k_analyze_full(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& A = *reinterpret_cast<AnalyzeSmem<CapF>*>(smem_raw);
     const uint32_t n = ws.counters[4];
@@ -706,14 +710,18 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     CclSmem<C>& S = E.c;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
+    constexpr int BT = C::BT;
+    const bool word = BT == NW || tid < NW;
     {
         const uint16_t* h = ws.thdr + (int64_t)tg.t * THDR;
         if ((int)h[0] > C::MR || (int)h[2] > C::NBC) return false;  // a larger class owns it
     }
-    const uint32_t vm = valid_mask(tg, r, w);
-    S.x[tid] = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
-    S.vm[tid] = vm;
-    E.ext[tid] = 0;
+    const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;
+    if (word) {
+        S.x[tid] = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
+        S.vm[tid] = vm;
+        E.ext[tid] = 0;
+    }
     const int64_t img0 = (int64_t)tg.b * g.H * g.ntx;
     const uint32_t offimg = ws.off[img0];
     if (tid < TH && tid < tg.th)
@@ -745,8 +753,8 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     {
         const int nr = wb.nruns, nl = S.nlc;
         const uint16_t* src = ws.rstore + ws.tmap[tg.t];
-        for (int i = tid; i < nr; i += NT) S.par[i] = src[i];
-        for (int l = tid; l < nl; l += NT) {
+        for (int i = tid; i < nr; i += BT) S.par[i] = src[i];
+        for (int l = tid; l < nl; l += BT) {
             S.lcrun[l] = src[nr + l];
             S.lcb[l] = src[nr + nl + l];
         }
@@ -757,7 +765,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
     const uint64_t cb = E.cb;
     const uint32_t nbase = (uint32_t)g.B + ws.tbase[tg.t];
-    for (int i = tid; i < nb; i += NT) {
+    for (int i = tid; i < nb; i += BT) {
         const uint32_t node = nbase + (uint32_t)i;
         const uint32_t root = ws.uf[node];
         const bool ext = root < (uint32_t)g.B;
@@ -790,7 +798,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     int nsurv = 0;
     for (int l0 = 0; l0 < max(nlc, 1); l0 += C::FCH) {
         const int l1 = min(l0 + C::FCH, nlc);
-        for (int i = tid; i < C::FCH; i += NT) {
+        for (int i = tid; i < C::FCH; i += BT) {
             E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
             E.frmax[i] = -1;
             E.fcmin[i] = 0x7FFFFFFF;
@@ -800,7 +808,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         RL_PHASE(tg.t, 19);
         // a component's runs never precede its first (root) run
         const int ifirst = (l0 == 0 || l0 >= nlc) ? 0 : S.lcrun[l0];
-        for (int i = ifirst + tid; i < nruns; i += NT) {
+        for (int i = ifirst + tid; i < nruns; i += BT) {
             const uint32_t lc = lc_of_run(S, i);
             const uint16_t lb = S.lcb[lc];
             if (l0 == 0 && !(lb & 0x8000u) && (E.bflag[lb] & 2u)) {
@@ -826,7 +834,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         __syncthreads();
         RL_PHASE(tg.t, 20);
         // pre-fill records, post-fill roots, survivor init
-        for (int lc = l0 + tid; lc < l1; lc += NT) {
+        for (int lc = l0 + tid; lc < l1; lc += BT) {
             if (lc_is_border(S, lc)) continue;
             const int k = lc - l0;
             const int fr = lc_row(S, lc), fc = lc_col(S, lc);
@@ -856,7 +864,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         __syncthreads();
         RL_PHASE(tg.t, 21);
         // fold non-survivors into their post-fill root
-        for (int lc = l0 + tid; lc < l1; lc += NT) {
+        for (int lc = l0 + tid; lc < l1; lc += BT) {
             if (lc_is_border(S, lc)) continue;
             const int k = lc - l0;
             int end;
@@ -891,7 +899,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         RL_PHASE(tg.t, 22);
     }
     // flush border-keyed folds (the survivors were initialised by k_tops)
-    for (int i = tid; i < FOLD_SLOTS; i += NT) {
+    for (int i = tid; i < FOLD_SLOTS; i += BT) {
         if (E.pkey[i] == 0xFFFF || !E.ps[i]) continue;
         Acc f;
         const int64_t s = E.ps[i];
@@ -904,7 +912,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         f.col_max = tg.x0 + E.pcmax[i];
         acc_atomic_fold(ws.filled + cb + E.banc[E.pkey[i]], f);
     }
-    nsurv = block_reduce_sum(nsurv, S.wsum);  // also orders the ext-mask atomics before use
+    nsurv = block_reduce_sum<BT>(nsurv, S.wsum);  // also orders the ext-mask atomics before use
     if (tid == 0 && nsurv) atomicAdd(&ws.img_surv[tg.b], (uint32_t)nsurv);
     RL_PHASE(tg.t, 23);
 
@@ -932,7 +940,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     }
     // ---- optional label image (Alg. 4 relabel, canonical ids), one lane per run
     if (g.label_mode) {
-        for (int i = tid; i < nruns; i += NT) {
+        for (int i = tid; i < nruns; i += BT) {
             const uint32_t lc = lc_of_run(S, i);
             uint32_t v = comp_cid(E, lc);
             if (g.label_mode == 2) {
@@ -962,7 +970,7 @@ __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
     emit_tile(E, g, ws, tile_geom_grid(g));
 }
 
-__global__ void __launch_bounds__(NT) k_emit_m(Geo g, Ws ws) {
+__global__ void __launch_bounds__(CapME::BT) k_emit_m(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ws.counters[1] || !comps_fit(g, ws)) return;
     auto& E = *reinterpret_cast<EmitSmem<CapME>*>(smem_raw);
@@ -973,7 +981,7 @@ __global__ void __launch_bounds__(NT) k_emit_m(Geo g, Ws ws) {
     }
 }
 
-__global__ void __launch_bounds__(NT) k_emit_full(Geo g, Ws ws) {
+__global__ void __launch_bounds__(CapFE::BT) k_emit_full(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ws.counters[1] || !comps_fit(g, ws)) return;
     auto& E = *reinterpret_cast<EmitSmem<CapFE>*>(smem_raw);
@@ -1051,8 +1059,8 @@ static int grid_for(int64_t n, int block, int maxgrid) {
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
     k_analyze<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
     // deferred heavier tiles: the grids loop over device-side lists (no host sync)
-    k_analyze_m<<<148 * 3, NT, sizeof(AnalyzeSmem<CapM>), s>>>(pix, g, ws);
-    k_analyze_full<<<148, NT, sizeof(AnalyzeSmem<CapF>), s>>>(pix, g, ws);
+    k_analyze_m<<<148 * 3, CapM::BT, sizeof(AnalyzeSmem<CapM>), s>>>(pix, g, ws);
+    k_analyze_full<<<148 * 2, CapF::BT, sizeof(AnalyzeSmem<CapF>), s>>>(pix, g, ws);
 }
 void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
     if (g.nty > 1) {
@@ -1081,8 +1089,8 @@ void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
 }
 void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s) {
     k_emit<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(EmitSmem<CapSE>), s>>>(g, ws);
-    k_emit_m<<<148 * 3, NT, sizeof(EmitSmem<CapME>), s>>>(g, ws);
-    k_emit_full<<<148, NT, sizeof(EmitSmem<CapFE>), s>>>(g, ws);
+    k_emit_m<<<148 * 3, CapME::BT, sizeof(EmitSmem<CapME>), s>>>(g, ws);
+    k_emit_full<<<148 * 2, CapFE::BT, sizeof(EmitSmem<CapFE>), s>>>(g, ws);
 }
 void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
                        cudaStream_t s, int sms) {

@@ -51,26 +51,31 @@ __device__ int g_phase_n = 0;
 //   M: <= MAXRUNS * 5/8 runs (0.62 runs/pixel, covers any random image), all border components;
 //   F: one run per pixel (checkerboards and other adversarial inputs).
 // EVC = union-event queue per warp; longer queues are processed in rounds.
-template <int MR_, int NBC_, int EVC_, int FCH_, class PT_>
+// BT = threads per CTA: one per word (256) for the sparse class; the dense classes add a second
+// thread per word so that their per-run and per-component loops run twice as wide.
+template <int MR_, int NBC_, int EVC_, int FCH_, class PT_, int BT_>
 struct Cap {
     static constexpr int MR = MR_;
     static constexpr int NBC = NBC_;
     static constexpr int EVC = EVC_;
     static constexpr int FCH = FCH_;  // interior-feature accumulator chunk (emit pass)
     using PT = PT_;                   // run-parent type: 32-bit for native atomicMin unions
+    static constexpr int BT = BT_;
+    static_assert(BT == NW || (BT == 2 * NW && EVC >= 32 * 32), "wide classes never need event rounds");
 };
 // analyze pass (union-find: 32-bit parents)
-using CapS = Cap<MAXRUNS * 3 / 16, NBMAX / 2, 192, 512, uint32_t>;
-using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 384, uint32_t>;
-using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t>;
+using CapS = Cap<MAXRUNS * 3 / 16, NBMAX / 2, 192, 512, uint32_t, NW>;
+using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 384, uint32_t, 2 * NW>;
+using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 // emit pass: same classes, no unions (16-bit component map, larger feature chunks)
-using CapSE = Cap<CapS::MR, CapS::NBC, 192, 512, uint16_t>;
-using CapME = Cap<CapM::MR, CapM::NBC, 1024, 640, uint16_t>;
-using CapFE = Cap<CapF::MR, CapF::NBC, 1024, 320, uint16_t>;
+using CapSE = Cap<CapS::MR, CapS::NBC, 192, 512, uint16_t, NW>;
+using CapME = Cap<CapM::MR, CapM::NBC, 1024, 640, uint16_t, 2 * NW>;
+using CapFE = Cap<CapF::MR, CapF::NBC, 1024, 320, uint16_t, 2 * NW>;
 
 template <class C>
 struct CclSmem {
     static constexpr int MR = C::MR;
+    static constexpr int BT = C::BT;
     uint32_t x[NW];            // 8-connected-value bits (pixel value XOR flip), 0 where invalid
     uint32_t vm[NW];           // valid-pixel masks
     uint32_t st[NW];           // run-start masks
@@ -87,7 +92,8 @@ struct CclSmem {
         uint16_t evq[NWARPS][C::EVC];  // union-event queues (dead before lcrun/lcb are written)
     };
     uint16_t blc[C::NBC];      // border index -> tile component
-    int wsum[NWARPS + 1];
+    int wsum[C::BT / 32 + 1];
+    int qtot[NWARPS];          // union events queued by each word warp
     int nruns, nlc, nb;
 };
 
@@ -189,27 +195,33 @@ __device__ __forceinline__ bool tile_runs(CclSmem<C>& S, WordBits& wb) {
     constexpr int MR = C::MR;
     const int tid = threadIdx.x;
     const int r = tid / WPR, w = tid % WPR;
-    wb.x = S.x[tid];
-    wb.vm = S.vm[tid];
-    wb.nx = ~wb.x;
-    // left neighbour word of the same row is lane - 1 (rows never straddle a warp)
-    const uint32_t xl = __shfl_up_sync(0xFFFFFFFFu, wb.x, 1);
-    const uint32_t vml = __shfl_up_sync(0xFFFFFFFFu, wb.vm, 1);
-    uint32_t c1 = 0, c0 = 0;
-    if (w > 0) {
-        const uint32_t lv = vml >> 31;
-        c1 = (xl >> 31) & lv;
-        c0 = ((~xl) >> 31) & lv;
+    // threads past NW (wide classes) own no word; their warps are uniformly idle here
+    const bool word = C::BT == NW || tid < NW;
+    wb = WordBits{};
+    if (word) {
+        wb.x = S.x[tid];
+        wb.vm = S.vm[tid];
+        wb.nx = ~wb.x;
+        // left neighbour word of the same row is lane - 1 (rows never straddle a warp)
+        const uint32_t xl = __shfl_up_sync(0xFFFFFFFFu, wb.x, 1);
+        const uint32_t vml = __shfl_up_sync(0xFFFFFFFFu, wb.vm, 1);
+        uint32_t c1 = 0, c0 = 0;
+        if (w > 0) {
+            const uint32_t lv = vml >> 31;
+            c1 = (xl >> 31) & lv;
+            c0 = ((~xl) >> 31) & lv;
+        }
+        wb.c1 = c1;
+        wb.s1 = wb.x & ~((wb.x << 1) | c1) & wb.vm;
+        wb.s0 = wb.nx & ~((wb.nx << 1) | c0) & wb.vm;
+        wb.st = wb.s1 | wb.s0;
+        S.st[tid] = wb.st;
     }
-    wb.c1 = c1;
-    wb.s1 = wb.x & ~((wb.x << 1) | c1) & wb.vm;
-    wb.s0 = wb.nx & ~((wb.nx << 1) | c0) & wb.vm;
-    wb.st = wb.s1 | wb.s0;
-    S.st[tid] = wb.st;
     int total;
-    const int rb = block_excl_scan(__popc(wb.st), S.wsum, total);  // contains __syncthreads
+    const int rb = block_excl_scan<C::BT>(__popc(wb.st), S.wsum, total);  // contains __syncthreads
     wb.nruns = total;
     if (total > MR) return false;
+    if (!word) return true;
     S.rbase[tid] = (uint16_t)rb;
     if (tid == 0) {
         S.rbase[NW] = (uint16_t)total;
@@ -238,8 +250,10 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     const uint32_t x = wb.x, nx = wb.nx, vm = wb.vm, c1 = wb.c1, s1 = wb.s1, s0 = wb.s0;
     // ---- union events with the row above (Alg. 2's overlap test, one event per pair),
     // compacted into the warp's queue: entry = (word << 7) | (type << 5) | bit
+    constexpr int BT = C::BT;
+    const bool word = BT == NW || tid < NW;
     uint32_t ev = 0, d1 = 0, d2 = 0;
-    if (r >= 1 && vm) {
+    if (word && r >= 1 && vm) {
         const int ta = tid - WPR;
         const uint32_t a = S.x[ta], vma = S.vm[ta];
         // above row's starts/carry are recomputed locally (no dependency on other warps)
@@ -264,7 +278,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     // is not queued.  Contacts are ordered by column: the up-left diagonal at the run start
     // (d1), vertical contacts (ev), the up-right diagonal past the run end (d2, stored at the
     // next column).  Vertical stacks of equal runs (rows of a g x g block) need no union at all.
-    if (r >= 1 && vm) {
+    if (word && r >= 1 && vm) {
         const int ta = tid - WPR;
         const uint32_t contacts = d1 | ev | (d2 >> 1);
         uint32_t m = wb.st;
@@ -310,7 +324,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
         const int nr = S.nruns;
         for (;;) {
             int changed = 0;
-            for (int i = tid; i < nr; i += NT) {
+            for (int i = tid; i < nr; i += BT) {
                 const uint32_t p = S.par[i];
                 const uint32_t gp = S.par[p];
                 if (gp != p) {
@@ -323,38 +337,52 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     }
     RL_PHASE(tg.t, 3);
     // compact the warp's events into its queue (in rounds of EVC) and resolve them lane-parallel
-    for (int done = 0; done < wtot; done += C::EVC) {
-        if (nev && my0 < done + C::EVC && my0 + nev > done) {
-            int o = my0;
-            const uint16_t wbase = (uint16_t)(tid << 7);
-            auto put = [&](uint32_t code) {
-                if (o >= done && o < done + C::EVC) S.evq[warp][o - done] = (uint16_t)code;
-                ++o;
-            };
-            for (uint32_t e = ev; e; e &= e - 1u) put(wbase | (__ffs(e) - 1));
-            for (uint32_t e = d1; e; e &= e - 1u) put(wbase | (1u << 5) | (__ffs(e) - 1));
-            for (uint32_t e = d2; e; e &= e - 1u) put(wbase | (2u << 5) | (__ffs(e) - 1));
+    auto put_events = [&](int done) {
+        int o = my0;
+        const uint16_t wbase = (uint16_t)(tid << 7);
+        auto put = [&](uint32_t code) {
+            if (o >= done && o < done + C::EVC) S.evq[warp][o - done] = (uint16_t)code;
+            ++o;
+        };
+        for (uint32_t e = ev; e; e &= e - 1u) put(wbase | (__ffs(e) - 1));
+        for (uint32_t e = d1; e; e &= e - 1u) put(wbase | (1u << 5) | (__ffs(e) - 1));
+        for (uint32_t e = d2; e; e &= e - 1u) put(wbase | (2u << 5) | (__ffs(e) - 1));
+    };
+    auto resolve_event = [&](uint32_t e) {
+        const int wd = (int)(e >> 7), type = (int)((e >> 5) & 3u), j = (int)(e & 31u);
+        const int wa = wd - WPR;
+        uint32_t ra, rb2;
+        if (type == 0) {
+            ra = (uint32_t)run_at(S, wd, j);
+            rb2 = (uint32_t)run_at(S, wa, j);
+        } else if (type == 1) {
+            ra = (uint32_t)run_at(S, wd, j);
+            rb2 = (uint32_t)run_left(S, wa, j);
+        } else {
+            ra = (uint32_t)run_left(S, wd, j);
+            rb2 = (uint32_t)run_at(S, wa, j);
         }
-        __syncwarp();
-        const int cnt = min(C::EVC, wtot - done);
-        for (int k = lane; k < cnt; k += 32) {
-            const uint32_t e = S.evq[warp][k];
-            const int word = (int)(e >> 7), type = (int)((e >> 5) & 3u), j = (int)(e & 31u);
-            const int wa = word - WPR;
-            uint32_t ra, rb2;
-            if (type == 0) {
-                ra = (uint32_t)run_at(S, word, j);
-                rb2 = (uint32_t)run_at(S, wa, j);
-            } else if (type == 1) {
-                ra = (uint32_t)run_at(S, word, j);
-                rb2 = (uint32_t)run_left(S, wa, j);
-            } else {
-                ra = (uint32_t)run_left(S, word, j);
-                rb2 = (uint32_t)run_at(S, wa, j);
-            }
-            sunion(S.par, ra, rb2);
+        sunion(S.par, ra, rb2);
+    };
+    if constexpr (BT == NW) {
+        for (int done = 0; done < wtot; done += C::EVC) {
+            if (nev && my0 < done + C::EVC && my0 + nev > done) put_events(done);
+            __syncwarp();
+            const int cnt = min(C::EVC, wtot - done);
+            for (int k = lane; k < cnt; k += 32) resolve_event(S.evq[warp][k]);
+            __syncwarp();
         }
-        __syncwarp();
+    } else {
+        // one round always suffices (<= 32 events per word); each queue is drained by the
+        // warp that filled it and by its partner warp past NW
+        if (word) {
+            if (nev) put_events(0);
+            if (lane == 0) S.qtot[warp] = wtot;
+        }
+        __syncthreads();
+        const int q = warp & (NWARPS - 1);
+        const int cnt = S.qtot[q];
+        for (int k = lane + 32 * (warp / NWARPS); k < cnt; k += 32 * (BT / NW)) resolve_event(S.evq[q][k]);
     }
     __syncthreads();
     RL_PHASE(tg.t, 4);
@@ -364,7 +392,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     const int nruns = S.nruns;
     for (int round = 0;; ++round) {
         int changed = 0;
-        for (int i = tid; i < nruns; i += NT) {
+        for (int i = tid; i < nruns; i += BT) {
             uint32_t p = S.par[i];
             const uint32_t p0 = p;
             for (int k = 0; k < 4; ++k) {
@@ -380,12 +408,12 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     RL_PHASE(tg.t, 5);
 
     // ---- tile components = root runs, numbered in raster order (contiguous run chunks)
-    const int per = (nruns + NT - 1) / NT;
+    const int per = (nruns + BT - 1) / BT;
     const int i0 = min(tid * per, nruns), i1 = min(i0 + per, nruns);
     int nroots = 0;
     for (int i = i0; i < i1; ++i) nroots += (S.par[i] == (uint32_t)i);
     int nlc;
-    int lc = block_excl_scan(nroots, S.wsum, nlc);
+    int lc = block_excl_scan<BT>(nroots, S.wsum, nlc);
     for (int i = i0; i < i1; ++i) {
         const int rr = run_row(S, i);
         if (S.rbase[rr * WPR] == i) S.rowlc[rr] = (uint16_t)lc;  // first run of its row
@@ -401,7 +429,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     __syncthreads();
     RL_PHASE(tg.t, 6);
     // resolve non-root runs; mark components touching the tile border (plain stores of 1)
-    for (int i = tid; i < nruns; i += NT) {
+    for (int i = tid; i < nruns; i += BT) {
         uint32_t p = S.par[i];
         if (!(p & TAG16)) {
             p = S.par[p];
@@ -415,12 +443,12 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     RL_PHASE(tg.t, 7);
 
     // ---- compact border components to border indices (raster order)
-    const int perl = (nlc + NT - 1) / NT;
+    const int perl = (nlc + BT - 1) / BT;
     const int l0 = min(tid * perl, nlc), l1 = min(l0 + perl, nlc);
     int cnt = 0;
     for (int l = l0; l < l1; ++l) cnt += S.lcb[l];
     int nb;
-    int bx = block_excl_scan(cnt, S.wsum, nb);
+    int bx = block_excl_scan<BT>(cnt, S.wsum, nb);
     if (nb > C::NBC) return false;  // more border components than this class holds
     for (int l = l0; l < l1; ++l) {
         if (S.lcb[l]) {
