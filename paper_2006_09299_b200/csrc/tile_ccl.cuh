@@ -29,7 +29,7 @@ namespace rlg {
 
 // Optional per-phase clock64() stamps of each tile CTA (profiling builds only:
 // -DRL_PHASE_PROF; tools/phase_prof.py).  Slot 32*tile + k holds the stamp of phase k
-// (analyze pass 0..12, emit pass 16..24).
+// (analyze pass 0..14, emit pass 16..24).
 #ifdef RL_PHASE_PROF
 __device__ unsigned long long* g_phase_buf = nullptr;
 __device__ int g_phase_n = 0;
@@ -273,6 +273,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
         d2 = xl1 & a & nx & ~al1 & both;  // (r, j-1) ~ (r-1, j)
     }
     __syncthreads();  // run bases of every word are visible (the init below reads the row above)
+    RL_PHASE(tg.t, 13);
     // ---- first contact: a run starting in this word takes the first run it touches in the
     // row above as its initial parent (cf. Alg. 2's `era[er] = find(above)`), and that contact
     // is not queued.  Contacts are ordered by column: the up-left diagonal at the run start
@@ -280,31 +281,26 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     // next column).  Vertical stacks of equal runs (rows of a g x g block) need no union at all.
     if (word && r >= 1 && vm) {
         const int ta = tid - WPR;
+        const uint32_t st = wb.st, sta = S.st[ta];
+        const int rb = S.rbase[tid], rba = S.rbase[ta];
+        // Bit-parallel "first contact of each run starting here": within each run segment
+        // [start, next start) the carry of (noncontact + start) stops at the first contact
+        // (a zero planted at each segment's last column stops it when there is none).
         const uint32_t contacts = d1 | ev | (d2 >> 1);
-        uint32_t m = wb.st;
-        int k = S.rbase[tid];
-        while (m) {
-            const int s = __ffs(m) - 1;
-            m &= m - 1u;
-            const uint32_t upto = m ? ((1u << (__ffs(m) - 1)) - 1u) : 0xFFFFFFFFu;
-            const uint32_t cseg = contacts & upto & ~((1u << s) - 1u);
-            if (cseg) {
-                const int j = __ffs(cseg) - 1;
-                const uint32_t bit = 1u << j;
-                int above;
-                if (d1 & bit) {
-                    above = run_left(S, ta, j);
-                    d1 &= ~bit;
-                } else if (ev & bit) {
-                    above = run_at(S, ta, j);
-                    ev &= ~bit;
-                } else {
-                    above = run_at(S, ta, j + 1);
-                    d2 &= ~(bit << 1);
-                }
-                S.par[k] = (uint16_t)above;
-            }
-            ++k;
+        const uint32_t nc = ~contacts & ~(st >> 1);
+        const uint32_t first = contacts & (nc + st) & ~nc;
+        const uint32_t f1 = first & d1, f2 = first & ev, f3 = first & ~d1 & ~ev;
+        d1 &= ~f1;
+        ev &= ~f2;
+        d2 &= ~(f3 << 1);
+        for (uint32_t m = first; m; m &= m - 1u) {
+            const int j = __ffs(m) - 1;
+            const uint32_t bit = 1u << j;
+            // above-row column of the contact: j - 1 (d1), j (ev), j + 1 (d2)
+            const uint32_t sh = (f1 & bit) ? 0u : (f2 & bit) ? 1u : 2u;
+            const int above = rba - 1 + __popc(sta & (((1u << sh) << j) - 1u));
+            const int k = rb - 1 + __popc(st & (0xFFFFFFFFu >> (31 - j)));
+            S.par[k] = (uint16_t)above;
         }
     }
     const int nev = __popc(ev) + __popc(d1) + __popc(d2);
@@ -317,6 +313,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     const int wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
     const int my0 = incl - nev;  // offset of this lane's first event in the warp's sequence
     __syncthreads();             // first-contact parents of every word are in place
+    RL_PHASE(tg.t, 14);
     // The first-contact forest links every run to one in the row above, so a vertical stack
     // of runs is a chain as tall as the stack.  Pointer jumping flattens it (log2 of the tile
     // height rounds) so that the finds of the union phase are short.

@@ -23,15 +23,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cells", default="0.5:1")
     ap.add_argument("--copies", type=int, default=4)
+    ap.add_argument("--cfg2", action="store_true", help="the cfg2 density/grain sweep, one image per cell")
     args = ap.parse_args()
     import numpy as np
     import torch
     from paper_2006_09299_b200 import Labeler, LabelingConfig, _native
-    from paper_2006_09299_b200.runlab import generate_device
+    from paper_2006_09299_b200.runlab import cfg2_cells, generate_device
 
     L = _native.load()
     L.rl_debug_phase_buffer.argtypes = [C.c_void_p, C.c_int]
     cells = [tuple(float(v) if i == 0 else int(v) for i, v in enumerate(c.split(":"))) for c in args.cells.split(",")]
+    if args.cfg2:
+        cells, args.copies = list(cfg2_cells()), 1
     S = 2048
     B = len(cells) * args.copies
     imgs = torch.empty((B, S, S), dtype=torch.uint8, device="cuda")
@@ -57,6 +60,10 @@ def main():
         print(f"  {NAMES[k + 1]:22s} {d[:, k].mean():9.0f} cycles  (p90 {np.percentile(d[:, k], 90):9.0f})")
     ok = (st[:, 16:25] > 0).all(axis=1)
     d = np.diff(st[ok, 16:25], axis=1)
+    ok = (st[:, 2:15] > 0).all(axis=1)
+    for name, a, b in [("  events (bit masks)", 2, 13), ("  first contact+prefix", 13, 14), ("  pre-flatten", 14, 3)]:
+        dd = st[ok, b] - st[ok, a]
+        print(f"  {name:22s} {dd.mean():9.0f} cycles  (p90 {np.percentile(dd, 90):9.0f})")
     print(f"emit: tiles with complete stamps: {ok.sum()} / {ntiles}; mean CTA latency "
           f"{(st[ok, 24] - st[ok, 16]).mean():.0f} cycles (chunk phases: last chunk)")
     for k, name in enumerate(["runs+map", "border-info+repx", "ext-mask", "features", "records",
