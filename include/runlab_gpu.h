@@ -132,18 +132,25 @@ typedef struct rl_host_outputs {
     uint32_t* labels;       /* [n*h*w] or NULL (requires cfg.relabel) */
     rl_component* comps;    /* [comp_capacity] or NULL */
     uint32_t* top;          /* [comp_capacity] or NULL */
-    rl_features* filled;    /* [comp_capacity] or NULL */
+    rl_features* filled;    /* [comp_capacity] or NULL; layout: see filled_layout */
     int64_t comp_capacity;
     int64_t* summary;       /* [n*5] C_pre, n_fg, n_holes, euler, C_post per image, or NULL */
     int64_t* comp_offset;   /* [n+1] or NULL */
     int64_t comps_needed;   /* out: total components of the batch */
     int64_t h2d_bytes;      /* out: bytes copied host->device */
     int64_t d2h_bytes;      /* out: bytes copied device->host */
+    int32_t filled_layout;  /* 0: filled[] indexed like comps[] (only post-fill roots are
+                               meaningful); 1: the post-fill roots only, in component order
+                               (sum over images of C_post entries) */
+    int32_t reserved;
 } rl_host_outputs;
 
 /* Host-buffer entry point with caller-owned outputs: H2D copy of the pixels, pipeline, D2H
- * copy of every non-NULL output, one stream sync.  RL_ENOSPC if comp_capacity is too small
- * (comps_needed tells the size; the non-component outputs are still filled). */
+ * copy of every non-NULL output.  Large batches are cut into chunks of whole images that are
+ * pipelined through several workspaces and streams, so that the host<->device copies of one
+ * chunk overlap the kernels and copies of the others; results are identical to one call over
+ * the whole batch.  RL_ENOSPC if comp_capacity is too small (comps_needed tells the size; the
+ * non-component outputs are still filled). */
 int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t width, int32_t height,
                   int32_t n_images, const rl_config* cfg, rl_host_outputs* out);
 

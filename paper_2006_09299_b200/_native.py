@@ -52,7 +52,8 @@ class RlHostOutputs(C.Structure):
     _fields_ = [("filled_image", C.c_void_p), ("labels", C.c_void_p), ("comps", C.c_void_p),
                 ("top", C.c_void_p), ("filled", C.c_void_p), ("comp_capacity", C.c_int64),
                 ("summary", C.c_void_p), ("comp_offset", C.c_void_p), ("comps_needed", C.c_int64),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("filled_layout", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 _lib = None

@@ -34,7 +34,9 @@ void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
 void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s);
 void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
                        cudaStream_t s, int sms);
-void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, const uint64_t* cbase,
+void launch_compact_filled(const Acc* filled, const uint32_t* flag, const uint32_t* rank, const uint64_t* total_p,
+                           uint64_t cap, Acc* out, cudaStream_t s, int sms);
+void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, const uint64_t* cbase, uint64_t cap,
                   cudaStream_t s, int sms);
 }  // namespace rlg
 
@@ -79,7 +81,9 @@ struct GraphKey {
     const void* summ;
     const void* rank;
     const void* flag;
+    const void* fcomp;
     uint64_t cap_comps;
+    int compact;
 };
 
 }  // namespace
@@ -97,7 +101,7 @@ struct rl_ctx {
     // workspace
     DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
     DevBuf cnt, off, counters, img_fg, img_surv, comps, top, filled, filled_img, labels, pix;
-    DevBuf cub_tmp, cbase, summ, rank, flag, ovf, ovf2, thdr, tmap, rstore, rused;
+    DevBuf cub_tmp, cbase, summ, rank, flag, ovf, ovf2, thdr, tmap, rstore, rused, fcomp;
     uint32_t cap_nodes = 0;
     uint64_t cap_comps = 0;
     uint64_t cap_rstore = 0;
@@ -118,6 +122,12 @@ struct rl_ctx {
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey{};
     cudaEvent_t gev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // post-fill features of the survivors compacted into `fcomp` (rl_label_into layout 1)
+    bool want_compact = false;
+    int64_t chunk_px = 32ll << 20;  // rl_label_into: pixels per chunk (env RUNLAB_GPU_CHUNK_PX)
+    // rl_label_into pipelines large batches through these (own workspace and stream each)
+    static constexpr int NKIDS = 3;
+    rl_ctx* kids[NKIDS] = {};
 };
 
 namespace {
@@ -216,7 +226,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)ncnt);
     size_t tmp2 = 0;
-    if (cfg->densify_labels && cfg->fill_holes)
+    if ((cfg->densify_labels && cfg->fill_holes) || ctx->want_compact)
         cub::DeviceScan::ExclusiveSum(nullptr, tmp2, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                       (int)std::min<uint64_t>(ctx->cap_comps + 1, 0x7FFFFFFF));
     if (!ensure(ctx->cub_tmp, std::max(tmp, tmp2))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
@@ -257,11 +267,14 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
 
     cudaStream_t s = ctx->stream;
     const bool densify_fill = cfg->densify_labels && cfg->fill_holes && g.label_mode;
-    if (densify_fill) {
+    const bool need_rank = densify_fill || ctx->want_compact;
+    if (need_rank) {
         const uint64_t total = ctx->cap_comps;
         if (!ensure(ctx->rank, (total + 1) * 4) || !ensure(ctx->flag, (total + 1) * 4))
             return set_err(ctx, RL_ENOMEM, "device allocation failed");
     }
+    if (ctx->want_compact && !ensure(ctx->fcomp, ctx->cap_comps * sizeof(Acc)))
+        return set_err(ctx, RL_ENOMEM, "device allocation failed");
     const size_t sn = (size_t)(B + 1) * 4;
     if (ctx->h_summ_n < sn) {
         if (ctx->h_summ) cudaFreeHost(ctx->h_summ);
@@ -282,7 +295,9 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     key.summ = ctx->h_summ;
     key.rank = ctx->rank.p;
     key.flag = ctx->flag.p;
+    key.fcomp = ctx->fcomp.p;
     key.cap_comps = ctx->cap_comps;
+    key.compact = ctx->want_compact ? 1 : 0;
     if (use_graph && ctx->gexec && std::memcmp(&key, &ctx->gkey, sizeof(key)) == 0) {
         const cudaError_t e = cudaGraphLaunch(ctx->gexec, s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "graph launch");
@@ -333,17 +348,25 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launches += 3;
     k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));
     ++launches;
-    if (densify_fill) {
-        // densified post-fill ids: rank of each survivor inside its image (labeling.hpp:231-236)
-        // total components is bounded by cap_comps; flags over [0, cap) are computed for the
-        // prefix that is in use (the remap only reads ranks of survivors).
+    if (need_rank) {
+        // rank of each post-fill root among the batch's components (labeling.hpp:231-236);
+        // total components is bounded by cap_comps, flags over [0, cap) are computed for the
+        // prefix in use (consumers only read ranks of survivors)
         const uint64_t total = ctx->cap_comps;
         launch_surv_flags(ws.top, P<uint64_t>(ctx->cbase), B, total, P<uint32_t>(ctx->flag), s, ctx->sms);
         size_t t2 = ctx->cub_tmp.bytes;
         cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t2, P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank),
                                       (int)std::min<uint64_t>(total + 1, 0x7FFFFFFF), s);
-        launch_remap(ws.labels, g.P, B, P<uint32_t>(ctx->rank), P<uint64_t>(ctx->cbase), s, ctx->sms);
-        launches += 3;
+        launches += 2;
+    }
+    if (densify_fill) {
+        launch_remap(ws.labels, g.P, B, P<uint32_t>(ctx->rank), P<uint64_t>(ctx->cbase), ctx->cap_comps, s, ctx->sms);
+        ++launches;
+    }
+    if (ctx->want_compact) {
+        launch_compact_filled(ws.filled, P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank), P<uint64_t>(ctx->cbase) + B,
+                              ctx->cap_comps, P<Acc>(ctx->fcomp), s, ctx->sms);
+        ++launches;
     }
     record_event(ctx->ev[3], s, use_graph);
     cudaMemcpyAsync(ctx->h_summ, ctx->summ.p, sn * 8, cudaMemcpyDeviceToHost, s);
@@ -467,6 +490,96 @@ int fetch(rl_ctx* ctx, rl_result* out) {
     return RL_OK;
 }
 
+
+// ---- rl_label_into: chunked, pipelined host-buffer path
+
+struct IntoState {
+    int64_t total = 0;  // components of the chunks posted so far
+    int64_t surv = 0;   // post-fill roots of the chunks posted so far
+    int64_t d2h = 0;
+    bool nospace = false;
+};
+
+void copy_fixed_outputs(rl_ctx* c, rl_host_outputs* out, int32_t b0) {
+    const Geo& g = c->geo;
+    const size_t npx = (size_t)(g.P * g.B), off = (size_t)g.P * b0;
+    if (out->filled_image)
+        cudaMemcpyAsync(out->filled_image + off, c->ws.filled_img, npx, cudaMemcpyDeviceToHost, c->stream);
+    if (out->labels && g.label_mode)
+        cudaMemcpyAsync(out->labels + off, c->ws.labels, npx * 4, cudaMemcpyDeviceToHost, c->stream);
+}
+
+// H2D of images [b0, b0 + n), the pipeline, and the D2H of the outputs whose size is fixed
+int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+                 rl_host_outputs* out, int32_t b0) {
+    const size_t npx = (size_t)w * h * n;
+    if (!ensure(c->pix, npx)) return set_err(c, RL_ENOMEM, "device allocation failed");
+    const cudaError_t e = cudaMemcpyAsync(c->pix.p, pixels, npx, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "copy in");
+    c->want_compact = out->filled && out->filled_layout == 1;
+    const int rc = enqueue(c, P<uint8_t>(c->pix), w, h, n, cfg);
+    if (rc) return rc;
+    copy_fixed_outputs(c, out, b0);
+    return RL_OK;
+}
+
+// after finish(c): per-image summaries and the component outputs of c's chunk (first image b0)
+int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st) {
+    const Geo& g = c->geo;
+    const int B = g.B;
+    if (c->reran) copy_fixed_outputs(c, out, b0);  // the pipeline re-ran after the first copies
+    if (out->filled_image) st.d2h += g.P * B;
+    if (out->labels && g.label_mode) st.d2h += g.P * B * 4;
+    const int64_t* s = c->h_summ;
+    const int64_t total = s[4 * B];
+    int64_t surv = 0;
+    for (int b = 0; b < B; ++b) surv += s[4 * b + 3];
+    st.d2h += (int64_t)(B + 1) * 32;
+    if (out->summary)
+        for (int b = 0; b < B; ++b) {
+            const int64_t cp = s[4 * b + 1], fg = s[4 * b + 2];
+            int64_t* o = out->summary + 5 * (int64_t)(b0 + b);
+            o[0] = cp;
+            o[1] = fg;
+            o[2] = cp - 1 - fg;
+            o[3] = fg - (cp - 1 - fg);
+            o[4] = s[4 * b + 3];
+        }
+    if (out->comp_offset) {
+        for (int b = 0; b < B; ++b) out->comp_offset[b0 + b] = st.total + s[4 * b];
+        out->comp_offset[b0 + B] = st.total + total;
+    }
+    const bool want_comps = out->comps || out->top || out->filled;
+    if (want_comps && st.total + total > out->comp_capacity) st.nospace = true;
+    if (!st.nospace) {
+        cudaStream_t cs = c->stream;
+        if (out->comps) {
+            cudaMemcpyAsync(out->comps + st.total, c->ws.comps, sizeof(rl_component) * total, cudaMemcpyDeviceToHost, cs);
+            st.d2h += (int64_t)sizeof(rl_component) * total;
+        }
+        if (out->top) {
+            cudaMemcpyAsync(out->top + st.total, c->ws.top, 4 * total, cudaMemcpyDeviceToHost, cs);
+            st.d2h += 4 * total;
+        }
+        if (out->filled && out->filled_layout == 0) {
+            cudaMemcpyAsync(out->filled + st.total, c->ws.filled, sizeof(rl_features) * total, cudaMemcpyDeviceToHost, cs);
+            st.d2h += (int64_t)sizeof(rl_features) * total;
+        } else if (out->filled) {
+            cudaMemcpyAsync(out->filled + st.surv, c->fcomp.p, sizeof(rl_features) * surv, cudaMemcpyDeviceToHost, cs);
+            st.d2h += (int64_t)sizeof(rl_features) * surv;
+        }
+    }
+    st.total += total;
+    st.surv += surv;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RL_OK : cuda_fail(c, e, "copy out");
+}
+
+int into_sync(rl_ctx* c) {
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    return e == cudaSuccess ? RL_OK : cuda_fail(c, e, "copy out");
+}
+
 }  // namespace
 
 extern "C" {
@@ -488,6 +601,7 @@ rl_ctx* rl_create(int device) {
     }
     c->stream = c->own_stream;
     if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
+    if (const char* v = std::getenv("RUNLAB_GPU_CHUNK_PX")) c->chunk_px = std::max(1ll, std::atoll(v));
     return c;
 }
 
@@ -499,7 +613,9 @@ void rl_destroy(rl_ctx* c) {
                       &c->nrec, &c->nrep, &c->nrootcid, &c->nparent, &c->nanccid, &c->cnt, &c->off,
                       &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
-                      &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused};
+                      &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,
+                      &c->fcomp};
+    for (rl_ctx* k : c->kids) rl_destroy(k);
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_summ) cudaFreeHost(c->h_summ);
@@ -517,6 +633,7 @@ int rl_label_device(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t h, 
     const int rc = check_args(ctx, w, h, n, cfg);
     if (rc) return rc;
     cudaSetDevice(ctx->device);
+    ctx->want_compact = false;
     return enqueue(ctx, d_pixels, w, h, n, cfg);
 }
 
@@ -544,6 +661,7 @@ int rl_label(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n
     if (!ensure(ctx->pix, npx)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
     cudaError_t e = cudaMemcpyAsync(ctx->pix.p, pixels, npx, cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "copy in");
+    ctx->want_compact = false;
     rc = enqueue(ctx, P<uint8_t>(ctx->pix), w, h, n, cfg);
     if (rc) return rc;
     rc = finish(ctx);
@@ -556,74 +674,55 @@ int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int3
     if (!out) return RL_EINVAL;
     out->comps_needed = 0;
     out->h2d_bytes = out->d2h_bytes = 0;
+    if (out->filled_layout != 0 && out->filled_layout != 1) return set_err(ctx, RL_EINVAL, "unknown filled_layout");
     int rc = check_args(ctx, w, h, n, cfg);
     if (rc) return rc;
     cudaSetDevice(ctx->device);
-    const size_t npx = (size_t)w * h * n;
-    if (!ensure(ctx->pix, npx)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
-    cudaStream_t st = ctx->stream;
-    cudaError_t e = cudaMemcpyAsync(ctx->pix.p, pixels, npx, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "copy in");
-    out->h2d_bytes = (int64_t)npx;
-    rc = enqueue(ctx, P<uint8_t>(ctx->pix), w, h, n, cfg);
-    if (rc) return rc;
-    // outputs whose size does not depend on the result go out on the same stream
-    int64_t d2h = 0;
-    if (out->filled_image) {
-        cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
-        d2h += (int64_t)npx;
-    }
-    if (out->labels && ctx->geo.label_mode) {
-        cudaMemcpyAsync(out->labels, ctx->ws.labels, npx * 4, cudaMemcpyDeviceToHost, st);
-        d2h += (int64_t)npx * 4;
-    }
-    rc = finish(ctx);  // syncs; reruns (and recopies above outputs' sources) on overflow
-    if (rc) return rc;
-    if (ctx->reran) {
-        // a capacity grew and the pipeline re-ran after the copies above: copy again
-        if (out->filled_image)
-            cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
-        if (out->labels && ctx->geo.label_mode)
-            cudaMemcpyAsync(out->labels, ctx->ws.labels, npx * 4, cudaMemcpyDeviceToHost, st);
-    }
-    const int B = ctx->geo.B;
-    const int64_t* s = ctx->h_summ;
-    const int64_t total = s[4 * B];
-    out->comps_needed = total;
-    d2h += (int64_t)(B + 1) * 32;
-    if (out->summary)
-        for (int b = 0; b < B; ++b) {
-            const int64_t cp = s[4 * b + 1], fg = s[4 * b + 2];
-            out->summary[5 * b + 0] = cp;
-            out->summary[5 * b + 1] = fg;
-            out->summary[5 * b + 2] = cp - 1 - fg;
-            out->summary[5 * b + 3] = fg - (cp - 1 - fg);
-            out->summary[5 * b + 4] = s[4 * b + 3];
+    const int64_t P = (int64_t)w * h;
+    // whole images per chunk, ~32 Mpx by default (pipelines of that size are graph-replayed)
+    const int32_t per = (int32_t)std::min<int64_t>(n, std::max<int64_t>(1, ctx->chunk_px / P));
+    const int32_t nch = (n + per - 1) / per;
+    IntoState st;
+    if (nch == 1) {
+        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0);
+        if (!rc) rc = finish(ctx);
+        if (!rc) rc = into_post(ctx, out, 0, st);
+        if (!rc) rc = into_sync(ctx);
+    } else {
+        for (rl_ctx*& k : ctx->kids)
+            if (!k) {
+                k = rl_create(ctx->device);
+                if (!k) return set_err(ctx, RL_ECUDA, "could not create a pipeline context");
+                k->graphs = ctx->graphs;
+            }
+        auto first_image = [&](int32_t c) { return c * per; };
+        auto images = [&](int32_t c) { return std::min(per, n - c * per); };
+        // chunk c runs on kid c % NKIDS; its component outputs are copied once its summary is
+        // in, just before the kid takes chunk c + NKIDS (outputs stay in chunk order)
+        auto post = [&](int32_t c) -> int {
+            rl_ctx* k = ctx->kids[c % rl_ctx::NKIDS];
+            int r = finish(k);
+            if (r) return set_err(ctx, r, k->err);
+            r = into_post(k, out, first_image(c), st);
+            return r ? set_err(ctx, r, k->err) : RL_OK;
+        };
+        for (int32_t c = 0; c < nch && !rc; ++c) {
+            if (c >= rl_ctx::NKIDS) rc = post(c - rl_ctx::NKIDS);
+            if (rc) break;
+            rl_ctx* k = ctx->kids[c % rl_ctx::NKIDS];
+            const int32_t b0 = first_image(c);
+            rc = into_enqueue(k, pixels + (size_t)b0 * P, w, h, images(c), cfg, out, b0);
+            if (rc) rc = set_err(ctx, rc, k->err);
         }
-    if (out->comp_offset) {
-        for (int b = 0; b < B; ++b) out->comp_offset[b] = s[4 * b];
-        out->comp_offset[B] = total;
+        for (int32_t c = std::max(0, nch - rl_ctx::NKIDS); c < nch && !rc; ++c) rc = post(c);
+        for (rl_ctx* k : ctx->kids)
+            if (!rc) rc = into_sync(k) ? set_err(ctx, RL_ECUDA, k->err) : RL_OK;
     }
-    const bool want_comps = out->comps || out->top || out->filled;
-    if (want_comps && total > out->comp_capacity) {
-        out->d2h_bytes = d2h;
-        return set_err(ctx, RL_ENOSPC, "component buffers too small");
-    }
-    if (out->comps) {
-        cudaMemcpyAsync(out->comps, ctx->ws.comps, sizeof(rl_component) * total, cudaMemcpyDeviceToHost, st);
-        d2h += (int64_t)sizeof(rl_component) * total;
-    }
-    if (out->top) {
-        cudaMemcpyAsync(out->top, ctx->ws.top, 4 * total, cudaMemcpyDeviceToHost, st);
-        d2h += 4 * total;
-    }
-    if (out->filled) {
-        cudaMemcpyAsync(out->filled, ctx->ws.filled, sizeof(rl_features) * total, cudaMemcpyDeviceToHost, st);
-        d2h += (int64_t)sizeof(rl_features) * total;
-    }
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "copy out");
-    out->d2h_bytes = d2h;
+    if (rc) return rc;
+    out->comps_needed = st.total;
+    out->h2d_bytes = (int64_t)P * n;
+    out->d2h_bytes = st.d2h;
+    if (st.nospace) return set_err(ctx, RL_ENOSPC, "component buffers too small");
     return RL_OK;
 }
 

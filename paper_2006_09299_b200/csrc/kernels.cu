@@ -284,7 +284,10 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
 }
 
 // class S: one CTA per tile on the (ntx, nty, B) grid; heavier tiles go to list A
-__global__ void __launch_bounds__(NT) k_analyze(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+#ifndef RL_ANALYZE_MINB
+#define RL_ANALYZE_MINB 8
+#endif
+__global__ void __launch_bounds__(NT, RL_ANALYZE_MINB) k_analyze(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& A = *reinterpret_cast<AnalyzeSmem<CapS>*>(smem_raw);
     const TileGeom tg = tile_geom_grid(g);
@@ -1001,7 +1004,8 @@ __global__ void k_surv_flags(const uint32_t* top, uint64_t n, uint32_t* flag) {
 }
 
 __global__ void k_remap_labels(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank,
-                               const uint64_t* cbase) {
+                               const uint64_t* cbase, uint64_t cap) {
+    if (cbase[B] > cap) return;  // components overflowed: no labels were emitted, the host re-runs
     const int64_t total = P * B;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = i / P;
@@ -1022,6 +1026,17 @@ __global__ void k_surv_flags_img(const uint32_t* top, const uint64_t* cbase, int
         }
         flag[i] = top[i] == (uint32_t)(i - cbase[lo]) ? 1u : 0u;
     }
+}
+
+// post-fill features of the survivors only, in component order (rank = exclusive scan of the
+// survivor flags); the batch's component count is cbase[B]
+__global__ void k_compact_filled(const Acc* __restrict__ filled, const uint32_t* __restrict__ flag,
+                                 const uint32_t* __restrict__ rank, const uint64_t* __restrict__ total_p,
+                                 uint64_t cap, Acc* __restrict__ out) {
+    const uint64_t total = *total_p;
+    if (total > cap) return;  // components overflowed (nothing was emitted): the host re-runs
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x)
+        if (flag[i]) out[rank[i]] = filled[i];
 }
 
 }  // namespace rlg
@@ -1096,9 +1111,13 @@ void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, ui
                        cudaStream_t s, int sms) {
     k_surv_flags_img<<<grid_for((int64_t)total, 256, sms * 8), 256, 0, s>>>(top, cbase, B, total, flag);
 }
+void launch_compact_filled(const Acc* filled, const uint32_t* flag, const uint32_t* rank, const uint64_t* total_p,
+                           uint64_t cap, Acc* out, cudaStream_t s, int sms) {
+    k_compact_filled<<<grid_for((int64_t)cap, 256, sms * 8), 256, 0, s>>>(filled, flag, rank, total_p, cap, out);
+}
 void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, const uint64_t* cbase,
-                  cudaStream_t s, int sms) {
-    k_remap_labels<<<grid_for(P * B, 256, sms * 16), 256, 0, s>>>(labels, P, B, rank, cbase);
+                  uint64_t cap, cudaStream_t s, int sms) {
+    k_remap_labels<<<grid_for(P * B, 256, sms * 16), 256, 0, s>>>(labels, P, B, rank, cbase, cap);
 }
 
 }  // namespace rlg

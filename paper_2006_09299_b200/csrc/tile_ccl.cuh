@@ -319,7 +319,10 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     // height rounds) so that the finds of the union phase are short.
     {
         const int nr = S.nruns;
-        for (;;) {
+#ifndef RL_PREFLAT_ROUNDS
+#define RL_PREFLAT_ROUNDS 0
+#endif
+        for (int round = 0;; ++round) {
             int changed = 0;
             for (int i = tid; i < nr; i += BT) {
                 const uint32_t p = S.par[i];
@@ -329,7 +332,12 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
                     changed = 1;
                 }
             }
-            if (!__syncthreads_or(changed)) break;
+            if (RL_PREFLAT_ROUNDS > 0) {
+                __syncthreads();
+                if (round + 1 == RL_PREFLAT_ROUNDS) break;
+            } else if (!__syncthreads_or(changed)) {
+                break;
+            }
         }
     }
     RL_PHASE(tg.t, 3);
