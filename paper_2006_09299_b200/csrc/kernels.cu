@@ -38,7 +38,7 @@ struct AnalyzeSmem {
 
 // Returns false when the tile exceeds the capacity class C (then nothing was written for it
 // except the packed bits; the caller defers it to the next class).
-template <class C>
+template <class C, bool RELOAD>
 __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* __restrict__ pix, const Geo& g,
                                              const Ws& ws, const TileGeom& tg) {
     CclSmem<C>& S = A.c;
@@ -48,25 +48,31 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     const bool word = BT == NW || tid < NW;
     RL_PHASE(tg.t, 0);
 
-    // ---- load 32 pixels (bytes) of this thread's word and pack them to bits
+    // ---- load 32 pixels (bytes) of this thread's word and pack them to bits (the deferred
+    // classes reload the bits the class-S attempt packed)
     const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;
-    uint32_t bits = 0;
-    if (vm) {
-        const uint8_t* src = pix + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
-        if (g.vec_ok && vm == 0xFFFFFFFFu) {
-            const uint4* s4 = reinterpret_cast<const uint4*>(src);
-            const uint4 v0 = __ldcs(s4), v1 = __ldcs(s4 + 1);
-            bits = pack16(v0) | (pack16(v1) << 16);
-        } else {
-            const int n = 32 - __clz(vm);
-            for (int j = 0; j < n; ++j) bits |= (uint32_t)(src[j] & 1u) << j;
-        }
-    }
-    const uint32_t x = (bits ^ (g.flip ? 0xFFFFFFFFu : 0u)) & vm;
     if (word) {
+        uint32_t x;
+        if (RELOAD) {
+            x = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
+        } else {
+            uint32_t bits = 0;
+            if (vm) {
+                const uint8_t* src = pix + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
+                if (g.vec_ok && vm == 0xFFFFFFFFu) {
+                    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+                    const uint4 v0 = __ldcs(s4), v1 = __ldcs(s4 + 1);
+                    bits = pack16(v0) | (pack16(v1) << 16);
+                } else {
+                    const int n = 32 - __clz(vm);
+                    for (int j = 0; j < n; ++j) bits |= (uint32_t)(src[j] & 1u) << j;
+                }
+            }
+            x = (bits ^ (g.flip ? 0xFFFFFFFFu : 0u)) & vm;
+            ws.bits[(int64_t)tg.t * NW + tid] = x;
+        }
         S.x[tid] = x;
         S.vm[tid] = vm;
-        ws.bits[(int64_t)tg.t * NW + tid] = x;
     }
     for (int i = tid; i < C::NBC; i += BT) {
         A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
@@ -291,18 +297,18 @@ __global__ void __launch_bounds__(NT, RL_ANALYZE_MINB) k_analyze(const uint8_t* 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& A = *reinterpret_cast<AnalyzeSmem<CapS>*>(smem_raw);
     const TileGeom tg = tile_geom_grid(g);
-    if (!analyze_tile(A, pix, g, ws, tg) && threadIdx.x == 0)
+    if (!analyze_tile<CapS, false>(A, pix, g, ws, tg) && threadIdx.x == 0)
         ws.ovf[atomicAdd(&ws.counters[2], 1u)] = (uint32_t)tg.t;
 }
 
 // class M over list A; heavier tiles go to list B
-__global__ void __launch_bounds__(CapM::BT) k_analyze_m(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+__global__ void __launch_bounds__(CapM::BT, 3) k_analyze_m(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& A = *reinterpret_cast<AnalyzeSmem<CapM>*>(smem_raw);
     const uint32_t n = ws.counters[2];
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
         const TileGeom tg = tile_geom(g, (int32_t)ws.ovf[k]);
-        if (!analyze_tile(A, pix, g, ws, tg) && threadIdx.x == 0)
+        if (!analyze_tile<CapM, true>(A, pix, g, ws, tg) && threadIdx.x == 0)
             ws.ovf2[atomicAdd(&ws.counters[4], 1u)] = (uint32_t)tg.t;
         __syncthreads();
     }
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(CapF::BT) k_analyze_full(const uint8_t* __rest
     const uint32_t n = ws.counters[4];
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
         const TileGeom tg = tile_geom(g, (int32_t)ws.ovf2[k]);
-        analyze_tile(A, pix, g, ws, tg);
+        analyze_tile<CapF, true>(A, pix, g, ws, tg);
         __syncthreads();
     }
 }
@@ -973,7 +979,7 @@ __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
     emit_tile(E, g, ws, tile_geom_grid(g));
 }
 
-__global__ void __launch_bounds__(CapME::BT) k_emit_m(Geo g, Ws ws) {
+__global__ void __launch_bounds__(CapME::BT, 3) k_emit_m(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ws.counters[1] || !comps_fit(g, ws)) return;
     auto& E = *reinterpret_cast<EmitSmem<CapME>*>(smem_raw);
