@@ -68,7 +68,10 @@ using CapS = Cap<MAXRUNS * 3 / 16, NBMAX / 2, 192, 512, uint32_t, NW>;
 using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 384, uint32_t, 2 * NW>;
 using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 // emit pass: same classes, no unions (16-bit component map, larger feature chunks)
-using CapSE = Cap<CapS::MR, CapS::NBC, 192, 512, uint16_t, NW>;
+#ifndef RL_SE_FCH
+#define RL_SE_FCH 256
+#endif
+using CapSE = Cap<CapS::MR, CapS::NBC, 192, RL_SE_FCH, uint16_t, NW>;
 using CapME = Cap<CapM::MR, CapM::NBC, 1024, 640, uint16_t, 2 * NW>;
 using CapFE = Cap<CapF::MR, CapF::NBC, 1024, 320, uint16_t, 2 * NW>;
 
