@@ -233,6 +233,109 @@ def run_reference_arm(args, wl: Workload, rank: int) -> None:
 
 
 # ------------------------------------------------------------------------------ our arm
+def run_strips(args, wl: Workload, rank: int, world: int, local: int) -> None:
+    """SURVEY 8(e): the single image of the workload cut into one horizontal strip per rank;
+    three collectives per step (strips.py).  Strong scaling: the image is fixed."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2006_09299_b200 import Labeler, LabelingConfig
+    from paper_2006_09299_b200.runlab import generate_rows_device
+    from paper_2006_09299_b200.strips import TorchCollectives, label_strip, strip_rows
+
+    if len(wl.specs) != 1 or wl.specs[0][0] != "gen":
+        raise SystemExit("--strips needs a single generated image (cfg1 or cfg5)")
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    y0, h = strip_rows(wl.H, world)[rank]
+    _, dens, gran, seed = wl.specs[0]
+    d = torch.empty((h, wl.W), dtype=torch.uint8, device="cuda")
+    generate_rows_device(d.data_ptr(), wl.W, wl.H, y0, h, dens, gran, seed)
+    torch.cuda.synchronize()
+    lab = Labeler(local)
+    coll = TorchCollectives()
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    stream = torch.cuda.ExternalStream(lab.stream())
+
+    def step(fetch=False):
+        return label_strip(lab, d.data_ptr(), wl.W, wl.H, y0, h, cfg, coll, fetch=fetch)
+
+    for _ in range(args.warmup):
+        res = step()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_busy = time.time() + 0.3  # the GPU is under load before the timed region
+    while time.time() < t_busy:
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    launches = lab.launch_count() * args.steps
+    t_busy = time.time() + 0.3
+    while time.time() < t_busy:
+        step()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_step = statistics.mean(times)
+    t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    P = wl.W * wl.H
+    # e2e: host strip in, owned outputs out (pinned), through the same phases
+    h_in = torch.empty((h, wl.W), dtype=torch.uint8, pin_memory=True)
+    h_in.copy_(d.cpu())
+    dist.barrier()
+    full = step(fetch=True)  # allocates the pinned staging buffers once
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(max(args.e2e_steps, 1)):
+        d.copy_(h_in, non_blocking=True)
+        torch.cuda.synchronize()
+        full = step(fetch=True)
+    e2e_s = (time.perf_counter() - t0) / max(args.e2e_steps, 1)
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    owned = full.comp_hi - full.comp_lo
+    c_pre, c_post = res.n_components, res.n_survivors
+    bytes_alg = 2 * P + 48 * c_pre + 40 * c_post
+    peak, peak_src = measured_peaks()
+    per_gpu_gbs = bytes_alg / world / (ms_step / 1e3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": P / (ms_step / 1e3) / 1e9, "unit": "Gpixel/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (reference generator on device, each rank generates its own rows)",
+            "config": {"workload": wl.desc + ", fg8_bg4, features+Euler+tree+hole fill",
+                       "images_per_gpu": 1.0 / world, "pixels_per_gpu": P // world,
+                       "l2": "inputs > L2 (no flush)" if P // world > 126e6 else "strip fits L2",
+                       "parallelism": f"horizontal strips x{world} (all-gather of border-component "
+                                      "tables, all-reduce of border survivors' partial features)"},
+            "roofline": {"bound": "hbm", "kernel": "whole strip step (per GPU)", "achieved": per_gpu_gbs,
+                         "peak": peak, "unit": "GB/s", "frac": per_gpu_gbs / peak, "traffic": None,
+                         "peak_source": peak_src, "c_pre": c_pre, "c_post": c_post},
+            "cpu_baseline": None,
+            "e2e": {"value": P / e2e_s / 1e9, "unit": "Gpixel/s", "h2d_bytes_per_step": h * wl.W,
+                    "d2h_bytes_per_step": h * wl.W + 92 * owned, "ms_per_step": e2e_s * 1e3,
+                    "api": "strips.label_strip (pinned host strip in, owned components + strip of the "
+                           "filled image out)"},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line))
+    lab.close()
+    dist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -243,6 +346,8 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=5.0, help="minimum timed wall time of the CPU baseline")
+    ap.add_argument("--strips", action="store_true",
+                    help="one image cut into horizontal strips across the ranks (default for cfg5 with N > 1)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -254,6 +359,9 @@ def main() -> None:
         run_reference_arm(args, wl, rank)
         return
     args.warmup = max(args.warmup, 3)
+    if args.strips or (wl.name == "cfg5" and world > 1):
+        run_strips(args, wl, rank, world, local)
+        return
 
     import torch
     import torch.distributed as dist

@@ -161,6 +161,9 @@ int rl_phase_times(const rl_ctx* ctx, int back, rl_times* out);
  * generate() (generator.hpp:46-83).  stream: cudaStream_t or NULL; d_out: w*h bytes. */
 int rl_generate(void* stream, uint8_t* d_out, int32_t w, int32_t h, double density, int32_t g,
                 uint64_t seed);
+/* Rows [y0, y0 + rows) of the same image (d_out: w*rows bytes; one strip of a large image). */
+int rl_generate_rows(void* stream, uint8_t* d_out, int32_t w, int32_t h, int32_t y0, int32_t rows,
+                     double density, int32_t g, uint64_t seed);
 int rl_generate_rings(void* stream, uint8_t* d_out, int32_t w, int32_t h, int32_t tile,
                       uint64_t seed, double salt);
 void rl_cfg4_params(uint64_t i, double* density, int32_t* g);
@@ -171,6 +174,58 @@ int rl_last_launch_count(const rl_ctx* ctx);
  * environment variable RUNLAB_GPU_NO_GRAPH).  Phase times of older calls (back > 0) are then
  * not kept. */
 int rl_last_used_graph(const rl_ctx* ctx);
+
+
+/* ---- One image cut into horizontal strips across ranks -----------------------
+ * Rank r holds rows [y0, y0 + h) of one w x H image in device memory (y0 a multiple of 32; h a
+ * multiple of 32 except for the last strip).  Phases, with the caller's collectives between them
+ * (paper_2006_09299_b200/strips.py does them with torch.distributed; NCCL on GPUs):
+ *   1. rl_strip_local   tile passes + seams inside the strip (cut rows are open, not frame)
+ *   2. [all-gather of every rank's rl_strip_local_info]
+ *   3. rl_strip_export  the strip's exchange record (border components, cut-row perimeter
+ *                       labels, per-row counts) into a device buffer of
+ *                       rl_strip_export_bytes(w, max_nodes, max_tile_rows) bytes
+ *   4. [all-gather of the records: n_strips consecutive records]
+ *   5. rl_strip_merge   union across the cuts and the merge over all strips' border components
+ *                       (identical on every rank), then the emit pass of this strip; returns
+ *                       this rank's partial post-fill sums of the border survivors
+ *   6. [all-reduce of the partials in place: d_sum SUM, d_min MIN, d_max MAX, d_count SUM]
+ *   7. rl_strip_finish  post-fill features; the canonical-id range [comp_lo, comp_hi) this strip
+ *                       owns (components whose first pixel lies in it; strip 0 also owns the
+ *                       exterior, id 0)
+ *   8. rl_strip_fetch   copies that range and the strip's filled/label image rows to the host.
+ * Concatenating the strips' outputs gives exactly the single-image result.  densify_labels is
+ * not supported in strip mode (RL_EINVAL). */
+typedef struct rl_strip_local_info {
+    int64_t n_nodes;      /* border components of the strip */
+    int64_t interior_fg;  /* foreground components inside single tiles */
+    int32_t ty0, ty1;     /* tile rows of the strip */
+    int32_t status, pad;
+} rl_strip_local_info;
+
+typedef struct rl_strip_partials {
+    void* d_sum;    /* int64 [k * 3]: S, Sx, Sy */
+    void* d_min;    /* int32 [k * 2]: row_min, col_min */
+    void* d_max;    /* int32 [k * 2]: row_max, col_max */
+    void* d_count;  /* int64 [1]: interior survivors of this strip */
+    int64_t k;      /* border survivors (identical on every rank) */
+} rl_strip_partials;
+
+typedef struct rl_strip_result {
+    int64_t comp_lo, comp_hi;  /* canonical ids owned by this strip */
+    int64_t n_components, n_fg, n_holes, euler, n_survivors;  /* whole image */
+    int32_t y0, h;
+} rl_strip_result;
+
+int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t width, int32_t height, int32_t y0,
+                   int32_t h, const rl_config* cfg, rl_strip_local_info* out);
+int64_t rl_strip_export_bytes(int32_t width, int64_t max_nodes, int32_t max_tile_rows);
+int rl_strip_export(rl_ctx* ctx, int64_t max_nodes, int32_t max_tile_rows, void* d_buf);
+int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const rl_strip_local_info* infos,
+                   int64_t max_nodes, int32_t max_tile_rows, rl_strip_partials* out);
+int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out);
+/* comps/top/filled (layout 0) of [comp_lo, comp_hi), filled_image/labels of the strip's rows */
+int rl_strip_fetch(rl_ctx* ctx, const rl_strip_result* r, rl_host_outputs* out);
 
 /* Tile geometry used by the kernels (for DESIGN/roofline bookkeeping). */
 void rl_tile_shape(int32_t* tile_h, int32_t* tile_w);

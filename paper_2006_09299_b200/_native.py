@@ -20,6 +20,8 @@ EXPORTED_SYMBOLS = (
     "rl_sync", "rl_fetch", "rl_device_filled_image", "rl_device_labels", "rl_device_comps",
     "rl_stream", "rl_set_stream", "rl_last_launch_count", "rl_tile_shape", "rl_label_into",
     "rl_phase_times", "rl_generate", "rl_generate_rings", "rl_cfg4_params", "rl_last_used_graph",
+    "rl_strip_local", "rl_strip_export_bytes", "rl_strip_export", "rl_strip_merge", "rl_strip_finish",
+    "rl_strip_fetch", "rl_generate_rows",
 )
 
 FEATURE_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),
@@ -54,6 +56,22 @@ class RlHostOutputs(C.Structure):
                 ("summary", C.c_void_p), ("comp_offset", C.c_void_p), ("comps_needed", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("filled_layout", C.c_int32),
                 ("reserved", C.c_int32)]
+
+
+class RlStripLocalInfo(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("interior_fg", C.c_int64), ("ty0", C.c_int32),
+                ("ty1", C.c_int32), ("status", C.c_int32), ("pad", C.c_int32)]
+
+
+class RlStripPartials(C.Structure):
+    _fields_ = [("d_sum", C.c_void_p), ("d_min", C.c_void_p), ("d_max", C.c_void_p),
+                ("d_count", C.c_void_p), ("k", C.c_int64)]
+
+
+class RlStripResult(C.Structure):
+    _fields_ = [("comp_lo", C.c_int64), ("comp_hi", C.c_int64), ("n_components", C.c_int64),
+                ("n_fg", C.c_int64), ("n_holes", C.c_int64), ("euler", C.c_int64),
+                ("n_survivors", C.c_int64), ("y0", C.c_int32), ("h", C.c_int32)]
 
 
 _lib = None
@@ -92,9 +110,20 @@ def load() -> C.CDLL:
     L.rl_phase_times.argtypes = [C.c_void_p, C.c_int, C.POINTER(RlTimes)]
     L.rl_generate.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_int32,
                               C.c_uint64]
+    L.rl_generate_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                   C.c_double, C.c_int32, C.c_uint64]
     L.rl_generate_rings.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_uint64, C.c_double]
     L.rl_cfg4_params.argtypes = [C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+    L.rl_strip_local.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                 C.POINTER(RlConfig), C.POINTER(RlStripLocalInfo)]
+    L.rl_strip_export_bytes.restype = C.c_int64
+    L.rl_strip_export_bytes.argtypes = [C.c_int32, C.c_int64, C.c_int32]
+    L.rl_strip_export.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
+    L.rl_strip_merge.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(RlStripLocalInfo),
+                                 C.c_int64, C.c_int32, C.POINTER(RlStripPartials)]
+    L.rl_strip_finish.argtypes = [C.c_void_p, C.POINTER(RlStripResult)]
+    L.rl_strip_fetch.argtypes = [C.c_void_p, C.POINTER(RlStripResult), C.POINTER(RlHostOutputs)]
     _lib = L
     return L
 

@@ -19,28 +19,11 @@
 #include <string>
 
 #include "common.cuh"
+#include "ctx.hpp"
 #include "runlab_gpu.h"
 
-namespace rlg {
-size_t analyze_smem();
-size_t emit_smem();
-cudaError_t configure_kernels();
-void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s);
-void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
-void launch_resolve(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
-void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
-void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
-void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
-void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s);
-void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
-                       cudaStream_t s, int sms);
-void launch_compact_filled(const Acc* filled, const uint32_t* flag, const uint32_t* rank, const uint64_t* total_p,
-                           uint64_t cap, Acc* out, cudaStream_t s, int sms);
-void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, const uint64_t* cbase, uint64_t cap,
-                  cudaStream_t s, int sms);
-}  // namespace rlg
-
 using namespace rlg;
+using namespace rlh;
 
 namespace {
 
@@ -66,71 +49,10 @@ __global__ void k_summary(Geo g, Ws ws, uint64_t* cbase, int64_t* summ) {
     }
 }
 
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-};
-
-// Everything a captured pipeline depends on (compared bytewise before a replay).
-struct GraphKey {
-    Geo g;
-    Ws ws;
-    rl_config cfg;
-    const void* pix;
-    cudaStream_t stream;
-    const void* summ;
-    const void* rank;
-    const void* flag;
-    const void* fcomp;
-    uint64_t cap_comps;
-    int compact;
-};
-
 }  // namespace
 
-struct rl_ctx {
-    int device = 0;
-    int sms = 148;
-    cudaStream_t stream = nullptr;
-    cudaStream_t own_stream = nullptr;
-    std::string err;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // events of the current call
-    static constexpr int RING = 64;
-    cudaEvent_t ring[RING][4] = {};
-    int64_t calls = 0;
-    // workspace
-    DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
-    DevBuf cnt, off, counters, img_fg, img_surv, comps, top, filled, filled_img, labels, pix;
-    DevBuf cub_tmp, cbase, summ, rank, flag, ovf, ovf2, thdr, tmap, rstore, rused, fcomp;
-    uint32_t cap_nodes = 0;
-    uint64_t cap_comps = 0;
-    uint64_t cap_rstore = 0;
-    // pinned host mirror of the summary
-    int64_t* h_summ = nullptr;
-    size_t h_summ_n = 0;
-    // last call
-    Geo geo{};
-    Ws ws{};
-    rl_config cfg{};
-    const uint8_t* last_pix = nullptr;
-    int launches = 0;
-    bool have_result = false;
-    bool reran = false;  // finish() had to grow a capacity and re-run
-    // CUDA graph of the last small pipeline
-    bool graphs = true;
-    bool used_graph = false;
-    cudaGraphExec_t gexec = nullptr;
-    GraphKey gkey{};
-    cudaEvent_t gev[4] = {nullptr, nullptr, nullptr, nullptr};
-    // post-fill features of the survivors compacted into `fcomp` (rl_label_into layout 1)
-    bool want_compact = false;
-    int64_t chunk_px = 32ll << 20;  // rl_label_into: pixels per chunk (env RUNLAB_GPU_CHUNK_PX)
-    // rl_label_into pipelines large batches through these (own workspace and stream each)
-    static constexpr int NKIDS = 3;
-    rl_ctx* kids[NKIDS] = {};
-};
 
-namespace {
+namespace rlh {
 
 int set_err(rl_ctx* c, int code, const std::string& msg) {
     if (c) c->err = msg;
@@ -156,11 +78,6 @@ bool ensure(DevBuf& b, size_t bytes) {
     return true;
 }
 
-template <class T>
-T* P(DevBuf& b) {
-    return static_cast<T*>(b.p);
-}
-
 int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cfg) {
     if (!ctx) return RL_EINVAL;
     if (!cfg) return set_err(ctx, RL_EINVAL, "null config");
@@ -177,17 +94,7 @@ int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cf
     return RL_OK;
 }
 
-// Phase-timing event.  Inside a stream capture a plain record only becomes an internal graph
-// dependency; the external flag makes it a real event record node that replays time.
-void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
-    if (capturing)
-        cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
-    else
-        cudaEventRecord(ev, s);
-}
-
-// (Re)build geometry, grow the workspace, enqueue the pipeline.
-int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg) {
+Geo make_geo(int32_t W, int32_t H, int32_t B, const rl_config* cfg, const void* dpix) {
     Geo g{};
     g.W = W;
     g.H = H;
@@ -196,21 +103,31 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     g.nty = (H + TH - 1) / TH;
     g.tpi = g.ntx * g.nty;
     const int64_t ntiles = (int64_t)g.tpi * B;
-    if (ntiles >= (1ll << 31)) return set_err(ctx, RL_EINVAL, "too many tiles");
-    g.ntiles = (int32_t)ntiles;
+    g.ntiles = ntiles >= (1ll << 31) ? -1 : (int32_t)ntiles;
     g.flip = cfg->connectivity == RL_FG4_BG8 ? 1 : 0;
     g.P = (int64_t)W * H;
     g.vec_ok = ((W % 16) == 0 && (reinterpret_cast<uintptr_t>(dpix) % 16) == 0) ? 1 : 0;
     g.label_mode = cfg->relabel ? (cfg->fill_holes ? 2 : 1) : 0;
+    g.ty0 = 0;
+    g.ty1 = g.nty;
+    g.prow0 = 0;
+    return g;
+}
 
-    const int64_t ncnt = (int64_t)B * H * g.ntx + 1;
+int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& tmp, int64_t out_px) {
+    const int32_t B = g.B;
+    const int64_t ntiles = g.ntiles;
+    const int64_t ncnt = (int64_t)B * g.H * g.ntx + 1;
     if (ctx->cap_nodes == 0) ctx->cap_nodes = (uint32_t)std::min<int64_t>(std::max<int64_t>(ntiles * 96, 4096), 0xF0000000ll);
     // initial estimate 0.02 components/pixel (random images: 0.003-0.13); grows on demand
     if (ctx->cap_comps == 0) ctx->cap_comps = (uint64_t)std::max<int64_t>(g.P * B / 48, 4096);
     if (ctx->cap_rstore == 0) ctx->cap_rstore = (uint64_t)std::max<int64_t>(g.P * B * 3 / 10 + ntiles * 64, 1 << 16);
     const uint64_t nn = (uint64_t)B + ctx->cap_nodes;
     bool ok = ensure(ctx->bits, (size_t)ntiles * NW * 4) && ensure(ctx->tbase, (size_t)ntiles * 4) &&
-              ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->ovf, (size_t)ntiles * 4) && ensure(ctx->ovf2, (size_t)ntiles * 4) && ensure(ctx->thdr, (size_t)ntiles * THDR * 2) && ensure(ctx->tmap, (size_t)ntiles * 8) && ensure(ctx->rstore, ctx->cap_rstore * 2) && ensure(ctx->rused, 64) && ensure(ctx->perim, (size_t)ntiles * PERIM * 2) &&
+              ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->ovf, (size_t)ntiles * 4) &&
+              ensure(ctx->ovf2, (size_t)ntiles * 4) && ensure(ctx->thdr, (size_t)ntiles * THDR * 2) &&
+              ensure(ctx->tmap, (size_t)ntiles * 8) && ensure(ctx->rstore, ctx->cap_rstore * 2) &&
+              ensure(ctx->rused, 64) && ensure(ctx->perim, (size_t)ntiles * PERIM * 2) &&
               ensure(ctx->uf, nn * 4) && ensure(ctx->nkey, nn * 8) && ensure(ctx->nmin, nn * 8) &&
               ensure(ctx->nacc, nn * sizeof(Acc)) && ensure(ctx->nrec, nn * sizeof(NodeRec)) &&
               ensure(ctx->nrep, nn) && ensure(ctx->nrootcid, nn * 4) && ensure(ctx->nparent, nn * 4) &&
@@ -219,11 +136,11 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
               ensure(ctx->img_fg, (size_t)B * 4) && ensure(ctx->img_surv, (size_t)B * 4) &&
               ensure(ctx->comps, ctx->cap_comps * sizeof(rl_component)) &&
               ensure(ctx->top, ctx->cap_comps * 4) && ensure(ctx->filled, ctx->cap_comps * sizeof(Acc)) &&
-              ensure(ctx->filled_img, (size_t)(g.P * B)) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
+              ensure(ctx->filled_img, (size_t)out_px) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
               ensure(ctx->summ, (size_t)(B + 1) * 32);
-    if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)(g.P * B) * 4);
+    if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)out_px * 4);
     if (!ok) return set_err(ctx, RL_ENOMEM, "device allocation failed");
-    size_t tmp = 0;
+    tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)ncnt);
     size_t tmp2 = 0;
     if ((cfg->densify_labels && cfg->fill_holes) || ctx->want_compact)
@@ -231,7 +148,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
                                       (int)std::min<uint64_t>(ctx->cap_comps + 1, 0x7FFFFFFF));
     if (!ensure(ctx->cub_tmp, std::max(tmp, tmp2))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
 
-    Ws ws{};
+    ws = Ws{};
     ws.bits = P<uint32_t>(ctx->bits);
     ws.tbase = P<uint32_t>(ctx->tbase);
     ws.tnb = P<uint32_t>(ctx->tnb);
@@ -264,6 +181,31 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     ws.filled = P<Acc>(ctx->filled);
     ws.filled_img = P<uint8_t>(ctx->filled_img);
     ws.labels = g.label_mode ? P<uint32_t>(ctx->labels) : nullptr;
+
+    return RL_OK;
+}
+
+}  // namespace rlh
+
+namespace {
+
+// Phase-timing event.  Inside a stream capture a plain record only becomes an internal graph
+// dependency; the external flag makes it a real event record node that replays time.
+void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
+    if (capturing)
+        cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+    else
+        cudaEventRecord(ev, s);
+}
+
+// (Re)build geometry, grow the workspace, enqueue the pipeline.
+int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg) {
+    const Geo g = make_geo(W, H, B, cfg, dpix);
+    if (g.ntiles < 0) return set_err(ctx, RL_EINVAL, "too many tiles");
+    const int64_t ncnt = (int64_t)B * H * g.ntx + 1;
+    Ws ws;
+    size_t tmp = 0;
+    if (const int rc = prepare_ws(ctx, g, cfg, ws, tmp, g.P * B)) return rc;
 
     cudaStream_t s = ctx->stream;
     const bool densify_fill = cfg->densify_labels && cfg->fill_holes && g.label_mode;
@@ -614,8 +556,9 @@ void rl_destroy(rl_ctx* c) {
                       &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
                       &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,
-                      &c->fcomp};
+                      &c->fcomp, &c->nleft, &c->scount};
     for (rl_ctx* k : c->kids) rl_destroy(k);
+    strip_free(c);
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_summ) cudaFreeHost(c->h_summ);

@@ -60,6 +60,12 @@ struct Geo {
     int64_t P;           // pixels per image
     int32_t vec_ok;      // 16-B vector pixel I/O allowed
     int32_t label_mode;  // 0 none, 1 pre-fill canonical id, 2 post-fill root id
+    // strip mode (one image cut into horizontal strips across ranks): the tile passes cover
+    // tile rows [ty0, ty1) and pixel row y lives at row y - prow0 of the pixel buffer
+    int32_t ty0, ty1;
+    int64_t prow0;
+    int32_t strip;       // 1: strip mode (border survivors' post-fill sums are completed later)
+    int32_t pad_;
 };
 
 struct Ws {
@@ -78,6 +84,7 @@ struct Ws {
     uint32_t* nrootcid;  // canonical id (valid at roots)
     uint32_t* nparent;   // root node of the surrounding component (valid at roots)
     uint32_t* nanccid;   // canonical id of the post-fill root (valid at roots)
+    uint32_t* nleft;     // strip mode: node of the pixel left of the first pixel (else null)
     // canonical numbering
     uint32_t* cnt;       // [B*H*ntx + 1] roots whose first pixel is in (image,row,tile col)
     uint32_t* off;       // exclusive scan of cnt
@@ -125,7 +132,7 @@ __device__ __forceinline__ TileGeom tile_geom(const Geo& g, int32_t t) {
 __device__ __forceinline__ TileGeom tile_geom_grid(const Geo& g) {
     TileGeom tg;
     tg.tx = blockIdx.x;
-    tg.ty = blockIdx.y;
+    tg.ty = blockIdx.y + g.ty0;
     tg.b = blockIdx.z;
     tg.t = (tg.b * g.nty + tg.ty) * g.ntx + tg.tx;
     tg.x0 = tg.tx * TW;

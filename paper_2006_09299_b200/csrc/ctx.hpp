@@ -1,0 +1,128 @@
+// ctx.hpp -- the host-side context (rl_ctx) and helpers shared by api.cu (single-GPU calls)
+// and strips.cu (one image split into horizontal strips across ranks).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "common.cuh"
+#include "runlab_gpu.h"
+
+namespace rlg {
+size_t analyze_smem();
+size_t emit_smem();
+cudaError_t configure_kernels();
+void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s);
+void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms);
+void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
+void launch_resolve(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
+void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
+void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
+void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
+void launch_tree_parts(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
+void launch_fold(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
+void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s);
+void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
+                       cudaStream_t s, int sms);
+void launch_compact_filled(const Acc* filled, const uint32_t* flag, const uint32_t* rank, const uint64_t* total_p,
+                           uint64_t cap, Acc* out, cudaStream_t s, int sms);
+void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, const uint64_t* cbase, uint64_t cap,
+                  cudaStream_t s, int sms);
+}  // namespace rlg
+
+
+namespace rlh {
+using namespace rlg;
+
+struct StripState;  // strips.cu
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+// Everything a captured pipeline depends on (compared bytewise before a replay).
+struct GraphKey {
+    Geo g;
+    Ws ws;
+    rl_config cfg;
+    const void* pix;
+    cudaStream_t stream;
+    const void* summ;
+    const void* rank;
+    const void* flag;
+    const void* fcomp;
+    uint64_t cap_comps;
+    int compact;
+};
+
+
+}  // namespace rlh
+
+struct rl_ctx {
+    using DevBuf = rlh::DevBuf;
+    using GraphKey = rlh::GraphKey;
+    using Geo = rlg::Geo;
+    using Ws = rlg::Ws;
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // events of the current call
+    static constexpr int RING = 64;
+    cudaEvent_t ring[RING][4] = {};
+    int64_t calls = 0;
+    // workspace
+    DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
+    DevBuf cnt, off, counters, img_fg, img_surv, comps, top, filled, filled_img, labels, pix;
+    DevBuf cub_tmp, cbase, summ, rank, flag, ovf, ovf2, thdr, tmap, rstore, rused, fcomp;
+    uint32_t cap_nodes = 0;
+    uint64_t cap_comps = 0;
+    uint64_t cap_rstore = 0;
+    // pinned host mirror of the summary
+    int64_t* h_summ = nullptr;
+    size_t h_summ_n = 0;
+    // last call
+    Geo geo{};
+    Ws ws{};
+    rl_config cfg{};
+    const uint8_t* last_pix = nullptr;
+    int launches = 0;
+    bool have_result = false;
+    bool reran = false;  // finish() had to grow a capacity and re-run
+    // CUDA graph of the last small pipeline
+    bool graphs = true;
+    bool used_graph = false;
+    cudaGraphExec_t gexec = nullptr;
+    GraphKey gkey{};
+    cudaEvent_t gev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // post-fill features of the survivors compacted into `fcomp` (rl_label_into layout 1)
+    bool want_compact = false;
+    int64_t chunk_px = 32ll << 20;  // rl_label_into: pixels per chunk (env RUNLAB_GPU_CHUNK_PX)
+    // rl_label_into pipelines large batches through these (own workspace and stream each)
+    static constexpr int NKIDS = 3;
+    rl_ctx* kids[NKIDS] = {};
+    // strip mode (strips.cu)
+    DevBuf nleft, scount;
+    rlh::StripState* strip = nullptr;
+};
+
+namespace rlh {
+using namespace rlg;
+int set_err(rl_ctx* c, int code, const std::string& msg);
+int cuda_fail(rl_ctx* c, cudaError_t e, const char* what);
+bool ensure(DevBuf& b, size_t bytes);
+template <class T>
+T* P(DevBuf& b) {
+    return static_cast<T*>(b.p);
+}
+int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cfg);
+// Geometry of a batch of n w x h images (all tile rows, no strip offset).
+Geo make_geo(int32_t w, int32_t h, int32_t n, const rl_config* cfg, const void* dpix);
+// Grow the workspace for geometry g and fill `ws`; `scan_tmp` = CUB temp bytes of the cnt scan.
+// `out_px` = pixels of the filled/label image buffers.
+int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& scan_tmp, int64_t out_px);
+void strip_free(rl_ctx* c);
+}  // namespace rlh

@@ -26,13 +26,14 @@ __host__ __device__ __forceinline__ uint64_t block_draw(uint64_t seed, uint64_t 
 }
 
 // one thread per 16 pixels of a row (16-byte stores when the row is aligned)
+// rows [y0, y0 + h) of the image (out holds just those rows)
 __global__ void k_generate(uint8_t* out, int32_t w, int32_t h, int32_t g, uint64_t seed, uint64_t thr,
-                           int always) {
+                           int always, int32_t y0) {
     const int32_t vpr = (w + 15) / 16;
     const int64_t total = (int64_t)vpr * h;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t y = (int32_t)(i / vpr);
+        const int32_t yo = (int32_t)(i / vpr), y = y0 + yo;
         const int32_t x0 = (int32_t)(i % vpr) * 16;
         const uint64_t sr = sm_step(sm_step(seed) ^ (uint64_t)(y / g));
         uint8_t v[16];
@@ -48,7 +49,7 @@ __global__ void k_generate(uint8_t* out, int32_t w, int32_t h, int32_t g, uint64
             }
             v[k] = x < w ? last : 0;
         }
-        uint8_t* dst = out + (int64_t)y * w + x0;
+        uint8_t* dst = out + (int64_t)yo * w + x0;
         if ((w % 16) == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0) {
             uint4 q;
             q.x = v[0] | (v[1] << 8) | (v[2] << 16) | ((uint32_t)v[3] << 24);
@@ -107,18 +108,23 @@ int grid_of(int64_t n) {
 extern "C" {
 
 // generator.hpp:46-83 on the device; d_out holds w*h bytes; stream = cudaStream_t or NULL
-int rl_generate(void* stream, uint8_t* d_out, int32_t w, int32_t h, double density, int32_t g, uint64_t seed) {
-    if (w < 1 || h < 1) return RL_EINVAL;
+int rl_generate_rows(void* stream, uint8_t* d_out, int32_t w, int32_t h, int32_t y0, int32_t rows, double density,
+                     int32_t g, uint64_t seed) {
+    if (w < 1 || h < 1 || y0 < 0 || rows < 1 || y0 + rows > h) return RL_EINVAL;
     if (density < 0.0 || density > 1.0) return RL_EINVAL;
     if (g < 1 || g > (w < h ? w : h)) return RL_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
-    if (density <= 0.0) return cudaMemsetAsync(d_out, 0, (size_t)w * h, s) == cudaSuccess ? RL_OK : RL_ECUDA;
+    if (density <= 0.0) return cudaMemsetAsync(d_out, 0, (size_t)w * rows, s) == cudaSuccess ? RL_OK : RL_ECUDA;
     const double scaled = density * 18446744073709551616.0;
     const int always = scaled >= 18446744073709551616.0;
     const uint64_t thr = always ? 0 : (uint64_t)scaled;
-    const int64_t n = (int64_t)((w + 15) / 16) * h;
-    k_generate<<<grid_of(n), 256, 0, s>>>(d_out, w, h, g, seed, thr, always);
+    const int64_t n = (int64_t)((w + 15) / 16) * rows;
+    k_generate<<<grid_of(n), 256, 0, s>>>(d_out, w, rows, g, seed, thr, always, y0);
     return cudaGetLastError() == cudaSuccess ? RL_OK : RL_ECUDA;
+}
+
+int rl_generate(void* stream, uint8_t* d_out, int32_t w, int32_t h, double density, int32_t g, uint64_t seed) {
+    return rl_generate_rows(stream, d_out, w, h, 0, h, density, g, seed);
 }
 
 int rl_generate_rings(void* stream, uint8_t* d_out, int32_t w, int32_t h, int32_t tile, uint64_t seed,

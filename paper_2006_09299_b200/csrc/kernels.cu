@@ -58,7 +58,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         } else {
             uint32_t bits = 0;
             if (vm) {
-                const uint8_t* src = pix + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
+                const uint8_t* src = pix + (int64_t)tg.b * g.P + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
                 if (g.vec_ok && vm == 0xFFFFFFFFu) {
                     const uint4* s4 = reinterpret_cast<const uint4*>(src);
                     const uint4 v0 = __ldcs(s4), v1 = __ldcs(s4 + 1);
@@ -333,17 +333,18 @@ __device__ __forceinline__ uint32_t node_of(const Ws& ws, const Geo& g, int64_t 
     return (uint32_t)g.B + ws.tbase[t] + (lab & 0x7FFFu);
 }
 
-// horizontal seams: between band s and s+1, one thread per image column
-__global__ void k_seam_h(Geo g, Ws ws) {
+// horizontal seams s0 .. s0+ns-1 (seam s lies between tile rows s and s+1), one thread per
+// image column
+__global__ void k_seam_h(Geo g, Ws ws, int32_t s0, int32_t ns) {
     if (ws.counters[1]) return;
-    const int64_t nseam = (int64_t)g.B * (g.nty - 1) * g.W;
+    const int64_t nseam = (int64_t)g.B * ns * g.W;
     const uint32_t v8 = g.flip ? 0u : 1u;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseam;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t x = (int32_t)(i % g.W);
         const int64_t bs = i / g.W;
-        const int32_t s = (int32_t)(bs % (g.nty - 1));
-        const int32_t b = (int32_t)(bs / (g.nty - 1));
+        const int32_t s = s0 + (int32_t)(bs % ns);
+        const int32_t b = (int32_t)(bs / ns);
         const int32_t tx = x / TW, c = x % TW;
         const int64_t tu = ((int64_t)b * g.nty + s) * g.ntx + tx, tl = tu + g.ntx;
         const uint16_t lu = ws.perim[tu * PERIM + TW + c], ld = ws.perim[tl * PERIM + c];
@@ -373,10 +374,12 @@ __global__ void k_seam_h(Geo g, Ws ws) {
     }
 }
 
-// vertical seams: between tile column s-1 and s, one thread per tile row
+// vertical seams: between tile column s-1 and s, one thread per pixel row of tile rows
+// [ty0, ty1)
 __global__ void k_seam_v(Geo g, Ws ws) {
     if (ws.counters[1]) return;
-    const int64_t nseam = (int64_t)g.B * g.nty * (g.ntx - 1) * TH;
+    const int32_t nrows = g.ty1 - g.ty0;
+    const int64_t nseam = (int64_t)g.B * nrows * (g.ntx - 1) * TH;
     const uint32_t v8 = g.flip ? 0u : 1u;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseam;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -384,8 +387,8 @@ __global__ void k_seam_v(Geo g, Ws ws) {
         int64_t q = i / TH;
         const int32_t s = 1 + (int32_t)(q % (g.ntx - 1));
         q /= (g.ntx - 1);
-        const int32_t ty = (int32_t)(q % g.nty);
-        const int32_t b = (int32_t)(q / g.nty);
+        const int32_t ty = g.ty0 + (int32_t)(q % nrows);
+        const int32_t b = (int32_t)(q / nrows);
         const int32_t th = min(TH, g.H - ty * TH);
         if (r >= th) continue;
         const int64_t tR = ((int64_t)b * g.nty + ty) * g.ntx + s, tL = tR - 1;
@@ -554,7 +557,9 @@ __global__ void k_parents(Geo g, Ws ws) {
         int32_t b, ty, tx;
         tile_of(g, rec.tile, b, ty, tx);
         uint32_t proot;
-        if (rec.leftkind == 0) {
+        if (ws.nleft) {  // strip mode: resolved before the exchange (k_strip_left)
+            proot = ws.uf[ws.nleft[n]];
+        } else if (rec.leftkind == 0) {
             proot = ws.uf[(uint32_t)g.B + ws.tbase[rec.tile] + rec.left];
         } else if (rec.leftkind == 1) {
             const uint32_t tl = rec.tile - 1;
@@ -603,7 +608,9 @@ __global__ void k_tops(Geo g, Ws ws) {
         const uint32_t cid = ws.nrootcid[root];
         ws.top[cb + cid] = anc;
         if (cur == root) {
-            ws.filled[cb + cid] = ws.nacc[root];
+            // strip mode: this rank's partial sums start empty; the border part is added after
+            // the cross-rank reduction (strips.cu)
+            ws.filled[cb + cid] = g.strip ? acc_empty() : ws.nacc[root];
             // warp-aggregated survivor count (same image for most lanes)
             const uint32_t active = __activemask();
             const uint32_t same = __match_any_sync(active, b);
@@ -928,7 +935,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
     if (vm) {
         const uint32_t fillbits = vm & ~E.ext[tid];
-        uint8_t* dst = ws.filled_img + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + r) * g.W + tg.x0 + 32 * w;
+        uint8_t* dst = ws.filled_img + (int64_t)tg.b * g.P + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
         if (g.vec_ok && vm == 0xFFFFFFFFu) {
             uint4 o0, o1;
             o0.x = nibble_to_bytes(fillbits & 0xF);
@@ -963,7 +970,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
                 }
             }
             const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
-            uint32_t* ldst = ws.labels + (int64_t)tg.b * g.P + (int64_t)(tg.y0 + rr) * g.W + tg.x0;
+            uint32_t* ldst = ws.labels + (int64_t)tg.b * g.P + (tg.y0 + rr - g.prow0) * g.W + tg.x0;
             for (int j = c0; j < c1; ++j) ldst[j] = v;
         }
     }
@@ -1077,19 +1084,22 @@ static int grid_for(int64_t n, int block, int maxgrid) {
     return (int)gr;
 }
 
+void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms) {
+    const int64_t n = (int64_t)g.B * ns * g.W;
+    k_seam_h<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(g, ws, s0, ns);
+}
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
-    k_analyze<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
+    k_analyze<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
     // deferred heavier tiles: the grids loop over device-side lists (no host sync)
     k_analyze_m<<<148 * 3, CapM::BT, sizeof(AnalyzeSmem<CapM>), s>>>(pix, g, ws);
     k_analyze_full<<<148 * 2, CapF::BT, sizeof(AnalyzeSmem<CapF>), s>>>(pix, g, ws);
 }
+// seams inside tile rows [ty0, ty1)
 void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
-    if (g.nty > 1) {
-        const int64_t n = (int64_t)g.B * (g.nty - 1) * g.W;
-        k_seam_h<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(g, ws);
-    }
+    const int32_t rows = g.ty1 - g.ty0;
+    if (rows > 1) launch_seam_rows(g, ws, g.ty0, rows - 1, s, sms);
     if (g.ntx > 1) {
-        const int64_t n = (int64_t)g.B * g.nty * (g.ntx - 1) * TH;
+        const int64_t n = (int64_t)g.B * rows * (g.ntx - 1) * TH;
         k_seam_v<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(g, ws);
     }
 }
@@ -1108,8 +1118,17 @@ void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
     k_tops<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
     k_fold<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
 }
+void launch_tree_parts(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
+    const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;
+    k_parents<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
+    k_tops<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
+}
+void launch_fold(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
+    const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;
+    k_fold<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
+}
 void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s) {
-    k_emit<<<dim3(g.ntx, g.nty, g.B), NT, sizeof(EmitSmem<CapSE>), s>>>(g, ws);
+    k_emit<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(EmitSmem<CapSE>), s>>>(g, ws);
     k_emit_m<<<148 * 3, CapME::BT, sizeof(EmitSmem<CapME>), s>>>(g, ws);
     k_emit_full<<<148 * 2, CapFE::BT, sizeof(EmitSmem<CapFE>), s>>>(g, ws);
 }

@@ -418,6 +418,15 @@ def generate_device(d_ptr: int, w: int, h: int, density: float, g: int, seed: in
         _raise(rc, "generate: invalid spec" if rc == N.RL_EINVAL else "generate failed")
 
 
+def generate_rows_device(d_ptr: int, w: int, h: int, y0: int, rows: int, density: float, g: int, seed: int,
+                         stream: int | None = None) -> None:
+    """Rows [y0, y0 + rows) of generate(w, h, density, g, seed) on the device (one strip)."""
+    rc = N.load().rl_generate_rows(C.c_void_p(stream or 0), C.c_void_p(d_ptr), w, h, y0, rows, float(density),
+                                   g, seed)
+    if rc != N.RL_OK:
+        raise ValueError("rl_generate_rows: invalid arguments")
+
+
 def generate_rings_device(d_ptr: int, w: int, h: int, tile: int = 64, seed: int = 3,
                           salt: float = 0.02, stream: int | None = None) -> None:
     """Config-3 nested-ring image on the device."""

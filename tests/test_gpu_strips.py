@@ -1,0 +1,128 @@
+"""§8(e): one image cut into horizontal strips, each strip on its own context, against the
+single-image pipeline (which the other GPU tests pin to the oracle) -- bit-exact tables, filled
+image and labels, for several strip counts, ragged last strips, both connectivities, nested
+holes spanning cuts and a percolating noise image."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2006_09299_b200 import Labeler, LabelingConfig
+from paper_2006_09299_b200.runlab import generate_device, generate_rings_device
+from paper_2006_09299_b200.strips import concat, label_strips_in_process, strip_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def labelers():
+    labs = [Labeler(0) for _ in range(8)]
+    yield labs
+    for lab in labs:
+        lab.close()
+
+
+def _compare(got: dict, ref, label: str):
+    im = ref.image(0)
+    assert got["n_components"] == im["n_components"], label
+    assert got["n_fg"] == im["n_fg"], label
+    assert got["n_holes"] == im["n_holes"], label
+    assert got["euler"] == im["euler"], label
+    assert got["n_survivors"] == im["n_survivors"], label
+    assert got["comps"].shape[0] == im["n_components"], label
+    bad = np.nonzero(got["comps"] != im["comps"])[0]
+    assert bad.size == 0, f"{label}: comps differ at {bad[:10]}"
+    np.testing.assert_array_equal(got["top"], im["top"], err_msg=label)
+    surv = im["top"] == np.arange(im["n_components"], dtype=np.uint32)
+    assert got["filled"][surv].tobytes() == im["filled"][surv].tobytes(), label
+    np.testing.assert_array_equal(got["filled_image"], im["filled_image"], err_msg=label)
+    if "labels" in got:
+        np.testing.assert_array_equal(got["labels"], im["labels"], err_msg=label)
+
+
+def _run(labelers, img_dev, W, H, n, cfg):
+    rows = strip_rows(H, n)
+    ptrs = [img_dev.data_ptr() + y0 * W for (y0, _) in rows]
+    return concat(label_strips_in_process(labelers[:n], ptrs, W, H, rows, cfg))
+
+
+CASES = [(0.5, 1), (0.45, 4), (0.3, 2), (0.7, 1), (0.6, 8), (0.05, 1), (0.95, 1)]
+
+
+@pytest.mark.parametrize("d,g", CASES)
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_strips_match_single_image(labelers, labeler, d, g, n):
+    W, H = 1536, 1000  # ragged last strip, 6 tile columns
+    img = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    generate_device(img.data_ptr(), W, H, d, g, 7)
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    ref = labeler.label_batch(img.cpu().numpy()[None], cfg)
+    _compare(_run(labelers, img, W, H, n, cfg), ref, f"d={d} g={g} n={n}")
+
+
+@pytest.mark.parametrize("conn", [0, 1])
+def test_strips_rings_and_labels(labelers, labeler, conn):
+    W = H = 1024
+    img = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    generate_rings_device(img.data_ptr(), W, H, 64, 3, 0.02)
+    cfg = LabelingConfig(connectivity=conn, compute_features=True, compute_euler=True, fill_holes=True,
+                         relabel=True)
+    ref = labeler.label_batch(img.cpu().numpy()[None], cfg)
+    _compare(_run(labelers, img, W, H, 4, cfg), ref, f"rings conn={conn}")
+
+
+def test_strips_nested_shapes_across_cuts(labelers, labeler):
+    """Concentric square rings centred on a cut: every ring, hole and the fill cross strips."""
+    W, H = 512, 256
+    img = np.zeros((H, W), dtype=np.uint8)
+    for k in range(0, 60, 3):
+        img[128 - 100 + k:128 + 100 - k, 256 - 200 + 2 * k:256 + 200 - 2 * k] = (k // 3) % 2 == 0
+    img[0, :] = 1  # a component touching the top frame only
+    img[:, 0] = 0
+    dev = torch.from_numpy(img).cuda()
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True, relabel=True)
+    ref = labeler.label_batch(img[None], cfg)
+    for n in (2, 4, 8):
+        _compare(_run(labelers, dev, W, H, n, cfg), ref, f"nested n={n}")
+
+
+def test_strips_uniform_images(labelers, labeler):
+    W, H = 300, 200
+    for v in (0, 1):
+        img = np.full((H, W), v, dtype=np.uint8)
+        dev = torch.from_numpy(img).cuda()
+        cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True, relabel=True)
+        ref = labeler.label_batch(img[None], cfg)
+        _compare(_run(labelers, dev, W, H, 3, cfg), ref, f"uniform {v}")
+
+
+def test_strips_against_oracle(labelers):
+    W, H = 777, 300
+    img = O.generate(W, H, 0.55, 1, 3)
+    dev = torch.from_numpy(img).cuda()
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    got = _run(labelers, dev, W, H, 4, cfg)
+    want = O.label_canonical(img, 0)
+    assert got["n_components"] == want.n_components
+    assert got["comps"].tobytes() == want.comps.tobytes()
+    np.testing.assert_array_equal(got["filled_image"], want.filled_image)
+
+
+def test_strips_reject_densify(labelers):
+    img = torch.zeros((64, 64), dtype=torch.uint8, device="cuda")
+    cfg = LabelingConfig(relabel=True, densify_labels=True, fill_holes=True)
+    with pytest.raises(ValueError):
+        _run(labelers, img, 64, 64, 2, cfg)
+
+
+def test_generate_rows_matches_full():
+    from paper_2006_09299_b200.runlab import generate_rows_device
+    W, H = 1000, 700
+    full = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    generate_device(full.data_ptr(), W, H, 0.45, 4, 5)
+    for y0, h in strip_rows(H, 3):
+        part = torch.empty((h, W), dtype=torch.uint8, device="cuda")
+        generate_rows_device(part.data_ptr(), W, H, y0, h, 0.45, 4, 5)
+        assert torch.equal(part, full[y0:y0 + h])

@@ -139,3 +139,60 @@ def test_multirank_reductions_gloo():
     res = sorted(q.get(timeout=10) for _ in procs)
     assert [r[1] for r in res] == [2.0, 2.0]
     assert [r[2] for r in res] == [105, 105]
+
+
+def test_strip_rows():
+    from paper_2006_09299_b200.strips import strip_rows
+    for H in (32, 33, 1000, 1024, 32768):
+        for n in (1, 2, 3, 5, 8):
+            if n > (H + 31) // 32:
+                with pytest.raises(ValueError):
+                    strip_rows(H, n)
+                continue
+            rows = strip_rows(H, n)
+            assert len(rows) == n
+            assert rows[0][0] == 0 and sum(h for _, h in rows) == H
+            for (y0, h), (y1, _) in zip(rows, rows[1:]):
+                assert y0 % 32 == 0 and h % 32 == 0 and y0 + h == y1
+
+
+def _strip_coll_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2006_09299_b200.strips import TorchCollectives, _maxima
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    coll = TorchCollectives()
+    infos = coll.gather_infos(np.array([10 + rank, 3 * rank, 4 * rank, 4 * rank + 4], dtype=np.int64), "cpu")
+    rec = torch.full((16,), rank + 1, dtype=torch.uint8)
+    gathered = coll.gather_records(rec)
+    psum = torch.tensor([rank + 1] * 3, dtype=torch.int64)
+    pmin = torch.tensor([5 - rank, 7 + rank], dtype=torch.int32)
+    pmax = torch.tensor([5 - rank, 7 + rank], dtype=torch.int32)
+    pcnt = torch.tensor([2 * rank + 1], dtype=torch.int64)
+    coll.reduce_partials(psum, pmin, pmax, pcnt)
+    dist.destroy_process_group()
+    q.put((rank, infos.tolist(), _maxima(infos), gathered.tolist(), psum.tolist(), pmin.tolist(),
+           pmax.tolist(), pcnt.tolist()))
+
+
+def test_strip_collectives_gloo():
+    """world_size-2 gloo run of the strip exchange's three collectives (host side of §8(e))."""
+    import multiprocessing as mp
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_strip_coll_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = sorted(q.get(timeout=10) for _ in procs)
+    for _, infos, mx, gathered, psum, pmin, pmax, pcnt in res:
+        assert infos == [[10, 0, 0, 4], [11, 3, 4, 8]]
+        assert mx == (11, 4)
+        assert gathered == [1] * 16 + [2] * 16
+        assert psum == [3, 3, 3] and pmin == [4, 7] and pmax == [5, 8] and pcnt == [4]
