@@ -227,6 +227,21 @@ int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out);
 /* comps/top/filled (layout 0) of [comp_lo, comp_hi), filled_image/labels of the strip's rows */
 int rl_strip_fetch(rl_ctx* ctx, const rl_strip_result* r, rl_host_outputs* out);
 
+/* Connected-operator filtering (analysis.hpp:89-125 filter_components) of one image's canonical
+ * pre-fill table d_comps[n] (device): every component with d_selected[id] != 0 merges, with
+ * everything embedded in it, into its surrounding component.  Outputs (device, n each):
+ * d_parent = absorbing survivor or the id itself (the filtered equivalence table),
+ * d_features = survivors accumulate the features they absorb (merged ones keep their own),
+ * d_adjacency = surrounding component of each component, redirected to its survivor for the
+ * components that survive (UINT32_MAX for the exterior).  The predicate of the reference is a
+ * selection mask here (computed by the caller, e.g. from the features on the device).
+ * RL_EINVAL if the exterior (id 0) is selected.  Synchronous on `stream`. */
+int rl_filter_components(void* stream, const rl_component* d_comps, int64_t n, const uint8_t* d_selected,
+                         uint32_t* d_parent, rl_features* d_features, uint32_t* d_adjacency);
+/* The same with host buffers (copies in and out; used by include/runlab_gpu.hpp). */
+int rl_filter_components_host(const rl_component* comps, int64_t n, const uint8_t* selected, uint32_t* parent,
+                              rl_features* features, uint32_t* adjacency);
+
 /* Tile geometry used by the kernels (for DESIGN/roofline bookkeeping). */
 void rl_tile_shape(int32_t* tile_h, int32_t* tile_w);
 

@@ -324,4 +324,43 @@ inline std::int64_t euler_number(const LabelingResult& res) {
     return *res.euler;
 }
 
+// analysis.hpp:89-125 filter_components, run on the GPU (rl_filter_components_host): every
+// component selected by the predicate merges, with what is embedded in it, into its
+// surrounding component.  The predicate is evaluated here, per record.  The GPU path takes
+// results labeled without fill_holes (every component is then a root of the table).
+template <class Predicate>
+inline LabelingResult filter_components(const LabelingResult& res, Predicate&& selected) {
+    const std::vector<ComponentRecord> recs = components(res);
+    if (selected(static_cast<const ComponentRecord&>(recs[0])))
+        throw std::invalid_argument("filter_components: predicate must not select the exterior");
+    const label_t n = res.equivalences.size();
+    if (static_cast<label_t>(recs.size()) != n)
+        throw std::logic_error("filter_components: the GPU path takes a result labeled without fill_holes");
+    std::vector<rl_component> comps(n);
+    std::vector<std::uint8_t> sel(n, 0);
+    for (const ComponentRecord& rec : recs) {
+        rl_component& c = comps[rec.root];
+        const FeatureAccumulator& f = rec.features;
+        c.f = rl_features{f.s, f.sx, f.sy, f.row_min, f.row_max, f.col_min, f.col_max};
+        c.parent = rec.root == 0 ? no_label : rec.parent_root;
+        c.flags = rec.foreground ? 1u : 0u;
+        sel[rec.root] = (rec.root != 0 && selected(static_cast<const ComponentRecord&>(rec))) ? 1 : 0;
+    }
+    std::vector<label_t> parent(n), adj(n);
+    std::vector<rl_features> feats(n);
+    const int rc = rl_filter_components_host(comps.data(), n, sel.data(), parent.data(), feats.data(), adj.data());
+    if (rc == RL_EINVAL) throw std::invalid_argument("filter_components: predicate must not select the exterior");
+    if (rc != RL_OK) throw std::runtime_error("filter_components: GPU call failed");
+    LabelingResult out = res;
+    out.labels.reset();
+    std::vector<std::uint8_t> fg(n);
+    for (label_t e = 0; e < n; ++e) fg[e] = res.equivalences.is_foreground(e) ? 1 : 0;
+    out.equivalences = EquivalenceTable(std::move(parent), std::move(fg));
+    adj[0] = no_label;
+    out.adjacency = AdjacencyTable(std::move(adj));
+    if (out.features)
+        for (label_t e = 0; e < n; ++e) (*out.features)[e] = gpu::to_acc(feats[e]);
+    return out;
+}
+
 }  // namespace runlab

@@ -103,6 +103,8 @@ def lib():
         L.orc_bitquad_euler.restype = C.c_int64
         L.orc_bitquad_euler.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int]
         L.orc_fill_holes.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int, C.c_void_p]
+        L.orc_filter_components.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_void_p]
         _lib = L
     return _lib
 
@@ -130,6 +132,8 @@ def ref():
         L.ref_flood_label.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int, C.c_void_p]
         L.ref_bitquad_euler.restype = C.c_int64
         L.ref_bitquad_euler.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int]
+        L.ref_filter_components.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int, C.c_void_p,
+                                             C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_time_batch.restype = C.c_double
         L.ref_time_batch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int, C.c_int,
                                      C.POINTER(C.c_int64)]
@@ -238,3 +242,37 @@ def ref_time_batch(imgs: np.ndarray, conn: int = 0, threads: int = 1) -> tuple[f
     chk = C.c_int64()
     secs = ref().ref_time_batch(_ptr(imgs), w, h, n, conn, threads, C.byref(chk))
     return secs, chk.value
+
+
+def filter_components(comps: np.ndarray, selected: np.ndarray):
+    """C restatement of analysis.hpp:89-125 on a canonical pre-fill table.
+    Returns (parent, features, adjacency); raises ValueError if the exterior is selected."""
+    comps = np.ascontiguousarray(comps, dtype=COMPONENT_DTYPE)
+    sel = np.ascontiguousarray(selected, dtype=np.uint8)
+    n = comps.shape[0]
+    parent = np.empty(n, dtype=np.uint32)
+    feats = np.empty(n, dtype=FEATURE_DTYPE)
+    adj = np.empty(n, dtype=np.uint32)
+    rc = lib().orc_filter_components(_ptr(comps), n, _ptr(sel), _ptr(parent), _ptr(feats), _ptr(adj))
+    if rc == -1:
+        raise ValueError("filter_components: predicate must not select the exterior")
+    if rc != 0:
+        raise RuntimeError(f"orc_filter_components failed ({rc})")
+    return parent, feats, adj
+
+
+def ref_filter_components(img: np.ndarray, selected: np.ndarray, conn: int = 0):
+    """The reference's own filter_components on its label_image result, canonical ids."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    sel = np.ascontiguousarray(selected, dtype=np.uint8)
+    n = sel.shape[0]
+    h, w = img.shape
+    parent = np.empty(n, dtype=np.uint32)
+    feats = np.empty(n, dtype=FEATURE_DTYPE)
+    adj = np.empty(n, dtype=np.uint32)
+    rc = ref().ref_filter_components(_ptr(img), w, h, conn, _ptr(sel), n, _ptr(parent), _ptr(feats), _ptr(adj))
+    if rc == -1:
+        raise ValueError("filter_components: predicate must not select the exterior")
+    if rc != 0:
+        raise RuntimeError(f"ref_filter_components failed ({rc})")
+    return parent, feats, adj

@@ -203,4 +203,42 @@ double ref_time_batch(const std::uint8_t* px, std::int32_t w, std::int32_t h, st
     return secs;
 }
 
+// filter_components (analysis.hpp:89-125) run by the reference on its own label_image result
+// (features, no fill); `selected` is indexed by canonical id (ascending root order).  Outputs
+// in canonical ids like orc_filter_components.  Returns -1 when the reference throws
+// invalid_argument (exterior selected).
+int ref_filter_components(const std::uint8_t* px, std::int32_t w, std::int32_t h, int conn,
+                          const std::uint8_t* selected, std::int64_t n, std::uint32_t* parent_out,
+                          orc_features* features_out, std::uint32_t* adjacency_out) {
+    try {
+        const BinaryImage img = to_image(px, w, h);
+        LabelingConfig ca;
+        ca.connectivity = conn_of(conn);
+        ca.compute_features = true;
+        const LabelingResult a = label_image(img, ca);
+        const label_t ne = a.equivalences.size();
+        std::vector<std::uint32_t> cid(ne, no_label);
+        std::int64_t nc = 0;
+        for (label_t e = 0; e < ne; ++e)
+            if (a.equivalences.is_root(e)) cid[e] = static_cast<std::uint32_t>(nc++);
+        if (nc != n) return -3;
+        const LabelingResult f = filter_components(
+            a, [&](const ComponentRecord& rec) { return selected[cid[rec.root]] != 0; });
+        for (label_t e = 0; e < ne; ++e) {
+            if (!a.equivalences.is_root(e)) continue;
+            const std::uint32_t c = cid[e];
+            parent_out[c] = cid[f.equivalences.parent(e)];
+            features_out[c] = conv((*f.features)[e]);
+            adjacency_out[c] = e == 0 ? no_label : cid[f.adjacency[e]];
+        }
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    } catch (const std::overflow_error&) {
+        return -2;
+    } catch (const std::exception&) {
+        return -4;
+    }
+}
+
 }  // extern "C"

@@ -647,3 +647,43 @@ void orc_fill_holes(const uint8_t* img, int32_t w, int32_t h, int conn, uint8_t*
     for (int64_t i = 0; i < P; ++i) out[i] = comp[i] == 0 ? 0 : 1;
     free(comp);
 }
+
+/* analysis.hpp:89-125.  components() lists the roots in ascending order (analysis.hpp:23-41),
+ * so a parent is always decided before its children: target[c] = target[parent] when the
+ * parent merged (embedded in a merged region), else the parent when c itself is selected. */
+int orc_filter_components(const orc_component* comps, int64_t n, const uint8_t* selected, uint32_t* parent_out,
+                          orc_features* features_out, uint32_t* adjacency_out) {
+    const uint32_t NONE = UINT32_MAX;
+    if (n < 1) return 0;
+    if (selected[0]) return -1; /* analysis.hpp:92-94 */
+    uint32_t* target = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n);
+    if (!target) return -3;
+    for (int64_t c = 0; c < n; ++c) {
+        target[c] = NONE;
+        features_out[c] = comps[c].f;
+    }
+    for (int64_t c = 1; c < n; ++c) { /* analysis.hpp:100-111 */
+        const uint32_t p = comps[c].parent;
+        uint32_t tgt = NONE;
+        if (target[p] != NONE)
+            tgt = target[p];
+        else if (selected[c])
+            tgt = p;
+        if (tgt != NONE) {
+            target[c] = tgt;
+            if (merge_into(&features_out[tgt], &comps[c].f)) {
+                free(target);
+                return -2;
+            }
+        }
+    }
+    for (int64_t c = 0; c < n; ++c) /* analysis.hpp:113-116 */
+        parent_out[c] = target[c] != NONE ? target[c] : (uint32_t)c;
+    adjacency_out[0] = NONE;
+    for (int64_t c = 1; c < n; ++c) { /* analysis.hpp:117-121: only components still roots */
+        const uint32_t pr = comps[c].parent;
+        adjacency_out[c] = (target[c] == NONE && target[pr] != NONE) ? target[pr] : pr;
+    }
+    free(target);
+    return 0;
+}

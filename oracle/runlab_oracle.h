@@ -52,6 +52,16 @@ typedef struct orc_result {
     uint32_t* labels;     /* [w*h] canonical id per pixel (pre-fill), or NULL */
 } orc_result;
 
+/* analysis.hpp:89-125 filter_components on the canonical pre-fill table: every component
+ * whose selected[] flag is set merges (with the subtree embedded in it) into its surrounding
+ * component.  Outputs per component id: parent_out = absorbing survivor or itself (the
+ * equivalence table), features_out = post-filter features (survivors accumulate; merged
+ * components keep their own), adjacency_out = surrounding component redirected to its
+ * survivor (UINT32_MAX for the exterior).  Returns -1 if the exterior is selected
+ * (std::invalid_argument, analysis.hpp:92-94), -2 on feature overflow. */
+int orc_filter_components(const orc_component* comps, int64_t n, const uint8_t* selected, uint32_t* parent_out,
+                          orc_features* features_out, uint32_t* adjacency_out);
+
 /* generator.hpp:28-41 / :46-83 */
 uint64_t orc_block_draw(uint64_t seed, uint64_t block_row, uint64_t block_col);
 int orc_generate(int32_t w, int32_t h, double density, int32_t g, uint64_t seed, uint8_t* out);

@@ -21,7 +21,8 @@ EXPORTED_SYMBOLS = (
     "rl_stream", "rl_set_stream", "rl_last_launch_count", "rl_tile_shape", "rl_label_into",
     "rl_phase_times", "rl_generate", "rl_generate_rings", "rl_cfg4_params", "rl_last_used_graph",
     "rl_strip_local", "rl_strip_export_bytes", "rl_strip_export", "rl_strip_merge", "rl_strip_finish",
-    "rl_strip_fetch", "rl_generate_rows",
+    "rl_strip_fetch", "rl_generate_rows", "rl_filter_components",
+    "rl_filter_components_host",
 )
 
 FEATURE_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),
@@ -110,6 +111,8 @@ def load() -> C.CDLL:
     L.rl_phase_times.argtypes = [C.c_void_p, C.c_int, C.POINTER(RlTimes)]
     L.rl_generate.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_int32,
                               C.c_uint64]
+    L.rl_filter_components.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p]
     L.rl_generate_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                    C.c_double, C.c_int32, C.c_uint64]
     L.rl_generate_rings.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,

@@ -418,6 +418,40 @@ def generate_device(d_ptr: int, w: int, h: int, density: float, g: int, seed: in
         _raise(rc, "generate: invalid spec" if rc == N.RL_EINVAL else "generate failed")
 
 
+def filter_components(comps, selected, stream: int | None = None):
+    """analysis.hpp:89-125 on one image's canonical component table (COMPONENT_DTYPE records,
+    host numpy or a CUDA uint8 tensor of n*48 bytes) with a selection mask (one flag per
+    component; the reference's predicate evaluated by the caller).  Returns host arrays
+    (parent, features, adjacency) -- see rl_filter_components.  ValueError if the exterior is
+    selected (std::invalid_argument in the reference)."""
+    import torch
+    if isinstance(comps, np.ndarray):
+        comps = np.ascontiguousarray(comps, dtype=N.COMPONENT_DTYPE)
+        n = comps.shape[0]
+        d_comps = torch.from_numpy(comps.view(np.uint8).reshape(-1)).cuda()
+    else:
+        d_comps = comps
+        n = d_comps.numel() // 48
+    sel = selected if isinstance(selected, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(selected, dtype=np.uint8))
+    d_sel = sel.to(device=d_comps.device, dtype=torch.uint8).contiguous()
+    if d_sel.numel() != n:
+        raise ValueError("selected must have one flag per component")
+    d_parent = torch.empty(n, dtype=torch.int32, device=d_comps.device)
+    d_feat = torch.empty(n * 40, dtype=torch.uint8, device=d_comps.device)
+    d_adj = torch.empty(n, dtype=torch.int32, device=d_comps.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(d_comps.device).cuda_stream
+    rc = N.load().rl_filter_components(C.c_void_p(stream), C.c_void_p(d_comps.data_ptr()), n,
+                                       C.c_void_p(d_sel.data_ptr()), C.c_void_p(d_parent.data_ptr()),
+                                       C.c_void_p(d_feat.data_ptr()), C.c_void_p(d_adj.data_ptr()))
+    if rc == N.RL_EINVAL:
+        raise ValueError("filter_components: predicate must not select the exterior")
+    if rc != N.RL_OK:
+        _raise(rc, "rl_filter_components failed")
+    return (d_parent.cpu().numpy().view(np.uint32), d_feat.cpu().numpy().view(N.FEATURE_DTYPE),
+            d_adj.cpu().numpy().view(np.uint32))
+
+
 def generate_rows_device(d_ptr: int, w: int, h: int, y0: int, rows: int, density: float, g: int, seed: int,
                          stream: int | None = None) -> None:
     """Rows [y0, y0 + rows) of generate(w, h, density, g, seed) on the device (one strip)."""

@@ -119,6 +119,26 @@ int main() {
         const LabelingResult res = label_image(img, cfg);
         CHECK(*res.fg_count == 2 && *res.euler == 2);
     }
+    // test_analysis.cpp:146-210: filtering the holes equals hole filling; exterior rejected
+    {
+        LabelingConfig cfg = full_config();
+        cfg.relabel = false;
+        const LabelingResult res = label_image(fig, cfg);
+        const LabelingResult f = filter_components(
+            res, [](const ComponentRecord& r) { return !r.foreground && r.root != 0; });
+        cfg.fill_holes = true;
+        const LabelingResult filled_res = label_image(fig, cfg);
+        CHECK(f.roots() == filled_res.roots());
+        for (label_t e : f.roots()) CHECK((*f.features)[e].s == (*filled_res.features)[e].s);
+        CHECK((*f.features)[1].s == 67 && !f.labels);
+        bool threw = false;
+        try {
+            filter_components(res, [](const ComponentRecord& r) { return r.root == 0; });
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
     // timed_label_image gives identical results (test_bench.cpp:31-60)
     {
         StepTimes t;
