@@ -40,6 +40,11 @@ extern "C" {
 #define RL_ENOMEM 5    /* std::bad_alloc */
 #define RL_EINTERNAL 6 /* std::runtime_error (invariant violated on device) */
 #define RL_ENOSPC 7    /* caller-provided output buffer too small (see comps_needed) */
+#define RL_EFORMAT 8   /* runlab::PbmParseError (io.hpp:16-23): byte offset in rl_pbm_info */
+
+/* pixel formats of the input batch and of the hole-filled image */
+#define RL_PIXELS_U8 0 /* one byte (0/1) per pixel, row-major (BinaryImage, image.hpp:14-43) */
+#define RL_PIXELS_P4 1 /* PBM P4 raster: rows of MSB-first bits padded to whole bytes (io.hpp:78-154) */
 
 /* types.hpp:18-21 */
 #define RL_FG8_BG4 0
@@ -153,6 +158,37 @@ typedef struct rl_host_outputs {
  * non-component outputs are still filled). */
 int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t width, int32_t height,
                   int32_t n_images, const rl_config* cfg, rl_host_outputs* out);
+
+/* The same with an explicit pixel format (RL_PIXELS_*) for the input and the filled image:
+ * with RL_PIXELS_P4 each image is height rows of ceil(width / 8) bytes, read and written by the
+ * tile kernels as bits (8x fewer bytes over PCIe and HBM); pad bits are ignored on input and
+ * zero on output like write_pbm. */
+int rl_label_device_fmt(rl_ctx* ctx, const uint8_t* d_pixels, int32_t width, int32_t height, int32_t n_images,
+                        const rl_config* cfg, int32_t pixel_format);
+int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t width, int32_t height, int32_t n_images,
+                      const rl_config* cfg, int32_t pixel_format, rl_host_outputs* out);
+
+/* ---- PBM files (io.hpp:74-154) ---------------------------------------------------------------
+ * rl_pbm_parse: header of a P1/P4 file with read_pbm's rules; RL_EFORMAT with the offending byte
+ * offset and message (PbmParseError) on malformed, truncated or oversized input.
+ * rl_fill_pbm: `runlab fill` (tools/runlab.cpp:128-137) as one call -- PBM bytes in, the
+ * hole-filled image out as a complete P4 file (write_pbm); the P4 raster is decoded and encoded
+ * by the tile kernels, P1 text is parsed on the host.  `extra` (optional) receives the other
+ * rl_label_into outputs (its filled_image is ignored).  RL_ENOSPC if out_cap is too small
+ * (*out_len = size needed). */
+typedef struct rl_pbm_info {
+    int32_t width, height;
+    int32_t format;        /* 1 (P1) or 4 (P4) */
+    int32_t pad;
+    int64_t raster_offset; /* byte offset of the raster */
+    int64_t error_offset;  /* RL_EFORMAT: PbmParseError::byte_offset; else -1 */
+    char message[96];
+} rl_pbm_info;
+int rl_pbm_parse(const uint8_t* bytes, size_t len, rl_pbm_info* info);
+int rl_pbm_p1_to_p4(const uint8_t* bytes, size_t len, rl_pbm_info* info, uint8_t* p4_rows);
+size_t rl_pbm_p4_header(int32_t width, int32_t height, char* out, size_t cap);
+int rl_fill_pbm(rl_ctx* ctx, const uint8_t* pbm, size_t len, const rl_config* cfg, uint8_t* out_pbm,
+                size_t out_cap, size_t* out_len, rl_host_outputs* extra, rl_pbm_info* info);
 
 /* Per-phase device times of the call `back` calls ago (0 = last; back < 64). */
 int rl_phase_times(const rl_ctx* ctx, int back, rl_times* out);

@@ -134,6 +134,10 @@ def ref():
         L.ref_bitquad_euler.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int]
         L.ref_filter_components.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int, C.c_void_p,
                                              C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_read_pbm.argtypes = [C.c_char_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        L.ref_write_pbm.restype = C.c_int64
+        L.ref_write_pbm.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int, C.c_char_p, C.c_int64]
         L.ref_time_batch.restype = C.c_double
         L.ref_time_batch.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int, C.c_int,
                                      C.POINTER(C.c_int64)]
@@ -276,3 +280,23 @@ def ref_filter_components(img: np.ndarray, selected: np.ndarray, conn: int = 0):
     if rc != 0:
         raise RuntimeError(f"ref_filter_components failed ({rc})")
     return parent, feats, adj
+
+
+def ref_read_pbm(data: bytes):
+    """The reference's read_pbm: (pixels uint8 [h, w], None) or (None, PbmParseError offset)."""
+    w, h, off = C.c_int32(0), C.c_int32(0), C.c_int64(-1)
+    cap = max(64, len(data) * 8 + 64)
+    px = np.zeros(cap, dtype=np.uint8)
+    rc = ref().ref_read_pbm(data, len(data), _ptr(px), cap, C.byref(w), C.byref(h), C.byref(off))
+    if rc != 0:
+        return None, int(off.value)
+    return px[: w.value * h.value].reshape(h.value, w.value).copy(), None
+
+
+def ref_write_pbm(img: np.ndarray, p1: bool = False) -> bytes:
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    h, w = img.shape
+    n = ref().ref_write_pbm(_ptr(img), w, h, int(p1), None, 0)
+    out = C.create_string_buffer(n)
+    ref().ref_write_pbm(_ptr(img), w, h, int(p1), out, n)
+    return out.raw[:n]

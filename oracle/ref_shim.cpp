@@ -241,4 +241,28 @@ int ref_filter_components(const std::uint8_t* px, std::int32_t w, std::int32_t h
     }
 }
 
+// read_pbm (io.hpp:74-124): 0 and the pixels, or -1 and PbmParseError::byte_offset
+int ref_read_pbm(const char* bytes, std::int64_t len, std::uint8_t* pixels, std::int64_t cap, std::int32_t* w,
+                 std::int32_t* h, std::int64_t* err_offset) {
+    try {
+        const BinaryImage img = read_pbm(std::string_view(bytes, static_cast<std::size_t>(len)));
+        *w = img.width;
+        *h = img.height;
+        if (static_cast<std::int64_t>(img.pixels.size()) <= cap)
+            std::memcpy(pixels, img.pixels.data(), img.pixels.size());
+        return 0;
+    } catch (const PbmParseError& e) {
+        *err_offset = static_cast<std::int64_t>(e.byte_offset);
+        return -1;
+    }
+}
+
+// write_pbm (io.hpp:126-154): bytes of the file (P4 unless p1), copied when they fit
+std::int64_t ref_write_pbm(const std::uint8_t* px, std::int32_t w, std::int32_t h, int p1, char* out,
+                           std::int64_t cap) {
+    const std::string s = write_pbm(to_image(px, w, h), p1 ? PbmFormat::p1 : PbmFormat::p4);
+    if (static_cast<std::int64_t>(s.size()) <= cap) std::memcpy(out, s.data(), s.size());
+    return static_cast<std::int64_t>(s.size());
+}
+
 }  // extern "C"

@@ -13,7 +13,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RUNLAB_GPU_LIB", os.path.join(HERE, "librunlab_gpu.so"))
 
-RL_OK, RL_EINVAL, RL_ELOGIC, RL_EOVERFLOW, RL_ECUDA, RL_ENOMEM, RL_EINTERNAL = range(7)
+RL_OK, RL_EINVAL, RL_ELOGIC, RL_EOVERFLOW, RL_ECUDA, RL_ENOMEM, RL_EINTERNAL, RL_ENOSPC, RL_EFORMAT = range(9)
+RL_PIXELS_U8, RL_PIXELS_P4 = 0, 1
 
 EXPORTED_SYMBOLS = (
     "rl_create", "rl_destroy", "rl_last_error", "rl_label", "rl_result_free", "rl_label_device",
@@ -22,7 +23,8 @@ EXPORTED_SYMBOLS = (
     "rl_phase_times", "rl_generate", "rl_generate_rings", "rl_cfg4_params", "rl_last_used_graph",
     "rl_strip_local", "rl_strip_export_bytes", "rl_strip_export", "rl_strip_merge", "rl_strip_finish",
     "rl_strip_fetch", "rl_generate_rows", "rl_filter_components",
-    "rl_filter_components_host",
+    "rl_filter_components_host", "rl_label_device_fmt", "rl_label_into_fmt", "rl_pbm_parse", "rl_pbm_p1_to_p4",
+    "rl_pbm_p4_header", "rl_fill_pbm",
 )
 
 FEATURE_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),
@@ -57,6 +59,11 @@ class RlHostOutputs(C.Structure):
                 ("summary", C.c_void_p), ("comp_offset", C.c_void_p), ("comps_needed", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("filled_layout", C.c_int32),
                 ("reserved", C.c_int32)]
+
+
+class RlPbmInfo(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("format", C.c_int32), ("pad", C.c_int32),
+                ("raster_offset", C.c_int64), ("error_offset", C.c_int64), ("message", C.c_char * 96)]
 
 
 class RlStripLocalInfo(C.Structure):
@@ -113,6 +120,16 @@ def load() -> C.CDLL:
                               C.c_uint64]
     L.rl_filter_components.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p]
+    L.rl_label_device_fmt.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                      C.POINTER(RlConfig), C.c_int32]
+    L.rl_label_into_fmt.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                    C.POINTER(RlConfig), C.c_int32, C.POINTER(RlHostOutputs)]
+    L.rl_pbm_parse.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(RlPbmInfo)]
+    L.rl_pbm_p1_to_p4.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(RlPbmInfo), C.c_void_p]
+    L.rl_pbm_p4_header.restype = C.c_size_t
+    L.rl_pbm_p4_header.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.c_size_t]
+    L.rl_fill_pbm.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(RlConfig), C.c_void_p, C.c_size_t,
+                              C.POINTER(C.c_size_t), C.POINTER(RlHostOutputs), C.POINTER(RlPbmInfo)]
     L.rl_generate_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                    C.c_double, C.c_int32, C.c_uint64]
     L.rl_generate_rings.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,

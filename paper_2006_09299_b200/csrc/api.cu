@@ -17,6 +17,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "ctx.hpp"
@@ -94,7 +95,7 @@ int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cf
     return RL_OK;
 }
 
-Geo make_geo(int32_t W, int32_t H, int32_t B, const rl_config* cfg, const void* dpix) {
+Geo make_geo(int32_t W, int32_t H, int32_t B, const rl_config* cfg, const void* dpix, int32_t fmt) {
     Geo g{};
     g.W = W;
     g.H = H;
@@ -106,7 +107,11 @@ Geo make_geo(int32_t W, int32_t H, int32_t B, const rl_config* cfg, const void* 
     g.ntiles = ntiles >= (1ll << 31) ? -1 : (int32_t)ntiles;
     g.flip = cfg->connectivity == RL_FG4_BG8 ? 1 : 0;
     g.P = (int64_t)W * H;
-    g.vec_ok = ((W % 16) == 0 && (reinterpret_cast<uintptr_t>(dpix) % 16) == 0) ? 1 : 0;
+    g.fmt = fmt;
+    g.rowb = fmt == RL_PIXELS_P4 ? (W + 7) / 8 : W;
+    g.fbytes = (int64_t)g.rowb * H;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dpix);
+    g.vec_ok = fmt == RL_PIXELS_P4 ? ((g.rowb % 4) == 0 && (a % 4) == 0) : ((W % 16) == 0 && (a % 16) == 0);
     g.label_mode = cfg->relabel ? (cfg->fill_holes ? 2 : 1) : 0;
     g.ty0 = 0;
     g.ty1 = g.nty;
@@ -136,7 +141,7 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
               ensure(ctx->img_fg, (size_t)B * 4) && ensure(ctx->img_surv, (size_t)B * 4) &&
               ensure(ctx->comps, ctx->cap_comps * sizeof(rl_component)) &&
               ensure(ctx->top, ctx->cap_comps * 4) && ensure(ctx->filled, ctx->cap_comps * sizeof(Acc)) &&
-              ensure(ctx->filled_img, (size_t)out_px) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
+              ensure(ctx->filled_img, (size_t)(out_px / g.W) * g.rowb) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
               ensure(ctx->summ, (size_t)(B + 1) * 32);
     if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)out_px * 4);
     if (!ok) return set_err(ctx, RL_ENOMEM, "device allocation failed");
@@ -199,8 +204,8 @@ void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
 }
 
 // (Re)build geometry, grow the workspace, enqueue the pipeline.
-int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg) {
-    const Geo g = make_geo(W, H, B, cfg, dpix);
+int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg, int32_t fmt) {
+    const Geo g = make_geo(W, H, B, cfg, dpix, fmt);
     if (g.ntiles < 0) return set_err(ctx, RL_EINVAL, "too many tiles");
     const int64_t ncnt = (int64_t)B * H * g.ntx + 1;
     Ws ws;
@@ -363,7 +368,7 @@ int finish(rl_ctx* ctx) {
         if (!grow) return RL_OK;
         ctx->reran = true;
         const rl_config cfg = ctx->cfg;
-        const int rc = enqueue(ctx, ctx->last_pix, ctx->geo.W, ctx->geo.H, ctx->geo.B, &cfg);
+        const int rc = enqueue(ctx, ctx->last_pix, ctx->geo.W, ctx->geo.H, ctx->geo.B, &cfg, ctx->geo.fmt);
         if (rc) return rc;
     }
     return set_err(ctx, RL_EINTERNAL, "capacity did not converge");
@@ -421,19 +426,33 @@ int fetch(rl_ctx* ctx, rl_result* out) {
     cudaMemcpyAsync(out->comps, ctx->ws.comps, sizeof(rl_component) * total, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(out->top, ctx->ws.top, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(out->filled, ctx->ws.filled, sizeof(rl_features) * total, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
+    std::vector<uint8_t> p4;
+    if (g.fmt == RL_PIXELS_P4) {  // rl_result holds one byte per pixel: unpack the P4 rows
+        p4.resize((size_t)(g.fbytes * B));
+        cudaMemcpyAsync(p4.data(), ctx->ws.filled_img, p4.size(), cudaMemcpyDeviceToHost, st);
+    } else {
+        cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
+    }
     if (g.label_mode) cudaMemcpyAsync(out->labels, ctx->ws.labels, npx * 4, cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
         rl_result_free(out);
         return cuda_fail(ctx, e, "fetch");
     }
+    if (!p4.empty())
+        for (int64_t r = 0; r < (int64_t)g.H * B; ++r)
+            for (int32_t j = 0; j < g.W; ++j)
+                out->filled_image[r * g.W + j] = (p4[r * g.rowb + j / 8] >> (7 - j % 8)) & 1u;
     fill_times(ctx, &out->times);
     return RL_OK;
 }
 
 
 // ---- rl_label_into: chunked, pipelined host-buffer path
+
+int64_t image_bytes(int32_t w, int32_t h, int32_t fmt) {
+    return (int64_t)(fmt == RL_PIXELS_P4 ? (w + 7) / 8 : w) * h;
+}
 
 struct IntoState {
     int64_t total = 0;  // components of the chunks posted so far
@@ -446,20 +465,21 @@ void copy_fixed_outputs(rl_ctx* c, rl_host_outputs* out, int32_t b0) {
     const Geo& g = c->geo;
     const size_t npx = (size_t)(g.P * g.B), off = (size_t)g.P * b0;
     if (out->filled_image)
-        cudaMemcpyAsync(out->filled_image + off, c->ws.filled_img, npx, cudaMemcpyDeviceToHost, c->stream);
+        cudaMemcpyAsync(out->filled_image + (size_t)g.fbytes * b0, c->ws.filled_img, (size_t)g.fbytes * g.B,
+                        cudaMemcpyDeviceToHost, c->stream);
     if (out->labels && g.label_mode)
         cudaMemcpyAsync(out->labels + off, c->ws.labels, npx * 4, cudaMemcpyDeviceToHost, c->stream);
 }
 
 // H2D of images [b0, b0 + n), the pipeline, and the D2H of the outputs whose size is fixed
 int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
-                 rl_host_outputs* out, int32_t b0) {
-    const size_t npx = (size_t)w * h * n;
+                 rl_host_outputs* out, int32_t b0, int32_t fmt) {
+    const size_t npx = (size_t)image_bytes(w, h, fmt) * n;
     if (!ensure(c->pix, npx)) return set_err(c, RL_ENOMEM, "device allocation failed");
     const cudaError_t e = cudaMemcpyAsync(c->pix.p, pixels, npx, cudaMemcpyHostToDevice, c->stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "copy in");
     c->want_compact = out->filled && out->filled_layout == 1;
-    const int rc = enqueue(c, P<uint8_t>(c->pix), w, h, n, cfg);
+    const int rc = enqueue(c, P<uint8_t>(c->pix), w, h, n, cfg, fmt);
     if (rc) return rc;
     copy_fixed_outputs(c, out, b0);
     return RL_OK;
@@ -470,7 +490,7 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st) {
     const Geo& g = c->geo;
     const int B = g.B;
     if (c->reran) copy_fixed_outputs(c, out, b0);  // the pipeline re-ran after the first copies
-    if (out->filled_image) st.d2h += g.P * B;
+    if (out->filled_image) st.d2h += g.fbytes * B;
     if (out->labels && g.label_mode) st.d2h += g.P * B * 4;
     const int64_t* s = c->h_summ;
     const int64_t total = s[4 * B];
@@ -572,12 +592,19 @@ void rl_destroy(rl_ctx* c) {
 
 const char* rl_last_error(const rl_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
-int rl_label_device(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg) {
+int rl_label_device_fmt(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+                        int32_t pixel_format) {
     const int rc = check_args(ctx, w, h, n, cfg);
     if (rc) return rc;
+    if (pixel_format != RL_PIXELS_U8 && pixel_format != RL_PIXELS_P4)
+        return set_err(ctx, RL_EINVAL, "unknown pixel format");
     cudaSetDevice(ctx->device);
     ctx->want_compact = false;
-    return enqueue(ctx, d_pixels, w, h, n, cfg);
+    return enqueue(ctx, d_pixels, w, h, n, cfg, pixel_format);
+}
+
+int rl_label_device(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg) {
+    return rl_label_device_fmt(ctx, d_pixels, w, h, n, cfg, RL_PIXELS_U8);
 }
 
 int rl_sync(rl_ctx* ctx) {
@@ -605,19 +632,20 @@ int rl_label(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n
     cudaError_t e = cudaMemcpyAsync(ctx->pix.p, pixels, npx, cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "copy in");
     ctx->want_compact = false;
-    rc = enqueue(ctx, P<uint8_t>(ctx->pix), w, h, n, cfg);
+    rc = enqueue(ctx, P<uint8_t>(ctx->pix), w, h, n, cfg, RL_PIXELS_U8);
     if (rc) return rc;
     rc = finish(ctx);
     if (rc) return rc;
     return fetch(ctx, out);
 }
 
-int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
-                  rl_host_outputs* out) {
+int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+                      int32_t fmt, rl_host_outputs* out) {
     if (!out) return RL_EINVAL;
     out->comps_needed = 0;
     out->h2d_bytes = out->d2h_bytes = 0;
     if (out->filled_layout != 0 && out->filled_layout != 1) return set_err(ctx, RL_EINVAL, "unknown filled_layout");
+    if (fmt != RL_PIXELS_U8 && fmt != RL_PIXELS_P4) return set_err(ctx, RL_EINVAL, "unknown pixel format");
     int rc = check_args(ctx, w, h, n, cfg);
     if (rc) return rc;
     cudaSetDevice(ctx->device);
@@ -627,7 +655,7 @@ int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int3
     const int32_t nch = (n + per - 1) / per;
     IntoState st;
     if (nch == 1) {
-        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0);
+        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt);
         if (!rc) rc = finish(ctx);
         if (!rc) rc = into_post(ctx, out, 0, st);
         if (!rc) rc = into_sync(ctx);
@@ -654,7 +682,7 @@ int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int3
             if (rc) break;
             rl_ctx* k = ctx->kids[c % rl_ctx::NKIDS];
             const int32_t b0 = first_image(c);
-            rc = into_enqueue(k, pixels + (size_t)b0 * P, w, h, images(c), cfg, out, b0);
+            rc = into_enqueue(k, pixels + (size_t)b0 * image_bytes(w, h, fmt), w, h, images(c), cfg, out, b0, fmt);
             if (rc) rc = set_err(ctx, rc, k->err);
         }
         for (int32_t c = std::max(0, nch - rl_ctx::NKIDS); c < nch && !rc; ++c) rc = post(c);
@@ -663,10 +691,15 @@ int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int3
     }
     if (rc) return rc;
     out->comps_needed = st.total;
-    out->h2d_bytes = (int64_t)P * n;
+    out->h2d_bytes = image_bytes(w, h, fmt) * n;
     out->d2h_bytes = st.d2h;
     if (st.nospace) return set_err(ctx, RL_ENOSPC, "component buffers too small");
     return RL_OK;
+}
+
+int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+                  rl_host_outputs* out) {
+    return rl_label_into_fmt(ctx, pixels, w, h, n, cfg, RL_PIXELS_U8, out);
 }
 
 int rl_phase_times(const rl_ctx* ctx, int back, rl_times* out) {

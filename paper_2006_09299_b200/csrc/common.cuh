@@ -65,7 +65,12 @@ struct Geo {
     int32_t ty0, ty1;
     int64_t prow0;
     int32_t strip;       // 1: strip mode (border survivors' post-fill sums are completed later)
+    // pixel format of the input and of the hole-filled image: 0 = one byte per pixel,
+    // 1 = PBM P4 raster rows (MSB-first bits, rows padded to whole bytes, io.hpp:78-154)
+    int32_t fmt;
+    int32_t rowb;        // bytes per row of those buffers (W or ceil(W / 8))
     int32_t pad_;
+    int64_t fbytes;      // bytes per image of those buffers (rowb * H)
 };
 
 struct Ws {
@@ -187,6 +192,33 @@ __device__ __forceinline__ int block_reduce_sum(int v, int* wsum) {
     int t;
     block_excl_scan<BT>(v, wsum, t);
     return t;
+}
+
+// P4 rows hold pixels MSB-first; tile words are LSB-first.  Reversing the bits inside each
+// byte converts in both directions.
+__device__ __forceinline__ uint32_t p4_swizzle(uint32_t v) { return __byte_perm(__brev(v), 0, 0x0123); }
+
+// word w (pixels 32w .. 32w+31) of a P4 row; `aligned`: row start and row bytes multiples of 4
+__device__ __forceinline__ uint32_t p4_load_word(const uint8_t* row, int32_t rowb, int32_t w, bool aligned) {
+    const int32_t o = 4 * w;
+    if (aligned) return p4_swizzle(__ldcs(reinterpret_cast<const uint32_t*>(row + o)));
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (o + k < rowb) v |= (uint32_t)row[o + k] << (8 * k);
+    return p4_swizzle(v);
+}
+
+__device__ __forceinline__ void p4_store_word(uint8_t* row, int32_t rowb, int32_t w, uint32_t bits, bool aligned) {
+    const int32_t o = 4 * w;
+    const uint32_t v = p4_swizzle(bits);
+    if (aligned) {
+        __stcs(reinterpret_cast<uint32_t*>(row + o), v);
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (o + k < rowb) row[o + k] = (uint8_t)(v >> (8 * k));
 }
 
 // 4 mask bits -> 4 bytes of 0/1 (bit k -> byte k)

@@ -120,9 +120,10 @@ T* P(DevBuf& b) {
 }
 int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cfg);
 // Geometry of a batch of n w x h images (all tile rows, no strip offset).
-Geo make_geo(int32_t w, int32_t h, int32_t n, const rl_config* cfg, const void* dpix);
+Geo make_geo(int32_t w, int32_t h, int32_t n, const rl_config* cfg, const void* dpix, int32_t fmt = 0);
 // Grow the workspace for geometry g and fill `ws`; `scan_tmp` = CUB temp bytes of the cnt scan.
-// `out_px` = pixels of the filled/label image buffers.
+// `out_px` = pixels of the label image buffer; the filled image takes g.fbytes per image
+// (scaled to out_px / P images).
 int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& scan_tmp, int64_t out_px);
 void strip_free(rl_ctx* c);
 }  // namespace rlh

@@ -57,8 +57,11 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
             x = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
         } else {
             uint32_t bits = 0;
-            if (vm) {
-                const uint8_t* src = pix + (int64_t)tg.b * g.P + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
+            if (vm && g.fmt == 1) {
+                const uint8_t* row = pix + tg.b * g.fbytes + (tg.y0 + r - g.prow0) * (int64_t)g.rowb;
+                bits = p4_load_word(row, g.rowb, (tg.x0 >> 5) + w, g.vec_ok);
+            } else if (vm) {
+                const uint8_t* src = pix + tg.b * g.fbytes + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
                 if (g.vec_ok && vm == 0xFFFFFFFFu) {
                     const uint4* s4 = reinterpret_cast<const uint4*>(src);
                     const uint4 v0 = __ldcs(s4), v1 = __ldcs(s4 + 1);
@@ -933,9 +936,12 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     RL_PHASE(tg.t, 23);
 
     // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
-    if (vm) {
+    if (vm && g.fmt == 1) {
+        uint8_t* row = ws.filled_img + tg.b * g.fbytes + (tg.y0 + r - g.prow0) * (int64_t)g.rowb;
+        p4_store_word(row, g.rowb, (tg.x0 >> 5) + w, vm & ~E.ext[tid], g.vec_ok);
+    } else if (vm) {
         const uint32_t fillbits = vm & ~E.ext[tid];
-        uint8_t* dst = ws.filled_img + (int64_t)tg.b * g.P + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
+        uint8_t* dst = ws.filled_img + tg.b * g.fbytes + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
         if (g.vec_ok && vm == 0xFFFFFFFFu) {
             uint4 o0, o1;
             o0.x = nibble_to_bytes(fillbits & 0xF);

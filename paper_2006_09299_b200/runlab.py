@@ -141,6 +141,35 @@ class BatchResult:
                     labels=None if self.labels is None else self.labels[i])
 
 
+class PbmParseError(ValueError):
+    """runlab::PbmParseError (io.hpp:16-23): malformed PBM input at `byte_offset`."""
+
+    def __init__(self, msg: str, byte_offset: int):
+        super().__init__(msg)
+        self.byte_offset = byte_offset
+
+
+def read_pbm_header(data: bytes) -> N.RlPbmInfo:
+    """Header of a P1/P4 file with the reference's rules (raises PbmParseError)."""
+    info = N.RlPbmInfo()
+    buf = C.create_string_buffer(bytes(data), len(data))
+    rc = N.load().rl_pbm_parse(buf, len(data), C.byref(info))
+    if rc == N.RL_EFORMAT:
+        raise PbmParseError(info.message.decode(), int(info.error_offset))
+    if rc != N.RL_OK:
+        _raise(rc, "rl_pbm_parse failed")
+    return info
+
+
+def pack_p4(img: np.ndarray) -> np.ndarray:
+    """uint8 [..., h, w] 0/1 pixels -> P4 rows [..., h, ceil(w/8)] (MSB-first, zero pad bits)."""
+    return np.packbits(np.asarray(img, dtype=np.uint8) & 1, axis=-1)
+
+
+def unpack_p4(rows: np.ndarray, w: int) -> np.ndarray:
+    return np.unpackbits(rows, axis=-1)[..., :w]
+
+
 def _raise(code: int, msg: str):
     if code == N.RL_EINVAL:
         raise ValueError(msg)
@@ -202,12 +231,12 @@ class Labeler:
             self._L.rl_result_free(C.byref(res))
 
     def label_device(self, d_ptr: int, w: int, h: int, n: int, config: LabelingConfig,
-                     stream: int | None = None):
+                     stream: int | None = None, pixel_format: int = N.RL_PIXELS_U8):
         """Enqueue the pipeline on a device-resident batch (no host copies, no sync)."""
         if stream is not None:
             self._L.rl_set_stream(self._ctx, C.c_void_p(stream))
         cfg = config.to_c()
-        rc = self._L.rl_label_device(self._ctx, C.c_void_p(d_ptr), w, h, n, C.byref(cfg))
+        rc = self._L.rl_label_device_fmt(self._ctx, C.c_void_p(d_ptr), w, h, n, C.byref(cfg), pixel_format)
         if rc != N.RL_OK:
             _raise(rc, self._err())
 
@@ -227,14 +256,30 @@ class Labeler:
             self._L.rl_result_free(C.byref(res))
 
     def label_into(self, pixels_ptr: int, w: int, h: int, n: int, config: LabelingConfig,
-                   outs: N.RlHostOutputs) -> N.RlHostOutputs:
+                   outs: N.RlHostOutputs, pixel_format: int = N.RL_PIXELS_U8) -> N.RlHostOutputs:
         """rl_label_into: host pixels in, caller-owned host outputs (the e2e entry point)."""
         cfg = config.to_c()
-        rc = self._L.rl_label_into(self._ctx, C.c_void_p(pixels_ptr), w, h, n, C.byref(cfg),
-                                   C.byref(outs))
+        rc = self._L.rl_label_into_fmt(self._ctx, C.c_void_p(pixels_ptr), w, h, n, C.byref(cfg), pixel_format,
+                                       C.byref(outs))
         if rc != N.RL_OK:
             _raise(rc, self._err())
         return outs
+
+    def fill_pbm(self, data: bytes, config: LabelingConfig | None = None) -> bytes:
+        """`runlab fill`: PBM (P1/P4) bytes in, the hole-filled image as a P4 file out."""
+        config = config or LabelingConfig(fill_holes=True)
+        info = read_pbm_header(data)
+        cap = 64 + ((info.width + 7) // 8) * info.height
+        out = C.create_string_buffer(cap)
+        n = C.c_size_t(0)
+        src = C.create_string_buffer(bytes(data), len(data))
+        rc = self._L.rl_fill_pbm(self._ctx, src, len(data), C.byref(config.to_c()), out, cap, C.byref(n), None,
+                                 C.byref(info))
+        if rc == N.RL_EFORMAT:
+            raise PbmParseError(info.message.decode(), int(info.error_offset))
+        if rc != N.RL_OK:
+            _raise(rc, self._err())
+        return out.raw[: n.value]
 
     def phase_times(self, back: int = 0) -> StepTimes:
         t = N.RlTimes()
