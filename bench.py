@@ -478,6 +478,28 @@ def main() -> None:
                "api": "rl_label_into (pinned host pixels in; filled image, component records, "
                       "post-fill roots, survivors' post-fill features, per-image counts out; "
                       "chunks of whole images pipelined over 3 streams)"}
+        # the same call with PBM P4 rasters in and out (1 bit per pixel over PCIe, the
+        # reference CLI's file format): reported beside, not as the headline
+        from paper_2006_09299_b200.runlab import pack_p4
+        h_p4 = torch.from_numpy(pack_p4(h_in.numpy())).pin_memory()
+        h_fp4 = torch.empty_like(h_p4).pin_memory()
+        outs4 = N.RlHostOutputs(h_fp4.data_ptr(), None, h_comps.data_ptr(), h_top.data_ptr(),
+                                h_filled.data_ptr(), cap, h_summ.data_ptr(), h_off.data_ptr(), 0, 0, 0, 1, 0)
+        lab.label_into(h_p4.data_ptr(), wl.W, wl.H, B, cfg, outs4, pixel_format=N.RL_PIXELS_P4)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            lab.label_into(h_p4.data_ptr(), wl.W, wl.H, B, cfg, outs4, pixel_format=N.RL_PIXELS_P4)
+        p4_s = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([p4_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            p4_s = float(t.item())
+        assert np.array_equal(h_summ.numpy().reshape(B, 5)[:, 0], res.n_components), "e2e P4 result mismatch"
+        e2e["p4"] = {"value": total_px / p4_s / 1e9, "unit": "Gpixel/s", "ms_per_step": p4_s * 1e3,
+                     "h2d_bytes_per_step": int(outs4.h2d_bytes), "d2h_bytes_per_step": int(outs4.d2h_bytes),
+                     "api": "rl_label_into_fmt(RL_PIXELS_P4): P4 rows in, filled image as P4 rows out"}
 
     # ---- CPU baseline: the reference itself on a bounded sample, rank 0 at N=1 only
     cpu = None
