@@ -33,11 +33,11 @@ struct AnalyzeSmem {
     int32_t brmax[C::NBC], bcmin[C::NBC], bcmax[C::NBC];
     uint8_t bimg[C::NBC];  // touches the image border
     uint32_t base;
-    unsigned long long moff;
 };
 
-// Returns false when the tile exceeds the capacity class C (then nothing was written for it
-// except the packed bits; the caller defers it to the next class).
+// Returns false when the tile exceeds the capacity class C (then nothing but the packed bits and
+// possibly a partial component map -- superseded by the next class's -- was written for it; the
+// caller defers it to the next class).
 template <class C, bool RELOAD>
 __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* __restrict__ pix, const Geo& g,
                                              const Ws& ws, const TileGeom& tg) {
@@ -77,13 +77,6 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         S.x[tid] = x;
         S.vm[tid] = vm;
     }
-    for (int i = tid; i < C::NBC; i += BT) {
-        A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
-        A.brmax[i] = -1;
-        A.bcmin[i] = 0x7FFFFFFF;
-        A.bcmax[i] = -1;
-        A.bimg[i] = 0;
-    }
     if (tg.tx == 0 && tg.ty == 0 && tid == 0) {
         // exterior node of image b
         const uint32_t e = (uint32_t)tg.b;
@@ -98,7 +91,8 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     __syncthreads();
 
     RL_PHASE(tg.t, 1);
-    if (!ccl_tile(S, tg)) return false;
+    const MapOut mo{ws.rused, ws.rstore, ws.cap_rstore, ws.tmap, ws.counters + 1};
+    if (!ccl_tile(S, tg, mo)) return false;
 
     const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
     // the two allocations are issued by different warps so their latencies overlap
@@ -108,13 +102,6 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         if ((uint64_t)base + nb > ws.cap_nodes) atomicOr(&ws.counters[1], ERR_NODE_CAP);
         ws.tbase[tg.t] = base;
         ws.tnb[tg.t] = (uint32_t)nb;
-    }
-    if (tid == 32) {
-        const unsigned long long need = (unsigned long long)nruns + 2ull * (unsigned long long)nlc;
-        const unsigned long long off = atomicAdd(ws.rused, need);
-        A.moff = off;
-        if (off + need > ws.cap_rstore) atomicOr(&ws.counters[1], ERR_RSTORE_CAP);
-        ws.tmap[tg.t] = off;
     }
     // ---- tile header (run/component counts, row tables) for the emit pass
     {
@@ -130,20 +117,14 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
             hdr[4 + TH + 1 + tid] = S.rowbx[tid];
         }
     }
-    __syncthreads();
-    // ---- component map: component of every run, first run and border index of every component
-    {
-        const unsigned long long off = A.moff;
-        if (off + (unsigned long long)nruns + 2ull * nlc <= ws.cap_rstore) {
-            uint16_t* dst = ws.rstore + off;
-            for (int i = tid; i < nruns; i += BT) dst[i] = (uint16_t)lc_of_run(S, i);
-            for (int l = tid; l < nlc; l += BT) {
-                dst[nruns + l] = S.lcrun[l];
-                dst[nruns + nlc + l] = S.lcb[l];
-            }
-        }
+    for (int i = tid; i < nb; i += BT) {  // border-component accumulators
+        A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
+        A.brmax[i] = -1;
+        A.bcmin[i] = 0x7FFFFFFF;
+        A.bcmax[i] = -1;
+        A.bimg[i] = 0;
     }
-
+    __syncthreads();
     RL_PHASE(tg.t, 9);
     // ---- border-component features and image-border contact (one lane per run)
     const bool top_img = tg.ty == 0, bot_img = (tg.y0 + tg.th == g.H);
@@ -286,9 +267,9 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         nfg += (int)(xbit(S, lc_row(S, l), lc_col(S, l)) ^ (uint32_t)flip);
     }
     RL_PHASE(tg.t, 11);
-    nfg = block_reduce_sum<BT>(nfg, S.wsum);
+    nfg = __reduce_add_sync(0xFFFFFFFFu, nfg);
+    if ((tid & 31) == 0 && nfg) atomicAdd(&ws.img_fg[tg.b], (uint32_t)nfg);
     RL_PHASE(tg.t, 12);
-    if (tid == 0 && nfg) atomicAdd(&ws.img_fg[tg.b], (uint32_t)nfg);
     return true;
 }
 

@@ -98,6 +98,17 @@ struct CclSmem {
     int wsum[C::BT / 32 + 1];
     int qtot[NWARPS];          // union events queued by each word warp
     int nruns, nlc, nb;
+    unsigned long long moff;   // offset of the tile's component map in the map store
+};
+
+// Where the analyze pass stores the tile's component map for the emit pass (written while
+// the labels are resolved, so the map costs no extra pass over the runs).
+struct MapOut {
+    unsigned long long* used;  // map-store elements allocated (atomic bump)
+    uint16_t* store;
+    unsigned long long cap;
+    uint64_t* tile_off;        // [tile] offset of its map
+    uint32_t* err;             // error bits (ERR_RSTORE_CAP)
 };
 
 template <class SM>
@@ -243,7 +254,7 @@ __device__ __forceinline__ bool tile_runs(CclSmem<C>& S, WordBits& wb) {
 }
 
 template <class C>
-__device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
+__device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int r = tid / WPR, w = tid % WPR;
@@ -433,9 +444,18 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
         }
     }
     if (tid == 0) S.nlc = nlc;
+    if (tid == 32) {  // the map: component of each run, first run and border index of each component
+        const unsigned long long need = (unsigned long long)nruns + 2ull * (unsigned long long)nlc;
+        const unsigned long long off = atomicAdd(mo.used, need);
+        if (off + need > mo.cap) atomicOr(mo.err, ERR_RSTORE_CAP);
+        S.moff = off + need > mo.cap ? ~0ull : off;
+        mo.tile_off[tg.t] = off;
+    }
     if (tid >= tg.th && tid <= TH) S.rowlc[tid] = (uint16_t)nlc;  // rows without pixels
     __syncthreads();
     RL_PHASE(tg.t, 6);
+    const unsigned long long moff = S.moff;
+    uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
     // resolve non-root runs; mark components touching the tile border (plain stores of 1)
     for (int i = tid; i < nruns; i += BT) {
         uint32_t p = S.par[i];
@@ -443,6 +463,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
             p = S.par[p];
             S.par[i] = (uint16_t)p;
         }
+        if (map) map[i] = (uint16_t)(p & 0x7FFFu);
         const int rr = run_row(S, i), c0 = run_col(S, i);
         if (rr == 0 || rr == tg.th - 1 || c0 == 0 || run_end(S, i, tg.tw) == tg.tw)
             S.lcb[p & 0x7FFFu] = 1;
@@ -459,11 +480,17 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg) {
     int bx = block_excl_scan<BT>(cnt, S.wsum, nb);
     if (nb > C::NBC) return false;  // more border components than this class holds
     for (int l = l0; l < l1; ++l) {
+        uint16_t v;
         if (S.lcb[l]) {
             S.blc[bx] = (uint16_t)l;
-            S.lcb[l] = (uint16_t)bx++;
+            v = (uint16_t)bx++;
         } else {
-            S.lcb[l] = (uint16_t)(0x8000 | bx);
+            v = (uint16_t)(0x8000 | bx);
+        }
+        S.lcb[l] = v;
+        if (map) {
+            map[nruns + l] = S.lcrun[l];
+            map[nruns + nlc + l] = v;
         }
     }
     if (tid == 0) S.nb = nb;
