@@ -187,6 +187,31 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
     return r;
 }
 
+// Exclusive scan of one (warp-uniform) value per warp over NWB warps; `wsum` is __shared__
+// int[NWB + 1].  Returns this warp's offset; `total` = sum over warps.
+template <int NWB>
+__device__ __forceinline__ int warp_segments_scan(int v, int* wsum, int& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) wsum[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        const int s = lane < NWB ? wsum[lane] : 0;
+        int si = s;
+#pragma unroll
+        for (int o = 1; o < NWB; o <<= 1) {
+            const int n = __shfl_up_sync(0xFFFFFFFFu, si, o);
+            if (lane >= o) si += n;
+        }
+        if (lane < NWB) wsum[lane] = si - s;
+        if (lane == NWB - 1) wsum[NWB] = si;
+    }
+    __syncthreads();
+    total = wsum[NWB];
+    const int r = wsum[warp];
+    __syncthreads();
+    return r;
+}
+
 template <int BT = NT>
 __device__ __forceinline__ int block_reduce_sum(int v, int* wsum) {
     int t;

@@ -426,22 +426,35 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     }
     RL_PHASE(tg.t, 5);
 
-    // ---- tile components = root runs, numbered in raster order (contiguous run chunks)
-    const int per = (nruns + BT - 1) / BT;
-    const int i0 = min(tid * per, nruns), i1 = min(i0 + per, nruns);
-    int nroots = 0;
-    for (int i = i0; i < i1; ++i) nroots += (S.par[i] == (uint32_t)i);
+    // ---- tile components = root runs, numbered in raster order.  Each warp owns a contiguous
+    // segment of runs and walks it 32 runs at a time (ballot prefixes, conflict-free); the
+    // warps' counts are scanned once.
+    constexpr int NWB = BT / 32;
+    const unsigned lt = (1u << lane) - 1u;
+    const int seg = ((nruns + NWB - 1) / NWB + 31) & ~31;
+    const int r0 = min(warp * seg, nruns), r1 = min(r0 + seg, nruns);
+    int cntw = 0;
+    for (int b = r0; b < r1; b += 32) {
+        const int i = b + lane;
+        cntw += __popc(__ballot_sync(0xFFFFFFFFu, i < r1 && S.par[i] == (uint32_t)i));
+    }
     int nlc;
-    int lc = block_excl_scan<BT>(nroots, S.wsum, nlc);
-    for (int i = i0; i < i1; ++i) {
-        const int rr = run_row(S, i);
-        if (S.rbase[rr * WPR] == i) S.rowlc[rr] = (uint16_t)lc;  // first run of its row
-        if (S.par[i] == (uint32_t)i) {
-            S.lcrun[lc] = (uint16_t)i;
-            S.lcb[lc] = 0;
-            S.par[i] = (uint16_t)(TAG16 | lc);
-            ++lc;
+    int lc = warp_segments_scan<NWB>(cntw, S.wsum, nlc);
+    for (int b = r0; b < r1; b += 32) {
+        const int i = b + lane;
+        const bool root = i < r1 && S.par[i] == (uint32_t)i;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, root);
+        const int my = lc + __popc(m & lt);
+        if (i < r1) {
+            const int rr = run_row(S, i);
+            if (S.rbase[rr * WPR] == i) S.rowlc[rr] = (uint16_t)my;  // first run of its row
         }
+        if (root) {
+            S.lcrun[my] = (uint16_t)i;
+            S.lcb[my] = 0;
+            S.par[i] = (uint16_t)(TAG16 | my);
+        }
+        lc += __popc(m);
     }
     if (tid == 0) S.nlc = nlc;
     if (tid == 32) {  // the map: component of each run, first run and border index of each component
@@ -471,27 +484,37 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     __syncthreads();
     RL_PHASE(tg.t, 7);
 
-    // ---- compact border components to border indices (raster order)
-    const int perl = (nlc + BT - 1) / BT;
-    const int l0 = min(tid * perl, nlc), l1 = min(l0 + perl, nlc);
-    int cnt = 0;
-    for (int l = l0; l < l1; ++l) cnt += S.lcb[l];
+    // ---- compact border components to border indices (raster order; warp segments again)
+    const int segl = ((nlc + NWB - 1) / NWB + 31) & ~31;
+    const int l0 = min(warp * segl, nlc), l1 = min(l0 + segl, nlc);
+    int cntb = 0;
+    for (int b = l0; b < l1; b += 32) {
+        const int l = b + lane;
+        cntb += __popc(__ballot_sync(0xFFFFFFFFu, l < l1 && S.lcb[l]));
+    }
     int nb;
-    int bx = block_excl_scan<BT>(cnt, S.wsum, nb);
+    int bx = warp_segments_scan<NWB>(cntb, S.wsum, nb);
     if (nb > C::NBC) return false;  // more border components than this class holds
-    for (int l = l0; l < l1; ++l) {
-        uint16_t v;
-        if (S.lcb[l]) {
-            S.blc[bx] = (uint16_t)l;
-            v = (uint16_t)bx++;
-        } else {
-            v = (uint16_t)(0x8000 | bx);
+    for (int b = l0; b < l1; b += 32) {
+        const int l = b + lane;
+        const bool border = l < l1 && S.lcb[l];
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, border);
+        const int my = bx + __popc(m & lt);
+        if (l < l1) {
+            uint16_t v;
+            if (border) {
+                S.blc[my] = (uint16_t)l;
+                v = (uint16_t)my;
+            } else {
+                v = (uint16_t)(0x8000 | my);
+            }
+            S.lcb[l] = v;
+            if (map) {
+                map[nruns + l] = S.lcrun[l];
+                map[nruns + nlc + l] = v;
+            }
         }
-        S.lcb[l] = v;
-        if (map) {
-            map[nruns + l] = S.lcrun[l];
-            map[nruns + nlc + l] = v;
-        }
+        bx += __popc(m);
     }
     if (tid == 0) S.nb = nb;
     __syncthreads();
