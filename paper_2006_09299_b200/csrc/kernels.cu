@@ -649,6 +649,8 @@ struct EmitSmem {
     uint32_t ext[NW];       // exterior-pixel masks of the tile words
     uint32_t rowoff[TH];    // canonical id offset of each tile row (relative to the image)
     uint64_t cb;
+    unsigned long long moff;  // offset of the tile's component map
+    int gate;                 // the merge phase succeeded (no capacity overflow)
 };
 
 // canonical id of tile component lc (any kind)
@@ -712,10 +714,11 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     const int r = tid / WPR, w = tid % WPR;
     constexpr int BT = C::BT;
     const bool word = BT == NW || tid < NW;
-    {
-        const uint16_t* h = ws.thdr + (int64_t)tg.t * THDR;
-        if ((int)h[0] > C::MR || (int)h[2] > C::NBC) return false;  // a larger class owns it
-    }
+    const uint16_t* hdr = ws.thdr + (int64_t)tg.t * THDR;
+    const int nb_h = hdr[2];
+    if ((int)hdr[0] > C::MR || nb_h > C::NBC) return false;  // a larger class owns it
+    // every global load the prologue needs is issued before the first barrier: bits, row
+    // offsets, header rows, map offset, and the border components' ids (node -> root -> ids)
     const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;
     if (word) {
         S.x[tid] = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
@@ -726,7 +729,13 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     const uint32_t offimg = ws.off[img0];
     if (tid < TH && tid < tg.th)
         E.rowoff[tid] = ws.off[img0 + (int64_t)(tg.y0 + tid) * g.ntx + tg.tx] - offimg;
-    if (tid == 0) E.cb = (uint64_t)offimg + (uint64_t)tg.b;
+    if (tid == 0) {
+        E.cb = (uint64_t)offimg + (uint64_t)tg.b;
+        E.gate = !ws.counters[1] && comps_fit(g, ws);
+        S.nlc = hdr[1];
+        S.nb = nb_h;
+    }
+    if (tid == 32) E.moff = ws.tmap[tg.t];
     if (tid < FOLD_SLOTS) {
         E.pkey[tid] = 0xFFFF;
         E.ps[tid] = E.psx[tid] = E.psy[tid] = 0;
@@ -735,16 +744,26 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         E.pcmin[tid] = 0x7FFFFFFF;
         E.pcmax[tid] = -1;
     }
-    const uint16_t* hdr = ws.thdr + (int64_t)tg.t * THDR;
-    if (tid == 0) {
-        S.nlc = hdr[1];
-        S.nb = hdr[2];
-    }
     if (tid <= TH) {
         S.rowlc[tid] = hdr[4 + tid];
         S.rowbx[tid] = hdr[4 + TH + 1 + tid];
     }
+    if (nb_h) {
+        const uint32_t nbase = (uint32_t)g.B + ws.tbase[tg.t];
+        const uint32_t nend = (uint32_t)g.B + ws.cap_nodes;  // loads stay in bounds even when
+        for (int i = tid; i < nb_h; i += BT) {                 // the gate below fails
+            const uint32_t node = nbase + (uint32_t)i;
+            if (node >= nend) break;
+            const uint32_t root = ws.uf[node];
+            if (root >= nend) continue;
+            const bool ext = root < (uint32_t)g.B;
+            E.bcid[i] = ws.nrootcid[root];
+            E.banc[i] = ext ? 0u : ws.nanccid[root];
+            E.bflag[i] = (uint8_t)((ws.nrep[node] ? 1u : 0u) | (ext ? 2u : 0u));
+        }
+    }
     __syncthreads();
+    if (!E.gate) return true;  // capacity overflow: the host grows and re-runs
 
     // runs again from the packed bits (cheap); the component map comes from the analyze pass
     RL_PHASE(tg.t, 16);
@@ -752,29 +771,17 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     if (!tile_runs<false>(S, wb)) return false;
     {
         const int nr = wb.nruns, nl = S.nlc;
-        const uint16_t* src = ws.rstore + ws.tmap[tg.t];
+        const uint16_t* src = ws.rstore + E.moff;
         for (int i = tid; i < nr; i += BT) S.par[i] = src[i];
         for (int l = tid; l < nl; l += BT) {
             S.lcrun[l] = src[nr + l];
             S.lcb[l] = src[nr + nl + l];
         }
     }
-    __syncthreads();
-
     RL_PHASE(tg.t, 17);
-    const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
+    const int nruns = wb.nruns, nlc = S.nlc, nb = S.nb;  // S.nruns is not visible before a barrier
     const uint64_t cb = E.cb;
-    const uint32_t nbase = (uint32_t)g.B + ws.tbase[tg.t];
-    for (int i = tid; i < nb; i += BT) {
-        const uint32_t node = nbase + (uint32_t)i;
-        const uint32_t root = ws.uf[node];
-        const bool ext = root < (uint32_t)g.B;
-        E.bcid[i] = ws.nrootcid[root];
-        E.banc[i] = ext ? 0u : ws.nanccid[root];
-        E.bflag[i] = (uint8_t)((ws.nrep[node] ? 1u : 0u) | (ext ? 2u : 0u));
-    }
-    __syncthreads();
-    if (tid < 32) {  // warp prefix of representative flags over border index
+    if (tid < 32) {  // warp prefix of representative flags over border index (flags are in)
         int carry = 0;
         for (int i0 = 0; i0 <= nb; i0 += 32) {
             const int i = i0 + tid;
@@ -968,14 +975,12 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
 // class S on the full grid (tiles of larger classes are skipped), M over list A, F over list B
 __global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (ws.counters[1] || !comps_fit(g, ws)) return;
     auto& E = *reinterpret_cast<EmitSmem<CapSE>*>(smem_raw);
     emit_tile(E, g, ws, tile_geom_grid(g));
 }
 
 __global__ void __launch_bounds__(CapME::BT, 3) k_emit_m(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (ws.counters[1] || !comps_fit(g, ws)) return;
     auto& E = *reinterpret_cast<EmitSmem<CapME>*>(smem_raw);
     const uint32_t n = ws.counters[2];
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
@@ -986,7 +991,6 @@ __global__ void __launch_bounds__(CapME::BT, 3) k_emit_m(Geo g, Ws ws) {
 
 __global__ void __launch_bounds__(CapFE::BT) k_emit_full(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (ws.counters[1] || !comps_fit(g, ws)) return;
     auto& E = *reinterpret_cast<EmitSmem<CapFE>*>(smem_raw);
     const uint32_t n = ws.counters[4];
     for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {

@@ -65,3 +65,11 @@ def test_cfg5_full(labeler):
     ref = O.label_canonical(img, 0)
     compare_image(got, ref, "cfg5")
     _invariants(got, img)
+
+
+def test_uniform_and_extreme_cells_batch(labeler):
+    """cfg2's extreme cells (d = 0, 0.05, 0.95, 1 at g = 1) as one batch of full-size images."""
+    imgs = np.stack([O.generate(2048, 2048, d, 1, 1) for d in (0.0, 0.05, 0.95, 1.0)])
+    res = labeler.label_batch(imgs, LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True))
+    for i in range(imgs.shape[0]):
+        compare_image(res.image(i), O.label_canonical(imgs[i], 0), f"extreme cell {i}")
