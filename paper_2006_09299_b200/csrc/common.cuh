@@ -248,7 +248,7 @@ __device__ __forceinline__ void p4_store_word(uint8_t* row, int32_t rowb, int32_
 
 // 4 mask bits -> 4 bytes of 0/1 (bit k -> byte k)
 __device__ __forceinline__ uint32_t nibble_to_bytes(uint32_t n) {
-    return ((n & 1u)) | ((n & 2u) << 7) | ((n & 4u) << 14) | ((n & 8u) << 21);
+    return (n * 0x00204081u) & 0x01010101u;  // the four shifted copies never overlap: no carries
 }
 
 // 16 pixel bytes (values 0/1) -> 16 mask bits

@@ -781,6 +781,12 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     RL_PHASE(tg.t, 17);
     const int nruns = wb.nruns, nlc = S.nlc, nb = S.nb;  // S.nruns is not visible before a barrier
     const uint64_t cb = E.cb;
+    for (int i = tid; i < min(C::FCH, nlc); i += BT) {  // first feature chunk's accumulators
+        E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
+        E.frmax[i] = -1;
+        E.fcmin[i] = 0x7FFFFFFF;
+        E.fcmax[i] = -1;
+    }
     if (tid < 32) {  // warp prefix of representative flags over border index (flags are in)
         int carry = 0;
         for (int i0 = 0; i0 <= nb; i0 += 32) {
@@ -805,13 +811,15 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     int nsurv = 0;
     for (int l0 = 0; l0 < max(nlc, 1); l0 += C::FCH) {
         const int l1 = min(l0 + C::FCH, nlc);
-        for (int i = tid; i < C::FCH; i += BT) {
-            E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
-            E.frmax[i] = -1;
-            E.fcmin[i] = 0x7FFFFFFF;
-            E.fcmax[i] = -1;
+        if (l0 > 0) {  // the first chunk's accumulators were cleared before the prefix barrier
+            for (int i = tid; i < l1 - l0; i += BT) {
+                E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
+                E.frmax[i] = -1;
+                E.fcmin[i] = 0x7FFFFFFF;
+                E.fcmax[i] = -1;
+            }
+            __syncthreads();
         }
-        __syncthreads();
         RL_PHASE(tg.t, 19);
         // a component's runs never precede its first (root) run
         const int ifirst = (l0 == 0 || l0 >= nlc) ? 0 : S.lcrun[l0];
