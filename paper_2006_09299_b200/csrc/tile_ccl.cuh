@@ -64,12 +64,15 @@ struct Cap {
     static_assert(BT == NW || (BT == 2 * NW && EVC >= 32 * 32), "wide classes never need event rounds");
 };
 // analyze pass (union-find: 32-bit parents)
-using CapS = Cap<MAXRUNS * 3 / 16, NBMAX / 2, 192, 512, uint32_t, NW>;
+#ifndef RL_S_MR
+#define RL_S_MR (MAXRUNS * 3 / 16)
+#endif
+using CapS = Cap<RL_S_MR, NBMAX / 2, 192, 512, uint32_t, NW>;
 using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 384, uint32_t, 2 * NW>;
 using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 // emit pass: same classes, no unions (16-bit component map, larger feature chunks)
 #ifndef RL_SE_FCH
-#define RL_SE_FCH 256
+#define RL_SE_FCH 192
 #endif
 using CapSE = Cap<CapS::MR, CapS::NBC, 192, RL_SE_FCH, uint16_t, NW>;
 using CapME = Cap<CapM::MR, CapM::NBC, 1024, 640, uint16_t, 2 * NW>;
