@@ -65,7 +65,7 @@ struct Cap {
 };
 // analyze pass (union-find: 32-bit parents)
 #ifndef RL_S_MR
-#define RL_S_MR (MAXRUNS * 3 / 16)
+#define RL_S_MR 2048  // 3072 and 1280 measured slower on config 2
 #endif
 using CapS = Cap<RL_S_MR, NBMAX / 2, 192, 512, uint32_t, NW>;
 using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 384, uint32_t, 2 * NW>;
