@@ -277,22 +277,37 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     cudaMemsetAsync(ws.img_fg, 0, (size_t)B * 4, s);
     cudaMemsetAsync(ws.img_surv, 0, (size_t)B * 4, s);
     cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
+    ctx->nkev = 0;
+    auto kt = [&]() {  // tuning aid: an event after each launch group
+        if (!ctx->ktimes || use_graph || ctx->nkev >= 24) return;
+        if (!ctx->kev[ctx->nkev]) cudaEventCreate(&ctx->kev[ctx->nkev]);
+        cudaEventRecord(ctx->kev[ctx->nkev++], s);
+    };
     record_event(ctx->ev[0], s, use_graph);
+    kt();
     launch_analyze(dpix, g, ws, s);
     launches += 3;
     record_event(ctx->ev[1], s, use_graph);
+    kt();
     launch_seams(g, ws, s, ctx->sms);
     launches += (g.nty > 1) + (g.ntx > 1);
+    kt();
     const int64_t hint = (int64_t)ctx->cap_nodes;
     launch_resolve(g, ws, s, ctx->sms, hint);
+    kt();
     launch_reps(g, ws, s, ctx->sms, hint);
+    kt();
     cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ws.cnt, ws.off, (int)ncnt, s);
+    kt();
     launch_cids(g, ws, s, ctx->sms);
+    kt();
     launch_tree(g, ws, s, ctx->sms, hint);
     launches += 2 + 1 + 1 + 3;
+    kt();
     record_event(ctx->ev[2], s, use_graph);
     launch_emit(g, ws, s);
     launches += 3;
+    kt();
     k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));
     ++launches;
     if (need_rank) {
@@ -563,6 +578,7 @@ rl_ctx* rl_create(int device) {
     }
     c->stream = c->own_stream;
     if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
+    if (std::getenv("RUNLAB_GPU_KTIMES")) c->ktimes = true;
     if (const char* v = std::getenv("RUNLAB_GPU_CHUNK_PX")) c->chunk_px = std::max(1ll, std::atoll(v));
     return c;
 }
@@ -586,6 +602,8 @@ void rl_destroy(rl_ctx* c) {
         for (auto& e : slot)
             if (e) cudaEventDestroy(e);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (auto& e : c->kev)
+        if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -755,3 +773,13 @@ void rl_tile_shape(int32_t* th, int32_t* tw) {
 }  // extern "C"
 
 extern "C" int rl_last_used_graph(const rl_ctx* c) { return c && c->used_graph ? 1 : 0; }
+
+// tuning aid (RUNLAB_GPU_KTIMES): ms between the events recorded after each launch group of the
+// last eager call: analyze, seams, resolve, reps, scan, cids, tree (parents+tops+fold), emit
+extern "C" int rl_debug_launch_times(rl_ctx* c, float* ms, int max_n) {
+    if (!c || c->nkev < 2) return 0;
+    cudaEventSynchronize(c->kev[c->nkev - 1]);
+    int n = 0;
+    for (int k = 1; k < c->nkev && n < max_n; ++k) cudaEventElapsedTime(&ms[n++], c->kev[k - 1], c->kev[k]);
+    return n;
+}

@@ -104,6 +104,10 @@ struct rl_ctx {
     // rl_label_into pipelines large batches through these (own workspace and stream each)
     static constexpr int NKIDS = 3;
     rl_ctx* kids[NKIDS] = {};
+    // per-launch timing for tuning (env RUNLAB_GPU_KTIMES; eager launches only)
+    bool ktimes = false;
+    cudaEvent_t kev[24] = {};
+    int nkev = 0;
     // strip mode (strips.cu)
     DevBuf nleft, scount;
     rlh::StripState* strip = nullptr;

@@ -17,6 +17,8 @@
 // (Alg. 1-3 + fill), :224-250 (Alg. 4), :354-360 (binarize_labels), features.hpp:33-66.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "tile_ccl.cuh"
 
@@ -317,44 +319,58 @@ __device__ __forceinline__ uint32_t node_of(const Ws& ws, const Geo& g, int64_t 
     return (uint32_t)g.B + ws.tbase[t] + (lab & 0x7FFFu);
 }
 
-// horizontal seams s0 .. s0+ns-1 (seam s lies between tile rows s and s+1), one thread per
-// image column
-__global__ void k_seam_h(Geo g, Ws ws, int32_t s0, int32_t ns) {
+// Horizontal seams s0 .. s0+ns-1 (seam s lies between tile rows s and s+1): one block per
+// tile pair, one thread per column.  The pairs a seam links are first united in shared memory
+// over the two tiles' border indices (a component crossing the seam at many columns -- the
+// percolating one -- becomes one link), then one global union per linked border component.
+__global__ void __launch_bounds__(TW) k_seam_h(Geo g, Ws ws, int32_t s0, int32_t ns) {
+    __shared__ uint32_t lp[2 * NBMAX];
     if (ws.counters[1]) return;
-    const int64_t nseam = (int64_t)g.B * ns * g.W;
     const uint32_t v8 = g.flip ? 0u : 1u;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseam;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t x = (int32_t)(i % g.W);
-        const int64_t bs = i / g.W;
-        const int32_t s = s0 + (int32_t)(bs % ns);
-        const int32_t b = (int32_t)(bs / ns);
-        const int32_t tx = x / TW, c = x % TW;
+    const int32_t tx = blockIdx.x, c = threadIdx.x, x = tx * TW + c;
+    for (int32_t bs = blockIdx.y; bs < g.B * ns; bs += gridDim.y) {
+        const int32_t s = s0 + bs % ns;
+        const int32_t b = bs / ns;
         const int64_t tu = ((int64_t)b * g.nty + s) * g.ntx + tx, tl = tu + g.ntx;
-        const uint16_t lu = ws.perim[tu * PERIM + TW + c], ld = ws.perim[tl * PERIM + c];
-        const uint32_t vu = lu >> 15, vd = ld >> 15;
-        uint16_t lul = PERIM_NONE, ldl = PERIM_NONE;
-        int64_t tul = tu, tll = tl;
-        if (x > 0) {
-            const int32_t cl = (x - 1) % TW;
-            if (c == 0) {
-                tul = tu - 1;
-                tll = tl - 1;
+        const int nbu = (int)ws.tnb[tu], nbd = (int)ws.tnb[tl];
+        for (int i = c; i < nbu + nbd; i += TW) lp[i] = (uint32_t)i;
+        __syncthreads();
+        if (x < g.W) {
+            const uint16_t lu = ws.perim[tu * PERIM + TW + c], ld = ws.perim[tl * PERIM + c];
+            const uint32_t vu = lu >> 15, vd = ld >> 15;
+            uint16_t lul = PERIM_NONE, ldl = PERIM_NONE;
+            if (x > 0) {
+                const int64_t tul = c == 0 ? tu - 1 : tu, tll = c == 0 ? tl - 1 : tl;
+                const int32_t cl = (x - 1) % TW;
+                lul = ws.perim[tul * PERIM + TW + cl];
+                ldl = ws.perim[tll * PERIM + cl];
             }
-            lul = ws.perim[tul * PERIM + TW + cl];
-            ldl = ws.perim[tll * PERIM + cl];
+            const uint32_t iu = lu & 0x7FFFu, id = (uint32_t)nbu + (ld & 0x7FFFu);
+            if (vu == vd && !(c > 0 && lul == lu && ldl == ld)) sunion(lp, iu, id);
+            if (x > 0) {
+                const uint32_t vul = lul >> 15, vdl = ldl >> 15;
+                if (vul == v8 && vd == v8 && vu != v8 && vdl != v8) {  // (r, x-1) ~ (r+1, x)
+                    if (c > 0) sunion(lp, lul & 0x7FFFu, id);
+                    else gunion(ws.uf, node_of(ws, g, tu - 1, lul), node_of(ws, g, tl, ld));
+                }
+                if (vu == v8 && vdl == v8 && vul != v8 && vd != v8) {  // (r, x) ~ (r+1, x-1)
+                    if (c > 0) sunion(lp, iu, (uint32_t)nbu + (ldl & 0x7FFFu));
+                    else gunion(ws.uf, node_of(ws, g, tu, lu), node_of(ws, g, tl - 1, ldl));
+                }
+            }
         }
-        if (vu == vd) {
-            const bool same = (c > 0) && lul == lu && ldl == ld;
-            if (!same) gunion(ws.uf, node_of(ws, g, tu, lu), node_of(ws, g, tl, ld));
+        __syncthreads();
+        // one global link per border component that joined another one here
+        const uint32_t bu = (uint32_t)g.B + ws.tbase[tu], bd = (uint32_t)g.B + ws.tbase[tl];
+        for (int i = c; i < nbu + nbd; i += TW) {
+            uint32_t r = lp[i];
+            if (r == (uint32_t)i) continue;
+            while (lp[r] != r) r = lp[r];
+            const uint32_t ni = i < nbu ? bu + i : bd + (i - nbu);
+            const uint32_t nr = r < (uint32_t)nbu ? bu + r : bd + (r - nbu);
+            gunion(ws.uf, ni, nr);
         }
-        if (x > 0) {
-            const uint32_t vul = lul >> 15, vdl = ldl >> 15;
-            if (vul == v8 && vd == v8 && vu != v8 && vdl != v8)
-                gunion(ws.uf, node_of(ws, g, tul, lul), node_of(ws, g, tl, ld));
-            if (vu == v8 && vdl == v8 && vul != v8 && vd != v8)
-                gunion(ws.uf, node_of(ws, g, tu, lu), node_of(ws, g, tll, ldl));
-        }
+        __syncthreads();
     }
 }
 
@@ -362,17 +378,15 @@ __global__ void k_seam_h(Geo g, Ws ws, int32_t s0, int32_t ns) {
 // [ty0, ty1)
 __global__ void k_seam_v(Geo g, Ws ws) {
     if (ws.counters[1]) return;
+    // pixel row r of a tile row (threadIdx.x & 31), seams over grid x, (image, tile row) over grid y
     const int32_t nrows = g.ty1 - g.ty0;
-    const int64_t nseam = (int64_t)g.B * nrows * (g.ntx - 1) * TH;
     const uint32_t v8 = g.flip ? 0u : 1u;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseam;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t r = (int32_t)(i % TH);
-        int64_t q = i / TH;
-        const int32_t s = 1 + (int32_t)(q % (g.ntx - 1));
-        q /= (g.ntx - 1);
-        const int32_t ty = g.ty0 + (int32_t)(q % nrows);
-        const int32_t b = (int32_t)(q / nrows);
+    const int32_t r = threadIdx.x & 31;
+    const int32_t s = 1 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (s >= g.ntx) return;
+    for (int32_t q = blockIdx.y; q < g.B * nrows; q += gridDim.y) {
+        const int32_t ty = g.ty0 + q % nrows;
+        const int32_t b = q / nrows;
         const int32_t th = min(TH, g.H - ty * TH);
         if (r >= th) continue;
         const int64_t tR = ((int64_t)b * g.nty + ty) * g.ntx + s, tL = tR - 1;
@@ -1084,8 +1098,9 @@ static int grid_for(int64_t n, int block, int maxgrid) {
 }
 
 void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms) {
-    const int64_t n = (int64_t)g.B * ns * g.W;
-    k_seam_h<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(g, ws, s0, ns);
+    const int64_t pairs = (int64_t)g.B * ns;
+    const dim3 grid(g.ntx, (unsigned)std::min<int64_t>(pairs, 65535));
+    k_seam_h<<<grid, TW, 0, s>>>(g, ws, s0, ns);
 }
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
     k_analyze<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
@@ -1098,8 +1113,9 @@ void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
     const int32_t rows = g.ty1 - g.ty0;
     if (rows > 1) launch_seam_rows(g, ws, g.ty0, rows - 1, s, sms);
     if (g.ntx > 1) {
-        const int64_t n = (int64_t)g.B * rows * (g.ntx - 1) * TH;
-        k_seam_v<<<grid_for(n, 256, sms * 16), 256, 0, s>>>(g, ws);
+        const int64_t pairs = (int64_t)g.B * rows;
+        const dim3 grid((g.ntx - 1 + 7) / 8, (unsigned)std::min<int64_t>(pairs, 65535));
+        k_seam_v<<<grid, 256, 0, s>>>(g, ws);
     }
 }
 void launch_resolve(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {

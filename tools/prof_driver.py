@@ -66,9 +66,18 @@ def main():
         cells = cfg2_cells()
         args.copies = 1
     B, t = run(cells, args.copies, args.iters)
-    print(json.dumps({"images": B, "analyze_ms": t.analyze_ms, "merge_ms": t.merge_ms,
-                      "emit_ms": t.emit_ms, "total_ms": t.total_ms,
-                      "gpx": B * S * S / (t.total_ms / 1e3) / 1e9}))
+    line = {"images": B, "analyze_ms": t.analyze_ms, "merge_ms": t.merge_ms, "emit_ms": t.emit_ms,
+            "total_ms": t.total_ms, "gpx": B * S * S / (t.total_ms / 1e3) / 1e9}
+    if os.environ.get("RUNLAB_GPU_KTIMES"):
+        import ctypes as C
+        from paper_2006_09299_b200 import _native as N
+        L = N.load()
+        L.rl_debug_launch_times.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int]
+        ms = (C.c_float * 16)()
+        n = L.rl_debug_launch_times(lab.ctx, ms, 16)
+        names = ["analyze", "seams", "resolve", "reps", "scan", "cids", "tree", "emit"]
+        line["launch_ms"] = {names[k] if k < len(names) else str(k): round(ms[k], 4) for k in range(n)}
+    print(json.dumps(line))
 
 
 if __name__ == "__main__":
