@@ -332,14 +332,38 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     __syncthreads();             // first-contact parents of every word are in place
     RL_PHASE(tg.t, 14);
     // The first-contact forest links every run to one in the row above, so a vertical stack
-    // of runs is a chain as tall as the stack.  Pointer jumping flattens it (log2 of the tile
-    // height rounds) so that the finds of the union phase are short.
-    {
-        const int nr = S.nruns;
-#ifndef RL_PREFLAT_ROUNDS
-#define RL_PREFLAT_ROUNDS 0
+    // of runs is a chain as tall as the stack.  It is flattened before the unions so that their
+    // finds are short: every run walks its chain to the root and links to it directly.  The
+    // walks run concurrently; a link read mid-walk is either the original one or a root
+    // already written by another walker, both ancestors, so walks only get shorter.  (Row
+    // groups with a barrier between them, RPS < TH, and pointer jumping, RPS = 0, were
+    // measured slower on config 2.)
+#ifndef RL_PREFLAT_RPS
+#define RL_PREFLAT_RPS TH
 #endif
-        for (int round = 0;; ++round) {
+    if constexpr (RL_PREFLAT_RPS > 0) {
+        // row groups top-down: runs above the group already point at their roots, so a run
+        // walks at most RPS first-contact links inside its group, then takes its root
+        constexpr int RPS = RL_PREFLAT_RPS;
+        const int nr = S.nruns;
+        for (int r0 = 1; r0 < tg.th; r0 += RPS) {
+            const int rs = S.rbase[r0 * WPR];
+            const int re = r0 + RPS < tg.th ? S.rbase[(r0 + RPS) * WPR] : nr;
+            for (int i = rs + tid; i < re; i += BT) {
+                uint32_t p = S.par[i];
+                if (p == (uint32_t)i) continue;  // no first contact: a root
+                while (p >= (uint32_t)rs) {      // links inside the group (final roots written
+                    const uint32_t q = S.par[p];  // concurrently are ancestors too)
+                    if (q == p) break;
+                    p = q;
+                }
+                S.par[i] = p < (uint32_t)rs ? S.par[p] : p;
+            }
+            __syncthreads();
+        }
+    } else {
+        const int nr = S.nruns;
+        for (;;) {
             int changed = 0;
             for (int i = tid; i < nr; i += BT) {
                 const uint32_t p = S.par[i];
@@ -349,12 +373,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
                     changed = 1;
                 }
             }
-            if (RL_PREFLAT_ROUNDS > 0) {
-                __syncthreads();
-                if (round + 1 == RL_PREFLAT_ROUNDS) break;
-            } else if (!__syncthreads_or(changed)) {
-                break;
-            }
+            if (!__syncthreads_or(changed)) break;
         }
     }
     RL_PHASE(tg.t, 3);
