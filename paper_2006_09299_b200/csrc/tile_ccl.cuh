@@ -428,24 +428,19 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     __syncthreads();
     RL_PHASE(tg.t, 4);
 
-    // ---- flatten (roots are final now): a short walk, then pointer jumping until every run
-    // points at its root (vertical stacks of runs form chains as long as the tile is tall)
+    // ---- flatten (roots are final now): every run walks to its root; concurrent writes of
+    // roots only shorten other walks (as in the pre-flatten)
     const int nruns = S.nruns;
-    for (int round = 0;; ++round) {
-        int changed = 0;
-        for (int i = tid; i < nruns; i += BT) {
-            uint32_t p = S.par[i];
-            const uint32_t p0 = p;
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t q = S.par[p];
-                if (q == p) break;
-                p = q;
-            }
-            if (p != p0) S.par[i] = (uint16_t)p;
-            changed |= (S.par[p] != p);
+    for (int i = tid; i < nruns; i += BT) {
+        uint32_t p = S.par[i];
+        for (;;) {
+            const uint32_t q = S.par[p];
+            if (q == p) break;
+            p = q;
         }
-        if (!__syncthreads_or(changed)) break;
+        S.par[i] = (uint16_t)p;
     }
+    __syncthreads();
     RL_PHASE(tg.t, 5);
 
     // ---- tile components = root runs, numbered in raster order.  Each warp owns a contiguous
