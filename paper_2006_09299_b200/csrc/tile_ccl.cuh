@@ -98,6 +98,8 @@ struct CclSmem {
         uint16_t evq[NWARPS][C::EVC];  // union-event queues (dead before lcrun/lcb are written)
     };
     uint16_t blc[C::NBC];      // border index -> tile component
+    uint32_t rmask[C::MR / 32 + 1];  // root runs of each 32-run block (ballot)
+    uint16_t rpre[C::MR / 32 + 1];   // root runs before each block
     int wsum[C::BT / 32 + 1];
     int qtot[NWARPS];          // union events queued by each word warp
     int nruns, nlc, nb;
@@ -429,50 +431,39 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     RL_PHASE(tg.t, 4);
 
     // ---- flatten (roots are final now): every run walks to its root; concurrent writes of
-    // roots only shorten other walks (as in the pre-flatten)
+    // roots only shorten other walks (as in the pre-flatten).  The walk of a 32-run block is
+    // one warp's, so the block's roots come out as a ballot mask.
     const int nruns = S.nruns;
-    for (int i = tid; i < nruns; i += BT) {
-        uint32_t p = S.par[i];
-        for (;;) {
-            const uint32_t q = S.par[p];
-            if (q == p) break;
-            p = q;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int b = warp * 32; b < nruns; b += BT) {
+        const int i = b + lane;
+        uint32_t p = i;
+        if (i < nruns) {
+            p = S.par[i];
+            for (;;) {
+                const uint32_t q = S.par[p];
+                if (q == p) break;
+                p = q;
+            }
+            S.par[i] = (uint16_t)p;
         }
-        S.par[i] = (uint16_t)p;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, i < nruns && p == (uint32_t)i);
+        if (lane == 0) S.rmask[b >> 5] = m;
     }
     __syncthreads();
     RL_PHASE(tg.t, 5);
 
-    // ---- tile components = root runs, numbered in raster order.  Each warp owns a contiguous
-    // segment of runs and walks it 32 runs at a time (ballot prefixes, conflict-free); the
-    // warps' counts are scanned once.
-    constexpr int NWB = BT / 32;
-    const unsigned lt = (1u << lane) - 1u;
-    const int seg = ((nruns + NWB - 1) / NWB + 31) & ~31;
-    const int r0 = min(warp * seg, nruns), r1 = min(r0 + seg, nruns);
-    int cntw = 0;
-    for (int b = r0; b < r1; b += 32) {
-        const int i = b + lane;
-        cntw += __popc(__ballot_sync(0xFFFFFFFFu, i < r1 && S.par[i] == (uint32_t)i));
-    }
+    // ---- tile components = root runs, numbered in raster order: prefix over the blocks' root
+    // counts; a run's component is then its root's rank (no tagging pass)
+    const int nblk = (nruns + 31) >> 5;
     int nlc;
-    int lc = warp_segments_scan<NWB>(cntw, S.wsum, nlc);
-    for (int b = r0; b < r1; b += 32) {
-        const int i = b + lane;
-        const bool root = i < r1 && S.par[i] == (uint32_t)i;
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, root);
-        const int my = lc + __popc(m & lt);
-        if (i < r1) {
-            const int rr = run_row(S, i);
-            if (S.rbase[rr * WPR] == i) S.rowlc[rr] = (uint16_t)my;  // first run of its row
-        }
-        if (root) {
-            S.lcrun[my] = (uint16_t)i;
-            S.lcb[my] = 0;
-            S.par[i] = (uint16_t)(TAG16 | my);
-        }
-        lc += __popc(m);
+    {
+        const int pre = block_excl_scan<BT>(tid < nblk ? __popc(S.rmask[tid]) : 0, S.wsum, nlc);
+        if (tid < nblk) S.rpre[tid] = (uint16_t)pre;
     }
+    auto rank_of = [&](uint32_t root) {  // valid once rpre is visible
+        return (uint32_t)S.rpre[root >> 5] + __popc(S.rmask[root >> 5] & ((1u << (root & 31)) - 1u));
+    };
     if (tid == 0) S.nlc = nlc;
     if (tid == 32) {  // the map: component of each run, first run and border index of each component
         const unsigned long long need = (unsigned long long)nruns + 2ull * (unsigned long long)nlc;
@@ -481,26 +472,29 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
         S.moff = off + need > mo.cap ? ~0ull : off;
         mo.tile_off[tg.t] = off;
     }
-    if (tid >= tg.th && tid <= TH) S.rowlc[tid] = (uint16_t)nlc;  // rows without pixels
+    for (int l = tid; l < nlc; l += BT) S.lcb[l] = 0;
     __syncthreads();
+    if (tid <= TH) {  // first component of each row: components before the row's first run
+        const int k = tid < tg.th ? S.rbase[tid * WPR] : nruns;
+        S.rowlc[tid] = (uint16_t)(k < nruns ? rank_of((uint32_t)k) : (uint32_t)nlc);
+    }
     RL_PHASE(tg.t, 6);
     const unsigned long long moff = S.moff;
     uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
-    // resolve non-root runs; mark components touching the tile border (plain stores of 1)
+    // every run: its component, the component's first run, border flags (plain stores of 1)
     for (int i = tid; i < nruns; i += BT) {
-        uint32_t p = S.par[i];
-        if (!(p & TAG16)) {
-            p = S.par[p];
-            S.par[i] = (uint16_t)p;
-        }
-        if (map) map[i] = (uint16_t)(p & 0x7FFFu);
+        const uint32_t root = S.par[i];
+        const uint32_t l = rank_of(root);
+        S.par[i] = (uint16_t)(TAG16 | l);
+        if (root == (uint32_t)i) S.lcrun[l] = (uint16_t)i;
+        if (map) map[i] = (uint16_t)l;
         const int rr = run_row(S, i), c0 = run_col(S, i);
-        if (rr == 0 || rr == tg.th - 1 || c0 == 0 || run_end(S, i, tg.tw) == tg.tw)
-            S.lcb[p & 0x7FFFu] = 1;
+        if (rr == 0 || rr == tg.th - 1 || c0 == 0 || run_end(S, i, tg.tw) == tg.tw) S.lcb[l] = 1;
     }
     __syncthreads();
     RL_PHASE(tg.t, 7);
 
+    constexpr int NWB = BT / 32;
     // ---- compact border components to border indices (raster order; warp segments again)
     const int segl = ((nlc + NWB - 1) / NWB + 31) & ~31;
     const int l0 = min(warp * segl, nlc), l1 = min(l0 + segl, nlc);
