@@ -540,13 +540,16 @@ __global__ void k_cids(Geo g, Ws ws) {
 __global__ void k_parents(Geo g, Ws ws) {
     if (ws.counters[1] || !comps_fit(g, ws)) return;
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid < g.B) {  // exterior records
+    if (gid < g.B) {  // exterior records (the exterior survives hole filling)
         const uint64_t cb = comp_base(g, ws, gid);
         rl_component c;
         c.f = ws.nacc[gid];
         c.parent = 0xFFFFFFFFu;
         c.flags = 0;
         ws.comps[cb] = c;
+        ws.top[cb] = 0;
+        ws.filled[cb] = c.f;
+        atomicAdd(&ws.img_surv[gid], 1u);
     }
     NODE_LOOP(n) {
         if (!ws.nrep[n]) continue;
@@ -571,50 +574,95 @@ __global__ void k_parents(Geo g, Ws ws) {
         }
         ws.nparent[root] = proot;
         const uint32_t cid = ws.nrootcid[root];
+        const uint64_t cb = comp_base(g, ws, b);
         rl_component c;
         c.f = ws.nacc[root];
         c.parent = ws.nrootcid[proot];
         c.flags = rec.fg;
-        ws.comps[comp_base(g, ws, b) + cid] = c;
-    }
-}
-
-__global__ void k_tops(Geo g, Ws ws) {
-    if (ws.counters[1] || !comps_fit(g, ws)) return;
-    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid < g.B) {
-        const uint64_t cb = comp_base(g, ws, gid);
-        ws.top[cb] = 0;
-        ws.filled[cb] = ws.nacc[gid];
-        atomicAdd(&ws.img_surv[gid], 1u);
-    }
-    NODE_LOOP(n) {
-        if (!ws.nrep[n]) continue;
-        const uint32_t root = ws.uf[n];
-        uint32_t cur = root;
-        for (;;) {
-            const uint32_t p = ws.nparent[cur];
-            if (p < (uint32_t)g.B) break;
-            cur = p;
-        }
-        const uint32_t anc = ws.nrootcid[cur];
-        ws.nanccid[root] = anc;
-        const NodeRec rec = ws.nrec[n];
-        int32_t b, ty, tx;
-        tile_of(g, rec.tile, b, ty, tx);
-        const uint64_t cb = comp_base(g, ws, b);
-        const uint32_t cid = ws.nrootcid[root];
-        ws.top[cb + cid] = anc;
-        if (cur == root) {
-            // strip mode: this rank's partial sums start empty; the border part is added after
-            // the cross-rank reduction (strips.cu)
-            ws.filled[cb + cid] = g.strip ? acc_empty() : ws.nacc[root];
-            // warp-aggregated survivor count (same image for most lanes)
-            const uint32_t active = __activemask();
+        ws.comps[cb + cid] = c;
+        if (proot < (uint32_t)g.B) {
+            // a child of the exterior survives hole filling: its post-fill features start as
+            // its own (strip mode: this rank's partial sums start empty, strips.cu)
+            ws.filled[cb + cid] = g.strip ? acc_empty() : c.f;
+            const uint32_t active = __activemask();  // survivors per image, warp-aggregated
             const uint32_t same = __match_any_sync(active, b);
             if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u)) atomicAdd(&ws.img_surv[b], (uint32_t)__popc(same));
         }
     }
+}
+
+// post-fill roots (depth-1 ancestors) of the border components; non-survivors fold their
+// features into their root right away (block-aggregated; the survivors were initialised by
+// k_parents).  Strip mode folds later, after the cross-rank reduction (k_fold).
+__global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
+    __shared__ FoldTable<FT_SLOTS> T;
+    if (ws.counters[1] || !comps_fit(g, ws)) return;
+    T.init();
+    __syncthreads();
+    const uint32_t nused = min(ws.counters[0], ws.cap_nodes);
+    const uint32_t chunk = (nused + gridDim.x - 1) / gridDim.x;
+    const uint32_t lo = (uint32_t)g.B + min(nused, blockIdx.x * chunk);
+    const uint32_t hi = (uint32_t)g.B + min(nused, (blockIdx.x + 1) * chunk);
+    const int lane = threadIdx.x & 31;
+    // whole warps iterate together: the folds of a warp into one root are reduced in registers
+    for (uint32_t base = lo + (threadIdx.x & ~31u); base < hi; base += blockDim.x) {
+        const uint32_t n = base + lane;
+        uint32_t dst = 0xFFFFFFFFu;
+        Acc f;
+        if (n < hi && ws.nrep[n]) {
+            const uint32_t root = ws.uf[n];
+            uint32_t cur = root;
+            for (;;) {
+                const uint32_t p = ws.nparent[cur];
+                if (p < (uint32_t)g.B) break;
+                cur = p;
+            }
+            const uint32_t anc = ws.nrootcid[cur];
+            ws.nanccid[root] = anc;
+            int32_t b, ty, tx;
+            tile_of(g, ws.nrec[n].tile, b, ty, tx);
+            const uint64_t cb = comp_base(g, ws, b);
+            const uint32_t cid = ws.nrootcid[root];
+            ws.top[cb + cid] = anc;
+            if (cur != root && !g.strip) {
+                dst = (uint32_t)(cb + anc);  // < 2^32 components
+                f = ws.nacc[root];
+            }
+        }
+        uint32_t pend = __ballot_sync(0xFFFFFFFFu, dst != 0xFFFFFFFFu);
+        while (pend) {  // one target at a time: butterfly over the lanes folding into it
+            const uint32_t cand = __shfl_sync(0xFFFFFFFFu, dst, __ffs(pend) - 1);
+            const bool mine = dst == cand;
+            long long s0 = mine ? f.s : 0, s1 = mine ? f.sx : 0, s2 = mine ? f.sy : 0;
+            int r0 = mine ? f.row_min : 0x7FFFFFFF, r1 = mine ? f.row_max : (int)0x80000000;
+            int c0 = mine ? f.col_min : 0x7FFFFFFF, c1 = mine ? f.col_max : (int)0x80000000;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
+                s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+                s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+            }
+            r0 = __reduce_min_sync(0xFFFFFFFFu, r0);
+            r1 = __reduce_max_sync(0xFFFFFFFFu, r1);
+            c0 = __reduce_min_sync(0xFFFFFFFFu, c0);
+            c1 = __reduce_max_sync(0xFFFFFFFFu, c1);
+            if (lane == __ffs(pend) - 1) {
+                Acc a;
+                a.s = s0;
+                a.sx = s1;
+                a.sy = s2;
+                a.row_min = r0;
+                a.row_max = r1;
+                a.col_min = c0;
+                a.col_max = c1;
+                if (!T.add(cand, a, ~0ull)) acc_atomic_fold(ws.filled + cand, a);
+            }
+            pend &= ~__ballot_sync(0xFFFFFFFFu, mine);
+        }
+    }
+    __syncthreads();
+    T.flush([&](uint32_t k) { return ws.filled + k; },
+            [&](uint32_t) { return static_cast<unsigned long long*>(nullptr); });
 }
 
 __global__ void __launch_bounds__(256) k_fold(Geo g, Ws ws) {
@@ -1130,8 +1178,7 @@ void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
 void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
     const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;
     k_parents<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
-    k_tops<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
-    k_fold<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
+    k_tops<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);  // folds too (single-GPU path)
 }
 void launch_tree_parts(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
     const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;
