@@ -340,6 +340,60 @@ struct FoldTable {
     }
 };
 
+// Warp-cooperative fold: every lane with dst != FT_EMPTY folds (f, key) into target dst.  The
+// lanes sharing a target are reduced in registers first (one target per round: the percolating
+// component's nodes all fold into one root), then one lane adds the sum to the block table --
+// 64-bit shared atomics are CAS loops, contention on one slot is what this avoids.  All 32
+// lanes must call it.  gdst(k) / gkey(k): global destinations when the table is full.
+template <class TT, class GD, class GK>
+__device__ __forceinline__ void warp_fold(TT& T, uint32_t dst, const Acc& f, unsigned long long key, GD&& gdst,
+                                          GK&& gkey) {
+    const int lane = threadIdx.x & 31;
+    auto add = [&](uint32_t k, const Acc& a, unsigned long long km) {
+        if (!T.add(k, a, km)) {
+            acc_atomic_fold(gdst(k), a);
+            unsigned long long* kd = gkey(k);
+            if (kd && km != ~0ull) atomicMin(kd, km);
+        }
+    };
+    // targets no other lane shares go straight in; shared ones are reduced first
+    const uint32_t grp = __match_any_sync(0xFFFFFFFFu, dst);
+    const bool alone = (grp & (grp - 1)) == 0;
+    if (alone && dst != FT_EMPTY) add(dst, f, key);
+    uint32_t pend = __ballot_sync(0xFFFFFFFFu, dst != FT_EMPTY && !alone);
+    while (pend) {
+        const int lead = __ffs(pend) - 1;
+        const uint32_t cand = __shfl_sync(0xFFFFFFFFu, dst, lead);
+        const bool mine = dst == cand;
+        long long s0 = mine ? f.s : 0, s1 = mine ? f.sx : 0, s2 = mine ? f.sy : 0;
+        unsigned long long km = mine ? key : ~0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
+            s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+            s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+            const unsigned long long ko = __shfl_xor_sync(0xFFFFFFFFu, km, o);
+            km = ko < km ? ko : km;
+        }
+        const int r0 = __reduce_min_sync(0xFFFFFFFFu, mine ? f.row_min : 0x7FFFFFFF);
+        const int r1 = __reduce_max_sync(0xFFFFFFFFu, mine ? f.row_max : (int)0x80000000);
+        const int c0 = __reduce_min_sync(0xFFFFFFFFu, mine ? f.col_min : 0x7FFFFFFF);
+        const int c1 = __reduce_max_sync(0xFFFFFFFFu, mine ? f.col_max : (int)0x80000000);
+        if (lane == lead) {
+            Acc a;
+            a.s = s0;
+            a.sx = s1;
+            a.sy = s2;
+            a.row_min = r0;
+            a.row_max = r1;
+            a.col_min = c0;
+            a.col_max = c1;
+            add(cand, a, km);
+        }
+        pend &= ~__ballot_sync(0xFFFFFFFFu, mine);
+    }
+}
+
 // ---- global union-find (lock-free; min-index linking, path halving) -------------------
 // Plain (L1-cacheable) reads are safe: parents only ever decrease, so a stale value is
 // still an ancestor, and the linking atomicMin returns the true old value.

@@ -433,17 +433,26 @@ __global__ void __launch_bounds__(256) k_resolve(Geo g, Ws ws) {
     if (ws.counters[1]) return;
     T.init();
     __syncthreads();
-    NODE_CHUNK(n) {
-        const uint32_t root = gfind_ro(ws.uf, n);
-        if (root != n) {
-            ws.uf[n] = root;
-            const Acc f = ws.nacc[n];
-            const unsigned long long key = ws.nkey[n];
-            if (!T.add(root, f, key)) {
-                acc_atomic_fold(ws.nacc + root, f);
-                atomicMin(reinterpret_cast<unsigned long long*>(ws.nmin + root), key);
+    const uint32_t nused = min(ws.counters[0], ws.cap_nodes);
+    const uint32_t chunk = (nused + gridDim.x - 1) / gridDim.x;
+    const uint32_t lo = (uint32_t)g.B + min(nused, blockIdx.x * chunk);
+    const uint32_t hi = (uint32_t)g.B + min(nused, (blockIdx.x + 1) * chunk);
+    for (uint32_t base = lo + (threadIdx.x & ~31u); base < hi; base += blockDim.x) {
+        const uint32_t n = base + (threadIdx.x & 31);
+        uint32_t dst = FT_EMPTY;
+        Acc f;
+        unsigned long long key = ~0ull;
+        if (n < hi) {
+            const uint32_t root = gfind_ro(ws.uf, n);
+            if (root != n) {
+                ws.uf[n] = root;
+                dst = root;
+                f = ws.nacc[n];
+                key = ws.nkey[n];
             }
         }
+        warp_fold(T, dst, f, key, [&](uint32_t k) { return ws.nacc + k; },
+                  [&](uint32_t k) { return reinterpret_cast<unsigned long long*>(ws.nmin + k); });
     }
     __syncthreads();
     T.flush([&](uint32_t k) { return ws.nacc + k; },
@@ -607,7 +616,7 @@ __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
     // whole warps iterate together: the folds of a warp into one root are reduced in registers
     for (uint32_t base = lo + (threadIdx.x & ~31u); base < hi; base += blockDim.x) {
         const uint32_t n = base + lane;
-        uint32_t dst = 0xFFFFFFFFu;
+        uint32_t dst = FT_EMPTY;
         Acc f;
         if (n < hi && ws.nrep[n]) {
             const uint32_t root = ws.uf[n];
@@ -629,58 +638,40 @@ __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
                 f = ws.nacc[root];
             }
         }
-        uint32_t pend = __ballot_sync(0xFFFFFFFFu, dst != 0xFFFFFFFFu);
-        while (pend) {  // one target at a time: butterfly over the lanes folding into it
-            const uint32_t cand = __shfl_sync(0xFFFFFFFFu, dst, __ffs(pend) - 1);
-            const bool mine = dst == cand;
-            long long s0 = mine ? f.s : 0, s1 = mine ? f.sx : 0, s2 = mine ? f.sy : 0;
-            int r0 = mine ? f.row_min : 0x7FFFFFFF, r1 = mine ? f.row_max : (int)0x80000000;
-            int c0 = mine ? f.col_min : 0x7FFFFFFF, c1 = mine ? f.col_max : (int)0x80000000;
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
-                s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
-                s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
-            }
-            r0 = __reduce_min_sync(0xFFFFFFFFu, r0);
-            r1 = __reduce_max_sync(0xFFFFFFFFu, r1);
-            c0 = __reduce_min_sync(0xFFFFFFFFu, c0);
-            c1 = __reduce_max_sync(0xFFFFFFFFu, c1);
-            if (lane == __ffs(pend) - 1) {
-                Acc a;
-                a.s = s0;
-                a.sx = s1;
-                a.sy = s2;
-                a.row_min = r0;
-                a.row_max = r1;
-                a.col_min = c0;
-                a.col_max = c1;
-                if (!T.add(cand, a, ~0ull)) acc_atomic_fold(ws.filled + cand, a);
-            }
-            pend &= ~__ballot_sync(0xFFFFFFFFu, mine);
-        }
+        warp_fold(T, dst, f, ~0ull, [&](uint32_t k) { return ws.filled + k; },
+                  [&](uint32_t) { return static_cast<unsigned long long*>(nullptr); });
     }
     __syncthreads();
     T.flush([&](uint32_t k) { return ws.filled + k; },
             [&](uint32_t) { return static_cast<unsigned long long*>(nullptr); });
 }
 
+// strip mode: border non-survivors into their post-fill roots, after the reduction (strips.cu)
 __global__ void __launch_bounds__(256) k_fold(Geo g, Ws ws) {
     __shared__ FoldTable<FT_SLOTS> T;
     if (ws.counters[1] || !comps_fit(g, ws)) return;
     T.init();
     __syncthreads();
-    NODE_CHUNK(n) {
-        if (!ws.nrep[n]) continue;
-        const uint32_t root = ws.uf[n];
-        const uint32_t anc = ws.nanccid[root];
-        const uint32_t cid = ws.nrootcid[root];
-        if (anc == cid) continue;
-        int32_t b, ty, tx;
-        tile_of(g, ws.nrec[n].tile, b, ty, tx);
-        const uint32_t dst = (uint32_t)(comp_base(g, ws, b) + anc);  // < 2^32 components
-        const Acc f = ws.nacc[root];
-        if (!T.add(dst, f, ~0ull)) acc_atomic_fold(ws.filled + dst, f);
+    const uint32_t nused = min(ws.counters[0], ws.cap_nodes);
+    const uint32_t chunk = (nused + gridDim.x - 1) / gridDim.x;
+    const uint32_t lo = (uint32_t)g.B + min(nused, blockIdx.x * chunk);
+    const uint32_t hi = (uint32_t)g.B + min(nused, (blockIdx.x + 1) * chunk);
+    for (uint32_t base = lo + (threadIdx.x & ~31u); base < hi; base += blockDim.x) {
+        const uint32_t n = base + (threadIdx.x & 31);
+        uint32_t dst = FT_EMPTY;
+        Acc f;
+        if (n < hi && ws.nrep[n]) {
+            const uint32_t root = ws.uf[n];
+            const uint32_t anc = ws.nanccid[root];
+            if (anc != ws.nrootcid[root]) {
+                int32_t b, ty, tx;
+                tile_of(g, ws.nrec[n].tile, b, ty, tx);
+                dst = (uint32_t)(comp_base(g, ws, b) + anc);  // < 2^32 components
+                f = ws.nacc[root];
+            }
+        }
+        warp_fold(T, dst, f, ~0ull, [&](uint32_t k) { return ws.filled + k; },
+                  [&](uint32_t) { return static_cast<unsigned long long*>(nullptr); });
     }
     __syncthreads();
     T.flush([&](uint32_t k) { return ws.filled + k; },
