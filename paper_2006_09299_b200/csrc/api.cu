@@ -289,7 +289,9 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launches += 3;
     record_event(ctx->ev[1], s, use_graph);
     kt();
-    launch_seams(g, ws, s, ctx->sms);
+    if (g.nty > 1) launch_seam_rows(g, ws, 0, g.nty - 1, s, ctx->sms);
+    kt();
+    launch_seam_cols(g, ws, s, ctx->sms);
     launches += (g.nty > 1) + (g.ntx > 1);
     kt();
     const int64_t hint = (int64_t)ctx->cap_nodes;

@@ -15,6 +15,7 @@ size_t emit_smem();
 cudaError_t configure_kernels();
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s);
 void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms);
+void launch_seam_cols(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
 void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
 void launch_resolve(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
 void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
