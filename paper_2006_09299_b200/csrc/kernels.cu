@@ -323,19 +323,26 @@ __device__ __forceinline__ uint32_t node_of(const Ws& ws, const Geo& g, int64_t 
 // tile pair, one thread per column.  The pairs a seam links are first united in shared memory
 // over the two tiles' border indices (a component crossing the seam at many columns -- the
 // percolating one -- becomes one link), then one global union per linked border component.
-__global__ void __launch_bounds__(TW) k_seam_h(Geo g, Ws ws, int32_t s0, int32_t ns) {
+#ifndef RL_SEAM_THREADS
+#define RL_SEAM_THREADS 64  // small blocks: more seams in flight per SM (latency-bound unions)
+#endif
+constexpr int SEAM_T = RL_SEAM_THREADS;  // threads per seam block (TW / SEAM_T columns each)
+
+__global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int32_t ns) {
     __shared__ uint32_t lp[2 * NBMAX];
     if (ws.counters[1]) return;
     const uint32_t v8 = g.flip ? 0u : 1u;
-    const int32_t tx = blockIdx.x, c = threadIdx.x, x = tx * TW + c;
+    const int32_t tx = blockIdx.x, tid = threadIdx.x;
     for (int32_t bs = blockIdx.y; bs < g.B * ns; bs += gridDim.y) {
         const int32_t s = s0 + bs % ns;
         const int32_t b = bs / ns;
         const int64_t tu = ((int64_t)b * g.nty + s) * g.ntx + tx, tl = tu + g.ntx;
         const int nbu = (int)ws.tnb[tu], nbd = (int)ws.tnb[tl];
-        for (int i = c; i < nbu + nbd; i += TW) lp[i] = (uint32_t)i;
+        for (int i = tid; i < nbu + nbd; i += SEAM_T) lp[i] = (uint32_t)i;
         __syncthreads();
-        if (x < g.W) {
+        for (int c = tid; c < TW; c += SEAM_T) {
+            const int32_t x = tx * TW + c;
+            if (x >= g.W) break;
             const uint16_t lu = ws.perim[tu * PERIM + TW + c], ld = ws.perim[tl * PERIM + c];
             const uint32_t vu = lu >> 15, vd = ld >> 15;
             uint16_t lul = PERIM_NONE, ldl = PERIM_NONE;
@@ -362,7 +369,7 @@ __global__ void __launch_bounds__(TW) k_seam_h(Geo g, Ws ws, int32_t s0, int32_t
         __syncthreads();
         // one global link per border component that joined another one here
         const uint32_t bu = (uint32_t)g.B + ws.tbase[tu], bd = (uint32_t)g.B + ws.tbase[tl];
-        for (int i = c; i < nbu + nbd; i += TW) {
+        for (int i = tid; i < nbu + nbd; i += SEAM_T) {
             uint32_t r = lp[i];
             if (r == (uint32_t)i) continue;
             while (lp[r] != r) r = lp[r];
@@ -1139,7 +1146,7 @@ static int grid_for(int64_t n, int block, int maxgrid) {
 void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms) {
     const int64_t pairs = (int64_t)g.B * ns;
     const dim3 grid(g.ntx, (unsigned)std::min<int64_t>(pairs, 65535));
-    k_seam_h<<<grid, TW, 0, s>>>(g, ws, s0, ns);
+    k_seam_h<<<grid, SEAM_T, 0, s>>>(g, ws, s0, ns);
 }
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
     k_analyze<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
