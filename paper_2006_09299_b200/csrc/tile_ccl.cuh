@@ -75,7 +75,10 @@ using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 #define RL_SE_FCH 192
 #endif
 using CapSE = Cap<CapS::MR, CapS::NBC, 192, RL_SE_FCH, uint16_t, NW>;
-using CapME = Cap<CapM::MR, CapM::NBC, 1024, 640, uint16_t, 2 * NW>;
+#ifndef RL_ME_FCH
+#define RL_ME_FCH 640
+#endif
+using CapME = Cap<CapM::MR, CapM::NBC, 1024, RL_ME_FCH, uint16_t, 2 * NW>;
 using CapFE = Cap<CapF::MR, CapF::NBC, 1024, 320, uint16_t, 2 * NW>;
 
 template <class C>
