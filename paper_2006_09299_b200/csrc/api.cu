@@ -12,6 +12,11 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -95,6 +100,13 @@ int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cf
     return RL_OK;
 }
 
+void set_output_format(Geo& g, int32_t ofmt) {  // the filled-image buffer is cudaMalloc'ed: aligned
+    g.ofmt = ofmt;
+    g.orowb = ofmt == RL_PIXELS_P4 ? (g.W + 7) / 8 : g.W;
+    g.ofbytes = (int64_t)g.orowb * g.H;
+    g.ovec_ok = ofmt == RL_PIXELS_P4 ? (g.orowb % 4) == 0 : (g.W % 16) == 0;
+}
+
 Geo make_geo(int32_t W, int32_t H, int32_t B, const rl_config* cfg, const void* dpix, int32_t fmt) {
     Geo g{};
     g.W = W;
@@ -112,6 +124,7 @@ Geo make_geo(int32_t W, int32_t H, int32_t B, const rl_config* cfg, const void* 
     g.fbytes = (int64_t)g.rowb * H;
     const uintptr_t a = reinterpret_cast<uintptr_t>(dpix);
     g.vec_ok = fmt == RL_PIXELS_P4 ? ((g.rowb % 4) == 0 && (a % 4) == 0) : ((W % 16) == 0 && (a % 16) == 0);
+    set_output_format(g, fmt);
     g.label_mode = cfg->relabel ? (cfg->fill_holes ? 2 : 1) : 0;
     g.ty0 = 0;
     g.ty1 = g.nty;
@@ -141,7 +154,7 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
               ensure(ctx->img_fg, (size_t)B * 4) && ensure(ctx->img_surv, (size_t)B * 4) &&
               ensure(ctx->comps, ctx->cap_comps * sizeof(rl_component)) &&
               ensure(ctx->top, ctx->cap_comps * 4) && ensure(ctx->filled, ctx->cap_comps * sizeof(Acc)) &&
-              ensure(ctx->filled_img, (size_t)(out_px / g.W) * g.rowb) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
+              ensure(ctx->filled_img, (size_t)(out_px / g.W) * g.orowb) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
               ensure(ctx->summ, (size_t)(B + 1) * 32);
     if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)out_px * 4);
     if (!ok) return set_err(ctx, RL_ENOMEM, "device allocation failed");
@@ -205,7 +218,8 @@ void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
 
 // (Re)build geometry, grow the workspace, enqueue the pipeline.
 int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg, int32_t fmt) {
-    const Geo g = make_geo(W, H, B, cfg, dpix, fmt);
+    Geo g = make_geo(W, H, B, cfg, dpix, fmt);
+    if (ctx->force_ofmt >= 0) set_output_format(g, ctx->force_ofmt);
     if (g.ntiles < 0) return set_err(ctx, RL_EINVAL, "too many tiles");
     const int64_t ncnt = (int64_t)B * H * g.ntx + 1;
     Ws ws;
@@ -385,7 +399,9 @@ int finish(rl_ctx* ctx) {
         if (!grow) return RL_OK;
         ctx->reran = true;
         const rl_config cfg = ctx->cfg;
+        ctx->force_ofmt = ctx->geo.ofmt != ctx->geo.fmt ? ctx->geo.ofmt : -1;
         const int rc = enqueue(ctx, ctx->last_pix, ctx->geo.W, ctx->geo.H, ctx->geo.B, &cfg, ctx->geo.fmt);
+        ctx->force_ofmt = -1;
         if (rc) return rc;
     }
     return set_err(ctx, RL_EINTERNAL, "capacity did not converge");
@@ -444,8 +460,8 @@ int fetch(rl_ctx* ctx, rl_result* out) {
     cudaMemcpyAsync(out->top, ctx->ws.top, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(out->filled, ctx->ws.filled, sizeof(rl_features) * total, cudaMemcpyDeviceToHost, st);
     std::vector<uint8_t> p4;
-    if (g.fmt == RL_PIXELS_P4) {  // rl_result holds one byte per pixel: unpack the P4 rows
-        p4.resize((size_t)(g.fbytes * B));
+    if (g.ofmt == RL_PIXELS_P4) {  // rl_result holds one byte per pixel: unpack the P4 rows
+        p4.resize((size_t)(g.ofbytes * B));
         cudaMemcpyAsync(p4.data(), ctx->ws.filled_img, p4.size(), cudaMemcpyDeviceToHost, st);
     } else {
         cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
@@ -459,7 +475,7 @@ int fetch(rl_ctx* ctx, rl_result* out) {
     if (!p4.empty())
         for (int64_t r = 0; r < (int64_t)g.H * B; ++r)
             for (int32_t j = 0; j < g.W; ++j)
-                out->filled_image[r * g.W + j] = (p4[r * g.rowb + j / 8] >> (7 - j % 8)) & 1u;
+                out->filled_image[r * g.W + j] = (p4[r * g.orowb + j / 8] >> (7 - j % 8)) & 1u;
     fill_times(ctx, &out->times);
     return RL_OK;
 }
@@ -469,6 +485,86 @@ int fetch(rl_ctx* ctx, rl_result* out) {
 
 int64_t image_bytes(int32_t w, int32_t h, int32_t fmt) {
     return (int64_t)(fmt == RL_PIXELS_P4 ? (w + 7) / 8 : w) * h;
+}
+
+// ---- host thread pool (expansion of packed filled images) ---------------------------------
+}  // namespace
+namespace rlh {
+struct HostPool {
+    std::vector<std::thread> workers;
+    std::mutex m;
+    std::condition_variable cv, done;
+    std::deque<std::pair<int, std::function<void()>>> q;
+    int pending[8] = {};
+    bool stop = false;
+    explicit HostPool(int n) {
+        for (int i = 0; i < n; ++i) workers.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : workers) t.join();
+    }
+    void loop() {
+        for (;;) {
+            std::pair<int, std::function<void()>> task;
+            {
+                std::unique_lock<std::mutex> lk(m);
+                cv.wait(lk, [&] { return stop || !q.empty(); });
+                if (q.empty()) return;
+                task = std::move(q.front());
+                q.pop_front();
+            }
+            task.second();
+            {
+                std::lock_guard<std::mutex> lk(m);
+                --pending[task.first];
+            }
+            done.notify_all();
+        }
+    }
+    void submit(int tag, std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            ++pending[tag];
+            q.emplace_back(tag, std::move(f));
+        }
+        cv.notify_one();
+    }
+    void wait(int tag) {
+        std::unique_lock<std::mutex> lk(m);
+        done.wait(lk, [&] { return pending[tag] == 0; });
+    }
+};
+void pool_free(rl_ctx* c) {
+    delete c->pool;
+    c->pool = nullptr;
+}
+}  // namespace rlh
+namespace {
+
+// P4 rows -> one byte per pixel (MSB-first bits; binarize_labels' layout, labeling.hpp:354-360)
+void expand_p4_rows(const uint8_t* src, int64_t rows, int32_t rowb, int32_t w, uint8_t* dst) {
+    static const struct Lut {
+        uint64_t v[256];
+        Lut() {
+            for (int b = 0; b < 256; ++b) {
+                uint64_t x = 0;
+                for (int k = 0; k < 8; ++k) x |= (uint64_t)((b >> (7 - k)) & 1) << (8 * k);
+                v[b] = x;
+            }
+        }
+    } lut;
+    const int32_t full = w / 8;
+    for (int64_t r = 0; r < rows; ++r) {
+        const uint8_t* s = src + r * rowb;
+        uint8_t* d = dst + r * w;
+        for (int32_t i = 0; i < full; ++i) std::memcpy(d + 8 * i, &lut.v[s[i]], 8);
+        for (int32_t j = 8 * full; j < w; ++j) d[j] = (s[j / 8] >> (7 - j % 8)) & 1u;
+    }
 }
 
 struct IntoState {
@@ -481,22 +577,55 @@ struct IntoState {
 void copy_fixed_outputs(rl_ctx* c, rl_host_outputs* out, int32_t b0) {
     const Geo& g = c->geo;
     const size_t npx = (size_t)(g.P * g.B), off = (size_t)g.P * b0;
-    if (out->filled_image)
-        cudaMemcpyAsync(out->filled_image + (size_t)g.fbytes * b0, c->ws.filled_img, (size_t)g.fbytes * g.B,
-                        cudaMemcpyDeviceToHost, c->stream);
+    if (out->filled_image) {
+        if (g.ofmt == g.fmt) {
+            cudaMemcpyAsync(out->filled_image + (size_t)g.fbytes * b0, c->ws.filled_img, (size_t)g.fbytes * g.B,
+                            cudaMemcpyDeviceToHost, c->stream);
+        } else {  // packed: into the staging buffer, expanded on the host once the chunk is done
+            cudaMemcpyAsync(c->h_stage, c->ws.filled_img, (size_t)g.ofbytes * g.B, cudaMemcpyDeviceToHost, c->stream);
+        }
+    }
     if (out->labels && g.label_mode)
         cudaMemcpyAsync(out->labels + off, c->ws.labels, npx * 4, cudaMemcpyDeviceToHost, c->stream);
 }
 
+// host expansion of chunk c's packed filled image (after its stream is synchronised)
+void expand_filled(rl_ctx* owner, rl_ctx* c, int tag, rl_host_outputs* out, int32_t b0) {
+    const Geo& g = c->geo;
+    if (!out->filled_image || g.ofmt == g.fmt) return;
+    const int64_t rows = (int64_t)g.H * g.B;
+    const int parts = (int)std::min<int64_t>(std::max<int64_t>(1, rows / 256), 8);
+    for (int k = 0; k < parts; ++k) {
+        const int64_t r0 = rows * k / parts, r1 = rows * (k + 1) / parts;
+        const uint8_t* src = c->h_stage + r0 * g.orowb;
+        uint8_t* dst = out->filled_image + (size_t)g.P * b0 + r0 * g.W;
+        const int32_t rowb = g.orowb, w = g.W;
+        owner->pool->submit(tag, [=] { expand_p4_rows(src, r1 - r0, rowb, w, dst); });
+    }
+}
+
 // H2D of images [b0, b0 + n), the pipeline, and the D2H of the outputs whose size is fixed
 int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
-                 rl_host_outputs* out, int32_t b0, int32_t fmt) {
+                 rl_host_outputs* out, int32_t b0, int32_t fmt, bool packed_out) {
     const size_t npx = (size_t)image_bytes(w, h, fmt) * n;
     if (!ensure(c->pix, npx)) return set_err(c, RL_ENOMEM, "device allocation failed");
     const cudaError_t e = cudaMemcpyAsync(c->pix.p, pixels, npx, cudaMemcpyHostToDevice, c->stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "copy in");
     c->want_compact = out->filled && out->filled_layout == 1;
+    const bool packed = packed_out && out->filled_image && fmt == RL_PIXELS_U8;
+    c->force_ofmt = packed ? RL_PIXELS_P4 : -1;
+    if (packed) {
+        const size_t need = (size_t)image_bytes(w, h, RL_PIXELS_P4) * n;
+        if (c->h_stage_n < need) {
+            if (c->h_stage) cudaFreeHost(c->h_stage);
+            c->h_stage = nullptr;
+            c->h_stage_n = 0;
+            if (cudaMallocHost(&c->h_stage, need) != cudaSuccess) return set_err(c, RL_ENOMEM, "pinned alloc failed");
+            c->h_stage_n = need;
+        }
+    }
     const int rc = enqueue(c, P<uint8_t>(c->pix), w, h, n, cfg, fmt);
+    c->force_ofmt = -1;  // finish() re-runs with the geometry of this call (kept in c->geo)
     if (rc) return rc;
     copy_fixed_outputs(c, out, b0);
     return RL_OK;
@@ -506,8 +635,11 @@ int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t
 int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st) {
     const Geo& g = c->geo;
     const int B = g.B;
-    if (c->reran) copy_fixed_outputs(c, out, b0);  // the pipeline re-ran after the first copies
-    if (out->filled_image) st.d2h += g.fbytes * B;
+    if (c->reran) {  // the pipeline re-ran after the first copies
+        copy_fixed_outputs(c, out, b0);
+        if (g.ofmt != g.fmt) cudaStreamSynchronize(c->stream);  // the staging buffer is expanded next
+    }
+    if (out->filled_image) st.d2h += g.ofbytes * B;
     if (out->labels && g.label_mode) st.d2h += g.P * B * 4;
     const int64_t* s = c->h_summ;
     const int64_t total = s[4 * B];
@@ -581,6 +713,7 @@ rl_ctx* rl_create(int device) {
     c->stream = c->own_stream;
     if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
     if (std::getenv("RUNLAB_GPU_KTIMES")) c->ktimes = true;
+    if (std::getenv("RUNLAB_GPU_NO_PACKED_D2H")) c->packed_d2h = false;
     if (const char* v = std::getenv("RUNLAB_GPU_CHUNK_PX")) c->chunk_px = std::max(1ll, std::atoll(v));
     return c;
 }
@@ -597,6 +730,8 @@ void rl_destroy(rl_ctx* c) {
                       &c->fcomp, &c->nleft, &c->scount};
     for (rl_ctx* k : c->kids) rl_destroy(k);
     strip_free(c);
+    pool_free(c);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_summ) cudaFreeHost(c->h_summ);
@@ -670,15 +805,26 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     if (rc) return rc;
     cudaSetDevice(ctx->device);
     const int64_t P = (int64_t)w * h;
+    // a byte-per-pixel filled image crosses PCIe as P4 bits and is expanded by host threads
+    const bool packed = ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
+    if (packed && !ctx->pool) {
+        const int hw = (int)std::thread::hardware_concurrency();
+        ctx->pool = new (std::nothrow) HostPool(std::max(2, std::min(hw > 0 ? hw : 4, 12)));
+        if (!ctx->pool) return set_err(ctx, RL_ENOMEM, "host thread pool");
+    }
     // whole images per chunk, ~32 Mpx by default (pipelines of that size are graph-replayed)
     const int32_t per = (int32_t)std::min<int64_t>(n, std::max<int64_t>(1, ctx->chunk_px / P));
     const int32_t nch = (n + per - 1) / per;
     IntoState st;
     if (nch == 1) {
-        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt);
+        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed);
         if (!rc) rc = finish(ctx);
         if (!rc) rc = into_post(ctx, out, 0, st);
         if (!rc) rc = into_sync(ctx);
+        if (!rc && packed) {
+            expand_filled(ctx, ctx, 0, out, 0);
+            ctx->pool->wait(0);
+        }
     } else {
         for (rl_ctx*& k : ctx->kids)
             if (!k) {
@@ -689,25 +835,33 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
         auto first_image = [&](int32_t c) { return c * per; };
         auto images = [&](int32_t c) { return std::min(per, n - c * per); };
         // chunk c runs on kid c % NKIDS; its component outputs are copied once its summary is
-        // in, just before the kid takes chunk c + NKIDS (outputs stay in chunk order)
+        // in (finish() synchronises the kid's stream, so its packed filled image is in the
+        // staging buffer and host threads expand it), before the kid takes chunk c + NKIDS
         auto post = [&](int32_t c) -> int {
-            rl_ctx* k = ctx->kids[c % rl_ctx::NKIDS];
+            const int kid = c % rl_ctx::NKIDS;
+            rl_ctx* k = ctx->kids[kid];
             int r = finish(k);
             if (r) return set_err(ctx, r, k->err);
             r = into_post(k, out, first_image(c), st);
+            if (!r && packed) expand_filled(ctx, k, kid, out, first_image(c));
             return r ? set_err(ctx, r, k->err) : RL_OK;
         };
         for (int32_t c = 0; c < nch && !rc; ++c) {
             if (c >= rl_ctx::NKIDS) rc = post(c - rl_ctx::NKIDS);
             if (rc) break;
-            rl_ctx* k = ctx->kids[c % rl_ctx::NKIDS];
+            const int kid = c % rl_ctx::NKIDS;
+            rl_ctx* k = ctx->kids[kid];
+            if (packed) ctx->pool->wait(kid);  // its staging buffer is about to be refilled
             const int32_t b0 = first_image(c);
-            rc = into_enqueue(k, pixels + (size_t)b0 * image_bytes(w, h, fmt), w, h, images(c), cfg, out, b0, fmt);
+            rc = into_enqueue(k, pixels + (size_t)b0 * image_bytes(w, h, fmt), w, h, images(c), cfg, out, b0, fmt,
+                              packed);
             if (rc) rc = set_err(ctx, rc, k->err);
         }
         for (int32_t c = std::max(0, nch - rl_ctx::NKIDS); c < nch && !rc; ++c) rc = post(c);
         for (rl_ctx* k : ctx->kids)
             if (!rc) rc = into_sync(k) ? set_err(ctx, RL_ECUDA, k->err) : RL_OK;
+        if (packed)
+            for (int kid = 0; kid < rl_ctx::NKIDS; ++kid) ctx->pool->wait(kid);
     }
     if (rc) return rc;
     out->comps_needed = st.total;

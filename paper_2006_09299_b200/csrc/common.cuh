@@ -68,9 +68,12 @@ struct Geo {
     // pixel format of the input and of the hole-filled image: 0 = one byte per pixel,
     // 1 = PBM P4 raster rows (MSB-first bits, rows padded to whole bytes, io.hpp:78-154)
     int32_t fmt;
-    int32_t rowb;        // bytes per row of those buffers (W or ceil(W / 8))
-    int32_t pad_;
-    int64_t fbytes;      // bytes per image of those buffers (rowb * H)
+    int32_t rowb;        // bytes per row of the input buffer (W or ceil(W / 8))
+    int32_t ofmt;        // pixel format of the hole-filled image (may differ from the input's)
+    int64_t fbytes;      // bytes per image of the input buffer (rowb * H)
+    int32_t orowb;       // bytes per row of the hole-filled image
+    int32_t ovec_ok;     // vector stores allowed for it
+    int64_t ofbytes;     // bytes per image of the hole-filled image
 };
 
 struct Ws {

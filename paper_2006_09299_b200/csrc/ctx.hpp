@@ -37,6 +37,7 @@ namespace rlh {
 using namespace rlg;
 
 struct StripState;  // strips.cu
+struct HostPool;    // api.cu
 
 struct DevBuf {
     void* p = nullptr;
@@ -109,6 +110,13 @@ struct rl_ctx {
     bool ktimes = false;
     cudaEvent_t kev[24] = {};
     int nkev = 0;
+    // rl_label_into: the filled image crosses PCIe as P4 bits (8x fewer bytes) into this pinned
+    // staging buffer and host threads expand it to bytes (env RUNLAB_GPU_NO_PACKED_D2H: off)
+    bool packed_d2h = true;
+    int32_t force_ofmt = -1;  // output format of the filled image for the next enqueue (-1: input's)
+    uint8_t* h_stage = nullptr;
+    size_t h_stage_n = 0;
+    rlh::HostPool* pool = nullptr;
     // strip mode (strips.cu)
     DevBuf nleft, scount;
     rlh::StripState* strip = nullptr;
@@ -126,9 +134,11 @@ T* P(DevBuf& b) {
 int check_args(rl_ctx* ctx, int32_t w, int32_t h, int32_t n, const rl_config* cfg);
 // Geometry of a batch of n w x h images (all tile rows, no strip offset).
 Geo make_geo(int32_t w, int32_t h, int32_t n, const rl_config* cfg, const void* dpix, int32_t fmt = 0);
+void set_output_format(Geo& g, int32_t ofmt);
 // Grow the workspace for geometry g and fill `ws`; `scan_tmp` = CUB temp bytes of the cnt scan.
 // `out_px` = pixels of the label image buffer; the filled image takes g.fbytes per image
 // (scaled to out_px / P images).
 int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& scan_tmp, int64_t out_px);
 void strip_free(rl_ctx* c);
+void pool_free(rl_ctx* c);
 }  // namespace rlh

@@ -992,13 +992,13 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     RL_PHASE(tg.t, 23);
 
     // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
-    if (vm && g.fmt == 1) {
-        uint8_t* row = ws.filled_img + tg.b * g.fbytes + (tg.y0 + r - g.prow0) * (int64_t)g.rowb;
-        p4_store_word(row, g.rowb, (tg.x0 >> 5) + w, vm & ~E.ext[tid], g.vec_ok);
+    if (vm && g.ofmt == 1) {
+        uint8_t* row = ws.filled_img + tg.b * g.ofbytes + (tg.y0 + r - g.prow0) * (int64_t)g.orowb;
+        p4_store_word(row, g.orowb, (tg.x0 >> 5) + w, vm & ~E.ext[tid], g.ovec_ok);
     } else if (vm) {
         const uint32_t fillbits = vm & ~E.ext[tid];
-        uint8_t* dst = ws.filled_img + tg.b * g.fbytes + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
-        if (g.vec_ok && vm == 0xFFFFFFFFu) {
+        uint8_t* dst = ws.filled_img + tg.b * g.ofbytes + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
+        if (g.ovec_ok && vm == 0xFFFFFFFFu) {
             uint4 o0, o1;
             o0.x = nibble_to_bytes(fillbits & 0xF);
             o0.y = nibble_to_bytes((fillbits >> 4) & 0xF);
