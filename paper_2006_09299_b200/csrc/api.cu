@@ -582,7 +582,8 @@ void copy_fixed_outputs(rl_ctx* c, rl_host_outputs* out, int32_t b0) {
             cudaMemcpyAsync(out->filled_image + (size_t)g.fbytes * b0, c->ws.filled_img, (size_t)g.fbytes * g.B,
                             cudaMemcpyDeviceToHost, c->stream);
         } else {  // packed: into the staging buffer, expanded on the host once the chunk is done
-            cudaMemcpyAsync(c->h_stage, c->ws.filled_img, (size_t)g.ofbytes * g.B, cudaMemcpyDeviceToHost, c->stream);
+            cudaMemcpyAsync(c->h_stage[c->stage], c->ws.filled_img, (size_t)g.ofbytes * g.B, cudaMemcpyDeviceToHost,
+                            c->stream);
         }
     }
     if (out->labels && g.label_mode)
@@ -597,7 +598,7 @@ void expand_filled(rl_ctx* owner, rl_ctx* c, int tag, rl_host_outputs* out, int3
     const int parts = (int)std::min<int64_t>(std::max<int64_t>(1, rows / 256), 8);
     for (int k = 0; k < parts; ++k) {
         const int64_t r0 = rows * k / parts, r1 = rows * (k + 1) / parts;
-        const uint8_t* src = c->h_stage + r0 * g.orowb;
+        const uint8_t* src = c->h_stage[c->stage] + r0 * g.orowb;
         uint8_t* dst = out->filled_image + (size_t)g.P * b0 + r0 * g.W;
         const int32_t rowb = g.orowb, w = g.W;
         owner->pool->submit(tag, [=] { expand_p4_rows(src, r1 - r0, rowb, w, dst); });
@@ -616,12 +617,13 @@ int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t
     c->force_ofmt = packed ? RL_PIXELS_P4 : -1;
     if (packed) {
         const size_t need = (size_t)image_bytes(w, h, RL_PIXELS_P4) * n;
-        if (c->h_stage_n < need) {
-            if (c->h_stage) cudaFreeHost(c->h_stage);
-            c->h_stage = nullptr;
-            c->h_stage_n = 0;
-            if (cudaMallocHost(&c->h_stage, need) != cudaSuccess) return set_err(c, RL_ENOMEM, "pinned alloc failed");
-            c->h_stage_n = need;
+        const int sb = c->stage;
+        if (c->h_stage_n[sb] < need) {
+            if (c->h_stage[sb]) cudaFreeHost(c->h_stage[sb]);
+            c->h_stage[sb] = nullptr;
+            c->h_stage_n[sb] = 0;
+            if (cudaMallocHost(&c->h_stage[sb], need) != cudaSuccess) return set_err(c, RL_ENOMEM, "pinned alloc failed");
+            c->h_stage_n[sb] = need;
         }
     }
     const int rc = enqueue(c, P<uint8_t>(c->pix), w, h, n, cfg, fmt);
@@ -731,7 +733,8 @@ void rl_destroy(rl_ctx* c) {
     for (rl_ctx* k : c->kids) rl_destroy(k);
     strip_free(c);
     pool_free(c);
-    if (c->h_stage) cudaFreeHost(c->h_stage);
+    for (uint8_t* p : c->h_stage)
+        if (p) cudaFreeHost(p);
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_summ) cudaFreeHost(c->h_summ);
@@ -843,7 +846,7 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
             int r = finish(k);
             if (r) return set_err(ctx, r, k->err);
             r = into_post(k, out, first_image(c), st);
-            if (!r && packed) expand_filled(ctx, k, kid, out, first_image(c));
+            if (!r && packed) expand_filled(ctx, k, 2 * kid + k->stage, out, first_image(c));
             return r ? set_err(ctx, r, k->err) : RL_OK;
         };
         for (int32_t c = 0; c < nch && !rc; ++c) {
@@ -851,7 +854,10 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
             if (rc) break;
             const int kid = c % rl_ctx::NKIDS;
             rl_ctx* k = ctx->kids[kid];
-            if (packed) ctx->pool->wait(kid);  // its staging buffer is about to be refilled
+            if (packed) {  // alternate the kid's staging buffers; wait for the older one's expansion
+                k->stage ^= 1;
+                ctx->pool->wait(2 * kid + k->stage);
+            }
             const int32_t b0 = first_image(c);
             rc = into_enqueue(k, pixels + (size_t)b0 * image_bytes(w, h, fmt), w, h, images(c), cfg, out, b0, fmt,
                               packed);
@@ -861,7 +867,7 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
         for (rl_ctx* k : ctx->kids)
             if (!rc) rc = into_sync(k) ? set_err(ctx, RL_ECUDA, k->err) : RL_OK;
         if (packed)
-            for (int kid = 0; kid < rl_ctx::NKIDS; ++kid) ctx->pool->wait(kid);
+            for (int tag = 0; tag < 2 * rl_ctx::NKIDS; ++tag) ctx->pool->wait(tag);
     }
     if (rc) return rc;
     out->comps_needed = st.total;

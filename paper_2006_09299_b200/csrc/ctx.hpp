@@ -114,8 +114,9 @@ struct rl_ctx {
     // staging buffer and host threads expand it to bytes (env RUNLAB_GPU_NO_PACKED_D2H: off)
     bool packed_d2h = true;
     int32_t force_ofmt = -1;  // output format of the filled image for the next enqueue (-1: input's)
-    uint8_t* h_stage = nullptr;
-    size_t h_stage_n = 0;
+    uint8_t* h_stage[2] = {nullptr, nullptr};  // alternating: one may still be expanding
+    size_t h_stage_n[2] = {0, 0};
+    int stage = 0;  // the buffer the last enqueue copies into
     rlh::HostPool* pool = nullptr;
     // strip mode (strips.cu)
     DevBuf nleft, scount;
