@@ -197,6 +197,8 @@ int rl_phase_times(const rl_ctx* ctx, int back, rl_times* out);
  * generate() (generator.hpp:46-83).  stream: cudaStream_t or NULL; d_out: w*h bytes. */
 int rl_generate(void* stream, uint8_t* d_out, int32_t w, int32_t h, double density, int32_t g,
                 uint64_t seed);
+/* The same into a host buffer of w*h bytes (synchronous). */
+int rl_generate_host(uint8_t* out, int32_t w, int32_t h, double density, int32_t g, uint64_t seed);
 /* Rows [y0, y0 + rows) of the same image (d_out: w*rows bytes; one strip of a large image). */
 int rl_generate_rows(void* stream, uint8_t* d_out, int32_t w, int32_t h, int32_t y0, int32_t rows,
                      double density, int32_t g, uint64_t seed);

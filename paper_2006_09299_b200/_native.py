@@ -24,7 +24,7 @@ EXPORTED_SYMBOLS = (
     "rl_strip_local", "rl_strip_export_bytes", "rl_strip_export", "rl_strip_merge", "rl_strip_finish",
     "rl_strip_fetch", "rl_generate_rows", "rl_filter_components",
     "rl_filter_components_host", "rl_label_device_fmt", "rl_label_into_fmt", "rl_pbm_parse", "rl_pbm_p1_to_p4",
-    "rl_pbm_p4_header", "rl_fill_pbm",
+    "rl_pbm_p4_header", "rl_fill_pbm", "rl_generate_host",
 )
 
 FEATURE_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),

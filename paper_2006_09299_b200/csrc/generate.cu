@@ -127,6 +127,21 @@ int rl_generate(void* stream, uint8_t* d_out, int32_t w, int32_t h, double densi
     return rl_generate_rows(stream, d_out, w, h, 0, h, density, g, seed);
 }
 
+// host-buffer variant (generated on the device, copied back)
+int rl_generate_host(uint8_t* out, int32_t w, int32_t h, double density, int32_t g, uint64_t seed) {
+    if (!out || w < 1 || h < 1) return RL_EINVAL;
+    uint8_t* d = nullptr;
+    const size_t n = (size_t)w * h;
+    if (cudaMalloc(&d, n) != cudaSuccess) {
+        cudaGetLastError();
+        return RL_ENOMEM;
+    }
+    int rc = rl_generate(nullptr, d, w, h, density, g, seed);
+    if (rc == RL_OK && cudaMemcpy(out, d, n, cudaMemcpyDeviceToHost) != cudaSuccess) rc = RL_ECUDA;
+    cudaFree(d);
+    return rc;
+}
+
 int rl_generate_rings(void* stream, uint8_t* d_out, int32_t w, int32_t h, int32_t tile, uint64_t seed,
                       double salt) {
     if (w < 1 || h < 1 || tile < 4 || salt < 0.0 || salt >= 1.0) return RL_EINVAL;

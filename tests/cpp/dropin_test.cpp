@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "runlab_gpu.hpp"
+#include "runlab_gpu_io.hpp"
 
 using namespace runlab;
 
@@ -138,6 +139,62 @@ int main() {
             threw = true;
         }
         CHECK(threw);
+    }
+    // test_io.cpp:64-132 restated with canonical ids (the Fig. 3 hole is component 2, the
+    // reference's provisional root label is 6)
+    {
+        LabelImage li(1, 1);
+        CHECK(write_label_image(li, LabelFormat::pgm16) == std::string("P5\n1 1\n65535\n") + '\0' + '\0');
+        li.labels[0] = 0x0102;
+        const std::string two = write_label_image(li, LabelFormat::pgm16);
+        CHECK(two.substr(two.size() - 2) == std::string("\x01\x02"));
+        li.labels[0] = 65536;
+        bool threw = false;
+        try {
+            write_label_image(li, LabelFormat::pgm16);
+        } catch (const std::overflow_error&) {
+            threw = true;
+        }
+        CHECK(threw);
+        LabelingConfig cfg;
+        cfg.relabel = true;
+        cfg.fill_holes = true;
+        const std::string csv = write_label_image(*label_image(fig, cfg).labels, LabelFormat::csv);
+        std::size_t pos = 0;
+        for (int skip = 0; skip < 3; ++skip) pos = csv.find('\n', pos) + 1;
+        CHECK(csv.substr(pos, csv.find('\n', pos) - pos) == "0,1,0,1,1,1,0,0,0,1,1,1,0,1,0");
+        LabelingConfig fc;
+        fc.compute_features = true;
+        const auto recs = components(label_image(fig, fc));
+        const std::string fcsv = write_features_csv(recs);
+        CHECK(fcsv.substr(0, fcsv.find('\n')) == "root,parity,parent,s,sx,sy,rmin,rmax,cmin,cmax");
+        CHECK(fcsv.find("\n1,FG,0,56,") != std::string::npos);
+        CHECK(fcsv.find("\n2,BG,1,11,") != std::string::npos);
+        CHECK(fcsv.substr(fcsv.find('\n') + 1, 5) == "0,BG,");
+        const std::string dense = write_features_csv(recs, true);
+        CHECK(dense.substr(0, dense.find('\n')) == "root,parity,parent,s,sx,sy,rmin,rmax,cmin,cmax,dense");
+        const ComponentTree tree = adjacency_tree(label_image(fig, fc));
+        CHECK(write_tree(tree, TreeFormat::dot) == "digraph components {\n  0;\n  1;\n  2;\n  1 -> 0;\n  2 -> 1;\n}\n");
+        const std::string json = write_tree(tree, TreeFormat::json);
+        CHECK(json.find("\"label\":1") != std::string::npos && json.find("\"s\":56") != std::string::npos);
+        CHECK(json.find("\"bbox\":[3,5,4,10]") != std::string::npos);
+        const ComponentTree empty = adjacency_tree(label_image(make_image({"00", "00"}), fc));
+        CHECK(write_tree(empty, TreeFormat::json) ==
+              "{\"label\":0,\"parity\":\"BG\",\"s\":4,\"sx\":2,\"sy\":2,\"bbox\":[0,1,0,1],\"children\":[]}\n");
+        // PBM round trips and the device fill path (`runlab fill`)
+        CHECK(read_pbm(write_pbm(fig, PbmFormat::p1)) == fig && read_pbm(write_pbm(fig, PbmFormat::p4)) == fig);
+        LabelingConfig fl;
+        fl.fill_holes = true;
+        fl.relabel = true;
+        const LabelingResult fr = label_image(fig, fl);
+        CHECK(fill_pbm(write_pbm(fig, PbmFormat::p4)) == write_pbm(binarize_labels(*fr.labels, fr.equivalences)));
+        bool threw2 = false;
+        try {
+            read_pbm("P4\n9 2\n\x80\xff");
+        } catch (const PbmParseError& e) {
+            threw2 = e.byte_offset == 9;
+        }
+        CHECK(threw2);
     }
     // timed_label_image gives identical results (test_bench.cpp:31-60)
     {
