@@ -708,6 +708,8 @@ struct EmitSmem {
     int32_t prmin[FOLD_SLOTS], prmax[FOLD_SLOTS], pcmin[FOLD_SLOTS], pcmax[FOLD_SLOTS];
     uint32_t ext[NW];       // exterior-pixel masks of the tile words
     uint32_t rowoff[TH];    // canonical id offset of each tile row (relative to the image)
+    uint16_t dfold[C::FCH];  // chunk components whose post-fill root is an interior survivor
+    int ndfold;
     uint64_t cb;
     unsigned long long moff;  // offset of the tile's component map
     int gate;                 // the merge phase succeeded (no capacity overflow)
@@ -908,7 +910,11 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         }
         __syncthreads();
         RL_PHASE(tg.t, 20);
-        // pre-fill records, post-fill roots, survivor init
+        // pre-fill records, post-fill roots, survivor init; folds into border-component roots
+        // (initialised by the merge phase) go to the shared table right away, folds into
+        // interior survivors wait until the survivors' own records are written (barrier)
+        if (tid == 0) E.ndfold = 0;
+        __syncthreads();
         for (int lc = l0 + tid; lc < l1; lc += BT) {
             if (lc_is_border(S, lc)) continue;
             const int k = lc - l0;
@@ -934,20 +940,8 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             if (anc == cid) {
                 ws.filled[cb + cid] = c.f;
                 ++nsurv;
+                continue;
             }
-        }
-        __syncthreads();
-        RL_PHASE(tg.t, 21);
-        // fold non-survivors into their post-fill root
-        for (int lc = l0 + tid; lc < l1; lc += BT) {
-            if (lc_is_border(S, lc)) continue;
-            const int k = lc - l0;
-            int end;
-            uint32_t surv;
-            const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
-            const uint32_t cid = comp_cid(E, (uint32_t)lc);
-            if (anc == cid) continue;
-            const int fr = lc_row(S, lc);
             const int slot = end >= 0 ? fold_slot(E, (uint32_t)end) : -1;
             if (slot >= 0) {
                 atomicAdd(&E.ps[slot], E.fs[k]);
@@ -957,18 +951,29 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
                 atomicMax(&E.prmax[slot], E.frmax[k]);
                 atomicMin(&E.pcmin[slot], E.fcmin[k]);
                 atomicMax(&E.pcmax[slot], E.fcmax[k]);
+            } else if (end >= 0) {
+                acc_atomic_fold(ws.filled + cb + anc, c.f);  // border root, table full
             } else {
-                Acc f;
-                const int64_t s = E.fs[k];
-                f.s = s;
-                f.sx = (int64_t)E.fsx[k] + s * tg.x0;
-                f.sy = (int64_t)E.fsy[k] + s * tg.y0;
-                f.row_min = tg.y0 + fr;
-                f.row_max = tg.y0 + E.frmax[k];
-                f.col_min = tg.x0 + E.fcmin[k];
-                f.col_max = tg.x0 + E.fcmax[k];
-                acc_atomic_fold(ws.filled + cb + anc, f);
+                E.dfold[atomicAdd(&E.ndfold, 1)] = (uint16_t)lc;
             }
+        }
+        __syncthreads();
+        RL_PHASE(tg.t, 21);
+        for (int q = tid; q < E.ndfold; q += BT) {  // folds into interior survivors
+            const int lc = E.dfold[q], k = lc - l0;
+            int end;
+            uint32_t surv;
+            const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
+            Acc f;
+            const int64_t s = E.fs[k];
+            f.s = s;
+            f.sx = (int64_t)E.fsx[k] + s * tg.x0;
+            f.sy = (int64_t)E.fsy[k] + s * tg.y0;
+            f.row_min = tg.y0 + lc_row(S, lc);
+            f.row_max = tg.y0 + E.frmax[k];
+            f.col_min = tg.x0 + E.fcmin[k];
+            f.col_max = tg.x0 + E.fcmax[k];
+            acc_atomic_fold(ws.filled + cb + anc, f);
         }
         __syncthreads();
         RL_PHASE(tg.t, 22);

@@ -101,8 +101,11 @@ struct CclSmem {
         uint16_t evq[NWARPS][C::EVC];  // union-event queues (dead before lcrun/lcb are written)
     };
     uint16_t blc[C::NBC];      // border index -> tile component
-    uint32_t rmask[C::MR / 32 + 1];  // root runs of each 32-run block (ballot)
-    uint16_t rpre[C::MR / 32 + 1];   // root runs before each block
+    // analyze pass only (32-bit parents): root runs of each 32-run block (ballot), and the
+    // root runs before each block
+    static constexpr int RB = std::is_same<typename C::PT, uint32_t>::value ? C::MR / 32 + 1 : 1;
+    uint32_t rmask[RB];
+    uint16_t rpre[RB];
     int wsum[C::BT / 32 + 1];
     int qtot[NWARPS];          // union events queued by each word warp
     int nruns, nlc, nb;
