@@ -318,7 +318,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launch_cids(g, ws, s, ctx->sms);
     kt();
     launch_tree(g, ws, s, ctx->sms, hint);
-    launches += 2 + 1 + 1 + 2;
+    launches += 2 + 1 + 1 + 1;
     kt();
     record_event(ctx->ev[2], s, use_graph);
     launch_emit(g, ws, s);

@@ -514,18 +514,53 @@ __device__ __forceinline__ bool comps_fit(const Geo& g, const Ws& ws) {
 // one warp per tile: canonical ids of the tile's border representatives.  The tile's border
 // components are in raster order of first pixel, so "representatives before me in my row"
 // is a prefix count inside the run of equal rows (match_any) plus a carry across chunks.
+// root node of the component surrounding node n's component: the pixel left of its first
+// pixel (same tile, the left tile's right column, or the image frame)
+__device__ __forceinline__ uint32_t surrounding_root(const Geo& g, const Ws& ws, uint32_t n, const NodeRec& rec,
+                                                     int32_t b) {
+    if (ws.nleft) return ws.uf[ws.nleft[n]];  // strip mode: resolved before the exchange
+    if (rec.leftkind == 0) return ws.uf[(uint32_t)g.B + ws.tbase[rec.tile] + rec.left];
+    if (rec.leftkind == 1) {
+        const uint32_t tl = rec.tile - 1;
+        const uint16_t lab = ws.perim[(int64_t)tl * PERIM + 2 * TW + TH + rec.left];
+        return ws.uf[(uint32_t)g.B + ws.tbase[tl] + (lab & 0x7FFFu)];
+    }
+    if (rec.leftkind == 2) return (uint32_t)b;
+    atomicOr(&ws.counters[1], ERR_INTERNAL);
+    return (uint32_t)b;
+}
+
+// One warp per tile: canonical ids of the tile's border representatives (the tile's border
+// components are in raster order of first pixel, so "representatives before me in my row" is
+// a prefix count inside the run of equal rows plus a carry across chunks), their surrounding
+// components and pre-fill records (the parent id is filled in by k_tops, once every class has
+// its id).  Children of the exterior survive hole filling and start their post-fill features.
 __global__ void k_cids(Geo g, Ws ws) {
     if (ws.counters[1]) return;
+    const bool fit = comps_fit(g, ws);
     const int lane = threadIdx.x & 31;
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (fit && gid < g.B) {  // exterior records (the exterior survives hole filling)
+        const uint64_t cb = comp_base(g, ws, gid);
+        rl_component c;
+        c.f = ws.nacc[gid];
+        c.parent = 0xFFFFFFFFu;
+        c.flags = 0;
+        ws.comps[cb] = c;
+        ws.top[cb] = 0;
+        ws.filled[cb] = c.f;
+        atomicAdd(&ws.img_surv[gid], 1u);
+    }
     const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < g.ntiles; t += warps) {
+    for (int32_t t = gid >> 5; t < g.ntiles; t += warps) {
         int32_t b, ty, tx;
         tile_of(g, (uint32_t)t, b, ty, tx);
         const uint32_t nb = ws.tnb[t];
         const uint32_t n0 = (uint32_t)g.B + ws.tbase[t];
         const int64_t img0 = (int64_t)b * g.H * g.ntx;
         const uint32_t offimg = ws.off[img0];
-        int carry_row = -1, carry = 0;
+        const uint64_t cb = (uint64_t)offimg + (uint64_t)b;
+        int carry_row = -1, carry = 0, nsurv = 0;
         for (uint32_t i0 = 0; i0 < nb; i0 += 32) {
             const uint32_t i = i0 + lane;
             const bool valid = i < nb;
@@ -541,7 +576,22 @@ __global__ void k_cids(Geo g, Ws ws) {
                 const NodeRec rec = ws.nrec[n];
                 const uint32_t cid = 1u + (ws.off[img0 + (int64_t)(ty * TH + rec.fr) * g.ntx + tx] - offimg) +
                                      rec.ibefore + (uint32_t)before;
-                ws.nrootcid[ws.uf[n]] = cid;
+                const uint32_t root = ws.uf[n];
+                ws.nrootcid[root] = cid;
+                const uint32_t proot = surrounding_root(g, ws, n, rec, b);
+                ws.nparent[root] = proot;
+                if (fit) {
+                    rl_component c;
+                    c.f = ws.nacc[root];
+                    c.parent = 0;  // k_tops
+                    c.flags = rec.fg;
+                    ws.comps[cb + cid] = c;
+                    if (proot < (uint32_t)g.B) {
+                        // strip mode: this rank's partial post-fill sums start empty (strips.cu)
+                        ws.filled[cb + cid] = g.strip ? acc_empty() : c.f;
+                        ++nsurv;
+                    }
+                }
             }
             // carry for the next chunk: reps of the chunk's last row (continuing rows only)
             const int last_row = __shfl_sync(0xFFFFFFFFu, row, 31);
@@ -550,66 +600,15 @@ __global__ void k_cids(Geo g, Ws ws) {
             carry = (last_row == carry_row ? carry : 0) + cnt_last;
             carry_row = last_row;
         }
+        nsurv = __reduce_add_sync(0xFFFFFFFFu, nsurv);
+        if (lane == 0 && nsurv) atomicAdd(&ws.img_surv[b], (uint32_t)nsurv);
     }
 }
 
-__global__ void k_parents(Geo g, Ws ws) {
-    if (ws.counters[1] || !comps_fit(g, ws)) return;
-    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid < g.B) {  // exterior records (the exterior survives hole filling)
-        const uint64_t cb = comp_base(g, ws, gid);
-        rl_component c;
-        c.f = ws.nacc[gid];
-        c.parent = 0xFFFFFFFFu;
-        c.flags = 0;
-        ws.comps[cb] = c;
-        ws.top[cb] = 0;
-        ws.filled[cb] = c.f;
-        atomicAdd(&ws.img_surv[gid], 1u);
-    }
-    NODE_LOOP(n) {
-        if (!ws.nrep[n]) continue;
-        const uint32_t root = ws.uf[n];
-        const NodeRec rec = ws.nrec[n];
-        int32_t b, ty, tx;
-        tile_of(g, rec.tile, b, ty, tx);
-        uint32_t proot;
-        if (ws.nleft) {  // strip mode: resolved before the exchange (k_strip_left)
-            proot = ws.uf[ws.nleft[n]];
-        } else if (rec.leftkind == 0) {
-            proot = ws.uf[(uint32_t)g.B + ws.tbase[rec.tile] + rec.left];
-        } else if (rec.leftkind == 1) {
-            const uint32_t tl = rec.tile - 1;
-            const uint16_t lab = ws.perim[(int64_t)tl * PERIM + 2 * TW + TH + rec.left];
-            proot = ws.uf[(uint32_t)g.B + ws.tbase[tl] + (lab & 0x7FFFu)];
-        } else if (rec.leftkind == 2) {
-            proot = (uint32_t)b;
-        } else {
-            atomicOr(&ws.counters[1], ERR_INTERNAL);
-            continue;
-        }
-        ws.nparent[root] = proot;
-        const uint32_t cid = ws.nrootcid[root];
-        const uint64_t cb = comp_base(g, ws, b);
-        rl_component c;
-        c.f = ws.nacc[root];
-        c.parent = ws.nrootcid[proot];
-        c.flags = rec.fg;
-        ws.comps[cb + cid] = c;
-        if (proot < (uint32_t)g.B) {
-            // a child of the exterior survives hole filling: its post-fill features start as
-            // its own (strip mode: this rank's partial sums start empty, strips.cu)
-            ws.filled[cb + cid] = g.strip ? acc_empty() : c.f;
-            const uint32_t active = __activemask();  // survivors per image, warp-aggregated
-            const uint32_t same = __match_any_sync(active, b);
-            if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u)) atomicAdd(&ws.img_surv[b], (uint32_t)__popc(same));
-        }
-    }
-}
 
 // post-fill roots (depth-1 ancestors) of the border components; non-survivors fold their
 // features into their root right away (block-aggregated; the survivors were initialised by
-// k_parents).  Strip mode folds later, after the cross-rank reduction (k_fold).
+// k_cids).  Strip mode folds later, after the cross-rank reduction (k_fold).
 __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
     __shared__ FoldTable<FT_SLOTS> T;
     if (ws.counters[1] || !comps_fit(g, ws)) return;
@@ -640,6 +639,7 @@ __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
             const uint64_t cb = comp_base(g, ws, b);
             const uint32_t cid = ws.nrootcid[root];
             ws.top[cb + cid] = anc;
+            ws.comps[cb + cid].parent = ws.nrootcid[ws.nparent[root]];
             if (cur != root && !g.strip) {
                 dst = (uint32_t)(cb + anc);  // < 2^32 components
                 f = ws.nacc[root];
@@ -1183,15 +1183,13 @@ void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
 void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
     k_cids<<<grid_for((int64_t)g.ntiles * 32, 256, sms * 16), 256, 0, s>>>(g, ws);
 }
+// (the surrounding components and pre-fill records of border components come from k_cids)
 void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
     const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;
-    k_parents<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
     k_tops<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);  // folds too (single-GPU path)
 }
 void launch_tree_parts(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
-    const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;
-    k_parents<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
-    k_tops<<<grid_for(n, 256, sms * 8), 256, 0, s>>>(g, ws);
+    launch_tree(g, ws, s, sms, nodes_hint);  // strip mode: k_tops skips the folds (g.strip)
 }
 void launch_fold(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
     const int64_t n = nodes_hint > g.B ? nodes_hint : g.B;

@@ -418,7 +418,7 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
         launch_reps(gm, ws, s, ctx->sms, n_total);
         cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ws.cnt, ws.off, (int)ncnt, s);
         launch_cids(gm, ws, s, ctx->sms);
-        launch_tree_parts(gm, ws, s, ctx->sms, n_total);  // parents + tops (no fold yet)
+        launch_tree_parts(gm, ws, s, ctx->sms, n_total);  // post-fill roots (no fold yet)
         // ---- emit this strip's tiles; interior survivors are counted into a private counter
         Ws we = ws;
         if (!ensure(ctx->scount, 64)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
@@ -468,7 +468,7 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
         S->merged = true;
         // unpack x n, exterior, cut seams, resolve, reps, scan x 2, cids, parents, tops, emit x 3,
         // flags, scan x 2, summary, partials, count
-        ctx->launches += n_strips + 1 + (n_strips - 1) + 16;
+        ctx->launches += n_strips + 1 + (n_strips - 1) + 15;
         return RL_OK;
     }
     return set_err(ctx, RL_EINTERNAL, "capacity did not converge");
