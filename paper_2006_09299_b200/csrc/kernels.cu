@@ -778,7 +778,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     const bool word = BT == NW || tid < NW;
     const uint16_t* hdr = ws.thdr + (int64_t)tg.t * THDR;
     const int nb_h = hdr[2];
-    if ((int)hdr[0] > C::MR || nb_h > C::NBC) return false;  // a larger class owns it
+    if ((int)hdr[0] > C::MR || (int)hdr[1] > C::NLC || nb_h > C::NBC) return false;  // a larger class owns it
     // every global load the prologue needs is issued before the first barrier: bits, row
     // offsets, header rows, map offset, and the border components' ids (node -> root -> ids)
     const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;

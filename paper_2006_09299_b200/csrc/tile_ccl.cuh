@@ -53,9 +53,10 @@ __device__ int g_phase_n = 0;
 // EVC = union-event queue per warp; longer queues are processed in rounds.
 // BT = threads per CTA: one per word (256) for the sparse class; the dense classes add a second
 // thread per word so that their per-run and per-component loops run twice as wide.
-template <int MR_, int NBC_, int EVC_, int FCH_, class PT_, int BT_>
+template <int MR_, int NBC_, int EVC_, int FCH_, class PT_, int BT_, int NLC_ = MR_>
 struct Cap {
     static constexpr int MR = MR_;
+    static constexpr int NLC = NLC_;  // tile components (a tile with more goes to the next class)
     static constexpr int NBC = NBC_;
     static constexpr int EVC = EVC_;
     static constexpr int FCH = FCH_;  // interior-feature accumulator chunk (emit pass)
@@ -67,14 +68,17 @@ struct Cap {
 #ifndef RL_S_MR
 #define RL_S_MR 2048  // 3072 and 1280 measured slower on config 2
 #endif
-using CapS = Cap<RL_S_MR, NBMAX / 2, 192, 512, uint32_t, NW>;
+#ifndef RL_S_NLC
+#define RL_S_NLC 960  // keeps the class-S tables within 8 CTAs per SM
+#endif
+using CapS = Cap<RL_S_MR, NBMAX / 2, 192, 512, uint32_t, NW, RL_S_NLC>;
 using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 384, uint32_t, 2 * NW>;
 using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 // emit pass: same classes, no unions (16-bit component map, larger feature chunks)
 #ifndef RL_SE_FCH
 #define RL_SE_FCH 192
 #endif
-using CapSE = Cap<CapS::MR, CapS::NBC, 192, RL_SE_FCH, uint16_t, NW>;
+using CapSE = Cap<CapS::MR, CapS::NBC, 192, RL_SE_FCH, uint16_t, NW, CapS::NLC>;
 #ifndef RL_ME_FCH
 #define RL_ME_FCH 640
 #endif
@@ -95,8 +99,8 @@ struct CclSmem {
     typename C::PT par[MR];    // union-find parent; then TAG | component of each run
     union {
         struct {
-            uint16_t lcrun[MR];     // root (first) run of each tile component
-            uint16_t lcb[MR];       // border index, or 0x8000 | (border components before it)
+            uint16_t lcrun[C::NLC];  // root (first) run of each tile component
+            uint16_t lcb[C::NLC];    // border index, or 0x8000 | (border components before it)
         };
         uint16_t evq[NWARPS][C::EVC];  // union-event queues (dead before lcrun/lcb are written)
     };
@@ -467,6 +471,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
         const int pre = block_excl_scan<BT>(tid < nblk ? __popc(S.rmask[tid]) : 0, S.wsum, nlc);
         if (tid < nblk) S.rpre[tid] = (uint16_t)pre;
     }
+    if (nlc > C::NLC) return false;  // more components than this class holds (uniform)
     auto rank_of = [&](uint32_t root) {  // valid once rpre is visible
         return (uint32_t)S.rpre[root >> 5] + __popc(S.rmask[root >> 5] & ((1u << (root & 31)) - 1u));
     };
