@@ -1046,7 +1046,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
 }
 
 // class S on the full grid (tiles of larger classes are skipped), M over list A, F over list B
-__global__ void __launch_bounds__(NT) k_emit(Geo g, Ws ws) {
+__global__ void __launch_bounds__(NT, 8) k_emit(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& E = *reinterpret_cast<EmitSmem<CapSE>*>(smem_raw);
     emit_tile(E, g, ws, tile_geom_grid(g));
