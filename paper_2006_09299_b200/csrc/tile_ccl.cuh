@@ -348,45 +348,21 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     // finds are short: every run walks its chain to the root and links to it directly.  The
     // walks run concurrently; a link read mid-walk is either the original one or a root
     // already written by another walker, both ancestors, so walks only get shorter.  (Row
-    // groups with a barrier between them, RPS < TH, and pointer jumping, RPS = 0, were
-    // measured slower on config 2.)
-#ifndef RL_PREFLAT_RPS
-#define RL_PREFLAT_RPS TH
-#endif
-    if constexpr (RL_PREFLAT_RPS > 0) {
-        // row groups top-down: runs above the group already point at their roots, so a run
-        // walks at most RPS first-contact links inside its group, then takes its root
-        constexpr int RPS = RL_PREFLAT_RPS;
+    // groups with a barrier between them and pointer-jumping rounds were measured slower.)
+    {
         const int nr = S.nruns;
-        for (int r0 = 1; r0 < tg.th; r0 += RPS) {
-            const int rs = S.rbase[r0 * WPR];
-            const int re = r0 + RPS < tg.th ? S.rbase[(r0 + RPS) * WPR] : nr;
-            for (int i = rs + tid; i < re; i += BT) {
-                uint32_t p = S.par[i];
-                if (p == (uint32_t)i) continue;  // no first contact: a root
-                while (p >= (uint32_t)rs) {      // links inside the group (final roots written
-                    const uint32_t q = S.par[p];  // concurrently are ancestors too)
-                    if (q == p) break;
-                    p = q;
-                }
-                S.par[i] = p < (uint32_t)rs ? S.par[p] : p;
+        const int rs = tg.th > 1 ? S.rbase[WPR] : nr;  // runs of row 0 have no first contact
+        for (int i = rs + tid; i < nr; i += BT) {
+            uint32_t p = S.par[i];
+            if (p == (uint32_t)i) continue;  // no first contact: a root
+            for (;;) {
+                const uint32_t q = S.par[p];
+                if (q == p) break;
+                p = q;
             }
-            __syncthreads();
+            S.par[i] = (uint16_t)p;
         }
-    } else {
-        const int nr = S.nruns;
-        for (;;) {
-            int changed = 0;
-            for (int i = tid; i < nr; i += BT) {
-                const uint32_t p = S.par[i];
-                const uint32_t gp = S.par[p];
-                if (gp != p) {
-                    S.par[i] = (uint16_t)gp;
-                    changed = 1;
-                }
-            }
-            if (!__syncthreads_or(changed)) break;
-        }
+        __syncthreads();
     }
     RL_PHASE(tg.t, 3);
     // compact the warp's events into its queue (in rounds of EVC) and resolve them lane-parallel
