@@ -141,5 +141,8 @@ void set_output_format(Geo& g, int32_t ofmt);
 // (scaled to out_px / P images).
 int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& scan_tmp, int64_t out_px);
 void strip_free(rl_ctx* c);
+int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg, int32_t fmt);
+int finish(rl_ctx* ctx);  // wait for the last enqueue; grow capacities and re-run on overflow
+int64_t image_bytes(int32_t w, int32_t h, int32_t fmt);
 void pool_free(rl_ctx* c);
 }  // namespace rlh

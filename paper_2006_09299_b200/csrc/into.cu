@@ -1,0 +1,323 @@
+// into.cu -- rl_label_into: the host-buffer entry point.  Large batches are cut into chunks of
+// whole images pipelined through three workspaces/streams (H2D of one chunk, kernels of
+// another and D2H of a third overlap); a byte-per-pixel filled image crosses PCIe as P4 bits
+// and a host thread pool expands it into the caller's buffer while later chunks are in flight.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <new>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.hpp"
+#include "runlab_gpu.h"
+
+using namespace rlg;
+using namespace rlh;
+
+namespace rlh {
+int64_t image_bytes(int32_t w, int32_t h, int32_t fmt) {
+    return (int64_t)(fmt == RL_PIXELS_P4 ? (w + 7) / 8 : w) * h;
+}
+}  // namespace rlh
+
+namespace rlh {
+struct HostPool {
+    std::vector<std::thread> workers;
+    std::mutex m;
+    std::condition_variable cv, done;
+    std::deque<std::pair<int, std::function<void()>>> q;
+    int pending[8] = {};
+    bool stop = false;
+    explicit HostPool(int n) {
+        for (int i = 0; i < n; ++i) workers.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : workers) t.join();
+    }
+    void loop() {
+        for (;;) {
+            std::pair<int, std::function<void()>> task;
+            {
+                std::unique_lock<std::mutex> lk(m);
+                cv.wait(lk, [&] { return stop || !q.empty(); });
+                if (q.empty()) return;
+                task = std::move(q.front());
+                q.pop_front();
+            }
+            task.second();
+            {
+                std::lock_guard<std::mutex> lk(m);
+                --pending[task.first];
+            }
+            done.notify_all();
+        }
+    }
+    void submit(int tag, std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            ++pending[tag];
+            q.emplace_back(tag, std::move(f));
+        }
+        cv.notify_one();
+    }
+    void wait(int tag) {
+        std::unique_lock<std::mutex> lk(m);
+        done.wait(lk, [&] { return pending[tag] == 0; });
+    }
+};
+void pool_free(rl_ctx* c) {
+    delete c->pool;
+    c->pool = nullptr;
+}
+}  // namespace rlh
+namespace {
+
+// P4 rows -> one byte per pixel (MSB-first bits; binarize_labels' layout, labeling.hpp:354-360)
+void expand_p4_rows(const uint8_t* src, int64_t rows, int32_t rowb, int32_t w, uint8_t* dst) {
+    static const struct Lut {
+        uint64_t v[256];
+        Lut() {
+            for (int b = 0; b < 256; ++b) {
+                uint64_t x = 0;
+                for (int k = 0; k < 8; ++k) x |= (uint64_t)((b >> (7 - k)) & 1) << (8 * k);
+                v[b] = x;
+            }
+        }
+    } lut;
+    const int32_t full = w / 8;
+    for (int64_t r = 0; r < rows; ++r) {
+        const uint8_t* s = src + r * rowb;
+        uint8_t* d = dst + r * w;
+        for (int32_t i = 0; i < full; ++i) std::memcpy(d + 8 * i, &lut.v[s[i]], 8);
+        for (int32_t j = 8 * full; j < w; ++j) d[j] = (s[j / 8] >> (7 - j % 8)) & 1u;
+    }
+}
+
+struct IntoState {
+    int64_t total = 0;  // components of the chunks posted so far
+    int64_t surv = 0;   // post-fill roots of the chunks posted so far
+    int64_t d2h = 0;
+    bool nospace = false;
+};
+
+void copy_fixed_outputs(rl_ctx* c, rl_host_outputs* out, int32_t b0) {
+    const Geo& g = c->geo;
+    const size_t npx = (size_t)(g.P * g.B), off = (size_t)g.P * b0;
+    if (out->filled_image) {
+        if (g.ofmt == g.fmt) {
+            cudaMemcpyAsync(out->filled_image + (size_t)g.fbytes * b0, c->ws.filled_img, (size_t)g.fbytes * g.B,
+                            cudaMemcpyDeviceToHost, c->stream);
+        } else {  // packed: into the staging buffer, expanded on the host once the chunk is done
+            cudaMemcpyAsync(c->h_stage[c->stage], c->ws.filled_img, (size_t)g.ofbytes * g.B, cudaMemcpyDeviceToHost,
+                            c->stream);
+        }
+    }
+    if (out->labels && g.label_mode)
+        cudaMemcpyAsync(out->labels + off, c->ws.labels, npx * 4, cudaMemcpyDeviceToHost, c->stream);
+}
+
+// host expansion of chunk c's packed filled image (after its stream is synchronised)
+void expand_filled(rl_ctx* owner, rl_ctx* c, int tag, rl_host_outputs* out, int32_t b0) {
+    const Geo& g = c->geo;
+    if (!out->filled_image || g.ofmt == g.fmt) return;
+    const int64_t rows = (int64_t)g.H * g.B;
+    const int parts = (int)std::min<int64_t>(std::max<int64_t>(1, rows / 256), 8);
+    for (int k = 0; k < parts; ++k) {
+        const int64_t r0 = rows * k / parts, r1 = rows * (k + 1) / parts;
+        const uint8_t* src = c->h_stage[c->stage] + r0 * g.orowb;
+        uint8_t* dst = out->filled_image + (size_t)g.P * b0 + r0 * g.W;
+        const int32_t rowb = g.orowb, w = g.W;
+        owner->pool->submit(tag, [=] { expand_p4_rows(src, r1 - r0, rowb, w, dst); });
+    }
+}
+
+// H2D of images [b0, b0 + n), the pipeline, and the D2H of the outputs whose size is fixed
+int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+                 rl_host_outputs* out, int32_t b0, int32_t fmt, bool packed_out) {
+    const size_t npx = (size_t)image_bytes(w, h, fmt) * n;
+    if (!ensure(c->pix, npx)) return set_err(c, RL_ENOMEM, "device allocation failed");
+    const cudaError_t e = cudaMemcpyAsync(c->pix.p, pixels, npx, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "copy in");
+    c->want_compact = out->filled && out->filled_layout == 1;
+    const bool packed = packed_out && out->filled_image && fmt == RL_PIXELS_U8;
+    c->force_ofmt = packed ? RL_PIXELS_P4 : -1;
+    if (packed) {
+        const size_t need = (size_t)image_bytes(w, h, RL_PIXELS_P4) * n;
+        const int sb = c->stage;
+        if (c->h_stage_n[sb] < need) {
+            if (c->h_stage[sb]) cudaFreeHost(c->h_stage[sb]);
+            c->h_stage[sb] = nullptr;
+            c->h_stage_n[sb] = 0;
+            if (cudaMallocHost(&c->h_stage[sb], need) != cudaSuccess) return set_err(c, RL_ENOMEM, "pinned alloc failed");
+            c->h_stage_n[sb] = need;
+        }
+    }
+    const int rc = enqueue(c, P<uint8_t>(c->pix), w, h, n, cfg, fmt);
+    c->force_ofmt = -1;  // finish() re-runs with the geometry of this call (kept in c->geo)
+    if (rc) return rc;
+    copy_fixed_outputs(c, out, b0);
+    return RL_OK;
+}
+
+// after finish(c): per-image summaries and the component outputs of c's chunk (first image b0)
+int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st) {
+    const Geo& g = c->geo;
+    const int B = g.B;
+    if (c->reran) {  // the pipeline re-ran after the first copies
+        copy_fixed_outputs(c, out, b0);
+        if (g.ofmt != g.fmt) cudaStreamSynchronize(c->stream);  // the staging buffer is expanded next
+    }
+    if (out->filled_image) st.d2h += g.ofbytes * B;
+    if (out->labels && g.label_mode) st.d2h += g.P * B * 4;
+    const int64_t* s = c->h_summ;
+    const int64_t total = s[4 * B];
+    int64_t surv = 0;
+    for (int b = 0; b < B; ++b) surv += s[4 * b + 3];
+    st.d2h += (int64_t)(B + 1) * 32;
+    if (out->summary)
+        for (int b = 0; b < B; ++b) {
+            const int64_t cp = s[4 * b + 1], fg = s[4 * b + 2];
+            int64_t* o = out->summary + 5 * (int64_t)(b0 + b);
+            o[0] = cp;
+            o[1] = fg;
+            o[2] = cp - 1 - fg;
+            o[3] = fg - (cp - 1 - fg);
+            o[4] = s[4 * b + 3];
+        }
+    if (out->comp_offset) {
+        for (int b = 0; b < B; ++b) out->comp_offset[b0 + b] = st.total + s[4 * b];
+        out->comp_offset[b0 + B] = st.total + total;
+    }
+    const bool want_comps = out->comps || out->top || out->filled;
+    if (want_comps && st.total + total > out->comp_capacity) st.nospace = true;
+    if (!st.nospace) {
+        cudaStream_t cs = c->stream;
+        if (out->comps) {
+            cudaMemcpyAsync(out->comps + st.total, c->ws.comps, sizeof(rl_component) * total, cudaMemcpyDeviceToHost, cs);
+            st.d2h += (int64_t)sizeof(rl_component) * total;
+        }
+        if (out->top) {
+            cudaMemcpyAsync(out->top + st.total, c->ws.top, 4 * total, cudaMemcpyDeviceToHost, cs);
+            st.d2h += 4 * total;
+        }
+        if (out->filled && out->filled_layout == 0) {
+            cudaMemcpyAsync(out->filled + st.total, c->ws.filled, sizeof(rl_features) * total, cudaMemcpyDeviceToHost, cs);
+            st.d2h += (int64_t)sizeof(rl_features) * total;
+        } else if (out->filled) {
+            cudaMemcpyAsync(out->filled + st.surv, c->fcomp.p, sizeof(rl_features) * surv, cudaMemcpyDeviceToHost, cs);
+            st.d2h += (int64_t)sizeof(rl_features) * surv;
+        }
+    }
+    st.total += total;
+    st.surv += surv;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RL_OK : cuda_fail(c, e, "copy out");
+}
+
+int into_sync(rl_ctx* c) {
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    return e == cudaSuccess ? RL_OK : cuda_fail(c, e, "copy out");
+}
+
+}  // namespace
+
+extern "C" {
+
+int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+                      int32_t fmt, rl_host_outputs* out) {
+    if (!out) return RL_EINVAL;
+    out->comps_needed = 0;
+    out->h2d_bytes = out->d2h_bytes = 0;
+    if (out->filled_layout != 0 && out->filled_layout != 1) return set_err(ctx, RL_EINVAL, "unknown filled_layout");
+    if (fmt != RL_PIXELS_U8 && fmt != RL_PIXELS_P4) return set_err(ctx, RL_EINVAL, "unknown pixel format");
+    int rc = check_args(ctx, w, h, n, cfg);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    const int64_t P = (int64_t)w * h;
+    // a byte-per-pixel filled image crosses PCIe as P4 bits and is expanded by host threads
+    const bool packed = ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
+    if (packed && !ctx->pool) {
+        const int hw = (int)std::thread::hardware_concurrency();
+        ctx->pool = new (std::nothrow) HostPool(std::max(2, std::min(hw > 0 ? hw : 4, 12)));
+        if (!ctx->pool) return set_err(ctx, RL_ENOMEM, "host thread pool");
+    }
+    // whole images per chunk, ~32 Mpx by default (pipelines of that size are graph-replayed)
+    const int32_t per = (int32_t)std::min<int64_t>(n, std::max<int64_t>(1, ctx->chunk_px / P));
+    const int32_t nch = (n + per - 1) / per;
+    IntoState st;
+    if (nch == 1) {
+        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed);
+        if (!rc) rc = finish(ctx);
+        if (!rc) rc = into_post(ctx, out, 0, st);
+        if (!rc) rc = into_sync(ctx);
+        if (!rc && packed) {
+            expand_filled(ctx, ctx, 0, out, 0);
+            ctx->pool->wait(0);
+        }
+    } else {
+        for (rl_ctx*& k : ctx->kids)
+            if (!k) {
+                k = rl_create(ctx->device);
+                if (!k) return set_err(ctx, RL_ECUDA, "could not create a pipeline context");
+                k->graphs = ctx->graphs;
+            }
+        auto first_image = [&](int32_t c) { return c * per; };
+        auto images = [&](int32_t c) { return std::min(per, n - c * per); };
+        // chunk c runs on kid c % NKIDS; its component outputs are copied once its summary is
+        // in (finish() synchronises the kid's stream, so its packed filled image is in the
+        // staging buffer and host threads expand it), before the kid takes chunk c + NKIDS
+        auto post = [&](int32_t c) -> int {
+            const int kid = c % rl_ctx::NKIDS;
+            rl_ctx* k = ctx->kids[kid];
+            int r = finish(k);
+            if (r) return set_err(ctx, r, k->err);
+            r = into_post(k, out, first_image(c), st);
+            if (!r && packed) expand_filled(ctx, k, 2 * kid + k->stage, out, first_image(c));
+            return r ? set_err(ctx, r, k->err) : RL_OK;
+        };
+        for (int32_t c = 0; c < nch && !rc; ++c) {
+            if (c >= rl_ctx::NKIDS) rc = post(c - rl_ctx::NKIDS);
+            if (rc) break;
+            const int kid = c % rl_ctx::NKIDS;
+            rl_ctx* k = ctx->kids[kid];
+            if (packed) {  // alternate the kid's staging buffers; wait for the older one's expansion
+                k->stage ^= 1;
+                ctx->pool->wait(2 * kid + k->stage);
+            }
+            const int32_t b0 = first_image(c);
+            rc = into_enqueue(k, pixels + (size_t)b0 * image_bytes(w, h, fmt), w, h, images(c), cfg, out, b0, fmt,
+                              packed);
+            if (rc) rc = set_err(ctx, rc, k->err);
+        }
+        for (int32_t c = std::max(0, nch - rl_ctx::NKIDS); c < nch && !rc; ++c) rc = post(c);
+        for (rl_ctx* k : ctx->kids)
+            if (!rc) rc = into_sync(k) ? set_err(ctx, RL_ECUDA, k->err) : RL_OK;
+        if (packed)
+            for (int tag = 0; tag < 2 * rl_ctx::NKIDS; ++tag) ctx->pool->wait(tag);
+    }
+    if (rc) return rc;
+    out->comps_needed = st.total;
+    out->h2d_bytes = image_bytes(w, h, fmt) * n;
+    out->d2h_bytes = st.d2h;
+    if (st.nospace) return set_err(ctx, RL_ENOSPC, "component buffers too small");
+    return RL_OK;
+}
+
+int rl_label_into(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
+                  rl_host_outputs* out) {
+    return rl_label_into_fmt(ctx, pixels, w, h, n, cfg, RL_PIXELS_U8, out);
+}
+
+}  // extern "C"
