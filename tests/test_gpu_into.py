@@ -142,3 +142,13 @@ def test_into_enospc_reports_total(small_chunks):
 def test_into_bad_layout(labeler):
     h_in = _batch(1, 64, 64)
     _into(labeler, h_in, LabelingConfig(), 2, 16, expect_error=ValueError)
+
+
+def test_into_chunked_densified_labels(small_chunks):
+    """densify_labels through the chunked path: ranks of post-fill roots per image."""
+    h_in = _batch(9, 512, 512, seed0=31)
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True, relabel=True,
+                         densify_labels=True)
+    ref = small_chunks.label_batch(h_in.numpy(), cfg)
+    o, outs = _into(small_chunks, h_in, cfg, 0, _cap(ref), labels=True)
+    _check(o, outs, ref, 0, labels=True)
