@@ -93,3 +93,19 @@ def test_adversarial_patterns(labeler, conn):
         pats = _patterns(w, h)
         imgs = np.stack(list(pats.values()) + [O.generate(w, h, 0.5, 1, 5)])
         _check_batch(labeler, imgs, conn, f"patterns {w}x{h}")
+
+
+def test_error_contract(labeler):
+    """labeling.hpp:271-273 and features.hpp:37-39: argument and overflow errors are raised
+    before anything is allocated or launched."""
+    from paper_2006_09299_b200 import LabelingConfig
+    with pytest.raises(OverflowError):  # Sx = sum of columns could exceed int64
+        labeler.label_device(0, 2**31 - 1, 2**31 - 1, 1, LabelingConfig(compute_features=True))
+    with pytest.raises(ValueError):  # densify without relabel
+        labeler.label_device(0, 64, 64, 1, LabelingConfig(relabel=False, densify_labels=True))
+    with pytest.raises(ValueError):  # empty image
+        labeler.label_device(0, 0, 64, 1, LabelingConfig())
+    # the context stays usable
+    img = O.generate(97, 65, 0.5, 1, 3)
+    compare_image(labeler.label_batch(img[None], LabelingConfig(compute_features=True)).image(0),
+                  O.label_canonical(img, 0), "after errors")
