@@ -341,7 +341,9 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     }
     const int wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
     const int my0 = incl - nev;  // offset of this lane's first event in the warp's sequence
-    __syncthreads();             // first-contact parents of every word are in place
+    // first-contact parents of every word are in place; tiles whose contacts were all first
+    // contacts (vertical stacks of equal runs, sparse tiles) skip the union phase
+    const int any_events = __syncthreads_or(nev);
     RL_PHASE(tg.t, 14);
     // The first-contact forest links every run to one in the row above, so a vertical stack
     // of runs is a chain as tall as the stack.  It is flattened before the unions so that their
@@ -393,7 +395,9 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
         }
         sunion(S.par, ra, rb2);
     };
-    if constexpr (BT == NW) {
+    if (!any_events) {
+        // nothing to unite
+    } else if constexpr (BT == NW) {
         for (int done = 0; done < wtot; done += C::EVC) {
             if (nev && my0 < done + C::EVC && my0 + nev > done) put_events(done);
             __syncwarp();
@@ -413,7 +417,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
         const int cnt = S.qtot[q];
         for (int k = lane + 32 * (warp / NWARPS); k < cnt; k += 32 * (BT / NW)) resolve_event(S.evq[q][k]);
     }
-    __syncthreads();
+    if (any_events) __syncthreads();
     RL_PHASE(tg.t, 4);
 
     // ---- flatten (roots are final now): every run walks to its root; concurrent writes of
