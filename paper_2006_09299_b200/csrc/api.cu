@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "ctx.hpp"
+#include "pack.cuh"
 #include "runlab_gpu.h"
 
 using namespace rlg;
@@ -155,7 +156,7 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
               ensure(ctx->comps, ctx->cap_comps * sizeof(rl_component)) &&
               ensure(ctx->top, ctx->cap_comps * 4) && ensure(ctx->filled, ctx->cap_comps * sizeof(Acc)) &&
               ensure(ctx->filled_img, (size_t)(out_px / g.W) * g.orowb) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
-              ensure(ctx->summ, (size_t)(B + 1) * 32);
+              ensure(ctx->summ, (size_t)(B + 2) * 32);
     if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)out_px * 4);
     if (!ok) return set_err(ctx, RL_ENOMEM, "device allocation failed");
     tmp = 0;
@@ -236,7 +237,14 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     }
     if (ctx->want_compact && !ensure(ctx->fcomp, ctx->cap_comps * sizeof(Acc)))
         return set_err(ctx, RL_ENOMEM, "device allocation failed");
-    const size_t sn = (size_t)(B + 1) * 4;
+    const int pack = ctx->want_pack & (ctx->want_compact ? 3 : 1);
+    if ((pack & 1) && !(ensure(ctx->pk, ctx->cap_comps * sizeof(rlp::Slot)) && ensure(ctx->pkpar, ctx->cap_comps * 4) &&
+                        ensure(ctx->pkesc, ctx->cap_comps * sizeof(rl_component))))
+        return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    if ((pack & 2) && !ensure(ctx->fpk, ctx->cap_comps * sizeof(rlp::Slot)))
+        return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    // summary rows 0..B-1 per image, B batch totals, B + 1 escape counts of the packed slots
+    const size_t sn = (size_t)(B + 2) * 4;
     if (ctx->h_summ_n < sn) {
         if (ctx->h_summ) cudaFreeHost(ctx->h_summ);
         ctx->h_summ = nullptr;
@@ -259,6 +267,11 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     key.fcomp = ctx->fcomp.p;
     key.cap_comps = ctx->cap_comps;
     key.compact = ctx->want_compact ? 1 : 0;
+    key.pack = pack;
+    key.pk[0] = ctx->pk.p;
+    key.pk[1] = ctx->pkpar.p;
+    key.pk[2] = ctx->pkesc.p;
+    key.pk[3] = ctx->fpk.p;
     if (use_graph && ctx->gexec && std::memcmp(&key, &ctx->gkey, sizeof(key)) == 0) {
         const cudaError_t e = cudaGraphLaunch(ctx->gexec, s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "graph launch");
@@ -291,6 +304,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     cudaMemsetAsync(ws.img_fg, 0, (size_t)B * 4, s);
     cudaMemsetAsync(ws.img_surv, 0, (size_t)B * 4, s);
     cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
+    cudaMemsetAsync(P<int64_t>(ctx->summ) + 4 * (B + 1), 0, 32, s);
     ctx->nkev = 0;
     auto kt = [&]() {  // tuning aid: an event after each launch group
         if (!ctx->ktimes || use_graph || ctx->nkev >= 24) return;
@@ -341,9 +355,20 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
         launch_remap(ws.labels, g.P, B, P<uint32_t>(ctx->rank), P<uint64_t>(ctx->cbase), ctx->cap_comps, s, ctx->sms);
         ++launches;
     }
-    if (ctx->want_compact) {
+    if (ctx->want_compact && !(pack & 2)) {
         launch_compact_filled(ws.filled, P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank), P<uint64_t>(ctx->cbase) + B,
                               ctx->cap_comps, P<Acc>(ctx->fcomp), s, ctx->sms);
+        ++launches;
+    }
+    if (pack & 1) {
+        launch_pack_comps(ws.comps, P<uint64_t>(ctx->cbase) + B, ctx->cap_comps, ctx->pk.p, P<uint32_t>(ctx->pkpar),
+                          P<rl_component>(ctx->pkesc), P<int64_t>(ctx->summ) + 4 * (B + 1), s, ctx->sms);
+        ++launches;
+    }
+    if (pack & 2) {
+        launch_pack_filled(ws.filled, P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank), P<uint64_t>(ctx->cbase) + B,
+                           ctx->cap_comps, ctx->fpk.p, P<Acc>(ctx->fcomp), P<int64_t>(ctx->summ) + 4 * (B + 1) + 1, s,
+                           ctx->sms);
         ++launches;
     }
     record_event(ctx->ev[3], s, use_graph);
@@ -506,6 +531,9 @@ rl_ctx* rl_create(int device) {
     if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
     if (std::getenv("RUNLAB_GPU_KTIMES")) c->ktimes = true;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_D2H")) c->packed_d2h = false;
+    if (std::getenv("RUNLAB_GPU_NO_PACKED_RECORDS")) c->packed_recs = false;
+    if (const char* v = std::getenv("RUNLAB_GPU_KIDS")) c->nkids = std::min(rl_ctx::MAXKIDS, std::max(1, std::atoi(v)));
+    if (const char* v = std::getenv("RUNLAB_GPU_HOST_THREADS")) c->host_threads = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("RUNLAB_GPU_CHUNK_PX")) c->chunk_px = std::max(1ll, std::atoll(v));
     return c;
 }
@@ -519,11 +547,13 @@ void rl_destroy(rl_ctx* c) {
                       &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
                       &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,
-                      &c->fcomp, &c->nleft, &c->scount};
+                      &c->fcomp, &c->nleft, &c->scount, &c->pk, &c->pkpar, &c->pkesc, &c->fpk};
     for (rl_ctx* k : c->kids) rl_destroy(k);
     strip_free(c);
     pool_free(c);
     for (uint8_t* p : c->h_stage)
+        if (p) cudaFreeHost(p);
+    for (uint8_t* p : c->h_rstage)
         if (p) cudaFreeHost(p);
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
@@ -548,6 +578,7 @@ int rl_label_device_fmt(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t
         return set_err(ctx, RL_EINVAL, "unknown pixel format");
     cudaSetDevice(ctx->device);
     ctx->want_compact = false;
+    ctx->want_pack = 0;
     return enqueue(ctx, d_pixels, w, h, n, cfg, pixel_format);
 }
 
@@ -580,6 +611,7 @@ int rl_label(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, int32_t n
     cudaError_t e = cudaMemcpyAsync(ctx->pix.p, pixels, npx, cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "copy in");
     ctx->want_compact = false;
+    ctx->want_pack = 0;
     rc = enqueue(ctx, P<uint8_t>(ctx->pix), w, h, n, cfg, RL_PIXELS_U8);
     if (rc) return rc;
     rc = finish(ctx);

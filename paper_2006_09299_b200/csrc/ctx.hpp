@@ -28,6 +28,10 @@ void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, ui
                        cudaStream_t s, int sms);
 void launch_compact_filled(const Acc* filled, const uint32_t* flag, const uint32_t* rank, const uint64_t* total_p,
                            uint64_t cap, Acc* out, cudaStream_t s, int sms);
+void launch_pack_comps(const rl_component* comps, const uint64_t* total_p, uint64_t cap, void* slots, uint32_t* parent,
+                       rl_component* esc, int64_t* nesc, cudaStream_t s, int sms);
+void launch_pack_filled(const Acc* filled, const uint32_t* flag, const uint32_t* rank, const uint64_t* total_p,
+                        uint64_t cap, void* slots, Acc* esc, int64_t* nesc, cudaStream_t s, int sms);
 void launch_remap(uint32_t* labels, int64_t P, int32_t B, const uint32_t* rank, const uint64_t* cbase, uint64_t cap,
                   cudaStream_t s, int sms);
 }  // namespace rlg
@@ -57,6 +61,8 @@ struct GraphKey {
     const void* fcomp;
     uint64_t cap_comps;
     int compact;
+    int pack;  // bit 0: records, bit 1: survivors' features
+    const void* pk[4];
 };
 
 
@@ -104,8 +110,9 @@ struct rl_ctx {
     bool want_compact = false;
     int64_t chunk_px = 32ll << 20;  // rl_label_into: pixels per chunk (env RUNLAB_GPU_CHUNK_PX)
     // rl_label_into pipelines large batches through these (own workspace and stream each)
-    static constexpr int NKIDS = 3;
-    rl_ctx* kids[NKIDS] = {};
+    static constexpr int MAXKIDS = 8;
+    int nkids = 3;  // env RUNLAB_GPU_KIDS
+    rl_ctx* kids[MAXKIDS] = {};
     // per-launch timing for tuning (env RUNLAB_GPU_KTIMES; eager launches only)
     bool ktimes = false;
     cudaEvent_t kev[24] = {};
@@ -118,6 +125,14 @@ struct rl_ctx {
     size_t h_stage_n[2] = {0, 0};
     int stage = 0;  // the buffer the last enqueue copies into
     rlh::HostPool* pool = nullptr;
+    int host_threads = 0;  // pool size (0: min(hardware threads, 12); env RUNLAB_GPU_HOST_THREADS)
+    // rl_label_into: component records and survivors' features cross PCIe as compact slots
+    // (pack.cuh) into pinned staging, decoded by host threads (env RUNLAB_GPU_NO_PACKED_RECORDS)
+    bool packed_recs = true;
+    int want_pack = 0;           // bit 0: records, bit 1: survivors' features (next enqueue)
+    DevBuf pk, pkpar, pkesc, fpk;  // record slots, parents, escaped records, feature slots
+    uint8_t* h_rstage[2] = {nullptr, nullptr};
+    size_t h_rstage_n[2] = {0, 0};
     // strip mode (strips.cu)
     DevBuf nleft, scount;
     rlh::StripState* strip = nullptr;

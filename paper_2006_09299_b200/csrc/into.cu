@@ -3,6 +3,7 @@
 // another and D2H of a third overlap); a byte-per-pixel filled image crosses PCIe as P4 bits
 // and a host thread pool expands it into the caller's buffer while later chunks are in flight.
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <condition_variable>
@@ -16,6 +17,7 @@
 
 #include "common.cuh"
 #include "ctx.hpp"
+#include "pack.cuh"
 #include "runlab_gpu.h"
 
 using namespace rlg;
@@ -33,7 +35,7 @@ struct HostPool {
     std::mutex m;
     std::condition_variable cv, done;
     std::deque<std::pair<int, std::function<void()>>> q;
-    int pending[8] = {};
+    int pending[2 * rl_ctx::MAXKIDS] = {};
     bool stop = false;
     explicit HostPool(int n) {
         for (int i = 0; i < n; ++i) workers.emplace_back([this] { loop(); });
@@ -72,6 +74,19 @@ struct HostPool {
         }
         cv.notify_one();
     }
+    // a placeholder task: keeps wait(tag) blocked until release(tag) (work submitted later, e.g.
+    // from a stream callback once a copy has landed)
+    void reserve(int tag) {
+        std::lock_guard<std::mutex> lk(m);
+        ++pending[tag];
+    }
+    void release(int tag) {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            --pending[tag];
+        }
+        done.notify_all();
+    }
     void wait(int tag) {
         std::unique_lock<std::mutex> lk(m);
         done.wait(lk, [&] { return pending[tag] == 0; });
@@ -100,10 +115,75 @@ void expand_p4_rows(const uint8_t* src, int64_t rows, int32_t rowb, int32_t w, u
     for (int64_t r = 0; r < rows; ++r) {
         const uint8_t* s = src + r * rowb;
         uint8_t* d = dst + r * w;
-        for (int32_t i = 0; i < full; ++i) std::memcpy(d + 8 * i, &lut.v[s[i]], 8);
+        if (((uintptr_t)d & 7) == 0) {  // streaming stores: the caller's buffer is not re-read here
+            for (int32_t i = 0; i < full; ++i) _mm_stream_si64((long long*)(d + 8 * i), (long long)lut.v[s[i]]);
+        } else {
+            for (int32_t i = 0; i < full; ++i) std::memcpy(d + 8 * i, &lut.v[s[i]], 8);
+        }
         for (int32_t j = 8 * full; j < w; ++j) d[j] = (s[j / 8] >> (7 - j % 8)) & 1u;
     }
+    _mm_sfence();
 }
+
+template <class T>
+inline void stream_store(T* dst, const T& v) {
+    static_assert(sizeof(T) % 8 == 0, "8-byte granules");
+    if (((uintptr_t)dst & 7) == 0) {
+        const long long* s = reinterpret_cast<const long long*>(&v);
+        long long* d = reinterpret_cast<long long*>(dst);
+        for (size_t k = 0; k < sizeof(T) / 8; ++k) _mm_stream_si64(d + k, s[k]);
+    } else {
+        std::memcpy(dst, &v, sizeof(T));
+    }
+}
+
+// compact slots (pack.cuh) -> the caller's records / features
+void decode_records(const rlp::Slot* sl, const uint32_t* par, const rl_component* esc, rl_component* dst, int64_t a,
+                    int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+        const rlp::Slot o = sl[i];
+        rl_component c;
+        if (rlp::is_escape(o)) {
+            c = esc[o.x];
+        } else {
+            rlp::decode(o, c.f, c.flags);
+            c.parent = par[i];
+        }
+        stream_store(dst + i, c);
+    }
+    _mm_sfence();
+}
+
+void decode_features(const rlp::Slot* sl, const rl_features* esc, rl_features* dst, int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+        const rlp::Slot o = sl[i];
+        rl_features f;
+        if (rlp::is_escape(o)) {
+            f = esc[o.x];
+        } else {
+            uint32_t fg;
+            rlp::decode(o, f, fg);
+        }
+        stream_store(dst + i, f);
+    }
+    _mm_sfence();
+}
+
+// decode tasks handed to the pool by a stream callback once the slots are in host memory
+struct Deferred {
+    HostPool* pool;
+    int tag;
+    std::vector<std::function<void()>> tasks;
+};
+
+void CUDART_CB run_deferred(void* p) {
+    Deferred* d = static_cast<Deferred*>(p);
+    for (auto& t : d->tasks) d->pool->submit(d->tag, std::move(t));
+    d->pool->release(d->tag);
+    delete d;
+}
+
+size_t up64(size_t v) { return (v + 63) & ~size_t{63}; }
 
 struct IntoState {
     int64_t total = 0;  // components of the chunks posted so far
@@ -145,12 +225,13 @@ void expand_filled(rl_ctx* owner, rl_ctx* c, int tag, rl_host_outputs* out, int3
 
 // H2D of images [b0, b0 + n), the pipeline, and the D2H of the outputs whose size is fixed
 int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
-                 rl_host_outputs* out, int32_t b0, int32_t fmt, bool packed_out) {
+                 rl_host_outputs* out, int32_t b0, int32_t fmt, bool packed_out, int pack) {
     const size_t npx = (size_t)image_bytes(w, h, fmt) * n;
     if (!ensure(c->pix, npx)) return set_err(c, RL_ENOMEM, "device allocation failed");
     const cudaError_t e = cudaMemcpyAsync(c->pix.p, pixels, npx, cudaMemcpyHostToDevice, c->stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "copy in");
     c->want_compact = out->filled && out->filled_layout == 1;
+    c->want_pack = pack;
     const bool packed = packed_out && out->filled_image && fmt == RL_PIXELS_U8;
     c->force_ofmt = packed ? RL_PIXELS_P4 : -1;
     if (packed) {
@@ -172,7 +253,7 @@ int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t
 }
 
 // after finish(c): per-image summaries and the component outputs of c's chunk (first image b0)
-int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st) {
+int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st, HostPool* pool, int tag) {
     const Geo& g = c->geo;
     const int B = g.B;
     if (c->reran) {  // the pipeline re-ran after the first copies
@@ -202,9 +283,65 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st) {
     }
     const bool want_comps = out->comps || out->top || out->filled;
     if (want_comps && st.total + total > out->comp_capacity) st.nospace = true;
+    const int pack = c->want_pack & (c->want_compact ? 3 : 1);
+    if (!st.nospace && pack) {
+        // compact slots into pinned staging; host threads decode them once the copies land
+        const int64_t nesc = (pack & 1) ? s[4 * (B + 1)] : 0, fesc = (pack & 2) ? s[4 * (B + 1) + 1] : 0;
+        const int64_t nrec = (pack & 1) ? total : 0, nfs = (pack & 2) ? surv : 0;
+        const size_t o_fs = up64(16 * (size_t)nrec), o_par = o_fs + up64(16 * (size_t)nfs);
+        const size_t o_esc = o_par + up64(4 * (size_t)nrec), o_fesc = o_esc + up64(sizeof(rl_component) * nesc);
+        const size_t need = o_fesc + sizeof(rl_features) * fesc + 64;
+        const int sb = c->stage;
+        if (c->h_rstage_n[sb] < need) {
+            if (c->h_rstage[sb]) cudaFreeHost(c->h_rstage[sb]);
+            c->h_rstage[sb] = nullptr;
+            c->h_rstage_n[sb] = 0;
+            if (cudaMallocHost(&c->h_rstage[sb], need + need / 4) != cudaSuccess)
+                return set_err(c, RL_ENOMEM, "pinned alloc failed");
+            c->h_rstage_n[sb] = need + need / 4;
+        }
+        uint8_t* h = c->h_rstage[sb];
+        cudaStream_t cs = c->stream;
+        Deferred* d = new Deferred{pool, tag, {}};
+        const int64_t t0 = st.total, s0 = st.surv;
+        if (nrec) {
+            cudaMemcpyAsync(h, c->pk.p, 16 * (size_t)nrec, cudaMemcpyDeviceToHost, cs);
+            cudaMemcpyAsync(h + o_par, c->pkpar.p, 4 * (size_t)nrec, cudaMemcpyDeviceToHost, cs);
+            if (nesc) cudaMemcpyAsync(h + o_esc, c->pkesc.p, sizeof(rl_component) * nesc, cudaMemcpyDeviceToHost, cs);
+            st.d2h += 20 * nrec + (int64_t)sizeof(rl_component) * nesc;
+            const rlp::Slot* sl = reinterpret_cast<const rlp::Slot*>(h);
+            const uint32_t* par = reinterpret_cast<const uint32_t*>(h + o_par);
+            const rl_component* esc = reinterpret_cast<const rl_component*>(h + o_esc);
+            rl_component* dst = out->comps + t0;
+            const int parts = (int)std::min<int64_t>(8, std::max<int64_t>(1, nrec / 65536));
+            for (int k = 0; k < parts; ++k) {
+                const int64_t a = nrec * k / parts, e = nrec * (k + 1) / parts;
+                d->tasks.emplace_back([=] { decode_records(sl, par, esc, dst, a, e); });
+            }
+        }
+        if (nfs) {
+            cudaMemcpyAsync(h + o_fs, c->fpk.p, 16 * (size_t)nfs, cudaMemcpyDeviceToHost, cs);
+            if (fesc) cudaMemcpyAsync(h + o_fesc, c->fcomp.p, sizeof(rl_features) * fesc, cudaMemcpyDeviceToHost, cs);
+            st.d2h += 16 * nfs + (int64_t)sizeof(rl_features) * fesc;
+            const rlp::Slot* sl = reinterpret_cast<const rlp::Slot*>(h + o_fs);
+            const rl_features* esc = reinterpret_cast<const rl_features*>(h + o_fesc);
+            rl_features* dst = out->filled + s0;
+            const int parts = (int)std::min<int64_t>(4, std::max<int64_t>(1, nfs / 65536));
+            for (int k = 0; k < parts; ++k) {
+                const int64_t a = nfs * k / parts, e = nfs * (k + 1) / parts;
+                d->tasks.emplace_back([=] { decode_features(sl, esc, dst, a, e); });
+            }
+        }
+        pool->reserve(tag);
+        if (cudaLaunchHostFunc(cs, run_deferred, d) != cudaSuccess) {
+            cudaGetLastError();
+            cudaStreamSynchronize(cs);
+            run_deferred(d);
+        }
+    }
     if (!st.nospace) {
         cudaStream_t cs = c->stream;
-        if (out->comps) {
+        if (out->comps && !(pack & 1)) {
             cudaMemcpyAsync(out->comps + st.total, c->ws.comps, sizeof(rl_component) * total, cudaMemcpyDeviceToHost, cs);
             st.d2h += (int64_t)sizeof(rl_component) * total;
         }
@@ -212,7 +349,8 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st) {
             cudaMemcpyAsync(out->top + st.total, c->ws.top, 4 * total, cudaMemcpyDeviceToHost, cs);
             st.d2h += 4 * total;
         }
-        if (out->filled && out->filled_layout == 0) {
+        if (pack & 2) {
+        } else if (out->filled && out->filled_layout == 0) {
             cudaMemcpyAsync(out->filled + st.total, c->ws.filled, sizeof(rl_features) * total, cudaMemcpyDeviceToHost, cs);
             st.d2h += (int64_t)sizeof(rl_features) * total;
         } else if (out->filled) {
@@ -248,9 +386,13 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     const int64_t P = (int64_t)w * h;
     // a byte-per-pixel filled image crosses PCIe as P4 bits and is expanded by host threads
     const bool packed = ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
-    if (packed && !ctx->pool) {
+    // component records and survivors' features cross PCIe as compact slots (pack.cuh)
+    const int pack = ctx->packed_recs ? ((out->comps ? 1 : 0) | (out->filled && out->filled_layout == 1 ? 2 : 0)) : 0;
+    const bool staged = packed || pack;
+    if (staged && !ctx->pool) {
         const int hw = (int)std::thread::hardware_concurrency();
-        ctx->pool = new (std::nothrow) HostPool(std::max(2, std::min(hw > 0 ? hw : 4, 12)));
+        const int nt = ctx->host_threads > 0 ? ctx->host_threads : std::max(2, std::min(hw > 0 ? hw : 4, 12));
+        ctx->pool = new (std::nothrow) HostPool(nt);
         if (!ctx->pool) return set_err(ctx, RL_ENOMEM, "host thread pool");
     }
     // whole images per chunk, ~32 Mpx by default (pipelines of that size are graph-replayed)
@@ -258,54 +400,61 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     const int32_t nch = (n + per - 1) / per;
     IntoState st;
     if (nch == 1) {
-        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed);
+        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed, pack);
         if (!rc) rc = finish(ctx);
-        if (!rc) rc = into_post(ctx, out, 0, st);
+        if (!rc) rc = into_post(ctx, out, 0, st, ctx->pool, 0);
         if (!rc) rc = into_sync(ctx);
-        if (!rc && packed) {
-            expand_filled(ctx, ctx, 0, out, 0);
-            ctx->pool->wait(0);
-        }
+        if (!rc && packed) expand_filled(ctx, ctx, 0, out, 0);
+        // host tasks of this call end before it returns (after a failed copy only if the
+        // stream still completes, i.e. its callbacks run)
+        if (staged && (!rc || cudaStreamSynchronize(ctx->stream) == cudaSuccess)) ctx->pool->wait(0);
     } else {
-        for (rl_ctx*& k : ctx->kids)
+        const int NK = ctx->nkids;
+        for (int i = 0; i < NK; ++i) {
+            rl_ctx*& k = ctx->kids[i];
             if (!k) {
                 k = rl_create(ctx->device);
                 if (!k) return set_err(ctx, RL_ECUDA, "could not create a pipeline context");
                 k->graphs = ctx->graphs;
             }
+            k->stage = 1;  // chunk -> staging buffer is the same every call (sizes settle once)
+        }
         auto first_image = [&](int32_t c) { return c * per; };
         auto images = [&](int32_t c) { return std::min(per, n - c * per); };
         // chunk c runs on kid c % NKIDS; its component outputs are copied once its summary is
         // in (finish() synchronises the kid's stream, so its packed filled image is in the
         // staging buffer and host threads expand it), before the kid takes chunk c + NKIDS
         auto post = [&](int32_t c) -> int {
-            const int kid = c % rl_ctx::NKIDS;
+            const int kid = c % NK;
             rl_ctx* k = ctx->kids[kid];
             int r = finish(k);
             if (r) return set_err(ctx, r, k->err);
-            r = into_post(k, out, first_image(c), st);
+            r = into_post(k, out, first_image(c), st, ctx->pool, 2 * kid + k->stage);
             if (!r && packed) expand_filled(ctx, k, 2 * kid + k->stage, out, first_image(c));
             return r ? set_err(ctx, r, k->err) : RL_OK;
         };
         for (int32_t c = 0; c < nch && !rc; ++c) {
-            if (c >= rl_ctx::NKIDS) rc = post(c - rl_ctx::NKIDS);
+            if (c >= NK) rc = post(c - NK);
             if (rc) break;
-            const int kid = c % rl_ctx::NKIDS;
+            const int kid = c % NK;
             rl_ctx* k = ctx->kids[kid];
-            if (packed) {  // alternate the kid's staging buffers; wait for the older one's expansion
+            if (staged) {  // alternate the kid's staging buffers; wait for the older one's expansion
                 k->stage ^= 1;
                 ctx->pool->wait(2 * kid + k->stage);
             }
             const int32_t b0 = first_image(c);
             rc = into_enqueue(k, pixels + (size_t)b0 * image_bytes(w, h, fmt), w, h, images(c), cfg, out, b0, fmt,
-                              packed);
+                              packed, pack);
             if (rc) rc = set_err(ctx, rc, k->err);
         }
-        for (int32_t c = std::max(0, nch - rl_ctx::NKIDS); c < nch && !rc; ++c) rc = post(c);
-        for (rl_ctx* k : ctx->kids)
-            if (!rc) rc = into_sync(k) ? set_err(ctx, RL_ECUDA, k->err) : RL_OK;
-        if (packed)
-            for (int tag = 0; tag < 2 * rl_ctx::NKIDS; ++tag) ctx->pool->wait(tag);
+        for (int32_t c = std::max(0, nch - NK); c < nch && !rc; ++c) rc = post(c);
+        for (int i = 0; i < NK; ++i)
+            if (!rc) rc = into_sync(ctx->kids[i]) ? set_err(ctx, RL_ECUDA, ctx->kids[i]->err) : RL_OK;
+        bool drained = true;
+        if (rc)
+            for (int i = 0; i < NK; ++i) drained = cudaStreamSynchronize(ctx->kids[i]->stream) == cudaSuccess && drained;
+        if (staged && drained)
+            for (int tag = 0; tag < 2 * NK; ++tag) ctx->pool->wait(tag);
     }
     if (rc) return rc;
     out->comps_needed = st.total;

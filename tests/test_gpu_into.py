@@ -152,3 +152,34 @@ def test_into_chunked_densified_labels(small_chunks):
     ref = small_chunks.label_batch(h_in.numpy(), cfg)
     o, outs = _into(small_chunks, h_in, cfg, 0, _cap(ref), labels=True)
     _check(o, outs, ref, 0, labels=True)
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_into_packed_slots_match_full_records(small_chunks, layout):
+    """Compact record/feature slots (pack.cuh) decode to exactly the full records.
+
+    Dense noise gives many one-tile components (slots); solid and coarse images give
+    components that span tiles, exteriors with s = 0 and features past the slot ranges
+    (escapes).  A context with RUNLAB_GPU_NO_PACKED_RECORDS copies the full tables."""
+    h_in = _batch(12, 512, 512, seed0=11)
+    h_in[3].fill_(1)
+    h_in[4].fill_(0)
+    h_in[5, 100:400, 50:500] = 1
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    ref = small_chunks.label_batch(h_in.numpy(), cfg)
+    o, outs = _into(small_chunks, h_in, cfg, layout, _cap(ref))
+    _check(o, outs, ref, layout)
+    os.environ["RUNLAB_GPU_NO_PACKED_RECORDS"] = "1"
+    os.environ["RUNLAB_GPU_CHUNK_PX"] = str(1 << 20)
+    try:
+        plain = Labeler(0)
+    finally:
+        del os.environ["RUNLAB_GPU_NO_PACKED_RECORDS"]
+        del os.environ["RUNLAB_GPU_CHUNK_PX"]
+    try:
+        o2, outs2 = _into(plain, h_in, cfg, layout, _cap(ref))
+        _check(o2, outs2, ref, layout)
+    finally:
+        plain.close()
+    total = int(ref.comp_offset[-1])
+    assert outs.d2h_bytes < outs2.d2h_bytes - 20 * total  # 48-B records became 20-B slots
