@@ -532,6 +532,7 @@ rl_ctx* rl_create(int device) {
     if (std::getenv("RUNLAB_GPU_KTIMES")) c->ktimes = true;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_D2H")) c->packed_d2h = false;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_RECORDS")) c->packed_recs = false;
+    if (const char* v = std::getenv("RUNLAB_GPU_PACKED_H2D")) c->packed_h2d = std::atoi(v) != 0;
     if (const char* v = std::getenv("RUNLAB_GPU_KIDS")) c->nkids = std::min(rl_ctx::MAXKIDS, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("RUNLAB_GPU_HOST_THREADS")) c->host_threads = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("RUNLAB_GPU_CHUNK_PX")) c->chunk_px = std::max(1ll, std::atoll(v));
@@ -555,6 +556,8 @@ void rl_destroy(rl_ctx* c) {
         if (p) cudaFreeHost(p);
     for (uint8_t* p : c->h_rstage)
         if (p) cudaFreeHost(p);
+    for (uint8_t* p : c->h_istage)
+        if (p) cudaFreeHost(p);
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (c->h_summ) cudaFreeHost(c->h_summ);
@@ -564,6 +567,16 @@ void rl_destroy(rl_ctx* c) {
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (auto& e : c->kev)
         if (e) cudaEventDestroy(e);
+    if (c->out_stream) {
+        cudaStreamSynchronize(c->out_stream);
+        cudaStreamDestroy(c->out_stream);
+    }
+    if (c->out_done) cudaEventDestroy(c->out_done);
+    if (c->in_stream) {
+        cudaStreamSynchronize(c->in_stream);
+        cudaStreamDestroy(c->in_stream);
+    }
+    if (c->in_done) cudaEventDestroy(c->in_done);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }

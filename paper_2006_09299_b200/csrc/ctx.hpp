@@ -133,6 +133,21 @@ struct rl_ctx {
     DevBuf pk, pkpar, pkesc, fpk;  // record slots, parents, escaped records, feature slots
     uint8_t* h_rstage[2] = {nullptr, nullptr};
     size_t h_rstage_n[2] = {0, 0};
+    // rl_label_into: byte-per-pixel input packed to P4 bits by the host pool before the H2D copy
+    // (env RUNLAB_GPU_PACKED_H2D=1; off by default: measured no faster on the pool's boxes, the
+    // host-side packing costs what the link saves); the caller's filled-image format
+    bool packed_h2d = false;
+    uint8_t* h_istage[2] = {nullptr, nullptr};
+    size_t h_istage_n[2] = {0, 0};
+    int32_t user_ofmt = 0;
+    // rl_label_into: component-table copies of a chunk run on their own stream so that the next
+    // chunk's H2D copy does not queue behind them; the next pipeline waits for out_done
+    cudaStream_t out_stream = nullptr;
+    cudaEvent_t out_done = nullptr;
+    // and the H2D copy on a stream of its own: a stream that copies in both directions shares
+    // one copy-engine queue with the D2H copies of other streams (measured: tools/copy_bench3.cu)
+    cudaStream_t in_stream = nullptr;
+    cudaEvent_t in_done = nullptr;
     // strip mode (strips.cu)
     DevBuf nleft, scount;
     rlh::StripState* strip = nullptr;

@@ -4,9 +4,14 @@
 // and a host thread pool expands it into the caller's buffer while later chunks are in flight.
 #include <cuda_runtime.h>
 #include <emmintrin.h>
+#include <immintrin.h>
 
 #include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstdio>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -35,7 +40,7 @@ struct HostPool {
     std::mutex m;
     std::condition_variable cv, done;
     std::deque<std::pair<int, std::function<void()>>> q;
-    int pending[2 * rl_ctx::MAXKIDS] = {};
+    int pending[2 * rl_ctx::MAXKIDS + 1] = {};  // last: input packing
     bool stop = false;
     explicit HostPool(int n) {
         for (int i = 0; i < n; ++i) workers.emplace_back([this] { loop(); });
@@ -66,11 +71,14 @@ struct HostPool {
             done.notify_all();
         }
     }
-    void submit(int tag, std::function<void()> f) {
+    void submit(int tag, std::function<void()> f, bool front = false) {
         {
             std::lock_guard<std::mutex> lk(m);
             ++pending[tag];
-            q.emplace_back(tag, std::move(f));
+            if (front)
+                q.emplace_front(tag, std::move(f));
+            else
+                q.emplace_back(tag, std::move(f));
         }
         cv.notify_one();
     }
@@ -99,6 +107,24 @@ void pool_free(rl_ctx* c) {
 }  // namespace rlh
 namespace {
 
+// bytes [i, full) of a P4 row, 4 at a time, into 32-B aligned streaming stores (d + 8 i is
+// 32-B aligned); returns the first byte not done
+__attribute__((target("avx2"))) int32_t expand_avx2(const uint8_t* s, int32_t i, int32_t full, uint8_t* d) {
+    const __m256i shuf = _mm256_setr_epi8(0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 3, 3,
+                                          3, 3, 3, 3, 3, 3);
+    const __m256i bits = _mm256_setr_epi8(-128, 64, 32, 16, 8, 4, 2, 1, -128, 64, 32, 16, 8, 4, 2, 1, -128, 64, 32, 16,
+                                          8, 4, 2, 1, -128, 64, 32, 16, 8, 4, 2, 1);
+    const __m256i one = _mm256_set1_epi8(1);
+    for (; i + 4 <= full; i += 4) {
+        uint32_t w;
+        std::memcpy(&w, s + i, 4);
+        __m256i v = _mm256_shuffle_epi8(_mm256_set1_epi32((int)w), shuf);
+        v = _mm256_and_si256(_mm256_cmpeq_epi8(_mm256_and_si256(v, bits), bits), one);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(d + 8 * i), v);
+    }
+    return i;
+}
+
 // P4 rows -> one byte per pixel (MSB-first bits; binarize_labels' layout, labeling.hpp:354-360)
 void expand_p4_rows(const uint8_t* src, int64_t rows, int32_t rowb, int32_t w, uint8_t* dst) {
     static const struct Lut {
@@ -112,17 +138,45 @@ void expand_p4_rows(const uint8_t* src, int64_t rows, int32_t rowb, int32_t w, u
         }
     } lut;
     const int32_t full = w / 8;
+    static const bool avx2 = __builtin_cpu_supports("avx2");
     for (int64_t r = 0; r < rows; ++r) {
         const uint8_t* s = src + r * rowb;
         uint8_t* d = dst + r * w;
         if (((uintptr_t)d & 7) == 0) {  // streaming stores: the caller's buffer is not re-read here
-            for (int32_t i = 0; i < full; ++i) _mm_stream_si64((long long*)(d + 8 * i), (long long)lut.v[s[i]]);
+            int32_t i = 0;
+            if (avx2) {
+                for (; i < full && ((uintptr_t)(d + 8 * i) & 31); ++i)
+                    _mm_stream_si64((long long*)(d + 8 * i), (long long)lut.v[s[i]]);
+                i = expand_avx2(s, i, full, d);
+            }
+            for (; i < full; ++i) _mm_stream_si64((long long*)(d + 8 * i), (long long)lut.v[s[i]]);
         } else {
             for (int32_t i = 0; i < full; ++i) std::memcpy(d + 8 * i, &lut.v[s[i]], 8);
         }
         for (int32_t j = 8 * full; j < w; ++j) d[j] = (s[j / 8] >> (7 - j % 8)) & 1u;
     }
     _mm_sfence();
+}
+
+// byte-per-pixel rows -> P4 rows (bit 0 of each byte, MSB-first; the device reads either):
+// the host-buffer path sends u8 input over PCIe as bits
+__attribute__((target("ssse3"))) void pack_rows_p4(const uint8_t* src, int64_t rows, int32_t w, uint8_t* dst,
+                                                   int32_t rowb) {
+    const __m128i rev = _mm_setr_epi8(7, 6, 5, 4, 3, 2, 1, 0, 15, 14, 13, 12, 11, 10, 9, 8);
+    for (int64_t r = 0; r < rows; ++r) {
+        const uint8_t* s = src + r * (int64_t)w;
+        uint8_t* d = dst + r * (int64_t)rowb;
+        int32_t i = 0;
+        for (; i + 16 <= w; i += 16) {
+            __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
+            v = _mm_slli_epi16(_mm_shuffle_epi8(v, rev), 7);
+            const int m = _mm_movemask_epi8(v);
+            d[i / 8] = (uint8_t)m;
+            d[i / 8 + 1] = (uint8_t)(m >> 8);
+        }
+        for (int32_t k = i / 8; k < rowb; ++k) d[k] = 0;
+        for (; i < w; ++i) d[i / 8] |= (uint8_t)((s[i] & 1u) << (7 - i % 8));
+    }
 }
 
 template <class T>
@@ -185,6 +239,52 @@ void CUDART_CB run_deferred(void* p) {
 
 size_t up64(size_t v) { return (v + 63) & ~size_t{63}; }
 
+// debugging aid (env RUNLAB_GPU_DEBUG_TIMELINE): per-chunk stream events and host stamps,
+// printed to stderr after the call
+struct Timeline {
+    bool on = std::getenv("RUNLAB_GPU_DEBUG_TIMELINE") != nullptr;
+    int chunk = 0;
+    cudaEvent_t start = nullptr;
+    std::chrono::steady_clock::time_point t0;
+    std::vector<std::array<cudaEvent_t, 10>> ev;
+    std::vector<std::array<double, 5>> host;
+    void begin(cudaStream_t s, int nch) {
+        if (!on) return;
+        for (auto& a : ev)
+            for (auto e : a)
+                if (e) cudaEventDestroy(e);
+        ev.assign(nch, {});
+        host.assign(nch, {0, 0, 0, 0, 0});
+        if (!start) cudaEventCreate(&start);
+        cudaEventRecord(start, s);
+        cudaEventSynchronize(start);
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(int k, cudaStream_t s) {
+        if (!on || chunk >= (int)ev.size()) return;
+        cudaEventCreate(&ev[chunk][k]);
+        cudaEventRecord(ev[chunk][k], s);
+    }
+    void hmark(int c, int k) {
+        if (!on || c >= (int)host.size()) return;
+        host[c][k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    void print() {
+        if (!on) return;
+        std::fprintf(stderr, "chunk  h2d0  h2d1  kern1  fill1 | out0  out1 | post0 post1 enq0 (ms)\n");
+        for (size_t c = 0; c < ev.size(); ++c) {
+            std::fprintf(stderr, "%3zu ", c);
+            for (int k = 0; k < 10; ++k) {
+                float ms = -1;
+                if (ev[c][k]) cudaEventElapsedTime(&ms, start, ev[c][k]);
+                std::fprintf(stderr, " %6.3f%s", ms, k == 3 ? " |" : "");
+            }
+            std::fprintf(stderr, " | %6.3f %6.3f %6.3f %6.3f %6.3f\n", host[c][0], host[c][1], host[c][2], host[c][3], host[c][4]);
+        }
+    }
+};
+Timeline tl;
+
 struct IntoState {
     int64_t total = 0;  // components of the chunks posted so far
     int64_t surv = 0;   // post-fill roots of the chunks posted so far
@@ -196,7 +296,7 @@ void copy_fixed_outputs(rl_ctx* c, rl_host_outputs* out, int32_t b0) {
     const Geo& g = c->geo;
     const size_t npx = (size_t)(g.P * g.B), off = (size_t)g.P * b0;
     if (out->filled_image) {
-        if (g.ofmt == g.fmt) {
+        if (g.ofmt == c->user_ofmt) {
             cudaMemcpyAsync(out->filled_image + (size_t)g.fbytes * b0, c->ws.filled_img, (size_t)g.fbytes * g.B,
                             cudaMemcpyDeviceToHost, c->stream);
         } else {  // packed: into the staging buffer, expanded on the host once the chunk is done
@@ -211,7 +311,7 @@ void copy_fixed_outputs(rl_ctx* c, rl_host_outputs* out, int32_t b0) {
 // host expansion of chunk c's packed filled image (after its stream is synchronised)
 void expand_filled(rl_ctx* owner, rl_ctx* c, int tag, rl_host_outputs* out, int32_t b0) {
     const Geo& g = c->geo;
-    if (!out->filled_image || g.ofmt == g.fmt) return;
+    if (!out->filled_image || g.ofmt == c->user_ofmt) return;
     const int64_t rows = (int64_t)g.H * g.B;
     const int parts = (int)std::min<int64_t>(std::max<int64_t>(1, rows / 256), 8);
     for (int k = 0; k < parts; ++k) {
@@ -225,11 +325,49 @@ void expand_filled(rl_ctx* owner, rl_ctx* c, int tag, rl_host_outputs* out, int3
 
 // H2D of images [b0, b0 + n), the pipeline, and the D2H of the outputs whose size is fixed
 int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
-                 rl_host_outputs* out, int32_t b0, int32_t fmt, bool packed_out, int pack) {
-    const size_t npx = (size_t)image_bytes(w, h, fmt) * n;
+                 rl_host_outputs* out, int32_t b0, int32_t fmt, bool packed_out, int pack, HostPool* pool) {
+    // u8 input crosses PCIe as P4 bits packed by the host pool into pinned staging
+    const bool pack_in = pool && fmt == RL_PIXELS_U8 && c->packed_h2d;
+    const int32_t dfmt = pack_in ? RL_PIXELS_P4 : fmt;
+    const size_t npx = (size_t)image_bytes(w, h, dfmt) * n;
     if (!ensure(c->pix, npx)) return set_err(c, RL_ENOMEM, "device allocation failed");
-    const cudaError_t e = cudaMemcpyAsync(c->pix.p, pixels, npx, cudaMemcpyHostToDevice, c->stream);
+    const uint8_t* src = pixels;
+    if (pack_in) {
+        const int sb = c->stage;
+        if (c->h_istage_n[sb] < npx) {
+            if (c->h_istage[sb]) cudaFreeHost(c->h_istage[sb]);
+            c->h_istage[sb] = nullptr;
+            c->h_istage_n[sb] = 0;
+            if (cudaMallocHost(&c->h_istage[sb], npx) != cudaSuccess) return set_err(c, RL_ENOMEM, "pinned alloc failed");
+            c->h_istage_n[sb] = npx;
+        }
+        const int64_t rows = (int64_t)h * n;
+        const int32_t rowb = (w + 7) / 8;
+        const int parts = (int)std::min<int64_t>(std::max<int64_t>(1, rows / 128), 12);
+        uint8_t* dst = c->h_istage[sb];
+        const int tag = 2 * rl_ctx::MAXKIDS;
+        for (int k = 0; k < parts; ++k) {
+            const int64_t r0 = rows * k / parts, r1 = rows * (k + 1) / parts;
+            pool->submit(tag, [=] { pack_rows_p4(pixels + r0 * w, r1 - r0, w, dst + r0 * rowb, rowb); }, true);
+        }
+        pool->wait(tag);
+        src = dst;
+    }
+    if (!c->in_stream) {
+        if (cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->in_done, cudaEventDisableTiming) != cudaSuccess)
+            return cuda_fail(c, cudaGetLastError(), "copy stream");
+    }
+    tl.hmark(tl.chunk, 3);
+    tl.mark(0, c->in_stream);
+    const cudaError_t e = cudaMemcpyAsync(c->pix.p, src, npx, cudaMemcpyHostToDevice, c->in_stream);
     if (e != cudaSuccess) return cuda_fail(c, e, "copy in");
+    cudaEventRecord(c->in_done, c->in_stream);
+    cudaStreamWaitEvent(c->stream, c->in_done, 0);
+    tl.mark(1, c->in_stream);
+    tl.hmark(tl.chunk, 4);
+    if (c->out_done) cudaStreamWaitEvent(c->stream, c->out_done, 0);  // last chunk's table copies
+    c->user_ofmt = fmt;
     c->want_compact = out->filled && out->filled_layout == 1;
     c->want_pack = pack;
     const bool packed = packed_out && out->filled_image && fmt == RL_PIXELS_U8;
@@ -245,10 +383,12 @@ int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t
             c->h_stage_n[sb] = need;
         }
     }
-    const int rc = enqueue(c, P<uint8_t>(c->pix), w, h, n, cfg, fmt);
+    const int rc = enqueue(c, P<uint8_t>(c->pix), w, h, n, cfg, dfmt);
     c->force_ofmt = -1;  // finish() re-runs with the geometry of this call (kept in c->geo)
     if (rc) return rc;
+    tl.mark(2, c->stream);
     copy_fixed_outputs(c, out, b0);
+    tl.mark(3, c->stream);
     return RL_OK;
 }
 
@@ -258,7 +398,7 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st, HostPo
     const int B = g.B;
     if (c->reran) {  // the pipeline re-ran after the first copies
         copy_fixed_outputs(c, out, b0);
-        if (g.ofmt != g.fmt) cudaStreamSynchronize(c->stream);  // the staging buffer is expanded next
+        if (g.ofmt != c->user_ofmt) cudaStreamSynchronize(c->stream);  // the staging buffer is expanded next
     }
     if (out->filled_image) st.d2h += g.ofbytes * B;
     if (out->labels && g.label_mode) st.d2h += g.P * B * 4;
@@ -284,6 +424,15 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st, HostPo
     const bool want_comps = out->comps || out->top || out->filled;
     if (want_comps && st.total + total > out->comp_capacity) st.nospace = true;
     const int pack = c->want_pack & (c->want_compact ? 3 : 1);
+    if (!c->out_stream) {
+        if (cudaStreamCreateWithFlags(&c->out_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->out_done, cudaEventDisableTiming) != cudaSuccess)
+            return cuda_fail(c, cudaGetLastError(), "copy stream");
+    }
+    // the pipeline's stream is synchronised (finish), so the copies may start right away
+    cudaStream_t cs = c->out_stream;
+    tl.mark(4, cs);
+    Deferred* dec = nullptr;
     if (!st.nospace && pack) {
         // compact slots into pinned staging; host threads decode them once the copies land
         const int64_t nesc = (pack & 1) ? s[4 * (B + 1)] : 0, fesc = (pack & 2) ? s[4 * (B + 1) + 1] : 0;
@@ -296,17 +445,19 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st, HostPo
             if (c->h_rstage[sb]) cudaFreeHost(c->h_rstage[sb]);
             c->h_rstage[sb] = nullptr;
             c->h_rstage_n[sb] = 0;
-            if (cudaMallocHost(&c->h_rstage[sb], need + need / 4) != cudaSuccess)
+            const cudaError_t ae = cudaMallocHost(&c->h_rstage[sb], need + need / 4);
+            if (ae != cudaSuccess)
                 return set_err(c, RL_ENOMEM, "pinned alloc failed");
             c->h_rstage_n[sb] = need + need / 4;
         }
         uint8_t* h = c->h_rstage[sb];
-        cudaStream_t cs = c->stream;
         Deferred* d = new Deferred{pool, tag, {}};
         const int64_t t0 = st.total, s0 = st.surv;
         if (nrec) {
-            cudaMemcpyAsync(h, c->pk.p, 16 * (size_t)nrec, cudaMemcpyDeviceToHost, cs);
             cudaMemcpyAsync(h + o_par, c->pkpar.p, 4 * (size_t)nrec, cudaMemcpyDeviceToHost, cs);
+            tl.mark(7, cs);
+            cudaMemcpyAsync(h, c->pk.p, 16 * (size_t)nrec, cudaMemcpyDeviceToHost, cs);
+            tl.mark(6, cs);
             if (nesc) cudaMemcpyAsync(h + o_esc, c->pkesc.p, sizeof(rl_component) * nesc, cudaMemcpyDeviceToHost, cs);
             st.d2h += 20 * nrec + (int64_t)sizeof(rl_component) * nesc;
             const rlp::Slot* sl = reinterpret_cast<const rlp::Slot*>(h);
@@ -322,6 +473,7 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st, HostPo
         if (nfs) {
             cudaMemcpyAsync(h + o_fs, c->fpk.p, 16 * (size_t)nfs, cudaMemcpyDeviceToHost, cs);
             if (fesc) cudaMemcpyAsync(h + o_fesc, c->fcomp.p, sizeof(rl_features) * fesc, cudaMemcpyDeviceToHost, cs);
+            tl.mark(8, cs);
             st.d2h += 16 * nfs + (int64_t)sizeof(rl_features) * fesc;
             const rlp::Slot* sl = reinterpret_cast<const rlp::Slot*>(h + o_fs);
             const rl_features* esc = reinterpret_cast<const rl_features*>(h + o_fesc);
@@ -332,21 +484,16 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st, HostPo
                 d->tasks.emplace_back([=] { decode_features(sl, esc, dst, a, e); });
             }
         }
-        pool->reserve(tag);
-        if (cudaLaunchHostFunc(cs, run_deferred, d) != cudaSuccess) {
-            cudaGetLastError();
-            cudaStreamSynchronize(cs);
-            run_deferred(d);
-        }
+        dec = d;
     }
     if (!st.nospace) {
-        cudaStream_t cs = c->stream;
         if (out->comps && !(pack & 1)) {
             cudaMemcpyAsync(out->comps + st.total, c->ws.comps, sizeof(rl_component) * total, cudaMemcpyDeviceToHost, cs);
             st.d2h += (int64_t)sizeof(rl_component) * total;
         }
         if (out->top) {
             cudaMemcpyAsync(out->top + st.total, c->ws.top, 4 * total, cudaMemcpyDeviceToHost, cs);
+            tl.mark(9, cs);
             st.d2h += 4 * total;
         }
         if (pack & 2) {
@@ -358,6 +505,16 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st, HostPo
             st.d2h += (int64_t)sizeof(rl_features) * surv;
         }
     }
+    cudaEventRecord(c->out_done, cs);
+    tl.mark(5, cs);
+    if (dec) {  // after out_done: the next pipeline on this workspace does not wait for the callback
+        pool->reserve(tag);
+        if (cudaLaunchHostFunc(cs, run_deferred, dec) != cudaSuccess) {
+            cudaGetLastError();
+            cudaStreamSynchronize(cs);
+            run_deferred(dec);
+        }
+    }
     st.total += total;
     st.surv += surv;
     const cudaError_t e = cudaGetLastError();
@@ -365,7 +522,8 @@ int into_post(rl_ctx* c, rl_host_outputs* out, int32_t b0, IntoState& st, HostPo
 }
 
 int into_sync(rl_ctx* c) {
-    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess && c->out_stream) e = cudaStreamSynchronize(c->out_stream);
     return e == cudaSuccess ? RL_OK : cuda_fail(c, e, "copy out");
 }
 
@@ -388,7 +546,7 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     const bool packed = ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
     // component records and survivors' features cross PCIe as compact slots (pack.cuh)
     const int pack = ctx->packed_recs ? ((out->comps ? 1 : 0) | (out->filled && out->filled_layout == 1 ? 2 : 0)) : 0;
-    const bool staged = packed || pack;
+    const bool staged = packed || pack || (fmt == RL_PIXELS_U8 && ctx->packed_h2d);
     if (staged && !ctx->pool) {
         const int hw = (int)std::thread::hardware_concurrency();
         const int nt = ctx->host_threads > 0 ? ctx->host_threads : std::max(2, std::min(hw > 0 ? hw : 4, 12));
@@ -399,15 +557,16 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     const int32_t per = (int32_t)std::min<int64_t>(n, std::max<int64_t>(1, ctx->chunk_px / P));
     const int32_t nch = (n + per - 1) / per;
     IntoState st;
+    tl.begin(ctx->stream, nch);
     if (nch == 1) {
-        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed, pack);
+        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed, pack, ctx->pool);
         if (!rc) rc = finish(ctx);
         if (!rc) rc = into_post(ctx, out, 0, st, ctx->pool, 0);
         if (!rc) rc = into_sync(ctx);
         if (!rc && packed) expand_filled(ctx, ctx, 0, out, 0);
         // host tasks of this call end before it returns (after a failed copy only if the
         // stream still completes, i.e. its callbacks run)
-        if (staged && (!rc || cudaStreamSynchronize(ctx->stream) == cudaSuccess)) ctx->pool->wait(0);
+        if (staged && (!rc || into_sync(ctx) == RL_OK)) ctx->pool->wait(0);
     } else {
         const int NK = ctx->nkids;
         for (int i = 0; i < NK; ++i) {
@@ -427,7 +586,11 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
         auto post = [&](int32_t c) -> int {
             const int kid = c % NK;
             rl_ctx* k = ctx->kids[kid];
+            tl.hmark(c, 0);
             int r = finish(k);
+            tl.hmark(c, 1);
+            if (tl.on && k->reran) std::fprintf(stderr, "chunk %d re-ran (capacity)\n", c);
+            tl.chunk = c;
             if (r) return set_err(ctx, r, k->err);
             r = into_post(k, out, first_image(c), st, ctx->pool, 2 * kid + k->stage);
             if (!r && packed) expand_filled(ctx, k, 2 * kid + k->stage, out, first_image(c));
@@ -443,8 +606,10 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
                 ctx->pool->wait(2 * kid + k->stage);
             }
             const int32_t b0 = first_image(c);
+            tl.chunk = c;
+            tl.hmark(c, 2);
             rc = into_enqueue(k, pixels + (size_t)b0 * image_bytes(w, h, fmt), w, h, images(c), cfg, out, b0, fmt,
-                              packed, pack);
+                              packed, pack, ctx->pool);
             if (rc) rc = set_err(ctx, rc, k->err);
         }
         for (int32_t c = std::max(0, nch - NK); c < nch && !rc; ++c) rc = post(c);
@@ -452,13 +617,14 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
             if (!rc) rc = into_sync(ctx->kids[i]) ? set_err(ctx, RL_ECUDA, ctx->kids[i]->err) : RL_OK;
         bool drained = true;
         if (rc)
-            for (int i = 0; i < NK; ++i) drained = cudaStreamSynchronize(ctx->kids[i]->stream) == cudaSuccess && drained;
+            for (int i = 0; i < NK; ++i) drained = into_sync(ctx->kids[i]) == RL_OK && drained;
         if (staged && drained)
             for (int tag = 0; tag < 2 * NK; ++tag) ctx->pool->wait(tag);
     }
     if (rc) return rc;
+    tl.print();
     out->comps_needed = st.total;
-    out->h2d_bytes = image_bytes(w, h, fmt) * n;
+    out->h2d_bytes = image_bytes(w, h, fmt == RL_PIXELS_U8 && ctx->packed_h2d ? RL_PIXELS_P4 : fmt) * n;
     out->d2h_bytes = st.d2h;
     if (st.nospace) return set_err(ctx, RL_ENOSPC, "component buffers too small");
     return RL_OK;

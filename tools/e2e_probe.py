@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--variants", default="base")
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--spin", action="store_true", help="keep one SM busy on a side stream (power-state probe)")
     args = ap.parse_args()
     import torch
     from paper_2006_09299_b200 import Labeler, LabelingConfig, _native as N
@@ -53,7 +54,11 @@ def main():
                                    cap, h_summ.data_ptr(), h_off.data_ptr(), 0, 0, 0, 1, 0)
             lab.label_into(src.data_ptr(), S, S, B, cfg, outs, pixel_format=fmt)
             ts = []
+            side = torch.cuda.Stream()
             for _ in range(args.steps):
+                if args.spin:
+                    with torch.cuda.stream(side):
+                        torch.cuda._sleep(2_000_000_00 // 10)  # ~10 ms at 2 GHz
                 t0 = time.perf_counter()
                 lab.label_into(src.data_ptr(), S, S, B, cfg, outs, pixel_format=fmt)
                 ts.append(time.perf_counter() - t0)
@@ -62,6 +67,19 @@ def main():
                   f"med {ts[len(ts)//2]*1e3:6.2f} ms  d2h {outs.d2h_bytes/1e6:6.1f} MB  "
                   f"{B*S*S/ts[len(ts)//2]/1e9:6.1f} Gpx/s", flush=True)
         lab.close()
+    # raw D2H bandwidth in this process afterwards (is something in the process throttling PCIe?)
+    N = 24 << 20
+    dbuf = torch.empty(N, dtype=torch.uint8, device="cuda")
+    hb = torch.empty(N, dtype=torch.uint8, pin_memory=True)
+    cs = torch.cuda.Stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cs)
+    with torch.cuda.stream(cs):
+        for _ in range(20):
+            hb.copy_(dbuf, non_blocking=True)
+    e1.record(cs)
+    torch.cuda.synchronize()
+    print(f"raw D2H in-process: {20 * N / e0.elapsed_time(e1) / 1e6:.1f} GB/s")
 
 
 if __name__ == "__main__":
