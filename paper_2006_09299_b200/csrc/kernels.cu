@@ -711,7 +711,6 @@ struct EmitSmem {
     uint16_t dfold[C::FCH];  // chunk components whose post-fill root is an interior survivor
     int ndfold;
     uint64_t cb;
-    unsigned long long moff;  // offset of the tile's component map
     int gate;                 // the merge phase succeeded (no capacity overflow)
 };
 
@@ -797,7 +796,19 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         S.nlc = hdr[1];
         S.nb = nb_h;
     }
-    if (tid == 32) E.moff = ws.tmap[tg.t];
+    {  // the run -> component map and component tables the analyze pass stored (tile_runs below
+       // does not touch them); bounds-checked so that a failed gate never reads past the store
+        const uint64_t moff = ws.tmap[tg.t];
+        const int nr = hdr[0], nl = hdr[1];
+        if (moff + (uint64_t)(nr + 2 * nl) <= ws.cap_rstore) {
+            const uint16_t* src = ws.rstore + moff;
+            for (int i = tid; i < nr; i += BT) S.par[i] = src[i];
+            for (int l = tid; l < nl; l += BT) {
+                S.lcrun[l] = src[nr + l];
+                S.lcb[l] = src[nr + nl + l];
+            }
+        }
+    }
     if (tid < FOLD_SLOTS) {
         E.pkey[tid] = 0xFFFF;
         E.ps[tid] = E.psx[tid] = E.psy[tid] = 0;
@@ -831,15 +842,6 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     RL_PHASE(tg.t, 16);
     WordBits wb;
     if (!tile_runs<false>(S, wb)) return false;
-    {
-        const int nr = wb.nruns, nl = S.nlc;
-        const uint16_t* src = ws.rstore + E.moff;
-        for (int i = tid; i < nr; i += BT) S.par[i] = src[i];
-        for (int l = tid; l < nl; l += BT) {
-            S.lcrun[l] = src[nr + l];
-            S.lcb[l] = src[nr + nl + l];
-        }
-    }
     RL_PHASE(tg.t, 17);
     const int nruns = wb.nruns, nlc = S.nlc, nb = S.nb;  // S.nruns is not visible before a barrier
     const uint64_t cb = E.cb;
