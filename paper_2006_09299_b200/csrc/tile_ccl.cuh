@@ -357,12 +357,14 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
         for (int i = rs + tid; i < nr; i += BT) {
             uint32_t p = S.par[i];
             if (p == (uint32_t)i) continue;  // no first contact: a root
+            // walk to the root, publishing each step: walks that pass through run i then jump
+            // as far as i's walk got (vertical stacks of runs: pointer jumping, log depth)
             for (;;) {
                 const uint32_t q = S.par[p];
                 if (q == p) break;
                 p = q;
+                S.par[i] = (uint16_t)p;
             }
-            S.par[i] = (uint16_t)p;
         }
         __syncthreads();
     }
@@ -434,8 +436,8 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
                 const uint32_t q = S.par[p];
                 if (q == p) break;
                 p = q;
+                S.par[i] = (uint16_t)p;  // published as it goes (see the pre-flatten)
             }
-            S.par[i] = (uint16_t)p;
         }
         const unsigned m = __ballot_sync(0xFFFFFFFFu, i < nruns && p == (uint32_t)i);
         if (lane == 0) S.rmask[b >> 5] = m;
