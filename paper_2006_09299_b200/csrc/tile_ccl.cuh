@@ -471,18 +471,29 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
         const int k = tid < tg.th ? S.rbase[tid * WPR] : nruns;
         S.rowlc[tid] = (uint16_t)(k < nruns ? rank_of((uint32_t)k) : (uint32_t)nlc);
     }
+    if (tid < tg.th) {  // border components through the left and right tile columns: every row's
+                        // first run starts at column 0 and its last run ends at the tile edge
+        // (a slot the loop below already rewrote holds TAG16 | component)
+        auto comp_of = [&](int k) {
+            const uint32_t v = S.par[k];
+            return (v & TAG16) ? (v & 0x7FFFu) : rank_of(v);
+        };
+        S.lcb[comp_of(S.rbase[tid * WPR])] = 1;
+        S.lcb[comp_of(S.rbase[(tid + 1) * WPR] - 1)] = 1;
+    }
     RL_PHASE(tg.t, 6);
     const unsigned long long moff = S.moff;
     uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
-    // every run: its component, the component's first run, border flags (plain stores of 1)
+    // every run: its component, the component's first run, border flags of the top and bottom
+    // rows' runs (plain stores of 1)
+    const int top_end = S.rbase[WPR], bot_begin = S.rbase[(tg.th - 1) * WPR];
     for (int i = tid; i < nruns; i += BT) {
         const uint32_t root = S.par[i];
         const uint32_t l = rank_of(root);
         S.par[i] = (uint16_t)(TAG16 | l);
         if (root == (uint32_t)i) S.lcrun[l] = (uint16_t)i;
         if (map) map[i] = (uint16_t)l;
-        const int rr = run_row(S, i), c0 = run_col(S, i);
-        if (rr == 0 || rr == tg.th - 1 || c0 == 0 || run_end(S, i, tg.tw) == tg.tw) S.lcb[l] = 1;
+        if (i < top_end || i >= bot_begin) S.lcb[l] = 1;
     }
     __syncthreads();
     RL_PHASE(tg.t, 7);
