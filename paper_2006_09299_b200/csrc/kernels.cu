@@ -994,8 +994,9 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         f.col_max = tg.x0 + E.pcmax[i];
         acc_atomic_fold(ws.filled + cb + E.banc[E.pkey[i]], f);
     }
-    nsurv = block_reduce_sum<BT>(nsurv, S.wsum);  // also orders the ext-mask atomics before use
-    if (tid == 0 && nsurv) atomicAdd(&ws.img_surv[tg.b], (uint32_t)nsurv);
+    nsurv = __reduce_add_sync(0xFFFFFFFFu, nsurv);
+    if ((tid & 31) == 0 && nsurv) atomicAdd(&ws.img_surv[tg.b], (uint32_t)nsurv);
+    __syncthreads();  // the ext-mask atomics are complete
     RL_PHASE(tg.t, 23);
 
     // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
