@@ -791,6 +791,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     if (tid < TH && tid < tg.th)
         E.rowoff[tid] = ws.off[img0 + (int64_t)(tg.y0 + tid) * g.ntx + tg.tx] - offimg;
     if (tid == 0) {
+        E.ndfold = 0;
         E.cb = (uint64_t)offimg + (uint64_t)tg.b;
         E.gate = !ws.counters[1] && comps_fit(g, ws);
         S.nlc = hdr[1];
@@ -882,6 +883,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
                 E.fcmin[i] = 0x7FFFFFFF;
                 E.fcmax[i] = -1;
             }
+            if (tid == 0) E.ndfold = 0;  // the last chunk's deferred folds were read before its final barrier
             __syncthreads();
         }
         RL_PHASE(tg.t, 19);
@@ -915,8 +917,6 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         // pre-fill records, post-fill roots, survivor init; folds into border-component roots
         // (initialised by the merge phase) go to the shared table right away, folds into
         // interior survivors wait until the survivors' own records are written (barrier)
-        if (tid == 0) E.ndfold = 0;
-        __syncthreads();
         for (int lc = l0 + tid; lc < l1; lc += BT) {
             if (lc_is_border(S, lc)) continue;
             const int k = lc - l0;
