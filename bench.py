@@ -235,7 +235,8 @@ def run_reference_arm(args, wl: Workload, rank: int) -> None:
 # ------------------------------------------------------------------------------ our arm
 def run_strips(args, wl: Workload, rank: int, world: int, local: int) -> None:
     """SURVEY 8(e): the single image of the workload cut into one horizontal strip per rank;
-    three collectives per step (strips.py).  Strong scaling: the image is fixed."""
+    four collectives per step, O(width) bytes each (strips.py).  Strong scaling: the image is
+    fixed."""
     import torch
     import torch.distributed as dist
 
@@ -318,8 +319,9 @@ def run_strips(args, wl: Workload, rank: int, world: int, local: int) -> None:
             "config": {"workload": wl.desc + ", fg8_bg4, features+Euler+tree+hole fill",
                        "images_per_gpu": 1.0 / world, "pixels_per_gpu": P // world,
                        "l2": "inputs > L2 (no flush)" if P // world > 126e6 else "strip fits L2",
-                       "parallelism": f"horizontal strips x{world} (all-gather of border-component "
-                                      "tables, all-reduce of border survivors' partial features)"},
+                       "parallelism": f"horizontal strips x{world} (all-gather of cut-class tables and "
+                                      "cut-row labels, all-reduce of cut components' links and of "
+                                      "cut survivors' partial features)"},
             "roofline": {"bound": "hbm", "kernel": "whole strip step (per GPU)", "achieved": per_gpu_gbs,
                          "peak": peak, "unit": "GB/s", "frac": per_gpu_gbs / peak, "traffic": None,
                          "peak_source": peak_src, "c_pre": c_pre, "c_post": c_post},

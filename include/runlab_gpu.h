@@ -216,37 +216,50 @@ int rl_last_used_graph(const rl_ctx* ctx);
 
 /* ---- One image cut into horizontal strips across ranks -----------------------
  * Rank r holds rows [y0, y0 + h) of one w x H image in device memory (y0 a multiple of 32; h a
- * multiple of 32 except for the last strip).  Phases, with the caller's collectives between them
- * (paper_2006_09299_b200/strips.py does them with torch.distributed; NCCL on GPUs):
- *   1. rl_strip_local   tile passes + seams inside the strip (cut rows are open, not frame)
+ * multiple of 32 except for the last strip).  Only O(w) data crosses ranks: the components that
+ * touch a cut row ("cut classes") and the two cut rows' labels.  Phases, with the caller's
+ * collectives between them (paper_2006_09299_b200/strips.py does them with torch.distributed;
+ * NCCL on GPUs):
+ *   1. rl_strip_local   tile passes, seams and flattening inside the strip (cut rows are open,
+ *                       not frame); numbers the strip's cut classes
  *   2. [all-gather of every rank's rl_strip_local_info]
- *   3. rl_strip_export  the strip's exchange record (border components, cut-row perimeter
- *                       labels, per-row counts) into a device buffer of
- *                       rl_strip_export_bytes(w, max_nodes, max_tile_rows) bytes
- *   4. [all-gather of the records: n_strips consecutive records]
- *   5. rl_strip_merge   union across the cuts and the merge over all strips' border components
- *                       (identical on every rank), then the emit pass of this strip; returns
- *                       this rank's partial post-fill sums of the border survivors
- *   6. [all-reduce of the partials in place: d_sum SUM, d_min MIN, d_max MAX, d_count SUM]
- *   7. rl_strip_finish  post-fill features; the canonical-id range [comp_lo, comp_hi) this strip
+ *   3. rl_strip_export  the strip's exchange record (per cut class: first-pixel key, features,
+ *                       foreground flag; the exterior's partial features; both cut rows as
+ *                       (value << 31) | class) into a device buffer of
+ *                       rl_strip_export_bytes(w, max_classes) bytes
+ *   4. [all-gather of the records: n_strips consecutive records, in image order]
+ *   5. rl_strip_merge   union across the cuts (identical on every rank), canonical numbering of
+ *                       this strip; returns the link table (canonical id and parent-chain exit of
+ *                       every cut component this strip owns; zero elsewhere)
+ *   6. [all-reduce SUM of the link table in place]
+ *   7. rl_strip_resolve depth-1 ancestors, tree and emit passes of this strip; returns this
+ *                       rank's partial post-fill sums of the survivors that cross a cut
+ *   8. [all-reduce of the partials in place: d_sum SUM, d_min MIN, d_max MAX, d_count SUM]
+ *   9. rl_strip_finish  post-fill features; the canonical-id range [comp_lo, comp_hi) this strip
  *                       owns (components whose first pixel lies in it; strip 0 also owns the
  *                       exterior, id 0)
- *   8. rl_strip_fetch   copies that range and the strip's filled/label image rows to the host.
+ *  10. rl_strip_fetch   copies that range and the strip's filled/label image rows to the host.
  * Concatenating the strips' outputs gives exactly the single-image result.  densify_labels is
  * not supported in strip mode (RL_EINVAL). */
 typedef struct rl_strip_local_info {
-    int64_t n_nodes;      /* border components of the strip */
-    int64_t interior_fg;  /* foreground components inside single tiles */
-    int32_t ty0, ty1;     /* tile rows of the strip */
+    int64_t n_classes;  /* cut classes: strip components touching a cut row (exterior excluded) */
+    int64_t n_comps;    /* strip components touching no cut row (exterior excluded) */
+    int64_t n_fg;       /* ... of which foreground */
+    int32_t ty0, ty1;   /* tile rows of the strip */
     int32_t status, pad;
 } rl_strip_local_info;
+
+typedef struct rl_strip_links {
+    void* d_links;  /* int64 [n]: all-reduced with SUM */
+    int64_t n;
+} rl_strip_links;
 
 typedef struct rl_strip_partials {
     void* d_sum;    /* int64 [k * 3]: S, Sx, Sy */
     void* d_min;    /* int32 [k * 2]: row_min, col_min */
     void* d_max;    /* int32 [k * 2]: row_max, col_max */
-    void* d_count;  /* int64 [1]: interior survivors of this strip */
-    int64_t k;      /* border survivors (identical on every rank) */
+    void* d_count;  /* int64 [1]: survivors of this strip that touch no cut */
+    int64_t k;      /* global cut-class slots (identical on every rank) */
 } rl_strip_partials;
 
 typedef struct rl_strip_result {
@@ -257,10 +270,11 @@ typedef struct rl_strip_result {
 
 int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t width, int32_t height, int32_t y0,
                    int32_t h, const rl_config* cfg, rl_strip_local_info* out);
-int64_t rl_strip_export_bytes(int32_t width, int64_t max_nodes, int32_t max_tile_rows);
-int rl_strip_export(rl_ctx* ctx, int64_t max_nodes, int32_t max_tile_rows, void* d_buf);
+int64_t rl_strip_export_bytes(int32_t width, int64_t max_classes);
+int rl_strip_export(rl_ctx* ctx, int64_t max_classes, void* d_buf);
 int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const rl_strip_local_info* infos,
-                   int64_t max_nodes, int32_t max_tile_rows, rl_strip_partials* out);
+                   int64_t max_classes, rl_strip_links* out);
+int rl_strip_resolve(rl_ctx* ctx, rl_strip_partials* out);
 int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out);
 /* comps/top/filled (layout 0) of [comp_lo, comp_hi), filled_image/labels of the strip's rows */
 int rl_strip_fetch(rl_ctx* ctx, const rl_strip_result* r, rl_host_outputs* out);

@@ -21,7 +21,8 @@ EXPORTED_SYMBOLS = (
     "rl_sync", "rl_fetch", "rl_device_filled_image", "rl_device_labels", "rl_device_comps",
     "rl_stream", "rl_set_stream", "rl_last_launch_count", "rl_tile_shape", "rl_label_into",
     "rl_phase_times", "rl_generate", "rl_generate_rings", "rl_cfg4_params", "rl_last_used_graph",
-    "rl_strip_local", "rl_strip_export_bytes", "rl_strip_export", "rl_strip_merge", "rl_strip_finish",
+    "rl_strip_local", "rl_strip_export_bytes", "rl_strip_export", "rl_strip_merge", "rl_strip_resolve",
+    "rl_strip_finish",
     "rl_strip_fetch", "rl_generate_rows", "rl_filter_components",
     "rl_filter_components_host", "rl_label_device_fmt", "rl_label_into_fmt", "rl_pbm_parse", "rl_pbm_p1_to_p4",
     "rl_pbm_p4_header", "rl_fill_pbm", "rl_generate_host",
@@ -67,8 +68,12 @@ class RlPbmInfo(C.Structure):
 
 
 class RlStripLocalInfo(C.Structure):
-    _fields_ = [("n_nodes", C.c_int64), ("interior_fg", C.c_int64), ("ty0", C.c_int32),
+    _fields_ = [("n_classes", C.c_int64), ("n_comps", C.c_int64), ("n_fg", C.c_int64), ("ty0", C.c_int32),
                 ("ty1", C.c_int32), ("status", C.c_int32), ("pad", C.c_int32)]
+
+
+class RlStripLinks(C.Structure):
+    _fields_ = [("d_links", C.c_void_p), ("n", C.c_int64)]
 
 
 class RlStripPartials(C.Structure):
@@ -138,10 +143,11 @@ def load() -> C.CDLL:
     L.rl_strip_local.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                  C.POINTER(RlConfig), C.POINTER(RlStripLocalInfo)]
     L.rl_strip_export_bytes.restype = C.c_int64
-    L.rl_strip_export_bytes.argtypes = [C.c_int32, C.c_int64, C.c_int32]
-    L.rl_strip_export.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
+    L.rl_strip_export_bytes.argtypes = [C.c_int32, C.c_int64]
+    L.rl_strip_export.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
     L.rl_strip_merge.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(RlStripLocalInfo),
-                                 C.c_int64, C.c_int32, C.POINTER(RlStripPartials)]
+                                 C.c_int64, C.POINTER(RlStripLinks)]
+    L.rl_strip_resolve.argtypes = [C.c_void_p, C.POINTER(RlStripPartials)]
     L.rl_strip_finish.argtypes = [C.c_void_p, C.POINTER(RlStripResult)]
     L.rl_strip_fetch.argtypes = [C.c_void_p, C.POINTER(RlStripResult), C.POINTER(RlHostOutputs)]
     _lib = L

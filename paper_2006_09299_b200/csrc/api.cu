@@ -548,7 +548,7 @@ void rl_destroy(rl_ctx* c) {
                       &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
                       &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,
-                      &c->fcomp, &c->nleft, &c->scount, &c->pk, &c->pkpar, &c->pkesc, &c->fpk};
+                      &c->fcomp, &c->nleft, &c->scount, &c->ncut, &c->xnode, &c->gtab, &c->pk, &c->pkpar, &c->pkesc, &c->fpk};
     for (rl_ctx* k : c->kids) rl_destroy(k);
     strip_free(c);
     pool_free(c);

@@ -93,6 +93,8 @@ struct Ws {
     uint32_t* nparent;   // root node of the surrounding component (valid at roots)
     uint32_t* nanccid;   // canonical id of the post-fill root (valid at roots)
     uint32_t* nleft;     // strip mode: node of the pixel left of the first pixel (else null)
+    uint32_t* ncut;      // strip mode: 1 + global root of the cut class at a cut-class root node,
+                         // 0 elsewhere (else null; strips.cu)
     // canonical numbering
     uint32_t* cnt;       // [B*H*ntx + 1] roots whose first pixel is in (image,row,tile col)
     uint32_t* off;       // exclusive scan of cnt

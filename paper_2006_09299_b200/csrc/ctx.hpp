@@ -149,7 +149,7 @@ struct rl_ctx {
     cudaStream_t in_stream = nullptr;
     cudaEvent_t in_done = nullptr;
     // strip mode (strips.cu)
-    DevBuf nleft, scount;
+    DevBuf nleft, scount, ncut, xnode, gtab;
     rlh::StripState* strip = nullptr;
 };
 

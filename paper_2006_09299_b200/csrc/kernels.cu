@@ -587,9 +587,11 @@ __global__ void k_cids(Geo g, Ws ws) {
                     c.flags = rec.fg;
                     ws.comps[cb + cid] = c;
                     if (proot < (uint32_t)g.B) {
-                        // strip mode: this rank's partial post-fill sums start empty (strips.cu)
-                        ws.filled[cb + cid] = g.strip ? acc_empty() : c.f;
-                        ++nsurv;
+                        // strip mode: a survivor crossing a cut collects every rank's partial
+                        // post-fill sums, so it starts empty and is counted globally (strips.cu)
+                        const bool cut = ws.ncut && ws.ncut[root];
+                        ws.filled[cb + cid] = cut ? acc_empty() : c.f;
+                        if (!cut) ++nsurv;
                     }
                 }
             }
@@ -626,21 +628,32 @@ __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
         Acc f;
         if (n < hi && ws.nrep[n]) {
             const uint32_t root = ws.uf[n];
-            uint32_t cur = root;
-            for (;;) {
-                const uint32_t p = ws.nparent[cur];
-                if (p < (uint32_t)g.B) break;
-                cur = p;
+            uint32_t anc;
+            if (ws.ncut && ws.ncut[root]) {
+                anc = ws.nanccid[root];  // strip mode: a class crossing a cut, resolved globally
+            } else {
+                uint32_t cur = root;
+                for (;;) {
+                    const uint32_t p = ws.nparent[cur];
+                    if (p < (uint32_t)g.B) {
+                        anc = ws.nrootcid[cur];
+                        break;
+                    }
+                    if (ws.ncut && ws.ncut[p]) {  // strip mode: the chain leaves the strip
+                        anc = ws.nanccid[p];
+                        break;
+                    }
+                    cur = p;
+                }
+                ws.nanccid[root] = anc;
             }
-            const uint32_t anc = ws.nrootcid[cur];
-            ws.nanccid[root] = anc;
             int32_t b, ty, tx;
             tile_of(g, ws.nrec[n].tile, b, ty, tx);
             const uint64_t cb = comp_base(g, ws, b);
             const uint32_t cid = ws.nrootcid[root];
             ws.top[cb + cid] = anc;
             ws.comps[cb + cid].parent = ws.nrootcid[ws.nparent[root]];
-            if (cur != root && !g.strip) {
+            if (anc != cid && !g.strip) {
                 dst = (uint32_t)(cb + anc);  // < 2^32 components
                 f = ws.nacc[root];
             }

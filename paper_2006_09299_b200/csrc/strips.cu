@@ -1,25 +1,41 @@
-// strips.cu -- one image cut into horizontal strips across ranks.
+// strips.cu -- one image cut into horizontal strips across ranks, with an O(W)
+// exchange: only the components touching a cut row ("cut classes") and the cut rows' labels
+// cross between ranks.
 //
 // Every rank runs the tile passes on its own strip with the geometry of the WHOLE image (tile
 // rows [ty0, ty1), pixel row y at row y - prow0 of the rank's buffer), so the image frame is
-// exterior only where it really is: cut rows are open.  The exchange is between three phases:
+// exterior only where it really is: cut rows are open.  Phases, with the caller's collectives
+// between them (paper_2006_09299_b200/strips.py, torch.distributed / NCCL):
 //
-//   local   analyze + seams inside the strip; every border component (node) gets the node of the
-//           pixel left of its first pixel (resolved now: that pixel is in the same row).
-//   merge   every rank imports all strips' node tables (shifted to one global numbering), the
-//           cut rows' perimeter labels and the per-row interior counts, unions across the cuts
-//           and runs the merge passes over all nodes (identical on every rank), then emits its
-//           own tiles.  Interior components fold their features into post-fill roots that may
-//           be owned by other strips, so border survivors collect per-rank partial sums.
-//   finish  the all-reduced partials plus the border part give the post-fill features.
+//   local    analyze + seams inside the strip, flatten (k_resolve); the local classes touching
+//            a cut row are numbered 1..n (0 = the exterior); the strip counts its components
+//            that touch no cut (interior + border ones).
+//   export   per cut class: first-pixel key, fold of its features, foreground flag; the
+//            strip's exterior partial features; both cut rows as (value << 31) | class.
+//            O(W) bytes per strip.                                     [all-gather]
+//   merge    (identical on every rank, over all strips' cut classes) union across the cuts,
+//            fold features and min keys into global cut classes (GCC), the representative
+//            class of every GCC (it holds the first pixel; its strip owns the GCC); per-strip
+//            component counts give every strip's canonical id offset.  Then this strip's
+//            numbering (k_reps / scan / k_cids with the GCC representatives counted only where
+//            owned) and, for every owned GCC, its canonical id and where its parent chain
+//            leaves the strip: the exterior (then its depth-1 ancestor is known) or another
+//            GCC.                                                        [all-reduce SUM]
+//   resolve  every GCC's depth-1 ancestor by walking the GCC links, then the unchanged tree
+//            pass (k_tops stops at cut classes), emit, border folds; this rank's partial
+//            post-fill sums of the GCC survivors.                        [all-reduce]
+//   finish   survivors that cross a cut: reduced partials + their own features.
 //
-// The collectives themselves (all-gather of the local infos and of the export records,
-// all-reduce of the partials) are the caller's: paper_2006_09299_b200/strips.py does them with
-// torch.distributed (NCCL over NVLink on GPUs).
+// Per-rank work is O(own strip + cut classes of all strips); nothing of another strip's
+// interior is imported.  Canonical ids stay the raster order of first pixels over the whole
+// image, so the strips' outputs concatenate to exactly the single-image result
+// (labeling.hpp:190-217 numbering via tables.hpp:68-76).
 //
-// Canonical ids stay the raster order of first pixels over the whole image, so the strips'
-// outputs concatenate to exactly the single-image result (labeling.hpp:190-217 numbering via
-// tables.hpp:68-76).
+// Why the GCC graph is all that crosses ranks: a component's parent is the component of the
+// pixel left of its first pixel (same row, same strip), and whatever surrounds a component
+// that touches a cut row also touches that cut (it has pixels on both sides of it), so every
+// ancestor of a cut class is a cut class or the exterior, and every post-fill fold that
+// crosses strips lands on a GCC survivor.
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
@@ -37,38 +53,77 @@ using namespace rlh;
 
 namespace {
 
-// exchange record of one border component
-struct NodeX {
-    uint32_t uf, nleft;  // local node ids (0 = exterior)
-    uint64_t key;
-    Acc acc;
-    NodeRec rec;
+// one cut class in the exchange record
+struct XClass {
+    uint64_t key;  // first pixel (global raster index); ~0 for the exterior entry
+    Acc acc;       // the class's features inside this strip
+    uint32_t fg, pad;
 };
-static_assert(sizeof(NodeX) == 72, "NodeX layout");
+static_assert(sizeof(XClass) == 56, "XClass layout");
 
 struct XHeader {
-    int64_t n_nodes;
+    int64_t n_classes;
     int32_t ty0, ty1;
     int64_t pad[6];
 };
 static_assert(sizeof(XHeader) == 64, "XHeader layout");
 
 struct XLayout {
-    size_t nodes, tiles, cnt, perim, bytes;
+    size_t classes, cut, bytes;
 };
 
 size_t align8(size_t v) { return (v + 7) & ~size_t(7); }
 
-XLayout x_layout(int32_t W, int64_t max_nodes, int32_t max_tile_rows) {
-    const int32_t ntx = (W + TW - 1) / TW;
+XLayout x_layout(int32_t W, int64_t max_classes) {
     XLayout L;
-    L.nodes = sizeof(XHeader);
-    L.tiles = L.nodes + align8((size_t)max_nodes * sizeof(NodeX));
-    L.cnt = L.tiles + align8((size_t)max_tile_rows * ntx * 8);
-    L.perim = L.cnt + align8((size_t)max_tile_rows * TH * ntx * 4);
-    L.bytes = L.perim + align8((size_t)ntx * 2 * TW * 2);
+    L.classes = sizeof(XHeader);
+    L.cut = L.classes + align8((size_t)(max_classes + 1) * sizeof(XClass));
+    L.bytes = L.cut + align8((size_t)2 * W * 4);
     return L;
 }
+
+// global cut-class tables (identical on every rank), laid out in ctx->gtab
+struct GTab {
+    uint32_t *uf, *root, *rep, *cid, *anc, *coff, *scnt, *gsurv;
+    uint64_t* kmin;
+    Acc* tot;
+    int64_t *links, *psum, *pcnt;
+    int32_t *pmin, *pmax;
+    size_t bytes;
+};
+
+GTab g_layout(void* base, int64_t C, int k) {
+    GTab T{};
+    uint8_t* p = static_cast<uint8_t*>(base);
+    size_t o = 0;
+    auto take = [&](size_t b) {
+        uint8_t* q = p ? p + o : nullptr;
+        o += align8(b);
+        return q;
+    };
+    T.links = reinterpret_cast<int64_t*>(take((size_t)C * 16));
+    T.psum = reinterpret_cast<int64_t*>(take((size_t)C * 24));
+    T.pcnt = reinterpret_cast<int64_t*>(take(8));
+    T.pmin = reinterpret_cast<int32_t*>(take((size_t)C * 8));
+    T.pmax = reinterpret_cast<int32_t*>(take((size_t)C * 8));
+    T.tot = reinterpret_cast<Acc*>(take((size_t)C * sizeof(Acc)));
+    T.kmin = reinterpret_cast<uint64_t*>(take((size_t)C * 8));
+    T.uf = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
+    T.root = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
+    T.rep = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
+    T.cid = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
+    T.anc = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
+    T.coff = reinterpret_cast<uint32_t*>(take((size_t)(k + 1) * 4));
+    T.scnt = reinterpret_cast<uint32_t*>(take((size_t)2 * k * 4));
+    T.gsurv = reinterpret_cast<uint32_t*>(take(8));
+    T.bytes = o;
+    return T;
+}
+
+#define GRID_LOOP(i, n) \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)(n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ---- local phase ----------------------------------------------------------------------------
 
 // node of the pixel left of each border component's first pixel (local numbering)
 __global__ void k_strip_left(Geo g, Ws ws) {
@@ -90,81 +145,8 @@ __global__ void k_strip_left(Geo g, Ws ws) {
     }
 }
 
-__global__ void k_strip_pack(Geo g, Ws ws, uint8_t* buf, XLayout L) {
-    const uint32_t n_used = min(ws.counters[0], ws.cap_nodes);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (tid == 0) {
-        XHeader h{};
-        h.n_nodes = n_used;
-        h.ty0 = g.ty0;
-        h.ty1 = g.ty1;
-        *reinterpret_cast<XHeader*>(buf) = h;
-    }
-    NodeX* xn = reinterpret_cast<NodeX*>(buf + L.nodes);
-    for (int64_t i = tid; i < n_used; i += stride) {
-        const uint32_t n = 1u + (uint32_t)i;
-        NodeX x;
-        x.uf = ws.uf[n];
-        x.nleft = ws.nleft[n];
-        x.key = ws.nkey[n];
-        x.acc = ws.nacc[n];
-        x.rec = ws.nrec[n];
-        xn[i] = x;
-    }
-    const int64_t t0 = (int64_t)g.ty0 * g.ntx, nt = (int64_t)(g.ty1 - g.ty0) * g.ntx;
-    uint32_t* xt = reinterpret_cast<uint32_t*>(buf + L.tiles);
-    for (int64_t i = tid; i < nt; i += stride) {
-        xt[2 * i] = ws.tbase[t0 + i];
-        xt[2 * i + 1] = ws.tnb[t0 + i];
-    }
-    const int64_t r0 = (int64_t)g.ty0 * TH, r1 = min((int64_t)g.ty1 * TH, (int64_t)g.H);
-    uint32_t* xc = reinterpret_cast<uint32_t*>(buf + L.cnt);
-    for (int64_t i = tid; i < (r1 - r0) * g.ntx; i += stride) xc[i] = ws.cnt[r0 * g.ntx + i];
-    // cut rows: top perimeter row of the first tile row, bottom row of the last one
-    uint16_t* xp = reinterpret_cast<uint16_t*>(buf + L.perim);
-    for (int64_t i = tid; i < (int64_t)g.ntx * 2 * TW; i += stride) {
-        const int64_t tx = i / (2 * TW), k = i % (2 * TW);
-        const int64_t t = (k < TW ? t0 : t0 + nt - g.ntx) + tx;
-        xp[i] = ws.perim[t * PERIM + k];  // k < TW: top row; TW <= k < 2TW: bottom row
-    }
-}
-
-// one source strip's record into the global tables
-__global__ void k_strip_unpack(Geo g, Ws ws, const uint8_t* buf, XLayout L, uint32_t off) {
-    const XHeader h = *reinterpret_cast<const XHeader*>(buf);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const NodeX* xn = reinterpret_cast<const NodeX*>(buf + L.nodes);
-    auto shift = [&](uint32_t v) { return v ? v + off : 0u; };
-    for (int64_t i = tid; i < h.n_nodes; i += stride) {
-        const NodeX x = xn[i];
-        const uint32_t n = 1u + off + (uint32_t)i;
-        ws.uf[n] = shift(x.uf);
-        ws.nleft[n] = shift(x.nleft);
-        ws.nkey[n] = x.key;
-        ws.nmin[n] = x.key;
-        ws.nacc[n] = x.acc;
-        ws.nrec[n] = x.rec;
-    }
-    const int64_t t0 = (int64_t)h.ty0 * g.ntx, nt = (int64_t)(h.ty1 - h.ty0) * g.ntx;
-    const uint32_t* xt = reinterpret_cast<const uint32_t*>(buf + L.tiles);
-    for (int64_t i = tid; i < nt; i += stride) {
-        ws.tbase[t0 + i] = xt[2 * i] + off;
-        ws.tnb[t0 + i] = xt[2 * i + 1];
-    }
-    const int64_t r0 = (int64_t)h.ty0 * TH, r1 = min((int64_t)h.ty1 * TH, (int64_t)g.H);
-    const uint32_t* xc = reinterpret_cast<const uint32_t*>(buf + L.cnt);
-    for (int64_t i = tid; i < (r1 - r0) * g.ntx; i += stride) ws.cnt[r0 * g.ntx + i] = xc[i];
-    const uint16_t* xp = reinterpret_cast<const uint16_t*>(buf + L.perim);
-    for (int64_t i = tid; i < (int64_t)g.ntx * 2 * TW; i += stride) {
-        const int64_t tx = i / (2 * TW), k = i % (2 * TW);
-        const int64_t t = (k < TW ? t0 : t0 + nt - g.ntx) + tx;
-        ws.perim[t * PERIM + k] = xp[i];
-    }
-}
-
-__global__ void k_strip_exterior(Ws ws, uint32_t n_total) {
+// the exterior node (analyze initialises it only in the image's first tile)
+__global__ void k_strip_exterior(Ws ws) {
     ws.uf[0] = 0;
     ws.nacc[0] = acc_empty();
     ws.nmin[0] = ~0ull;
@@ -172,70 +154,306 @@ __global__ void k_strip_exterior(Ws ws, uint32_t n_total) {
     ws.nparent[0] = 0;
     ws.nanccid[0] = 0;
     ws.nrep[0] = 0;
-    ws.counters[0] = n_total;
-    ws.counters[1] = 0;
 }
 
-// border survivors (post-fill roots that are border components), flagged at their root node
-__global__ void k_strip_surv_flags(Geo g, Ws ws, uint32_t* flag) {
-    const uint32_t n_total = ws.counters[0];
-    for (uint32_t n = 1u + blockIdx.x * blockDim.x + threadIdx.x; n < 1u + n_total; n += gridDim.x * blockDim.x) {
-        if (!ws.nrep[n]) continue;
-        const uint32_t root = ws.uf[n];
-        if (ws.nanccid[root] == ws.nrootcid[root]) flag[root] = 1u;
+// root node of the cut-row pixel i (slot 0: the strip's top row, 1: its bottom row)
+__device__ __forceinline__ uint32_t cut_root(const Geo& g, const Ws& ws, int64_t i, uint32_t& val) {
+    const int32_t slot = (int32_t)(i / g.W), x = (int32_t)(i % g.W);
+    const int32_t ty = slot ? g.ty1 - 1 : g.ty0;
+    const int64_t t = (int64_t)ty * g.ntx + x / TW;
+    const uint16_t lab = ws.perim[t * PERIM + (slot ? TW : 0) + x % TW];
+    val = lab >> 15;
+    return ws.uf[1u + ws.tbase[t] + (lab & 0x7FFFu)];
+}
+
+__global__ void k_strip_mark(Geo g, Ws ws, uint32_t* flag, int top, int bot) {
+    GRID_LOOP(i, 2 * (int64_t)g.W) {
+        if ((i < g.W && !top) || (i >= g.W && !bot)) continue;
+        uint32_t val;
+        const uint32_t root = cut_root(g, ws, i, val);
+        if (root != 0) flag[root] = 1u;
     }
 }
 
-// this rank's partial post-fill sums of the border survivors, in root-node order
-__global__ void k_strip_partials(Geo g, Ws ws, const uint32_t* flag, const uint32_t* sidx, int64_t* psum,
-                                 int32_t* pmin, int32_t* pmax) {
-    const uint32_t n_total = ws.counters[0];
-    for (uint32_t n = 1u + blockIdx.x * blockDim.x + threadIdx.x; n < 1u + n_total; n += gridDim.x * blockDim.x) {
-        if (!flag[n]) continue;
-        const uint32_t k = sidx[n];
-        const Acc f = ws.filled[ws.nrootcid[n]];
-        psum[3 * k] = f.s;
-        psum[3 * k + 1] = f.sx;
-        psum[3 * k + 2] = f.sy;
-        pmin[2 * k] = f.row_min;
-        pmin[2 * k + 1] = f.col_min;
-        pmax[2 * k] = f.row_max;
-        pmax[2 * k + 1] = f.col_max;
+// cut class -> root node; components touching no cut (border roots here, interior counts from
+// the analyze pass's per-row counts): out[0] count, out[1] foreground
+__global__ void k_strip_count(Geo g, Ws ws, const uint32_t* flag, const uint32_t* rank, uint32_t* xnode,
+                              unsigned long long* out) {
+    const uint32_t n_used = min(ws.counters[0], ws.cap_nodes);
+    uint32_t cnt = 0, fg = 0;
+    GRID_LOOP(i, n_used) {
+        const uint32_t n = 1u + (uint32_t)i;
+        if (ws.uf[n] != n) continue;
+        if (flag[n]) {
+            xnode[1u + rank[n]] = n;
+        } else {
+            ++cnt;
+            fg += ws.nrec[n].fg;
+        }
+    }
+    const int64_t r0 = (int64_t)g.ty0 * TH, r1 = min((int64_t)g.ty1 * TH, (int64_t)g.H);
+    GRID_LOOP(i, (r1 - r0) * g.ntx) cnt += ws.cnt[r0 * g.ntx + i];
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    fg = __reduce_add_sync(0xFFFFFFFFu, fg);
+    if ((threadIdx.x & 31) == 0) {
+        if (cnt) atomicAdd(out, (unsigned long long)cnt);
+        if (fg) atomicAdd(out + 1, (unsigned long long)fg);
     }
 }
 
-// reduced partials + the border component's own features
-__global__ void k_strip_apply(Geo g, Ws ws, const uint32_t* flag, const uint32_t* sidx, const int64_t* psum,
-                              const int32_t* pmin, const int32_t* pmax) {
-    const uint32_t n_total = ws.counters[0];
-    for (uint32_t n = 1u + blockIdx.x * blockDim.x + threadIdx.x; n < 1u + n_total; n += gridDim.x * blockDim.x) {
-        if (!flag[n]) continue;
-        const uint32_t k = sidx[n];
-        const Acc a = ws.nacc[n];
+__global__ void k_strip_pack(Geo g, Ws ws, const uint32_t* rank, const uint32_t* xnode, int64_t ncls, uint8_t* buf,
+                             XLayout L, int top, int bot) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        XHeader h{};
+        h.n_classes = ncls;
+        h.ty0 = g.ty0;
+        h.ty1 = g.ty1;
+        *reinterpret_cast<XHeader*>(buf) = h;
+    }
+    XClass* xc = reinterpret_cast<XClass*>(buf + L.classes);
+    GRID_LOOP(c, ncls + 1) {
+        XClass x;
+        if (c == 0) {
+            x.key = ~0ull;
+            x.acc = ws.nacc[0];
+            x.fg = 0;
+        } else {
+            const uint32_t n = xnode[c];
+            x.key = ws.nmin[n];
+            x.acc = ws.nacc[n];
+            x.fg = ws.nrec[n].fg;
+        }
+        x.pad = 0;
+        xc[c] = x;
+    }
+    uint32_t* xr = reinterpret_cast<uint32_t*>(buf + L.cut);
+    GRID_LOOP(i, 2 * (int64_t)g.W) {
+        if ((i < g.W && !top) || (i >= g.W && !bot)) {
+            xr[i] = 0xFFFFFFFFu;
+            continue;
+        }
+        uint32_t val;
+        const uint32_t root = cut_root(g, ws, i, val);
+        xr[i] = (val << 31) | (root ? 1u + rank[root] : 0u);
+    }
+}
+
+// ---- merge phase: global cut classes ----------------------------------------------------------
+
+struct XSrc {
+    const uint8_t* buf;  // n_strips consecutive records
+    XLayout L;
+    int32_t k;
+};
+
+__device__ __forceinline__ int32_t strip_of(const GTab& T, int32_t k, uint32_t i) {
+    int32_t q = 0;
+    while (q + 1 < k && T.coff[q + 1] <= i) ++q;
+    return q;
+}
+
+__device__ __forceinline__ const XClass& xclass(const XSrc& X, int32_t q, uint32_t c) {
+    return reinterpret_cast<const XClass*>(X.buf + (size_t)q * X.L.bytes + X.L.classes)[c];
+}
+
+__global__ void k_g_init(GTab T, int64_t C) {
+    GRID_LOOP(i, C) {
+        T.uf[i] = (uint32_t)i;
+        T.kmin[i] = ~0ull;
+        T.tot[i] = acc_empty();
+        T.rep[i] = 0;
+        T.links[2 * i] = 0;
+        T.links[2 * i + 1] = 0;
+    }
+}
+
+// cut q: the bottom row of strip q against the top row of strip q + 1
+__global__ void k_g_cut(XSrc X, GTab T, int32_t q, int32_t W, uint32_t v8) {
+    const uint32_t* up = reinterpret_cast<const uint32_t*>(X.buf + (size_t)q * X.L.bytes + X.L.cut) + W;
+    const uint32_t* dn = reinterpret_cast<const uint32_t*>(X.buf + (size_t)(q + 1) * X.L.bytes + X.L.cut);
+    const uint32_t cu0 = T.coff[q] - 1u, cd0 = T.coff[q + 1] - 1u;
+    auto gi = [](uint32_t lab, uint32_t c0) { const uint32_t c = lab & 0x7FFFFFFFu; return c ? c0 + c : 0u; };
+    GRID_LOOP(x, W) {
+        const uint32_t lu = up[x], ld = dn[x];
+        const uint32_t vu = lu >> 31, vd = ld >> 31;
+        const uint32_t gu = gi(lu, cu0), gd = gi(ld, cd0);
+        if (vu == vd) gunion(T.uf, gu, gd);
+        if (x > 0) {
+            const uint32_t lul = up[x - 1], ldl = dn[x - 1];
+            if ((lul >> 31) == v8 && vd == v8) gunion(T.uf, gi(lul, cu0), gd);     // (r, x-1) ~ (r+1, x)
+            if (vu == v8 && (ldl >> 31) == v8) gunion(T.uf, gu, gi(ldl, cd0));     // (r, x) ~ (r+1, x-1)
+        }
+    }
+}
+
+// roots, folded features and min keys; the strips' exterior partials fold into class 0
+__global__ void k_g_fold(XSrc X, GTab T, int64_t C) {
+    GRID_LOOP(i, C) {
+        if (i == 0) {
+            T.root[0] = 0;
+            continue;
+        }
+        const uint32_t root = gfind_ro(T.uf, (uint32_t)i);
+        T.root[i] = root;
+        const int32_t q = strip_of(T, X.k, (uint32_t)i);
+        const XClass& x = xclass(X, q, (uint32_t)i - T.coff[q] + 1u);
+        acc_atomic_fold(T.tot + root, x.acc);
+        if (root) atomicMin(reinterpret_cast<unsigned long long*>(T.kmin + root), (unsigned long long)x.key);
+    }
+    GRID_LOOP(q, X.k) acc_atomic_fold(T.tot, xclass(X, (int32_t)q, 0).acc);
+}
+
+// representative class of every GCC (it holds the first pixel; its strip owns the GCC);
+// scnt[q] = GCCs owned by strip q, scnt[k + q] = foreground ones
+__global__ void k_g_reps(XSrc X, GTab T, int64_t C) {
+    GRID_LOOP(i, C) {
+        if (i == 0) continue;
+        const uint32_t root = T.root[i];
+        if (!root) continue;
+        const int32_t q = strip_of(T, X.k, (uint32_t)i);
+        const XClass& x = xclass(X, q, (uint32_t)i - T.coff[q] + 1u);
+        if (x.key != T.kmin[root]) continue;
+        T.rep[i] = 1u;
+        atomicAdd(T.scnt + q, 1u);
+        if (x.fg) atomicAdd(T.scnt + X.k + q, 1u);
+    }
+}
+
+// this strip's cut classes take their GCC's status: joined to the exterior (relinked), owned
+// (features = the GCC's total) or represented elsewhere (no representative node here, no
+// features of its own: the owner folds the total)
+__global__ void k_g_apply(Ws ws, GTab T, const uint32_t* xnode, int64_t ncls, uint32_t c0) {
+    GRID_LOOP(c, ncls + 1) {
+        if (c == 0) {
+            ws.nacc[0] = T.tot[0];
+            continue;
+        }
+        const uint32_t i = c0 + (uint32_t)c, n = xnode[c], root = T.root[i];
+        if (root == 0) {
+            ws.uf[n] = 0;
+        } else {
+            ws.ncut[n] = 1u + root;
+            if (T.rep[i]) {
+                ws.nacc[n] = T.tot[root];
+            } else {
+                ws.nacc[n] = acc_empty();
+                ws.nmin[n] = ~0ull;  // matches no key: the class has no representative here
+            }
+        }
+    }
+}
+
+__global__ void k_g_reflatten(Ws ws) {
+    const uint32_t n_used = min(ws.counters[0], ws.cap_nodes);
+    GRID_LOOP(i, n_used) {
+        const uint32_t n = 1u + (uint32_t)i, u = ws.uf[n];
+        if (u) ws.uf[n] = ws.uf[u];  // roots point at themselves or (now) at the exterior
+    }
+}
+
+// owned GCCs: canonical id and where the parent chain leaves this strip.  links[2 root] = id,
+// links[2 root + 1] = depth-1 ancestor's id (> 0) when the chain reaches the exterior inside
+// the strip, -(GCC root) when it reaches another cut class first.
+__global__ void k_g_links(Ws ws, GTab T, const uint32_t* xnode, int64_t ncls, uint32_t c0, uint32_t n_local) {
+    GRID_LOOP(c, ncls + 1) {
+        if (c == 0) continue;
+        const uint32_t i = c0 + (uint32_t)c;
+        if (!T.rep[i]) continue;
+        const uint32_t n = xnode[c], root = T.root[i];
+        int64_t link = 0;
+        uint32_t cur = n;
+        for (uint32_t it = 0; it <= n_local; ++it) {
+            const uint32_t p = ws.nparent[cur];
+            if (p == 0) {
+                link = (int64_t)ws.nrootcid[cur];
+                break;
+            }
+            if (ws.ncut[p]) {
+                link = -(int64_t)(ws.ncut[p] - 1u);
+                break;
+            }
+            cur = p;
+        }
+        if (link == 0) atomicOr(&ws.counters[1], ERR_INTERNAL);
+        T.links[2 * root] = (int64_t)ws.nrootcid[n];
+        T.links[2 * root + 1] = link;
+    }
+}
+
+// ---- resolve phase ----------------------------------------------------------------------------
+
+// every GCC's id and depth-1 ancestor (walk of the GCC links); survivors' post-fill slots start
+// empty on every rank (they collect this rank's folds)
+__global__ void k_g_anc(Ws ws, GTab T, int64_t C) {
+    uint32_t ns = 0;
+    GRID_LOOP(i, C) {
+        if (i == 0 || T.root[i] != (uint32_t)i) continue;
+        const uint32_t cid = (uint32_t)T.links[2 * i];
+        uint32_t e = (uint32_t)i, anc = 0;
+        for (int64_t it = 0; it < C; ++it) {
+            const int64_t l = T.links[2 * e + 1];
+            if (l > 0) {
+                anc = (uint32_t)l;
+                break;
+            }
+            if (l == 0) break;
+            e = (uint32_t)(-l);
+        }
+        if (!anc || !cid) atomicOr(&ws.counters[1], ERR_INTERNAL);
+        T.cid[i] = cid;
+        T.anc[i] = anc;
+        if (anc == cid && cid) {
+            ws.filled[cid] = acc_empty();
+            ++ns;
+        }
+    }
+    ns = __reduce_add_sync(0xFFFFFFFFu, ns);
+    if ((threadIdx.x & 31) == 0 && ns) atomicAdd(T.gsurv, ns);
+}
+
+__global__ void k_g_own(Ws ws, GTab T, const uint32_t* xnode, int64_t ncls, uint32_t c0) {
+    GRID_LOOP(c, ncls + 1) {
+        if (c == 0) continue;
+        const uint32_t root = T.root[c0 + (uint32_t)c];
+        if (!root) continue;
+        const uint32_t n = xnode[c];
+        ws.nrootcid[n] = T.cid[root];
+        ws.nanccid[n] = T.anc[root];
+    }
+}
+
+// this rank's partial post-fill sums of the GCC survivors (neutral elsewhere), indexed by GCC root
+__global__ void k_g_partials(Ws ws, GTab T, int64_t C, const uint32_t* surv_a, const uint32_t* surv_b, int32_t sub) {
+    GRID_LOOP(i, C) {
+        Acc f = acc_empty();
+        if (i > 0 && T.root[i] == (uint32_t)i && T.anc[i] == T.cid[i]) f = ws.filled[T.cid[i]];
+        T.psum[3 * i] = f.s;
+        T.psum[3 * i + 1] = f.sx;
+        T.psum[3 * i + 2] = f.sy;
+        T.pmin[2 * i] = f.row_min;
+        T.pmin[2 * i + 1] = f.col_min;
+        T.pmax[2 * i] = f.row_max;
+        T.pmax[2 * i + 1] = f.col_max;
+    }
+    // survivors that touch no cut (interior + border; the exterior counted on strip 0 only)
+    if (blockIdx.x == 0 && threadIdx.x == 0) *T.pcnt = (int64_t)*surv_a + (int64_t)*surv_b - sub;
+}
+
+__global__ void k_g_finish(Ws ws, GTab T, int64_t C) {
+    GRID_LOOP(i, C) {
+        if (i == 0 || T.root[i] != (uint32_t)i || T.anc[i] != T.cid[i]) continue;
+        const Acc a = T.tot[i];
         Acc f;
-        f.s = psum[3 * k] + a.s;
-        f.sx = psum[3 * k + 1] + a.sx;
-        f.sy = psum[3 * k + 2] + a.sy;
-        f.row_min = min(pmin[2 * k], a.row_min);
-        f.col_min = min(pmin[2 * k + 1], a.col_min);
-        f.row_max = max(pmax[2 * k], a.row_max);
-        f.col_max = max(pmax[2 * k + 1], a.col_max);
-        ws.filled[ws.nrootcid[n]] = f;
+        f.s = T.psum[3 * i] + a.s;
+        f.sx = T.psum[3 * i + 1] + a.sx;
+        f.sy = T.psum[3 * i + 2] + a.sy;
+        f.row_min = min(T.pmin[2 * i], a.row_min);
+        f.col_min = min(T.pmin[2 * i + 1], a.col_min);
+        f.row_max = max(T.pmax[2 * i], a.row_max);
+        f.col_max = max(T.pmax[2 * i + 1], a.col_max);
+        ws.filled[T.cid[i]] = f;
     }
 }
-
-__global__ void k_strip_summary(Geo g, Ws ws, int64_t* out, int32_t r0, int32_t r1, int32_t first) {
-    // [0] total components, [1] fg, [2] survivors, [3] owned lo, [4] owned hi, [5] error bits
-    const int64_t rows = (int64_t)g.H * g.ntx;
-    out[0] = (int64_t)ws.off[rows] + 1;
-    out[1] = ws.img_fg[0];
-    out[2] = ws.img_surv[0];
-    out[3] = first ? 0 : 1 + (int64_t)ws.off[(int64_t)r0 * g.ntx];
-    out[4] = 1 + (int64_t)ws.off[(int64_t)r1 * g.ntx];
-    out[5] = ws.counters[1];
-}
-
-__global__ void k_copy_count(const uint32_t* src, int64_t* dst) { *dst = (int64_t)*src; }
 
 int grid(int64_t n, int sms) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8)); }
 
@@ -247,12 +465,14 @@ struct StripState {
     Geo g{};
     rl_config cfg{};
     int32_t y0 = 0, h = 0;
-    int64_t n_local = 0, interior_fg = 0;
+    int32_t rank = -1, n_strips = 0;
     const uint8_t* pix = nullptr;
+    int64_t n_local = 0, n_classes = 0, n_comps = 0, n_fg = 0;
     // global phase
-    int64_t n_total = 0, k_surv = 0;
-    int64_t summary[6] = {};
-    bool merged = false;
+    int64_t C = 0;          // global class slots (1 + all strips' cut classes)
+    int64_t total = 0, fg = 0, comp_lo = 0, comp_hi = 0;
+    uint32_t c0 = 0;        // this strip's classes are global slots c0 + 1 .. c0 + n_classes
+    int phase = 0;          // 1 local, 2 exported, 3 merged, 4 resolved
 };
 
 }  // namespace rlh
@@ -269,6 +489,11 @@ int sync_err(rl_ctx* c, const char* what) {
     return e == cudaSuccess ? RL_OK : cuda_fail(c, e, what);
 }
 
+GTab gtab(rl_ctx* ctx) {
+    const StripState* S = ctx->strip;
+    return g_layout(ctx->gtab.p, S->C, S->n_strips);
+}
+
 }  // namespace
 
 namespace rlh {
@@ -280,8 +505,8 @@ void strip_free(rl_ctx* c) {
 
 extern "C" {
 
-int64_t rl_strip_export_bytes(int32_t w, int64_t max_nodes, int32_t max_tile_rows) {
-    return (int64_t)x_layout(w, max_nodes, max_tile_rows).bytes;
+int64_t rl_strip_export_bytes(int32_t w, int64_t max_classes) {
+    return (int64_t)x_layout(w, max_classes).bytes;
 }
 
 int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, int32_t y0, int32_t h,
@@ -305,21 +530,29 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
     S->y0 = y0;
     S->h = h;
     S->pix = d_strip;
-    S->merged = false;
+    S->phase = 0;
     ctx->want_compact = false;
     cudaStream_t s = ctx->stream;
+    const int top = g.ty0 > 0, bot = g.ty1 < g.nty;
     for (int attempt = 0; attempt < 4; ++attempt) {
         Ws ws;
         size_t tmp = 0;
         if ((rc = prepare_ws(ctx, g, cfg, ws, tmp, (int64_t)h * w))) return rc;
-        if (!ensure(ctx->nleft, ((size_t)ctx->cap_nodes + 1) * 4)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+        const size_t nn = (size_t)ctx->cap_nodes + 1;
+        if (!ensure(ctx->nleft, nn * 4) || !ensure(ctx->ncut, nn * 4) || !ensure(ctx->flag, nn * 4) ||
+            !ensure(ctx->rank, nn * 4) || !ensure(ctx->xnode, nn * 4) || !ensure(ctx->scount, 64))
+            return set_err(ctx, RL_ENOMEM, "device allocation failed");
+        size_t tmp3 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nn);
+        if (!ensure(ctx->cub_tmp, std::max(tmp, tmp3))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
         ws.nleft = P<uint32_t>(ctx->nleft);
+        ws.ncut = P<uint32_t>(ctx->ncut);
         const int64_t ncnt = (int64_t)H * g.ntx + 1;
         cudaMemsetAsync(ws.counters, 0, 64, s);
         cudaMemsetAsync(ws.rused, 0, 8, s);
         cudaMemsetAsync(ws.img_fg, 0, 4, s);
-        cudaMemsetAsync(ws.uf, 0, 4, s);  // the exterior node (strip 0's first tile also sets it)
-        cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
+        cudaMemsetAsync(ws.tnb, 0, (size_t)g.ntiles * 4, s);  // tiles of other strips: no nodes here
+        cudaMemsetAsync(ws.cnt, 0, (size_t)ncnt * 4, s);     // rows of other strips: counted elsewhere
         launch_analyze(d_strip, g, ws, s);
         launch_seams(g, ws, s, ctx->sms);
         k_strip_left<<<grid((int64_t)ctx->cap_nodes, ctx->sms), 256, 0, s>>>(g, ws);
@@ -331,18 +564,44 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         unsigned long long rused = 0;
         cudaMemcpyAsync(&rused, ws.rused, 8, cudaMemcpyDeviceToHost, s);
         if ((rc = sync_err(ctx, "strip local"))) return rc;
-        ctx->ws = ws;
-        ctx->geo = g;
         if (hc[1] & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip left link)");
         if (hc[1] & (ERR_NODE_CAP | ERR_RSTORE_CAP)) {
             if (hc[1] & ERR_NODE_CAP) ctx->cap_nodes = (uint32_t)std::min<uint64_t>(hc[0] + hc[0] / 4 + 1024, 0xF0000000ull);
             if (hc[1] & ERR_RSTORE_CAP) ctx->cap_rstore = rused + rused / 8 + 4096;
             continue;
         }
-        S->n_local = hc[0];
-        S->interior_fg = fg;
-        out->n_nodes = hc[0];
-        out->interior_fg = fg;
+        const int64_t n_local = hc[0];
+        // flatten inside the strip; cut classes = roots seen on a cut row, numbered by a scan
+        k_strip_exterior<<<1, 1, 0, s>>>(ws);
+        launch_resolve(g, ws, s, ctx->sms, n_local);
+        uint32_t* flag = P<uint32_t>(ctx->flag);
+        uint32_t* rank = P<uint32_t>(ctx->rank);
+        cudaMemsetAsync(flag, 0, (size_t)(n_local + 1) * 4, s);
+        cudaMemsetAsync(ws.ncut, 0, (size_t)(n_local + 1) * 4, s);
+        k_strip_mark<<<grid(2 * (int64_t)w, ctx->sms), 256, 0, s>>>(g, ws, flag, top, bot);
+        size_t t3 = ctx->cub_tmp.bytes;
+        cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t3, flag, rank, (int)(n_local + 1), s);
+        unsigned long long* cnt2 = P<unsigned long long>(ctx->scount);
+        cudaMemsetAsync(cnt2, 0, 16, s);
+        k_strip_count<<<grid(std::max<int64_t>(n_local, (int64_t)(g.ty1 - g.ty0) * TH * g.ntx), ctx->sms), 256, 0, s>>>(
+            g, ws, flag, rank, P<uint32_t>(ctx->xnode), cnt2);
+        uint32_t klast[2] = {};
+        unsigned long long hcnt[2] = {};
+        cudaMemcpyAsync(&klast[0], rank + n_local, 4, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&klast[1], flag + n_local, 4, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(hcnt, cnt2, 16, cudaMemcpyDeviceToHost, s);
+        if ((rc = sync_err(ctx, "strip local classes"))) return rc;
+        ctx->launches += 6;
+        ctx->ws = ws;
+        ctx->geo = g;
+        S->n_local = n_local;
+        S->n_classes = (int64_t)klast[0] + klast[1];
+        S->n_comps = (int64_t)hcnt[0];
+        S->n_fg = (int64_t)hcnt[1] + fg;
+        S->phase = 1;
+        out->n_classes = S->n_classes;
+        out->n_comps = S->n_comps;
+        out->n_fg = S->n_fg;
         out->ty0 = g.ty0;
         out->ty1 = g.ty1;
         out->status = 0;
@@ -352,159 +611,169 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
     return set_err(ctx, RL_EINTERNAL, "capacity did not converge");
 }
 
-int rl_strip_export(rl_ctx* ctx, int64_t max_nodes, int32_t max_tile_rows, void* d_buf) {
+int rl_strip_export(rl_ctx* ctx, int64_t max_classes, void* d_buf) {
     if (!ctx || !d_buf) return RL_EINVAL;
     StripState* S = ctx->strip;
-    if (!S || !S->g.strip) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_local first");
-    if (S->n_local > max_nodes || S->g.ty1 - S->g.ty0 > max_tile_rows)
-        return set_err(ctx, RL_EINVAL, "strips: export record too small");
+    if (!S || S->phase < 1) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_local first");
+    if (S->n_classes > max_classes) return set_err(ctx, RL_EINVAL, "strips: export record too small");
     cudaSetDevice(ctx->device);
-    const XLayout L = x_layout(S->g.W, max_nodes, max_tile_rows);
-    k_strip_pack<<<grid(std::max<int64_t>(max_nodes, (int64_t)S->g.ntx * 2 * TW), ctx->sms), 256, 0, ctx->stream>>>(
-        S->g, ctx->ws, static_cast<uint8_t*>(d_buf), L);
+    const Geo& g = S->g;
+    const XLayout L = x_layout(g.W, max_classes);
+    k_strip_pack<<<grid(std::max<int64_t>(S->n_classes + 1, 2 * (int64_t)g.W), ctx->sms), 256, 0, ctx->stream>>>(
+        g, ctx->ws, P<uint32_t>(ctx->rank), P<uint32_t>(ctx->xnode), S->n_classes, static_cast<uint8_t*>(d_buf), L,
+        g.ty0 > 0, g.ty1 < g.nty);
     ctx->launches += 1;
+    S->phase = 2;
     return sync_err(ctx, "strip export");
 }
 
 int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const rl_strip_local_info* infos,
-                   int64_t max_nodes, int32_t max_tile_rows, rl_strip_partials* out) {
+                   int64_t max_classes, rl_strip_links* out) {
     if (!ctx || !d_gathered || !infos || !out || n_strips < 1) return RL_EINVAL;
     StripState* S = ctx->strip;
-    if (!S || !S->g.strip) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_local first");
+    if (!S || S->phase < 2) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_export first");
     cudaSetDevice(ctx->device);
-    const XLayout L = x_layout(S->g.W, max_nodes, max_tile_rows);
-    int64_t n_total = 0, fg_int = 0;
-    std::vector<uint32_t> offs(n_strips);
-    for (int q = 0; q < n_strips; ++q) {
-        offs[q] = (uint32_t)n_total;
-        n_total += infos[q].n_nodes;
-        fg_int += infos[q].interior_fg;
-        if (infos[q].n_nodes > max_nodes) return set_err(ctx, RL_EINVAL, "strips: inconsistent node counts");
-    }
-    if (n_total + 1 >= 0xF0000000ll) return set_err(ctx, RL_EINVAL, "strips: too many border components");
     Geo g = S->g;
-    const rl_config* cfg = &S->cfg;
     cudaStream_t s = ctx->stream;
-    if (ctx->cap_nodes < (uint64_t)n_total + 1) ctx->cap_nodes = (uint32_t)(n_total + n_total / 8 + 1024);
-    for (int attempt = 0; attempt < 4; ++attempt) {
-        Ws ws;
-        size_t tmp = 0;
-        int rc = prepare_ws(ctx, g, cfg, ws, tmp, (int64_t)S->h * g.W);
-        if (rc) return rc;
-        const size_t nn = (size_t)ctx->cap_nodes + 1;
-        if (!ensure(ctx->nleft, nn * 4) || !ensure(ctx->flag, nn * 4) || !ensure(ctx->rank, nn * 4))
-            return set_err(ctx, RL_ENOMEM, "device allocation failed");
-        size_t tmp3 = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(n_total + 1));
-        if (!ensure(ctx->cub_tmp, std::max(tmp, tmp3))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
-        ws.nleft = P<uint32_t>(ctx->nleft);
-        const int64_t ncnt = (int64_t)g.H * g.ntx + 1;
-        // ---- import every strip's record into one global numbering
-        const uint8_t* gb = static_cast<const uint8_t*>(d_gathered);
-        for (int q = 0; q < n_strips; ++q)
-            k_strip_unpack<<<grid(std::max<int64_t>(max_nodes, (int64_t)g.ntx * 2 * TW), ctx->sms), 256, 0, s>>>(
-                g, ws, gb + (size_t)q * L.bytes, L, offs[q]);
-        k_strip_exterior<<<1, 1, 0, s>>>(ws, (uint32_t)n_total);
-        const uint32_t fg32 = (uint32_t)fg_int;
-        cudaMemcpyAsync(ws.img_fg, &fg32, 4, cudaMemcpyHostToDevice, s);
-        cudaMemsetAsync(ws.img_surv, 0, 4, s);
-        cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
-        // ---- union across the cuts, then the merge passes over all border components
-        for (int q = 0; q + 1 < n_strips; ++q) launch_seam_rows(g, ws, infos[q].ty1 - 1, 1, s, ctx->sms);
-        Geo gm = g;  // merge kernels: whole image
-        gm.ty0 = 0;
-        gm.ty1 = g.nty;
-        launch_resolve(gm, ws, s, ctx->sms, n_total);
-        launch_reps(gm, ws, s, ctx->sms, n_total);
-        cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ws.cnt, ws.off, (int)ncnt, s);
-        launch_cids(gm, ws, s, ctx->sms);
-        launch_tree_parts(gm, ws, s, ctx->sms, n_total);  // post-fill roots (no fold yet)
-        // ---- emit this strip's tiles; interior survivors are counted into a private counter
-        Ws we = ws;
-        if (!ensure(ctx->scount, 64)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
-        we.img_surv = P<uint32_t>(ctx->scount);
-        cudaMemsetAsync(we.img_surv, 0, 4, s);
-        launch_emit(g, we, s);
-        // ---- border survivors: flags, index, this rank's partial sums
-        uint32_t* flag = P<uint32_t>(ctx->flag);
-        cudaMemsetAsync(flag, 0, (size_t)(n_total + 1) * 4, s);
-        k_strip_surv_flags<<<grid(n_total, ctx->sms), 256, 0, s>>>(gm, ws, flag);
-        size_t t3 = ctx->cub_tmp.bytes;
-        cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t3, flag, P<uint32_t>(ctx->rank), (int)(n_total + 1), s);
-        int64_t hs[6] = {};
-        uint32_t klast[2] = {};
-        cudaMemcpyAsync(&klast[0], P<uint32_t>(ctx->rank) + n_total, 4, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(&klast[1], flag + n_total, 4, cudaMemcpyDeviceToHost, s);
-        if (!ensure(ctx->summ, 64)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
-        const int32_t r1 = std::min(g.ty1 * TH, g.H);
-        k_strip_summary<<<1, 1, 0, s>>>(g, ws, P<int64_t>(ctx->summ), g.ty0 * TH, r1, g.ty0 == 0 ? 1 : 0);
-        cudaMemcpyAsync(hs, ctx->summ.p, 48, cudaMemcpyDeviceToHost, s);
-        if ((rc = sync_err(ctx, "strip merge"))) return rc;
-        if (hs[5] & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (tree reference)");
-        if ((uint64_t)hs[0] > ctx->cap_comps) {  // identical on every rank: all grow and re-run
-            ctx->cap_comps = (uint64_t)hs[0] + (uint64_t)hs[0] / 8 + 1024;
-            continue;
-        }
-        const int64_t K = (int64_t)klast[0] + klast[1];
-        S->k_surv = K;
-        S->n_total = n_total;
-        std::memcpy(S->summary, hs, sizeof(hs));
-        if (!ensure(ctx->fcomp, (size_t)std::max<int64_t>(K, 1) * 40 + 8)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
-        int64_t* psum = P<int64_t>(ctx->fcomp);
-        int32_t* pmin = reinterpret_cast<int32_t*>(psum + 3 * K);
-        int32_t* pmax = pmin + 2 * K;
-        int64_t* pcnt = reinterpret_cast<int64_t*>(P<uint8_t>(ctx->fcomp) + (size_t)K * 40);
-        k_strip_partials<<<grid(n_total, ctx->sms), 256, 0, s>>>(gm, ws, flag, P<uint32_t>(ctx->rank), psum, pmin, pmax);
-        // interior survivors of this strip as an int64 for the reduction
-        k_copy_count<<<1, 1, 0, s>>>(we.img_surv, pcnt);
-        if ((rc = sync_err(ctx, "strip partials"))) return rc;
-        ctx->ws = ws;
-        ctx->geo = g;
-        out->k = K;
-        out->d_sum = psum;
-        out->d_min = pmin;
-        out->d_max = pmax;
-        out->d_count = pcnt;
-        S->merged = true;
-        // unpack x n, exterior, cut seams, resolve, reps, scan x 2, cids, parents, tops, emit x 3,
-        // flags, scan x 2, summary, partials, count
-        ctx->launches += n_strips + 1 + (n_strips - 1) + 15;
-        return RL_OK;
+    // this strip's position among the records: strips are given in image order
+    int me = -1;
+    int64_t C = 1;
+    std::vector<uint32_t> coff(n_strips + 1);
+    for (int q = 0; q < n_strips; ++q) {
+        if (infos[q].n_classes > max_classes || infos[q].n_classes < 0)
+            return set_err(ctx, RL_EINVAL, "strips: inconsistent class counts");
+        if (q > 0 && infos[q].ty0 != infos[q - 1].ty1) return set_err(ctx, RL_EINVAL, "strips: records not in image order");
+        if (infos[q].ty0 == g.ty0) me = q;
+        coff[q] = (uint32_t)C;
+        C += infos[q].n_classes;
     }
-    return set_err(ctx, RL_EINTERNAL, "capacity did not converge");
+    coff[n_strips] = (uint32_t)C;
+    if (me < 0 || infos[me].n_classes != S->n_classes) return set_err(ctx, RL_EINVAL, "strips: this strip is not among the records");
+    if (infos[0].ty0 != 0 || infos[n_strips - 1].ty1 != g.nty) return set_err(ctx, RL_EINVAL, "strips: records do not cover the image");
+    if (C >= 0x7FFFFFFFll) return set_err(ctx, RL_EINVAL, "strips: too many cut classes");
+    S->rank = me;
+    S->n_strips = n_strips;
+    S->C = C;
+    S->c0 = coff[me] - 1u;
+    if (!ensure(ctx->gtab, g_layout(nullptr, C, n_strips).bytes)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    GTab T = gtab(ctx);
+    const XSrc X{static_cast<const uint8_t*>(d_gathered), x_layout(g.W, max_classes), n_strips};
+    cudaMemcpyAsync(T.coff, coff.data(), (n_strips + 1) * 4, cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(T.scnt, 0, (size_t)2 * n_strips * 4, s);
+    cudaMemsetAsync(T.gsurv, 0, 4, s);
+    // ---- global cut classes (identical on every rank)
+    k_g_init<<<grid(C, ctx->sms), 256, 0, s>>>(T, C);
+    const uint32_t v8 = g.flip ? 0u : 1u;
+    for (int q = 0; q + 1 < n_strips; ++q) k_g_cut<<<grid(g.W, ctx->sms), 256, 0, s>>>(X, T, q, g.W, v8);
+    k_g_fold<<<grid(C, ctx->sms), 256, 0, s>>>(X, T, C);
+    k_g_reps<<<grid(C, ctx->sms), 256, 0, s>>>(X, T, C);
+    std::vector<uint32_t> sc(2 * n_strips);
+    cudaMemcpyAsync(sc.data(), T.scnt, sc.size() * 4, cudaMemcpyDeviceToHost, s);
+    int rc = sync_err(ctx, "strip cut merge");
+    if (rc) return rc;
+    int64_t total = 1, fg = 0, off_me = 0;
+    for (int q = 0; q < n_strips; ++q) {
+        if (q == me) off_me = total - 1;
+        total += infos[q].n_comps + sc[q];
+        fg += infos[q].n_fg + sc[n_strips + q];
+    }
+    if (total >= 0xFFFFFFFFll) return set_err(ctx, RL_EINVAL, "strips: too many components");
+    S->total = total;
+    S->fg = fg;
+    S->comp_lo = me == 0 ? 0 : 1 + off_me;
+    S->comp_hi = 1 + off_me + infos[me].n_comps + sc[me];
+    // ---- this strip's numbering with the GCC status applied (ids index the whole image)
+    if (ctx->cap_comps < (uint64_t)total) ctx->cap_comps = (uint64_t)total + (uint64_t)total / 8 + 1024;
+    Ws ws;
+    size_t tmp = 0;
+    if ((rc = prepare_ws(ctx, g, &S->cfg, ws, tmp, (int64_t)S->h * g.W))) return rc;
+    ws.nleft = P<uint32_t>(ctx->nleft);
+    ws.ncut = P<uint32_t>(ctx->ncut);
+    const uint32_t* xnode = P<uint32_t>(ctx->xnode);
+    k_g_apply<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0);
+    k_g_reflatten<<<grid(S->n_local, ctx->sms), 256, 0, s>>>(ws);
+    const int64_t ncnt = (int64_t)g.H * g.ntx + 1;
+    if (me > 0) {
+        const uint32_t before = (uint32_t)off_me;  // components of the strips above
+        cudaMemcpyAsync(ws.cnt, &before, 4, cudaMemcpyHostToDevice, s);
+    }
+    cudaMemsetAsync(ws.img_surv, 0, 4, s);
+    launch_reps(g, ws, s, ctx->sms, S->n_local);
+    cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ws.cnt, ws.off, (int)ncnt, s);
+    launch_cids(g, ws, s, ctx->sms);
+    k_g_links<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0,
+                                                                 (uint32_t)S->n_local);
+    uint32_t err = 0;
+    cudaMemcpyAsync(&err, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
+    if ((rc = sync_err(ctx, "strip merge"))) return rc;
+    if (err & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip links)");
+    ctx->ws = ws;
+    ctx->geo = g;
+    ctx->launches += 4 + (n_strips - 1) + 7;
+    out->d_links = T.links;
+    out->n = 2 * C;
+    S->phase = 3;
+    return RL_OK;
+}
+
+int rl_strip_resolve(rl_ctx* ctx, rl_strip_partials* out) {
+    if (!ctx || !out) return RL_EINVAL;
+    StripState* S = ctx->strip;
+    if (!S || S->phase < 3) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_merge first");
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    Ws ws = ctx->ws;
+    const Geo& g = S->g;
+    GTab T = gtab(ctx);
+    const int64_t C = S->C;
+    k_g_anc<<<grid(C, ctx->sms), 256, 0, s>>>(ws, T, C);
+    k_g_own<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, P<uint32_t>(ctx->xnode), S->n_classes, S->c0);
+    launch_tree_parts(g, ws, s, ctx->sms, S->n_local);  // post-fill roots (no fold yet)
+    // emit this strip's tiles; interior survivors are counted into a private counter
+    Ws we = ws;
+    uint32_t* isurv = P<uint32_t>(ctx->scount) + 4;
+    we.img_surv = isurv;
+    cudaMemsetAsync(isurv, 0, 4, s);
+    launch_emit(g, we, s);
+    launch_fold(g, ws, s, ctx->sms, S->n_local);  // border non-survivors of this strip
+    k_g_partials<<<grid(C, ctx->sms), 256, 0, s>>>(ws, T, C, ws.img_surv, isurv, S->rank > 0 ? 1 : 0);
+    uint32_t err = 0;
+    cudaMemcpyAsync(&err, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
+    const int rc = sync_err(ctx, "strip resolve");
+    if (rc) return rc;
+    if (err & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip tree)");
+    ctx->launches += 2 + 1 + 3 + 1 + 1;
+    out->d_sum = T.psum;
+    out->d_min = T.pmin;
+    out->d_max = T.pmax;
+    out->d_count = T.pcnt;
+    out->k = C;
+    S->phase = 4;
+    return RL_OK;
 }
 
 int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out) {
     if (!ctx || !out) return RL_EINVAL;
     StripState* S = ctx->strip;
-    if (!S || !S->merged) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_merge first");
+    if (!S || S->phase < 4) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_resolve first");
     cudaSetDevice(ctx->device);
     cudaStream_t s = ctx->stream;
-    Ws ws = ctx->ws;
-    Geo gm = S->g;
-    gm.ty0 = 0;
-    gm.ty1 = gm.nty;
-    const int64_t K = S->k_surv;
-    int64_t* psum = P<int64_t>(ctx->fcomp);
-    int32_t* pmin = reinterpret_cast<int32_t*>(psum + 3 * K);
-    int32_t* pmax = pmin + 2 * K;
-    int64_t* pcnt = reinterpret_cast<int64_t*>(P<uint8_t>(ctx->fcomp) + (size_t)K * 40);
-    k_strip_apply<<<grid(S->n_total, ctx->sms), 256, 0, s>>>(gm, ws, P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank),
-                                                             psum, pmin, pmax);
-    launch_fold(gm, ws, s, ctx->sms, S->n_total);
-    ctx->launches += 2;
-    int64_t surv_int = 0;
-    cudaMemcpyAsync(&surv_int, pcnt, 8, cudaMemcpyDeviceToHost, s);
+    GTab T = gtab(ctx);
+    k_g_finish<<<grid(S->C, ctx->sms), 256, 0, s>>>(ctx->ws, T, S->C);
+    ctx->launches += 1;
+    int64_t surv = 0;
+    uint32_t gsurv = 0;
+    cudaMemcpyAsync(&surv, T.pcnt, 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&gsurv, T.gsurv, 4, cudaMemcpyDeviceToHost, s);
     const int rc = sync_err(ctx, "strip finish");
     if (rc) return rc;
-    const int64_t* hs = S->summary;
-    out->n_components = hs[0];
-    out->n_fg = hs[1];
-    out->n_holes = hs[0] - 1 - hs[1];
-    out->euler = hs[1] - out->n_holes;
-    out->n_survivors = hs[2] + surv_int;
-    out->comp_lo = hs[3];
-    out->comp_hi = hs[4];
+    out->n_components = S->total;
+    out->n_fg = S->fg;
+    out->n_holes = S->total - 1 - S->fg;
+    out->euler = S->fg - out->n_holes;
+    out->n_survivors = surv + gsurv;
+    out->comp_lo = S->comp_lo;
+    out->comp_hi = S->comp_hi;
     out->y0 = S->y0;
     out->h = S->h;
     return RL_OK;
@@ -513,7 +782,7 @@ int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out) {
 int rl_strip_fetch(rl_ctx* ctx, const rl_strip_result* r, rl_host_outputs* out) {
     if (!ctx || !r || !out) return RL_EINVAL;
     StripState* S = ctx->strip;
-    if (!S || !S->merged) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_finish first");
+    if (!S || S->phase < 4) return set_err(ctx, RL_ELOGIC, "strips: rl_strip_finish first");
     cudaSetDevice(ctx->device);
     cudaStream_t s = ctx->stream;
     const size_t npx = (size_t)S->h * S->g.W;

@@ -1,13 +1,17 @@
 """One image across ranks as horizontal strips, over the C ABI's strip phases.
 
-Each rank holds its strip of rows in device memory.  The phases (include/runlab_gpu.h) are
-separated by three collectives, which this module does with torch.distributed (NCCL over
-NVLink between GPUs; any backend whose tensors live where the buffers live):
+Each rank holds its strip of rows in device memory.  Only O(width) data crosses ranks: the
+strip's components that touch a cut row ("cut classes": first-pixel key, features, foreground
+flag) and the two cut rows' class labels.  The phases (include/runlab_gpu.h) are separated by
+four collectives, which this module does with torch.distributed (NCCL over NVLink between GPUs;
+any backend whose tensors live where the buffers live):
 
-1. all-gather of the per-strip counts (border components, interior foreground components);
-2. all-gather of the strips' exchange records (border-component tables, cut-row perimeter
-   labels, per-row counts) -- one equal-size record per rank;
-3. all-reduce (SUM / MIN / MAX) of the border survivors' partial post-fill features.
+1. all-gather of the per-strip counts (cut classes, components touching no cut, foreground);
+2. all-gather of the strips' exchange records (one equal-size record per rank);
+3. all-reduce SUM of the link table (canonical id and parent-chain exit of every cut component,
+   filled in by the strip that owns it);
+4. all-reduce (SUM / MIN / MAX) of the partial post-fill features of the survivors that cross a
+   cut.
 
 ``label_strip`` is the per-rank entry point.  ``label_strips_in_process`` runs all strips of an
 image in one process on one device, phase by phase in lockstep, with the collectives done by
@@ -99,26 +103,31 @@ class StripPhases:
         self._check(self.L.rl_strip_local(self.ctx, C.c_void_p(d_ptr), W, H, y0, h, C.byref(cfg.to_c()),
                                           C.byref(info)))
         self.info = info
-        return np.array([info.n_nodes, info.interior_fg, info.ty0, info.ty1], dtype=np.int64)
+        return np.array([info.n_classes, info.n_comps, info.n_fg, info.ty0, info.ty1], dtype=np.int64)
 
-    def export_bytes(self, max_nodes: int, max_rows: int) -> int:
-        return int(self.L.rl_strip_export_bytes(self.W, max_nodes, max_rows))
+    def export_bytes(self, max_classes: int) -> int:
+        return int(self.L.rl_strip_export_bytes(self.W, max_classes))
 
-    def export(self, max_nodes: int, max_rows: int):
+    def export(self, max_classes: int):
         import torch
-        buf = torch.empty(self.export_bytes(max_nodes, max_rows), dtype=torch.uint8, device="cuda")
-        self._check(self.L.rl_strip_export(self.ctx, max_nodes, max_rows, C.c_void_p(buf.data_ptr())))
+        buf = torch.empty(self.export_bytes(max_classes), dtype=torch.uint8, device="cuda")
+        self._check(self.L.rl_strip_export(self.ctx, max_classes, C.c_void_p(buf.data_ptr())))
         return buf
 
-    def merge(self, gathered, infos: np.ndarray, max_nodes: int, max_rows: int):
+    def merge(self, gathered, infos: np.ndarray, max_classes: int):
         n = infos.shape[0]
         arr = (N.RlStripLocalInfo * n)()
         for q in range(n):
-            arr[q].n_nodes, arr[q].interior_fg = int(infos[q, 0]), int(infos[q, 1])
-            arr[q].ty0, arr[q].ty1 = int(infos[q, 2]), int(infos[q, 3])
+            arr[q].n_classes, arr[q].n_comps, arr[q].n_fg = (int(v) for v in infos[q, :3])
+            arr[q].ty0, arr[q].ty1 = int(infos[q, 3]), int(infos[q, 4])
+        lk = N.RlStripLinks()
+        self._check(self.L.rl_strip_merge(self.ctx, C.c_void_p(gathered.data_ptr()), n, arr, max_classes,
+                                          C.byref(lk)))
+        return _view(lk.d_links, int(lk.n), "<i8")
+
+    def resolve(self):
         p = N.RlStripPartials()
-        self._check(self.L.rl_strip_merge(self.ctx, C.c_void_p(gathered.data_ptr()), n, arr, max_nodes, max_rows,
-                                          C.byref(p)))
+        self._check(self.L.rl_strip_resolve(self.ctx, C.byref(p)))
         k = int(p.k)
         return (_view(p.d_sum, 3 * k, "<i8"), _view(p.d_min, 2 * k, "<i4"), _view(p.d_max, 2 * k, "<i4"),
                 _view(p.d_count, 1, "<i8"))
@@ -155,12 +164,12 @@ class StripPhases:
                            None if labels is None else labels.numpy()[: npx * 4].view(np.uint32).reshape(int(r.h), self.W))
 
 
-def _maxima(infos: np.ndarray) -> tuple[int, int]:
-    return int(infos[:, 0].max()), int((infos[:, 3] - infos[:, 2]).max())
+def _max_classes(infos: np.ndarray) -> int:
+    return int(infos[:, 0].max())
 
 
 class TorchCollectives:
-    """The three strip collectives over a torch.distributed process group."""
+    """The four strip collectives over a torch.distributed process group."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -176,17 +185,32 @@ class TorchCollectives:
         self.dist.all_gather_into_tensor(out, t, group=self.group)
         return out.cpu().numpy().reshape(self.world, -1)
 
+    @staticmethod
+    def _done(t):
+        """The strip phases run on the library's own stream: the collective's result must be in
+        memory before the next phase is enqueued."""
+        import torch
+        if t.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+
     def gather_records(self, rec):
         import torch
         out = torch.empty(self.world * rec.numel(), dtype=rec.dtype, device=rec.device)
         self.dist.all_gather_into_tensor(out, rec, group=self.group)
+        self._done(out)
         return out
+
+    def reduce_links(self, links):
+        if links.numel():
+            self.dist.all_reduce(links, op=self.dist.ReduceOp.SUM, group=self.group)
+            self._done(links)
 
     def reduce_partials(self, psum, pmin, pmax, pcnt):
         R = self.dist.ReduceOp
         for t, op in ((psum, R.SUM), (pmin, R.MIN), (pmax, R.MAX), (pcnt, R.SUM)):
             if t.numel():
                 self.dist.all_reduce(t, op=op, group=self.group)
+        self._done(pcnt)
 
 
 _PHASES: dict[int, StripPhases] = {}
@@ -200,9 +224,10 @@ def label_strip(labeler, d_strip_ptr: int, W: int, H: int, y0: int, h: int, conf
     if ph is None or ph.lab is not labeler:
         ph = _PHASES[id(labeler)] = StripPhases(labeler)
     infos = coll.gather_infos(ph.local(d_strip_ptr, W, H, y0, h, config), "cuda")
-    mn, mr = _maxima(infos)
-    gathered = coll.gather_records(ph.export(mn, mr))
-    psum, pmin, pmax, pcnt = ph.merge(gathered, infos, mn, mr)
+    mc = _max_classes(infos)
+    gathered = coll.gather_records(ph.export(mc))
+    coll.reduce_links(ph.merge(gathered, infos, mc))
+    psum, pmin, pmax, pcnt = ph.resolve()
     coll.reduce_partials(psum, pmin, pmax, pcnt)
     r = ph.finish()
     if not fetch:
@@ -216,9 +241,15 @@ def label_strips_in_process(labelers, d_strip_ptrs, W: int, H: int, rows, config
     import torch
     phs = [StripPhases(lab) for lab in labelers]
     infos = np.stack([ph.local(p, W, H, y0, h, config) for ph, p, (y0, h) in zip(phs, d_strip_ptrs, rows)])
-    mn, mr = _maxima(infos)
-    gathered = torch.cat([ph.export(mn, mr) for ph in phs])
-    parts = [ph.merge(gathered, infos, mn, mr) for ph in phs]
+    mc = _max_classes(infos)
+    gathered = torch.cat([ph.export(mc) for ph in phs])
+    torch.cuda.synchronize()
+    links = [ph.merge(gathered, infos, mc) for ph in phs]
+    tot = torch.stack(links).sum(dim=0)
+    for lk in links:
+        lk.copy_(tot)
+    torch.cuda.synchronize()
+    parts = [ph.resolve() for ph in phs]
     for j, red in enumerate((torch.sum, torch.amin, torch.amax, torch.sum)):
         if parts[0][j].numel():
             stacked = torch.stack([p[j] for p in parts])

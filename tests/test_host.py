@@ -159,24 +159,28 @@ def test_strip_rows():
 def _strip_coll_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
-    from paper_2006_09299_b200.strips import TorchCollectives, _maxima
+    from paper_2006_09299_b200.strips import TorchCollectives, _max_classes
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     coll = TorchCollectives()
-    infos = coll.gather_infos(np.array([10 + rank, 3 * rank, 4 * rank, 4 * rank + 4], dtype=np.int64), "cpu")
+    infos = coll.gather_infos(np.array([10 + rank, 3 * rank, rank, 4 * rank, 4 * rank + 4], dtype=np.int64), "cpu")
     rec = torch.full((16,), rank + 1, dtype=torch.uint8)
     gathered = coll.gather_records(rec)
+    links = torch.zeros(6, dtype=torch.int64)
+    links[2 * rank] = 7 + rank
+    links[2 * rank + 1] = -(rank + 1)
+    coll.reduce_links(links)
     psum = torch.tensor([rank + 1] * 3, dtype=torch.int64)
     pmin = torch.tensor([5 - rank, 7 + rank], dtype=torch.int32)
     pmax = torch.tensor([5 - rank, 7 + rank], dtype=torch.int32)
     pcnt = torch.tensor([2 * rank + 1], dtype=torch.int64)
     coll.reduce_partials(psum, pmin, pmax, pcnt)
     dist.destroy_process_group()
-    q.put((rank, infos.tolist(), _maxima(infos), gathered.tolist(), psum.tolist(), pmin.tolist(),
-           pmax.tolist(), pcnt.tolist()))
+    q.put((rank, infos.tolist(), _max_classes(infos), gathered.tolist(), links.tolist(), psum.tolist(),
+           pmin.tolist(), pmax.tolist(), pcnt.tolist()))
 
 
 def test_strip_collectives_gloo():
-    """world_size-2 gloo run of the strip exchange's three collectives (host side of §8(e))."""
+    """world_size-2 gloo run of the strip exchange's four collectives (host side of §8(e))."""
     import multiprocessing as mp
     import socket
     s = socket.socket()
@@ -191,8 +195,9 @@ def test_strip_collectives_gloo():
     for p in procs:
         p.join(120)
     res = sorted(q.get(timeout=10) for _ in procs)
-    for _, infos, mx, gathered, psum, pmin, pmax, pcnt in res:
-        assert infos == [[10, 0, 0, 4], [11, 3, 4, 8]]
-        assert mx == (11, 4)
+    for _, infos, mx, gathered, links, psum, pmin, pmax, pcnt in res:
+        assert infos == [[10, 0, 0, 0, 4], [11, 3, 1, 4, 8]]
+        assert mx == 11
         assert gathered == [1] * 16 + [2] * 16
+        assert links == [7, -1, 8, -2, 0, 0]
         assert psum == [3, 3, 3] and pmin == [4, 7] and pmax == [5, 8] and pcnt == [4]

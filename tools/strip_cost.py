@@ -1,7 +1,10 @@
 #!/usr/bin/env python
-"""Cost model inputs of the strip path on one GPU: per-strip border components (the exchange
-volume) and the phase times of one rank, for config 5 cut into N strips (in process)."""
+"""Cost model inputs of the strip path on one GPU: per-strip exchange volume (cut classes,
+record bytes) and the wall time of every phase of every strip, for config 5 cut into N strips
+(run in process, phase by phase in lockstep).  The projected N-GPU step is the sum over phases
+of the slowest strip's time (plus the four collectives, O(width) bytes each)."""
 import argparse
+import json
 import os
 import sys
 import time
@@ -14,12 +17,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--strips", type=int, default=8)
     ap.add_argument("--size", type=int, default=32768)
+    ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
     import numpy as np
     import torch
     from paper_2006_09299_b200 import Labeler, LabelingConfig
     from paper_2006_09299_b200.runlab import generate_rows_device
-    from paper_2006_09299_b200.strips import StripPhases, _maxima, strip_rows
+    from paper_2006_09299_b200.strips import StripPhases, _max_classes, strip_rows
     W = H = args.size
     rows = strip_rows(H, args.strips)
     cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
@@ -30,25 +34,65 @@ def main():
         bufs.append(d)
         phs.append(StripPhases(Labeler(0)))
     torch.cuda.synchronize()
-    for rep in range(2):
-        t = {}
+
+    def timed(fn):
         t0 = time.perf_counter()
-        infos = np.stack([ph.local(b.data_ptr(), W, H, y0, h, cfg) for ph, b, (y0, h) in zip(phs, bufs, rows)])
+        r = fn()
         torch.cuda.synchronize()
-        t["local_all_ms"] = (time.perf_counter() - t0) * 1e3
-        mn, mr = _maxima(infos)
-        t0 = time.perf_counter()
-        recs = [ph.export(mn, mr) for ph in phs]
+        return r, (time.perf_counter() - t0) * 1e3
+
+    best = None
+    for _ in range(args.reps):
+        t = {k: [] for k in ("local", "export", "merge", "resolve", "finish")}
+        infos = []
+        for ph, b, (y0, h) in zip(phs, bufs, rows):
+            info, ms = timed(lambda: ph.local(b.data_ptr(), W, H, y0, h, cfg))
+            infos.append(info)
+            t["local"].append(ms)
+        infos = np.stack(infos)
+        mc = _max_classes(infos)
+        recs = []
+        for ph in phs:
+            rec, ms = timed(lambda: ph.export(mc))
+            recs.append(rec)
+            t["export"].append(ms)
         gathered = torch.cat(recs)
         torch.cuda.synchronize()
-        t["export_ms"] = (time.perf_counter() - t0) * 1e3
-        t0 = time.perf_counter()
-        parts = phs[0].merge(gathered, infos, mn, mr)
+        links = []
+        for ph in phs:
+            lk, ms = timed(lambda: ph.merge(gathered, infos, mc))
+            links.append(lk)
+            t["merge"].append(ms)
+        tot = torch.stack(links).sum(dim=0)
+        for lk in links:
+            lk.copy_(tot)
         torch.cuda.synchronize()
-        t["merge_one_rank_ms"] = (time.perf_counter() - t0) * 1e3
-    print({"strips": args.strips, "nodes_per_strip": infos[:, 0].tolist(),
-           "record_MB_per_strip": recs[0].numel() / 1e6, "gathered_MB": gathered.numel() / 1e6,
-           "partials_k": int(parts[0].numel() // 3)} | t)
+        parts = []
+        for ph in phs:
+            p, ms = timed(lambda: ph.resolve())
+            parts.append(p)
+            t["resolve"].append(ms)
+        for j, red in enumerate((torch.sum, torch.amin, torch.amax, torch.sum)):
+            red_t = red(torch.stack([p[j] for p in parts]), dim=0)
+            for p in parts:
+                p[j].copy_(red_t)
+        torch.cuda.synchronize()
+        for ph in phs:
+            _, ms = timed(lambda: ph.finish())
+            t["finish"].append(ms)
+        proj = sum(max(v) for v in t.values())
+        if best is None or proj < best[0]:
+            best = (proj, t)
+    proj, t = best
+    print(json.dumps({
+        "strips": args.strips, "size": args.size,
+        "cut_classes_per_strip": infos[:, 0].tolist(),
+        "record_KB_per_strip": recs[0].numel() / 1e3, "gathered_KB": gathered.numel() / 1e3,
+        "links_KB": links[0].numel() * 8 / 1e3, "partials_KB": parts[0][0].numel() * 8 * 5 / 3 / 1e3,
+        "phase_ms_max_over_strips": {k: round(max(v), 3) for k, v in t.items()},
+        "phase_ms_per_strip": {k: [round(x, 3) for x in v] for k, v in t.items()},
+        "projected_step_ms_wall": round(proj, 3),
+    }))
 
 
 if __name__ == "__main__":
