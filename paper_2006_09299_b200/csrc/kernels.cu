@@ -552,7 +552,9 @@ __global__ void k_cids(Geo g, Ws ws) {
         atomicAdd(&ws.img_surv[gid], 1u);
     }
     const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int32_t t = gid >> 5; t < g.ntiles; t += warps) {
+    // strip mode: this rank's tile rows only (the tiles of other strips hold no nodes here)
+    const int32_t t_lo = g.strip ? g.ty0 * g.ntx : 0, t_hi = g.strip ? g.ty1 * g.ntx : g.ntiles;
+    for (int32_t t = t_lo + (gid >> 5); t < t_hi; t += warps) {
         int32_t b, ty, tx;
         tile_of(g, (uint32_t)t, b, ty, tx);
         const uint32_t nb = ws.tnb[t];

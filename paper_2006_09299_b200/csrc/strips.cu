@@ -351,6 +351,11 @@ __global__ void k_g_reflatten(Ws ws) {
     }
 }
 
+__global__ void k_strip_offsets(Ws ws, int64_t c_lo, int64_t c_hi, int64_t ncnt) {
+    ws.off[ncnt - 1] = ws.off[c_hi];
+    ws.off[0] = 0;  // strip 0: c_lo == 0, already 0
+}
+
 // owned GCCs: canonical id and where the parent chain leaves this strip.  links[2 root] = id,
 // links[2 root + 1] = depth-1 ancestor's id (> 0) when the chain reaches the exterior inside
 // the strip, -(GCC root) when it reaches another cut class first.
@@ -547,12 +552,11 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         if (!ensure(ctx->cub_tmp, std::max(tmp, tmp3))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
         ws.nleft = P<uint32_t>(ctx->nleft);
         ws.ncut = P<uint32_t>(ctx->ncut);
-        const int64_t ncnt = (int64_t)H * g.ntx + 1;
         cudaMemsetAsync(ws.counters, 0, 64, s);
         cudaMemsetAsync(ws.rused, 0, 8, s);
         cudaMemsetAsync(ws.img_fg, 0, 4, s);
-        cudaMemsetAsync(ws.tnb, 0, (size_t)g.ntiles * 4, s);  // tiles of other strips: no nodes here
-        cudaMemsetAsync(ws.cnt, 0, (size_t)ncnt * 4, s);     // rows of other strips: counted elsewhere
+        // the numbering scan reads one cell past this strip's rows (the analyze pass writes the rest)
+        cudaMemsetAsync(ws.cnt + std::min<int64_t>((int64_t)g.ty1 * TH, H) * g.ntx, 0, 4, s);
         launch_analyze(d_strip, g, ws, s);
         launch_seams(g, ws, s, ctx->sms);
         k_strip_left<<<grid((int64_t)ctx->cap_nodes, ctx->sms), 256, 0, s>>>(g, ws);
@@ -693,13 +697,19 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     k_g_apply<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0);
     k_g_reflatten<<<grid(S->n_local, ctx->sms), 256, 0, s>>>(ws);
     const int64_t ncnt = (int64_t)g.H * g.ntx + 1;
-    if (me > 0) {
-        const uint32_t before = (uint32_t)off_me;  // components of the strips above
-        cudaMemcpyAsync(ws.cnt, &before, 4, cudaMemcpyHostToDevice, s);
-    }
     cudaMemsetAsync(ws.img_surv, 0, 4, s);
     launch_reps(g, ws, s, ctx->sms, S->n_local);
-    cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ws.cnt, ws.off, (int)ncnt, s);
+    // offsets of this strip's rows only, starting at the components of the strips above; off[0]
+    // (the image base) and the end cell are what the numbering passes read outside them
+    const int64_t c_lo = (int64_t)g.ty0 * TH * g.ntx, c_hi = std::min<int64_t>((int64_t)g.ty1 * TH, g.H) * g.ntx;
+    size_t tscan = 0;
+    cub::DeviceScan::ExclusiveScan(nullptr, tscan, ws.cnt + c_lo, ws.off + c_lo, cub::Sum(), (uint32_t)0,
+                                   (int)(c_hi - c_lo + 1), s);
+    if (!ensure(ctx->cub_tmp, tscan)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    tscan = ctx->cub_tmp.bytes;
+    cub::DeviceScan::ExclusiveScan(ctx->cub_tmp.p, tscan, ws.cnt + c_lo, ws.off + c_lo, cub::Sum(), (uint32_t)off_me,
+                                   (int)(c_hi - c_lo + 1), s);
+    k_strip_offsets<<<1, 1, 0, s>>>(ws, c_lo, c_hi, ncnt);
     launch_cids(g, ws, s, ctx->sms);
     k_g_links<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0,
                                                                  (uint32_t)S->n_local);
