@@ -15,6 +15,7 @@
 //
 // Reference (paths relative to /root/reference/proj/include/runlab/): labeling.hpp:81-217
 // (Alg. 1-3 + fill), :224-250 (Alg. 4), :354-360 (binarize_labels), features.hpp:33-66.
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -886,7 +887,14 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     RL_PHASE(tg.t, 18);
 
     // ---- interior components, in chunks of C::FCH tile components.  The first chunk's run
-    // pass also marks exterior pixels (for the hole-filled image).
+    // pass also marks exterior pixels (for the hole-filled image) and records, in a register,
+    // the chunk of each of the thread's runs (4 bits per run i = tid + j * BT: the chunk, 14 for
+    // chunk >= 14, 15 for runs with nothing to accumulate), so that a later chunk revisits
+    // only its own runs instead of rescanning the tile.
+    constexpr int RPT = (C::MR + BT - 1) / BT;  // runs per thread
+    static_assert(RPT <= 16, "4-bit run codes fit 64 bits");
+    using CodeT = typename std::conditional<RPT * 4 <= 32, uint32_t, unsigned long long>::type;
+    CodeT codes = 0;
     const int flip = g.flip;
     int nsurv = 0;
     for (int l0 = 0; l0 < max(nlc, 1); l0 += C::FCH) {
@@ -902,21 +910,36 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             __syncthreads();
         }
         RL_PHASE(tg.t, 19);
-        // a component's runs never precede its first (root) run
-        const int ifirst = (l0 == 0 || l0 >= nlc) ? 0 : S.lcrun[l0];
-        for (int i = ifirst + tid; i < nruns; i += BT) {
-            const uint32_t lc = lc_of_run(S, i);
-            const uint16_t lb = S.lcb[lc];
-            if (l0 == 0 && !(lb & 0x8000u) && (E.bflag[lb] & 2u)) {
-                const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
-                for (int wd = c0 >> 5; wd <= ((c1 - 1) >> 5); ++wd) {
-                    const int lo = max(c0 - 32 * wd, 0), hi = min(c1 - 32 * wd, 32);
-                    const uint32_t m = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
-                    atomicOr(&E.ext[rr * WPR + wd], m);
+        const int ch = l0 / C::FCH;
+        const uint32_t want = (uint32_t)min(ch, 14);
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int i = tid + j * BT;
+            if (i >= nruns) break;
+            uint32_t lc;
+            if (l0 == 0) {
+                lc = lc_of_run(S, i);
+                const uint16_t lb = S.lcb[lc];
+                uint32_t code = 15u;
+                if (!(lb & 0x8000u)) {
+                    if (E.bflag[lb] & 2u) {
+                        const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
+                        for (int wd = c0 >> 5; wd <= ((c1 - 1) >> 5); ++wd) {
+                            const int lo = max(c0 - 32 * wd, 0), hi = min(c1 - 32 * wd, 32);
+                            const uint32_t m = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+                            atomicOr(&E.ext[rr * WPR + wd], m);
+                        }
+                    }
+                } else {
+                    code = (uint32_t)min((int)lc / C::FCH, 14);
                 }
-                continue;
+                codes |= (CodeT)code << (4 * j);
+                if (code != 0u) continue;
+            } else {
+                if ((uint32_t)((codes >> (4 * j)) & 15u) != want) continue;
+                lc = lc_of_run(S, i);
+                if (ch >= 14 && ((int)lc < l0 || (int)lc >= l1)) continue;
             }
-            if ((int)lc < l0 || (int)lc >= l1 || !(lb & 0x8000u)) continue;
             const int k = (int)lc - l0;
             const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
             const uint32_t n = (uint32_t)(c1 - c0);
