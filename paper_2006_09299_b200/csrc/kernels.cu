@@ -955,47 +955,70 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         // pre-fill records, post-fill roots, survivor init; folds into border-component roots
         // (initialised by the merge phase) go to the shared table right away, folds into
         // interior survivors wait until the survivors' own records are written (barrier)
-        for (int lc = l0 + tid; lc < l1; lc += BT) {
-            if (lc_is_border(S, lc)) continue;
-            const int k = lc - l0;
-            const int fr = lc_row(S, lc), fc = lc_col(S, lc);
-            const uint32_t cid = comp_cid(E, (uint32_t)lc);
-            const uint32_t pcid = comp_cid(E, lc_at(S, fr, fc - 1));
-            int end;
-            uint32_t surv;
-            const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
-            const int64_t s = E.fs[k];
-            rl_component c;
-            c.f.s = s;
-            c.f.sx = (int64_t)E.fsx[k] + s * tg.x0;
-            c.f.sy = (int64_t)E.fsy[k] + s * tg.y0;
-            c.f.row_min = tg.y0 + fr;
-            c.f.row_max = tg.y0 + E.frmax[k];
-            c.f.col_min = tg.x0 + E.fcmin[k];
-            c.f.col_max = tg.x0 + E.fcmax[k];
-            c.parent = pcid;
-            c.flags = xbit(S, fr, fc) ^ (uint32_t)flip;
-            ws.comps[cb + cid] = c;
-            ws.top[cb + cid] = anc;
-            if (anc == cid) {
-                ws.filled[cb + cid] = c.f;
-                ++nsurv;
-                continue;
+        // whole warps iterate together: the folds of a warp into one border survivor's slot (the
+        // percolating component's, typically) are reduced in registers first, so the shared
+        // table sees one update per warp instead of 32 same-address atomics
+        for (int base = l0 + (tid & ~31); base < l1; base += BT) {
+            const int lc = base + (tid & 31);
+            int slot = -1, k = 0, fr = 0;
+            if (lc < l1 && !lc_is_border(S, lc)) {
+                k = lc - l0;
+                fr = lc_row(S, lc);
+                const int fc = lc_col(S, lc);
+                const uint32_t cid = comp_cid(E, (uint32_t)lc);
+                const uint32_t pcid = comp_cid(E, lc_at(S, fr, fc - 1));
+                int end;
+                uint32_t surv;
+                const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
+                const int64_t s = E.fs[k];
+                rl_component c;
+                c.f.s = s;
+                c.f.sx = (int64_t)E.fsx[k] + s * tg.x0;
+                c.f.sy = (int64_t)E.fsy[k] + s * tg.y0;
+                c.f.row_min = tg.y0 + fr;
+                c.f.row_max = tg.y0 + E.frmax[k];
+                c.f.col_min = tg.x0 + E.fcmin[k];
+                c.f.col_max = tg.x0 + E.fcmax[k];
+                c.parent = pcid;
+                c.flags = xbit(S, fr, fc) ^ (uint32_t)flip;
+                ws.comps[cb + cid] = c;
+                ws.top[cb + cid] = anc;
+                if (anc == cid) {
+                    ws.filled[cb + cid] = c.f;
+                    ++nsurv;
+                } else {
+                    slot = end >= 0 ? fold_slot(E, (uint32_t)end) : -1;
+                    if (slot < 0) {
+                        if (end >= 0) acc_atomic_fold(ws.filled + cb + anc, c.f);  // border root, table full
+                        else E.dfold[atomicAdd(&E.ndfold, 1)] = (uint16_t)lc;
+                    }
+                }
             }
-            const int slot = end >= 0 ? fold_slot(E, (uint32_t)end) : -1;
-            if (slot >= 0) {
-                atomicAdd(&E.ps[slot], E.fs[k]);
-                atomicAdd(&E.psx[slot], E.fsx[k]);
-                atomicAdd(&E.psy[slot], E.fsy[k]);
-                atomicMin(&E.prmin[slot], fr);
-                atomicMax(&E.prmax[slot], E.frmax[k]);
-                atomicMin(&E.pcmin[slot], E.fcmin[k]);
-                atomicMax(&E.pcmax[slot], E.fcmax[k]);
-            } else if (end >= 0) {
-                acc_atomic_fold(ws.filled + cb + anc, c.f);  // border root, table full
-            } else {
-                E.dfold[atomicAdd(&E.ndfold, 1)] = (uint16_t)lc;
+            const uint32_t act = __ballot_sync(0xFFFFFFFFu, slot >= 0);
+            if (!act) continue;
+            const int lead = __ffs(act) - 1;
+            const int dom = __shfl_sync(0xFFFFFFFFu, slot, lead);
+            const uint32_t grp = __ballot_sync(0xFFFFFFFFu, slot == dom);
+            if (slot < 0) continue;
+            uint32_t vs = E.fs[k], vsx = E.fsx[k], vsy = E.fsy[k];
+            int vrmin = fr, vrmax = E.frmax[k], vcmin = E.fcmin[k], vcmax = E.fcmax[k];
+            if (slot == dom) {
+                vs = __reduce_add_sync(grp, vs);
+                vsx = __reduce_add_sync(grp, vsx);
+                vsy = __reduce_add_sync(grp, vsy);
+                vrmin = __reduce_min_sync(grp, vrmin);
+                vrmax = __reduce_max_sync(grp, vrmax);
+                vcmin = __reduce_min_sync(grp, vcmin);
+                vcmax = __reduce_max_sync(grp, vcmax);
+                if ((tid & 31) != lead) continue;
             }
+            atomicAdd(&E.ps[slot], vs);
+            atomicAdd(&E.psx[slot], vsx);
+            atomicAdd(&E.psy[slot], vsy);
+            atomicMin(&E.prmin[slot], vrmin);
+            atomicMax(&E.prmax[slot], vrmax);
+            atomicMin(&E.pcmin[slot], vcmin);
+            atomicMax(&E.pcmax[slot], vcmax);
         }
         __syncthreads();
         RL_PHASE(tg.t, 21);
