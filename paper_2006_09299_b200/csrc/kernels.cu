@@ -816,13 +816,19 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     {  // the run -> component map and component tables the analyze pass stored (tile_runs below
        // does not touch them); bounds-checked so that a failed gate never reads past the store
         const uint64_t moff = ws.tmap[tg.t];
-        const int nr = hdr[0], nl = hdr[1];
+        const int nr = map_pad(hdr[0]), nl = map_pad(hdr[1]);
+        static_assert(C::MR % 8 == 0 && C::NLC % 8 == 0, "padded map sections fit the tables");
         if (moff + (uint64_t)(nr + 2 * nl) <= ws.cap_rstore) {
-            const uint16_t* src = ws.rstore + moff;
-            for (int i = tid; i < nr; i += BT) S.par[i] = src[i];
-            for (int l = tid; l < nl; l += BT) {
-                S.lcrun[l] = src[nr + l];
-                S.lcb[l] = src[nr + nl + l];
+            const uint4* src = reinterpret_cast<const uint4*>(ws.rstore + moff);  // 16-B aligned
+            uint4* dpar = reinterpret_cast<uint4*>(S.par);
+            uint4* drun = reinterpret_cast<uint4*>(S.lcrun);
+            uint4* dlcb = reinterpret_cast<uint4*>(S.lcb);
+            const int vr = nr >> 3, vl = nl >> 3;
+            for (int i = tid; i < vr + 2 * vl; i += BT) {
+                const uint4 v = src[i];
+                if (i < vr) dpar[i] = v;
+                else if (i < vr + vl) drun[i - vr] = v;
+                else dlcb[i - vr - vl] = v;
             }
         }
     }

@@ -96,11 +96,11 @@ struct CclSmem {
     uint16_t rowlc[TH + 1];    // first tile component of each row
     uint16_t rowbx[TH + 1];    // border components before each row start
     uint16_t runpos[MR];       // (row << 8) | col of each run start, raster order
-    typename C::PT par[MR];    // union-find parent; then TAG | component of each run
+    alignas(16) typename C::PT par[MR];  // union-find parent; then TAG | component of each run
     union {
         struct {
-            uint16_t lcrun[C::NLC];  // root (first) run of each tile component
-            uint16_t lcb[C::NLC];    // border index, or 0x8000 | (border components before it)
+            alignas(16) uint16_t lcrun[C::NLC];  // root (first) run of each tile component
+            alignas(16) uint16_t lcb[C::NLC];    // border index, or 0x8000 | (border components before it)
         };
         uint16_t evq[NWARPS][C::EVC];  // union-event queues (dead before lcrun/lcb are written)
     };
@@ -125,6 +125,9 @@ struct MapOut {
     uint64_t* tile_off;        // [tile] offset of its map
     uint32_t* err;             // error bits (ERR_RSTORE_CAP)
 };
+
+// map-store sections are padded to whole 16-B vectors
+__host__ __device__ __forceinline__ int map_pad(int n) { return (n + 7) & ~7; }
 
 template <class SM>
 __device__ __forceinline__ int run_at(const SM& S, int word, int bit) {
@@ -459,7 +462,8 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     };
     if (tid == 0) S.nlc = nlc;
     if (tid == 32) {  // the map: component of each run, first run and border index of each component
-        const unsigned long long need = (unsigned long long)nruns + 2ull * (unsigned long long)nlc;
+        // (three sections, each padded to 8 elements: the emit pass copies them with 16-B loads)
+        const unsigned long long need = (unsigned long long)map_pad(nruns) + 2ull * (unsigned long long)map_pad(nlc);
         const unsigned long long off = atomicAdd(mo.used, need);
         if (off + need > mo.cap) atomicOr(mo.err, ERR_RSTORE_CAP);
         S.moff = off + need > mo.cap ? ~0ull : off;
@@ -525,8 +529,8 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
             }
             S.lcb[l] = v;
             if (map) {
-                map[nruns + l] = S.lcrun[l];
-                map[nruns + nlc + l] = v;
+                map[map_pad(nruns) + l] = S.lcrun[l];
+                map[map_pad(nruns) + map_pad(nlc) + l] = v;
             }
         }
         bx += __popc(m);
