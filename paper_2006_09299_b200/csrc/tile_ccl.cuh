@@ -346,7 +346,14 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     const int my0 = incl - nev;  // offset of this lane's first event in the warp's sequence
     // first-contact parents of every word are in place; tiles whose contacts were all first
     // contacts (vertical stacks of equal runs, sparse tiles) skip the union phase
-    const int any_events = __syncthreads_or(nev);
+    // bit 0: some thread has events; bit 1: some warp has more than one queue of them
+    const int evflags = __syncthreads_or((nev ? 1 : 0) | (wtot > C::EVC ? 2 : 0));
+    const int any_events = evflags & 1;
+    // class S with every warp's events in one queue: the warps fill their queues now (before the
+    // pre-flatten barrier) and after it all threads drain all queues together, so a warp with
+    // many events does not hold the others at the next barrier
+    constexpr bool kSharedDrain = C::BT == NW;
+    const bool shared_drain = kSharedDrain && evflags == 1;
     RL_PHASE(tg.t, 14);
     // The first-contact forest links every run to one in the row above, so a vertical stack
     // of runs is a chain as tall as the stack.  It is flattened before the unions so that their
@@ -354,6 +361,14 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     // walks run concurrently; a link read mid-walk is either the original one or a root
     // already written by another walker, both ancestors, so walks only get shorter.  (Row
     // groups with a barrier between them and pointer-jumping rounds were measured slower.)
+    if (shared_drain) {
+        int o = my0;
+        const uint16_t wbase = (uint16_t)(tid << 7);
+        for (uint32_t e = ev; e; e &= e - 1u) S.evq[warp][o++] = (uint16_t)(wbase | (__ffs(e) - 1));
+        for (uint32_t e = d1; e; e &= e - 1u) S.evq[warp][o++] = (uint16_t)(wbase | (1u << 5) | (__ffs(e) - 1));
+        for (uint32_t e = d2; e; e &= e - 1u) S.evq[warp][o++] = (uint16_t)(wbase | (2u << 5) | (__ffs(e) - 1));
+        if (lane == 0) S.qtot[warp] = wtot;
+    }
     {
         const int nr = S.nruns;
         const int rs = tg.th > 1 ? S.rbase[WPR] : nr;  // runs of row 0 have no first contact
@@ -402,6 +417,21 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     };
     if (!any_events) {
         // nothing to unite
+    } else if (shared_drain) {
+        int qoff[NWARPS + 1];
+        qoff[0] = 0;
+#pragma unroll
+        for (int q = 0; q < NWARPS; ++q) qoff[q + 1] = qoff[q] + S.qtot[q];
+        for (int k = tid; k < qoff[NWARPS]; k += BT) {
+            int q = 0, base = 0;
+#pragma unroll
+            for (int t = 1; t < NWARPS; ++t)
+                if (k >= qoff[t]) {
+                    q = t;
+                    base = qoff[t];
+                }
+            resolve_event(S.evq[q][k - base]);
+        }
     } else if constexpr (BT == NW) {
         for (int done = 0; done < wtot; done += C::EVC) {
             if (nev && my0 < done + C::EVC && my0 + nev > done) put_events(done);
