@@ -331,6 +331,11 @@ constexpr int SEAM_T = RL_SEAM_THREADS;  // threads per seam block (TW / SEAM_T 
 
 __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int32_t ns) {
     __shared__ uint32_t lp[2 * NBMAX];
+    // the seam's two perimeter rows (bottom of the upper tile, top of the lower one), staged
+    // with 16-B loads, and the left tiles' last columns
+    __shared__ __align__(16) uint16_t rowu[TW], rowd[TW];
+    __shared__ uint16_t leftu, leftd;
+    static_assert(SEAM_T >= 2 * (TW / 8), "one 16-B load per thread stages both rows");
     if (ws.counters[1]) return;
     const uint32_t v8 = g.flip ? 0u : 1u;
     const int32_t tx = blockIdx.x, tid = threadIdx.x;
@@ -339,19 +344,25 @@ __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int
         const int32_t b = bs / ns;
         const int64_t tu = ((int64_t)b * g.nty + s) * g.ntx + tx, tl = tu + g.ntx;
         const int nbu = (int)ws.tnb[tu], nbd = (int)ws.tnb[tl];
+        if (tid < TW / 8)
+            reinterpret_cast<uint4*>(rowu)[tid] = reinterpret_cast<const uint4*>(ws.perim + tu * PERIM + TW)[tid];
+        else if (tid < TW / 4)
+            reinterpret_cast<uint4*>(rowd)[tid - TW / 8] = reinterpret_cast<const uint4*>(ws.perim + tl * PERIM)[tid - TW / 8];
+        if (tid == 0 && tx > 0) {
+            leftu = ws.perim[(tu - 1) * PERIM + TW + TW - 1];
+            leftd = ws.perim[(tl - 1) * PERIM + TW - 1];
+        }
         for (int i = tid; i < nbu + nbd; i += SEAM_T) lp[i] = (uint32_t)i;
         __syncthreads();
         for (int c = tid; c < TW; c += SEAM_T) {
             const int32_t x = tx * TW + c;
             if (x >= g.W) break;
-            const uint16_t lu = ws.perim[tu * PERIM + TW + c], ld = ws.perim[tl * PERIM + c];
+            const uint16_t lu = rowu[c], ld = rowd[c];
             const uint32_t vu = lu >> 15, vd = ld >> 15;
             uint16_t lul = PERIM_NONE, ldl = PERIM_NONE;
             if (x > 0) {
-                const int64_t tul = c == 0 ? tu - 1 : tu, tll = c == 0 ? tl - 1 : tl;
-                const int32_t cl = (x - 1) % TW;
-                lul = ws.perim[tul * PERIM + TW + cl];
-                ldl = ws.perim[tll * PERIM + cl];
+                lul = c ? rowu[c - 1] : leftu;
+                ldl = c ? rowd[c - 1] : leftd;
             }
             const uint32_t iu = lu & 0x7FFFu, id = (uint32_t)nbu + (ld & 0x7FFFu);
             if (vu == vd && !(c > 0 && lul == lu && ldl == ld)) sunion(lp, iu, id);
