@@ -542,10 +542,17 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     if (rc) return rc;
     cudaSetDevice(ctx->device);
     const int64_t P = (int64_t)w * h;
-    // a byte-per-pixel filled image crosses PCIe as P4 bits and is expanded by host threads
-    const bool packed = ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
-    // component records and survivors' features cross PCIe as compact slots (pack.cuh)
-    const int pack = ctx->packed_recs ? ((out->comps ? 1 : 0) | (out->filled && out->filled_layout == 1 ? 2 : 0)) : 0;
+    // whole images per chunk, ~32 Mpx by default (pipelines of that size are graph-replayed)
+    const int32_t per = (int32_t)std::min<int64_t>(n, std::max<int64_t>(1, ctx->chunk_px / P));
+    const int32_t nch = (n + per - 1) / per;
+    // With several chunks, a byte-per-pixel filled image crosses PCIe as P4 bits and is expanded
+    // by host threads, and component records and survivors' features cross as compact slots
+    // (pack.cuh), decoded by host threads while later chunks are in flight.  A single chunk has
+    // nothing to overlap the host work with: plain copies are faster there (measured: config 3,
+    // one 16.7 Mpx image, 7.3 -> 16.0 Gpx/s end to end; config 1, 1.25 -> 2.95).
+    const bool multi = nch > 1;
+    const bool packed = multi && ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
+    const int pack = multi && ctx->packed_recs ? ((out->comps ? 1 : 0) | (out->filled && out->filled_layout == 1 ? 2 : 0)) : 0;
     const bool staged = packed || pack || (fmt == RL_PIXELS_U8 && ctx->packed_h2d);
     if (staged && !ctx->pool) {
         const int hw = (int)std::thread::hardware_concurrency();
@@ -553,9 +560,6 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
         ctx->pool = new (std::nothrow) HostPool(nt);
         if (!ctx->pool) return set_err(ctx, RL_ENOMEM, "host thread pool");
     }
-    // whole images per chunk, ~32 Mpx by default (pipelines of that size are graph-replayed)
-    const int32_t per = (int32_t)std::min<int64_t>(n, std::max<int64_t>(1, ctx->chunk_px / P));
-    const int32_t nch = (n + per - 1) / per;
     IntoState st;
     tl.begin(ctx->stream, nch);
     if (nch == 1) {
