@@ -127,6 +127,9 @@ GTab g_layout(void* base, int64_t C, int k) {
 
 // node of the pixel left of each border component's first pixel (local numbering)
 __global__ void k_strip_left(Geo g, Ws ws) {
+    // after a capacity overflow the nodes of the tiles that did not fit were never written (the
+    // host grows the tables and re-runs): their records must not be read
+    if (ws.counters[1]) return;
     const uint32_t n_used = min(ws.counters[0], ws.cap_nodes);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_used; i += gridDim.x * blockDim.x) {
         const uint32_t n = 1u + i;
@@ -555,6 +558,7 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         cudaMemsetAsync(ws.counters, 0, 64, s);
         cudaMemsetAsync(ws.rused, 0, 8, s);
         cudaMemsetAsync(ws.img_fg, 0, 4, s);
+        cudaMemsetAsync(ws.uf, 0, 4, s);  // the exterior node: seams reach it before k_strip_exterior
         // the numbering scan reads one cell past this strip's rows (the analyze pass writes the rest)
         cudaMemsetAsync(ws.cnt + std::min<int64_t>((int64_t)g.ty1 * TH, H) * g.ntx, 0, 4, s);
         launch_analyze(d_strip, g, ws, s);
