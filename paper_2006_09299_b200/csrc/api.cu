@@ -82,6 +82,9 @@ bool ensure(DevBuf& b, size_t bytes) {
         return false;
     }
     b.bytes = want;
+    // debugging aid: fill new workspace with a pattern so reads of unwritten entries show up
+    // (fresh device pages are zero, which hides them; env RUNLAB_GPU_POISON=1)
+    if (std::getenv("RUNLAB_GPU_POISON")) cudaMemset(b.p, 0xA5, want);
     return true;
 }
 

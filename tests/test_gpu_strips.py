@@ -126,3 +126,23 @@ def test_generate_rows_matches_full():
         part = torch.empty((h, W), dtype=torch.uint8, device="cuda")
         generate_rows_device(part.data_ptr(), W, H, y0, h, 0.45, 4, 5)
         assert torch.equal(part, full[y0:y0 + h])
+
+
+def test_strips_poisoned_workspace(labeler):
+    """Fresh contexts whose workspaces start filled with a pattern instead of zeros (recycled
+    device memory): every table the strip phases read must have been written first."""
+    import os
+    os.environ["RUNLAB_GPU_POISON"] = "1"
+    labs = [Labeler(0) for _ in range(3)]
+    try:
+        W, H = 1536, 1000
+        img = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+        cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True, relabel=True)
+        for d, g in ((0.5, 1), (0.45, 4)):
+            generate_device(img.data_ptr(), W, H, d, g, 11)
+            ref = labeler.label_batch(img.cpu().numpy()[None], cfg)
+            _compare(_run(labs, img, W, H, 3, cfg), ref, f"poisoned d={d} g={g}")
+    finally:
+        del os.environ["RUNLAB_GPU_POISON"]
+        for lab in labs:
+            lab.close()
