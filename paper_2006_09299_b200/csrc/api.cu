@@ -84,7 +84,10 @@ bool ensure(DevBuf& b, size_t bytes) {
     b.bytes = want;
     // debugging aid: fill new workspace with a pattern so reads of unwritten entries show up
     // (fresh device pages are zero, which hides them; env RUNLAB_GPU_POISON=1)
-    if (std::getenv("RUNLAB_GPU_POISON")) cudaMemset(b.p, 0xA5, want);
+    if (std::getenv("RUNLAB_GPU_POISON")) {
+        cudaMemset(b.p, 0xA5, want);  // may be asynchronous: done before any stream uses it
+        cudaDeviceSynchronize();
+    }
     return true;
 }
 

@@ -41,6 +41,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -497,6 +498,20 @@ int sync_err(rl_ctx* c, const char* what) {
     return e == cudaSuccess ? RL_OK : cuda_fail(c, e, what);
 }
 
+// RUNLAB_GPU_STRIP_DEBUG=1: synchronise after every launch of the strip phases and name the
+// kernel that failed (diagnostics; the phases otherwise synchronise once at their end)
+bool strip_debug() {
+    static const bool on = std::getenv("RUNLAB_GPU_STRIP_DEBUG") != nullptr;
+    return on;
+}
+#define STRIP_STEP(ctx, name)                                                                     \
+    do {                                                                                          \
+        if (strip_debug()) {                                                                      \
+            const cudaError_t e_ = cudaStreamSynchronize((ctx)->stream);                          \
+            if (e_ != cudaSuccess) return cuda_fail(ctx, e_, name);                               \
+        }                                                                                         \
+    } while (0)
+
 GTab gtab(rl_ctx* ctx) {
     const StripState* S = ctx->strip;
     return g_layout(ctx->gtab.p, S->C, S->n_strips);
@@ -562,8 +577,11 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         // the numbering scan reads one cell past this strip's rows (the analyze pass writes the rest)
         cudaMemsetAsync(ws.cnt + std::min<int64_t>((int64_t)g.ty1 * TH, H) * g.ntx, 0, 4, s);
         launch_analyze(d_strip, g, ws, s);
+        STRIP_STEP(ctx, "launch_analyze");
         launch_seams(g, ws, s, ctx->sms);
+        STRIP_STEP(ctx, "launch_seams");
         k_strip_left<<<grid((int64_t)ctx->cap_nodes, ctx->sms), 256, 0, s>>>(g, ws);
+        STRIP_STEP(ctx, "k_strip_left");
         ctx->launches = 3 + (g.ty1 - g.ty0 > 1) + (g.ntx > 1) + 1;
         uint32_t hc[8] = {};
         cudaMemcpyAsync(hc, ws.counters, 32, cudaMemcpyDeviceToHost, s);
@@ -581,18 +599,22 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         const int64_t n_local = hc[0];
         // flatten inside the strip; cut classes = roots seen on a cut row, numbered by a scan
         k_strip_exterior<<<1, 1, 0, s>>>(ws);
+        STRIP_STEP(ctx, "k_strip_exterior");
         launch_resolve(g, ws, s, ctx->sms, n_local);
+        STRIP_STEP(ctx, "launch_resolve");
         uint32_t* flag = P<uint32_t>(ctx->flag);
         uint32_t* rank = P<uint32_t>(ctx->rank);
         cudaMemsetAsync(flag, 0, (size_t)(n_local + 1) * 4, s);
         cudaMemsetAsync(ws.ncut, 0, (size_t)(n_local + 1) * 4, s);
         k_strip_mark<<<grid(2 * (int64_t)w, ctx->sms), 256, 0, s>>>(g, ws, flag, top, bot);
+        STRIP_STEP(ctx, "k_strip_mark");
         size_t t3 = ctx->cub_tmp.bytes;
         cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t3, flag, rank, (int)(n_local + 1), s);
         unsigned long long* cnt2 = P<unsigned long long>(ctx->scount);
         cudaMemsetAsync(cnt2, 0, 16, s);
         k_strip_count<<<grid(std::max<int64_t>(n_local, (int64_t)(g.ty1 - g.ty0) * TH * g.ntx), ctx->sms), 256, 0, s>>>(
             g, ws, flag, rank, P<uint32_t>(ctx->xnode), cnt2);
+        STRIP_STEP(ctx, "k_strip_count");
         uint32_t klast[2] = {};
         unsigned long long hcnt[2] = {};
         cudaMemcpyAsync(&klast[0], rank + n_local, 4, cudaMemcpyDeviceToHost, s);
@@ -630,6 +652,7 @@ int rl_strip_export(rl_ctx* ctx, int64_t max_classes, void* d_buf) {
     k_strip_pack<<<grid(std::max<int64_t>(S->n_classes + 1, 2 * (int64_t)g.W), ctx->sms), 256, 0, ctx->stream>>>(
         g, ctx->ws, P<uint32_t>(ctx->rank), P<uint32_t>(ctx->xnode), S->n_classes, static_cast<uint8_t*>(d_buf), L,
         g.ty0 > 0, g.ty1 < g.nty);
+    STRIP_STEP(ctx, "k_strip_pack");
     ctx->launches += 1;
     S->phase = 2;
     return sync_err(ctx, "strip export");
@@ -671,10 +694,14 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     cudaMemsetAsync(T.gsurv, 0, 4, s);
     // ---- global cut classes (identical on every rank)
     k_g_init<<<grid(C, ctx->sms), 256, 0, s>>>(T, C);
+    STRIP_STEP(ctx, "k_g_init");
     const uint32_t v8 = g.flip ? 0u : 1u;
     for (int q = 0; q + 1 < n_strips; ++q) k_g_cut<<<grid(g.W, ctx->sms), 256, 0, s>>>(X, T, q, g.W, v8);
+    STRIP_STEP(ctx, "k_g_cut");
     k_g_fold<<<grid(C, ctx->sms), 256, 0, s>>>(X, T, C);
+    STRIP_STEP(ctx, "k_g_fold");
     k_g_reps<<<grid(C, ctx->sms), 256, 0, s>>>(X, T, C);
+    STRIP_STEP(ctx, "k_g_reps");
     std::vector<uint32_t> sc(2 * n_strips);
     cudaMemcpyAsync(sc.data(), T.scnt, sc.size() * 4, cudaMemcpyDeviceToHost, s);
     int rc = sync_err(ctx, "strip cut merge");
@@ -699,10 +726,13 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     ws.ncut = P<uint32_t>(ctx->ncut);
     const uint32_t* xnode = P<uint32_t>(ctx->xnode);
     k_g_apply<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0);
+    STRIP_STEP(ctx, "k_g_apply");
     k_g_reflatten<<<grid(S->n_local, ctx->sms), 256, 0, s>>>(ws);
+    STRIP_STEP(ctx, "k_g_reflatten");
     const int64_t ncnt = (int64_t)g.H * g.ntx + 1;
     cudaMemsetAsync(ws.img_surv, 0, 4, s);
     launch_reps(g, ws, s, ctx->sms, S->n_local);
+    STRIP_STEP(ctx, "launch_reps");
     // offsets of this strip's rows only, starting at the components of the strips above; off[0]
     // (the image base) and the end cell are what the numbering passes read outside them
     const int64_t c_lo = (int64_t)g.ty0 * TH * g.ntx, c_hi = std::min<int64_t>((int64_t)g.ty1 * TH, g.H) * g.ntx;
@@ -714,9 +744,12 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     cub::DeviceScan::ExclusiveScan(ctx->cub_tmp.p, tscan, ws.cnt + c_lo, ws.off + c_lo, cub::Sum(), (uint32_t)off_me,
                                    (int)(c_hi - c_lo + 1), s);
     k_strip_offsets<<<1, 1, 0, s>>>(ws, c_lo, c_hi, ncnt);
+    STRIP_STEP(ctx, "k_strip_offsets");
     launch_cids(g, ws, s, ctx->sms);
+    STRIP_STEP(ctx, "launch_cids");
     k_g_links<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0,
                                                                  (uint32_t)S->n_local);
+    STRIP_STEP(ctx, "k_g_links");
     uint32_t err = 0;
     cudaMemcpyAsync(&err, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
     if ((rc = sync_err(ctx, "strip merge"))) return rc;
@@ -741,16 +774,22 @@ int rl_strip_resolve(rl_ctx* ctx, rl_strip_partials* out) {
     GTab T = gtab(ctx);
     const int64_t C = S->C;
     k_g_anc<<<grid(C, ctx->sms), 256, 0, s>>>(ws, T, C);
+    STRIP_STEP(ctx, "k_g_anc");
     k_g_own<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, P<uint32_t>(ctx->xnode), S->n_classes, S->c0);
+    STRIP_STEP(ctx, "k_g_own");
     launch_tree_parts(g, ws, s, ctx->sms, S->n_local);  // post-fill roots (no fold yet)
+    STRIP_STEP(ctx, "launch_tree_parts");
     // emit this strip's tiles; interior survivors are counted into a private counter
     Ws we = ws;
     uint32_t* isurv = P<uint32_t>(ctx->scount) + 4;
     we.img_surv = isurv;
     cudaMemsetAsync(isurv, 0, 4, s);
     launch_emit(g, we, s);
+    STRIP_STEP(ctx, "launch_emit");
     launch_fold(g, ws, s, ctx->sms, S->n_local);  // border non-survivors of this strip
+    STRIP_STEP(ctx, "launch_fold");
     k_g_partials<<<grid(C, ctx->sms), 256, 0, s>>>(ws, T, C, ws.img_surv, isurv, S->rank > 0 ? 1 : 0);
+    STRIP_STEP(ctx, "k_g_partials");
     uint32_t err = 0;
     cudaMemcpyAsync(&err, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
     const int rc = sync_err(ctx, "strip resolve");
@@ -774,6 +813,7 @@ int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out) {
     cudaStream_t s = ctx->stream;
     GTab T = gtab(ctx);
     k_g_finish<<<grid(S->C, ctx->sms), 256, 0, s>>>(ctx->ws, T, S->C);
+    STRIP_STEP(ctx, "k_g_finish");
     ctx->launches += 1;
     int64_t surv = 0;
     uint32_t gsurv = 0;
