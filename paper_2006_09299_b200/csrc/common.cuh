@@ -277,6 +277,15 @@ __device__ __forceinline__ void acc_atomic_fold(Acc* dst, const Acc& f) {
     atomicMax(&dst->col_max, f.col_max);
 }
 
+// Hole-filling fold (labeling.hpp:199-210): only the sums change.  Everything folded into a
+// post-fill root lies inside one of its holes, hence inside its bounding box, so the root's
+// own box (which its post-fill slot starts from) is already the filled component's box.
+__device__ __forceinline__ void acc_atomic_fold_fill(Acc* dst, int64_t s, int64_t sx, int64_t sy) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&dst->s), static_cast<unsigned long long>(s));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&dst->sx), static_cast<unsigned long long>(sx));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&dst->sy), static_cast<unsigned long long>(sy));
+}
+
 __device__ __forceinline__ Acc acc_empty() {
     Acc a;
     a.s = a.sx = a.sy = 0;

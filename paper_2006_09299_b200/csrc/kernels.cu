@@ -730,9 +730,9 @@ struct EmitSmem {
     uint16_t repx[C::NBC + 1];  // exclusive prefix of representative flags over border index
     // fold of interior components into border-derived survivors: small open-addressing
     // table keyed by border index (overflow goes straight to global atomics)
+    // (sums only: see acc_atomic_fold_fill)
     uint16_t pkey[FOLD_SLOTS];
     uint32_t ps[FOLD_SLOTS], psx[FOLD_SLOTS], psy[FOLD_SLOTS];
-    int32_t prmin[FOLD_SLOTS], prmax[FOLD_SLOTS], pcmin[FOLD_SLOTS], pcmax[FOLD_SLOTS];
     uint32_t ext[NW];       // exterior-pixel masks of the tile words
     uint32_t rowoff[TH];    // canonical id offset of each tile row (relative to the image)
     uint16_t dfold[C::FCH];  // chunk components whose post-fill root is an interior survivor
@@ -846,10 +846,6 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     if (tid < FOLD_SLOTS) {
         E.pkey[tid] = 0xFFFF;
         E.ps[tid] = E.psx[tid] = E.psy[tid] = 0;
-        E.prmin[tid] = 0x7FFFFFFF;
-        E.prmax[tid] = -1;
-        E.pcmin[tid] = 0x7FFFFFFF;
-        E.pcmax[tid] = -1;
     }
     if (tid <= TH) {
         S.rowlc[tid] = hdr[4 + tid];
@@ -1006,7 +1002,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
                 } else {
                     slot = end >= 0 ? fold_slot(E, (uint32_t)end) : -1;
                     if (slot < 0) {
-                        if (end >= 0) acc_atomic_fold(ws.filled + cb + anc, c.f);  // border root, table full
+                        if (end >= 0) acc_atomic_fold_fill(ws.filled + cb + anc, c.f.s, c.f.sx, c.f.sy);  // table full
                         else E.dfold[atomicAdd(&E.ndfold, 1)] = (uint16_t)lc;
                     }
                 }
@@ -1018,24 +1014,15 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             const uint32_t grp = __ballot_sync(0xFFFFFFFFu, slot == dom);
             if (slot < 0) continue;
             uint32_t vs = E.fs[k], vsx = E.fsx[k], vsy = E.fsy[k];
-            int vrmin = fr, vrmax = E.frmax[k], vcmin = E.fcmin[k], vcmax = E.fcmax[k];
             if (slot == dom) {
                 vs = __reduce_add_sync(grp, vs);
                 vsx = __reduce_add_sync(grp, vsx);
                 vsy = __reduce_add_sync(grp, vsy);
-                vrmin = __reduce_min_sync(grp, vrmin);
-                vrmax = __reduce_max_sync(grp, vrmax);
-                vcmin = __reduce_min_sync(grp, vcmin);
-                vcmax = __reduce_max_sync(grp, vcmax);
                 if ((tid & 31) != lead) continue;
             }
             atomicAdd(&E.ps[slot], vs);
             atomicAdd(&E.psx[slot], vsx);
             atomicAdd(&E.psy[slot], vsy);
-            atomicMin(&E.prmin[slot], vrmin);
-            atomicMax(&E.prmax[slot], vrmax);
-            atomicMin(&E.pcmin[slot], vcmin);
-            atomicMax(&E.pcmax[slot], vcmax);
         }
         __syncthreads();
         RL_PHASE(tg.t, 21);
@@ -1044,16 +1031,8 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             int end;
             uint32_t surv;
             const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
-            Acc f;
             const int64_t s = E.fs[k];
-            f.s = s;
-            f.sx = (int64_t)E.fsx[k] + s * tg.x0;
-            f.sy = (int64_t)E.fsy[k] + s * tg.y0;
-            f.row_min = tg.y0 + lc_row(S, lc);
-            f.row_max = tg.y0 + E.frmax[k];
-            f.col_min = tg.x0 + E.fcmin[k];
-            f.col_max = tg.x0 + E.fcmax[k];
-            acc_atomic_fold(ws.filled + cb + anc, f);
+            acc_atomic_fold_fill(ws.filled + cb + anc, s, (int64_t)E.fsx[k] + s * tg.x0, (int64_t)E.fsy[k] + s * tg.y0);
         }
         __syncthreads();
         RL_PHASE(tg.t, 22);
@@ -1061,16 +1040,9 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     // flush border-keyed folds (the survivors were initialised by k_tops)
     for (int i = tid; i < FOLD_SLOTS; i += BT) {
         if (E.pkey[i] == 0xFFFF || !E.ps[i]) continue;
-        Acc f;
         const int64_t s = E.ps[i];
-        f.s = s;
-        f.sx = (int64_t)E.psx[i] + s * tg.x0;
-        f.sy = (int64_t)E.psy[i] + s * tg.y0;
-        f.row_min = tg.y0 + E.prmin[i];
-        f.row_max = tg.y0 + E.prmax[i];
-        f.col_min = tg.x0 + E.pcmin[i];
-        f.col_max = tg.x0 + E.pcmax[i];
-        acc_atomic_fold(ws.filled + cb + E.banc[E.pkey[i]], f);
+        acc_atomic_fold_fill(ws.filled + cb + E.banc[E.pkey[i]], s, (int64_t)E.psx[i] + s * tg.x0,
+                             (int64_t)E.psy[i] + s * tg.y0);
     }
     nsurv = __reduce_add_sync(0xFFFFFFFFu, nsurv);
     if ((tid & 31) == 0 && nsurv) atomicAdd(&ws.img_surv[tg.b], (uint32_t)nsurv);
