@@ -162,7 +162,7 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
               ensure(ctx->comps, ctx->cap_comps * sizeof(rl_component)) &&
               ensure(ctx->top, ctx->cap_comps * 4) && ensure(ctx->filled, ctx->cap_comps * sizeof(Acc)) &&
               ensure(ctx->filled_img, (size_t)(out_px / g.W) * g.orowb) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
-              ensure(ctx->summ, (size_t)(B + 2) * 32);
+              ensure(ctx->summ, (size_t)(B + 2) * 32) && ensure(ctx->ftab, (size_t)FT_SHARDS * FT_HS * 28);
     if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)out_px * 4);
     if (!ok) return set_err(ctx, RL_ENOMEM, "device allocation failed");
     tmp = 0;
@@ -206,6 +206,8 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
     ws.filled = P<Acc>(ctx->filled);
     ws.filled_img = P<uint8_t>(ctx->filled_img);
     ws.labels = g.label_mode ? P<uint32_t>(ctx->labels) : nullptr;
+    ws.ftsum = P<unsigned long long>(ctx->ftab);
+    ws.ftkey = reinterpret_cast<uint32_t*>(ws.ftsum + 3ull * FT_SHARDS * FT_HS);
 
     return RL_OK;
 }
@@ -342,7 +344,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     kt();
     record_event(ctx->ev[2], s, use_graph);
     launch_emit(g, ws, s);
-    launches += 3;
+    launches += 3 + (g.tpi >= 8192 ? 1 : 0);  // + the shard-table flush (kernels.cu FT_MIN_TILES)
     kt();
     k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));
     ++launches;
@@ -554,7 +556,7 @@ void rl_destroy(rl_ctx* c) {
                       &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
                       &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,
-                      &c->fcomp, &c->nleft, &c->scount, &c->ncut, &c->xnode, &c->gtab, &c->pk, &c->pkpar, &c->pkesc, &c->fpk};
+                      &c->fcomp, &c->nleft, &c->scount, &c->ncut, &c->xnode, &c->gtab, &c->ftab, &c->pk, &c->pkpar, &c->pkesc, &c->fpk};
     for (rl_ctx* k : c->kids) rl_destroy(k);
     strip_free(c);
     pool_free(c);

@@ -93,6 +93,10 @@ struct Ws {
     uint32_t* nparent;   // root node of the surrounding component (valid at roots)
     uint32_t* nanccid;   // canonical id of the post-fill root (valid at roots)
     uint32_t* nleft;     // strip mode: node of the pixel left of the first pixel (else null)
+    // sharded hole-fill accumulators: tiles flush their folds into shard (tile % FT_SHARDS) of a
+    // hash table keyed by the post-fill root's slot; k_ftab_flush folds the table into `filled`
+    uint32_t* ftkey;     // [FT_SHARDS * FT_HS] target slot in `filled`, FT_KEY_EMPTY when free
+    unsigned long long* ftsum;  // [FT_SHARDS * FT_HS * 3] S, Sx, Sy
     uint32_t* ncut;      // strip mode: 1 + global root of the cut class at a cut-class root node,
                          // 0 elsewhere (else null; strips.cu)
     // canonical numbering
@@ -119,6 +123,10 @@ struct Ws {
     uint8_t* filled_img;
     uint32_t* labels;
 };
+
+constexpr int FT_SHARDS = 32;        // hole-fill accumulator shards
+constexpr int FT_HS = 1 << 13;        // hash slots per shard
+constexpr uint32_t FT_KEY_EMPTY = 0xFFFFFFFFu;
 
 struct TileGeom {
     int32_t t, b, ty, tx, x0, y0, tw, th;

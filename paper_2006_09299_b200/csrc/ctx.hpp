@@ -149,7 +149,7 @@ struct rl_ctx {
     cudaStream_t in_stream = nullptr;
     cudaEvent_t in_done = nullptr;
     // strip mode (strips.cu)
-    DevBuf nleft, scount, ncut, xnode, gtab;
+    DevBuf nleft, scount, ncut, xnode, gtab, ftab;
     rlh::StripState* strip = nullptr;
 };
 

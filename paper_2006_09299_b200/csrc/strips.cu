@@ -795,7 +795,7 @@ int rl_strip_resolve(rl_ctx* ctx, rl_strip_partials* out) {
     const int rc = sync_err(ctx, "strip resolve");
     if (rc) return rc;
     if (err & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip tree)");
-    ctx->launches += 2 + 1 + 3 + 1 + 1;
+    ctx->launches += 2 + 1 + 3 + (g.tpi >= 8192 ? 1 : 0) + 1 + 1;
     out->d_sum = T.psum;
     out->d_min = T.pmin;
     out->d_max = T.pmax;
