@@ -310,8 +310,10 @@ __device__ __forceinline__ Acc acc_empty() {
 // by the target, then flushes one global atomic fold per distinct target.
 constexpr uint32_t FT_EMPTY = 0xFFFFFFFFu;
 
-template <int SLOTS>
+// BOX = false: hole-filling folds, sums only (acc_atomic_fold_fill)
+template <int SLOTS, bool BOX = true>
 struct FoldTable {
+    static constexpr bool kBox = BOX;
     uint32_t key[SLOTS];
     unsigned long long s[SLOTS], sx[SLOTS], sy[SLOTS], kmin[SLOTS];
     int32_t rmin[SLOTS], rmax[SLOTS], cmin[SLOTS], cmax[SLOTS];
@@ -335,10 +337,12 @@ struct FoldTable {
             atomicAdd(&s[h], (unsigned long long)f.s);
             atomicAdd(&sx[h], (unsigned long long)f.sx);
             atomicAdd(&sy[h], (unsigned long long)f.sy);
-            atomicMin(&rmin[h], f.row_min);
-            atomicMax(&rmax[h], f.row_max);
-            atomicMin(&cmin[h], f.col_min);
-            atomicMax(&cmax[h], f.col_max);
+            if (BOX) {
+                atomicMin(&rmin[h], f.row_min);
+                atomicMax(&rmax[h], f.row_max);
+                atomicMin(&cmin[h], f.col_min);
+                atomicMax(&cmax[h], f.col_max);
+            }
             if (km != ~0ull) atomicMin(&kmin[h], km);
             return true;
         }
@@ -356,7 +360,8 @@ struct FoldTable {
             f.row_max = rmax[i];
             f.col_min = cmin[i];
             f.col_max = cmax[i];
-            acc_atomic_fold(dst(key[i]), f);
+            if (BOX) acc_atomic_fold(dst(key[i]), f);
+            else acc_atomic_fold_fill(dst(key[i]), f.s, f.sx, f.sy);
             if (kmin[i] != ~0ull) atomicMin(kdst(key[i]), kmin[i]);
         }
     }
@@ -373,7 +378,8 @@ __device__ __forceinline__ void warp_fold(TT& T, uint32_t dst, const Acc& f, uns
     const int lane = threadIdx.x & 31;
     auto add = [&](uint32_t k, const Acc& a, unsigned long long km) {
         if (!T.add(k, a, km)) {
-            acc_atomic_fold(gdst(k), a);
+            if (TT::kBox) acc_atomic_fold(gdst(k), a);
+            else acc_atomic_fold_fill(gdst(k), a.s, a.sx, a.sy);
             unsigned long long* kd = gkey(k);
             if (kd && km != ~0ull) atomicMin(kd, km);
         }
@@ -397,10 +403,13 @@ __device__ __forceinline__ void warp_fold(TT& T, uint32_t dst, const Acc& f, uns
             const unsigned long long ko = __shfl_xor_sync(0xFFFFFFFFu, km, o);
             km = ko < km ? ko : km;
         }
-        const int r0 = __reduce_min_sync(0xFFFFFFFFu, mine ? f.row_min : 0x7FFFFFFF);
-        const int r1 = __reduce_max_sync(0xFFFFFFFFu, mine ? f.row_max : (int)0x80000000);
-        const int c0 = __reduce_min_sync(0xFFFFFFFFu, mine ? f.col_min : 0x7FFFFFFF);
-        const int c1 = __reduce_max_sync(0xFFFFFFFFu, mine ? f.col_max : (int)0x80000000);
+        int r0 = 0, r1 = 0, c0 = 0, c1 = 0;
+        if (TT::kBox) {
+            r0 = __reduce_min_sync(0xFFFFFFFFu, mine ? f.row_min : 0x7FFFFFFF);
+            r1 = __reduce_max_sync(0xFFFFFFFFu, mine ? f.row_max : (int)0x80000000);
+            c0 = __reduce_min_sync(0xFFFFFFFFu, mine ? f.col_min : 0x7FFFFFFF);
+            c1 = __reduce_max_sync(0xFFFFFFFFu, mine ? f.col_max : (int)0x80000000);
+        }
         if (lane == lead) {
             Acc a;
             a.s = s0;

@@ -626,7 +626,7 @@ __global__ void k_cids(Geo g, Ws ws) {
 // features into their root right away (block-aggregated; the survivors were initialised by
 // k_cids).  Strip mode folds later, after the cross-rank reduction (k_fold).
 __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
-    __shared__ FoldTable<FT_SLOTS> T;
+    __shared__ FoldTable<FT_SLOTS, false> T;  // hole-filling folds: sums only
     if (ws.counters[1] || !comps_fit(g, ws)) return;
     T.init();
     __syncthreads();
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
 
 // strip mode: border non-survivors into their post-fill roots, after the reduction (strips.cu)
 __global__ void __launch_bounds__(256) k_fold(Geo g, Ws ws) {
-    __shared__ FoldTable<FT_SLOTS> T;
+    __shared__ FoldTable<FT_SLOTS, false> T;  // hole-filling folds: sums only
     if (ws.counters[1] || !comps_fit(g, ws)) return;
     T.init();
     __syncthreads();
