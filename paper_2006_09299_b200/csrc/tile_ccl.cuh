@@ -80,7 +80,7 @@ using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 #endif
 using CapSE = Cap<CapS::MR, CapS::NBC, 192, RL_SE_FCH, uint16_t, NW, CapS::NLC>;
 #ifndef RL_ME_FCH
-#define RL_ME_FCH 640
+#define RL_ME_FCH 768  // the largest chunk with 3 CTAs per SM (640: -0.2% cfg2)
 #endif
 using CapME = Cap<CapM::MR, CapM::NBC, 1024, RL_ME_FCH, uint16_t, 2 * NW>;
 using CapFE = Cap<CapF::MR, CapF::NBC, 1024, 320, uint16_t, 2 * NW>;
