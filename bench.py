@@ -11,9 +11,17 @@ configs (cfg4 shards its 4096 images across ranks; the others run one replica pe
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfgX]
 
-Under torchrun each rank times its own work with CUDA events; time = max over ranks; value =
-all ranks' pixels / time.  `--impl reference` times the reference's own CPU path
-(oracle/_ref, compiled from the unmodified reference headers) on the host cores, rank 0 only.
+`--gpus N` without torchrun re-launches itself under `torch.distributed.run` with N ranks
+(one process per GPU, NCCL).  Batches (cfg2, cfg4) are sharded by image across the ranks --
+the image -> rank assignment balances the expected per-image cost (distributed.py) -- so the
+total work is fixed (strong scaling); cfg1/cfg3 run one replica per rank; cfg5 is cut into
+horizontal strips (strips.py).  Each rank times its own work with CUDA events; time = max
+over ranks; value = all ranks' pixels / time.  `--impl reference` times the reference's own
+CPU path (oracle/_ref, compiled from the unmodified reference headers) on the host cores,
+rank 0 only.
+
+After the timed region every image of the timed batch is compared bit-exactly with the
+reference run on the host (`parity` in the JSON line; `--no-parity` skips it).
 """
 from __future__ import annotations
 
@@ -49,7 +57,7 @@ class Workload:
             self.W = self.H = 2048
             self.specs = [("gen", d, g, 1) for d, g in cfg2_cells()]
             self.desc = "cfg2: 105 x 2048x2048, density k/20 (k=0..20) x granularity {1,2,4,8,16}, seed 1"
-            self.shard = False
+            self.shard = True
         elif name == "cfg3":
             self.W = self.H = 4096
             self.specs = [("rings", 64, 3, 0.02)]
@@ -69,11 +77,13 @@ class Workload:
             raise SystemExit(f"unknown config {name}")
 
     def local_specs(self, rank: int, world: int):
+        """This rank's images: the whole list for replicated single-image configs, else a
+        cost-balanced share of the batch (images are independent)."""
         if not self.shard:
             return self.specs
-        from paper_2006_09299_b200.distributed import shard_range
-        lo, hi = shard_range(len(self.specs), rank, world)
-        return self.specs[lo:hi]
+        from paper_2006_09299_b200.distributed import balanced_shards, image_cost
+        costs = [image_cost(s[1], s[2]) for s in self.specs]
+        return [self.specs[i] for i in balanced_shards(costs, world)[rank]]
 
     def make_device(self, specs):
         import torch
@@ -232,6 +242,67 @@ def run_reference_arm(args, wl: Workload, rank: int) -> None:
     }))
 
 
+def _compare_image(got: dict, ref) -> str | None:
+    """None when one image's GPU outputs equal the reference's canonical result bit for bit,
+    else the first differing field (SURVEY 8(d) parity list)."""
+    for k in ("n_components", "n_fg", "n_holes", "euler", "n_survivors"):
+        if got[k] != getattr(ref, k):
+            return k
+    if got["comps"].tobytes() != ref.comps.tobytes():
+        return "comps"
+    if not np.array_equal(got["top"], ref.top):
+        return "top"
+    surv = ref.top == np.arange(ref.n_components, dtype=np.uint32)
+    if got["filled"][surv].tobytes() != ref.filled[surv].tobytes():
+        return "filled"
+    if not np.array_equal(got["filled_image"], ref.filled_image):
+        return "filled_image"
+    return None
+
+
+def parity_check(wl: Workload, specs, res, threads: int) -> dict:
+    """Every image of the timed batch against the reference compiled from its own headers
+    (oracle/_ref; the C restatement when it is absent), outside the timed region.  Images are
+    generated on the host with the oracle's generator, labeled by the reference and compared
+    with `res` (the fetched device result) by a pool of host threads (the ctypes calls release
+    the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    use_ref = O.ref_available()
+    label = O.ref_label_canonical if use_ref else O.label_canonical
+    t0 = time.perf_counter()
+
+    def one(i: int):
+        s = specs[i]
+        img = (O.generate(wl.W, wl.H, s[1], s[2], s[3]) if s[0] == "gen"
+               else O.generate_rings(wl.W, wl.H, s[1], s[2], s[3]))
+        return _compare_image(res.image(i), label(img, 0))
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        bad = [(i, f) for i, f in enumerate(ex.map(one, range(len(specs)))) if f is not None]
+    n = len(specs)
+    return {"images": n, "mismatches": len(bad), "first_mismatch": bad[:3] or None,
+            "against": "reference (oracle/_ref)" if use_ref else "C restatement (oracle/liboracle.so)",
+            "summary": (f"bit-exact {n - len(bad)}/{n}" if not bad else f"MISMATCH {len(bad)}/{n}"),
+            "seconds": time.perf_counter() - t0}
+
+
+def relaunch_distributed(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: run this script under torch.distributed.run with
+    N ranks on this node (the driver's own launch line), NCCL_DEBUG=INFO into a log file."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", os.path.join("/tmp", "runlab_bench_nccl.%h.%p.log"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 # ------------------------------------------------------------------------------ our arm
 def run_strips(args, wl: Workload, rank: int, world: int, local: int) -> None:
     """SURVEY 8(e): the single image of the workload cut into one horizontal strip per rank;
@@ -347,11 +418,14 @@ def main() -> None:
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the bit-exact check against the reference")
     ap.add_argument("--cpu-seconds", type=float, default=5.0, help="minimum timed wall time of the CPU baseline")
     ap.add_argument("--strips", action="store_true",
                     help="one image cut into horizontal strips across the ranks (default for cfg5 with N > 1)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        raise SystemExit(relaunch_distributed(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -370,6 +444,7 @@ def main() -> None:
 
     from paper_2006_09299_b200 import Labeler, LabelingConfig
     from paper_2006_09299_b200 import _native as N
+    from paper_2006_09299_b200.distributed import sum_over_ranks
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -503,6 +578,16 @@ def main() -> None:
                      "h2d_bytes_per_step": int(outs4.h2d_bytes), "d2h_bytes_per_step": int(outs4.d2h_bytes),
                      "api": "rl_label_into_fmt(RL_PIXELS_P4): P4 rows in, filled image as P4 rows out"}
 
+    # ---- parity of the timed batch (every image, every output) against the reference
+    parity = None
+    if not args.no_parity:
+        parity = parity_check(wl, specs, res, max(1, cpu_threads() // world))
+        if world > 1:
+            bad = sum_over_ranks(parity["mismatches"], device="cuda")
+            tot = sum_over_ranks(parity["images"], device="cuda")
+            parity["images"], parity["mismatches"] = tot, bad
+            parity["summary"] = f"bit-exact {tot - bad}/{tot}" if not bad else f"MISMATCH {bad}/{tot}"
+
     # ---- CPU baseline: the reference itself on a bounded sample, rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -538,8 +623,10 @@ def main() -> None:
             "config": {"workload": wl.desc + ", fg8_bg4, features+Euler+tree+hole fill",
                        "images_per_gpu": B, "pixels_per_gpu": px,
                        "l2": "inputs > L2 (no flush)" if px > 126e6 else "inputs fit L2 (cfg1/cfg3 are launch-bound single images)",
-                       "parallelism": (f"batch sharded by image x{world}" if wl.shard and world > 1
+                       "parallelism": (f"batch sharded by image x{world} (cost-balanced, no data-path "
+                                       "collective)" if wl.shard and world > 1
                                        else f"replica per rank x{world}")},
+            "parity": parity,
             "roofline": {"bound": "hbm", "kernel": dom[0] + " (+ deferred-class launches)", "achieved": dom_gbs,
                          "peak": peak, "unit": "GB/s", "frac": dom_gbs / peak, "traffic": traffic,
                          "traffic_source": traffic_src, "peak_source": peak_src,

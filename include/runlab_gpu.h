@@ -14,7 +14,7 @@
  *
  * POD types only (no C++/torch types), so the reference (namespace runlab) and this
  * library can be linked into one test binary without an ODR clash.  The C++ drop-in
- * header include/runlab/gpu_labeling.hpp rebuilds runlab::LabelingResult from it.
+ * header include/runlab_gpu.hpp rebuilds runlab::LabelingResult from it.
  *
  * Canonical numbering: every component (foreground or background) gets the rank of its
  * raster-first pixel; id 0 is the exterior background.  This equals the ascending order

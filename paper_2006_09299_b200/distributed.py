@@ -31,6 +31,29 @@ def shard_range(n_items: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+def balanced_shards(costs: list[float], world: int) -> list[list[int]]:
+    """Items -> ranks so that the ranks' summed costs are even (longest-processing-time
+    greedy: items by decreasing cost, each to the currently lightest rank; ties go to the
+    lower rank).  Deterministic, so every rank computes the same assignment without a
+    collective.  Each rank's list is returned in ascending item order."""
+    if world < 1:
+        raise ValueError("bad world")
+    load = [0.0] * world
+    out: list[list[int]] = [[] for _ in range(world)]
+    for i in sorted(range(len(costs)), key=lambda k: (-costs[k], k)):
+        r = min(range(world), key=lambda q: (load[q], q))
+        load[r] += costs[i]
+        out[r].append(i)
+    return [sorted(x) for x in out]
+
+
+def image_cost(density: float, granularity: int) -> float:
+    """Relative device cost of one generated image per pixel: a fixed per-pixel part plus a
+    part proportional to the expected runs per pixel, 2 d (1 - d) / g for the reference
+    generator's g x g blocks (generator.hpp:46-83)."""
+    return 1.0 + 8.0 * 2.0 * density * (1.0 - density) / max(granularity, 1)
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar (e.g. a CUDA-event time) over the process group."""
     import torch

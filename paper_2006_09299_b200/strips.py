@@ -213,6 +213,32 @@ class TorchCollectives:
         self._done(pcnt)
 
 
+class HostStagedCollectives(TorchCollectives):
+    """The same four collectives over a CPU backend (gloo): device tensors are staged through
+    host memory around each collective.  For process groups without NCCL -- e.g. ranks that
+    share one GPU, where NCCL refuses duplicate devices."""
+
+    def gather_infos(self, info: np.ndarray, device) -> np.ndarray:
+        return super().gather_infos(info, "cpu")
+
+    def gather_records(self, rec):
+        out = super().gather_records(rec.cpu())
+        return out.to(rec.device)
+
+    def reduce_links(self, links):
+        h = links.cpu()
+        super().reduce_links(h)
+        links.copy_(h)
+        self._done(links)
+
+    def reduce_partials(self, psum, pmin, pmax, pcnt):
+        hs = [t.cpu() for t in (psum, pmin, pmax, pcnt)]
+        super().reduce_partials(*hs)
+        for d, h in zip((psum, pmin, pmax, pcnt), hs):
+            d.copy_(h)
+        self._done(pcnt)
+
+
 _PHASES: dict[int, StripPhases] = {}
 
 

@@ -110,15 +110,54 @@ def test_shard_range():
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_balanced_shards():
+    from paper_2006_09299_b200.distributed import balanced_shards, image_cost
+    from paper_2006_09299_b200.runlab import cfg2_cells
+    costs = [image_cost(d, g) for d, g in cfg2_cells()]
+    for world in (1, 2, 3, 4, 8):
+        parts = balanced_shards(costs, world)
+        assert sorted(i for p in parts for i in p) == list(range(105))
+        loads = [sum(costs[i] for i in p) for p in parts]
+        # LPT: the heaviest rank exceeds the lightest by at most the largest item
+        assert max(loads) - min(loads) <= max(costs) + 1e-9
+        assert parts == balanced_shards(costs, world)  # deterministic
+    assert balanced_shards([1.0] * 5, 8)[5:] == [[], [], []]
+
+
+def test_bench_relaunch_command(monkeypatch):
+    """`bench.py --gpus N` outside torchrun re-runs itself under torch.distributed.run."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    seen = {}
+
+    def fake_call(cmd, env=None):
+        seen["cmd"], seen["env"] = cmd, env
+        return 0
+
+    monkeypatch.setattr(bench.subprocess, "call", fake_call)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "5"])
+    assert bench.relaunch_distributed(4) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "5"]
+    assert seen["env"]["NCCL_DEBUG"] == "INFO"
+
+
 def _gloo_worker(rank, world, port, q):
+    import sys
     import torch.distributed as dist
     from paper_2006_09299_b200.distributed import max_over_ranks, shard_range, sum_over_ranks
+    sys.path.insert(0, ROOT)
+    import bench
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     lo, hi = shard_range(105, rank, world)
     t = max_over_ranks(1.0 + rank)
     n = sum_over_ranks(hi - lo)
+    mine = {c: [s[1:] for s in bench.Workload(c).local_specs(rank, world)] for c in ("cfg2", "cfg4")}
+    counts = {c: sum_over_ranks(len(v)) for c, v in mine.items()}
     dist.destroy_process_group()
-    q.put((rank, t, n))
+    q.put((rank, t, n, mine, counts))
 
 
 def test_multirank_reductions_gloo():
@@ -134,11 +173,17 @@ def test_multirank_reductions_gloo():
     procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
+    res = sorted((q.get(timeout=120) for _ in procs), key=lambda r: r[0])  # before join: large items
     for p in procs:
         p.join(120)
-    res = sorted(q.get(timeout=10) for _ in procs)
     assert [r[1] for r in res] == [2.0, 2.0]
     assert [r[2] for r in res] == [105, 105]
+    # the bench's batch sharding: every image on exactly one rank, both ranks agree on the split
+    import bench
+    for c, total in (("cfg2", 105), ("cfg4", 4096)):
+        assert [r[4][c] for r in res] == [total, total]
+        both = sorted(res[0][3][c] + res[1][3][c])
+        assert both == sorted(s[1:] for s in bench.Workload(c).specs)
 
 
 def test_strip_rows():
