@@ -77,8 +77,11 @@ typedef struct rl_component {
 typedef struct rl_times {
     float analyze_ms;  /* K1a tile scan: segments + tile union-find + border tables */
     float merge_ms;    /* cross-tile union, closure, canonical ids, tree, fill fold */
-    float emit_ms;     /* K1b second tile pass: records, filled image, labels */
+    float emit_ms;     /* K1b second tile pass: records, filled image, label image (relabel
+                          of labeling.hpp:224-250 is fused into this pass) */
     float total_ms;
+    float relabel_ms;  /* after the emit pass: densified label ids (labeling.hpp:231-236) and
+                          survivor compaction; 0 when neither is requested */
 } rl_times;
 
 /* Result of one call over n_images images of identical size, library-allocated

@@ -7,8 +7,9 @@
 //
 //   label_t, no_label, Connectivity          types.hpp:10-21
 //   BinaryImage, LabelImage                  image.hpp:14-67
-//   FeatureAccumulator, FeatureTable         features.hpp:14-30
-//   EquivalenceTable, AdjacencyTable         tables.hpp:37-108 (result-side accessors)
+//   FeatureAccumulator, FeatureTable, merge_into, merge_features, segment_features
+//                                            features.hpp:14-66
+//   EquivalenceTable, AdjacencyTable         tables.hpp:37-108
 //   LabelingConfig, LabelingResult           labeling.hpp:20-50
 //   StepTimes, label_image, timed_label_image, binarize_labels   labeling.hpp:253-360
 //   ComponentRecord, components, holes, ComponentTree, adjacency_tree, euler_number
@@ -21,10 +22,13 @@
 // std::logic_error, std::overflow_error; device failures throw std::runtime_error.
 #pragma once
 
+#include <algorithm>
+#include <cassert>
 #include <cstdint>
 #include <limits>
 #include <memory>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -49,6 +53,9 @@ struct BinaryImage {
     std::int64_t pixel_count() const { return static_cast<std::int64_t>(width) * height; }
     std::uint8_t operator()(std::int32_t r, std::int32_t c) const { return pixels[static_cast<std::size_t>(r) * width + c]; }
     std::uint8_t& operator()(std::int32_t r, std::int32_t c) { return pixels[static_cast<std::size_t>(r) * width + c]; }
+    std::span<const std::uint8_t> row(std::int32_t r) const {  // image.hpp:37-41
+        return {pixels.data() + static_cast<std::size_t>(r) * width, static_cast<std::size_t>(width)};
+    }
     bool operator==(const BinaryImage&) const = default;
 };
 
@@ -61,6 +68,7 @@ struct LabelImage {
     LabelImage(std::int32_t w, std::int32_t h)
         : width(w), height(h), labels(static_cast<std::size_t>(w) * static_cast<std::size_t>(h), 0) {}
     label_t operator()(std::int32_t r, std::int32_t c) const { return labels[static_cast<std::size_t>(r) * width + c]; }
+    label_t& operator()(std::int32_t r, std::int32_t c) { return labels[static_cast<std::size_t>(r) * width + c]; }
     bool operator==(const LabelImage&) const = default;
 };
 
@@ -75,32 +83,90 @@ struct FeatureAccumulator {
 };
 using FeatureTable = std::vector<FeatureAccumulator>;
 
-// Result-side equivalence table: parent and parity per label (no scan-time mutators).
+// features.hpp:33-45: sums add (std::overflow_error on 64-bit overflow), boxes take the envelope
+inline void merge_into(FeatureAccumulator& a, const FeatureAccumulator& b) {
+    bool ovf = __builtin_add_overflow(a.s, b.s, &a.s);
+    ovf |= __builtin_add_overflow(a.sx, b.sx, &a.sx);
+    ovf |= __builtin_add_overflow(a.sy, b.sy, &a.sy);
+    if (ovf) throw std::overflow_error("feature accumulator overflow: image exceeds supported sizes");
+    a.row_min = std::min(a.row_min, b.row_min);
+    a.row_max = std::max(a.row_max, b.row_max);
+    a.col_min = std::min(a.col_min, b.col_min);
+    a.col_max = std::max(a.col_max, b.col_max);
+}
+
+// features.hpp:48-52
+inline FeatureAccumulator merge_features(FeatureAccumulator a, const FeatureAccumulator& b) {
+    merge_into(a, b);
+    return a;
+}
+
+// features.hpp:56-66: moments of the run [j0, j1) of `row` in closed form (the device kernels
+// evaluate the same expressions per run)
+inline FeatureAccumulator segment_features(std::int32_t row, std::int32_t j0, std::int32_t j1) {
+    FeatureAccumulator f;
+    const std::int64_t n = j1 - j0;
+    f.s = n;
+    f.sx = n * (j0 + j1 - 1) / 2;
+    f.sy = static_cast<std::int64_t>(row) * n;
+    f.row_min = f.row_max = row;
+    f.col_min = j0;
+    f.col_max = j1 - 1;
+    return f;
+}
+
+// tables.hpp:37-84: union-find over labels with the min-label rule and one parity bit per
+// label.  A default table holds the exterior (label 0, background), like the reference's; the
+// GPU fills results through the (parent, parity) constructor, and the scan-time mutators are
+// kept so reference code that builds or edits tables compiles and behaves the same.
 class EquivalenceTable {
 public:
-    EquivalenceTable() = default;
+    EquivalenceTable() : t_{0}, fg_{0} {}
     EquivalenceTable(std::vector<label_t> parent, std::vector<std::uint8_t> fg)
         : t_(std::move(parent)), fg_(std::move(fg)) {}
     label_t size() const { return static_cast<label_t>(t_.size()); }
+    label_t make_label(bool foreground) {
+        const label_t e = size();
+        t_.push_back(e);
+        fg_.push_back(foreground ? 1 : 0);
+        return e;
+    }
     bool is_foreground(label_t e) const { return fg_[e] != 0; }
     label_t parent(label_t e) const { return t_[e]; }
     bool is_root(label_t e) const { return t_[e] == e; }
+    void set_parent(label_t e, label_t p) {
+        assert(p <= e);
+        t_[e] = p;
+    }
     label_t find(label_t e) const {
         while (t_[e] != e) e = t_[e];
         return e;
     }
+    label_t union_min(label_t ra, label_t rb) {
+        assert(is_root(ra) && is_root(rb));
+        if (ra < rb) {
+            t_[rb] = ra;
+            return ra;
+        }
+        if (rb < ra) t_[ra] = rb;
+        return rb;
+    }
+    void attach_to_exterior(label_t e) { t_[find(e)] = 0; }
 
 private:
     std::vector<label_t> t_;
     std::vector<std::uint8_t> fg_;
 };
 
+// tables.hpp:94-108: surrounding component per label; entry 0 is the no_label sentinel
 class AdjacencyTable {
 public:
-    AdjacencyTable() = default;
+    AdjacencyTable() : i_{no_label} {}
     explicit AdjacencyTable(std::vector<label_t> i) : i_(std::move(i)) {}
     label_t size() const { return static_cast<label_t>(i_.size()); }
+    void push(label_t initial) { i_.push_back(initial); }
     label_t operator[](label_t e) const { return i_[e]; }
+    void redirect(label_t e, label_t root) { i_[e] = root; }
 
 private:
     std::vector<label_t> i_;
@@ -135,11 +201,20 @@ struct LabelingResult {
     }
 };
 
-// Device phase times (ms, CUDA events), cf. labeling.hpp:253-259.
+// labeling.hpp:253-259, filled from the device phases (CUDA events on the context stream).
+// The device pipeline is not row-sequential, so the reference's per-row phases map to passes:
+//   encode_ns  = the tile analysis pass: segment detection (Alg. 1) fused with the tile-local
+//                part of unification (Alg. 2) and the border tables;
+//   unify_ns   = the cross-tile merge: seam unions (rest of Alg. 2), closure of the border
+//                classes, canonical ids, adjacency tree and hole-fill targets (Alg. 3);
+//   closure_ns = the emit pass: per-component records and fill folds (the rest of Alg. 3),
+//                the hole-filled image and, with relabel, the label image (Alg. 4, fused);
+//   relabel_ns = what runs after the emit pass: densified label ids (labeling.hpp:231-236);
+//   total_ns   = the whole pipeline.
 struct StepTimes {
-    double encode_ns = 0;   // tile analysis pass (segments + tile union-find)
-    double unify_ns = 0;    // cross-tile merge, canonical ids, tree, fill fold
-    double closure_ns = 0;  // emit pass (records, filled image)
+    double encode_ns = 0;
+    double unify_ns = 0;
+    double closure_ns = 0;
     double relabel_ns = 0;
     double total_ns = 0;
 };
@@ -240,7 +315,7 @@ inline LabelingResult run(const BinaryImage& image, const LabelingConfig& config
         times->encode_ns = r.times.analyze_ms * 1e6;
         times->unify_ns = r.times.merge_ms * 1e6;
         times->closure_ns = r.times.emit_ms * 1e6;
-        times->relabel_ns = 0;
+        times->relabel_ns = r.times.relabel_ms * 1e6;
         times->total_ns = r.times.total_ms * 1e6;
     }
     return res;
@@ -324,42 +399,64 @@ inline std::int64_t euler_number(const LabelingResult& res) {
     return *res.euler;
 }
 
-// analysis.hpp:89-125 filter_components, run on the GPU (rl_filter_components_host): every
-// component selected by the predicate merges, with what is embedded in it, into its
-// surrounding component.  The predicate is evaluated here, per record.  The GPU path takes
-// results labeled without fill_holes (every component is then a root of the table).
+// analysis.hpp:89-125 filter_components.  The predicate is evaluated on the host in the
+// reference's order (ascending roots, skipped for a component whose surrounding component
+// already merged); the merge itself -- targets by pointer jumping, feature folds, tree
+// redirection -- runs on the GPU (rl_filter_components_host) over the table of roots, which for
+// a hole-filled result holds only the post-fill roots.  Every label then follows its root.
 template <class Predicate>
 inline LabelingResult filter_components(const LabelingResult& res, Predicate&& selected) {
     const std::vector<ComponentRecord> recs = components(res);
     if (selected(static_cast<const ComponentRecord&>(recs[0])))
         throw std::invalid_argument("filter_components: predicate must not select the exterior");
+    const std::size_t m = recs.size();
     const label_t n = res.equivalences.size();
-    if (static_cast<label_t>(recs.size()) != n)
-        throw std::logic_error("filter_components: the GPU path takes a result labeled without fill_holes");
-    std::vector<rl_component> comps(n);
-    std::vector<std::uint8_t> sel(n, 0);
-    for (const ComponentRecord& rec : recs) {
-        rl_component& c = comps[rec.root];
+    std::vector<label_t> index(n, no_label);  // root label -> position among the roots
+    for (std::size_t k = 0; k < m; ++k) index[recs[k].root] = static_cast<label_t>(k);
+    std::vector<rl_component> comps(m);
+    std::vector<std::uint8_t> sel(m, 0), merged(m, 0);
+    for (std::size_t k = 0; k < m; ++k) {
+        const ComponentRecord& rec = recs[k];
+        rl_component& c = comps[k];
         const FeatureAccumulator& f = rec.features;
         c.f = rl_features{f.s, f.sx, f.sy, f.row_min, f.row_max, f.col_min, f.col_max};
-        c.parent = rec.root == 0 ? no_label : rec.parent_root;
         c.flags = rec.foreground ? 1u : 0u;
-        sel[rec.root] = (rec.root != 0 && selected(static_cast<const ComponentRecord&>(rec))) ? 1 : 0;
+        if (k == 0) {
+            c.parent = no_label;
+            continue;
+        }
+        const label_t pk = index[rec.parent_root];
+        c.parent = pk;
+        if (merged[pk]) {
+            merged[k] = 1;  // embedded in a merged region: the predicate is not asked
+        } else if (selected(static_cast<const ComponentRecord&>(rec))) {
+            sel[k] = merged[k] = 1;
+        }
     }
-    std::vector<label_t> parent(n), adj(n);
-    std::vector<rl_features> feats(n);
-    const int rc = rl_filter_components_host(comps.data(), n, sel.data(), parent.data(), feats.data(), adj.data());
+    std::vector<label_t> target(m), adj(m);
+    std::vector<rl_features> feats(m);
+    const int rc = rl_filter_components_host(comps.data(), static_cast<std::int64_t>(m), sel.data(), target.data(),
+                                             feats.data(), adj.data());
     if (rc == RL_EINVAL) throw std::invalid_argument("filter_components: predicate must not select the exterior");
     if (rc != RL_OK) throw std::runtime_error("filter_components: GPU call failed");
     LabelingResult out = res;
     out.labels.reset();
+    std::vector<label_t> t(n), adjacency(n);
     std::vector<std::uint8_t> fg(n);
-    for (label_t e = 0; e < n; ++e) fg[e] = res.equivalences.is_foreground(e) ? 1 : 0;
-    out.equivalences = EquivalenceTable(std::move(parent), std::move(fg));
-    adj[0] = no_label;
-    out.adjacency = AdjacencyTable(std::move(adj));
+    for (label_t e = 0; e < n; ++e) {
+        const label_t r = res.equivalences.parent(e);  // a root: results are closed (flattened)
+        const label_t k = index[r];
+        t[e] = target[k] != k ? recs[target[k]].root : r;
+        fg[e] = res.equivalences.is_foreground(e) ? 1 : 0;
+        adjacency[e] = res.adjacency[e];
+    }
+    for (std::size_t k = 1; k < m; ++k)
+        if (target[k] == k) adjacency[recs[k].root] = recs[adj[k]].root;
+    out.equivalences = EquivalenceTable(std::move(t), std::move(fg));
+    out.adjacency = AdjacencyTable(std::move(adjacency));
     if (out.features)
-        for (label_t e = 0; e < n; ++e) (*out.features)[e] = gpu::to_acc(feats[e]);
+        for (std::size_t k = 0; k < m; ++k)
+            if (target[k] == k) (*out.features)[recs[k].root] = gpu::to_acc(feats[k]);
     return out;
 }
 

@@ -43,7 +43,7 @@ class RlConfig(C.Structure):
 
 class RlTimes(C.Structure):
     _fields_ = [("analyze_ms", C.c_float), ("merge_ms", C.c_float), ("emit_ms", C.c_float),
-                ("total_ms", C.c_float)]
+                ("total_ms", C.c_float), ("relabel_ms", C.c_float)]
 
 
 class RlResult(C.Structure):

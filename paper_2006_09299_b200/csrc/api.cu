@@ -283,7 +283,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     if (use_graph && ctx->gexec && std::memcmp(&key, &ctx->gkey, sizeof(key)) == 0) {
         const cudaError_t e = cudaGraphLaunch(ctx->gexec, s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "graph launch");
-        for (int k = 0; k < 4; ++k) ctx->ev[k] = ctx->gev[k];
+        for (int k = 0; k < rl_ctx::NEV; ++k) ctx->ev[k] = ctx->gev[k];
         ctx->geo = g;
         ctx->ws = ws;
         ctx->cfg = *cfg;
@@ -294,7 +294,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     }
     {
         const int slot = (int)(ctx->calls % rl_ctx::RING);
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < rl_ctx::NEV; ++k) {
             if (!ctx->ring[slot][k]) cudaEventCreate(&ctx->ring[slot][k]);
             ctx->ev[k] = ctx->ring[slot][k];
         }
@@ -348,6 +348,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     kt();
     k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));
     ++launches;
+    record_event(ctx->ev[3], s, use_graph);
     if (need_rank) {
         // rank of each post-fill root among the batch's components (labeling.hpp:231-236);
         // total components is bounded by cap_comps, flags over [0, cap) are computed for the
@@ -379,7 +380,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
                            ctx->sms);
         ++launches;
     }
-    record_event(ctx->ev[3], s, use_graph);
+    record_event(ctx->ev[4], s, use_graph);
     cudaMemcpyAsync(ctx->h_summ, ctx->summ.p, sn * 8, cudaMemcpyDeviceToHost, s);
     if (use_graph) {
         cudaGraph_t graph = nullptr;
@@ -392,7 +393,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
             return cuda_fail(ctx, e, "graph instantiate");
         }
         ctx->gkey = key;
-        for (int k = 0; k < 4; ++k) ctx->gev[k] = ctx->ev[k];
+        for (int k = 0; k < rl_ctx::NEV; ++k) ctx->gev[k] = ctx->ev[k];
     }
     ctx->used_graph = use_graph;
     const cudaError_t e = cudaGetLastError();
@@ -440,17 +441,23 @@ int finish(rl_ctx* ctx) {
     return set_err(ctx, RL_EINTERNAL, "capacity did not converge");
 }
 
-void fill_times(rl_ctx* ctx, rl_times* t) {
-    float a = 0, m = 0, e = 0, tot = 0;
-    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
-    cudaEventElapsedTime(&m, ctx->ev[1], ctx->ev[2]);
-    cudaEventElapsedTime(&e, ctx->ev[2], ctx->ev[3]);
-    cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[3]);
+static int times_of(cudaEvent_t const* ev, rl_times* t) {
+    float a = 0, m = 0, e = 0, r = 0, tot = 0;
+    if (cudaEventElapsedTime(&a, ev[0], ev[1]) != cudaSuccess || cudaEventElapsedTime(&m, ev[1], ev[2]) != cudaSuccess ||
+        cudaEventElapsedTime(&e, ev[2], ev[3]) != cudaSuccess || cudaEventElapsedTime(&r, ev[3], ev[4]) != cudaSuccess ||
+        cudaEventElapsedTime(&tot, ev[0], ev[4]) != cudaSuccess) {
+        cudaGetLastError();
+        return RL_ECUDA;
+    }
     t->analyze_ms = a;
     t->merge_ms = m;
     t->emit_ms = e;
+    t->relabel_ms = r;
     t->total_ms = tot;
+    return RL_OK;
 }
+
+void fill_times(rl_ctx* ctx, rl_times* t) { times_of(ctx->ev, t); }
 
 int fetch(rl_ctx* ctx, rl_result* out) {
     std::memset(out, 0, sizeof(*out));
@@ -646,17 +653,7 @@ int rl_phase_times(const rl_ctx* ctx, int back, rl_times* out) {
     // the captured ones); older calls come from the ring of eagerly enqueued calls
     const int slot = (int)((ctx->calls - 1 - back) % rl_ctx::RING);
     cudaEvent_t const* ev = back == 0 ? ctx->ev : ctx->ring[slot];
-    float a = 0, m = 0, e = 0, t = 0;
-    if (cudaEventElapsedTime(&a, ev[0], ev[1]) != cudaSuccess || cudaEventElapsedTime(&m, ev[1], ev[2]) != cudaSuccess ||
-        cudaEventElapsedTime(&e, ev[2], ev[3]) != cudaSuccess || cudaEventElapsedTime(&t, ev[0], ev[3]) != cudaSuccess) {
-        cudaGetLastError();
-        return RL_ECUDA;
-    }
-    out->analyze_ms = a;
-    out->merge_ms = m;
-    out->emit_ms = e;
-    out->total_ms = t;
-    return RL_OK;
+    return times_of(ev, out);
 }
 
 void rl_result_free(rl_result* r) {

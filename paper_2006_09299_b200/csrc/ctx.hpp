@@ -78,9 +78,10 @@ struct rl_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     std::string err;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // events of the current call
+    static constexpr int NEV = 5;  // start, after analyze, after merge, after emit, end
+    cudaEvent_t ev[NEV] = {};  // events of the current call
     static constexpr int RING = 64;
-    cudaEvent_t ring[RING][4] = {};
+    cudaEvent_t ring[RING][NEV] = {};
     int64_t calls = 0;
     // workspace
     DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
@@ -105,7 +106,7 @@ struct rl_ctx {
     bool used_graph = false;
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey{};
-    cudaEvent_t gev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t gev[NEV] = {};
     // post-fill features of the survivors compacted into `fcomp` (rl_label_into layout 1)
     bool want_compact = false;
     int64_t chunk_px = 32ll << 20;  // rl_label_into: pixels per chunk (env RUNLAB_GPU_CHUNK_PX)

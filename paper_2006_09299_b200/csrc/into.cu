@@ -240,7 +240,8 @@ void CUDART_CB run_deferred(void* p) {
 size_t up64(size_t v) { return (v + 63) & ~size_t{63}; }
 
 // debugging aid (env RUNLAB_GPU_DEBUG_TIMELINE): per-chunk stream events and host stamps,
-// printed to stderr after the call
+// printed to stderr after the call.  One per host thread (thread_local): a context belongs to
+// one thread, so concurrent rl_label_into calls on different contexts never share it.
 struct Timeline {
     bool on = std::getenv("RUNLAB_GPU_DEBUG_TIMELINE") != nullptr;
     int chunk = 0;
@@ -283,7 +284,7 @@ struct Timeline {
         }
     }
 };
-Timeline tl;
+thread_local Timeline tl;
 
 struct IntoState {
     int64_t total = 0;  // components of the chunks posted so far

@@ -68,6 +68,7 @@ class StepTimes:
     merge_ms: float = 0.0
     emit_ms: float = 0.0
     total_ms: float = 0.0
+    relabel_ms: float = 0.0  # densified label ids / survivor compaction after the emit pass
 
 
 @dataclass
@@ -286,7 +287,7 @@ class Labeler:
         rc = self._L.rl_phase_times(self._ctx, back, C.byref(t))
         if rc != N.RL_OK:
             _raise(rc, "phase times unavailable")
-        return StepTimes(t.analyze_ms, t.merge_ms, t.emit_ms, t.total_ms)
+        return StepTimes(t.analyze_ms, t.merge_ms, t.emit_ms, t.total_ms, t.relabel_ms)
 
     def stream(self) -> int:
         return int(self._L.rl_stream(self._ctx) or 0)
@@ -322,7 +323,7 @@ class Labeler:
             filled_image=N.copy_out(res.filled_image, np.uint8, n * h * w).reshape(n, h, w),
             labels=labels,
             times=StepTimes(res.times.analyze_ms, res.times.merge_ms, res.times.emit_ms,
-                            res.times.total_ms))
+                            res.times.total_ms, res.times.relabel_ms))
 
 
 _default: Labeler | None = None

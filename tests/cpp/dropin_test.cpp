@@ -2,7 +2,9 @@
 // drop-in (include/runlab_gpu.hpp) running on the GPU.  Each check cites the reference test
 // it mirrors (paths relative to /root/reference/proj/tests/).  Exit code = failures.
 #include <cstdio>
+#include <limits>
 #include <stdexcept>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -36,7 +38,91 @@ static LabelingConfig full_config() {
     return cfg;
 }
 
+static FeatureAccumulator acc(std::int64_t s, std::int64_t sx, std::int64_t sy, std::int32_t rmin, std::int32_t rmax,
+                              std::int32_t cmin, std::int32_t cmax) {
+    FeatureAccumulator f;
+    f.s = s;
+    f.sx = sx;
+    f.sy = sy;
+    f.row_min = rmin;
+    f.row_max = rmax;
+    f.col_min = cmin;
+    f.col_max = cmax;
+    return f;
+}
+
+// The filtering rule of analysis.hpp:89-125, written out over the drop-in's own types as the
+// test's independent expectation: ascending roots, a component merges into its surrounding
+// component's target when that one merged, else into its surrounding component when selected.
+template <class Pred>
+static std::pair<std::vector<label_t>, FeatureTable> expected_filter(const LabelingResult& res, Pred pred) {
+    const auto recs = components(res);
+    std::vector<label_t> dest(res.equivalences.size(), no_label);
+    FeatureTable f = *res.features;
+    for (std::size_t i = 1; i < recs.size(); ++i) {
+        const label_t up = dest[recs[i].parent_root];
+        const label_t to = up != no_label ? up : (pred(recs[i]) ? recs[i].parent_root : no_label);
+        if (to == no_label) continue;
+        dest[recs[i].root] = to;
+        merge_into(f[to], f[recs[i].root]);
+    }
+    std::vector<label_t> parent(res.equivalences.size());
+    for (label_t e = 0; e < parent.size(); ++e) {
+        const label_t r = res.equivalences.parent(e);
+        parent[e] = dest[r] != no_label ? dest[r] : r;
+    }
+    return {parent, f};
+}
+
+static std::vector<label_t> parents_of(const EquivalenceTable& eq) {
+    std::vector<label_t> p(eq.size());
+    for (label_t e = 0; e < eq.size(); ++e) p[e] = eq.parent(e);
+    return p;
+}
+
 int main() {
+    // test_core.cpp:30-78 feature algebra and tables (host code of the drop-in)
+    {
+        const auto a = acc(3, 6, 6, 2, 2, 1, 3), b = acc(2, 9, 6, 3, 3, 4, 5);
+        CHECK(merge_features(a, b) == acc(5, 15, 12, 2, 3, 1, 5));
+        CHECK(merge_features(b, a) == merge_features(a, b));
+        CHECK(merge_features(a, a) == acc(6, 12, 12, 2, 2, 1, 3));
+        const auto c = acc(5, 4, 40, 3, 3, 7, 7);
+        CHECK(merge_features(merge_features(a, b), c) == merge_features(a, merge_features(b, c)));
+        bool threw = false;
+        try {
+            auto big = acc(1, std::numeric_limits<std::int64_t>::max(), 0, 0, 0, 0, 0);
+            merge_into(big, acc(1, 1, 0, 0, 0, 0, 0));
+        } catch (const std::overflow_error&) {
+            threw = true;
+        }
+        CHECK(threw);
+        CHECK(segment_features(2, 1, 4) == acc(3, 6, 6, 2, 2, 1, 3));
+        CHECK(segment_features(0, 0, 1) == acc(1, 0, 0, 0, 0, 0, 0));
+        CHECK(segment_features(5, 4, 11) == acc(7, 49, 35, 5, 5, 4, 10));
+        EquivalenceTable eq;
+        CHECK(eq.size() == 1 && !eq.is_foreground(0));
+        CHECK(eq.make_label(true) == 1 && eq.make_label(false) == 2 && eq.make_label(true) == 3);
+        eq.set_parent(2, 0);
+        eq.set_parent(3, 2);
+        CHECK(eq.find(3) == 0 && eq.parent(3) == 2 && eq.find(0) == 0);
+        EquivalenceTable u;
+        for (int i = 0; i < 4; ++i) u.make_label(true);
+        CHECK(u.union_min(4, 1) == 1 && u.parent(4) == 1 && u.find(4) == 1);
+        CHECK(u.union_min(2, 3) == 2 && u.parent(3) == 2 && u.union_min(2, 2) == 2);
+        u.attach_to_exterior(3);
+        CHECK(u.find(3) == 0 && u.parent(2) == 0);
+        CHECK(u.is_foreground(1) && !eq.is_foreground(2));
+        AdjacencyTable adj;
+        CHECK(adj.size() == 1 && adj[0] == no_label);
+        adj.push(0);
+        CHECK(adj[1] == 0);
+        adj.push(1);
+        adj.redirect(2, 0);
+        CHECK(adj[2] == 0 && adj.size() == 3);
+        BinaryImage img = make_image({"010", "110"});
+        CHECK(img.row(1).size() == 3 && img.row(1)[0] == 1 && img.row(1)[2] == 0 && img.row(0)[1] == 1);
+    }
     const BinaryImage fig = make_image({"011111111111110", "010000010000010", "010111010111010",
                                         "010101000101010", "010101111101010", "010100000001000",
                                         "011111111111110"});
@@ -139,6 +225,64 @@ int main() {
             threw = true;
         }
         CHECK(threw);
+    }
+    // test_analysis.cpp:146-210 more: small holes, a lone dot, always-false, the predicate's call
+    // order, and filtering a hole-filled result (the reference accepts any closed result)
+    {
+        LabelingConfig cfg;
+        cfg.compute_features = true;
+        cfg.compute_euler = true;
+        const LabelingResult base = label_image(fig, cfg);
+        auto small_bg = [](const ComponentRecord& r) { return !r.foreground && r.root != 0 && r.features.s < 20; };
+        const LabelingResult f = filter_components(base, small_bg);
+        LabelingConfig fc = cfg;
+        fc.fill_holes = true;
+        const LabelingResult filled = label_image(fig, fc);
+        CHECK(parents_of(f.equivalences) == parents_of(filled.equivalences));
+        for (label_t e : f.roots()) CHECK((*f.features)[e] == (*filled.features)[e]);
+        const LabelingResult same = filter_components(base, [](const ComponentRecord&) { return false; });
+        CHECK(parents_of(same.equivalences) == parents_of(base.equivalences) && *same.features == *base.features);
+        const BinaryImage dot = make_image({"000", "010", "000"});
+        const LabelingResult gone = filter_components(label_image(dot, cfg), [](const ComponentRecord& r) {
+            return r.foreground && r.features.s < 2;
+        });
+        CHECK((gone.roots() == std::vector<label_t>{0}) && (*gone.features)[0].s == 9);
+        // ring-hole-dot: selecting the ring merges everything inside it; the predicate is asked
+        // about the ring, not about the hole and dot embedded in it
+        const BinaryImage rhd = make_image({"0000000", "0111110", "0100010", "0101010", "0100010", "0111110", "0000000"});
+        const LabelingResult r0 = label_image(rhd, cfg);
+        std::vector<label_t> asked;
+        auto ring = [&](const ComponentRecord& r) {
+            asked.push_back(r.root);
+            return r.root == 1;
+        };
+        const LabelingResult rf = filter_components(r0, ring);
+        CHECK((asked == std::vector<label_t>{0, 1}));
+        CHECK((rf.roots() == std::vector<label_t>{0}) && (*rf.features)[0].s == 49);
+        // a hole-filled result: the table of post-fill roots is filtered, every label follows
+        for (const std::uint64_t seed : {71ull, 72ull, 73ull}) {
+            BinaryImage img(26, 22);
+            std::uint64_t x = seed * 0x9E3779B97F4A7C15ull;
+            for (auto& px : img.pixels) {
+                x ^= x << 13, x ^= x >> 7, x ^= x << 17;
+                px = (x >> 33) % 10 < 6;
+            }
+            const LabelingResult fr = label_image(img, fc);
+            auto odd = [](const ComponentRecord& r) { return r.root % 2 == 1 && r.features.s < 30; };
+            const LabelingResult got = filter_components(fr, odd);
+            const auto [want_parent, want_feat] = expected_filter(fr, odd);
+            CHECK(parents_of(got.equivalences) == want_parent);
+            for (label_t e : got.roots()) CHECK((*got.features)[e] == want_feat[e]);
+            const LabelingResult nf = label_image(img, cfg);
+            auto holes_only = [](const ComponentRecord& r) { return !r.foreground && r.root != 0; };
+            const LabelingResult g2 = filter_components(nf, holes_only);
+            const auto [p2, f2] = expected_filter(nf, holes_only);
+            CHECK(parents_of(g2.equivalences) == p2);
+            for (label_t e : g2.roots()) CHECK((*g2.features)[e] == f2[e]);
+            std::int64_t mass = 0;
+            for (label_t e : g2.roots()) mass += (*g2.features)[e].s;
+            CHECK(mass == img.pixel_count());
+        }
     }
     // test_io.cpp:64-132 restated with canonical ids (the Fig. 3 hole is component 2, the
     // reference's provisional root label is 6)
