@@ -95,9 +95,64 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
 
     RL_PHASE(tg.t, 1);
     const MapOut mo{ws.rused, ws.rstore, ws.cap_rstore, ws.tmap, ws.counters + 1};
-    if (!ccl_tile(S, tg, mo)) return false;
+    // border-component features, fed by the map pass of ccl_tile (one call per 32-run block).
+    // Runs of one large border component (the percolating one) would all hit the same shared
+    // accumulators: per call, the component of the first border run is the candidate, its lanes
+    // reduce in registers (REDUX) and one lane does the atomics; the other lanes accumulate
+    // directly.
+    struct BorderFeatures {
+        AnalyzeSmem<C>& A;
+        int tw;
+        __device__ void init(int nb) {
+            for (int i = threadIdx.x; i < nb; i += C::BT) {
+                A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
+                A.brmax[i] = -1;
+                A.bcmin[i] = 0x7FFFFFFF;
+                A.bcmax[i] = -1;
+                A.bimg[i] = 0;
+            }
+        }
+        __device__ void operator()(int bi, int i) {
+            const CclSmem<C>& S = A.c;
+            int rr = 0, c0 = 0x7FFFFFFF, cl = -1;
+            uint32_t n = 0, sx = 0, sy = 0;
+            if (bi >= 0) {
+                const uint16_t rp = S.runpos[i];
+                const uint16_t nx = (i + 1 < S.nruns) ? S.runpos[i + 1] : 0xFFFF;
+                rr = rp >> 8;
+                c0 = rp & 0xFF;
+                const int c1 = ((nx >> 8) == rr) ? (nx & 0xFF) : tw;
+                n = (uint32_t)(c1 - c0);
+                sx = n * (uint32_t)(c0 + c1 - 1) / 2u;
+                sy = n * (uint32_t)rr;
+                cl = c1 - 1;
+            }
+            const uint32_t valid = __ballot_sync(0xFFFFFFFFu, bi >= 0);
+            if (!valid) return;
+            const int cand = __shfl_sync(0xFFFFFFFFu, bi, __ffs(valid) - 1);
+            const uint32_t grp = __ballot_sync(0xFFFFFFFFu, bi == cand);
+            if (bi == cand) {
+                n = __reduce_add_sync(grp, n);
+                sx = __reduce_add_sync(grp, sx);
+                sy = __reduce_add_sync(grp, sy);
+                rr = __reduce_max_sync(grp, rr);
+                c0 = __reduce_min_sync(grp, c0);
+                cl = __reduce_max_sync(grp, cl);
+                if ((int)(threadIdx.x & 31) != __ffs(grp) - 1) bi = -1;  // the leader commits the group
+            }
+            if (bi >= 0) {
+                atomicAdd(&A.bs[bi], n);
+                atomicAdd(&A.bsx[bi], sx);
+                atomicAdd(&A.bsy[bi], sy);
+                atomicMax(&A.brmax[bi], rr);
+                atomicMin(&A.bcmin[bi], c0);
+                atomicMax(&A.bcmax[bi], cl);
+            }
+        }
+    };
+    if (!ccl_tile(S, tg, mo, BorderFeatures{A, tg.tw})) return false;
 
-    const int nruns = S.nruns, nlc = S.nlc, nb = S.nb;
+    const int nlc = S.nlc, nb = S.nb;
     // the two allocations are issued by different warps so their latencies overlap
     if (tid == 0) {
         const uint32_t base = atomicAdd(&ws.counters[0], (uint32_t)nb);
@@ -110,7 +165,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     {
         uint16_t* hdr = ws.thdr + (int64_t)tg.t * THDR;
         if (tid == 0) {
-            hdr[0] = (uint16_t)nruns;
+            hdr[0] = (uint16_t)S.nruns;
             hdr[1] = (uint16_t)nlc;
             hdr[2] = (uint16_t)nb;
             hdr[3] = 0;
@@ -120,82 +175,35 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
             hdr[4 + TH + 1 + tid] = S.rowbx[tid];
         }
     }
-    for (int i = tid; i < nb; i += BT) {  // border-component accumulators
-        A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
-        A.brmax[i] = -1;
-        A.bcmin[i] = 0x7FFFFFFF;
-        A.bcmax[i] = -1;
-        A.bimg[i] = 0;
-    }
-    __syncthreads();
-    RL_PHASE(tg.t, 9);
-    // ---- border-component features and image-border contact (one lane per run)
+    RL_PHASE(tg.t, 10);
+    const int flip = g.flip;
+    // ---- perimeter labels: (value << 15) | border index; perimeter pixels on the image frame
+    // mark their component as touching it
     const bool top_img = tg.ty == 0, bot_img = (tg.y0 + tg.th == g.H);
     const bool left_img = tg.tx == 0, right_img = (tg.x0 + tg.tw == g.W);
-    // Runs of one large border component (the percolating one) would all hit the same shared
-    // accumulators.  Per warp iteration, the component of the first border run is the candidate:
-    // its lanes reduce in registers (REDUX) and one lane does the atomics; the other lanes
-    // accumulate directly.
-    constexpr int U = 4;  // loads of U iterations are issued together (latency hiding)
-    for (int j0 = 0; j0 < nruns; j0 += U * BT) {
-      uint16_t lbv[U], rpv[U], nxv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-          const int i = j0 + u * BT + tid;
-          const bool ok = i < nruns;
-          const uint32_t lc = ok ? lc_of_run(S, i) : 0u;
-          rpv[u] = ok ? S.runpos[i] : 0;
-          nxv[u] = (i + 1 < nruns) ? S.runpos[i + 1] : 0xFFFF;
-          lbv[u] = ok ? S.lcb[lc] : 0x8000;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        int bi = -1, rr = 0, c0 = 0x7FFFFFFF, cl = -1;
-        uint32_t n = 0, sx = 0, sy = 0, img = 0;
-        if (!(lbv[u] & 0x8000u)) {
-            bi = lbv[u];
-            rr = rpv[u] >> 8;
-            c0 = rpv[u] & 0xFF;
-            const int c1 = ((nxv[u] >> 8) == rr) ? (nxv[u] & 0xFF) : tg.tw;
-            n = (uint32_t)(c1 - c0);
-            sx = n * (uint32_t)(c0 + c1 - 1) / 2u;
-            sy = n * (uint32_t)rr;
-            cl = c1 - 1;
-            img = ((top_img && rr == 0) || (bot_img && rr == tg.th - 1) || (left_img && c0 == 0) ||
-                   (right_img && c1 == tg.tw)) ? 1u : 0u;
+    for (int q = tid; q < PERIM; q += BT) {
+        int pr, pc;
+        bool frame;
+        if (q < TW) { pr = 0; pc = q; frame = top_img; }
+        else if (q < 2 * TW) { pr = tg.th - 1; pc = q - TW; frame = bot_img; }
+        else if (q < 2 * TW + TH) { pr = q - 2 * TW; pc = 0; frame = left_img; }
+        else { pr = q - 2 * TW - TH; pc = tg.tw - 1; frame = right_img; }
+        uint16_t v = PERIM_NONE;
+        if (pr >= 0 && pr < tg.th && pc >= 0 && pc < tg.tw) {
+            const uint32_t lc = lc_at(S, pr, pc);
+            const uint32_t val = xbit(S, pr, pc) ^ (uint32_t)flip;
+            const uint32_t bi = S.lcb[lc] & 0x7FFF;
+            v = (uint16_t)((val << 15) | bi);
+            if (frame) A.bimg[bi] = 1;
         }
-        const uint32_t valid = __ballot_sync(0xFFFFFFFFu, bi >= 0);
-        if (!valid) continue;
-        const int cand = __shfl_sync(0xFFFFFFFFu, bi, __ffs(valid) - 1);
-        const uint32_t grp = __ballot_sync(0xFFFFFFFFu, bi == cand);
-        if (bi == cand) {
-            n = __reduce_add_sync(grp, n);
-            sx = __reduce_add_sync(grp, sx);
-            sy = __reduce_add_sync(grp, sy);
-            rr = __reduce_max_sync(grp, rr);
-            c0 = __reduce_min_sync(grp, c0);
-            cl = __reduce_max_sync(grp, cl);
-            img = __reduce_or_sync(grp, img);
-            if ((int)(tid & 31) != __ffs(grp) - 1) bi = -1;  // the leader commits the group
-        }
-        if (bi >= 0) {
-            atomicAdd(&A.bs[bi], n);
-            atomicAdd(&A.bsx[bi], sx);
-            atomicAdd(&A.bsy[bi], sy);
-            atomicMax(&A.brmax[bi], rr);
-            atomicMin(&A.bcmin[bi], c0);
-            atomicMax(&A.bcmax[bi], cl);
-            if (img) A.bimg[bi] = 1;
-        }
-      }
+        ws.perim[(int64_t)tg.t * PERIM + q] = v;
     }
     __syncthreads();
 
-    RL_PHASE(tg.t, 10);
+    RL_PHASE(tg.t, 11);
     // ---- border-component nodes
     const uint32_t base = A.base;
     const bool node_ok = (uint64_t)base + nb <= ws.cap_nodes;
-    const int flip = g.flip;
     for (int i = tid; i < nb && node_ok; i += BT) {
         const int lc = S.blc[i];
         const int fr = lc_row(S, lc), fc = lc_col(S, lc);
@@ -242,22 +250,6 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         ws.uf[node] = (!fg && A.bimg[i]) ? (uint32_t)tg.b : node;
     }
 
-    // ---- perimeter labels: (value << 15) | border index
-    for (int q = tid; q < PERIM; q += BT) {
-        int pr, pc;
-        if (q < TW) { pr = 0; pc = q; }
-        else if (q < 2 * TW) { pr = tg.th - 1; pc = q - TW; }
-        else if (q < 2 * TW + TH) { pr = q - 2 * TW; pc = 0; }
-        else { pr = q - 2 * TW - TH; pc = tg.tw - 1; }
-        uint16_t v = PERIM_NONE;
-        if (pr >= 0 && pr < tg.th && pc >= 0 && pc < tg.tw) {
-            const uint32_t lc = lc_at(S, pr, pc);
-            const uint32_t val = xbit(S, pr, pc) ^ (uint32_t)flip;
-            v = (uint16_t)((val << 15) | (S.lcb[lc] & 0x7FFF));
-        }
-        ws.perim[(int64_t)tg.t * PERIM + q] = v;
-    }
-
     // ---- interior components per row, foreground interior components
     if (tid < tg.th) {
         const int nl = S.rowlc[tid + 1] - S.rowlc[tid];
@@ -269,7 +261,6 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         if (lc_is_border(S, l)) continue;
         nfg += (int)(xbit(S, lc_row(S, l), lc_col(S, l)) ^ (uint32_t)flip);
     }
-    RL_PHASE(tg.t, 11);
     nfg = __reduce_add_sync(0xFFFFFFFFu, nfg);
     if ((tid & 31) == 0 && nfg) atomicAdd(&ws.img_fg[tg.b], (uint32_t)nfg);
     RL_PHASE(tg.t, 12);

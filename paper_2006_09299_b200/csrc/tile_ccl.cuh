@@ -271,8 +271,11 @@ __device__ __forceinline__ bool tile_runs(CclSmem<C>& S, WordBits& wb) {
     return true;
 }
 
-template <class C>
-__device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
+// `border` is called by every lane of every warp, once per 32-run block of the map pass, with
+// the run index and its border index (-1 for runs of interior components and past the last
+// run); border.init(nb) clears the border-component accumulators before that pass.
+template <class C, class Border>
+__device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Border&& border) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int r = tid / WPR, w = tid % WPR;
@@ -501,39 +504,28 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     }
     for (int l = tid; l < nlc; l += BT) S.lcb[l] = 0;
     __syncthreads();
+    RL_PHASE(tg.t, 6);
+    // ---- border components (plain stores of 1): every row's first and last run (the left and
+    // right tile columns: a row's first run starts at column 0, its last ends at the tile edge)
+    // and every run of the top and bottom rows.  par[] holds each run's root here.
+    const int top_end = S.rbase[WPR], bot_begin = S.rbase[(tg.th - 1) * WPR];
     if (tid <= TH) {  // first component of each row: components before the row's first run
         const int k = tid < tg.th ? S.rbase[tid * WPR] : nruns;
         S.rowlc[tid] = (uint16_t)(k < nruns ? rank_of((uint32_t)k) : (uint32_t)nlc);
     }
-    if (tid < tg.th) {  // border components through the left and right tile columns: every row's
-                        // first run starts at column 0 and its last run ends at the tile edge
-        // (a slot the loop below already rewrote holds TAG16 | component)
-        auto comp_of = [&](int k) {
-            const uint32_t v = S.par[k];
-            return (v & TAG16) ? (v & 0x7FFFu) : rank_of(v);
-        };
-        S.lcb[comp_of(S.rbase[tid * WPR])] = 1;
-        S.lcb[comp_of(S.rbase[(tid + 1) * WPR] - 1)] = 1;
+    if (tid < tg.th) {
+        S.lcb[rank_of(S.par[S.rbase[tid * WPR]])] = 1;
+        S.lcb[rank_of(S.par[S.rbase[(tid + 1) * WPR] - 1])] = 1;
     }
-    RL_PHASE(tg.t, 6);
-    const unsigned long long moff = S.moff;
-    uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
-    // every run: its component, the component's first run, border flags of the top and bottom
-    // rows' runs (plain stores of 1)
-    const int top_end = S.rbase[WPR], bot_begin = S.rbase[(tg.th - 1) * WPR];
-    for (int i = tid; i < nruns; i += BT) {
-        const uint32_t root = S.par[i];
-        const uint32_t l = rank_of(root);
-        S.par[i] = (uint16_t)(TAG16 | l);
-        if (root == (uint32_t)i) S.lcrun[l] = (uint16_t)i;
-        if (map) map[i] = (uint16_t)l;
-        if (i < top_end || i >= bot_begin) S.lcb[l] = 1;
-    }
+    for (int i = tid; i < top_end; i += BT) S.lcb[rank_of(S.par[i])] = 1;
+    for (int i = bot_begin + tid; i < nruns; i += BT) S.lcb[rank_of(S.par[i])] = 1;
     __syncthreads();
     RL_PHASE(tg.t, 7);
 
+    const unsigned long long moff = S.moff;
+    uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
     constexpr int NWB = BT / 32;
-    // ---- compact border components to border indices (raster order; warp segments again)
+    // ---- compact border components to border indices (raster order; warp segments)
     const int segl = ((nlc + NWB - 1) / NWB + 31) & ~31;
     const int l0 = min(warp * segl, nlc), l1 = min(l0 + segl, nlc);
     int cntb = 0;
@@ -546,33 +538,51 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo) {
     if (nb > C::NBC) return false;  // more border components than this class holds
     for (int b = l0; b < l1; b += 32) {
         const int l = b + lane;
-        const bool border = l < l1 && S.lcb[l];
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, border);
+        const bool isb = l < l1 && S.lcb[l];
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, isb);
         const int my = bx + __popc(m & lt);
         if (l < l1) {
             uint16_t v;
-            if (border) {
+            if (isb) {
                 S.blc[my] = (uint16_t)l;
                 v = (uint16_t)my;
             } else {
                 v = (uint16_t)(0x8000 | my);
             }
             S.lcb[l] = v;
-            if (map) {
-                map[map_pad(nruns) + l] = S.lcrun[l];
-                map[map_pad(nruns) + map_pad(nlc) + l] = v;
-            }
+            if (map) map[map_pad(nruns) + map_pad(nlc) + l] = v;
         }
         bx += __popc(m);
     }
     if (tid == 0) S.nb = nb;
+    border.init(nb);
     __syncthreads();
+    RL_PHASE(tg.t, 8);
+
+    // ---- every run: its component (par becomes TAG | component), the component's first run, the
+    // map entry; runs of border components feed the border features
     if (tid <= TH) {
         const int l = S.rowlc[tid];
         S.rowbx[tid] = l < nlc ? (uint16_t)(S.lcb[l] & 0x7FFF) : (uint16_t)nb;
     }
+    for (int b = warp * 32; b < nruns; b += BT) {
+        const int i = b + lane;
+        int bi = -1;
+        if (i < nruns) {
+            const uint32_t root = S.par[i];
+            const uint32_t l = rank_of(root);
+            S.par[i] = (uint16_t)(TAG16 | l);
+            if (root == (uint32_t)i) S.lcrun[l] = (uint16_t)i;
+            if (map) map[i] = (uint16_t)l;
+            const uint16_t lb = S.lcb[l];
+            if (!(lb & 0x8000u)) bi = lb;
+        }
+        border(bi, i);
+    }
     __syncthreads();
-    RL_PHASE(tg.t, 8);
+    if (map)
+        for (int l = tid; l < nlc; l += BT) map[map_pad(nruns) + l] = S.lcrun[l];
+    RL_PHASE(tg.t, 9);
     return true;
 }
 
