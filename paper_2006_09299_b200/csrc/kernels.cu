@@ -103,6 +103,8 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     struct BorderFeatures {
         AnalyzeSmem<C>& A;
         int tw;
+        uint32_t flip;
+        int nfg;  // foreground interior components seen by this thread
         __device__ void init(int nb) {
             for (int i = threadIdx.x; i < nb; i += C::BT) {
                 A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
@@ -112,8 +114,9 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
                 A.bimg[i] = 0;
             }
         }
-        __device__ void operator()(int bi, int i) {
+        __device__ void operator()(int bi, int i, bool iroot) {
             const CclSmem<C>& S = A.c;
+            if (iroot) nfg += (int)(((S.x[(S.runpos[i] >> 8) * WPR + ((S.runpos[i] & 0xFF) >> 5)] >> (S.runpos[i] & 31)) & 1u) ^ flip);
             int rr = 0, c0 = 0x7FFFFFFF, cl = -1;
             uint32_t n = 0, sx = 0, sy = 0;
             if (bi >= 0) {
@@ -150,7 +153,8 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
             }
         }
     };
-    if (!ccl_tile(S, tg, mo, BorderFeatures{A, tg.tw})) return false;
+    BorderFeatures bf{A, tg.tw, (uint32_t)g.flip, 0};
+    if (!ccl_tile(S, tg, mo, bf)) return false;
 
     const int nlc = S.nlc, nb = S.nb;
     // the two allocations are issued by different warps so their latencies overlap
@@ -256,12 +260,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         const int nbr = S.rowbx[tid + 1] - S.rowbx[tid];
         ws.cnt[((int64_t)tg.b * g.H + tg.y0 + tid) * g.ntx + tg.tx] = (uint32_t)(nl - nbr);
     }
-    int nfg = 0;
-    for (int l = tid; l < nlc; l += BT) {
-        if (lc_is_border(S, l)) continue;
-        nfg += (int)(xbit(S, lc_row(S, l), lc_col(S, l)) ^ (uint32_t)flip);
-    }
-    nfg = __reduce_add_sync(0xFFFFFFFFu, nfg);
+    const int nfg = __reduce_add_sync(0xFFFFFFFFu, bf.nfg);
     if ((tid & 31) == 0 && nfg) atomicAdd(&ws.img_fg[tg.b], (uint32_t)nfg);
     RL_PHASE(tg.t, 12);
     return true;
@@ -926,12 +925,17 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
                 const uint16_t lb = S.lcb[lc];
                 uint32_t code = 15u;
                 if (!(lb & 0x8000u)) {
-                    if (E.bflag[lb] & 2u) {
+                    if (E.bflag[lb] & 2u) {  // exterior run: its pixels in the row's words
                         const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
-                        for (int wd = c0 >> 5; wd <= ((c1 - 1) >> 5); ++wd) {
-                            const int lo = max(c0 - 32 * wd, 0), hi = min(c1 - 32 * wd, 32);
-                            const uint32_t m = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
-                            atomicOr(&E.ext[rr * WPR + wd], m);
+                        const int w0 = c0 >> 5, w1 = (c1 - 1) >> 5;
+                        uint32_t* ext = E.ext + rr * WPR;
+                        const uint32_t mlo = 0xFFFFFFFFu << (c0 & 31), mhi = 0xFFFFFFFFu >> (31 - ((c1 - 1) & 31));
+                        if (w0 == w1) {
+                            atomicOr(ext + w0, mlo & mhi);
+                        } else {  // words strictly inside the run belong to it alone
+                            atomicOr(ext + w0, mlo);
+                            for (int wd = w0 + 1; wd < w1; ++wd) ext[wd] = 0xFFFFFFFFu;
+                            atomicOr(ext + w1, mhi);
                         }
                     }
                 } else {

@@ -272,8 +272,9 @@ __device__ __forceinline__ bool tile_runs(CclSmem<C>& S, WordBits& wb) {
 }
 
 // `border` is called by every lane of every warp, once per 32-run block of the map pass, with
-// the run index and its border index (-1 for runs of interior components and past the last
-// run); border.init(nb) clears the border-component accumulators before that pass.
+// the run index, its border index (-1 for runs of interior components and past the last run)
+// and whether the run is the first run of an interior component; border.init(nb) clears the
+// border-component accumulators before that pass.
 template <class C, class Border>
 __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Border&& border) {
     const int tid = threadIdx.x;
@@ -568,6 +569,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
     for (int b = warp * 32; b < nruns; b += BT) {
         const int i = b + lane;
         int bi = -1;
+        bool iroot = false;
         if (i < nruns) {
             const uint32_t root = S.par[i];
             const uint32_t l = rank_of(root);
@@ -576,8 +578,9 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
             if (map) map[i] = (uint16_t)l;
             const uint16_t lb = S.lcb[l];
             if (!(lb & 0x8000u)) bi = lb;
+            else iroot = root == (uint32_t)i;
         }
-        border(bi, i);
+        border(bi, i, iroot);
     }
     __syncthreads();
     if (map)
