@@ -32,7 +32,9 @@ template <class C>
 struct AnalyzeSmem {
     CclSmem<C> c;
     // border-component accumulators (tile-local coordinates)
-    uint32_t bs[C::NBC], bsx[C::NBC], bsy[C::NBC];
+    // S | (Sy << 14) in one word: a tile holds <= 8192 pixels (14 bits) and their row sum is
+    // < 8192 * 32 (18 bits), so one atomic adds both without carries between the fields
+    uint32_t bssy[C::NBC], bsx[C::NBC];
     int32_t brmax[C::NBC], bcmin[C::NBC], bcmax[C::NBC];
     uint8_t bimg[C::NBC];  // touches the image border
     uint32_t base;
@@ -107,7 +109,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         int nfg;  // foreground interior components seen by this thread
         __device__ void init(int nb) {
             for (int i = threadIdx.x; i < nb; i += C::BT) {
-                A.bs[i] = A.bsx[i] = A.bsy[i] = 0;
+                A.bssy[i] = A.bsx[i] = 0;
                 A.brmax[i] = -1;
                 A.bcmin[i] = 0x7FFFFFFF;
                 A.bcmax[i] = -1;
@@ -118,16 +120,16 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
             const CclSmem<C>& S = A.c;
             if (iroot) nfg += (int)(((S.x[(S.runpos[i] >> 8) * WPR + ((S.runpos[i] & 0xFF) >> 5)] >> (S.runpos[i] & 31)) & 1u) ^ flip);
             int rr = 0, c0 = 0x7FFFFFFF, cl = -1;
-            uint32_t n = 0, sx = 0, sy = 0;
+            uint32_t nsy = 0, sx = 0;
             if (bi >= 0) {
                 const uint16_t rp = S.runpos[i];
                 const uint16_t nx = (i + 1 < S.nruns) ? S.runpos[i + 1] : 0xFFFF;
                 rr = rp >> 8;
                 c0 = rp & 0xFF;
                 const int c1 = ((nx >> 8) == rr) ? (nx & 0xFF) : tw;
-                n = (uint32_t)(c1 - c0);
+                const uint32_t n = (uint32_t)(c1 - c0);
                 sx = n * (uint32_t)(c0 + c1 - 1) / 2u;
-                sy = n * (uint32_t)rr;
+                nsy = n | ((n * (uint32_t)rr) << 14);
                 cl = c1 - 1;
             }
             const uint32_t valid = __ballot_sync(0xFFFFFFFFu, bi >= 0);
@@ -135,18 +137,16 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
             const int cand = __shfl_sync(0xFFFFFFFFu, bi, __ffs(valid) - 1);
             const uint32_t grp = __ballot_sync(0xFFFFFFFFu, bi == cand);
             if (bi == cand) {
-                n = __reduce_add_sync(grp, n);
+                nsy = __reduce_add_sync(grp, nsy);
                 sx = __reduce_add_sync(grp, sx);
-                sy = __reduce_add_sync(grp, sy);
                 rr = __reduce_max_sync(grp, rr);
                 c0 = __reduce_min_sync(grp, c0);
                 cl = __reduce_max_sync(grp, cl);
                 if ((int)(threadIdx.x & 31) != __ffs(grp) - 1) bi = -1;  // the leader commits the group
             }
             if (bi >= 0) {
-                atomicAdd(&A.bs[bi], n);
+                atomicAdd(&A.bssy[bi], nsy);
                 atomicAdd(&A.bsx[bi], sx);
-                atomicAdd(&A.bsy[bi], sy);
                 atomicMax(&A.brmax[bi], rr);
                 atomicMin(&A.bcmin[bi], c0);
                 atomicMax(&A.bcmax[bi], cl);
@@ -238,10 +238,10 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         const uint32_t node = (uint32_t)g.B + base + (uint32_t)i;
         const uint64_t key = (uint64_t)(tg.y0 + fr) * (uint64_t)g.W + (uint64_t)(tg.x0 + fc);
         Acc f;
-        const int64_t s = A.bs[i];
+        const int64_t s = A.bssy[i] & 0x3FFFu;
         f.s = s;
         f.sx = (int64_t)A.bsx[i] + s * tg.x0;
-        f.sy = (int64_t)A.bsy[i] + s * tg.y0;
+        f.sy = (int64_t)(A.bssy[i] >> 14) + s * tg.y0;
         f.row_min = tg.y0 + fr;
         f.row_max = tg.y0 + A.brmax[i];
         f.col_min = tg.x0 + A.bcmin[i];
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(NT, RL_ANALYZE_MINB) k_analyze(const uint8_t* 
 }
 
 // class M over list A; heavier tiles go to list B
-__global__ void __launch_bounds__(CapM::BT, 3) k_analyze_m(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+__global__ void __launch_bounds__(CapM::BT, 4) k_analyze_m(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& A = *reinterpret_cast<AnalyzeSmem<CapM>*>(smem_raw);
     const uint32_t n = ws.counters[2];
@@ -1127,7 +1127,7 @@ __global__ void __launch_bounds__(NT, 8) k_emit(Geo g, Ws ws) {
     emit_tile(E, g, ws, tile_geom_grid(g));
 }
 
-__global__ void __launch_bounds__(CapME::BT, 3) k_emit_m(Geo g, Ws ws) {
+__global__ void __launch_bounds__(CapME::BT, 4) k_emit_m(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& E = *reinterpret_cast<EmitSmem<CapME>*>(smem_raw);
     const uint32_t n = ws.counters[2];
@@ -1231,7 +1231,7 @@ void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaSt
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
     k_analyze<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
     // deferred heavier tiles: the grids loop over device-side lists (no host sync)
-    k_analyze_m<<<148 * 3, CapM::BT, sizeof(AnalyzeSmem<CapM>), s>>>(pix, g, ws);
+    k_analyze_m<<<148 * 4, CapM::BT, sizeof(AnalyzeSmem<CapM>), s>>>(pix, g, ws);
     k_analyze_full<<<148 * 2, CapF::BT, sizeof(AnalyzeSmem<CapF>), s>>>(pix, g, ws);
 }
 void launch_seam_cols(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
@@ -1284,7 +1284,7 @@ void launch_emit(const Geo& g, const Ws& ws0, cudaStream_t s) {
         ws.ftkey = nullptr;
     }
     k_emit<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(EmitSmem<CapSE>), s>>>(g, ws);
-    k_emit_m<<<148 * 3, CapME::BT, sizeof(EmitSmem<CapME>), s>>>(g, ws);
+    k_emit_m<<<148 * 4, CapME::BT, sizeof(EmitSmem<CapME>), s>>>(g, ws);
     k_emit_full<<<148 * 2, CapFE::BT, sizeof(EmitSmem<CapFE>), s>>>(g, ws);
     if (sharded) k_ftab_flush<<<FT_SHARDS * FT_HS / 256, 256, 0, s>>>(ws);
 }

@@ -62,7 +62,7 @@ struct Cap {
     static constexpr int FCH = FCH_;  // interior-feature accumulator chunk (emit pass)
     using PT = PT_;                   // run-parent type: 32-bit for native atomicMin unions
     static constexpr int BT = BT_;
-    static_assert(BT == NW || (BT == 2 * NW && EVC >= 32 * 32), "wide classes never need event rounds");
+    static_assert(BT == NW || BT == 2 * NW, "one or two threads per word");
 };
 // analyze pass (union-find: 32-bit parents)
 #ifndef RL_S_MR
@@ -72,7 +72,9 @@ struct Cap {
 #define RL_S_NLC 960  // keeps the class-S tables within 8 CTAs per SM
 #endif
 using CapS = Cap<RL_S_MR, NBMAX / 2, 192, 512, uint32_t, NW, RL_S_NLC>;
-using CapM = Cap<MAXRUNS * 5 / 8, NBMAX, 1024, 384, uint32_t, 2 * NW>;
+// M: <= 0.5625 runs/pixel (random g = 1 noise at any density: 0.5), <= 2048 components; sized so
+// that 4 CTAs of 512 threads fit one SM (full occupancy); events are queued in rounds of 512
+using CapM = Cap<MAXRUNS * 9 / 16, NBMAX, 512, 384, uint32_t, 2 * NW, 2048>;
 using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 // emit pass: same classes, no unions (16-bit component map, larger feature chunks)
 #ifndef RL_SE_FCH
@@ -80,9 +82,9 @@ using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 #endif
 using CapSE = Cap<CapS::MR, CapS::NBC, 192, RL_SE_FCH, uint16_t, NW, CapS::NLC>;
 #ifndef RL_ME_FCH
-#define RL_ME_FCH 768  // the largest chunk with 3 CTAs per SM (640: -0.2% cfg2)
+#define RL_ME_FCH 512  // the largest chunk with 4 CTAs per SM
 #endif
-using CapME = Cap<CapM::MR, CapM::NBC, 1024, RL_ME_FCH, uint16_t, 2 * NW>;
+using CapME = Cap<CapM::MR, CapM::NBC, 32, RL_ME_FCH, uint16_t, 2 * NW, CapM::NLC>;
 using CapFE = Cap<CapF::MR, CapF::NBC, 1024, 320, uint16_t, 2 * NW>;
 
 template <class C>
@@ -445,18 +447,23 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
             __syncwarp();
         }
     } else {
-        // one round always suffices (<= 32 events per word); each queue is drained by the
-        // warp that filled it and by its partner warp past NW
-        if (word) {
-            if (nev) put_events(0);
-            if (lane == 0) S.qtot[warp] = wtot;
-        }
+        // each queue is drained by the warp that filled it and by its partner warp past NW, in
+        // rounds of EVC events (a word has <= 32 events: a warp <= 1024)
+        if (word && lane == 0) S.qtot[warp] = wtot;
         __syncthreads();
+        int maxq = 0;
+#pragma unroll
+        for (int q = 0; q < NWARPS; ++q) maxq = max(maxq, S.qtot[q]);
         const int q = warp & (NWARPS - 1);
-        const int cnt = S.qtot[q];
-        for (int k = lane + 32 * (warp / NWARPS); k < cnt; k += 32 * (BT / NW)) resolve_event(S.evq[q][k]);
+        for (int done = 0; done < maxq; done += C::EVC) {
+            if (word && nev && my0 < done + C::EVC && my0 + nev > done) put_events(done);
+            __syncthreads();
+            const int cnt = min(C::EVC, S.qtot[q] - done);
+            for (int k = lane + 32 * (warp / NWARPS); k < cnt; k += 32 * (BT / NW)) resolve_event(S.evq[q][k]);
+            __syncthreads();
+        }
     }
-    if (any_events) __syncthreads();
+    if (any_events && BT == NW) __syncthreads();
     RL_PHASE(tg.t, 4);
 
     // ---- flatten (roots are final now): every run walks to its root; concurrent writes of
