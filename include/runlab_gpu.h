@@ -211,6 +211,9 @@ void rl_cfg4_params(uint64_t i, double* density, int32_t* g);
 
 /* Number of kernel launches the last pipeline enqueued. */
 int rl_last_launch_count(const rl_ctx* ctx);
+/* Device workspace bytes the context holds (all grow-only tables).  For a strip context this
+ * follows the strip's size, not the whole image's. */
+int64_t rl_workspace_bytes(const rl_ctx* ctx);
 /* 1 when the last call replayed a captured CUDA graph (small workloads; disable with the
  * environment variable RUNLAB_GPU_NO_GRAPH).  Phase times of older calls (back > 0) are then
  * not kept. */

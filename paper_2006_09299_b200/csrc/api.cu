@@ -136,17 +136,22 @@ Geo make_geo(int32_t W, int32_t H, int32_t B, const rl_config* cfg, const void* 
     g.ty0 = 0;
     g.ty1 = g.nty;
     g.prow0 = 0;
+    g.cell_end = (int64_t)B * H * g.ntx;
+    g.cid_lo = g.cid_hi = g.cid_extra = 0;
     return g;
 }
 
 int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& tmp, int64_t out_px) {
     const int32_t B = g.B;
-    const int64_t ntiles = g.ntiles;
-    const int64_t ncnt = (int64_t)B * g.H * g.ntx + 1;
+    // tables for the tiles and cells of this call: the whole batch, or the strip's tile rows
+    const int64_t ntiles = (int64_t)(g.ty1 - g.ty0) * g.ntx * B;
+    const int64_t ncnt = g.strip ? (std::min<int64_t>((int64_t)g.ty1 * TH, g.H) - (int64_t)g.ty0 * TH) * g.ntx + 1
+                                 : (int64_t)B * g.H * g.ntx + 1;
+    const int64_t npx = (int64_t)(g.ty1 - g.ty0) * TH * g.W * B;  // pixels covered (rounded up)
     if (ctx->cap_nodes == 0) ctx->cap_nodes = (uint32_t)std::min<int64_t>(std::max<int64_t>(ntiles * 96, 4096), 0xF0000000ll);
     // initial estimate 0.02 components/pixel (random images: 0.003-0.13); grows on demand
-    if (ctx->cap_comps == 0) ctx->cap_comps = (uint64_t)std::max<int64_t>(g.P * B / 48, 4096);
-    if (ctx->cap_rstore == 0) ctx->cap_rstore = (uint64_t)std::max<int64_t>(g.P * B * 3 / 10 + ntiles * 64, 1 << 16);
+    if (ctx->cap_comps == 0) ctx->cap_comps = (uint64_t)std::max<int64_t>(npx / 48, 4096);
+    if (ctx->cap_rstore == 0) ctx->cap_rstore = (uint64_t)std::max<int64_t>(npx * 3 / 10 + ntiles * 64, 1 << 16);
     const uint64_t nn = (uint64_t)B + ctx->cap_nodes;
     bool ok = ensure(ctx->bits, (size_t)ntiles * NW * 4) && ensure(ctx->tbase, (size_t)ntiles * 4) &&
               ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->ovf, (size_t)ntiles * 4) &&
@@ -208,6 +213,22 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
     ws.labels = g.label_mode ? P<uint32_t>(ctx->labels) : nullptr;
     ws.ftsum = P<unsigned long long>(ctx->ftab);
     ws.ftkey = reinterpret_cast<uint32_t*>(ws.ftsum + 3ull * FT_SHARDS * FT_HS);
+    if (g.strip) {
+        // the strip's tables start at its first tile / first cell / first owned id (kernels use
+        // whole-image numbers; only the strip's range is ever accessed through these bases)
+        const int64_t t0 = (int64_t)g.ty0 * g.ntx, c0 = (int64_t)g.ty0 * TH * g.ntx;
+        ws.bits = shift_base(ws.bits, t0 * NW);
+        ws.tbase = shift_base(ws.tbase, t0);
+        ws.tnb = shift_base(ws.tnb, t0);
+        ws.perim = shift_base(ws.perim, t0 * PERIM);
+        ws.thdr = shift_base(ws.thdr, t0 * THDR);
+        ws.tmap = shift_base(ws.tmap, t0);
+        ws.cnt = shift_base(ws.cnt, c0);
+        ws.off = shift_base(ws.off, c0);
+        ws.comps = shift_base(ws.comps, g.cid_lo);
+        ws.top = shift_base(ws.top, g.cid_lo);
+        ws.filled = shift_base(ws.filled, g.cid_lo);
+    }
 
     return RL_OK;
 }
@@ -525,7 +546,31 @@ int fetch(rl_ctx* ctx, rl_result* out) {
 
 }  // namespace rlh
 
+namespace {
+
+// every grow-only device table of a context
+template <class F>
+void for_each_buf(rl_ctx* c, F&& f) {
+    DevBuf* bufs[] = {&c->bits, &c->tbase, &c->tnb, &c->perim, &c->uf, &c->nkey, &c->nmin, &c->nacc,
+                      &c->nrec, &c->nrep, &c->nrootcid, &c->nparent, &c->nanccid, &c->cnt, &c->off,
+                      &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
+                      &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
+                      &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,
+                      &c->fcomp, &c->nleft, &c->scount, &c->ncut, &c->nfold, &c->xnode, &c->gtab, &c->ftab,
+                      &c->pk, &c->pkpar, &c->pkesc, &c->fpk};
+    for (DevBuf* b : bufs) f(*b);
+}
+
+}  // namespace
+
 extern "C" {
+
+int64_t rl_workspace_bytes(const rl_ctx* c) {
+    if (!c) return 0;
+    int64_t n = 0;
+    for_each_buf(const_cast<rl_ctx*>(c), [&](DevBuf& b) { n += (int64_t)b.bytes; });
+    return n;
+}
 
 rl_ctx* rl_create(int device) {
     rl_ctx* c = new (std::nothrow) rl_ctx();
@@ -558,12 +603,7 @@ void rl_destroy(rl_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    DevBuf* bufs[] = {&c->bits, &c->tbase, &c->tnb, &c->perim, &c->uf, &c->nkey, &c->nmin, &c->nacc,
-                      &c->nrec, &c->nrep, &c->nrootcid, &c->nparent, &c->nanccid, &c->cnt, &c->off,
-                      &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
-                      &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
-                      &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,
-                      &c->fcomp, &c->nleft, &c->scount, &c->ncut, &c->xnode, &c->gtab, &c->ftab, &c->pk, &c->pkpar, &c->pkesc, &c->fpk};
+
     for (rl_ctx* k : c->kids) rl_destroy(k);
     strip_free(c);
     pool_free(c);
@@ -573,8 +613,9 @@ void rl_destroy(rl_ctx* c) {
         if (p) cudaFreeHost(p);
     for (uint8_t* p : c->h_istage)
         if (p) cudaFreeHost(p);
-    for (DevBuf* b : bufs)
-        if (b->p) cudaFree(b->p);
+    for_each_buf(c, [](DevBuf& b) {
+        if (b.p) cudaFree(b.p);
+    });
     if (c->h_summ) cudaFreeHost(c->h_summ);
     for (auto& slot : c->ring)
         for (auto& e : slot)

@@ -74,6 +74,13 @@ struct Geo {
     int32_t orowb;       // bytes per row of the hole-filled image
     int32_t ovec_ok;     // vector stores allowed for it
     int64_t ofbytes;     // bytes per image of the hole-filled image
+    // where the tables of this call live.  Kernels index tiles, (image, row, tile column) cells
+    // and components with whole-image numbers; in strip mode the device tables hold only the
+    // strip's part and their base pointers are shifted accordingly (strips.cu), so that a rank's
+    // memory follows its strip, not the image:
+    int64_t cell_end;    // the end cell of the canonical-id offsets (B * H * ntx; strip: its last row's end)
+    int64_t cid_lo, cid_hi;  // strip: canonical ids owned by this strip (component tables hold them)
+    int64_t cid_extra;   // strip: component slots past cid_hi for cut survivors owned elsewhere
 };
 
 struct Ws {
@@ -97,6 +104,7 @@ struct Ws {
     // hash table keyed by the post-fill root's slot; k_ftab_flush folds the table into `filled`
     uint32_t* ftkey;     // [FT_SHARDS * FT_HS] target slot in `filled`, FT_KEY_EMPTY when free
     unsigned long long* ftsum;  // [FT_SHARDS * FT_HS * 3] S, Sx, Sy
+    uint32_t* nfold;     // strip mode: slot in `filled` that a root's hole-fill folds go to (else null)
     uint32_t* ncut;      // strip mode: 1 + global root of the cut class at a cut-class root node,
                          // 0 elsewhere (else null; strips.cu)
     // canonical numbering

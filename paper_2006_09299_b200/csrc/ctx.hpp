@@ -48,6 +48,14 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
+// A table base moved back by n elements, for tables that hold only a window [n, ...) of a
+// numbering the kernels use whole (strip mode).  Integer arithmetic: the moved pointer itself is
+// never dereferenced outside the window.
+template <class T>
+inline T* shift_base(T* p, int64_t n) {
+    return reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) - (uintptr_t)(n * (int64_t)sizeof(T)));
+}
+
 // Everything a captured pipeline depends on (compared bytewise before a replay).
 struct GraphKey {
     Geo g;
@@ -150,7 +158,7 @@ struct rl_ctx {
     cudaStream_t in_stream = nullptr;
     cudaEvent_t in_done = nullptr;
     // strip mode (strips.cu)
-    DevBuf nleft, scount, ncut, xnode, gtab, ftab;
+    DevBuf nleft, scount, ncut, nfold, xnode, gtab, ftab;
     rlh::StripState* strip = nullptr;
 };
 

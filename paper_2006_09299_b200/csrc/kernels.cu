@@ -505,12 +505,20 @@ __global__ void k_reps(Geo g, Ws ws) {
     }
 }
 
-__device__ __forceinline__ uint64_t comp_base(const Geo& g, const Ws& ws, int32_t b) {
-    return (uint64_t)ws.off[(int64_t)b * g.H * g.ntx] + (uint64_t)b;
+// canonical-id offset of image b's first cell (strip mode: 0, the strip's cells are scanned from
+// the components of the strips above, so ids come out whole-image)
+__device__ __forceinline__ uint32_t img_off(const Geo& g, const Ws& ws, int32_t b) {
+    return g.strip ? 0u : ws.off[(int64_t)b * g.H * g.ntx];
 }
 
+__device__ __forceinline__ uint64_t comp_base(const Geo& g, const Ws& ws, int32_t b) {
+    return (uint64_t)img_off(g, ws, b) + (uint64_t)b;
+}
+
+// the component tables hold every id of this call (strip mode: the owned ids plus the cut
+// survivors' scratch slots)
 __device__ __forceinline__ bool comps_fit(const Geo& g, const Ws& ws) {
-    return (uint64_t)ws.off[(int64_t)g.B * g.H * g.ntx] + (uint64_t)g.B <= ws.cap_comps;
+    return (uint64_t)ws.off[g.cell_end] + (uint64_t)g.B - (uint64_t)g.cid_lo + (uint64_t)g.cid_extra <= ws.cap_comps;
 }
 
 // one warp per tile: canonical ids of the tile's border representatives.  The tile's border
@@ -543,14 +551,16 @@ __global__ void k_cids(Geo g, Ws ws) {
     const int lane = threadIdx.x & 31;
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (fit && gid < g.B) {  // exterior records (the exterior survives hole filling)
-        const uint64_t cb = comp_base(g, ws, gid);
-        rl_component c;
-        c.f = ws.nacc[gid];
-        c.parent = 0xFFFFFFFFu;
-        c.flags = 0;
-        ws.comps[cb] = c;
-        ws.top[cb] = 0;
-        ws.filled[cb] = c.f;
+        if (g.cid_lo == 0) {  // strip mode: strip 0 owns id 0 (the others count it, strips.cu)
+            const uint64_t cb = comp_base(g, ws, gid);
+            rl_component c;
+            c.f = ws.nacc[gid];
+            c.parent = 0xFFFFFFFFu;
+            c.flags = 0;
+            ws.comps[cb] = c;
+            ws.top[cb] = 0;
+            ws.filled[cb] = c.f;
+        }
         atomicAdd(&ws.img_surv[gid], 1u);
     }
     const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -562,7 +572,7 @@ __global__ void k_cids(Geo g, Ws ws) {
         const uint32_t nb = ws.tnb[t];
         const uint32_t n0 = (uint32_t)g.B + ws.tbase[t];
         const int64_t img0 = (int64_t)b * g.H * g.ntx;
-        const uint32_t offimg = ws.off[img0];
+        const uint32_t offimg = img_off(g, ws, b);
         const uint64_t cb = (uint64_t)offimg + (uint64_t)b;
         int carry_row = -1, carry = 0, nsurv = 0;
         for (uint32_t i0 = 0; i0 < nb; i0 += 32) {
@@ -636,20 +646,22 @@ __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
             if (ws.ncut && ws.ncut[root]) {
                 anc = ws.nanccid[root];  // strip mode: a class crossing a cut, resolved globally
             } else {
-                uint32_t cur = root;
+                uint32_t cur = root, fold;
                 for (;;) {
                     const uint32_t p = ws.nparent[cur];
                     if (p < (uint32_t)g.B) {
-                        anc = ws.nrootcid[cur];
+                        anc = fold = ws.nrootcid[cur];
                         break;
                     }
                     if (ws.ncut && ws.ncut[p]) {  // strip mode: the chain leaves the strip
                         anc = ws.nanccid[p];
+                        fold = ws.nfold[p];
                         break;
                     }
                     cur = p;
                 }
                 ws.nanccid[root] = anc;
+                if (ws.nfold) ws.nfold[root] = fold;
             }
             int32_t b, ty, tx;
             tile_of(g, ws.nrec[n].tile, b, ty, tx);
@@ -688,9 +700,7 @@ __global__ void __launch_bounds__(256) k_fold(Geo g, Ws ws) {
             const uint32_t root = ws.uf[n];
             const uint32_t anc = ws.nanccid[root];
             if (anc != ws.nrootcid[root]) {
-                int32_t b, ty, tx;
-                tile_of(g, ws.nrec[n].tile, b, ty, tx);
-                dst = (uint32_t)(comp_base(g, ws, b) + anc);  // < 2^32 components
+                dst = ws.nfold[root];  // the survivor's slot (it may be owned by another strip)
                 f = ws.nacc[root];
             }
         }
@@ -804,7 +814,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         E.ext[tid] = 0;
     }
     const int64_t img0 = (int64_t)tg.b * g.H * g.ntx;
-    const uint32_t offimg = ws.off[img0];
+    const uint32_t offimg = img_off(g, ws, tg.b);
     if (tid < TH && tid < tg.th)
         E.rowoff[tid] = ws.off[img0 + (int64_t)(tg.y0 + tid) * g.ntx + tg.tx] - offimg;
     if (tid == 0) {
@@ -997,7 +1007,10 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
                 } else {
                     slot = end >= 0 ? fold_slot(E, (uint32_t)end) : -1;
                     if (slot < 0) {
-                        if (end >= 0) acc_atomic_fold_fill(ws.filled + cb + anc, c.f.s, c.f.sx, c.f.sy);  // table full
+                        if (end >= 0)  // table full
+                            acc_atomic_fold_fill(ws.filled + (ws.nfold ? (uint64_t)ws.nfold[ws.uf[(uint32_t)g.B + ws.tbase[tg.t] + end]]
+                                                                       : cb + anc),
+                                                 c.f.s, c.f.sx, c.f.sy);
                         else E.dfold[atomicAdd(&E.ndfold, 1)] = (uint16_t)lc;
                     }
                 }
@@ -1038,7 +1051,9 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     for (int i = tid; i < FOLD_SLOTS; i += BT) {
         if (E.pkey[i] == 0xFFFF || !E.ps[i]) continue;
         const int64_t s = E.ps[i];
-        const uint32_t key = (uint32_t)(cb + E.banc[E.pkey[i]]);
+        // strip mode: the survivor's slot in `filled` (it may be owned by another strip)
+        const uint32_t key = ws.nfold ? ws.nfold[ws.uf[(uint32_t)g.B + ws.tbase[tg.t] + E.pkey[i]]]
+                                      : (uint32_t)(cb + E.banc[E.pkey[i]]);
         const int64_t sx = (int64_t)E.psx[i] + s * tg.x0, sy = (int64_t)E.psy[i] + s * tg.y0;
         const uint32_t base = (uint32_t)(tg.t % FT_SHARDS) * FT_HS;
         uint32_t h = (key * 2654435761u) >> (32 - 13);

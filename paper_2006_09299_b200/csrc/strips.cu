@@ -85,7 +85,7 @@ XLayout x_layout(int32_t W, int64_t max_classes) {
 
 // global cut-class tables (identical on every rank), laid out in ctx->gtab
 struct GTab {
-    uint32_t *uf, *root, *rep, *cid, *anc, *coff, *scnt, *gsurv;
+    uint32_t *uf, *root, *rep, *cid, *anc, *ancslot, *coff, *scnt, *gsurv;
     uint64_t* kmin;
     Acc* tot;
     int64_t *links, *psum, *pcnt;
@@ -114,6 +114,7 @@ GTab g_layout(void* base, int64_t C, int k) {
     T.rep = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
     T.cid = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
     T.anc = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
+    T.ancslot = reinterpret_cast<uint32_t*>(take((size_t)C * 4));
     T.coff = reinterpret_cast<uint32_t*>(take((size_t)(k + 1) * 4));
     T.scnt = reinterpret_cast<uint32_t*>(take((size_t)2 * k * 4));
     T.gsurv = reinterpret_cast<uint32_t*>(take(8));
@@ -355,9 +356,11 @@ __global__ void k_g_reflatten(Ws ws) {
     }
 }
 
-__global__ void k_strip_offsets(Ws ws, int64_t c_lo, int64_t c_hi, int64_t ncnt) {
-    ws.off[ncnt - 1] = ws.off[c_hi];
-    ws.off[0] = 0;  // strip 0: c_lo == 0, already 0
+// slot in this strip's `filled` of GCC survivor e: its own id when this strip owns it, else one
+// of the scratch slots past the owned range (where this strip's partial post-fill sums gather)
+__device__ __forceinline__ uint32_t gcc_slot(const GTab& T, const Geo& g, uint32_t e) {
+    const uint32_t cid = T.cid[e];
+    return ((int64_t)cid >= g.cid_lo && (int64_t)cid < g.cid_hi) ? cid : (uint32_t)g.cid_hi + e;
 }
 
 // owned GCCs: canonical id and where the parent chain leaves this strip.  links[2 root] = id,
@@ -393,7 +396,7 @@ __global__ void k_g_links(Ws ws, GTab T, const uint32_t* xnode, int64_t ncls, ui
 
 // every GCC's id and depth-1 ancestor (walk of the GCC links); survivors' post-fill slots start
 // empty on every rank (they collect this rank's folds)
-__global__ void k_g_anc(Ws ws, GTab T, int64_t C) {
+__global__ void k_g_anc(Geo g, Ws ws, GTab T, int64_t C) {
     uint32_t ns = 0;
     GRID_LOOP(i, C) {
         if (i == 0 || T.root[i] != (uint32_t)i) continue;
@@ -401,7 +404,7 @@ __global__ void k_g_anc(Ws ws, GTab T, int64_t C) {
         uint32_t e = (uint32_t)i, anc = 0;
         for (int64_t it = 0; it < C; ++it) {
             const int64_t l = T.links[2 * e + 1];
-            if (l > 0) {
+            if (l > 0) {  // e is a child of the exterior: the depth-1 ancestor (l is its id)
                 anc = (uint32_t)l;
                 break;
             }
@@ -411,16 +414,22 @@ __global__ void k_g_anc(Ws ws, GTab T, int64_t C) {
         if (!anc || !cid) atomicOr(&ws.counters[1], ERR_INTERNAL);
         T.cid[i] = cid;
         T.anc[i] = anc;
-        if (anc == cid && cid) {
-            ws.filled[cid] = acc_empty();
-            ++ns;
-        }
+        T.ancslot[i] = e;
+        if (anc == cid && cid) ++ns;
     }
     ns = __reduce_add_sync(0xFFFFFFFFu, ns);
     if ((threadIdx.x & 31) == 0 && ns) atomicAdd(T.gsurv, ns);
 }
 
-__global__ void k_g_own(Ws ws, GTab T, const uint32_t* xnode, int64_t ncls, uint32_t c0) {
+// survivors' post-fill slots start empty on every rank (they collect this rank's folds)
+__global__ void k_g_surv_init(Geo g, Ws ws, GTab T, int64_t C) {
+    GRID_LOOP(i, C) {
+        if (i == 0 || T.root[i] != (uint32_t)i || T.anc[i] != T.cid[i]) continue;
+        ws.filled[gcc_slot(T, g, (uint32_t)i)] = acc_empty();
+    }
+}
+
+__global__ void k_g_own(Geo g, Ws ws, GTab T, const uint32_t* xnode, int64_t ncls, uint32_t c0) {
     GRID_LOOP(c, ncls + 1) {
         if (c == 0) continue;
         const uint32_t root = T.root[c0 + (uint32_t)c];
@@ -428,14 +437,16 @@ __global__ void k_g_own(Ws ws, GTab T, const uint32_t* xnode, int64_t ncls, uint
         const uint32_t n = xnode[c];
         ws.nrootcid[n] = T.cid[root];
         ws.nanccid[n] = T.anc[root];
+        ws.nfold[n] = gcc_slot(T, g, T.ancslot[root]);
     }
 }
 
 // this rank's partial post-fill sums of the GCC survivors (neutral elsewhere), indexed by GCC root
-__global__ void k_g_partials(Ws ws, GTab T, int64_t C, const uint32_t* surv_a, const uint32_t* surv_b, int32_t sub) {
+__global__ void k_g_partials(Geo g, Ws ws, GTab T, int64_t C, const uint32_t* surv_a, const uint32_t* surv_b,
+                             int32_t sub) {
     GRID_LOOP(i, C) {
         Acc f = acc_empty();
-        if (i > 0 && T.root[i] == (uint32_t)i && T.anc[i] == T.cid[i]) f = ws.filled[T.cid[i]];
+        if (i > 0 && T.root[i] == (uint32_t)i && T.anc[i] == T.cid[i]) f = ws.filled[gcc_slot(T, g, (uint32_t)i)];
         T.psum[3 * i] = f.s;
         T.psum[3 * i + 1] = f.sx;
         T.psum[3 * i + 2] = f.sy;
@@ -448,7 +459,7 @@ __global__ void k_g_partials(Ws ws, GTab T, int64_t C, const uint32_t* surv_a, c
     if (blockIdx.x == 0 && threadIdx.x == 0) *T.pcnt = (int64_t)*surv_a + (int64_t)*surv_b - sub;
 }
 
-__global__ void k_g_finish(Ws ws, GTab T, int64_t C) {
+__global__ void k_g_finish(Geo g, Ws ws, GTab T, int64_t C) {
     GRID_LOOP(i, C) {
         if (i == 0 || T.root[i] != (uint32_t)i || T.anc[i] != T.cid[i]) continue;
         const Acc a = T.tot[i];
@@ -460,7 +471,7 @@ __global__ void k_g_finish(Ws ws, GTab T, int64_t C) {
         f.col_min = min(T.pmin[2 * i + 1], a.col_min);
         f.row_max = max(T.pmax[2 * i], a.row_max);
         f.col_max = max(T.pmax[2 * i + 1], a.col_max);
-        ws.filled[T.cid[i]] = f;
+        ws.filled[gcc_slot(T, g, (uint32_t)i)] = f;  // kept (fetched) where owned
     }
 }
 
@@ -548,6 +559,7 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
     g.ty1 = (y0 + h + TH - 1) / TH;
     g.prow0 = y0;
     g.strip = 1;
+    g.cell_end = std::min<int64_t>((int64_t)g.ty1 * TH, H) * g.ntx;  // the strip's end cell
     S->g = g;
     S->cfg = *cfg;
     S->y0 = y0;
@@ -562,7 +574,8 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         size_t tmp = 0;
         if ((rc = prepare_ws(ctx, g, cfg, ws, tmp, (int64_t)h * w))) return rc;
         const size_t nn = (size_t)ctx->cap_nodes + 1;
-        if (!ensure(ctx->nleft, nn * 4) || !ensure(ctx->ncut, nn * 4) || !ensure(ctx->flag, nn * 4) ||
+        if (!ensure(ctx->nleft, nn * 4) || !ensure(ctx->ncut, nn * 4) || !ensure(ctx->nfold, nn * 4) ||
+            !ensure(ctx->flag, nn * 4) ||
             !ensure(ctx->rank, nn * 4) || !ensure(ctx->xnode, nn * 4) || !ensure(ctx->scount, 64))
             return set_err(ctx, RL_ENOMEM, "device allocation failed");
         size_t tmp3 = 0;
@@ -570,6 +583,7 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         if (!ensure(ctx->cub_tmp, std::max(tmp, tmp3))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
         ws.nleft = P<uint32_t>(ctx->nleft);
         ws.ncut = P<uint32_t>(ctx->ncut);
+        ws.nfold = P<uint32_t>(ctx->nfold);
         cudaMemsetAsync(ws.counters, 0, 64, s);
         cudaMemsetAsync(ws.rused, 0, 8, s);
         cudaMemsetAsync(ws.img_fg, 0, 4, s);
@@ -717,19 +731,25 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     S->fg = fg;
     S->comp_lo = me == 0 ? 0 : 1 + off_me;
     S->comp_hi = 1 + off_me + infos[me].n_comps + sc[me];
-    // ---- this strip's numbering with the GCC status applied (ids index the whole image)
-    if (ctx->cap_comps < (uint64_t)total) ctx->cap_comps = (uint64_t)total + (uint64_t)total / 8 + 1024;
+    // ---- this strip's numbering with the GCC status applied (ids index the whole image; the
+    // component tables hold the owned ids [comp_lo, comp_hi) and one scratch slot per cut class)
+    g.cid_lo = S->comp_lo;
+    g.cid_hi = S->comp_hi;
+    g.cid_extra = C;
+    S->g = g;
+    const uint64_t need = (uint64_t)(S->comp_hi - S->comp_lo) + (uint64_t)C;
+    if (ctx->cap_comps < need) ctx->cap_comps = need + need / 8 + 1024;
     Ws ws;
     size_t tmp = 0;
     if ((rc = prepare_ws(ctx, g, &S->cfg, ws, tmp, (int64_t)S->h * g.W))) return rc;
     ws.nleft = P<uint32_t>(ctx->nleft);
     ws.ncut = P<uint32_t>(ctx->ncut);
+    ws.nfold = P<uint32_t>(ctx->nfold);
     const uint32_t* xnode = P<uint32_t>(ctx->xnode);
     k_g_apply<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0);
     STRIP_STEP(ctx, "k_g_apply");
     k_g_reflatten<<<grid(S->n_local, ctx->sms), 256, 0, s>>>(ws);
     STRIP_STEP(ctx, "k_g_reflatten");
-    const int64_t ncnt = (int64_t)g.H * g.ntx + 1;
     cudaMemsetAsync(ws.img_surv, 0, 4, s);
     launch_reps(g, ws, s, ctx->sms, S->n_local);
     STRIP_STEP(ctx, "launch_reps");
@@ -743,8 +763,6 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     tscan = ctx->cub_tmp.bytes;
     cub::DeviceScan::ExclusiveScan(ctx->cub_tmp.p, tscan, ws.cnt + c_lo, ws.off + c_lo, cub::Sum(), (uint32_t)off_me,
                                    (int)(c_hi - c_lo + 1), s);
-    k_strip_offsets<<<1, 1, 0, s>>>(ws, c_lo, c_hi, ncnt);
-    STRIP_STEP(ctx, "k_strip_offsets");
     launch_cids(g, ws, s, ctx->sms);
     STRIP_STEP(ctx, "launch_cids");
     k_g_links<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0,
@@ -756,7 +774,7 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     if (err & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip links)");
     ctx->ws = ws;
     ctx->geo = g;
-    ctx->launches += 4 + (n_strips - 1) + 7;
+    ctx->launches += 4 + (n_strips - 1) + 6;
     out->d_links = T.links;
     out->n = 2 * C;
     S->phase = 3;
@@ -773,9 +791,11 @@ int rl_strip_resolve(rl_ctx* ctx, rl_strip_partials* out) {
     const Geo& g = S->g;
     GTab T = gtab(ctx);
     const int64_t C = S->C;
-    k_g_anc<<<grid(C, ctx->sms), 256, 0, s>>>(ws, T, C);
+    k_g_anc<<<grid(C, ctx->sms), 256, 0, s>>>(g, ws, T, C);
     STRIP_STEP(ctx, "k_g_anc");
-    k_g_own<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, P<uint32_t>(ctx->xnode), S->n_classes, S->c0);
+    k_g_surv_init<<<grid(C, ctx->sms), 256, 0, s>>>(g, ws, T, C);
+    STRIP_STEP(ctx, "k_g_surv_init");
+    k_g_own<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(g, ws, T, P<uint32_t>(ctx->xnode), S->n_classes, S->c0);
     STRIP_STEP(ctx, "k_g_own");
     launch_tree_parts(g, ws, s, ctx->sms, S->n_local);  // post-fill roots (no fold yet)
     STRIP_STEP(ctx, "launch_tree_parts");
@@ -788,14 +808,14 @@ int rl_strip_resolve(rl_ctx* ctx, rl_strip_partials* out) {
     STRIP_STEP(ctx, "launch_emit");
     launch_fold(g, ws, s, ctx->sms, S->n_local);  // border non-survivors of this strip
     STRIP_STEP(ctx, "launch_fold");
-    k_g_partials<<<grid(C, ctx->sms), 256, 0, s>>>(ws, T, C, ws.img_surv, isurv, S->rank > 0 ? 1 : 0);
+    k_g_partials<<<grid(C, ctx->sms), 256, 0, s>>>(g, ws, T, C, ws.img_surv, isurv, S->rank > 0 ? 1 : 0);
     STRIP_STEP(ctx, "k_g_partials");
     uint32_t err = 0;
     cudaMemcpyAsync(&err, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
     const int rc = sync_err(ctx, "strip resolve");
     if (rc) return rc;
     if (err & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip tree)");
-    ctx->launches += 2 + 1 + 3 + (g.tpi >= 8192 ? 1 : 0) + 1 + 1;
+    ctx->launches += 3 + 1 + 3 + (g.tpi >= 8192 ? 1 : 0) + 1 + 1;
     out->d_sum = T.psum;
     out->d_min = T.pmin;
     out->d_max = T.pmax;
@@ -812,7 +832,7 @@ int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out) {
     cudaSetDevice(ctx->device);
     cudaStream_t s = ctx->stream;
     GTab T = gtab(ctx);
-    k_g_finish<<<grid(S->C, ctx->sms), 256, 0, s>>>(ctx->ws, T, S->C);
+    k_g_finish<<<grid(S->C, ctx->sms), 256, 0, s>>>(S->g, ctx->ws, T, S->C);
     STRIP_STEP(ctx, "k_g_finish");
     ctx->launches += 1;
     int64_t surv = 0;

@@ -292,6 +292,10 @@ class Labeler:
     def stream(self) -> int:
         return int(self._L.rl_stream(self._ctx) or 0)
 
+    def workspace_bytes(self) -> int:
+        """Device bytes held by this context's grow-only tables."""
+        return int(self._L.rl_workspace_bytes(self._ctx))
+
     def launch_count(self) -> int:
         return int(self._L.rl_last_launch_count(self._ctx))
 

@@ -146,3 +146,26 @@ def test_strips_poisoned_workspace(labeler):
         del os.environ["RUNLAB_GPU_POISON"]
         for lab in labs:
             lab.close()
+
+
+def test_strip_workspace_follows_the_strip(labeler):
+    """A strip context's device tables are sized by its strip: tile tables, cells,
+    nodes and component tables hold the strip's share, not the whole image's."""
+    W = H = 8192
+    img = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    generate_device(img.data_ptr(), W, H, 0.45, 4, 5)
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    whole = Labeler(0)
+    labs = [Labeler(0) for _ in range(8)]
+    try:
+        whole.label_device(img.data_ptr(), W, H, 1, cfg)
+        ref = whole.fetch()
+        full = whole.workspace_bytes()
+        got = _run(labs, img, W, H, 8, cfg)
+        _compare(got, ref, "8192^2 in 8 strips")
+        per = [lab.workspace_bytes() for lab in labs]
+        assert max(per) < 0.3 * full, (per, full)
+    finally:
+        whole.close()
+        for lab in labs:
+            lab.close()
