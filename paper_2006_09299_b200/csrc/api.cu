@@ -250,6 +250,18 @@ void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
 int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg, int32_t fmt) {
     Geo g = make_geo(W, H, B, cfg, dpix, fmt);
     if (ctx->force_ofmt >= 0) set_output_format(g, ctx->force_ofmt);
+    if (ctx->permute) {  // testing aid: a multiplier coprime to the tile count
+        int64_t m = ctx->permute % std::max<int64_t>(g.ntiles, 1), a, b;
+        for (;; ++m) {
+            for (a = m, b = g.ntiles; b;) {
+                const int64_t t = a % b;
+                a = b;
+                b = t;
+            }
+            if (a == 1 || g.ntiles <= 1) break;
+        }
+        g.permute = g.ntiles > 1 ? m : 0;
+    }
     if (g.ntiles < 0) return set_err(ctx, RL_EINVAL, "too many tiles");
     const int64_t ncnt = (int64_t)B * H * g.ntx + 1;
     Ws ws;
@@ -589,6 +601,7 @@ rl_ctx* rl_create(int device) {
     }
     c->stream = c->own_stream;
     if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
+    if (const char* v = std::getenv("RUNLAB_GPU_PERMUTE")) c->permute = std::max(0ll, std::atoll(v));
     if (std::getenv("RUNLAB_GPU_KTIMES")) c->ktimes = true;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_D2H")) c->packed_d2h = false;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_RECORDS")) c->packed_recs = false;

@@ -81,6 +81,10 @@ struct Geo {
     int64_t cell_end;    // the end cell of the canonical-id offsets (B * H * ntx; strip: its last row's end)
     int64_t cid_lo, cid_hi;  // strip: canonical ids owned by this strip (component tables hold them)
     int64_t cid_extra;   // strip: component slots past cid_hi for cut survivors owned elsewhere
+    // testing aid (env RUNLAB_GPU_PERMUTE): the (ntx, rows, B) grid's CTAs take their tiles in a
+    // permuted order (CTA k -> tile (k * permute) mod tiles, permute coprime to the tile count),
+    // so the lock-free unions see other completion orders; 0 = identity
+    int64_t permute;
 };
 
 struct Ws {
@@ -160,6 +164,14 @@ __device__ __forceinline__ TileGeom tile_geom_grid(const Geo& g) {
     tg.tx = blockIdx.x;
     tg.ty = blockIdx.y + g.ty0;
     tg.b = blockIdx.z;
+    if (g.permute) {
+        const int64_t rows = g.ty1 - g.ty0, n = (int64_t)g.ntx * rows * g.B;
+        const int64_t k = ((int64_t)blockIdx.z * rows + blockIdx.y) * g.ntx + blockIdx.x;
+        const int64_t p = (k * g.permute) % n;
+        tg.tx = (int32_t)(p % g.ntx);
+        tg.ty = (int32_t)((p / g.ntx) % rows) + g.ty0;
+        tg.b = (int32_t)(p / (g.ntx * rows));
+    }
     tg.t = (tg.b * g.nty + tg.ty) * g.ntx + tg.tx;
     tg.x0 = tg.tx * TW;
     tg.y0 = tg.ty * TH;

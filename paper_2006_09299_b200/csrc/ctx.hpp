@@ -111,6 +111,7 @@ struct rl_ctx {
     bool reran = false;  // finish() had to grow a capacity and re-run
     // CUDA graph of the last small pipeline
     bool graphs = true;
+    int64_t permute = 0;  // env RUNLAB_GPU_PERMUTE (testing aid, Geo::permute)
     bool used_graph = false;
     cudaGraphExec_t gexec = nullptr;
     GraphKey gkey{};

@@ -69,3 +69,29 @@ def test_parse_error_offset(cli, tmp_path):
     bad.write_bytes(b"P4\n9 2\n\x80\xff")
     r = subprocess.run([cli, "euler", str(bad)], capture_output=True)
     assert r.returncode == 1 and b"truncated P4 raster (byte 9)" in r.stderr
+
+
+def test_bench_sweep_csv(cli, tmp_path):
+    """runlab bench (tools/runlab.cpp:245-275, bench.hpp:89-207): same sweep, variants, rows and
+    CSV columns; step times are the device phases."""
+    out = tmp_path / "b.csv"
+    run(cli, "bench", "--size", "256", "--densities", "0.2:0.5:0.3", "--granularities", "1,4", "--seeds", "2",
+        "--iters", "2", "--clock-ghz", "2.0", "-o", str(out))
+    rows = out.read_text().strip().split("\n")
+    assert rows[0] == "d,g,config,step,min_ns_px,med_ns_px,max_ns_px,min_cpp,med_cpp,max_cpp"
+    body = [r.split(",") for r in rows[1:]]
+    # per cell: base encode/unify/closure/total, then euler/fill/features (total, extra) and
+    # relabel (relabel, total, extra)
+    assert len(body) == 2 * 2 * 13
+    assert [b[2] + ":" + b[3] for b in body[:13]] == [
+        "base:encode", "base:unify", "base:closure", "base:total", "euler:total", "euler:extra", "fill:total",
+        "fill:extra", "features:total", "features:extra", "relabel:relabel", "relabel:total", "relabel:extra"]
+    assert {(b[0], b[1]) for b in body} == {("0.2", "1"), ("0.2", "4"), ("0.5", "1"), ("0.5", "4")}
+    for b in body:
+        mn, md, mx = float(b[4]), float(b[5]), float(b[6])
+        assert mn <= md <= mx
+        if b[3] != "extra":
+            assert mn > 0 and abs(float(b[8]) - 2.0 * md) < 1e-3 * max(1.0, md)
+    txt = run(cli, "bench", "--size", "64", "--densities", "0.5", "--granularities", "2", "--seeds", "1",
+              "--iters", "1", "--no-euler", "--no-fill", "--no-features", "--no-relabel").decode()
+    assert len(txt.strip().split("\n")) == 1 + 4 and txt.strip().endswith(",,,")

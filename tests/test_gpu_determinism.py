@@ -1,0 +1,64 @@
+"""Stress of the lock-free union-find: the tile passes unite with atomicMin
+and path halving whose interleaving depends on which CTAs run when.  The result must not:
+
+* the same batch labeled repeatedly on one context gives identical bytes every time;
+* contexts whose tile grid takes the tiles in permuted orders (RUNLAB_GPU_PERMUTE: CTA k gets
+  tile k * m mod n) give the same bytes, and they equal the oracle.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2006_09299_b200 import Labeler, LabelingConfig
+from tests.parity_util import compare_image
+
+pytestmark = pytest.mark.gpu
+
+CELLS = [(0.3, 1), (0.45, 1), (0.5, 1), (0.6, 1), (0.75, 1), (0.45, 2), (0.55, 2), (0.45, 4), (0.6, 4),
+         (0.5, 8), (0.05, 1), (0.95, 1)]
+CFG = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True, relabel=True)
+
+
+@pytest.fixture(scope="module")
+def batch():
+    return np.stack([O.generate(1024, 768, d, g, 17 + i) for i, (d, g) in enumerate(CELLS)])
+
+
+def _digest(res) -> str:
+    h = hashlib.sha256()
+    for a in (res.n_components, res.n_fg, res.n_survivors, res.comp_offset, res.comps, res.top,
+              res.filled_image, res.labels):
+        h.update(np.ascontiguousarray(a).tobytes())
+    surv = res.top == np.concatenate([np.arange(res.comp_offset[i + 1] - res.comp_offset[i], dtype=np.uint32)
+                                      for i in range(len(res.n_components))])
+    h.update(res.filled[surv].tobytes())
+    return h.hexdigest()
+
+
+def test_repeated_runs_identical(labeler, batch):
+    first = _digest(labeler.label_batch(batch, CFG))
+    for _ in range(7):
+        assert _digest(labeler.label_batch(batch, CFG)) == first
+
+
+@pytest.mark.parametrize("perm", [7, 101, 997])
+def test_permuted_tile_order_identical(labeler, batch, perm):
+    want = labeler.label_batch(batch, CFG)
+    os.environ["RUNLAB_GPU_PERMUTE"] = str(perm)
+    try:
+        lab = Labeler(0)
+    finally:
+        del os.environ["RUNLAB_GPU_PERMUTE"]
+    try:
+        got = lab.label_batch(batch, CFG)
+    finally:
+        lab.close()
+    assert _digest(got) == _digest(want)
+    if perm == 7:
+        for i in range(batch.shape[0]):
+            compare_image(got.image(i), O.label_canonical(batch[i], 0), f"perm {perm} #{i}")

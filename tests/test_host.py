@@ -93,10 +93,10 @@ def test_analysis_projections_host_side():
 
 
 def test_cpp_dropin_header_compiles():
-    out = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"),
-                          os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp")],
-                         capture_output=True, text=True)
-    assert out.returncode == 0, out.stderr
+    for src in (os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp"), os.path.join(ROOT, "tools", "runlab_gpu.cpp")):
+        out = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"), src],
+                             capture_output=True, text=True)
+        assert out.returncode == 0, out.stderr
 
 
 def test_shard_range():

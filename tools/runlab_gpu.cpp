@@ -1,7 +1,7 @@
 // runlab_gpu -- the reference CLI's subcommands (tools/runlab.cpp:57-275: label, tree, euler,
-// fill, gen) over the B200 drop-in (include/runlab_gpu.hpp, include/runlab_gpu_io.hpp), with a
-// small hand-written argument parser (CLI11 is not available).  The benchmark sweep lives in
-// bench.py.
+// fill, gen, bench) over the B200 drop-in (include/runlab_gpu.hpp, include/runlab_gpu_io.hpp,
+// include/runlab_gpu_bench.hpp), with a small hand-written argument parser (CLI11 is not
+// available).
 //
 //   runlab_gpu label IN.pbm [-o OUT.pgm|OUT.csv] [--features-csv F.csv] [--features]
 //                    [--relabel] [--densify] [--fill] [--connectivity fg8bg4|fg4bg8]
@@ -10,12 +10,17 @@
 //   runlab_gpu fill IN.pbm OUT.pbm [--format p4|p1] [--connectivity ...]
 //   runlab_gpu gen OUT.pbm --size N | --width W --height H [--density D] [--granularity G]
 //                    [--seed S] [--format p4|p1]
+//   runlab_gpu bench [--size N] [--densities A:B:STEP|D1,D2,..] [--granularities G1,G2,..]
+//                    [--seeds K] [--seed S] [--warmup W] [--iters I] [--clock-ghz F] [-o OUT.csv]
+//                    [--no-euler] [--no-fill] [--no-features] [--no-relabel] [--connectivity ...]
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
 
+#include "runlab_gpu_bench.hpp"
 #include "runlab_gpu_io.hpp"
 
 using namespace runlab;
@@ -29,7 +34,7 @@ struct Args {
 };
 
 [[noreturn]] void usage(const char* msg) {
-    std::fprintf(stderr, "runlab_gpu: %s\nsubcommands: label tree euler fill gen (see tools/runlab_gpu.cpp)\n", msg);
+    std::fprintf(stderr, "runlab_gpu: %s\nsubcommands: label tree euler fill gen bench (see tools/runlab_gpu.cpp)\n", msg);
     std::exit(2);
 }
 
@@ -150,6 +155,55 @@ int cmd_gen(const Args& a) {
     return 0;
 }
 
+// tools/runlab.cpp:33-55: "start:stop:step" (inclusive, the step accumulated as the reference's
+// CLI does) or a comma list; every value in [0, 1]
+std::vector<double> parse_densities(const std::string& text) {
+    std::vector<double> out;
+    if (text.find(':') != std::string::npos) {
+        double a = 0, b = 0, step = 0;
+        if (std::sscanf(text.c_str(), "%lf:%lf:%lf", &a, &b, &step) != 3 || step <= 0)
+            usage("--densities: expected start:stop:step");
+        for (double d = a; d <= b + 1e-9; d += step) out.push_back(std::min(d, 1.0));
+    } else {
+        for (std::size_t pos = 0; pos <= text.size();) {
+            const std::size_t comma = std::min(text.find(',', pos), text.size());
+            out.push_back(std::atof(text.substr(pos, comma - pos).c_str()));
+            pos = comma + 1;
+        }
+    }
+    for (const double d : out)
+        if (d < 0 || d > 1) usage("--densities: values must be in [0, 1]");
+    return out;
+}
+
+// tools/runlab.cpp:158-172 + 245-275: the sweep as a CSV report
+int cmd_bench(const Args& a) {
+    if (!a.pos.empty()) usage("bench: no positional arguments");
+    auto num = [&](const char* k, const char* d) { return a.opt.count(k) ? a.opt.at(k) : std::string(d); };
+    BenchSpec spec;
+    spec.width = spec.height = std::atoi(num("--size", "2048").c_str());
+    spec.densities = parse_densities(num("--densities", "0:1:0.05"));
+    const std::string gl = num("--granularities", "1,2,4,8,16");
+    for (std::size_t pos = 0; pos <= gl.size();) {
+        const std::size_t comma = std::min(gl.find(',', pos), gl.size());
+        spec.granularities.push_back(std::atoi(gl.substr(pos, comma - pos).c_str()));
+        pos = comma + 1;
+    }
+    spec.seeds = std::atoi(num("--seeds", "5").c_str());
+    spec.base_seed = std::strtoull(num("--seed", "1").c_str(), nullptr, 10);
+    spec.warmup = std::atoi(num("--warmup", "1").c_str());
+    spec.iterations = std::atoi(num("--iters", "3").c_str());
+    spec.clock_ghz = std::atof(num("--clock-ghz", "0").c_str());
+    spec.report_cpp = spec.clock_ghz > 0;
+    spec.connectivity = conn_of(a);
+    spec.measure_euler = !a.flag.count("--no-euler");
+    spec.measure_fill = !a.flag.count("--no-fill");
+    spec.measure_features = !a.flag.count("--no-features");
+    spec.measure_relabel = !a.flag.count("--no-relabel");
+    emit(a.opt.count("--output") ? a.opt.at("--output") : "", export_csv(run(spec)));
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -162,6 +216,10 @@ int main(int argc, char** argv) {
         if (cmd == "tree") return cmd_tree(parse(argc, argv, {"--fill"}, {"--output", "--format", "--connectivity"}));
         if (cmd == "euler") return cmd_euler(parse(argc, argv, {}, {"--connectivity"}));
         if (cmd == "fill") return cmd_fill(parse(argc, argv, {}, {"--format", "--connectivity"}));
+        if (cmd == "bench")
+            return cmd_bench(parse(argc, argv, {"--no-euler", "--no-fill", "--no-features", "--no-relabel"},
+                                   {"--size", "--densities", "--granularities", "--seeds", "--seed", "--warmup",
+                                    "--iters", "--clock-ghz", "--output", "--connectivity"}));
         if (cmd == "gen")
             return cmd_gen(parse(argc, argv, {},
                                  {"--size", "--width", "--height", "--density", "--granularity", "--seed", "--format"}));
