@@ -160,7 +160,7 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
               ensure(ctx->rused, 64) && ensure(ctx->perim, (size_t)ntiles * PERIM * 2) &&
               ensure(ctx->uf, nn * 4) && ensure(ctx->nkey, nn * 8) && ensure(ctx->nmin, nn * 8) &&
               ensure(ctx->nacc, nn * sizeof(Acc)) && ensure(ctx->nrec, nn * sizeof(NodeRec)) &&
-              ensure(ctx->nrep, nn) && ensure(ctx->nrootcid, nn * 4) && ensure(ctx->nparent, nn * 4) &&
+              ensure(ctx->nrep, nn) && ensure(ctx->ninfo, nn * 8) && ensure(ctx->nrootcid, nn * 4) && ensure(ctx->nparent, nn * 4) &&
               ensure(ctx->nanccid, nn * 4) && ensure(ctx->cnt, (size_t)ncnt * 4) &&
               ensure(ctx->off, (size_t)ncnt * 4) && ensure(ctx->counters, 64) &&
               ensure(ctx->img_fg, (size_t)B * 4) && ensure(ctx->img_surv, (size_t)B * 4) &&
@@ -196,6 +196,7 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
     ws.nacc = P<Acc>(ctx->nacc);
     ws.nrec = P<NodeRec>(ctx->nrec);
     ws.nrep = P<uint8_t>(ctx->nrep);
+    ws.ninfo = P<uint2>(ctx->ninfo);
     ws.nrootcid = P<uint32_t>(ctx->nrootcid);
     ws.nparent = P<uint32_t>(ctx->nparent);
     ws.nanccid = P<uint32_t>(ctx->nanccid);
@@ -564,7 +565,7 @@ namespace {
 template <class F>
 void for_each_buf(rl_ctx* c, F&& f) {
     DevBuf* bufs[] = {&c->bits, &c->tbase, &c->tnb, &c->perim, &c->uf, &c->nkey, &c->nmin, &c->nacc,
-                      &c->nrec, &c->nrep, &c->nrootcid, &c->nparent, &c->nanccid, &c->cnt, &c->off,
+                      &c->nrec, &c->nrep, &c->ninfo, &c->nrootcid, &c->nparent, &c->nanccid, &c->cnt, &c->off,
                       &c->counters, &c->img_fg, &c->img_surv, &c->comps, &c->top, &c->filled,
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
                       &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,

@@ -99,7 +99,10 @@ struct Ws {
     uint64_t* nmin;      // min key over the class (valid at roots)
     Acc* nacc;           // own features, then class features at roots
     NodeRec* nrec;
-    uint8_t* nrep;       // node holds its component's first pixel
+    uint8_t* nrep;       // bit 0: node holds its component's first pixel; bit 1 (from k_tops on):
+                         // its component is the exterior
+    uint2* ninfo;        // per node, from k_tops on: canonical id of its component, of its
+                         // post-fill root (what the emit pass needs of a tile's border components)
     uint32_t* nrootcid;  // canonical id (valid at roots)
     uint32_t* nparent;   // root node of the surrounding component (valid at roots)
     uint32_t* nanccid;   // canonical id of the post-fill root (valid at roots)

@@ -92,7 +92,7 @@ struct rl_ctx {
     cudaEvent_t ring[RING][NEV] = {};
     int64_t calls = 0;
     // workspace
-    DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, nrootcid, nparent, nanccid;
+    DevBuf bits, tbase, tnb, perim, uf, nkey, nmin, nacc, nrec, nrep, ninfo, nrootcid, nparent, nanccid;
     DevBuf cnt, off, counters, img_fg, img_surv, comps, top, filled, filled_img, labels, pix;
     DevBuf cub_tmp, cbase, summ, rank, flag, ovf, ovf2, thdr, tmap, rstore, rused, fcomp;
     uint32_t cap_nodes = 0;

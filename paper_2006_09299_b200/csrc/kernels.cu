@@ -624,7 +624,10 @@ __global__ void k_cids(Geo g, Ws ws) {
 
 // post-fill roots (depth-1 ancestors) of the border components; non-survivors fold their
 // features into their root right away (block-aggregated; the survivors were initialised by
-// k_cids).  Strip mode folds later, after the cross-rank reduction (k_fold).
+// k_cids).  Strip mode folds later, after the cross-rank reduction (k_fold).  Every node (not
+// only the representatives) also gets what the emit pass needs of it -- its component's id and
+// post-fill root's id, the exterior flag -- next to the tile's other nodes, so that the emit
+// prologue reads them with one load instead of chasing node -> root -> ids.
 __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
     __shared__ FoldTable<FT_SLOTS, false> T;  // hole-filling folds: sums only
     if (ws.counters[1] || !comps_fit(g, ws)) return;
@@ -640,29 +643,41 @@ __global__ void __launch_bounds__(256) k_tops(Geo g, Ws ws) {
         const uint32_t n = base + lane;
         uint32_t dst = FT_EMPTY;
         Acc f;
-        if (n < hi && ws.nrep[n]) {
-            const uint32_t root = ws.uf[n];
-            uint32_t anc;
-            if (ws.ncut && ws.ncut[root]) {
-                anc = ws.nanccid[root];  // strip mode: a class crossing a cut, resolved globally
+        const uint32_t rep = n < hi ? ws.nrep[n] : 0u;
+        uint32_t root = 0, anc = 0;
+        if (n < hi) {
+            root = ws.uf[n];
+            uint32_t cid = 0;
+            if (root < (uint32_t)g.B) {
+                ws.nrep[n] = (uint8_t)(rep | 2u);  // the exterior
             } else {
-                uint32_t cur = root, fold;
-                for (;;) {
-                    const uint32_t p = ws.nparent[cur];
-                    if (p < (uint32_t)g.B) {
-                        anc = fold = ws.nrootcid[cur];
-                        break;
+                cid = ws.nrootcid[root];
+                if (ws.ncut && ws.ncut[root]) {
+                    anc = ws.nanccid[root];  // strip mode: a class crossing a cut, resolved globally
+                } else {
+                    uint32_t cur = root, fold;
+                    for (;;) {
+                        const uint32_t p = ws.nparent[cur];
+                        if (p < (uint32_t)g.B) {
+                            anc = fold = ws.nrootcid[cur];
+                            break;
+                        }
+                        if (ws.ncut && ws.ncut[p]) {  // strip mode: the chain leaves the strip
+                            anc = ws.nanccid[p];
+                            fold = ws.nfold[p];
+                            break;
+                        }
+                        cur = p;
                     }
-                    if (ws.ncut && ws.ncut[p]) {  // strip mode: the chain leaves the strip
-                        anc = ws.nanccid[p];
-                        fold = ws.nfold[p];
-                        break;
+                    if (rep) {
+                        ws.nanccid[root] = anc;
+                        if (ws.nfold) ws.nfold[root] = fold;
                     }
-                    cur = p;
                 }
-                ws.nanccid[root] = anc;
-                if (ws.nfold) ws.nfold[root] = fold;
             }
+            ws.ninfo[n] = make_uint2(cid, anc);
+        }
+        if (rep) {
             int32_t b, ty, tx;
             tile_of(g, ws.nrec[n].tile, b, ty, tx);
             const uint64_t cb = comp_base(g, ws, b);
@@ -696,7 +711,7 @@ __global__ void __launch_bounds__(256) k_fold(Geo g, Ws ws) {
         const uint32_t n = base + (threadIdx.x & 31);
         uint32_t dst = FT_EMPTY;
         Acc f;
-        if (n < hi && ws.nrep[n]) {
+        if (n < hi && (ws.nrep[n] & 1u)) {
             const uint32_t root = ws.uf[n];
             const uint32_t anc = ws.nanccid[root];
             if (anc != ws.nrootcid[root]) {
@@ -802,11 +817,16 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     const int r = tid / WPR, w = tid % WPR;
     constexpr int BT = C::BT;
     const bool word = BT == NW || tid < NW;
+    // every global load the prologue needs is issued up front: the tile header, map offset and
+    // node base (independent of each other), then the bits, row offsets, the stored component map
+    // and the border components' ids (k_tops put them next to the tile's nodes)
     const uint16_t* hdr = ws.thdr + (int64_t)tg.t * THDR;
+    const uint32_t h01 = *reinterpret_cast<const uint32_t*>(hdr);  // 4-B aligned: THDR is even
     const int nb_h = hdr[2];
-    if ((int)hdr[0] > C::MR || (int)hdr[1] > C::NLC || nb_h > C::NBC) return false;  // a larger class owns it
-    // every global load the prologue needs is issued before the first barrier: bits, row
-    // offsets, header rows, map offset, and the border components' ids (node -> root -> ids)
+    const uint64_t moff = ws.tmap[tg.t];
+    const uint32_t tb = ws.tbase[tg.t];
+    const int nruns_h = (int)(h01 & 0xFFFFu), nlc_h = (int)(h01 >> 16);
+    if (nruns_h > C::MR || nlc_h > C::NLC || nb_h > C::NBC) return false;  // a larger class owns it
     const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;
     if (word) {
         S.x[tid] = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
@@ -821,14 +841,14 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         E.ndfold = 0;
         E.cb = (uint64_t)offimg + (uint64_t)tg.b;
         E.gate = !ws.counters[1] && comps_fit(g, ws);
-        S.nlc = hdr[1];
+        S.nlc = nlc_h;
         S.nb = nb_h;
     }
     {  // the run -> component map and component tables the analyze pass stored (tile_runs below
        // does not touch them); bounds-checked so that a failed gate never reads past the store
-        const uint64_t moff = ws.tmap[tg.t];
-        const int nr = map_pad(hdr[0]), nl = map_pad(hdr[1]);
+        const int nr = map_pad(nruns_h), nl = map_pad(nlc_h);
         static_assert(C::MR % 8 == 0 && C::NLC % 8 == 0, "padded map sections fit the tables");
+        static_assert(THDR % 2 == 0, "tile headers start 4-B aligned");
         if (moff + (uint64_t)(nr + 2 * nl) <= ws.cap_rstore) {
             const uint4* src = reinterpret_cast<const uint4*>(ws.rstore + moff);  // 16-B aligned
             uint4* dpar = reinterpret_cast<uint4*>(S.par);
@@ -851,18 +871,16 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         S.rowlc[tid] = hdr[4 + tid];
         S.rowbx[tid] = hdr[4 + TH + 1 + tid];
     }
-    if (nb_h) {
-        const uint32_t nbase = (uint32_t)g.B + ws.tbase[tg.t];
+    {
+        const uint32_t nbase = (uint32_t)g.B + tb;
         const uint32_t nend = (uint32_t)g.B + ws.cap_nodes;  // loads stay in bounds even when
         for (int i = tid; i < nb_h; i += BT) {                 // the gate below fails
             const uint32_t node = nbase + (uint32_t)i;
             if (node >= nend) break;
-            const uint32_t root = ws.uf[node];
-            if (root >= nend) continue;
-            const bool ext = root < (uint32_t)g.B;
-            E.bcid[i] = ws.nrootcid[root];
-            E.banc[i] = ext ? 0u : ws.nanccid[root];
-            E.bflag[i] = (uint8_t)((ws.nrep[node] ? 1u : 0u) | (ext ? 2u : 0u));
+            const uint2 info = ws.ninfo[node];
+            E.bcid[i] = info.x;
+            E.banc[i] = info.y;
+            E.bflag[i] = ws.nrep[node];
         }
     }
     __syncthreads();
