@@ -151,7 +151,8 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
     if (ctx->cap_nodes == 0) ctx->cap_nodes = (uint32_t)std::min<int64_t>(std::max<int64_t>(ntiles * 96, 4096), 0xF0000000ll);
     // initial estimate 0.02 components/pixel (random images: 0.003-0.13); grows on demand
     if (ctx->cap_comps == 0) ctx->cap_comps = (uint64_t)std::max<int64_t>(npx / 48, 4096);
-    if (ctx->cap_rstore == 0) ctx->cap_rstore = (uint64_t)std::max<int64_t>(npx * 3 / 10 + ntiles * 64, 1 << 16);
+    // tile maps: ~2 runs' worth of u16 per run plus 4 per component and the word bases
+    if (ctx->cap_rstore == 0) ctx->cap_rstore = (uint64_t)std::max<int64_t>(npx * 6 / 10 + ntiles * 320, 1 << 16);
     const uint64_t nn = (uint64_t)B + ctx->cap_nodes;
     bool ok = ensure(ctx->bits, (size_t)ntiles * NW * 4) && ensure(ctx->tbase, (size_t)ntiles * 4) &&
               ensure(ctx->tnb, (size_t)ntiles * 4) && ensure(ctx->ovf, (size_t)ntiles * 4) &&

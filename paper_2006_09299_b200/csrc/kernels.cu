@@ -828,10 +828,22 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     const int nruns_h = (int)(h01 & 0xFFFFu), nlc_h = (int)(h01 >> 16);
     if (nruns_h > C::MR || nlc_h > C::NLC || nb_h > C::NBC) return false;  // a larger class owns it
     const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;
-    if (word) {
-        S.x[tid] = __ldcs(ws.bits + (int64_t)tg.t * NW + tid);
-        S.vm[tid] = vm;
-        E.ext[tid] = 0;
+    {
+        // bits and run starts (the run positions and word bases come with the stored map)
+        const uint32_t x = word ? __ldcs(ws.bits + (int64_t)tg.t * NW + tid) : 0u;
+        const uint32_t xl = __shfl_up_sync(0xFFFFFFFFu, x, 1), vml = __shfl_up_sync(0xFFFFFFFFu, vm, 1);
+        if (word) {
+            uint32_t c1 = 0, c0 = 0;
+            if (w > 0) {  // left neighbour word of the same row (rows never straddle a warp)
+                const uint32_t lv = vml >> 31;
+                c1 = (xl >> 31) & lv;
+                c0 = ((~xl) >> 31) & lv;
+            }
+            S.x[tid] = x;
+            S.vm[tid] = vm;
+            S.st[tid] = ((x & ~((x << 1) | c1)) | (~x & ~((~x << 1) | c0))) & vm;
+            E.ext[tid] = 0;
+        }
     }
     const int64_t img0 = (int64_t)tg.b * g.H * g.ntx;
     const uint32_t offimg = img_off(g, ws, tg.b);
@@ -843,24 +855,27 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         E.gate = !ws.counters[1] && comps_fit(g, ws);
         S.nlc = nlc_h;
         S.nb = nb_h;
+        S.nruns = nruns_h;
     }
     {  // the run -> component map and component tables the analyze pass stored (tile_runs below
        // does not touch them); bounds-checked so that a failed gate never reads past the store
-        const int nr = map_pad(nruns_h), nl = map_pad(nlc_h);
+        const MapLayout ML(nruns_h, nlc_h);
         static_assert(C::MR % 8 == 0 && C::NLC % 8 == 0, "padded map sections fit the tables");
         static_assert(THDR % 2 == 0, "tile headers start 4-B aligned");
-        if (moff + (uint64_t)(nr + 2 * nl) <= ws.cap_rstore) {
+        static_assert((NW + 1) / 8 * 16 <= sizeof(S.rbase), "word bases: whole vectors fit");
+        if (moff + (uint64_t)ML.total <= ws.cap_rstore) {
             const uint4* src = reinterpret_cast<const uint4*>(ws.rstore + moff);  // 16-B aligned
-            uint4* dpar = reinterpret_cast<uint4*>(S.par);
-            uint4* drun = reinterpret_cast<uint4*>(S.lcrun);
-            uint4* dlcb = reinterpret_cast<uint4*>(S.lcb);
-            const int vr = nr >> 3, vl = nl >> 3;
-            for (int i = tid; i < vr + 2 * vl; i += BT) {
+            // sections in 16-B vectors: map -> par, lcrun, lcb, rbase
+            const int v1 = ML.lcrun >> 3, v2 = ML.lcb >> 3, v4 = ML.rbase >> 3;
+            const int vend = v4 + ((NW + 1) >> 3);  // rbase: the full vectors (the last element below)
+            for (int i = tid; i < vend; i += BT) {
                 const uint4 v = src[i];
-                if (i < vr) dpar[i] = v;
-                else if (i < vr + vl) drun[i - vr] = v;
-                else dlcb[i - vr - vl] = v;
+                if (i < v1) reinterpret_cast<uint4*>(S.par)[i] = v;
+                else if (i < v2) reinterpret_cast<uint4*>(S.lcrun)[i - v1] = v;
+                else if (i < v4) reinterpret_cast<uint4*>(S.lcb)[i - v2] = v;
+                else reinterpret_cast<uint4*>(S.rbase)[i - v4] = v;
             }
+            if (tid == 0) S.rbase[NW] = ws.rstore[moff + ML.rbase + NW];
         }
     }
     if (tid < FOLD_SLOTS) {
@@ -888,10 +903,11 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
 
     // runs again from the packed bits (cheap); the component map comes from the analyze pass
     RL_PHASE(tg.t, 16);
-    WordBits wb;
-    if (!tile_runs<false>(S, wb)) return false;
-    RL_PHASE(tg.t, 17);
-    const int nruns = wb.nruns, nlc = S.nlc, nb = S.nb;  // S.nruns is not visible before a barrier
+    const int nruns = nruns_h, nlc = nlc_h, nb = nb_h;
+    if (word) {  // run positions of this word's run starts (the word bases are the analyze pass's)
+        int i = S.rbase[tid];
+        for (uint32_t m = S.st[tid]; m; m &= m - 1u) S.runpos[i++] = (uint16_t)((r << 8) | (32 * w + __ffs(m) - 1));
+    }
     const uint64_t cb = E.cb;
     for (int i = tid; i < min(C::FCH, nlc); i += BT) {  // first feature chunk's accumulators
         E.fs[i] = E.fsx[i] = E.fsy[i] = 0;

@@ -94,10 +94,10 @@ struct CclSmem {
     uint32_t x[NW];            // 8-connected-value bits (pixel value XOR flip), 0 where invalid
     uint32_t vm[NW];           // valid-pixel masks
     uint32_t st[NW];           // run-start masks
-    uint16_t rbase[NW + 1];    // first run index of each word
+    alignas(16) uint16_t rbase[NW + 1];  // first run index of each word
     uint16_t rowlc[TH + 1];    // first tile component of each row
     uint16_t rowbx[TH + 1];    // border components before each row start
-    uint16_t runpos[MR];       // (row << 8) | col of each run start, raster order
+    alignas(16) uint16_t runpos[MR];  // (row << 8) | col of each run start, raster order
     alignas(16) typename C::PT par[MR];  // union-find parent; then TAG | component of each run
     union {
         struct {
@@ -130,6 +130,19 @@ struct MapOut {
 
 // map-store sections are padded to whole 16-B vectors
 __host__ __device__ __forceinline__ int map_pad(int n) { return (n + 7) & ~7; }
+
+// A tile's stored map, in u16 elements: [component of each run | first run of each component |
+// border index of each component | first run of each word], each section padded to 8 elements.
+// With the word bases stored, the emit pass needs no run scan of its own.
+struct MapLayout {
+    int lcrun, lcb, rbase, total;
+    __host__ __device__ MapLayout(int nruns, int nlc) {
+        lcrun = map_pad(nruns);
+        lcb = lcrun + map_pad(nlc);
+        rbase = lcb + map_pad(nlc);
+        total = rbase + map_pad(NW + 1);
+    }
+};
 
 template <class SM>
 __device__ __forceinline__ int run_at(const SM& S, int word, int bit) {
@@ -504,7 +517,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
     if (tid == 0) S.nlc = nlc;
     if (tid == 32) {  // the map: component of each run, first run and border index of each component
         // (three sections, each padded to 8 elements: the emit pass copies them with 16-B loads)
-        const unsigned long long need = (unsigned long long)map_pad(nruns) + 2ull * (unsigned long long)map_pad(nlc);
+        const unsigned long long need = (unsigned long long)MapLayout(nruns, nlc).total;
         const unsigned long long off = atomicAdd(mo.used, need);
         if (off + need > mo.cap) atomicOr(mo.err, ERR_RSTORE_CAP);
         S.moff = off + need > mo.cap ? ~0ull : off;
@@ -532,6 +545,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
 
     const unsigned long long moff = S.moff;
     uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
+    const MapLayout ML(nruns, nlc);
     constexpr int NWB = BT / 32;
     // ---- compact border components to border indices (raster order; warp segments)
     const int segl = ((nlc + NWB - 1) / NWB + 31) & ~31;
@@ -558,7 +572,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
                 v = (uint16_t)(0x8000 | my);
             }
             S.lcb[l] = v;
-            if (map) map[map_pad(nruns) + map_pad(nlc) + l] = v;
+            if (map) map[MapLayout(nruns, nlc).lcb + l] = v;
         }
         bx += __popc(m);
     }
@@ -590,8 +604,10 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
         border(bi, i, iroot);
     }
     __syncthreads();
-    if (map)
-        for (int l = tid; l < nlc; l += BT) map[map_pad(nruns) + l] = S.lcrun[l];
+    if (map) {
+        for (int l = tid; l < nlc; l += BT) map[ML.lcrun + l] = S.lcrun[l];
+        for (int k = tid; k <= NW; k += BT) map[ML.rbase + k] = S.rbase[k];
+    }
     RL_PHASE(tg.t, 9);
     return true;
 }
