@@ -366,16 +366,14 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launches += (g.nty > 1) + (g.ntx > 1);
     kt();
     const int64_t hint = (int64_t)ctx->cap_nodes;
-    launch_resolve(g, ws, s, ctx->sms, hint);
-    kt();
-    launch_reps(g, ws, s, ctx->sms, hint);
+    launch_resolve(g, ws, s, ctx->sms, hint);  // + representatives and their counts
     kt();
     cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ws.cnt, ws.off, (int)ncnt, s);
     kt();
     launch_cids(g, ws, s, ctx->sms);
     kt();
     launch_tree(g, ws, s, ctx->sms, hint);
-    launches += 2 + 1 + 1 + 1;
+    launches += 1 + 1 + 1 + 1;
     kt();
     record_event(ctx->ev[2], s, use_graph);
     launch_emit(g, ws, s);

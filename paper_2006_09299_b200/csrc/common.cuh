@@ -395,7 +395,7 @@ struct FoldTable {
 // component's nodes all fold into one root), then one lane adds the sum to the block table --
 // 64-bit shared atomics are CAS loops, contention on one slot is what this avoids.  All 32
 // lanes must call it.  gdst(k) / gkey(k): global destinations when the table is full.
-template <class TT, class GD, class GK>
+template <bool KEYS = true, class TT, class GD, class GK>
 __device__ __forceinline__ void warp_fold(TT& T, uint32_t dst, const Acc& f, unsigned long long key, GD&& gdst,
                                           GK&& gkey) {
     const int lane = threadIdx.x & 31;
@@ -423,8 +423,10 @@ __device__ __forceinline__ void warp_fold(TT& T, uint32_t dst, const Acc& f, uns
             s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
             s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
             s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
-            const unsigned long long ko = __shfl_xor_sync(0xFFFFFFFFu, km, o);
-            km = ko < km ? ko : km;
+            if (KEYS) {
+                const unsigned long long ko = __shfl_xor_sync(0xFFFFFFFFu, km, o);
+                km = ko < km ? ko : km;
+            }
         }
         int r0 = 0, r1 = 0, c0 = 0, c1 = 0;
         if (TT::kBox) {
@@ -469,6 +471,28 @@ __device__ __forceinline__ uint32_t gfind_ro(const uint32_t* uf, uint32_t a) {
         const uint32_t p = uf[a];
         if (p == a) return a;
         a = p;
+    }
+}
+
+// Union of border nodes ordered by first-pixel key instead of index: the root of every class
+// is its raster-first node, i.e. the component's representative (no min-key reduction needed).
+// Image exteriors (nodes < B) order first.  Lock-free: a root is linked with a CAS that expects it
+// to still be a root; a failed CAS continues from the parent it returned (a plain load could
+// keep returning a stale L1 copy).
+__device__ __forceinline__ void gunion_key(uint32_t* uf, const uint64_t* key, uint32_t a, uint32_t b, uint32_t B) {
+    a = gfind(uf, a);
+    for (;;) {
+        b = gfind(uf, b);
+        if (a == b) return;
+        const uint64_t ka = a < B ? 0ull : key[a] + 1ull, kb = b < B ? 0ull : key[b] + 1ull;
+        if (ka < kb) {  // link the later-keyed root under the earlier one
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        const uint32_t old = atomicCAS(uf + a, a, b);
+        if (old == a) return;
+        a = gfind(uf, old);
     }
 }
 

@@ -360,11 +360,11 @@ __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int
                 const uint32_t vul = lul >> 15, vdl = ldl >> 15;
                 if (vul == v8 && vd == v8 && vu != v8 && vdl != v8) {  // (r, x-1) ~ (r+1, x)
                     if (c > 0) sunion(lp, lul & 0x7FFFu, id);
-                    else gunion(ws.uf, node_of(ws, g, tu - 1, lul), node_of(ws, g, tl, ld));
+                    else gunion_key(ws.uf, ws.nkey, node_of(ws, g, tu - 1, lul), node_of(ws, g, tl, ld), (uint32_t)g.B);
                 }
                 if (vu == v8 && vdl == v8 && vul != v8 && vd != v8) {  // (r, x) ~ (r+1, x-1)
                     if (c > 0) sunion(lp, iu, (uint32_t)nbu + (ldl & 0x7FFFu));
-                    else gunion(ws.uf, node_of(ws, g, tu, lu), node_of(ws, g, tl - 1, ldl));
+                    else gunion_key(ws.uf, ws.nkey, node_of(ws, g, tu, lu), node_of(ws, g, tl - 1, ldl), (uint32_t)g.B);
                 }
             }
         }
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int
             while (lp[r] != r) r = lp[r];
             const uint32_t ni = i < nbu ? bu + i : bd + (i - nbu);
             const uint32_t nr = r < (uint32_t)nbu ? bu + r : bd + (r - nbu);
-            gunion(ws.uf, ni, nr);
+            gunion_key(ws.uf, ws.nkey, ni, nr, (uint32_t)g.B);
         }
         __syncthreads();
     }
@@ -405,15 +405,15 @@ __global__ void k_seam_v(Geo g, Ws ws) {
         const uint32_t vL = lL >> 15, vR = lR >> 15;
         if (vL == vR) {
             const bool same = r > 0 && pL[r - 1] == lL && pR[r - 1] == lR;
-            if (!same) gunion(ws.uf, node_of(ws, g, tL, lL), node_of(ws, g, tR, lR));
+            if (!same) gunion_key(ws.uf, ws.nkey, node_of(ws, g, tL, lL), node_of(ws, g, tR, lR), (uint32_t)g.B);
         }
         if (r + 1 < th) {
             const uint16_t lL1 = pL[r + 1], lR1 = pR[r + 1];
             const uint32_t vL1 = lL1 >> 15, vR1 = lR1 >> 15;
             if (vL == v8 && vR1 == v8 && vR != v8 && vL1 != v8)
-                gunion(ws.uf, node_of(ws, g, tL, lL), node_of(ws, g, tR, lR1));
+                gunion_key(ws.uf, ws.nkey, node_of(ws, g, tL, lL), node_of(ws, g, tR, lR1), (uint32_t)g.B);
             if (vL1 == v8 && vR == v8 && vL != v8 && vR1 != v8)
-                gunion(ws.uf, node_of(ws, g, tL, lL1), node_of(ws, g, tR, lR));
+                gunion_key(ws.uf, ws.nkey, node_of(ws, g, tL, lL1), node_of(ws, g, tR, lR), (uint32_t)g.B);
         }
     }
 }
@@ -437,6 +437,17 @@ __global__ void k_seam_v(Geo g, Ws ws) {
 
 constexpr int FT_SLOTS = 512;
 
+__device__ __forceinline__ void tile_of(const Geo& g, uint32_t t, int32_t& b, int32_t& ty, int32_t& tx) {
+    b = (int32_t)(t / (uint32_t)g.tpi);
+    const int32_t rem = (int32_t)(t - (uint32_t)b * g.tpi);
+    ty = rem / g.ntx;
+    tx = rem - ty * g.ntx;
+}
+
+// Flatten, fold node features into the roots and -- outside strip mode, where the cut classes'
+// status is settled later (k_reps, strips.cu) -- count the representatives: the root of a class
+// is its raster-first node (gunion_key), so it represents the component and is counted in the
+// (image, row, tile column) cell of its first pixel.
 __global__ void __launch_bounds__(256) k_resolve(Geo g, Ws ws) {
     __shared__ FoldTable<FT_SLOTS> T;
     if (ws.counters[1]) return;
@@ -450,31 +461,43 @@ __global__ void __launch_bounds__(256) k_resolve(Geo g, Ws ws) {
         const uint32_t n = base + (threadIdx.x & 31);
         uint32_t dst = FT_EMPTY;
         Acc f;
-        unsigned long long key = ~0ull;
+        bool fgrep = false;
+        int32_t b = -1;
         if (n < hi) {
             const uint32_t root = gfind_ro(ws.uf, n);
             if (root != n) {
                 ws.uf[n] = root;
                 dst = root;
                 f = ws.nacc[n];
-                key = ws.nkey[n];
+            }
+            if (!g.strip) {
+                ws.nrep[n] = root == n ? 1 : 0;
+                if (root == n) {
+                    const NodeRec rec = ws.nrec[n];
+                    int32_t ty, tx;
+                    tile_of(g, rec.tile, b, ty, tx);
+                    atomicAdd(&ws.cnt[((int64_t)b * g.H + ty * TH + rec.fr) * g.ntx + tx], 1u);
+                    fgrep = rec.fg != 0;
+                }
             }
         }
-        warp_fold(T, dst, f, key, [&](uint32_t k) { return ws.nacc + k; },
-                  [&](uint32_t k) { return reinterpret_cast<unsigned long long*>(ws.nmin + k); });
+        warp_fold<false>(T, dst, f, ~0ull, [&](uint32_t k) { return ws.nacc + k; },
+                         [&](uint32_t) { return static_cast<unsigned long long*>(nullptr); });
+        const uint32_t fgmask = __ballot_sync(0xFFFFFFFFu, fgrep);
+        if (fgmask) {  // foreground representatives per image, aggregated per warp
+            const uint32_t same = __match_any_sync(0xFFFFFFFFu, fgrep ? b : -1);
+            if (fgrep && (__ffs(same & fgmask) - 1) == (int)(threadIdx.x & 31u))
+                atomicAdd(&ws.img_fg[b], (uint32_t)__popc(same & fgmask));
+        }
     }
     __syncthreads();
     T.flush([&](uint32_t k) { return ws.nacc + k; },
-            [&](uint32_t k) { return reinterpret_cast<unsigned long long*>(ws.nmin + k); });
+            [&](uint32_t) { return static_cast<unsigned long long*>(nullptr); });
 }
 
-__device__ __forceinline__ void tile_of(const Geo& g, uint32_t t, int32_t& b, int32_t& ty, int32_t& tx) {
-    b = (int32_t)(t / (uint32_t)g.tpi);
-    const int32_t rem = (int32_t)(t - (uint32_t)b * g.tpi);
-    ty = rem / g.ntx;
-    tx = rem - ty * g.ntx;
-}
 
+// strip mode's representatives, once the cut classes' status is applied (strips.cu): a root
+// whose min key was cleared is represented in another strip
 __global__ void k_reps(Geo g, Ws ws) {
     if (ws.counters[1]) return;
     const uint32_t nused = min(ws.counters[0], ws.cap_nodes);
