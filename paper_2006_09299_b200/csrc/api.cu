@@ -295,9 +295,10 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
         ctx->h_summ_n = sn;
     }
 
-    // Small workloads are launch-bound: the whole pipeline is captured once into a CUDA graph
-    // and replayed while the geometry, configuration and workspace stay the same.
-    const bool use_graph = ctx->graphs && (double)g.P * B <= 64.0 * 1024 * 1024;
+    // The whole pipeline is captured once into a CUDA graph and replayed while the geometry,
+    // configuration and workspace stay the same (small workloads are launch-bound; large ones
+    // still lose the gaps between their ~12 launches).
+    const bool use_graph = ctx->graphs && (double)g.P * B <= ctx->graph_max_px;
     GraphKey key{};
     key.g = g;
     key.ws = ws;
@@ -601,6 +602,7 @@ rl_ctx* rl_create(int device) {
     }
     c->stream = c->own_stream;
     if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
+    if (const char* v = std::getenv("RUNLAB_GPU_GRAPH_MPX")) c->graph_max_px = std::atof(v) * 1024 * 1024;
     if (const char* v = std::getenv("RUNLAB_GPU_PERMUTE")) c->permute = std::max(0ll, std::atoll(v));
     if (std::getenv("RUNLAB_GPU_KTIMES")) c->ktimes = true;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_D2H")) c->packed_d2h = false;

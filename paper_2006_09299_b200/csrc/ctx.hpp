@@ -111,6 +111,9 @@ struct rl_ctx {
     bool reran = false;  // finish() had to grow a capacity and re-run
     // CUDA graph of the last small pipeline
     bool graphs = true;
+    // pipelines are captured into a CUDA graph and replayed (config 2, 440 Mpx: 2.367 -> 2.339 ms
+    // per step against eager launches); env RUNLAB_GPU_GRAPH_MPX caps the workload size
+    double graph_max_px = 1e18;
     int64_t permute = 0;  // env RUNLAB_GPU_PERMUTE (testing aid, Geo::permute)
     bool used_graph = false;
     cudaGraphExec_t gexec = nullptr;
