@@ -9,7 +9,6 @@
 // binarize_labels (labeling.hpp:354-360); error mapping per labeling.hpp:271-273.
 #include <cuda_runtime.h>
 
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <condition_variable>
@@ -171,12 +170,10 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
               ensure(ctx->summ, (size_t)(B + 2) * 32) && ensure(ctx->ftab, (size_t)FT_SHARDS * FT_HS * 28);
     if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)out_px * 4);
     if (!ok) return set_err(ctx, RL_ENOMEM, "device allocation failed");
-    tmp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)ncnt);
+    tmp = scan_state_bytes(ncnt);  // scan.cu
     size_t tmp2 = 0;
     if ((cfg->densify_labels && cfg->fill_holes) || ctx->want_compact)
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp2, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                      (int)std::min<uint64_t>(ctx->cap_comps + 1, 0x7FFFFFFF));
+        tmp2 = scan_state_bytes((int64_t)std::min<uint64_t>(ctx->cap_comps + 1, 0x7FFFFFFF));
     if (!ensure(ctx->cub_tmp, std::max(tmp, tmp2))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
 
     ws = Ws{};
@@ -369,7 +366,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     const int64_t hint = (int64_t)ctx->cap_nodes;
     launch_resolve(g, ws, s, ctx->sms, hint);  // + representatives and their counts
     kt();
-    cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tmp, ws.cnt, ws.off, (int)ncnt, s);
+    launch_scan(ws.cnt, ws.off, ncnt, 0u, ctx->cub_tmp.p, s);  // canonical-id offsets of the cells
     kt();
     launch_cids(g, ws, s, ctx->sms);
     kt();
@@ -389,9 +386,8 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
         // prefix in use (consumers only read ranks of survivors)
         const uint64_t total = ctx->cap_comps;
         launch_surv_flags(ws.top, P<uint64_t>(ctx->cbase), B, total, P<uint32_t>(ctx->flag), s, ctx->sms);
-        size_t t2 = ctx->cub_tmp.bytes;
-        cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t2, P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank),
-                                      (int)std::min<uint64_t>(total + 1, 0x7FFFFFFF), s);
+        launch_scan(P<uint32_t>(ctx->flag), P<uint32_t>(ctx->rank), (int64_t)std::min<uint64_t>(total + 1, 0x7FFFFFFF),
+                    0u, ctx->cub_tmp.p, s);
         launches += 2;
     }
     if (densify_fill) {

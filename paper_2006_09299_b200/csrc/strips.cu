@@ -38,7 +38,6 @@
 // crosses strips lands on a GCC survivor.
 #include <cuda_runtime.h>
 
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdlib>
@@ -578,9 +577,8 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
             !ensure(ctx->flag, nn * 4) ||
             !ensure(ctx->rank, nn * 4) || !ensure(ctx->xnode, nn * 4) || !ensure(ctx->scount, 64))
             return set_err(ctx, RL_ENOMEM, "device allocation failed");
-        size_t tmp3 = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nn);
-        if (!ensure(ctx->cub_tmp, std::max(tmp, tmp3))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+        if (!ensure(ctx->cub_tmp, std::max(tmp, scan_state_bytes((int64_t)nn))))
+            return set_err(ctx, RL_ENOMEM, "device allocation failed");
         ws.nleft = P<uint32_t>(ctx->nleft);
         ws.ncut = P<uint32_t>(ctx->ncut);
         ws.nfold = P<uint32_t>(ctx->nfold);
@@ -622,8 +620,7 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         cudaMemsetAsync(ws.ncut, 0, (size_t)(n_local + 1) * 4, s);
         k_strip_mark<<<grid(2 * (int64_t)w, ctx->sms), 256, 0, s>>>(g, ws, flag, top, bot);
         STRIP_STEP(ctx, "k_strip_mark");
-        size_t t3 = ctx->cub_tmp.bytes;
-        cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t3, flag, rank, (int)(n_local + 1), s);
+        launch_scan(flag, rank, n_local + 1, 0u, ctx->cub_tmp.p, s);
         unsigned long long* cnt2 = P<unsigned long long>(ctx->scount);
         cudaMemsetAsync(cnt2, 0, 16, s);
         k_strip_count<<<grid(std::max<int64_t>(n_local, (int64_t)(g.ty1 - g.ty0) * TH * g.ntx), ctx->sms), 256, 0, s>>>(
@@ -756,13 +753,8 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     // offsets of this strip's rows only, starting at the components of the strips above; off[0]
     // (the image base) and the end cell are what the numbering passes read outside them
     const int64_t c_lo = (int64_t)g.ty0 * TH * g.ntx, c_hi = std::min<int64_t>((int64_t)g.ty1 * TH, g.H) * g.ntx;
-    size_t tscan = 0;
-    cub::DeviceScan::ExclusiveScan(nullptr, tscan, ws.cnt + c_lo, ws.off + c_lo, cub::Sum(), (uint32_t)0,
-                                   (int)(c_hi - c_lo + 1), s);
-    if (!ensure(ctx->cub_tmp, tscan)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
-    tscan = ctx->cub_tmp.bytes;
-    cub::DeviceScan::ExclusiveScan(ctx->cub_tmp.p, tscan, ws.cnt + c_lo, ws.off + c_lo, cub::Sum(), (uint32_t)off_me,
-                                   (int)(c_hi - c_lo + 1), s);
+    if (!ensure(ctx->cub_tmp, scan_state_bytes(c_hi - c_lo + 1))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    launch_scan(ws.cnt + c_lo, ws.off + c_lo, c_hi - c_lo + 1, (uint32_t)off_me, ctx->cub_tmp.p, s);
     launch_cids(g, ws, s, ctx->sms);
     STRIP_STEP(ctx, "launch_cids");
     k_g_links<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0,
