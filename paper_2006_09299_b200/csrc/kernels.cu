@@ -118,11 +118,11 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         }
         __device__ void operator()(int bi, int i, bool iroot) {
             const CclSmem<C>& S = A.c;
-            if (iroot) nfg += (int)(((S.x[(S.runpos[i] >> 8) * WPR + ((S.runpos[i] & 0xFF) >> 5)] >> (S.runpos[i] & 31)) & 1u) ^ flip);
             int rr = 0, c0 = 0x7FFFFFFF, cl = -1;
             uint32_t nsy = 0, sx = 0;
+            const uint16_t rp = (iroot || bi >= 0) ? S.runpos[i] : 0;
+            if (iroot) nfg += (int)(((S.x[(rp >> 8) * WPR + ((rp & 0xFF) >> 5)] >> (rp & 31)) & 1u) ^ flip);
             if (bi >= 0) {
-                const uint16_t rp = S.runpos[i];
                 const uint16_t nx = (i + 1 < S.nruns) ? S.runpos[i + 1] : 0xFFFF;
                 rr = rp >> 8;
                 c0 = rp & 0xFF;

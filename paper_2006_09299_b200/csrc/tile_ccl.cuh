@@ -523,7 +523,8 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
         S.moff = off + need > mo.cap ? ~0ull : off;
         mo.tile_off[tg.t] = off;
     }
-    for (int l = tid; l < nlc; l += BT) S.lcb[l] = 0;
+    static_assert(C::NLC % 8 == 0, "border flags clear in whole 16-B vectors");
+    for (int v = tid; v < (nlc + 7) >> 3; v += BT) reinterpret_cast<uint4*>(S.lcb)[v] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     RL_PHASE(tg.t, 6);
     // ---- border components (plain stores of 1): every row's first and last run (the left and
