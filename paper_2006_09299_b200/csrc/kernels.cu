@@ -759,7 +759,8 @@ template <class C>
 struct EmitSmem {
     CclSmem<C> c;
     // interior-feature chunk accumulators (tile-local coordinates)
-    uint32_t fs[C::FCH], fsx[C::FCH], fsy[C::FCH];
+    // S | (Sy << 14): the components of one tile hold <= 8192 pixels in all (see AnalyzeSmem)
+    uint32_t fssy[C::FCH], fsx[C::FCH];
     int32_t frmax[C::FCH], fcmin[C::FCH], fcmax[C::FCH];
     // border components of this tile
     uint32_t bcid[C::NBC];   // canonical id of the component
@@ -933,7 +934,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     }
     const uint64_t cb = E.cb;
     for (int i = tid; i < min(C::FCH, nlc); i += BT) {  // first feature chunk's accumulators
-        E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
+        E.fssy[i] = E.fsx[i] = 0;
         E.frmax[i] = -1;
         E.fcmin[i] = 0x7FFFFFFF;
         E.fcmax[i] = -1;
@@ -971,7 +972,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         const int l1 = min(l0 + C::FCH, nlc);
         if (l0 > 0) {  // the first chunk's accumulators were cleared before the prefix barrier
             for (int i = tid; i < l1 - l0; i += BT) {
-                E.fs[i] = E.fsx[i] = E.fsy[i] = 0;
+                E.fssy[i] = E.fsx[i] = 0;
                 E.frmax[i] = -1;
                 E.fcmin[i] = 0x7FFFFFFF;
                 E.fcmax[i] = -1;
@@ -1018,9 +1019,8 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             const int k = (int)lc - l0;
             const int rr = run_row(S, i), c0 = run_col(S, i), c1 = run_end(S, i, tg.tw);
             const uint32_t n = (uint32_t)(c1 - c0);
-            atomicAdd(&E.fs[k], n);
+            atomicAdd(&E.fssy[k], n | ((n * (uint32_t)rr) << 14));
             atomicAdd(&E.fsx[k], n * (uint32_t)(c0 + c1 - 1) / 2u);
-            atomicAdd(&E.fsy[k], n * (uint32_t)rr);
             atomicMax(&E.frmax[k], rr);
             atomicMin(&E.fcmin[k], c0);
             atomicMax(&E.fcmax[k], c1 - 1);
@@ -1045,11 +1045,11 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
                 int end;
                 uint32_t surv;
                 const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
-                const int64_t s = E.fs[k];
+                const int64_t s = E.fssy[k] & 0x3FFFu;
                 rl_component c;
                 c.f.s = s;
                 c.f.sx = (int64_t)E.fsx[k] + s * tg.x0;
-                c.f.sy = (int64_t)E.fsy[k] + s * tg.y0;
+                c.f.sy = (int64_t)(E.fssy[k] >> 14) + s * tg.y0;
                 c.f.row_min = tg.y0 + fr;
                 c.f.row_max = tg.y0 + E.frmax[k];
                 c.f.col_min = tg.x0 + E.fcmin[k];
@@ -1078,16 +1078,15 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             const int dom = __shfl_sync(0xFFFFFFFFu, slot, lead);
             const uint32_t grp = __ballot_sync(0xFFFFFFFFu, slot == dom);
             if (slot < 0) continue;
-            uint32_t vs = E.fs[k], vsx = E.fsx[k], vsy = E.fsy[k];
+            uint32_t vssy = E.fssy[k], vsx = E.fsx[k];
             if (slot == dom) {
-                vs = __reduce_add_sync(grp, vs);
+                vssy = __reduce_add_sync(grp, vssy);  // a tile's sums stay within the packed fields
                 vsx = __reduce_add_sync(grp, vsx);
-                vsy = __reduce_add_sync(grp, vsy);
                 if ((tid & 31) != lead) continue;
             }
-            atomicAdd(&E.ps[slot], vs);
+            atomicAdd(&E.ps[slot], vssy & 0x3FFFu);
             atomicAdd(&E.psx[slot], vsx);
-            atomicAdd(&E.psy[slot], vsy);
+            atomicAdd(&E.psy[slot], vssy >> 14);
         }
         __syncthreads();
         RL_PHASE(tg.t, 21);
@@ -1096,8 +1095,9 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             int end;
             uint32_t surv;
             const uint32_t anc = interior_top(E, (uint32_t)lc, end, surv);
-            const int64_t s = E.fs[k];
-            acc_atomic_fold_fill(ws.filled + cb + anc, s, (int64_t)E.fsx[k] + s * tg.x0, (int64_t)E.fsy[k] + s * tg.y0);
+            const int64_t s = E.fssy[k] & 0x3FFFu;
+            acc_atomic_fold_fill(ws.filled + cb + anc, s, (int64_t)E.fsx[k] + s * tg.x0,
+                                 (int64_t)(E.fssy[k] >> 14) + s * tg.y0);
         }
         __syncthreads();
         RL_PHASE(tg.t, 22);

@@ -78,11 +78,11 @@ using CapM = Cap<MAXRUNS * 9 / 16, NBMAX, 512, 384, uint32_t, 2 * NW, 2048>;
 using CapF = Cap<MAXRUNS, NBMAX, 1024, 320, uint32_t, 2 * NW>;
 // emit pass: same classes, no unions (16-bit component map, larger feature chunks)
 #ifndef RL_SE_FCH
-#define RL_SE_FCH 192
+#define RL_SE_FCH 288  // the largest chunk with 8 CTAs per SM (packed S|Sy accumulators)
 #endif
 using CapSE = Cap<CapS::MR, CapS::NBC, 192, RL_SE_FCH, uint16_t, NW, CapS::NLC>;
 #ifndef RL_ME_FCH
-#define RL_ME_FCH 512  // the largest chunk with 4 CTAs per SM
+#define RL_ME_FCH 704  // the largest chunk with 4 CTAs per SM
 #endif
 using CapME = Cap<CapM::MR, CapM::NBC, 32, RL_ME_FCH, uint16_t, 2 * NW, CapM::NLC>;
 using CapFE = Cap<CapF::MR, CapF::NBC, 1024, 320, uint16_t, 2 * NW>;
