@@ -48,10 +48,13 @@ def balanced_shards(costs: list[float], world: int) -> list[list[int]]:
 
 
 def image_cost(density: float, granularity: int) -> float:
-    """Relative device cost of one generated image per pixel: a fixed per-pixel part plus a
-    part proportional to the expected runs per pixel, 2 d (1 - d) / g for the reference
-    generator's g x g blocks (generator.hpp:46-83)."""
-    return 1.0 + 8.0 * 2.0 * density * (1.0 - density) / max(granularity, 1)
+    """Relative device cost of one generated image per pixel: a fixed part plus a part growing
+    with the expected run density 2 d (1 - d) / g of the reference generator's g x g blocks
+    (generator.hpp:46-83).  Fitted to the per-cell device times of the config-2 sweep on a
+    B200 (tools/prof_driver.py --sweep: 13.1 + 116 (2d(1-d))^0.86 / g^1.6 us per 2048^2 image,
+    within 23% on every cell)."""
+    r = 2.0 * density * (1.0 - density)
+    return 1.0 + 8.87 * r ** 0.86 / max(granularity, 1) ** 1.6
 
 
 def max_over_ranks(value: float, device=None) -> float:
