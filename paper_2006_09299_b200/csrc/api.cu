@@ -55,6 +55,23 @@ __global__ void k_summary(Geo g, Ws ws, uint64_t* cbase, int64_t* summ) {
     }
 }
 
+// the per-call counters, per-image counts, the summary's tail row and the look-back state of
+// the offset scan, zeroed by one launch instead of a memset each
+__global__ void k_init(Ws ws, int32_t B, uint32_t* cnt_end, int64_t* summ_tail, unsigned long long* scan_state,
+                       int64_t scan_words) {
+    const int64_t n = max((int64_t)max(B, 16), scan_words);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < 16) ws.counters[i] = 0;
+        if (i == 0) {
+            *ws.rused = 0;
+            *cnt_end = 0;
+        }
+        if (i < 4) summ_tail[i] = 0;
+        if (i < B) ws.img_fg[i] = ws.img_surv[i] = 0;
+        if (i < scan_words) scan_state[i] = 0;
+    }
+}
+
 }  // namespace
 
 
@@ -340,12 +357,14 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
             return cuda_fail(ctx, cudaGetLastError(), "graph capture");
     }
     int launches = 0;
-    cudaMemsetAsync(ws.counters, 0, 64, s);
-    cudaMemsetAsync(ws.rused, 0, 8, s);
-    cudaMemsetAsync(ws.img_fg, 0, (size_t)B * 4, s);
-    cudaMemsetAsync(ws.img_surv, 0, (size_t)B * 4, s);
-    cudaMemsetAsync(ws.cnt + (ncnt - 1), 0, 4, s);
-    cudaMemsetAsync(P<int64_t>(ctx->summ) + 4 * (B + 1), 0, 32, s);
+    {
+        const int64_t sw = (int64_t)(scan_state_bytes(ncnt) / 8);
+        const int64_t n = std::max<int64_t>(std::max(B, 16), sw);
+        k_init<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, s>>>(
+            ws, B, ws.cnt + (ncnt - 1), P<int64_t>(ctx->summ) + 4 * (B + 1),
+            static_cast<unsigned long long*>(ctx->cub_tmp.p), sw);
+        ++launches;
+    }
     ctx->nkev = 0;
     auto kt = [&]() {  // tuning aid: an event after each launch group
         if (!ctx->ktimes || use_graph || ctx->nkev >= 24) return;
@@ -366,7 +385,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     const int64_t hint = (int64_t)ctx->cap_nodes;
     launch_resolve(g, ws, s, ctx->sms, hint);  // + representatives and their counts
     kt();
-    launch_scan(ws.cnt, ws.off, ncnt, 0u, ctx->cub_tmp.p, s);  // canonical-id offsets of the cells
+    launch_scan(ws.cnt, ws.off, ncnt, 0u, ctx->cub_tmp.p, s, true);  // canonical-id offsets (state zeroed by k_init)
     kt();
     launch_cids(g, ws, s, ctx->sms);
     kt();

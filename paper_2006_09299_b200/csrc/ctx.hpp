@@ -15,7 +15,8 @@ size_t emit_smem();
 cudaError_t configure_kernels();
 // scan.cu: out[i] = init + sum(in[0 .. i)); `state`: scan_state_bytes(n) bytes of device memory
 size_t scan_state_bytes(int64_t n);
-void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t init, void* state, cudaStream_t s);
+void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t init, void* state, cudaStream_t s,
+                 bool zeroed = false);
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s);
 void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms);
 void launch_seam_cols(const Geo& g, const Ws& ws, cudaStream_t s, int sms);

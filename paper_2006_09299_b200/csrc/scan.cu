@@ -143,10 +143,12 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(const uint32_t* __restrict__ in
 size_t scan_state_bytes(int64_t n) { return (size_t)(1 + (n + SCAN_BLOCK - 1) / SCAN_BLOCK) * 8; }
 
 // out[i] = init + sum(in[0 .. i)), i < n; `state` holds scan_state_bytes(n) bytes of device memory
-void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t init, void* state, cudaStream_t s) {
+// (zeroed here unless the caller already did, `zeroed`)
+void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t init, void* state, cudaStream_t s,
+                 bool zeroed) {
     if (n <= 0) return;
     const int64_t blocks = (n + SCAN_BLOCK - 1) / SCAN_BLOCK;
-    cudaMemsetAsync(state, 0, scan_state_bytes(n), s);
+    if (!zeroed) cudaMemsetAsync(state, 0, scan_state_bytes(n), s);
     k_scan<<<(unsigned)blocks, SCAN_T, 0, s>>>(in, out, n, init, static_cast<unsigned long long*>(state));
 }
 
