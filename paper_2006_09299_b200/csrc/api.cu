@@ -377,9 +377,21 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launches += 3;
     record_event(ctx->ev[1], s, use_graph);
     kt();
+    // horizontal and vertical seams concurrently (both only unite border nodes, lock-free):
+    // the vertical ones on a stream forked from and joined back into the pipeline stream
+    const bool fork = ctx->seam_stream && g.ntx > 1 && !ctx->ktimes;
+    if (fork) {
+        cudaEventRecord(ctx->seam_fork, s);
+        cudaStreamWaitEvent(ctx->seam_stream, ctx->seam_fork, 0);
+        launch_seam_cols(g, ws, ctx->seam_stream, ctx->sms);
+        cudaEventRecord(ctx->seam_join, ctx->seam_stream);
+    }
     if (g.nty > 1) launch_seam_rows(g, ws, 0, g.nty - 1, s, ctx->sms);
     kt();
-    launch_seam_cols(g, ws, s, ctx->sms);
+    if (fork)
+        cudaStreamWaitEvent(s, ctx->seam_join, 0);
+    else
+        launch_seam_cols(g, ws, s, ctx->sms);
     launches += (g.nty > 1) + (g.ntx > 1);
     kt();
     const int64_t hint = (int64_t)ctx->cap_nodes;
@@ -616,6 +628,12 @@ rl_ctx* rl_create(int device) {
         return nullptr;
     }
     c->stream = c->own_stream;
+    if (cudaStreamCreateWithFlags(&c->seam_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->seam_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->seam_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        c->seam_stream = nullptr;  // the seams then run one after the other
+    }
     if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
     if (const char* v = std::getenv("RUNLAB_GPU_GRAPH_MPX")) c->graph_max_px = std::atof(v) * 1024 * 1024;
     if (const char* v = std::getenv("RUNLAB_GPU_PERMUTE")) c->permute = std::max(0ll, std::atoll(v));
@@ -663,6 +681,9 @@ void rl_destroy(rl_ctx* c) {
         cudaStreamDestroy(c->in_stream);
     }
     if (c->in_done) cudaEventDestroy(c->in_done);
+    if (c->seam_stream) cudaStreamDestroy(c->seam_stream);
+    if (c->seam_fork) cudaEventDestroy(c->seam_fork);
+    if (c->seam_join) cudaEventDestroy(c->seam_join);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }

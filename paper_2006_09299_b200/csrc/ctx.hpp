@@ -89,6 +89,9 @@ struct rl_ctx {
     int sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
+    // the vertical seams run beside the horizontal ones (independent unions): a forked stream
+    cudaStream_t seam_stream = nullptr;
+    cudaEvent_t seam_fork = nullptr, seam_join = nullptr;
     std::string err;
     static constexpr int NEV = 5;  // start, after analyze, after merge, after emit, end
     cudaEvent_t ev[NEV] = {};  // events of the current call
