@@ -405,7 +405,10 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launches += 1 + 1 + 1 + 1;
     kt();
     record_event(ctx->ev[2], s, use_graph);
-    launch_emit(g, ws, s);
+    if (ctx->seam_stream && !ctx->ktimes)
+        launch_emit(g, ws, s, ctx->seam_stream, ctx->seam_fork, ctx->seam_join);
+    else
+        launch_emit(g, ws, s);
     launches += 3 + (g.tpi >= 8192 ? 1 : 0);  // + the shard-table flush (kernels.cu FT_MIN_TILES)
     kt();
     k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));

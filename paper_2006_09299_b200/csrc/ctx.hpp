@@ -27,7 +27,8 @@ void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
 void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
 void launch_tree_parts(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
 void launch_fold(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
-void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s);
+void launch_emit(const Geo& g, const Ws& ws, cudaStream_t s, cudaStream_t s2 = nullptr, cudaEvent_t fork = nullptr,
+                 cudaEvent_t join = nullptr);
 void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
                        cudaStream_t s, int sms);
 void launch_compact_filled(const Acc* filled, const uint32_t* flag, const uint32_t* rank, const uint64_t* total_p,

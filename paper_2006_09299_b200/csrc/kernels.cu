@@ -1346,7 +1346,9 @@ void launch_fold(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
 // 131 K tiles into the percolating component, emit 1.9 -> 1.1 ms); with a few hundred tiles
 // per image the direct atomics are cheaper than the table (config 2: +4% emit with it).
 constexpr int FT_MIN_TILES = 8192;
-void launch_emit(const Geo& g, const Ws& ws0, cudaStream_t s) {
+// The three classes emit disjoint tiles: with a second stream (`s2`, with fork/join events) the
+// deferred classes run beside class S instead of after it (no tail between them).
+void launch_emit(const Geo& g, const Ws& ws0, cudaStream_t s, cudaStream_t s2, cudaEvent_t fork, cudaEvent_t join) {
     const bool sharded = g.tpi >= FT_MIN_TILES;
     Ws ws = ws0;
     if (sharded) {
@@ -1355,9 +1357,16 @@ void launch_emit(const Geo& g, const Ws& ws0, cudaStream_t s) {
     } else {
         ws.ftkey = nullptr;
     }
+    const cudaStream_t sd = s2 ? s2 : s;
+    if (s2) {
+        cudaEventRecord(fork, s);
+        cudaStreamWaitEvent(s2, fork, 0);
+    }
+    k_emit_m<<<148 * 4, CapME::BT, sizeof(EmitSmem<CapME>), sd>>>(g, ws);
+    k_emit_full<<<148 * 2, CapFE::BT, sizeof(EmitSmem<CapFE>), sd>>>(g, ws);
+    if (s2) cudaEventRecord(join, s2);
     k_emit<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(EmitSmem<CapSE>), s>>>(g, ws);
-    k_emit_m<<<148 * 4, CapME::BT, sizeof(EmitSmem<CapME>), s>>>(g, ws);
-    k_emit_full<<<148 * 2, CapFE::BT, sizeof(EmitSmem<CapFE>), s>>>(g, ws);
+    if (s2) cudaStreamWaitEvent(s, join, 0);
     if (sharded) k_ftab_flush<<<FT_SHARDS * FT_HS / 256, 256, 0, s>>>(ws);
 }
 void launch_surv_flags(const uint32_t* top, const uint64_t* cbase, int32_t B, uint64_t total, uint32_t* flag,
