@@ -253,6 +253,26 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
 
 namespace rlh {
 
+// Horizontal and vertical seams of tile rows [ty0, ty1) concurrently (both only unite border
+// nodes, lock-free): the vertical ones on a stream forked from and joined back into `s`.
+// Returns the number of launches.
+int enqueue_seams(rl_ctx* ctx, const Geo& g, const Ws& ws, cudaStream_t s) {
+    const int32_t rows = g.ty1 - g.ty0;
+    const bool fork = ctx->seam_stream && g.ntx > 1 && !ctx->ktimes;
+    if (fork) {
+        cudaEventRecord(ctx->seam_fork, s);
+        cudaStreamWaitEvent(ctx->seam_stream, ctx->seam_fork, 0);
+        launch_seam_cols(g, ws, ctx->seam_stream, ctx->sms);
+        cudaEventRecord(ctx->seam_join, ctx->seam_stream);
+    }
+    if (rows > 1) launch_seam_rows(g, ws, g.ty0, rows - 1, s, ctx->sms);
+    if (fork)
+        cudaStreamWaitEvent(s, ctx->seam_join, 0);
+    else
+        launch_seam_cols(g, ws, s, ctx->sms);
+    return (rows > 1) + (g.ntx > 1);
+}
+
 // Phase-timing event.  Inside a stream capture a plain record only becomes an internal graph
 // dependency; the external flag makes it a real event record node that replays time.
 void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
@@ -377,22 +397,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     launches += 3;
     record_event(ctx->ev[1], s, use_graph);
     kt();
-    // horizontal and vertical seams concurrently (both only unite border nodes, lock-free):
-    // the vertical ones on a stream forked from and joined back into the pipeline stream
-    const bool fork = ctx->seam_stream && g.ntx > 1 && !ctx->ktimes;
-    if (fork) {
-        cudaEventRecord(ctx->seam_fork, s);
-        cudaStreamWaitEvent(ctx->seam_stream, ctx->seam_fork, 0);
-        launch_seam_cols(g, ws, ctx->seam_stream, ctx->sms);
-        cudaEventRecord(ctx->seam_join, ctx->seam_stream);
-    }
-    if (g.nty > 1) launch_seam_rows(g, ws, 0, g.nty - 1, s, ctx->sms);
-    kt();
-    if (fork)
-        cudaStreamWaitEvent(s, ctx->seam_join, 0);
-    else
-        launch_seam_cols(g, ws, s, ctx->sms);
-    launches += (g.nty > 1) + (g.ntx > 1);
+    launches += enqueue_seams(ctx, g, ws, s);
     kt();
     const int64_t hint = (int64_t)ctx->cap_nodes;
     launch_resolve(g, ws, s, ctx->sms, hint);  // + representatives and their counts

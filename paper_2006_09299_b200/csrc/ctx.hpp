@@ -20,7 +20,6 @@ void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t init, vo
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s);
 void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms);
 void launch_seam_cols(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
-void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
 void launch_resolve(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
 void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);
 void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
@@ -176,6 +175,7 @@ struct rl_ctx {
 
 namespace rlh {
 using namespace rlg;
+int enqueue_seams(rl_ctx* ctx, const Geo& g, const Ws& ws, cudaStream_t s);
 int set_err(rl_ctx* c, int code, const std::string& msg);
 int cuda_fail(rl_ctx* c, cudaError_t e, const char* what);
 bool ensure(DevBuf& b, size_t bytes);

@@ -1307,12 +1307,6 @@ void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t
     k_analyze_full<<<148 * 2, CapF::BT, sizeof(AnalyzeSmem<CapF>), s>>>(pix, g, ws);
 }
 void launch_seam_cols(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
-// seams inside tile rows [ty0, ty1)
-void launch_seams(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
-    const int32_t rows = g.ty1 - g.ty0;
-    if (rows > 1) launch_seam_rows(g, ws, g.ty0, rows - 1, s, sms);
-    launch_seam_cols(g, ws, s, sms);
-}
 void launch_seam_cols(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
     const int32_t rows = g.ty1 - g.ty0;
     if (g.ntx > 1) {

@@ -171,6 +171,7 @@ __device__ __forceinline__ uint32_t cut_root(const Geo& g, const Ws& ws, int64_t
 }
 
 __global__ void k_strip_mark(Geo g, Ws ws, uint32_t* flag, int top, int bot) {
+    if (ws.counters[1]) return;  // capacity overflow: nodes missing, the phase re-runs
     GRID_LOOP(i, 2 * (int64_t)g.W) {
         if ((i < g.W && !top) || (i >= g.W && !bot)) continue;
         uint32_t val;
@@ -271,8 +272,10 @@ __global__ void k_g_init(GTab T, int64_t C) {
     }
 }
 
-// cut q: the bottom row of strip q against the top row of strip q + 1
-__global__ void k_g_cut(XSrc X, GTab T, int32_t q, int32_t W, uint32_t v8) {
+// cut q = blockIdx.y: the bottom row of strip q against the top row of strip q + 1 (all cuts in
+// one launch)
+__global__ void k_g_cut(XSrc X, GTab T, int32_t W, uint32_t v8) {
+    const int32_t q = blockIdx.y;
     const uint32_t* up = reinterpret_cast<const uint32_t*>(X.buf + (size_t)q * X.L.bytes + X.L.cut) + W;
     const uint32_t* dn = reinterpret_cast<const uint32_t*>(X.buf + (size_t)(q + 1) * X.L.bytes + X.L.cut);
     const uint32_t cu0 = T.coff[q] - 1u, cd0 = T.coff[q + 1] - 1u;
@@ -290,20 +293,36 @@ __global__ void k_g_cut(XSrc X, GTab T, int32_t q, int32_t W, uint32_t v8) {
     }
 }
 
-// roots, folded features and min keys; the strips' exterior partials fold into class 0
-__global__ void k_g_fold(XSrc X, GTab T, int64_t C) {
-    GRID_LOOP(i, C) {
+// roots, folded features and min keys; the strips' exterior partials fold into class 0.  The
+// percolating component's classes (one per strip and cut) all fold into one root: lanes and
+// blocks aggregate first (warp_fold + a shared table), as in k_resolve.
+__global__ void __launch_bounds__(256) k_g_fold(XSrc X, GTab T, int64_t C) {
+    __shared__ FoldTable<256> F;
+    F.init();
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < C; base += stride) {
+        const int64_t i = base + (threadIdx.x & 31);
+        uint32_t dst = FT_EMPTY;
+        Acc f;
+        unsigned long long key = ~0ull;
         if (i == 0) {
             T.root[0] = 0;
-            continue;
+        } else if (i < C) {
+            const uint32_t root = gfind_ro(T.uf, (uint32_t)i);
+            T.root[i] = root;
+            const int32_t q = strip_of(T, X.k, (uint32_t)i);
+            const XClass& x = xclass(X, q, (uint32_t)i - T.coff[q] + 1u);
+            dst = root;
+            f = x.acc;
+            if (root) key = x.key;
         }
-        const uint32_t root = gfind_ro(T.uf, (uint32_t)i);
-        T.root[i] = root;
-        const int32_t q = strip_of(T, X.k, (uint32_t)i);
-        const XClass& x = xclass(X, q, (uint32_t)i - T.coff[q] + 1u);
-        acc_atomic_fold(T.tot + root, x.acc);
-        if (root) atomicMin(reinterpret_cast<unsigned long long*>(T.kmin + root), (unsigned long long)x.key);
+        warp_fold(F, dst, f, key, [&](uint32_t k) { return T.tot + k; },
+                  [&](uint32_t k) { return reinterpret_cast<unsigned long long*>(T.kmin + k); });
     }
+    __syncthreads();
+    F.flush([&](uint32_t k) { return T.tot + k; },
+            [&](uint32_t k) { return reinterpret_cast<unsigned long long*>(T.kmin + k); });
     GRID_LOOP(q, X.k) acc_atomic_fold(T.tot, xclass(X, (int32_t)q, 0).acc);
 }
 
@@ -590,17 +609,43 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         cudaMemsetAsync(ws.cnt + std::min<int64_t>((int64_t)g.ty1 * TH, H) * g.ntx, 0, 4, s);
         launch_analyze(d_strip, g, ws, s);
         STRIP_STEP(ctx, "launch_analyze");
-        launch_seams(g, ws, s, ctx->sms);
+        enqueue_seams(ctx, g, ws, s);
         STRIP_STEP(ctx, "launch_seams");
         k_strip_left<<<grid((int64_t)ctx->cap_nodes, ctx->sms), 256, 0, s>>>(g, ws);
         STRIP_STEP(ctx, "k_strip_left");
         ctx->launches = 3 + (g.ty1 - g.ty0 > 1) + (g.ntx > 1) + 1;
+        // flatten inside the strip; cut classes = roots seen on a cut row, numbered by a scan.
+        // No host round trip in between: grids and tables are sized by the node capacity (the
+        // kernels read the node count on the device), and a capacity overflow is found at the
+        // phase's one synchronisation below (the host then grows the tables and re-runs)
+        const int64_t nmax = (int64_t)ctx->cap_nodes;
+        k_strip_exterior<<<1, 1, 0, s>>>(ws);
+        STRIP_STEP(ctx, "k_strip_exterior");
+        launch_resolve(g, ws, s, ctx->sms, nmax);
+        STRIP_STEP(ctx, "launch_resolve");
+        uint32_t* flag = P<uint32_t>(ctx->flag);
+        uint32_t* rank = P<uint32_t>(ctx->rank);
+        cudaMemsetAsync(flag, 0, (size_t)(nmax + 1) * 4, s);
+        cudaMemsetAsync(ws.ncut, 0, (size_t)(nmax + 1) * 4, s);
+        k_strip_mark<<<grid(2 * (int64_t)w, ctx->sms), 256, 0, s>>>(g, ws, flag, top, bot);
+        STRIP_STEP(ctx, "k_strip_mark");
+        launch_scan(flag, rank, nmax + 1, 0u, ctx->cub_tmp.p, s);
+        unsigned long long* cnt2 = P<unsigned long long>(ctx->scount);
+        cudaMemsetAsync(cnt2, 0, 16, s);
+        k_strip_count<<<grid(std::max<int64_t>(nmax, (int64_t)(g.ty1 - g.ty0) * TH * g.ntx), ctx->sms), 256, 0, s>>>(
+            g, ws, flag, rank, P<uint32_t>(ctx->xnode), cnt2);
+        STRIP_STEP(ctx, "k_strip_count");
         uint32_t hc[8] = {};
         cudaMemcpyAsync(hc, ws.counters, 32, cudaMemcpyDeviceToHost, s);
         uint32_t fg = 0;
         cudaMemcpyAsync(&fg, ws.img_fg, 4, cudaMemcpyDeviceToHost, s);
         unsigned long long rused = 0;
         cudaMemcpyAsync(&rused, ws.rused, 8, cudaMemcpyDeviceToHost, s);
+        uint32_t klast[2] = {};
+        unsigned long long hcnt[2] = {};
+        cudaMemcpyAsync(&klast[0], rank + nmax, 4, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&klast[1], flag + nmax, 4, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(hcnt, cnt2, 16, cudaMemcpyDeviceToHost, s);
         if ((rc = sync_err(ctx, "strip local"))) return rc;
         if (hc[1] & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip left link)");
         if (hc[1] & (ERR_NODE_CAP | ERR_RSTORE_CAP)) {
@@ -609,29 +654,6 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
             continue;
         }
         const int64_t n_local = hc[0];
-        // flatten inside the strip; cut classes = roots seen on a cut row, numbered by a scan
-        k_strip_exterior<<<1, 1, 0, s>>>(ws);
-        STRIP_STEP(ctx, "k_strip_exterior");
-        launch_resolve(g, ws, s, ctx->sms, n_local);
-        STRIP_STEP(ctx, "launch_resolve");
-        uint32_t* flag = P<uint32_t>(ctx->flag);
-        uint32_t* rank = P<uint32_t>(ctx->rank);
-        cudaMemsetAsync(flag, 0, (size_t)(n_local + 1) * 4, s);
-        cudaMemsetAsync(ws.ncut, 0, (size_t)(n_local + 1) * 4, s);
-        k_strip_mark<<<grid(2 * (int64_t)w, ctx->sms), 256, 0, s>>>(g, ws, flag, top, bot);
-        STRIP_STEP(ctx, "k_strip_mark");
-        launch_scan(flag, rank, n_local + 1, 0u, ctx->cub_tmp.p, s);
-        unsigned long long* cnt2 = P<unsigned long long>(ctx->scount);
-        cudaMemsetAsync(cnt2, 0, 16, s);
-        k_strip_count<<<grid(std::max<int64_t>(n_local, (int64_t)(g.ty1 - g.ty0) * TH * g.ntx), ctx->sms), 256, 0, s>>>(
-            g, ws, flag, rank, P<uint32_t>(ctx->xnode), cnt2);
-        STRIP_STEP(ctx, "k_strip_count");
-        uint32_t klast[2] = {};
-        unsigned long long hcnt[2] = {};
-        cudaMemcpyAsync(&klast[0], rank + n_local, 4, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(&klast[1], flag + n_local, 4, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(hcnt, cnt2, 16, cudaMemcpyDeviceToHost, s);
-        if ((rc = sync_err(ctx, "strip local classes"))) return rc;
         ctx->launches += 6;
         ctx->ws = ws;
         ctx->geo = g;
@@ -707,7 +729,9 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     k_g_init<<<grid(C, ctx->sms), 256, 0, s>>>(T, C);
     STRIP_STEP(ctx, "k_g_init");
     const uint32_t v8 = g.flip ? 0u : 1u;
-    for (int q = 0; q + 1 < n_strips; ++q) k_g_cut<<<grid(g.W, ctx->sms), 256, 0, s>>>(X, T, q, g.W, v8);
+    if (n_strips > 1)
+        k_g_cut<<<dim3((unsigned)std::min<int64_t>((g.W + 255) / 256, 4096), (unsigned)(n_strips - 1)), 256, 0, s>>>(
+            X, T, g.W, v8);
     STRIP_STEP(ctx, "k_g_cut");
     k_g_fold<<<grid(C, ctx->sms), 256, 0, s>>>(X, T, C);
     STRIP_STEP(ctx, "k_g_fold");
@@ -766,7 +790,7 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     if (err & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip links)");
     ctx->ws = ws;
     ctx->geo = g;
-    ctx->launches += 4 + (n_strips - 1) + 6;
+    ctx->launches += 4 + (n_strips > 1) + 6;
     out->d_links = T.links;
     out->n = 2 * C;
     S->phase = 3;
@@ -796,7 +820,10 @@ int rl_strip_resolve(rl_ctx* ctx, rl_strip_partials* out) {
     uint32_t* isurv = P<uint32_t>(ctx->scount) + 4;
     we.img_surv = isurv;
     cudaMemsetAsync(isurv, 0, 4, s);
-    launch_emit(g, we, s);
+    if (ctx->seam_stream)
+        launch_emit(g, we, s, ctx->seam_stream, ctx->seam_fork, ctx->seam_join);
+    else
+        launch_emit(g, we, s);
     STRIP_STEP(ctx, "launch_emit");
     launch_fold(g, ws, s, ctx->sms, S->n_local);  // border non-survivors of this strip
     STRIP_STEP(ctx, "launch_fold");
