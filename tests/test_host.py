@@ -246,3 +246,24 @@ def test_strip_collectives_gloo():
         assert gathered == [1] * 16 + [2] * 16
         assert links == [7, -1, 8, -2, 0, 0]
         assert psum == [3, 3, 3] and pmin == [4, 7] and pmax == [5, 8] and pcnt == [4]
+
+
+def test_bench_reference_arm_json_contract():
+    """`bench.py --impl reference` (the driver's reference arm): one JSON line with the contract's
+    keys, the reference's own CPU path from oracle/_ref, same metric/config as our arm."""
+    import json
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg1",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    if "unavailable" in line:
+        pytest.skip(line["unavailable"])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["unit"] == "Gpixel/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    import bench
+    assert line["metric"] == bench.METRIC and line["config"]["workload"].startswith("cfg1")
