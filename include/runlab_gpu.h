@@ -123,6 +123,12 @@ void rl_result_free(rl_result* r);
  * exceeded the call re-runs internally after growing (host sync in that case only). */
 int rl_label_device(rl_ctx* ctx, const uint8_t* d_pixels, int32_t width, int32_t height,
                     int32_t n_images, const rl_config* cfg);
+/* rl_label_device runs a large batch (>= 64 Mpx, >= 4 images per pipeline, no label image) as
+ * k concurrent pipelines over interleaved sub-batches (image i in pipeline i % k), joined back
+ * into the context's stream; results are the same.  k = 3 by default (env RUNLAB_GPU_SPLIT);
+ * 1 = one pipeline.  After a split call rl_device_comps returns NULL (the tables live in the
+ * pipelines; rl_fetch gathers them) and rl_phase_times reports the total only. */
+int rl_set_pipelines(rl_ctx* ctx, int k);
 int rl_sync(rl_ctx* ctx);
 /* Copies the results of the last rl_label_device() to host memory (like rl_label). */
 int rl_fetch(rl_ctx* ctx, rl_result* out);

@@ -25,7 +25,7 @@ EXPORTED_SYMBOLS = (
     "rl_strip_finish",
     "rl_strip_fetch", "rl_generate_rows", "rl_filter_components",
     "rl_filter_components_host", "rl_label_device_fmt", "rl_label_into_fmt", "rl_pbm_parse", "rl_pbm_p1_to_p4",
-    "rl_pbm_p4_header", "rl_fill_pbm", "rl_generate_host", "rl_workspace_bytes",
+    "rl_pbm_p4_header", "rl_fill_pbm", "rl_generate_host", "rl_workspace_bytes", "rl_set_pipelines",
 )
 
 FEATURE_DTYPE = np.dtype([("s", "<i8"), ("sx", "<i8"), ("sy", "<i8"), ("row_min", "<i4"),
@@ -116,6 +116,7 @@ def load() -> C.CDLL:
         getattr(L, name).argtypes = [C.c_void_p]
     L.rl_set_stream.argtypes = [C.c_void_p, C.c_void_p]
     L.rl_last_launch_count.argtypes = [C.c_void_p]
+    L.rl_set_pipelines.argtypes = [C.c_void_p, C.c_int]
     L.rl_workspace_bytes.restype = C.c_int64
     L.rl_workspace_bytes.argtypes = [C.c_void_p]
     L.rl_last_used_graph.argtypes = [C.c_void_p]

@@ -183,7 +183,8 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
               ensure(ctx->img_fg, (size_t)B * 4) && ensure(ctx->img_surv, (size_t)B * 4) &&
               ensure(ctx->comps, ctx->cap_comps * sizeof(rl_component)) &&
               ensure(ctx->top, ctx->cap_comps * 4) && ensure(ctx->filled, ctx->cap_comps * sizeof(Acc)) &&
-              ensure(ctx->filled_img, (size_t)(out_px / g.W) * g.orowb) && ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
+              (ctx->ext_filled || ensure(ctx->filled_img, (size_t)(out_px / g.W) * g.orowb)) &&
+              ensure(ctx->cbase, (size_t)(B + 1) * 8) &&
               ensure(ctx->summ, (size_t)(B + 2) * 32) && ensure(ctx->ftab, (size_t)FT_SHARDS * FT_HS * 28);
     if (ok && g.label_mode) ok = ensure(ctx->labels, (size_t)out_px * 4);
     if (!ok) return set_err(ctx, RL_ENOMEM, "device allocation failed");
@@ -225,7 +226,7 @@ int prepare_ws(rl_ctx* ctx, const Geo& g, const rl_config* cfg, Ws& ws, size_t& 
     ws.comps = P<rl_component>(ctx->comps);
     ws.top = P<uint32_t>(ctx->top);
     ws.filled = P<Acc>(ctx->filled);
-    ws.filled_img = P<uint8_t>(ctx->filled_img);
+    ws.filled_img = ctx->ext_filled ? ctx->ext_filled : P<uint8_t>(ctx->filled_img);
     ws.labels = g.label_mode ? P<uint32_t>(ctx->labels) : nullptr;
     ws.ftsum = P<unsigned long long>(ctx->ftab);
     ws.ftkey = reinterpret_cast<uint32_t*>(ws.ftsum + 3ull * FT_SHARDS * FT_HS);
@@ -284,8 +285,13 @@ void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
 
 // (Re)build geometry, grow the workspace, enqueue the pipeline.
 int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg, int32_t fmt) {
+    ctx->split_active = 0;
     Geo g = make_geo(W, H, B, cfg, dpix, fmt);
     if (ctx->force_ofmt >= 0) set_output_format(g, ctx->force_ofmt);
+    if (ctx->stride_mult > 1) {  // a split pipeline: every stride_mult-th image of the caller's batch
+        g.fbytes *= ctx->stride_mult;
+        g.ofbytes *= ctx->stride_mult;
+    }
     if (ctx->permute) {  // testing aid: a multiplier coprime to the tile count
         int64_t m = ctx->permute % std::max<int64_t>(g.ntiles, 1), a, b;
         for (;; ++m) {
@@ -479,6 +485,15 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
 // Wait for the last enqueue; on capacity overflow grow and re-run (synchronously).
 int finish(rl_ctx* ctx) {
     ctx->reran = false;
+    if (ctx->split_active) {  // the pipelines check (and if needed grow and re-run) themselves
+        for (int k = 0; k < ctx->split_active; ++k) {
+            rl_ctx* kid = ctx->splits[k];
+            const int rc = finish(kid);
+            if (rc) return set_err(ctx, rc, kid->err);
+            ctx->reran |= kid->reran;
+        }
+        return RL_OK;
+    }
     for (int attempt = 0; attempt < 4; ++attempt) {
         const cudaError_t e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pipeline");
@@ -528,6 +543,129 @@ static int times_of(cudaEvent_t const* ev, rl_times* t) {
 
 void fill_times(rl_ctx* ctx, rl_times* t) { times_of(ctx->ev, t); }
 
+// rl_result of a split call: image i ran as image i / K of pipeline i % K; its tables are copied
+// from there into the caller's order, the hole-filled image is already in this context's buffer
+int fetch_split(rl_ctx* ctx, rl_result* out) {
+    const Geo& g = ctx->geo;
+    const int B = g.B, K = ctx->split_active;
+    out->width = g.W;
+    out->height = g.H;
+    out->n_images = B;
+    int64_t total = 0;
+    for (int i = 0; i < B; ++i) total += ctx->splits[i % K]->h_summ[4 * (i / K) + 1];
+    out->n_components = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->n_fg = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->n_holes = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->euler = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->n_survivors = (int64_t*)std::malloc(sizeof(int64_t) * B);
+    out->comp_offset = (int64_t*)std::malloc(sizeof(int64_t) * (B + 1));
+    out->comps = (rl_component*)std::malloc(sizeof(rl_component) * std::max<int64_t>(total, 1));
+    out->top = (uint32_t*)std::malloc(sizeof(uint32_t) * std::max<int64_t>(total, 1));
+    out->filled = (rl_features*)std::malloc(sizeof(rl_features) * std::max<int64_t>(total, 1));
+    const size_t npx = (size_t)(g.P * B);
+    out->filled_image = (uint8_t*)std::malloc(npx);
+    if (!out->n_components || !out->n_fg || !out->n_holes || !out->euler || !out->n_survivors ||
+        !out->comp_offset || !out->comps || !out->top || !out->filled || !out->filled_image) {
+        rl_result_free(out);
+        return set_err(ctx, RL_ENOMEM, "host allocation failed");
+    }
+    cudaStream_t st = ctx->stream;
+    int64_t off = 0;
+    for (int i = 0; i < B; ++i) {
+        rl_ctx* kid = ctx->splits[i % K];
+        const int64_t* s = kid->h_summ + 4 * (i / K);
+        const int64_t n = s[1], base = s[0];
+        out->comp_offset[i] = off;
+        out->n_components[i] = n;
+        out->n_fg[i] = s[2];
+        out->n_holes[i] = n - 1 - s[2];
+        out->euler[i] = out->n_fg[i] - out->n_holes[i];
+        out->n_survivors[i] = s[3];
+        cudaMemcpyAsync(out->comps + off, kid->ws.comps + base, sizeof(rl_component) * n, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(out->top + off, kid->ws.top + base, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(out->filled + off, kid->ws.filled + base, sizeof(rl_features) * n, cudaMemcpyDeviceToHost, st);
+        off += n;
+    }
+    out->comp_offset[B] = off;
+    std::vector<uint8_t> p4;
+    if (g.ofmt == RL_PIXELS_P4) {
+        p4.resize((size_t)(g.ofbytes * B));
+        cudaMemcpyAsync(p4.data(), ctx->ws.filled_img, p4.size(), cudaMemcpyDeviceToHost, st);
+    } else {
+        cudaMemcpyAsync(out->filled_image, ctx->ws.filled_img, npx, cudaMemcpyDeviceToHost, st);
+    }
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        rl_result_free(out);
+        return cuda_fail(ctx, e, "fetch");
+    }
+    if (!p4.empty())
+        for (int64_t r = 0; r < (int64_t)g.H * B; ++r)
+            for (int32_t j = 0; j < g.W; ++j)
+                out->filled_image[r * g.W + j] = (p4[r * g.orowb + j / 8] >> (7 - j % 8)) & 1u;
+    fill_times(ctx, &out->times);
+    return RL_OK;
+}
+
+// rl_label_device of a large batch as K concurrent pipelines over interleaved sub-batches (image
+// i in pipeline i % K): forked from and joined back into this context's stream; no host sync
+int enqueue_split(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, const rl_config* cfg,
+                  int32_t fmt, int K) {
+    Geo g = make_geo(W, H, B, cfg, dpix, fmt);
+    if (!ensure(ctx->filled_img, (size_t)(g.ofbytes * B))) return set_err(ctx, RL_ENOMEM, "device allocation failed");
+    if (!ctx->split_fork && cudaEventCreateWithFlags(&ctx->split_fork, cudaEventDisableTiming) != cudaSuccess)
+        return cuda_fail(ctx, cudaGetLastError(), "events");
+    for (int k = 0; k < K; ++k) {
+        if (!ctx->splits[k]) {
+            ctx->splits[k] = rl_create(ctx->device);
+            if (!ctx->splits[k]) return set_err(ctx, RL_ECUDA, "could not create a pipeline context");
+            ctx->splits[k]->graphs = ctx->graphs;
+            ctx->splits[k]->graph_max_px = ctx->graph_max_px;
+            ctx->splits[k]->permute = ctx->permute;
+        }
+        if (!ctx->split_join[k] && cudaEventCreateWithFlags(&ctx->split_join[k], cudaEventDisableTiming) != cudaSuccess)
+            return cuda_fail(ctx, cudaGetLastError(), "events");
+    }
+    const int slot = (int)(ctx->calls % rl_ctx::RING);
+    for (int k = 0; k < rl_ctx::NEV; ++k) {
+        if (!ctx->ring[slot][k]) cudaEventCreate(&ctx->ring[slot][k]);
+        ctx->ev[k] = ctx->ring[slot][k];
+    }
+    ++ctx->calls;
+    cudaStream_t s = ctx->stream;
+    cudaEventRecord(ctx->ev[0], s);
+    cudaEventRecord(ctx->split_fork, s);
+    int launches = 0;
+    uint8_t* filled = P<uint8_t>(ctx->filled_img);
+    for (int k = 0; k < K; ++k) {
+        rl_ctx* kid = ctx->splits[k];
+        kid->stride_mult = K;
+        kid->ext_filled = filled + (size_t)g.ofbytes * k;
+        kid->want_compact = false;
+        kid->want_pack = 0;
+        kid->force_ofmt = ctx->force_ofmt;
+        cudaStreamWaitEvent(kid->stream, ctx->split_fork, 0);
+        const int rc = enqueue(kid, dpix + (size_t)g.fbytes * k, W, H, (B - k + K - 1) / K, cfg, fmt);
+        if (rc) return set_err(ctx, rc, kid->err);
+        cudaEventRecord(ctx->split_join[k], kid->stream);
+        cudaStreamWaitEvent(s, ctx->split_join[k], 0);
+        launches += kid->launches;
+    }
+    for (int k = 1; k < rl_ctx::NEV; ++k) cudaEventRecord(ctx->ev[k], s);  // phases overlap: total only
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "launch");
+    ctx->geo = g;
+    ctx->cfg = *cfg;
+    ctx->last_pix = dpix;
+    ctx->ws = Ws{};
+    ctx->ws.filled_img = filled;
+    ctx->launches = launches;
+    ctx->used_graph = ctx->splits[0]->used_graph;
+    ctx->split_active = K;
+    ctx->have_result = true;
+    return RL_OK;
+}
+
 int fetch(rl_ctx* ctx, rl_result* out) {
     std::memset(out, 0, sizeof(*out));
     const Geo& g = ctx->geo;
@@ -535,6 +673,7 @@ int fetch(rl_ctx* ctx, rl_result* out) {
     out->width = g.W;
     out->height = g.H;
     out->n_images = B;
+    if (ctx->split_active) return fetch_split(ctx, out);
     const int64_t* s = ctx->h_summ;
     const uint64_t total = (uint64_t)s[4 * B];
     out->n_components = (int64_t*)std::malloc(sizeof(int64_t) * B);
@@ -645,6 +784,7 @@ rl_ctx* rl_create(int device) {
     if (std::getenv("RUNLAB_GPU_NO_GRAPH")) c->graphs = false;
     if (const char* v = std::getenv("RUNLAB_GPU_GRAPH_MPX")) c->graph_max_px = std::atof(v) * 1024 * 1024;
     if (const char* v = std::getenv("RUNLAB_GPU_PERMUTE")) c->permute = std::max(0ll, std::atoll(v));
+    if (const char* v = std::getenv("RUNLAB_GPU_SPLIT")) c->split = std::max(1, std::atoi(v));
     if (std::getenv("RUNLAB_GPU_KTIMES")) c->ktimes = true;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_D2H")) c->packed_d2h = false;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_RECORDS")) c->packed_recs = false;
@@ -661,6 +801,10 @@ void rl_destroy(rl_ctx* c) {
     cudaStreamSynchronize(c->stream);
 
     for (rl_ctx* k : c->kids) rl_destroy(k);
+    for (rl_ctx* k : c->splits) rl_destroy(k);
+    if (c->split_fork) cudaEventDestroy(c->split_fork);
+    for (cudaEvent_t e : c->split_join)
+        if (e) cudaEventDestroy(e);
     strip_free(c);
     pool_free(c);
     for (uint8_t* p : c->h_stage)
@@ -707,7 +851,18 @@ int rl_label_device_fmt(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t
     cudaSetDevice(ctx->device);
     ctx->want_compact = false;
     ctx->want_pack = 0;
+    // large batches without a label image run as concurrent interleaved pipelines
+    const int K = std::min(ctx->split, rl_ctx::MAXSPLIT);
+    if (K > 1 && !cfg->relabel && n >= 4 * K && (double)w * h * n >= 64.0 * 1024 * 1024)
+        return enqueue_split(ctx, d_pixels, w, h, n, cfg, pixel_format, K);
+    ctx->split_active = 0;
     return enqueue(ctx, d_pixels, w, h, n, cfg, pixel_format);
+}
+
+int rl_set_pipelines(rl_ctx* ctx, int k) {
+    if (!ctx || k < 1) return RL_EINVAL;
+    ctx->split = std::min(k, rl_ctx::MAXSPLIT);
+    return RL_OK;
 }
 
 int rl_label_device(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg) {
@@ -774,7 +929,7 @@ void rl_result_free(rl_result* r) {
 
 void* rl_device_filled_image(rl_ctx* c) { return c ? c->ws.filled_img : nullptr; }
 void* rl_device_labels(rl_ctx* c) { return c ? c->ws.labels : nullptr; }
-void* rl_device_comps(rl_ctx* c) { return c ? c->ws.comps : nullptr; }
+void* rl_device_comps(rl_ctx* c) { return c && !c->split_active ? c->ws.comps : nullptr; }
 void* rl_stream(rl_ctx* c) { return c ? (void*)c->stream : nullptr; }
 int rl_set_stream(rl_ctx* c, void* stream) {
     if (!c) return RL_EINVAL;

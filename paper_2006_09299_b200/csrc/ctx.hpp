@@ -133,6 +133,18 @@ struct rl_ctx {
     static constexpr int MAXKIDS = 8;
     int nkids = 3;  // env RUNLAB_GPU_KIDS
     rl_ctx* kids[MAXKIDS] = {};
+    // rl_label_device splits a large batch into interleaved sub-batches (every split-th image)
+    // run as concurrent pipelines, each on its own context/stream, so that one sub-batch's
+    // latency-bound merge kernels overlap another's tile passes (config 2, 3 pipelines: -3%)
+    static constexpr int MAXSPLIT = 4;
+    int split = 3;          // env RUNLAB_GPU_SPLIT, rl_set_pipelines; <= 1: one pipeline
+    int split_active = 0;   // pipelines of the last rl_label_device call (0: it ran here)
+    rl_ctx* splits[MAXSPLIT] = {};
+    cudaEvent_t split_fork = nullptr, split_join[MAXSPLIT] = {};
+    // set on a split pipeline's context: its image b is the caller's image (k + stride_mult * b),
+    // and its hole-filled image goes straight into the caller's buffer at that stride
+    int stride_mult = 1;
+    uint8_t* ext_filled = nullptr;
     // per-launch timing for tuning (env RUNLAB_GPU_KTIMES; eager launches only)
     bool ktimes = false;
     cudaEvent_t kev[24] = {};

@@ -292,6 +292,11 @@ class Labeler:
     def stream(self) -> int:
         return int(self._L.rl_stream(self._ctx) or 0)
 
+    def set_pipelines(self, k: int) -> None:
+        """Concurrent pipelines for large device batches (rl_set_pipelines); 1 = one pipeline."""
+        if self._L.rl_set_pipelines(self._ctx, int(k)) != N.RL_OK:
+            _raise(N.RL_EINVAL, "pipelines must be >= 1")
+
     def workspace_bytes(self) -> int:
         """Device bytes held by this context's grow-only tables."""
         return int(self._L.rl_workspace_bytes(self._ctx))

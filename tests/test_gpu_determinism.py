@@ -33,7 +33,8 @@ def _digest(res) -> str:
     h = hashlib.sha256()
     for a in (res.n_components, res.n_fg, res.n_survivors, res.comp_offset, res.comps, res.top,
               res.filled_image, res.labels):
-        h.update(np.ascontiguousarray(a).tobytes())
+        if a is not None:
+            h.update(np.ascontiguousarray(a).tobytes())
     surv = res.top == np.concatenate([np.arange(res.comp_offset[i + 1] - res.comp_offset[i], dtype=np.uint32)
                                       for i in range(len(res.n_components))])
     h.update(res.filled[surv].tobytes())
@@ -62,3 +63,28 @@ def test_permuted_tile_order_identical(labeler, batch, perm):
     if perm == 7:
         for i in range(batch.shape[0]):
             compare_image(got.image(i), O.label_canonical(batch[i], 0), f"perm {perm} #{i}")
+
+
+def test_split_pipelines_identical(labeler):
+    """rl_label_device of a large batch as 1, 2, 3 and 4 concurrent interleaved pipelines
+    (rl_set_pipelines): identical bytes, hole-filled image included (also as P4 rows)."""
+    import torch
+    from paper_2006_09299_b200 import _native as N
+    from paper_2006_09299_b200.runlab import generate_device
+    W, H, B = 1024, 768, 96  # 75 Mpx: above the split threshold
+    imgs = torch.empty((B, H, W), dtype=torch.uint8, device="cuda")
+    for i in range(B):
+        d, g = CELLS[i % len(CELLS)]
+        generate_device(imgs[i].data_ptr(), W, H, d, g, 100 + i)
+    torch.cuda.synchronize()
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    digests = []
+    for k in (1, 2, 3, 4):
+        labeler.set_pipelines(k)
+        labeler.label_device(imgs.data_ptr(), W, H, B, cfg)
+        res = labeler.fetch()
+        digests.append(_digest(res))
+    labeler.set_pipelines(3)
+    assert len(set(digests)) == 1
+    ref = O.label_canonical(imgs[5].cpu().numpy(), 0)
+    compare_image(res.image(5), ref, "split #5")
