@@ -39,7 +39,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Gpixel/s full FG/BG CCA (features+Euler+tree+hole fill); % of HBM roofline"
-PIPELINES = 3  # concurrent pipelines per large device batch (rl_set_pipelines; the library default)
+# concurrent pipelines per large device batch (rl_set_pipelines; the library default 3; env
+# RUNLAB_GPU_SPLIT=1 for one pipeline, e.g. for per-kernel profiles of the whole batch)
+PIPELINES = int(os.environ.get("RUNLAB_GPU_SPLIT", "3"))
 
 
 # ------------------------------------------------------------------------------ workloads
