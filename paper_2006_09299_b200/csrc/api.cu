@@ -785,6 +785,7 @@ rl_ctx* rl_create(int device) {
     if (const char* v = std::getenv("RUNLAB_GPU_GRAPH_MPX")) c->graph_max_px = std::atof(v) * 1024 * 1024;
     if (const char* v = std::getenv("RUNLAB_GPU_PERMUTE")) c->permute = std::max(0ll, std::atoll(v));
     if (const char* v = std::getenv("RUNLAB_GPU_SPLIT")) c->split = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("RUNLAB_GPU_SPLIT_MPX")) c->split_min_px = std::atof(v) * 1024 * 1024;
     if (std::getenv("RUNLAB_GPU_KTIMES")) c->ktimes = true;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_D2H")) c->packed_d2h = false;
     if (std::getenv("RUNLAB_GPU_NO_PACKED_RECORDS")) c->packed_recs = false;
@@ -853,7 +854,7 @@ int rl_label_device_fmt(rl_ctx* ctx, const uint8_t* d_pixels, int32_t w, int32_t
     ctx->want_pack = 0;
     // large batches without a label image run as concurrent interleaved pipelines
     const int K = std::min(ctx->split, rl_ctx::MAXSPLIT);
-    if (K > 1 && !cfg->relabel && n >= 4 * K && (double)w * h * n >= 64.0 * 1024 * 1024)
+    if (K > 1 && !cfg->relabel && n >= 4 * K && (double)w * h * n >= ctx->split_min_px)
         return enqueue_split(ctx, d_pixels, w, h, n, cfg, pixel_format, K);
     ctx->split_active = 0;
     return enqueue(ctx, d_pixels, w, h, n, cfg, pixel_format);

@@ -138,6 +138,7 @@ struct rl_ctx {
     // latency-bound merge kernels overlap another's tile passes (config 2, 3 pipelines: -3%)
     static constexpr int MAXSPLIT = 4;
     int split = 3;          // env RUNLAB_GPU_SPLIT, rl_set_pipelines; <= 1: one pipeline
+    double split_min_px = 64.0 * 1024 * 1024;  // env RUNLAB_GPU_SPLIT_MPX
     int split_active = 0;   // pipelines of the last rl_label_device call (0: it ran here)
     rl_ctx* splits[MAXSPLIT] = {};
     cudaEvent_t split_fork = nullptr, split_join[MAXSPLIT] = {};
