@@ -480,19 +480,26 @@ __device__ __forceinline__ uint32_t gfind_ro(const uint32_t* uf, uint32_t a) {
 // to still be a root; a failed CAS continues from the parent it returned (a plain load could
 // keep returning a stale L1 copy).
 __device__ __forceinline__ void gunion_key(uint32_t* uf, const uint64_t* key, uint32_t a, uint32_t b, uint32_t B) {
+    // a root's key is loaded as soon as the root is known, so that its latency overlaps the
+    // other find
     a = gfind(uf, a);
+    uint64_t ka = a < B ? 0ull : key[a] + 1ull;
     for (;;) {
         b = gfind(uf, b);
         if (a == b) return;
-        const uint64_t ka = a < B ? 0ull : key[a] + 1ull, kb = b < B ? 0ull : key[b] + 1ull;
+        uint64_t kb = b < B ? 0ull : key[b] + 1ull;
         if (ka < kb) {  // link the later-keyed root under the earlier one
             const uint32_t t = a;
             a = b;
             b = t;
+            const uint64_t tk = ka;
+            ka = kb;
+            kb = tk;
         }
         const uint32_t old = atomicCAS(uf + a, a, b);
         if (old == a) return;
         a = gfind(uf, old);
+        ka = a < B ? 0ull : key[a] + 1ull;
     }
 }
 

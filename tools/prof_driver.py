@@ -75,7 +75,7 @@ def main():
         L.rl_debug_launch_times.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int]
         ms = (C.c_float * 16)()
         n = L.rl_debug_launch_times(lab.ctx, ms, 16)
-        names = ["analyze", "seam_h", "seam_v", "resolve", "scan", "cids", "tree", "emit"]
+        names = ["analyze", "seams", "resolve", "scan", "cids", "tree", "emit"]
         line["launch_ms"] = {names[k] if k < len(names) else str(k): round(ms[k], 4) for k in range(n)}
     print(json.dumps(line))
 
