@@ -42,6 +42,7 @@ METRIC = "Gpixel/s full FG/BG CCA (features+Euler+tree+hole fill); % of HBM roof
 # concurrent pipelines per large device batch (rl_set_pipelines; the library default 3; env
 # RUNLAB_GPU_SPLIT=1 for one pipeline, e.g. for per-kernel profiles of the whole batch)
 PIPELINES = int(os.environ.get("RUNLAB_GPU_SPLIT", "3"))
+BACKEND = "nccl"  # one process per GPU
 
 
 # ------------------------------------------------------------------------------ workloads
@@ -316,19 +317,19 @@ def run_strips(args, wl: Workload, rank: int, world: int, local: int) -> None:
 
     from paper_2006_09299_b200 import Labeler, LabelingConfig
     from paper_2006_09299_b200.runlab import generate_rows_device
-    from paper_2006_09299_b200.strips import TorchCollectives, label_strip, strip_rows
+    from paper_2006_09299_b200.strips import HostStagedCollectives, TorchCollectives, label_strip, strip_rows
 
     if len(wl.specs) != 1 or wl.specs[0][0] != "gen":
         raise SystemExit("--strips needs a single generated image (cfg1 or cfg5)")
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist.init_process_group(BACKEND, device_id=torch.device("cuda", local) if BACKEND == "nccl" else None)
     y0, h = strip_rows(wl.H, world)[rank]
     _, dens, gran, seed = wl.specs[0]
     d = torch.empty((h, wl.W), dtype=torch.uint8, device="cuda")
     generate_rows_device(d.data_ptr(), wl.W, wl.H, y0, h, dens, gran, seed)
     torch.cuda.synchronize()
     lab = Labeler(local)
-    coll = TorchCollectives()
+    coll = TorchCollectives() if BACKEND == "nccl" else HostStagedCollectives()
     cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
     stream = torch.cuda.ExternalStream(lab.stream())
 
@@ -432,6 +433,11 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # testing aid for the N > 1 code path on a one-GPU box: every rank on GPU 0 over gloo
+    # (RUNLAB_BENCH_SHARED_GPU=1); never set by the driver
+    global BACKEND
+    if os.environ.get("RUNLAB_BENCH_SHARED_GPU"):
+        local, BACKEND = 0, "gloo"
     wl = Workload(args.config)
 
     if args.impl == "reference":
@@ -451,7 +457,7 @@ def main() -> None:
 
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(BACKEND, device_id=torch.device("cuda", local) if BACKEND == "nccl" else None)
 
     specs = wl.local_specs(rank, world)
     B = len(specs)
