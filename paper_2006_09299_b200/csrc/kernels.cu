@@ -185,22 +185,41 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     // mark their component as touching it
     const bool top_img = tg.ty == 0, bot_img = (tg.y0 + tg.th == g.H);
     const bool left_img = tg.tx == 0, right_img = (tg.x0 + tg.tw == g.W);
-    for (int q = tid; q < PERIM; q += BT) {
-        int pr, pc;
-        bool frame;
-        if (q < TW) { pr = 0; pc = q; frame = top_img; }
-        else if (q < 2 * TW) { pr = tg.th - 1; pc = q - TW; frame = bot_img; }
-        else if (q < 2 * TW + TH) { pr = q - 2 * TW; pc = 0; frame = left_img; }
-        else { pr = q - 2 * TW - TH; pc = tg.tw - 1; frame = right_img; }
-        uint16_t v = PERIM_NONE;
-        if (pr >= 0 && pr < tg.th && pc >= 0 && pc < tg.tw) {
-            const uint32_t lc = lc_at(S, pr, pc);
-            const uint32_t val = xbit(S, pr, pc) ^ (uint32_t)flip;
-            const uint32_t bi = S.lcb[lc] & 0x7FFF;
-            v = (uint16_t)((val << 15) | bi);
-            if (frame) A.bimg[bi] = 1;
+    uint16_t* const perim = ws.perim + (int64_t)tg.t * PERIM;
+    auto label = [&](int pr, int pc, bool frame) -> uint32_t {
+        const uint32_t lc = lc_at(S, pr, pc);
+        const uint32_t bi = S.lcb[lc] & 0x7FFF;
+        if (frame) A.bimg[bi] = 1;
+        return ((xbit(S, pr, pc) ^ (uint32_t)flip) << 15) | bi;
+    };
+    // top and bottom rows: two neighbouring pixels per thread (same word), one 4-B store
+    for (int q = tid; q < TW; q += BT) {
+        const bool bot = q >= TW / 2;
+        const int c = 2 * (q & (TW / 2 - 1)), pr = bot ? tg.th - 1 : 0;
+        const bool frame = bot ? bot_img : top_img;
+        uint32_t v = 0xFFFFFFFFu;  // PERIM_NONE twice
+        if (c < tg.tw) {
+            const int word = pr * WPR + (c >> 5), b = c & 31;
+            const uint32_t st = S.st[word], xw = S.x[word];
+            const int run0 = (int)S.rbase[word] + __popc(st & (0xFFFFFFFFu >> (31 - b))) - 1;
+            const uint32_t bi0 = S.lcb[lc_of_run(S, run0)] & 0x7FFF;
+            v = (((((xw >> b) & 1u) ^ (uint32_t)flip) << 15) | bi0) | 0xFFFF0000u;
+            if (frame) A.bimg[bi0] = 1;
+            if (c + 1 < tg.tw) {
+                const int run1 = run0 + (int)((st >> (b + 1)) & 1u);  // a run starts at c + 1?
+                const uint32_t bi1 = run1 == run0 ? bi0 : S.lcb[lc_of_run(S, run1)] & 0x7FFF;
+                v = (v & 0xFFFFu) | ((((((xw >> (b + 1)) & 1u) ^ (uint32_t)flip) << 15) | bi1) << 16);
+                if (frame && run1 != run0) A.bimg[bi1] = 1;
+            }
         }
-        ws.perim[(int64_t)tg.t * PERIM + q] = v;
+        reinterpret_cast<uint32_t*>(perim + (bot ? TW : 0))[c >> 1] = v;
+    }
+    // left and right columns
+    for (int q = tid; q < 2 * TH; q += BT) {
+        const bool right = q >= TH;
+        const int pr = right ? q - TH : q;
+        perim[2 * TW + q] = pr < tg.th ? (uint16_t)label(pr, right ? tg.tw - 1 : 0, right ? right_img : left_img)
+                                       : PERIM_NONE;
     }
     __syncthreads();
 
