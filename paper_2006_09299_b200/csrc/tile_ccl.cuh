@@ -111,7 +111,9 @@ struct CclSmem {
     // root runs before each block
     static constexpr int RB = std::is_same<typename C::PT, uint32_t>::value ? C::MR / 32 + 1 : 1;
     uint32_t rmask[RB];
+    uint32_t rbmask[RB];       // root runs of border components
     uint16_t rpre[RB];
+    uint16_t bpre[RB];         // border components before each block
     int wsum[C::BT / 32 + 1];
     int qtot[NWARPS];          // union events queued by each word warp
     int nruns, nlc, nb;
@@ -226,8 +228,9 @@ template <class SM>
 __device__ __forceinline__ int lc_col(const SM& S, uint32_t lc) { return run_col(S, S.lcrun[lc]); }
 
 // Full tile labeling.  Pre: S.x / S.vm filled for all NW words and a __syncthreads().
-// Post (all synced): S.par[run] = TAG | component, S.runpos, S.lcrun, S.lcb (border flags
-// compacted to border indices), S.blc, S.rowlc, S.rowbx, S.nruns, S.nlc, S.nb.
+// Post (all synced): S.par[run] = TAG | component, S.runpos, S.lcrun, S.lcb (border index, or
+// 0x8000 | border components before it), S.blc, S.nruns, S.nlc, S.nb; S.rowlc[r] and S.rowbx[r]
+// are written by thread r only (visible to the others after the caller's next barrier).
 // Returns false (uniformly) when the tile has more runs than the tables hold.
 // Per-thread word state shared by the run and union phases.
 struct WordBits {
@@ -483,7 +486,6 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
     // roots only shorten other walks (as in the pre-flatten).  The walk of a 32-run block is
     // one warp's, so the block's roots come out as a ballot mask.
     const int nruns = S.nruns;
-    const unsigned lt = (1u << lane) - 1u;
     for (int b = warp * 32; b < nruns; b += BT) {
         const int i = b + lane;
         uint32_t p = i;
@@ -497,97 +499,73 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
             }
         }
         const unsigned m = __ballot_sync(0xFFFFFFFFu, i < nruns && p == (uint32_t)i);
-        if (lane == 0) S.rmask[b >> 5] = m;
+        if (lane == 0) {
+            S.rmask[b >> 5] = m;
+            S.rbmask[b >> 5] = 0;
+        }
     }
     __syncthreads();
     RL_PHASE(tg.t, 5);
 
-    // ---- tile components = root runs, numbered in raster order: prefix over the blocks' root
-    // counts; a run's component is then its root's rank (no tagging pass)
-    const int nblk = (nruns + 31) >> 5;
-    int nlc;
+    // ---- border components, marked at their root run: every row's first and last run (the
+    // left and right tile columns: a row's first run starts at column 0, its last ends at the
+    // tile edge) and every run of the top and bottom rows.  par[] holds each run's root here.
     {
-        const int pre = block_excl_scan<BT>(tid < nblk ? __popc(S.rmask[tid]) : 0, S.wsum, nlc);
-        if (tid < nblk) S.rpre[tid] = (uint16_t)pre;
+        const int top_end = S.rbase[WPR], bot_begin = S.rbase[(tg.th - 1) * WPR];
+        auto mark = [&](uint32_t root) { atomicOr(&S.rbmask[root >> 5], 1u << (root & 31)); };
+        if (tid < tg.th) {
+            mark(S.par[S.rbase[tid * WPR]]);
+            mark(S.par[S.rbase[(tid + 1) * WPR] - 1]);
+        }
+        for (int i = tid; i < top_end; i += BT) mark(S.par[i]);
+        for (int i = bot_begin + tid; i < nruns; i += BT) mark(S.par[i]);
+    }
+    __syncthreads();
+    RL_PHASE(tg.t, 6);
+
+    // ---- tile components = root runs, numbered in raster order, and border components among
+    // them, by ONE prefix over the 32-run blocks of (roots | border roots << 16): a run's
+    // component is its root's rank, a border component's index its root's rank among border
+    // roots (no tagging pass, no separate compaction)
+    const int nblk = (nruns + 31) >> 5;
+    int nlc, nb;
+    {
+        int tot;
+        const int pre = block_excl_scan<BT>(
+            tid < nblk ? (__popc(S.rmask[tid]) | (__popc(S.rbmask[tid]) << 16)) : 0, S.wsum, tot);
+        if (tid < nblk) {
+            S.rpre[tid] = (uint16_t)(pre & 0xFFFF);
+            S.bpre[tid] = (uint16_t)(pre >> 16);
+        }
+        nlc = tot & 0xFFFF;
+        nb = tot >> 16;
     }
     if (nlc > C::NLC) return false;  // more components than this class holds (uniform)
+    if (nb > C::NBC) return false;   // more border components than this class holds
     auto rank_of = [&](uint32_t root) {  // valid once rpre is visible
         return (uint32_t)S.rpre[root >> 5] + __popc(S.rmask[root >> 5] & ((1u << (root & 31)) - 1u));
     };
-    if (tid == 0) S.nlc = nlc;
-    if (tid == 32) {  // the map: component of each run, first run and border index of each component
-        // (three sections, each padded to 8 elements: the emit pass copies them with 16-B loads)
+    if (tid == 0) {
+        S.nlc = nlc;
+        S.nb = nb;
+    }
+    if (tid == 32) {  // the map (sections: MapLayout; the emit pass copies them with 16-B loads)
         const unsigned long long need = (unsigned long long)MapLayout(nruns, nlc).total;
         const unsigned long long off = atomicAdd(mo.used, need);
         if (off + need > mo.cap) atomicOr(mo.err, ERR_RSTORE_CAP);
         S.moff = off + need > mo.cap ? ~0ull : off;
         mo.tile_off[tg.t] = off;
     }
-    static_assert(C::NLC % 8 == 0, "border flags clear in whole 16-B vectors");
-    for (int v = tid; v < (nlc + 7) >> 3; v += BT) reinterpret_cast<uint4*>(S.lcb)[v] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    RL_PHASE(tg.t, 6);
-    // ---- border components (plain stores of 1): every row's first and last run (the left and
-    // right tile columns: a row's first run starts at column 0, its last ends at the tile edge)
-    // and every run of the top and bottom rows.  par[] holds each run's root here.
-    const int top_end = S.rbase[WPR], bot_begin = S.rbase[(tg.th - 1) * WPR];
-    if (tid <= TH) {  // first component of each row: components before the row's first run
-        const int k = tid < tg.th ? S.rbase[tid * WPR] : nruns;
-        S.rowlc[tid] = (uint16_t)(k < nruns ? rank_of((uint32_t)k) : (uint32_t)nlc);
-    }
-    if (tid < tg.th) {
-        S.lcb[rank_of(S.par[S.rbase[tid * WPR]])] = 1;
-        S.lcb[rank_of(S.par[S.rbase[(tid + 1) * WPR] - 1])] = 1;
-    }
-    for (int i = tid; i < top_end; i += BT) S.lcb[rank_of(S.par[i])] = 1;
-    for (int i = bot_begin + tid; i < nruns; i += BT) S.lcb[rank_of(S.par[i])] = 1;
-    __syncthreads();
-    RL_PHASE(tg.t, 7);
-
-    const unsigned long long moff = S.moff;
-    uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
-    const MapLayout ML(nruns, nlc);
-    constexpr int NWB = BT / 32;
-    // ---- compact border components to border indices (raster order; warp segments)
-    const int segl = ((nlc + NWB - 1) / NWB + 31) & ~31;
-    const int l0 = min(warp * segl, nlc), l1 = min(l0 + segl, nlc);
-    int cntb = 0;
-    for (int b = l0; b < l1; b += 32) {
-        const int l = b + lane;
-        cntb += __popc(__ballot_sync(0xFFFFFFFFu, l < l1 && S.lcb[l]));
-    }
-    int nb;
-    int bx = warp_segments_scan<NWB>(cntb, S.wsum, nb);
-    if (nb > C::NBC) return false;  // more border components than this class holds
-    for (int b = l0; b < l1; b += 32) {
-        const int l = b + lane;
-        const bool isb = l < l1 && S.lcb[l];
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, isb);
-        const int my = bx + __popc(m & lt);
-        if (l < l1) {
-            uint16_t v;
-            if (isb) {
-                S.blc[my] = (uint16_t)l;
-                v = (uint16_t)my;
-            } else {
-                v = (uint16_t)(0x8000 | my);
-            }
-            S.lcb[l] = v;
-            if (map) map[MapLayout(nruns, nlc).lcb + l] = v;
-        }
-        bx += __popc(m);
-    }
-    if (tid == 0) S.nb = nb;
     border.init(nb);
     __syncthreads();
     RL_PHASE(tg.t, 8);
 
-    // ---- every run: its component (par becomes TAG | component), the component's first run, the
-    // map entry; runs of border components feed the border features
-    if (tid <= TH) {
-        const int l = S.rowlc[tid];
-        S.rowbx[tid] = l < nlc ? (uint16_t)(S.lcb[l] & 0x7FFF) : (uint16_t)nb;
-    }
+    const unsigned long long moff = S.moff;
+    uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
+    const MapLayout ML(nruns, nlc);
+    // ---- every run: its component (par becomes TAG | component), the map entry; a component's
+    // first (root) run writes its first-run, border-index entries; runs of border components
+    // feed the border features
     for (int b = warp * 32; b < nruns; b += BT) {
         const int i = b + lane;
         int bi = -1;
@@ -595,16 +573,32 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
         if (i < nruns) {
             const uint32_t root = S.par[i];
             const uint32_t l = rank_of(root);
+            const uint32_t bm = S.rbmask[root >> 5], bit = 1u << (root & 31);
+            const uint32_t bx = (uint32_t)S.bpre[root >> 5] + __popc(bm & (bit - 1u));
+            const bool isb = (bm & bit) != 0;
             S.par[i] = (uint16_t)(TAG16 | l);
-            if (root == (uint32_t)i) S.lcrun[l] = (uint16_t)i;
             if (map) map[i] = (uint16_t)l;
-            const uint16_t lb = S.lcb[l];
-            if (!(lb & 0x8000u)) bi = lb;
-            else iroot = root == (uint32_t)i;
+            if (isb) bi = (int)bx;
+            if (root == (uint32_t)i) {
+                const uint16_t v = (uint16_t)(isb ? bx : (0x8000u | bx));
+                S.lcrun[l] = (uint16_t)i;
+                S.lcb[l] = v;
+                if (isb) S.blc[bx] = (uint16_t)l;
+                if (map) map[ML.lcb + l] = v;
+                iroot = !isb;
+            }
         }
         border(bi, i, iroot);
     }
     __syncthreads();
+    // first component of each row (components before the row's first run) and the border
+    // components before it; read by other threads only after the caller's next barrier
+    if (tid <= TH) {
+        const int k = tid < tg.th ? S.rbase[tid * WPR] : nruns;
+        const int l = k < nruns ? (int)rank_of((uint32_t)k) : nlc;
+        S.rowlc[tid] = (uint16_t)l;
+        S.rowbx[tid] = l < nlc ? (uint16_t)(S.lcb[l] & 0x7FFF) : (uint16_t)nb;
+    }
     if (map) {
         for (int l = tid; l < nlc; l += BT) map[ML.lcrun + l] = S.lcrun[l];
         for (int k = tid; k <= NW; k += BT) map[ML.rbase + k] = S.rbase[k];
