@@ -166,10 +166,10 @@ struct rl_ctx {
     DevBuf pk, pkpar, pkesc, fpk;  // record slots, parents, escaped records, feature slots
     uint8_t* h_rstage[2] = {nullptr, nullptr};
     size_t h_rstage_n[2] = {0, 0};
-    // rl_label_into: byte-per-pixel input packed to P4 bits by the host pool before the H2D copy
-    // (env RUNLAB_GPU_PACKED_H2D=1; off by default: measured no faster on the pool's boxes, the
-    // host-side packing costs what the link saves); the caller's filled-image format
-    bool packed_h2d = false;
+    // rl_label_into: byte-per-pixel input packed to P4 bits by the host pool (AVX-512, one chunk
+    // ahead of the H2D) before the copy: 8x fewer bytes on the link; the host reads the input
+    // instead of the DMA engine (env RUNLAB_GPU_PACKED_H2D=0: plain u8 copies)
+    bool packed_h2d = true;
     uint8_t* h_istage[2] = {nullptr, nullptr};
     size_t h_istage_n[2] = {0, 0};
     int32_t user_ofmt = 0;

@@ -40,7 +40,9 @@ struct HostPool {
     std::mutex m;
     std::condition_variable cv, done;
     std::deque<std::pair<int, std::function<void()>>> q;
-    int pending[2 * rl_ctx::MAXKIDS + 1] = {};  // last: input packing
+    // tags: [0, 2 MAXKIDS) a kid's output staging buffers, [2 MAXKIDS, 4 MAXKIDS) its input
+    // staging buffers, 4 MAXKIDS the single-chunk input packing
+    int pending[4 * rl_ctx::MAXKIDS + 1] = {};
     bool stop = false;
     explicit HostPool(int n) {
         for (int i = 0; i < n; ++i) workers.emplace_back([this] { loop(); });
@@ -158,15 +160,32 @@ void expand_p4_rows(const uint8_t* src, int64_t rows, int32_t rowb, int32_t w, u
     _mm_sfence();
 }
 
+// 64 pixels per step: the bytes of each 8-pixel group reversed (P4 is MSB-first), then one
+// mask of their bit 0 = 8 P4 bytes; returns the first pixel not done
+__attribute__((target("avx512f,avx512bw"))) int32_t pack_avx512(const uint8_t* s, int32_t w, uint8_t* d) {
+    const __m512i rev = _mm512_set_epi8(8, 9, 10, 11, 12, 13, 14, 15, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14,
+                                        15, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 0, 1, 2, 3, 4, 5, 6, 7,
+                                        8, 9, 10, 11, 12, 13, 14, 15, 0, 1, 2, 3, 4, 5, 6, 7);
+    const __m512i one = _mm512_set1_epi8(1);
+    int32_t i = 0;
+    for (; i + 64 <= w; i += 64) {
+        const __m512i v = _mm512_shuffle_epi8(_mm512_loadu_si512(s + i), rev);
+        const uint64_t m = _mm512_test_epi8_mask(v, one);
+        std::memcpy(d + i / 8, &m, 8);
+    }
+    return i;
+}
+
 // byte-per-pixel rows -> P4 rows (bit 0 of each byte, MSB-first; the device reads either):
 // the host-buffer path sends u8 input over PCIe as bits
 __attribute__((target("ssse3"))) void pack_rows_p4(const uint8_t* src, int64_t rows, int32_t w, uint8_t* dst,
                                                    int32_t rowb) {
+    static const bool avx512 = __builtin_cpu_supports("avx512bw");
     const __m128i rev = _mm_setr_epi8(7, 6, 5, 4, 3, 2, 1, 0, 15, 14, 13, 12, 11, 10, 9, 8);
     for (int64_t r = 0; r < rows; ++r) {
         const uint8_t* s = src + r * (int64_t)w;
         uint8_t* d = dst + r * (int64_t)rowb;
-        int32_t i = 0;
+        int32_t i = avx512 ? pack_avx512(s, w, d) : 0;
         for (; i + 16 <= w; i += 16) {
             __m128i v = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
             v = _mm_slli_epi16(_mm_shuffle_epi8(v, rev), 7);
@@ -298,7 +317,7 @@ void copy_fixed_outputs(rl_ctx* c, rl_host_outputs* out, int32_t b0) {
     const size_t npx = (size_t)(g.P * g.B), off = (size_t)g.P * b0;
     if (out->filled_image) {
         if (g.ofmt == c->user_ofmt) {
-            cudaMemcpyAsync(out->filled_image + (size_t)g.fbytes * b0, c->ws.filled_img, (size_t)g.fbytes * g.B,
+            cudaMemcpyAsync(out->filled_image + (size_t)g.ofbytes * b0, c->ws.filled_img, (size_t)g.ofbytes * g.B,
                             cudaMemcpyDeviceToHost, c->stream);
         } else {  // packed: into the staging buffer, expanded on the host once the chunk is done
             cudaMemcpyAsync(c->h_stage[c->stage], c->ws.filled_img, (size_t)g.ofbytes * g.B, cudaMemcpyDeviceToHost,
@@ -324,35 +343,47 @@ void expand_filled(rl_ctx* owner, rl_ctx* c, int tag, rl_host_outputs* out, int3
     }
 }
 
-// H2D of images [b0, b0 + n), the pipeline, and the D2H of the outputs whose size is fixed
+// u8 images [n] -> P4 rows in c's input staging buffer sb, by the host pool (tasks under `tag`,
+// ahead of the queued output work)
+int submit_pack(rl_ctx* c, int sb, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, HostPool* pool, int tag) {
+    const size_t npx = (size_t)image_bytes(w, h, RL_PIXELS_P4) * n;
+    if (c->h_istage_n[sb] < npx) {
+        if (c->h_istage[sb]) cudaFreeHost(c->h_istage[sb]);
+        c->h_istage[sb] = nullptr;
+        c->h_istage_n[sb] = 0;
+        if (cudaMallocHost(&c->h_istage[sb], npx) != cudaSuccess) return set_err(c, RL_ENOMEM, "pinned alloc failed");
+        c->h_istage_n[sb] = npx;
+    }
+    const int64_t rows = (int64_t)h * n;
+    const int32_t rowb = (w + 7) / 8;
+    const int parts = (int)std::min<int64_t>(std::max<int64_t>(1, rows / 128), 12);
+    uint8_t* dst = c->h_istage[sb];
+    for (int k = 0; k < parts; ++k) {
+        const int64_t r0 = rows * k / parts, r1 = rows * (k + 1) / parts;
+        pool->submit(tag, [=] { pack_rows_p4(pixels + r0 * w, r1 - r0, w, dst + r0 * rowb, rowb); }, true);
+    }
+    return RL_OK;
+}
+
+constexpr int in_tag(int kid, int sb) { return 2 * rl_ctx::MAXKIDS + 2 * kid + sb; }
+constexpr int SYNC_IN_TAG = 4 * rl_ctx::MAXKIDS;
+
+// H2D of images [b0, b0 + n), the pipeline, and the D2H of the outputs whose size is fixed.
+// `pack_in`: u8 input crosses PCIe as P4 bits from c's input staging buffer c->stage, packed
+// there by the host pool -- already (`prepacked`, the caller waited for it) or here.
 int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t n, const rl_config* cfg,
-                 rl_host_outputs* out, int32_t b0, int32_t fmt, bool packed_out, int pack, HostPool* pool) {
-    // u8 input crosses PCIe as P4 bits packed by the host pool into pinned staging
-    const bool pack_in = pool && fmt == RL_PIXELS_U8 && c->packed_h2d;
+                 rl_host_outputs* out, int32_t b0, int32_t fmt, bool packed_out, int pack, HostPool* pool,
+                 bool pack_in, bool prepacked) {
     const int32_t dfmt = pack_in ? RL_PIXELS_P4 : fmt;
     const size_t npx = (size_t)image_bytes(w, h, dfmt) * n;
     if (!ensure(c->pix, npx)) return set_err(c, RL_ENOMEM, "device allocation failed");
     const uint8_t* src = pixels;
     if (pack_in) {
-        const int sb = c->stage;
-        if (c->h_istage_n[sb] < npx) {
-            if (c->h_istage[sb]) cudaFreeHost(c->h_istage[sb]);
-            c->h_istage[sb] = nullptr;
-            c->h_istage_n[sb] = 0;
-            if (cudaMallocHost(&c->h_istage[sb], npx) != cudaSuccess) return set_err(c, RL_ENOMEM, "pinned alloc failed");
-            c->h_istage_n[sb] = npx;
+        if (!prepacked) {
+            if (const int rc = submit_pack(c, c->stage, pixels, w, h, n, pool, SYNC_IN_TAG)) return rc;
+            pool->wait(SYNC_IN_TAG);
         }
-        const int64_t rows = (int64_t)h * n;
-        const int32_t rowb = (w + 7) / 8;
-        const int parts = (int)std::min<int64_t>(std::max<int64_t>(1, rows / 128), 12);
-        uint8_t* dst = c->h_istage[sb];
-        const int tag = 2 * rl_ctx::MAXKIDS;
-        for (int k = 0; k < parts; ++k) {
-            const int64_t r0 = rows * k / parts, r1 = rows * (k + 1) / parts;
-            pool->submit(tag, [=] { pack_rows_p4(pixels + r0 * w, r1 - r0, w, dst + r0 * rowb, rowb); }, true);
-        }
-        pool->wait(tag);
-        src = dst;
+        src = c->h_istage[c->stage];
     }
     if (!c->in_stream) {
         if (cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -372,7 +403,9 @@ int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t
     c->want_compact = out->filled && out->filled_layout == 1;
     c->want_pack = pack;
     const bool packed = packed_out && out->filled_image && fmt == RL_PIXELS_U8;
-    c->force_ofmt = packed ? RL_PIXELS_P4 : -1;
+    // the filled image: P4 bits expanded on the host, else the caller's format (also when the
+    // input crossed packed)
+    c->force_ofmt = packed ? RL_PIXELS_P4 : (dfmt != fmt ? fmt : -1);
     if (packed) {
         const size_t need = (size_t)image_bytes(w, h, RL_PIXELS_P4) * n;
         const int sb = c->stage;
@@ -554,7 +587,10 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     const bool multi = nch > 1;
     const bool packed = multi && ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
     const int pack = multi && ctx->packed_recs ? ((out->comps ? 1 : 0) | (out->filled && out->filled_layout == 1 ? 2 : 0)) : 0;
-    const bool staged = packed || pack || (fmt == RL_PIXELS_U8 && ctx->packed_h2d);
+    // u8 input crosses PCIe as P4 bits packed by the host pool one chunk ahead (a single chunk
+    // would wait for its packing: plain copy)
+    const bool pack_in = multi && fmt == RL_PIXELS_U8 && ctx->packed_h2d;
+    const bool staged = packed || pack || pack_in;
     if (staged && !ctx->pool) {
         const int hw = (int)std::thread::hardware_concurrency();
         const int nt = ctx->host_threads > 0 ? ctx->host_threads : std::max(2, std::min(hw > 0 ? hw : 4, 12));
@@ -564,7 +600,7 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     IntoState st;
     tl.begin(ctx->stream, nch);
     if (nch == 1) {
-        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed, pack, ctx->pool);
+        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed, pack, ctx->pool, false, false);
         if (!rc) rc = finish(ctx);
         if (!rc) rc = into_post(ctx, out, 0, st, ctx->pool, 0);
         if (!rc) rc = into_sync(ctx);
@@ -601,6 +637,16 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
             if (!r && packed) expand_filled(ctx, k, 2 * kid + k->stage, out, first_image(c));
             return r ? set_err(ctx, r, k->err) : RL_OK;
         };
+        // chunk c's input, packed into the staging buffer its kid takes next (the buffer's last
+        // H2D, chunk c - 2 NK's, completed before post(c - 2 NK) returned)
+        auto prepack = [&](int32_t c) -> int {
+            const int kid = c % NK;
+            rl_ctx* k = ctx->kids[kid];
+            const int r = submit_pack(k, k->stage ^ 1, pixels + (size_t)first_image(c) * image_bytes(w, h, fmt), w, h,
+                                      images(c), ctx->pool, in_tag(kid, k->stage ^ 1));
+            return r ? set_err(ctx, r, k->err) : RL_OK;
+        };
+        if (pack_in) rc = prepack(0);
         for (int32_t c = 0; c < nch && !rc; ++c) {
             if (c >= NK) rc = post(c - NK);
             if (rc) break;
@@ -610,11 +656,16 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
                 k->stage ^= 1;
                 ctx->pool->wait(2 * kid + k->stage);
             }
+            if (pack_in) {  // this chunk's input is packed; start packing the next one
+                ctx->pool->wait(in_tag(kid, k->stage));
+                if (c + 1 < nch) rc = prepack(c + 1);
+                if (rc) break;
+            }
             const int32_t b0 = first_image(c);
             tl.chunk = c;
             tl.hmark(c, 2);
             rc = into_enqueue(k, pixels + (size_t)b0 * image_bytes(w, h, fmt), w, h, images(c), cfg, out, b0, fmt,
-                              packed, pack, ctx->pool);
+                              packed, pack, ctx->pool, pack_in, true);
             if (rc) rc = set_err(ctx, rc, k->err);
         }
         for (int32_t c = std::max(0, nch - NK); c < nch && !rc; ++c) rc = post(c);
@@ -624,12 +675,16 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
         if (rc)
             for (int i = 0; i < NK; ++i) drained = into_sync(ctx->kids[i]) == RL_OK && drained;
         if (staged && drained)
-            for (int tag = 0; tag < 2 * NK; ++tag) ctx->pool->wait(tag);
+            for (int kid = 0; kid < NK; ++kid)
+                for (int sb = 0; sb < 2; ++sb) {
+                    ctx->pool->wait(2 * kid + sb);
+                    ctx->pool->wait(in_tag(kid, sb));
+                }
     }
     if (rc) return rc;
     tl.print();
     out->comps_needed = st.total;
-    out->h2d_bytes = image_bytes(w, h, fmt == RL_PIXELS_U8 && ctx->packed_h2d ? RL_PIXELS_P4 : fmt) * n;
+    out->h2d_bytes = image_bytes(w, h, pack_in ? RL_PIXELS_P4 : fmt) * n;
     out->d2h_bytes = st.d2h;
     if (st.nospace) return set_err(ctx, RL_ENOSPC, "component buffers too small");
     return RL_OK;

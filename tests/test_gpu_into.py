@@ -94,7 +94,7 @@ def _check(o, outs, ref, layout, labels=False):
     if labels:
         np.testing.assert_array_equal(o["labels"].numpy().view(np.uint32), ref.labels)
     n_, h_, w_ = o["fill"].shape
-    # byte-per-pixel input crosses as P4 bits unless RUNLAB_GPU_NO_PACKED_H2D
+    # byte-per-pixel input crosses as P4 bits unless RUNLAB_GPU_PACKED_H2D=0
     assert outs.h2d_bytes in (o["fill"].numel(), n_ * h_ * ((w_ + 7) // 8))
 
 
@@ -185,3 +185,31 @@ def test_into_packed_slots_match_full_records(small_chunks, layout):
         plain.close()
     total = int(ref.comp_offset[-1])
     assert outs.d2h_bytes < outs2.d2h_bytes - 20 * total  # 48-B records became 20-B slots
+
+
+@pytest.mark.parametrize("env", [{"RUNLAB_GPU_PACKED_H2D": "0"}, {"RUNLAB_GPU_NO_PACKED_D2H": "1"},
+                                 {"RUNLAB_GPU_NO_PACKED_D2H": "1", "RUNLAB_GPU_NO_PACKED_RECORDS": "1"}])
+def test_into_copy_variants(env):
+    """The chunked path with the u8 input copied plainly (no host-side P4 packing), and with the
+    input packed but the filled image (and records) copied plainly: same outputs; the reported
+    H2D bytes follow the input format on the link."""
+    h_in = _batch(13, 512, 384, seed0=23)
+    h_in[2].fill_(1)
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    os.environ.update(env)
+    os.environ["RUNLAB_GPU_CHUNK_PX"] = str(1 << 20)
+    try:
+        lab = Labeler(0)
+    finally:
+        for k in list(env) + ["RUNLAB_GPU_CHUNK_PX"]:
+            del os.environ[k]
+    try:
+        ref = lab.label_batch(h_in.numpy(), cfg)
+        for _ in range(2):
+            o, outs = _into(lab, h_in, cfg, 1, _cap(ref))
+            _check(o, outs, ref, 1)
+        n, h, w = h_in.shape
+        want = n * h * w if env.get("RUNLAB_GPU_PACKED_H2D") == "0" else n * h * ((w + 7) // 8)
+        assert outs.h2d_bytes == want
+    finally:
+        lab.close()
