@@ -40,6 +40,105 @@ struct AnalyzeSmem {
     uint32_t base;
 };
 
+// Border-component features (S | Sy << 14, Sx, last row, first and last column), by words: each
+// thread walks the run segments of its part of a word in column order (one word per thread in
+// class S, half a word in the 512-thread classes).  A row's runs alternate between the two
+// values, so two register accumulators -- one per value -- absorb the consecutive segments of one
+// component (the percolating component's many runs of a row cost register adds, not shared
+// atomics) and go to the shared accumulators when the component changes; the last ones are
+// reduced per warp first (REDUX over the lanes holding the same component).  The row is the
+// thread's, so Sy = S * row.  Pre: ccl_tile's map pass (par = TAG | component, lcb final).
+template <class C>
+__device__ __forceinline__ void border_words(AnalyzeSmem<C>& A) {
+    const CclSmem<C>& S = A.c;
+    constexpr int PARTS = C::BT / NW, PB = 32 / PARTS;
+    constexpr uint32_t EMPTY = 0x3FFu;  // key = border index | first column << 10 | last column << 18
+    static_assert(NBMAX < (int)EMPTY && TW <= 256, "key fields");
+    const int tid = threadIdx.x;
+    const int wd = tid % NW, part = tid / NW;
+    const uint32_t r = (uint32_t)(wd / WPR), cw = 32u * (uint32_t)(wd % WPR);
+    const uint32_t vm = S.vm[wd];
+    const int lo = part * PB;
+    const int hi = min(lo + PB, 32 - __clz(vm));  // valid pixels are contiguous from bit 0
+    auto commit = [&](uint32_t bi, uint32_t ssy, uint32_t sx, int rr, int c0, int c1) {
+        atomicAdd(&A.bssy[bi], ssy);
+        atomicAdd(&A.bsx[bi], sx);
+        atomicMax(&A.brmax[bi], rr);
+        atomicMin(&A.bcmin[bi], c0);
+        atomicMax(&A.bcmax[bi], c1);
+    };
+    // v = S | Sx << 6 of the accumulated segments (<= 32 pixels of one row)
+    auto flush = [&](uint32_t key, uint32_t v) {
+        if ((key & EMPTY) != EMPTY)
+            commit(key & EMPTY, (v & 63u) | (((v & 63u) * r) << 14), v >> 6, (int)r, (int)((key >> 10) & 0xFFu),
+                   (int)(key >> 18));
+    };
+    uint32_t ka = EMPTY, kb = EMPTY, va = 0, vb = 0;
+    if (lo < hi) {
+        const uint32_t st = S.st[wd];
+        const uint32_t upto = 0xFFFFFFFFu >> (31 - lo);  // bits 0..lo
+        int k = (int)S.rbase[wd] + __popc(st & upto) - 1;  // the run covering bit lo
+        uint32_t rem = st & ~upto;
+        if (hi < 32) rem &= (1u << hi) - 1u;
+        uint32_t j0 = (uint32_t)lo;
+        auto step = [&](uint32_t& key, uint32_t& v) -> bool {
+            const uint32_t j1 = rem ? (uint32_t)(__ffs(rem) - 1) : (uint32_t)hi;
+            const uint32_t lb = S.lcb[lc_of_run(S, k)];
+            if (!(lb & 0x8000u)) {
+                const uint32_t c0 = cw + j0, n = j1 - j0;
+                const uint32_t sx = n * (2u * c0 + n - 1u) / 2u;
+                if ((key & EMPTY) == lb) {
+                    v += n | (sx << 6);
+                    key = (key & 0x3FFFFu) | ((c0 + n - 1u) << 18);
+                } else {
+                    flush(key, v);
+                    key = lb | (c0 << 10) | ((c0 + n - 1u) << 18);
+                    v = n | (sx << 6);
+                }
+            }
+            if (!rem) return true;
+            rem &= rem - 1u;
+            j0 = j1;
+            ++k;
+            return false;
+        };
+        for (;;) {
+            if (step(ka, va)) break;
+            if (step(kb, vb)) break;
+        }
+        // ka holds the value of the part's first pixel: make it the value-1 accumulator, so that
+        // the lanes' accumulators of the percolating component line up for the warp reduction
+        if (!((S.x[wd] >> lo) & 1u)) {
+            const uint32_t t = ka, u = va;
+            ka = kb;
+            va = vb;
+            kb = t;
+            vb = u;
+        }
+    }
+    auto warp_flush = [&](uint32_t key, uint32_t v) {
+        const bool has = (key & EMPTY) != EMPTY;
+        const uint32_t valid = __ballot_sync(0xFFFFFFFFu, has);
+        if (!valid) return;
+        const uint32_t cand = __shfl_sync(0xFFFFFFFFu, key & EMPTY, __ffs(valid) - 1);
+        const bool in = has && (key & EMPTY) == cand;
+        const uint32_t grp = __ballot_sync(0xFFFFFFFFu, in);
+        if (in) {
+            const uint32_t s = v & 63u;
+            const uint32_t ssy = __reduce_add_sync(grp, s | ((s * r) << 14));
+            const uint32_t sx = __reduce_add_sync(grp, v >> 6);
+            const int rr = (int)__reduce_max_sync(grp, r);
+            const int c0 = (int)__reduce_min_sync(grp, (key >> 10) & 0xFFu);
+            const int c1 = (int)__reduce_max_sync(grp, key >> 18);
+            if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) commit(cand, ssy, sx, rr, c0, c1);
+        } else {
+            flush(key, v);
+        }
+    };
+    warp_flush(ka, va);
+    warp_flush(kb, vb);
+}
+
 // Returns false when the tile exceeds the capacity class C (then nothing but the packed bits and
 // possibly a partial component map -- superseded by the next class's -- was written for it; the
 // caller defers it to the next class).
@@ -97,11 +196,14 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
 
     RL_PHASE(tg.t, 1);
     const MapOut mo{ws.rused, ws.rstore, ws.cap_rstore, ws.tmap, ws.counters + 1};
-    // border-component features, fed by the map pass of ccl_tile (one call per 32-run block).
-    // Runs of one large border component (the percolating one) would all hit the same shared
-    // accumulators: per call, the component of the first border run is the candidate, its lanes
-    // reduce in registers (REDUX) and one lane does the atomics; the other lanes accumulate
-    // directly.
+    // The map pass of ccl_tile counts the foreground interior components (at their root runs),
+    // and in class S feeds the border features (one call per 32-run block): runs of one large
+    // border component (the percolating one) would all hit the same shared accumulators, so per
+    // call the component of the first border run is the candidate, its lanes reduce in registers
+    // (REDUX) and one lane does the atomics; the other lanes accumulate directly.  The dense
+    // classes (16 runs per word) take the features from the word pass instead (border_words:
+    // measured 5% faster on dense tiles, 5% slower on sparse ones).
+    constexpr bool kWords = C::BT != NW;
     struct BorderFeatures {
         AnalyzeSmem<C>& A;
         int tw;
@@ -118,10 +220,12 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         }
         __device__ void operator()(int bi, int i, bool iroot) {
             const CclSmem<C>& S = A.c;
-            int rr = 0, c0 = 0x7FFFFFFF, cl = -1;
-            uint32_t nsy = 0, sx = 0;
+            if (kWords) bi = -1;
             const uint16_t rp = (iroot || bi >= 0) ? S.runpos[i] : 0;
             if (iroot) nfg += (int)(((S.x[(rp >> 8) * WPR + ((rp & 0xFF) >> 5)] >> (rp & 31)) & 1u) ^ flip);
+            if (kWords) return;
+            int rr = 0, c0 = 0x7FFFFFFF, cl = -1;
+            uint32_t nsy = 0, sx = 0;
             if (bi >= 0) {
                 const uint16_t nx = (i + 1 < S.nruns) ? S.runpos[i + 1] : 0xFFFF;
                 rr = rp >> 8;
@@ -155,6 +259,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     };
     BorderFeatures bf{A, tg.tw, (uint32_t)g.flip, 0};
     if (!ccl_tile(S, tg, mo, bf)) return false;
+    if (kWords) border_words(A);
 
     const int nlc = S.nlc, nb = S.nb;
     // the two allocations are issued by different warps so their latencies overlap

@@ -98,7 +98,7 @@ struct CclSmem {
     uint16_t rowlc[TH + 1];    // first tile component of each row
     uint16_t rowbx[TH + 1];    // border components before each row start
     alignas(16) uint16_t runpos[MR];  // (row << 8) | col of each run start, raster order
-    alignas(16) typename C::PT par[MR];  // union-find parent; then TAG | component of each run
+    alignas(16) typename C::PT par[MR];  // union-find parent; then component << 16 | root (analyze), component (emit)
     union {
         struct {
             alignas(16) uint16_t lcrun[C::NLC];  // root (first) run of each tile component
@@ -185,9 +185,13 @@ __device__ __forceinline__ void sunion(uint32_t* par, uint32_t a, uint32_t b) {
     }
 }
 
+// tile component of a run once the map pass is done: the analyze pass (32-bit parents) keeps the
+// root run in the low half and stores the component in the high half; the emit pass loads the
+// 16-bit map itself
 template <class SM>
 __device__ __forceinline__ uint32_t lc_of_run(const SM& S, int run) {
-    return S.par[run] & 0x7FFFu;
+    if constexpr (sizeof(S.par[0]) == 4) return S.par[run] >> 16;
+    else return S.par[run] & 0x7FFFu;
 }
 
 template <class SM>
@@ -482,23 +486,13 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
     if (any_events && BT == NW) __syncthreads();
     RL_PHASE(tg.t, 4);
 
-    // ---- flatten (roots are final now): every run walks to its root; concurrent writes of
-    // roots only shorten other walks (as in the pre-flatten).  The walk of a 32-run block is
-    // one warp's, so the block's roots come out as a ballot mask.
+    // ---- roots (final now): a run is a root iff it is its own parent; each warp's ballot over a
+    // 32-run block gives the block's roots.  The runs are not flattened here: the map pass walks
+    // each run to its root (one pass over the runs instead of two).
     const int nruns = S.nruns;
     for (int b = warp * 32; b < nruns; b += BT) {
         const int i = b + lane;
-        uint32_t p = i;
-        if (i < nruns) {
-            p = S.par[i];
-            for (;;) {
-                const uint32_t q = S.par[p];
-                if (q == p) break;
-                p = q;
-                S.par[i] = (uint16_t)p;  // published as it goes (see the pre-flatten)
-            }
-        }
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, i < nruns && p == (uint32_t)i);
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, i < nruns && S.par[i] == (uint32_t)i);
         if (lane == 0) {
             S.rmask[b >> 5] = m;
             S.rbmask[b >> 5] = 0;
@@ -509,16 +503,24 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
 
     // ---- border components, marked at their root run: every row's first and last run (the
     // left and right tile columns: a row's first run starts at column 0, its last ends at the
-    // tile edge) and every run of the top and bottom rows.  par[] holds each run's root here.
+    // tile edge) and every run of the top and bottom rows
     {
         const int top_end = S.rbase[WPR], bot_begin = S.rbase[(tg.th - 1) * WPR];
-        auto mark = [&](uint32_t root) { atomicOr(&S.rbmask[root >> 5], 1u << (root & 31)); };
+        auto mark = [&](uint32_t i) {
+            uint32_t p = S.par[i];
+            for (;;) {
+                const uint32_t q = S.par[p];
+                if (q == p) break;
+                p = q;
+            }
+            atomicOr(&S.rbmask[p >> 5], 1u << (p & 31));
+        };
         if (tid < tg.th) {
-            mark(S.par[S.rbase[tid * WPR]]);
-            mark(S.par[S.rbase[(tid + 1) * WPR] - 1]);
+            mark(S.rbase[tid * WPR]);
+            mark(S.rbase[(tid + 1) * WPR] - 1);
         }
-        for (int i = tid; i < top_end; i += BT) mark(S.par[i]);
-        for (int i = bot_begin + tid; i < nruns; i += BT) mark(S.par[i]);
+        for (int i = tid; i < top_end; i += BT) mark(i);
+        for (int i = bot_begin + tid; i < nruns; i += BT) mark(i);
     }
     __syncthreads();
     RL_PHASE(tg.t, 6);
@@ -563,20 +565,28 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
     const unsigned long long moff = S.moff;
     uint16_t* map = moff != ~0ull ? mo.store + moff : nullptr;
     const MapLayout ML(nruns, nlc);
-    // ---- every run: its component (par becomes TAG | component), the map entry; a component's
-    // first (root) run writes its first-run, border-index entries; runs of border components
-    // feed the border features
+    // ---- every run: walk to its root (the walks publish the roots they reach in the low half of
+    // par, so concurrent walks through this run stop short; par's low half is an ancestor at
+    // all times), then its component (the high half of par: component << 16 | root) and the map
+    // entry; a component's first (root) run writes its first-run, border-index entries; runs of
+    // border components feed the border features
     for (int b = warp * 32; b < nruns; b += BT) {
         const int i = b + lane;
         int bi = -1;
         bool iroot = false;
         if (i < nruns) {
-            const uint32_t root = S.par[i];
+            uint32_t root = S.par[i] & 0xFFFFu;
+            for (;;) {
+                const uint32_t q = S.par[root] & 0xFFFFu;
+                if (q == root) break;
+                root = q;
+                S.par[i] = root;
+            }
             const uint32_t l = rank_of(root);
             const uint32_t bm = S.rbmask[root >> 5], bit = 1u << (root & 31);
             const uint32_t bx = (uint32_t)S.bpre[root >> 5] + __popc(bm & (bit - 1u));
             const bool isb = (bm & bit) != 0;
-            S.par[i] = (uint16_t)(TAG16 | l);
+            S.par[i] = (l << 16) | root;
             if (map) map[i] = (uint16_t)l;
             if (isb) bi = (int)bx;
             if (root == (uint32_t)i) {
