@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tile_ccl.cuh"
@@ -441,8 +442,10 @@ __device__ __forceinline__ uint32_t node_of(const Ws& ws, const Geo& g, int64_t 
 #ifndef RL_SEAM_THREADS
 #define RL_SEAM_THREADS 64  // small blocks: more seams in flight per SM (latency-bound unions)
 #endif
-constexpr int SEAM_T = RL_SEAM_THREADS;  // threads per seam block (TW / SEAM_T columns each)
+constexpr int SEAM_T0 = RL_SEAM_THREADS;  // threads per seam block (TW / SEAM_T columns each)
+constexpr int SEAM_TW = 256;              // calls with few tiles: more threads per seam (shorter chains)
 
+template <int SEAM_T>
 __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int32_t ns) {
     __shared__ uint32_t lp[2 * NBMAX];
     // the seam's two perimeter rows (bottom of the upper tile, top of the lower one), staged
@@ -768,6 +771,101 @@ __global__ void k_cids(Geo g, Ws ws) {
     }
 }
 
+
+// The same with one block per tile: the tile's node rows and representative flags are staged in
+// shared memory and prefix-summed once, so every node's "representatives before me in my row" is
+// two lookups (the first node of its row by binary search over the sorted rows) and all of the
+// tile's nodes are processed in parallel instead of in warp-sized chunks one after another.
+constexpr int CIDS_T = 256;
+__global__ void __launch_bounds__(CIDS_T) k_cids_blk(Geo g, Ws ws) {
+    __shared__ uint16_t srow[NBMAX];
+    __shared__ uint16_t spre[NBMAX + 1];
+    __shared__ int wsum[CIDS_T / 32 + 1];
+    if (ws.counters[1]) return;
+    const bool fit = comps_fit(g, ws);
+    const int tid = threadIdx.x;
+    const int gid = blockIdx.x * CIDS_T + tid;
+    if (fit && gid < g.B) {  // exterior records (the exterior survives hole filling)
+        if (g.cid_lo == 0) {  // strip mode: strip 0 owns id 0 (the others count it, strips.cu)
+            const uint64_t cb = comp_base(g, ws, gid);
+            rl_component c;
+            c.f = ws.nacc[gid];
+            c.parent = 0xFFFFFFFFu;
+            c.flags = 0;
+            ws.comps[cb] = c;
+            ws.top[cb] = 0;
+            ws.filled[cb] = c.f;
+        }
+        atomicAdd(&ws.img_surv[gid], 1u);
+    }
+    constexpr int PER = (NBMAX + CIDS_T - 1) / CIDS_T;  // consecutive nodes per thread in the scan
+    const int32_t t_lo = g.strip ? g.ty0 * g.ntx : 0, t_hi = g.strip ? g.ty1 * g.ntx : g.ntiles;
+    for (int32_t t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x) {
+        int32_t b, ty, tx;
+        tile_of(g, (uint32_t)t, b, ty, tx);
+        const int nb = (int)ws.tnb[t];
+        const uint32_t n0 = (uint32_t)g.B + ws.tbase[t];
+        int cnt = 0;
+        uint32_t repbits = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int i = tid * PER + q;
+            if (i < nb) {
+                srow[i] = ws.nrec[n0 + i].fr;
+                const bool rep = ws.nrep[n0 + i] != 0;
+                repbits |= (uint32_t)rep << q;
+                cnt += rep;
+            }
+        }
+        int tot;
+        int pre = block_excl_scan<CIDS_T>(cnt, wsum, tot);  // contains __syncthreads
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int i = tid * PER + q;
+            if (i < nb) spre[i] = (uint16_t)pre;
+            pre += (repbits >> q) & 1u;
+        }
+        __syncthreads();
+        const int64_t img0 = (int64_t)b * g.H * g.ntx;
+        const uint32_t offimg = img_off(g, ws, b);
+        const uint64_t cb = (uint64_t)offimg + (uint64_t)b;
+        int nsurv = 0;
+        for (int i = tid; i < nb; i += CIDS_T) {
+            const uint32_t n = n0 + (uint32_t)i;
+            if (!ws.nrep[n]) continue;
+            const NodeRec rec = ws.nrec[n];
+            // first node of this row: rows are ascending over the tile's nodes
+            int lo = 0, hi = i;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (srow[mid] < rec.fr) lo = mid + 1;
+                else hi = mid;
+            }
+            const uint32_t before = (uint32_t)(spre[i] - spre[lo]);
+            const uint32_t cid = 1u + (ws.off[img0 + (int64_t)(ty * TH + rec.fr) * g.ntx + tx] - offimg) +
+                                 rec.ibefore + before;
+            const uint32_t root = ws.uf[n];
+            ws.nrootcid[root] = cid;
+            const uint32_t proot = surrounding_root(g, ws, n, rec, b);
+            ws.nparent[root] = proot;
+            if (fit) {
+                rl_component c;
+                c.f = ws.nacc[root];
+                c.parent = 0;  // k_tops
+                c.flags = rec.fg;
+                ws.comps[cb + cid] = c;
+                if (proot < (uint32_t)g.B) {
+                    const bool cut = ws.ncut && ws.ncut[root];
+                    ws.filled[cb + cid] = cut ? acc_empty() : c.f;
+                    if (!cut) ++nsurv;
+                }
+            }
+        }
+        nsurv = __reduce_add_sync(0xFFFFFFFFu, nsurv);
+        if ((tid & 31) == 0 && nsurv) atomicAdd(&ws.img_surv[b], (uint32_t)nsurv);
+        __syncthreads();  // srow / spre are rewritten by the next tile
+    }
+}
 
 // post-fill roots (depth-1 ancestors) of the border components; non-survivors fold their
 // features into their root right away (block-aggregated; the survivors were initialised by
@@ -1402,6 +1500,15 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// Calls with few tiles (single images up to ~2 waves) are latency-bound: their seams run in
+// 256-thread blocks (shorter chains of global unions per block; cfg1 merge 48 -> 42 us) and their
+// canonical ids one block per tile (k_cids_blk; cfg1 merge 42 -> 38 us).  Dense
+// tiles in 1024-thread class-M CTAs were measured too: no gain (the tile's critical path is its
+// word phases and barriers).  (env RUNLAB_GPU_WIDE_TILES)
+static int64_t g_wide_tiles = 4096;
+static bool wide_call(const Geo& g) { return (int64_t)g.B * g.tpi <= g_wide_tiles; }
+static bool g_cids_blk = true;  // wide calls: one block per tile in k_cids_blk (env RUNLAB_GPU_CIDS_BLK=0: off)
+
 cudaError_t configure_kernels() {
     cudaError_t e = set_smem(k_analyze, sizeof(AnalyzeSmem<CapS>));
     if (e == cudaSuccess) e = set_smem(k_analyze_m, sizeof(AnalyzeSmem<CapM>));
@@ -1409,6 +1516,8 @@ cudaError_t configure_kernels() {
     if (e == cudaSuccess) e = set_smem(k_emit, sizeof(EmitSmem<CapSE>));
     if (e == cudaSuccess) e = set_smem(k_emit_m, sizeof(EmitSmem<CapME>));
     if (e == cudaSuccess) e = set_smem(k_emit_full, sizeof(EmitSmem<CapFE>));
+    if (const char* v = std::getenv("RUNLAB_GPU_WIDE_TILES")) g_wide_tiles = std::atoll(v);
+    if (const char* v = std::getenv("RUNLAB_GPU_CIDS_BLK")) g_cids_blk = std::atoi(v) != 0;
     return e;
 }
 
@@ -1422,7 +1531,10 @@ static int grid_for(int64_t n, int block, int maxgrid) {
 void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms) {
     const int64_t pairs = (int64_t)g.B * ns;
     const dim3 grid(g.ntx, (unsigned)std::min<int64_t>(pairs, 65535));
-    k_seam_h<<<grid, SEAM_T, 0, s>>>(g, ws, s0, ns);
+    if (wide_call(g))
+        k_seam_h<SEAM_TW><<<grid, SEAM_TW, 0, s>>>(g, ws, s0, ns);
+    else
+        k_seam_h<SEAM_T0><<<grid, SEAM_T0, 0, s>>>(g, ws, s0, ns);
 }
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
     k_analyze<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
@@ -1446,7 +1558,10 @@ void launch_reps(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t no
     k_reps<<<grid_for(nodes_hint, 256, sms * 8), 256, 0, s>>>(g, ws);
 }
 void launch_cids(const Geo& g, const Ws& ws, cudaStream_t s, int sms) {
-    k_cids<<<grid_for((int64_t)g.ntiles * 32, 256, sms * 16), 256, 0, s>>>(g, ws);
+    if (g_cids_blk && wide_call(g))  // large calls: one warp per tile is faster (cfg2 merge 0.42 vs 0.51 ms)
+        k_cids_blk<<<grid_for((int64_t)g.ntiles * CIDS_T, CIDS_T, sms * 16), CIDS_T, 0, s>>>(g, ws);
+    else
+        k_cids<<<grid_for((int64_t)g.ntiles * 32, 256, sms * 16), 256, 0, s>>>(g, ws);
 }
 // (the surrounding components and pre-fill records of border components come from k_cids)
 void launch_tree(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint) {
