@@ -7,7 +7,8 @@ whole sweep of 105 images of 2048 x 2048, density k/20 (k = 0..20) x granularity
 {1, 2, 4, 8, 16}, seed 1.  Inputs are generated on the device with the reference's generator
 (bit-identical: tests/test_gpu_generate.py) and stay resident in HBM (440 MB > 126 MB L2, so
 no L2 flush is needed between steps).  `--config cfg1|cfg3|cfg4|cfg5` runs the other BASELINE
-configs (cfg4 shards its 4096 images across ranks; the others run one replica per rank).
+configs (cfg2 and cfg4 shard their images across ranks, cfg5 splits into strips, cfg1/cfg3 run
+one replica per rank).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfgX]
 

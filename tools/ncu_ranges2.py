@@ -12,9 +12,9 @@ MARKS = {
     "tile_ccl.cuh": [("helpers", "__device__ __forceinline__ int run_at("), ("tile_runs", "bool tile_runs("),
                      ("events", "__device__ bool ccl_tile("), ("first-contact", "---- first contact"),
                      ("prefix", "const int nev = __popc(ev)"), ("pre-flatten", "The first-contact forest links"),
-                     ("union", "compact the warp's events into its queue"), ("flatten", "---- flatten (roots are final"),
+                     ("union", "compact the warp's events into its queue"), ("roots", "---- roots (final now)"),
                      ("border-mark", "---- border components, marked"), ("scan/alloc", "---- tile components = root runs"),
-                     ("map-pass", "---- every run: its component"), ("rows/map-tail", "first component of each row"),
+                     ("map-pass", "---- every run: walk to its root"), ("rows/map-tail", "first component of each row"),
                      ("end", "}  // namespace rlg")],
     "kernels.cu": [("border_words", "__device__ __forceinline__ void border_words("),
                    ("a:load", "bool analyze_tile("), ("a:border-op", "The map pass of ccl_tile counts"),
