@@ -15,8 +15,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("RUNLAB_GPU_LIB", os.path.join(ROOT, "paper_2006_09299_b200", "librunlab_gpu_prof.so"))
 
-NAMES = ["start", "load+init", "runs(scan)", "events+first-contact", "union", "flatten", "lc-assign",
-         "relabel+flags", "border-compact", "header+map", "border-features", "nodes+perim+cnt", "fg-reduce"]
 
 
 def main():
@@ -52,23 +50,24 @@ def main():
     lab.label_device(imgs.data_ptr(), S, S, B, cfg)
     lab.sync()
     st = buf.view(ntiles, 32).cpu().numpy().astype(np.float64)
-    ok = (st[:, :13] > 0).all(axis=1)
-    d = np.diff(st[ok, :13], axis=1)
-    print(f"analyze: tiles with complete stamps: {ok.sum()} / {ntiles}; mean CTA latency "
-          f"{(st[ok, 12] - st[ok, 0]).mean():.0f} cycles")
-    for k in range(12):
-        print(f"  {NAMES[k + 1]:22s} {d[:, k].mean():9.0f} cycles  (p90 {np.percentile(d[:, k], 90):9.0f})")
-    ok = (st[:, 16:25] > 0).all(axis=1)
-    d = np.diff(st[ok, 16:25], axis=1)
-    ok = (st[:, 2:15] > 0).all(axis=1)
-    for name, a, b in [("  events (bit masks)", 2, 13), ("  first contact+prefix", 13, 14), ("  pre-flatten", 14, 3)]:
-        dd = st[ok, b] - st[ok, a]
-        print(f"  {name:22s} {dd.mean():9.0f} cycles  (p90 {np.percentile(dd, 90):9.0f})")
-    print(f"emit: tiles with complete stamps: {ok.sum()} / {ntiles}; mean CTA latency "
-          f"{(st[ok, 24] - st[ok, 16]).mean():.0f} cycles (chunk phases: last chunk)")
-    for k, name in enumerate(["runs+map", "border-info+repx", "ext-mask", "features", "records",
-                              "fold", "flush+reduce", "filled-image"]):
-        print(f"  {name:22s} {d[:, k].mean():9.0f} cycles  (p90 {np.percentile(d[:, k], 90):9.0f})")
+    # stamps in execution order (tile_ccl.cuh / kernels.cu RL_PHASE ids)
+    seqs = {"analyze": [(0, "start"), (1, "load+init"), (2, "runs(scan)"), (13, "events (bit masks)"),
+                        (14, "first contact+prefix"), (3, "pre-flatten"), (4, "union"), (5, "roots"),
+                        (6, "border-mark"), (8, "scan/alloc"), (9, "map pass (walks)"),
+                        (10, "border features+hdr"), (11, "perimeter"), (12, "nodes+cnt")],
+            "emit": [(16, "prologue"), (18, "runs+prefix"), (19, "chunk init"), (20, "features"),
+                     (21, "records+folds"), (22, "deferred folds"), (23, "flush"), (24, "filled image")]}
+    for name, seq in seqs.items():
+        ids = [k for k, _ in seq]
+        ok = (st[:, ids] > 0).all(axis=1)
+        if not ok.any():
+            print(f"{name}: no tile with complete stamps")
+            continue
+        print(f"{name}: tiles with complete stamps: {ok.sum()} / {ntiles}; mean CTA latency "
+              f"{(st[ok, ids[-1]] - st[ok, ids[0]]).mean():.0f} cycles (chunk phases: last chunk)")
+        for (a, _), (b, label) in zip(seq, seq[1:]):
+            d = st[ok, b] - st[ok, a]
+            print(f"  {label:24s} {d.mean():9.0f} cycles  (p90 {np.percentile(d, 90):9.0f})")
 
 
 if __name__ == "__main__":
