@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--cells", default="0.5:1")
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--cfg2", action="store_true", help="the cfg2 density/grain sweep, one image per cell")
+    ap.add_argument("--size", type=int, default=2048)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -33,7 +34,7 @@ def main():
     cells = [tuple(float(v) if i == 0 else int(v) for i, v in enumerate(c.split(":"))) for c in args.cells.split(",")]
     if args.cfg2:
         cells, args.copies = list(cfg2_cells()), 1
-    S = 2048
+    S = args.size
     B = len(cells) * args.copies
     imgs = torch.empty((B, S, S), dtype=torch.uint8, device="cuda")
     for i in range(B):
