@@ -291,6 +291,20 @@ int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out);
 /* comps/top/filled (layout 0) of [comp_lo, comp_hi), filled_image/labels of the strip's rows */
 int rl_strip_fetch(rl_ctx* ctx, const rl_strip_result* r, rl_host_outputs* out);
 
+/* Rows of n strips: multiples of the 32-row tile height, the remainder spread over the first
+ * strips, the last strip takes the image's ragged end (y0[n], h[n]).  RL_EINVAL if n exceeds
+ * the tile rows. */
+int rl_strip_rows(int32_t height, int32_t n_strips, int32_t* y0, int32_t* h);
+/* The whole strip protocol in one call, for the strips of one image held by k contexts of this
+ * process (one per GPU of a node, or several on one GPU): d_strips[r] = rows [y0[r], y0[r] + h[r])
+ * of rl_strip_rows(height, k) on ctx[r]'s device.  The phases run on one host thread per strip;
+ * the collectives are device-to-device copies between the contexts' devices (peer access over
+ * NVLink where available) and a reduction kernel on every device.  results[r] as from
+ * rl_strip_finish; rl_strip_fetch(ctx[r], &results[r], ...) then copies strip r's part out.  Errors
+ * of any strip are reported on ctx[0]. */
+int rl_label_strips(rl_ctx* const* ctx, int32_t k, const uint8_t* const* d_strips, int32_t width, int32_t height,
+                    const rl_config* cfg, rl_strip_result* results);
+
 /* Connected-operator filtering (analysis.hpp:89-125 filter_components) of one image's canonical
  * pre-fill table d_comps[n] (device): every component with d_selected[id] != 0 merges, with
  * everything embedded in it, into its surrounding component.  Outputs (device, n each):

@@ -744,7 +744,7 @@ void for_each_buf(rl_ctx* c, F&& f) {
                       &c->filled_img, &c->labels, &c->pix, &c->cub_tmp, &c->cbase, &c->summ,
                       &c->rank, &c->flag, &c->ovf, &c->ovf2, &c->thdr, &c->tmap, &c->rstore, &c->rused,
                       &c->fcomp, &c->nleft, &c->scount, &c->ncut, &c->nfold, &c->xnode, &c->gtab, &c->ftab,
-                      &c->pk, &c->pkpar, &c->pkesc, &c->fpk};
+                      &c->pk, &c->pkpar, &c->pkesc, &c->fpk, &c->xrec, &c->xgath, &c->xred};
     for (DevBuf* b : bufs) f(*b);
 }
 

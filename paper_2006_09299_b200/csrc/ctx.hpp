@@ -183,6 +183,7 @@ struct rl_ctx {
     cudaEvent_t in_done = nullptr;
     // strip mode (strips.cu)
     DevBuf nleft, scount, ncut, nfold, xnode, gtab, ftab;
+    DevBuf xrec, xgath, xred;  // rl_label_strips: own record, gathered records, reduction staging
     rlh::StripState* strip = nullptr;
 };
 

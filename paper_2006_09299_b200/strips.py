@@ -293,6 +293,38 @@ def label_strips_in_process(labelers, d_strip_ptrs, W: int, H: int, rows, config
     return out
 
 
+def label_strips_native(labelers, d_strip_ptrs, W: int, H: int, config: LabelingConfig,
+                        fetch: bool = True) -> list[StripResult]:
+    """All strips of one image through the library's single-call driver (rl_label_strips): one
+    context per strip -- one per GPU of the node, or several on one GPU -- with the collectives
+    done as device-to-device copies (peer access over NVLink) and reduction kernels, the strips'
+    phases on one host thread each.  Rows per strip: strip_rows(H, len(labelers))."""
+    k = len(labelers)
+    L = labelers[0]._L
+    ctxs = (C.c_void_p * k)(*[lab.ctx for lab in labelers])
+    ptrs = (C.c_void_p * k)(*d_strip_ptrs)
+    res = (N.RlStripResult * k)()
+    rc = L.rl_label_strips(ctxs, k, ptrs, W, H, C.byref(config.to_c()), res)
+    if rc != N.RL_OK:
+        _raise(rc, labelers[0]._err())
+    out = []
+    for lab, r in zip(labelers, res):
+        ph = _PHASES.get(id(lab))
+        if ph is None or ph.lab is not lab:
+            ph = _PHASES[id(lab)] = StripPhases(lab)
+        ph.W, ph.H = W, H
+        if not fetch:
+            out.append(StripResult(int(r.comp_lo), int(r.comp_hi), int(r.n_components), int(r.n_fg),
+                                   int(r.n_holes), int(r.euler), int(r.n_survivors), int(r.y0), int(r.h)))
+            continue
+        sr = ph.fetch(r, config.relabel)
+        for f in ("comps", "top", "filled", "filled_image", "labels"):  # the staging is per context
+            v = getattr(sr, f)
+            setattr(sr, f, None if v is None else v.copy())
+        out.append(sr)
+    return out
+
+
 def concat(results: list[StripResult]) -> dict:
     """Whole-image tables from the strips' owned ranges (comparable with a single-image call)."""
     rs = sorted(results, key=lambda r: r.y0)

@@ -96,15 +96,22 @@ def test_cfg5_unsplit_vs_reference(labeler, cfg5):
 
 
 @pytest.mark.timeout(1200)
-def test_cfg5_eight_strips_full_size(labeler, cfg5):
-    from paper_2006_09299_b200.strips import concat, label_strips_in_process, strip_rows
+@pytest.mark.parametrize("driver", ["lockstep", "native"])
+def test_cfg5_eight_strips_full_size(labeler, cfg5, driver):
+    """Config 5 in 8 full-size strips: the Python lockstep driver, and the library's own
+    single-call driver (rl_label_strips: host thread per strip, device-to-device collectives)."""
+    from paper_2006_09299_b200.strips import concat, label_strips_in_process, label_strips_native, strip_rows
     W = H = 32768
     labeler.label_device(cfg5.data_ptr(), W, H, 1, FULL)
     whole = labeler.fetch().image(0)
     rows = strip_rows(H, 8)
     labs = [Labeler(0) for _ in range(8)]
+    ptrs = [cfg5.data_ptr() + y0 * W for y0, _ in rows]
     try:
-        got = concat(label_strips_in_process(labs, [cfg5.data_ptr() + y0 * W for y0, _ in rows], W, H, rows, FULL))
+        if driver == "native":
+            got = concat(label_strips_native(labs, ptrs, W, H, FULL))
+        else:
+            got = concat(label_strips_in_process(labs, ptrs, W, H, rows, FULL))
     finally:
         for lab in labs:
             lab.close()

@@ -169,3 +169,58 @@ def test_strip_workspace_follows_the_strip(labeler):
         whole.close()
         for lab in labs:
             lab.close()
+
+
+# ---- the library's single-call driver (rl_label_strips): strips on several contexts of one
+# process, collectives as device-to-device copies + reduction kernels
+def _run_native(labelers, img_dev, W, H, n, cfg):
+    from paper_2006_09299_b200.strips import label_strips_native
+    rows = strip_rows(H, n)
+    ptrs = [img_dev.data_ptr() + y0 * W for (y0, _) in rows]
+    return concat(label_strips_native(labelers[:n], ptrs, W, H, cfg))
+
+
+@pytest.mark.parametrize("d,g", [(0.5, 1), (0.45, 4), (0.95, 1)])
+@pytest.mark.parametrize("n", [1, 2, 5, 8])
+def test_native_strips_match_single_image(labelers, labeler, d, g, n):
+    W, H = 1536, 1000
+    img = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    generate_device(img.data_ptr(), W, H, d, g, 11)
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    labeler.label_device(img.data_ptr(), W, H, 1, cfg)
+    labeler.sync()
+    ref = labeler.fetch()
+    _compare(_run_native(labelers, img, W, H, n, cfg), ref, f"native d={d} g={g} n={n}")
+    # repeated calls reuse the contexts' exchange buffers
+    _compare(_run_native(labelers, img, W, H, n, cfg), ref, f"native again d={d} g={g} n={n}")
+
+
+def test_native_strips_rings_labels_and_oracle(labelers):
+    W, H = 777, 300
+    img = O.generate_rings(W, H, 64, 3, 0.02)
+    dev = torch.from_numpy(img).cuda()
+    for conn in (0, 1):
+        ref = O.label_canonical(img, conn, want_labels=True)
+        cfg = LabelingConfig(connectivity=conn, compute_features=True, compute_euler=True, fill_holes=True)
+        got = _run_native(labelers, dev, W, H, 4, cfg)
+        assert got["n_components"] == ref.n_components and got["euler"] == ref.euler
+        assert got["comps"].tobytes() == ref.comps.tobytes()
+        np.testing.assert_array_equal(got["top"], ref.top)
+        np.testing.assert_array_equal(got["filled_image"], ref.filled_image)
+        # the label image (pre-fill canonical ids, Alg. 4 relabel)
+        cfg = LabelingConfig(connectivity=conn, compute_features=True, relabel=True)
+        got = _run_native(labelers, dev, W, H, 4, cfg)
+        np.testing.assert_array_equal(got["labels"], ref.labels)
+
+
+def test_native_strip_rows_and_errors(labelers):
+    import ctypes as C
+    from paper_2006_09299_b200.strips import label_strips_native
+    L = labelers[0]._L
+    y0, h = (C.c_int32 * 5)(), (C.c_int32 * 5)()
+    assert L.rl_strip_rows(1000, 5, y0, h) == 0
+    assert [(a, b) for a, b in zip(y0, h)] == strip_rows(1000, 5)
+    assert L.rl_strip_rows(64, 3, y0, h) != 0  # more strips than tile rows
+    img = torch.zeros((64, 64), dtype=torch.uint8, device="cuda")
+    with pytest.raises(Exception):
+        label_strips_native(labelers[:3], [img.data_ptr()] * 3, 64, 64, LabelingConfig())
