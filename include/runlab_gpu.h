@@ -304,6 +304,10 @@ int rl_strip_rows(int32_t height, int32_t n_strips, int32_t* y0, int32_t* h);
  * of any strip are reported on ctx[0]. */
 int rl_label_strips(rl_ctx* const* ctx, int32_t k, const uint8_t* const* d_strips, int32_t width, int32_t height,
                     const rl_config* cfg, rl_strip_result* results);
+/* The same from a host image (row-major w x H bytes): each strip's rows are copied to its
+ * context's device first. */
+int rl_label_strips_host(rl_ctx* const* ctx, int32_t k, const uint8_t* pixels, int32_t width, int32_t height,
+                         const rl_config* cfg, rl_strip_result* results);
 
 /* Connected-operator filtering (analysis.hpp:89-125 filter_components) of one image's canonical
  * pre-fill table d_comps[n] (device): every component with d_selected[id] != 0 merges, with

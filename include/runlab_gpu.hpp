@@ -262,10 +262,7 @@ inline FeatureAccumulator to_acc(const rl_features& f) {
     return a;
 }
 
-inline LabelingResult run(const BinaryImage& image, const LabelingConfig& config, StepTimes* times) {
-    if (config.densify_labels && !config.relabel)
-        throw std::invalid_argument("label_image: densify_labels requires relabel");
-    rl_ctx* ctx = thread_context().get();
+inline rl_config to_c(const LabelingConfig& config) {
     rl_config c{};
     c.connectivity = config.connectivity == Connectivity::fg4_bg8 ? RL_FG4_BG8 : RL_FG8_BG4;
     c.fill_holes = config.fill_holes;
@@ -273,6 +270,52 @@ inline LabelingResult run(const BinaryImage& image, const LabelingConfig& config
     c.relabel = config.relabel;
     c.densify_labels = config.densify_labels;
     c.compute_euler = config.compute_euler;
+    return c;
+}
+
+// LabelingResult of one image from its canonical tables (ids in raster order of first pixel):
+// pre-fill records, post-fill roots and their features, label image, counts.
+inline LabelingResult assemble(std::int32_t width, std::int32_t height, const LabelingConfig& config, std::int64_t n,
+                               const rl_component* comps, const std::uint32_t* top, const rl_features* filled,
+                               const std::uint32_t* labels, std::int64_t n_fg, std::int64_t n_holes,
+                               std::int64_t euler) {
+    std::vector<label_t> t(static_cast<std::size_t>(n)), adj(static_cast<std::size_t>(n));
+    std::vector<std::uint8_t> fg(static_cast<std::size_t>(n));
+    for (std::int64_t e = 0; e < n; ++e) {
+        t[e] = config.fill_holes ? top[e] : static_cast<label_t>(e);
+        adj[e] = e == 0 ? no_label : comps[e].parent;
+        fg[e] = static_cast<std::uint8_t>(comps[e].flags & 1u);
+    }
+    LabelingResult res;
+    res.width = width;
+    res.height = height;
+    res.config = config;
+    if (config.compute_features) {
+        FeatureTable ft(static_cast<std::size_t>(n));
+        for (std::int64_t e = 0; e < n; ++e)
+            ft[e] = to_acc((config.fill_holes && top[e] == e) ? filled[e] : comps[e].f);
+        res.features = std::move(ft);
+    }
+    if (config.relabel) {
+        LabelImage li(width, height);
+        std::copy(labels, labels + li.labels.size(), li.labels.begin());
+        res.labels = std::move(li);
+    }
+    if (config.compute_euler) {
+        res.fg_count = n_fg;
+        res.hole_count = n_holes;
+        res.euler = euler;
+    }
+    res.equivalences = EquivalenceTable(std::move(t), std::move(fg));
+    res.adjacency = AdjacencyTable(std::move(adj));
+    return res;
+}
+
+inline LabelingResult run(const BinaryImage& image, const LabelingConfig& config, StepTimes* times) {
+    if (config.densify_labels && !config.relabel)
+        throw std::invalid_argument("label_image: densify_labels requires relabel");
+    rl_ctx* ctx = thread_context().get();
+    const rl_config c = to_c(config);
     rl_result r{};
     const int rc = rl_label(ctx, image.pixels.data(), image.width, image.height, 1, &c, &r);
     if (rc != RL_OK) raise(rc, ctx);
@@ -280,37 +323,8 @@ inline LabelingResult run(const BinaryImage& image, const LabelingConfig& config
         rl_result* r;
         ~Free() { rl_result_free(r); }
     } guard{&r};
-
-    const std::int64_t n = r.n_components[0];
-    std::vector<label_t> t(static_cast<std::size_t>(n)), adj(static_cast<std::size_t>(n));
-    std::vector<std::uint8_t> fg(static_cast<std::size_t>(n));
-    for (std::int64_t e = 0; e < n; ++e) {
-        t[e] = config.fill_holes ? r.top[e] : static_cast<label_t>(e);
-        adj[e] = e == 0 ? no_label : r.comps[e].parent;
-        fg[e] = static_cast<std::uint8_t>(r.comps[e].flags & 1u);
-    }
-    LabelingResult res;
-    res.width = image.width;
-    res.height = image.height;
-    res.config = config;
-    if (config.compute_features) {
-        FeatureTable ft(static_cast<std::size_t>(n));
-        for (std::int64_t e = 0; e < n; ++e)
-            ft[e] = to_acc((config.fill_holes && r.top[e] == e) ? r.filled[e] : r.comps[e].f);
-        res.features = std::move(ft);
-    }
-    if (config.relabel) {
-        LabelImage li(image.width, image.height);
-        std::copy(r.labels, r.labels + li.labels.size(), li.labels.begin());
-        res.labels = std::move(li);
-    }
-    if (config.compute_euler) {
-        res.fg_count = r.n_fg[0];
-        res.hole_count = r.n_holes[0];
-        res.euler = r.euler[0];
-    }
-    res.equivalences = EquivalenceTable(std::move(t), std::move(fg));
-    res.adjacency = AdjacencyTable(std::move(adj));
+    LabelingResult res = assemble(image.width, image.height, config, r.n_components[0], r.comps, r.top, r.filled,
+                                  r.labels, r.n_fg[0], r.n_holes[0], r.euler[0]);
     if (times) {
         times->encode_ns = r.times.analyze_ms * 1e6;
         times->unify_ns = r.times.merge_ms * 1e6;
@@ -319,6 +333,41 @@ inline LabelingResult run(const BinaryImage& image, const LabelingConfig& config
         times->total_ns = r.times.total_ms * 1e6;
     }
     return res;
+}
+
+// One image across several GPUs of this process (one entry of `devices` per strip; a device may
+// repeat): horizontal strips exchanging only the components that touch the cut rows
+// (rl_label_strips_host).  The result equals label_image(image, config).
+// densify_labels is not supported in strip mode (std::invalid_argument).
+inline LabelingResult label_image_strips(const BinaryImage& image, const LabelingConfig& config,
+                                         const std::vector<int>& devices) {
+    if (devices.empty()) throw std::invalid_argument("label_image_strips: no devices");
+    std::vector<Context> ctxs;
+    ctxs.reserve(devices.size());
+    for (int d : devices) ctxs.emplace_back(d);
+    std::vector<rl_ctx*> raw;
+    for (auto& c : ctxs) raw.push_back(c.get());
+    const int k = static_cast<int>(raw.size());
+    const rl_config c = to_c(config);
+    std::vector<rl_strip_result> res(static_cast<std::size_t>(k));
+    int rc = rl_label_strips_host(raw.data(), k, image.pixels.data(), image.width, image.height, &c, res.data());
+    if (rc != RL_OK) raise(rc, raw[0]);
+    const std::int64_t n = res[0].n_components;
+    std::vector<rl_component> comps(static_cast<std::size_t>(n));
+    std::vector<std::uint32_t> top(static_cast<std::size_t>(n));
+    std::vector<rl_features> filled(static_cast<std::size_t>(n));
+    std::vector<std::uint32_t> labels(config.relabel ? image.pixels.size() : 0);
+    for (int r = 0; r < k; ++r) {
+        rl_host_outputs o{};
+        o.comps = comps.data() + res[r].comp_lo;
+        o.top = top.data() + res[r].comp_lo;
+        o.filled = filled.data() + res[r].comp_lo;
+        o.comp_capacity = res[r].comp_hi - res[r].comp_lo;
+        o.labels = config.relabel ? labels.data() + static_cast<std::size_t>(res[r].y0) * image.width : nullptr;
+        if ((rc = rl_strip_fetch(raw[r], &res[r], &o)) != RL_OK) raise(rc, raw[r]);
+    }
+    return assemble(image.width, image.height, config, n, comps.data(), top.data(), filled.data(), labels.data(),
+                    res[0].n_fg, res[0].n_holes, res[0].euler);
 }
 
 }  // namespace gpu

@@ -23,7 +23,7 @@ EXPORTED_SYMBOLS = (
     "rl_phase_times", "rl_generate", "rl_generate_rings", "rl_cfg4_params", "rl_last_used_graph",
     "rl_strip_local", "rl_strip_export_bytes", "rl_strip_export", "rl_strip_merge", "rl_strip_resolve",
     "rl_strip_finish",
-    "rl_strip_fetch", "rl_strip_rows", "rl_label_strips", "rl_generate_rows", "rl_filter_components",
+    "rl_strip_fetch", "rl_strip_rows", "rl_label_strips", "rl_label_strips_host", "rl_generate_rows", "rl_filter_components",
     "rl_filter_components_host", "rl_label_device_fmt", "rl_label_into_fmt", "rl_pbm_parse", "rl_pbm_p1_to_p4",
     "rl_pbm_p4_header", "rl_fill_pbm", "rl_generate_host", "rl_workspace_bytes", "rl_set_pipelines",
 )
@@ -156,6 +156,8 @@ def load() -> C.CDLL:
     L.rl_strip_rows.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.rl_label_strips.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p), C.c_int32, C.c_int32,
                                   C.POINTER(RlConfig), C.POINTER(RlStripResult)]
+    L.rl_label_strips_host.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                                       C.POINTER(RlConfig), C.POINTER(RlStripResult)]
     _lib = L
     return L
 

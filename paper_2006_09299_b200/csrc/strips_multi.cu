@@ -227,4 +227,29 @@ int rl_label_strips(rl_ctx* const* ctx, int32_t k, const uint8_t* const* d_strip
     return RL_OK;
 }
 
+int rl_label_strips_host(rl_ctx* const* ctx, int32_t k, const uint8_t* pixels, int32_t width, int32_t height,
+                         const rl_config* cfg, rl_strip_result* results) {
+    if (!ctx || !pixels || k < 1 || width < 1) return RL_EINVAL;
+    std::vector<int32_t> y0(k), h(k);
+    if (rl_strip_rows(height, k, y0.data(), h.data()) != RL_OK)
+        return ctx[0] ? set_err(ctx[0], RL_EINVAL, "strips: cannot cut the image into that many strips of whole tile rows")
+                      : RL_EINVAL;
+    std::vector<const uint8_t*> d(k);
+    for (int r = 0; r < k; ++r) {  // each strip's rows into its context's input buffer
+        if (!ctx[r]) return RL_EINVAL;
+        cudaSetDevice(ctx[r]->device);
+        const size_t bytes = (size_t)h[r] * width;
+        if (!ensure(ctx[r]->pix, bytes)) return set_err(ctx[r], RL_ENOMEM, "device allocation failed");
+        const cudaError_t e = cudaMemcpyAsync(ctx[r]->pix.p, pixels + (size_t)y0[r] * width, bytes,
+                                              cudaMemcpyHostToDevice, ctx[r]->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx[r], e, "strips: copy in");
+        d[r] = P<uint8_t>(ctx[r]->pix);
+    }
+    for (int r = 0; r < k; ++r) {
+        const cudaError_t e = cudaStreamSynchronize(ctx[r]->stream);
+        if (e != cudaSuccess) return cuda_fail(ctx[r], e, "strips: copy in");
+    }
+    return rl_label_strips(ctx, k, d.data(), width, height, cfg, results);
+}
+
 }  // extern "C"

@@ -347,6 +347,35 @@ int main() {
         const LabelingResult b = label_image(fig, full_config());
         CHECK(*a.labels == *b.labels && t.total_ns > 0);
     }
+    // one image as horizontal strips over several contexts (rl_label_strips_host) == label_image
+    {
+        BinaryImage big(700, 300);
+        std::uint64_t x = 12345;
+        for (auto& p : big.pixels) {  // blocky noise with holes crossing the strip cuts
+            x = x * 6364136223846793005ull + 1442695040888963407ull;
+            p = (x >> 61) < 4 ? 1 : 0;
+        }
+        for (int y = 40; y < 260; ++y)  // a ring around the cuts
+            for (int c = 40; c < 660; ++c)
+                if (y < 44 || y >= 256 || c < 44 || c >= 656) big.pixels[y * 700 + c] = 1;
+        for (bool fill : {false, true}) {
+            LabelingConfig cfg = full_config();
+            cfg.fill_holes = fill;
+            cfg.relabel = !fill;
+            const LabelingResult a = label_image(big, cfg);
+            for (int k : {1, 3, 5}) {
+                const LabelingResult b = gpu::label_image_strips(big, cfg, std::vector<int>(k, 0));
+                CHECK(b.equivalences.size() == a.equivalences.size());
+                CHECK(parents_of(b.equivalences) == parents_of(a.equivalences));
+                bool same_adj = b.adjacency.size() == a.adjacency.size();
+                for (label_t e = 0; same_adj && e < a.adjacency.size(); ++e) same_adj = a.adjacency[e] == b.adjacency[e];
+                CHECK(same_adj);
+                CHECK(*b.features == *a.features);
+                CHECK(*b.euler == *a.euler && *b.fg_count == *a.fg_count && *b.hole_count == *a.hole_count);
+                if (!fill) CHECK(*b.labels == *a.labels);
+            }
+        }
+    }
     std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
     return failures;
 }
