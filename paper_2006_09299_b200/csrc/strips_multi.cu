@@ -50,17 +50,24 @@ struct Barrier {
     std::condition_variable cv;
     int n, waiting = 0;
     unsigned gen = 0;
+    bool broken = false;  // a strip thread could not be started: every wait returns at once
     explicit Barrier(int n_) : n(n_) {}
     void wait() {
         std::unique_lock<std::mutex> lk(m);
+        if (broken) return;
         const unsigned g = gen;
         if (++waiting == n) {
             waiting = 0;
             ++gen;
             cv.notify_all();
         } else {
-            cv.wait(lk, [&] { return gen != g; });
+            cv.wait(lk, [&] { return gen != g || broken; });
         }
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lk(m);
+        broken = true;
+        cv.notify_all();
     }
 };
 
@@ -94,9 +101,28 @@ int rl_strip_rows(int32_t height, int32_t n_strips, int32_t* y0, int32_t* h) {
     return RL_OK;
 }
 
+namespace {
+int label_strips(rl_ctx* const* ctx, int32_t k, const uint8_t* const* d_strips, int32_t width, int32_t height,
+                 const rl_config* cfg, rl_strip_result* results);
+}
+
 int rl_label_strips(rl_ctx* const* ctx, int32_t k, const uint8_t* const* d_strips, int32_t width, int32_t height,
                     const rl_config* cfg, rl_strip_result* results) {
     if (!ctx || !d_strips || !cfg || !results || k < 1) return RL_EINVAL;
+    try {  // no C++ exception crosses the C ABI (thread creation, allocation)
+        return label_strips(ctx, k, d_strips, width, height, cfg, results);
+    } catch (const std::bad_alloc&) {
+        return ctx[0] ? set_err(ctx[0], RL_ENOMEM, "strips: host allocation failed") : RL_ENOMEM;
+    } catch (const std::exception& e) {
+        return ctx[0] ? set_err(ctx[0], RL_EINTERNAL, std::string("strips: ") + e.what()) : RL_EINTERNAL;
+    }
+}
+
+}  // extern "C"
+
+namespace {
+int label_strips(rl_ctx* const* ctx, int32_t k, const uint8_t* const* d_strips, int32_t width, int32_t height,
+                 const rl_config* cfg, rl_strip_result* results) {
     for (int r = 0; r < k; ++r) {
         if (!ctx[r] || !d_strips[r]) return RL_EINVAL;
         for (int q = 0; q < r; ++q)
@@ -216,8 +242,15 @@ int rl_label_strips(rl_ctx* const* ctx, int32_t k, const uint8_t* const* d_strip
     };
     std::vector<std::thread> th;
     th.reserve(k);
-    for (int r = 1; r < k; ++r) th.emplace_back(rank, r);
-    rank(0);
+    bool started = true;
+    try {
+        for (int r = 1; r < k; ++r) th.emplace_back(rank, r);
+    } catch (const std::exception&) {  // no thread for every strip: the started ones bail out
+        started = false;
+        fail(0, set_err(ctx[0], RL_EINTERNAL, "strips: could not start the strip threads"));
+        bar.abort();
+    }
+    if (started) rank(0);
     for (auto& t : th) t.join();
     for (int r = 0; r < k; ++r)
         if (rc[r]) {
@@ -226,6 +259,9 @@ int rl_label_strips(rl_ctx* const* ctx, int32_t k, const uint8_t* const* d_strip
         }
     return RL_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int rl_label_strips_host(rl_ctx* const* ctx, int32_t k, const uint8_t* pixels, int32_t width, int32_t height,
                          const rl_config* cfg, rl_strip_result* results) {
