@@ -818,6 +818,7 @@ void rl_destroy(rl_ctx* c) {
         if (b.p) cudaFree(b.p);
     });
     if (c->h_summ) cudaFreeHost(c->h_summ);
+    if (c->h_strip) cudaFreeHost(c->h_strip);
     for (auto& slot : c->ring)
         for (auto& e : slot)
             if (e) cudaEventDestroy(e);

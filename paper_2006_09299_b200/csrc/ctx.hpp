@@ -184,6 +184,8 @@ struct rl_ctx {
     // strip mode (strips.cu)
     DevBuf nleft, scount, ncut, nfold, xnode, gtab, ftab;
     DevBuf xrec, xgath, xred;  // rl_label_strips: own record, gathered records, reduction staging
+    uint8_t* h_strip = nullptr;  // pinned staging of the strip phases' small host<->device transfers
+    size_t h_strip_n = 0;
     rlh::StripState* strip = nullptr;
 };
 

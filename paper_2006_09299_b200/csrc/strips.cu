@@ -522,6 +522,24 @@ StripState* strip_state(rl_ctx* c) {
     return c->strip;
 }
 
+// Pinned staging for the phases' small transfers: copies from or to pageable host memory would
+// each wait for the stream (a host round trip per counter); these are asynchronous and the phase
+// synchronises once.
+uint8_t* strip_pinned(rl_ctx* c, size_t bytes) {
+    if (c->h_strip_n < bytes) {
+        if (c->h_strip) cudaFreeHost(c->h_strip);
+        c->h_strip = nullptr;
+        c->h_strip_n = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        if (cudaMallocHost(&c->h_strip, want) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        c->h_strip_n = want;
+    }
+    return c->h_strip;
+}
+
 int sync_err(rl_ctx* c, const char* what) {
     const cudaError_t e = cudaStreamSynchronize(c->stream);
     return e == cudaSuccess ? RL_OK : cuda_fail(c, e, what);
@@ -635,18 +653,22 @@ int rl_strip_local(rl_ctx* ctx, const uint8_t* d_strip, int32_t w, int32_t H, in
         k_strip_count<<<grid(std::max<int64_t>(nmax, (int64_t)(g.ty1 - g.ty0) * TH * g.ntx), ctx->sms), 256, 0, s>>>(
             g, ws, flag, rank, P<uint32_t>(ctx->xnode), cnt2);
         STRIP_STEP(ctx, "k_strip_count");
-        uint32_t hc[8] = {};
+        uint8_t* hp = strip_pinned(ctx, 96);
+        if (!hp) return set_err(ctx, RL_ENOMEM, "pinned alloc failed");
+        uint32_t* hc = reinterpret_cast<uint32_t*>(hp);                      // [8] counters
+        uint32_t* hfg = reinterpret_cast<uint32_t*>(hp + 32);                // img_fg
+        unsigned long long* hrused = reinterpret_cast<unsigned long long*>(hp + 40);
+        uint32_t* klast = reinterpret_cast<uint32_t*>(hp + 48);             // [2]
+        unsigned long long* hcnt = reinterpret_cast<unsigned long long*>(hp + 56);  // [2]
         cudaMemcpyAsync(hc, ws.counters, 32, cudaMemcpyDeviceToHost, s);
-        uint32_t fg = 0;
-        cudaMemcpyAsync(&fg, ws.img_fg, 4, cudaMemcpyDeviceToHost, s);
-        unsigned long long rused = 0;
-        cudaMemcpyAsync(&rused, ws.rused, 8, cudaMemcpyDeviceToHost, s);
-        uint32_t klast[2] = {};
-        unsigned long long hcnt[2] = {};
+        cudaMemcpyAsync(hfg, ws.img_fg, 4, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(hrused, ws.rused, 8, cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(&klast[0], rank + nmax, 4, cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(&klast[1], flag + nmax, 4, cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(hcnt, cnt2, 16, cudaMemcpyDeviceToHost, s);
         if ((rc = sync_err(ctx, "strip local"))) return rc;
+        const uint32_t fg = *hfg;
+        const unsigned long long rused = *hrused;
         if (hc[1] & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip left link)");
         if (hc[1] & (ERR_NODE_CAP | ERR_RSTORE_CAP)) {
             if (hc[1] & ERR_NODE_CAP) ctx->cap_nodes = (uint32_t)std::min<uint64_t>(hc[0] + hc[0] / 4 + 1024, 0xF0000000ull);
@@ -722,7 +744,12 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     if (!ensure(ctx->gtab, g_layout(nullptr, C, n_strips).bytes)) return set_err(ctx, RL_ENOMEM, "device allocation failed");
     GTab T = gtab(ctx);
     const XSrc X{static_cast<const uint8_t*>(d_gathered), x_layout(g.W, max_classes), n_strips};
-    cudaMemcpyAsync(T.coff, coff.data(), (n_strips + 1) * 4, cudaMemcpyHostToDevice, s);
+    uint8_t* hp = strip_pinned(ctx, (size_t)(n_strips + 1) * 4 + (size_t)2 * n_strips * 4 + 64);
+    if (!hp) return set_err(ctx, RL_ENOMEM, "pinned alloc failed");
+    uint32_t* hcoff = reinterpret_cast<uint32_t*>(hp);
+    uint32_t* hsc = hcoff + (n_strips + 1);
+    std::copy(coff.begin(), coff.end(), hcoff);
+    cudaMemcpyAsync(T.coff, hcoff, (n_strips + 1) * 4, cudaMemcpyHostToDevice, s);
     cudaMemsetAsync(T.scnt, 0, (size_t)2 * n_strips * 4, s);
     cudaMemsetAsync(T.gsurv, 0, 4, s);
     // ---- global cut classes (identical on every rank)
@@ -737,10 +764,10 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     STRIP_STEP(ctx, "k_g_fold");
     k_g_reps<<<grid(C, ctx->sms), 256, 0, s>>>(X, T, C);
     STRIP_STEP(ctx, "k_g_reps");
-    std::vector<uint32_t> sc(2 * n_strips);
-    cudaMemcpyAsync(sc.data(), T.scnt, sc.size() * 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hsc, T.scnt, (size_t)2 * n_strips * 4, cudaMemcpyDeviceToHost, s);
     int rc = sync_err(ctx, "strip cut merge");
     if (rc) return rc;
+    const std::vector<uint32_t> sc(hsc, hsc + 2 * n_strips);
     int64_t total = 1, fg = 0, off_me = 0;
     for (int q = 0; q < n_strips; ++q) {
         if (q == me) off_me = total - 1;
@@ -784,9 +811,10 @@ int rl_strip_merge(rl_ctx* ctx, const void* d_gathered, int32_t n_strips, const 
     k_g_links<<<grid(S->n_classes + 1, ctx->sms), 256, 0, s>>>(ws, T, xnode, S->n_classes, S->c0,
                                                                  (uint32_t)S->n_local);
     STRIP_STEP(ctx, "k_g_links");
-    uint32_t err = 0;
-    cudaMemcpyAsync(&err, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
+    uint32_t* herr = reinterpret_cast<uint32_t*>(strip_pinned(ctx, 64));  // the buffer exists (grown above)
+    cudaMemcpyAsync(herr, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
     if ((rc = sync_err(ctx, "strip merge"))) return rc;
+    const uint32_t err = *herr;
     if (err & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip links)");
     ctx->ws = ws;
     ctx->geo = g;
@@ -829,10 +857,12 @@ int rl_strip_resolve(rl_ctx* ctx, rl_strip_partials* out) {
     STRIP_STEP(ctx, "launch_fold");
     k_g_partials<<<grid(C, ctx->sms), 256, 0, s>>>(g, ws, T, C, ws.img_surv, isurv, S->rank > 0 ? 1 : 0);
     STRIP_STEP(ctx, "k_g_partials");
-    uint32_t err = 0;
-    cudaMemcpyAsync(&err, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
+    uint32_t* herr = reinterpret_cast<uint32_t*>(strip_pinned(ctx, 64));
+    if (!herr) return set_err(ctx, RL_ENOMEM, "pinned alloc failed");
+    cudaMemcpyAsync(herr, ws.counters + 1, 4, cudaMemcpyDeviceToHost, s);
     const int rc = sync_err(ctx, "strip resolve");
     if (rc) return rc;
+    const uint32_t err = *herr;
     if (err & ERR_INTERNAL) return set_err(ctx, RL_EINTERNAL, "device invariant violated (strip tree)");
     ctx->launches += 3 + 1 + 3 + (g.tpi >= 8192 ? 1 : 0) + 1 + 1;
     out->d_sum = T.psum;
@@ -854,12 +884,14 @@ int rl_strip_finish(rl_ctx* ctx, rl_strip_result* out) {
     k_g_finish<<<grid(S->C, ctx->sms), 256, 0, s>>>(S->g, ctx->ws, T, S->C);
     STRIP_STEP(ctx, "k_g_finish");
     ctx->launches += 1;
-    int64_t surv = 0;
-    uint32_t gsurv = 0;
-    cudaMemcpyAsync(&surv, T.pcnt, 8, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&gsurv, T.gsurv, 4, cudaMemcpyDeviceToHost, s);
+    uint8_t* hp = strip_pinned(ctx, 64);
+    if (!hp) return set_err(ctx, RL_ENOMEM, "pinned alloc failed");
+    cudaMemcpyAsync(hp, T.pcnt, 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hp + 8, T.gsurv, 4, cudaMemcpyDeviceToHost, s);
     const int rc = sync_err(ctx, "strip finish");
     if (rc) return rc;
+    const int64_t surv = *reinterpret_cast<const int64_t*>(hp);
+    const uint32_t gsurv = *reinterpret_cast<const uint32_t*>(hp + 8);
     out->n_components = S->total;
     out->n_fg = S->fg;
     out->n_holes = S->total - 1 - S->fg;
