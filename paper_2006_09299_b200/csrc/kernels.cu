@@ -1150,9 +1150,17 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     // runs again from the packed bits (cheap); the component map comes from the analyze pass
     RL_PHASE(tg.t, 16);
     const int nruns = nruns_h, nlc = nlc_h, nb = nb_h;
-    if (word) {  // run positions of this word's run starts (the word bases are the analyze pass's)
+    // run positions of the run starts (the word bases are the analyze pass's); the 512-thread
+    // classes give each half of a word to its own thread
+    if constexpr (BT == NW) {
         int i = S.rbase[tid];
         for (uint32_t m = S.st[tid]; m; m &= m - 1u) S.runpos[i++] = (uint16_t)((r << 8) | (32 * w + __ffs(m) - 1));
+    } else {
+        const int wd = tid % NW, half = tid / NW;
+        const uint32_t st = S.st[wd], lo = 0xFFFFu;
+        int i = S.rbase[wd] + (half ? __popc(st & lo) : 0);
+        const uint16_t rw = (uint16_t)(((wd / WPR) << 8) | (32 * (wd % WPR)));
+        for (uint32_t m = half ? (st & ~lo) : (st & lo); m; m &= m - 1u) S.runpos[i++] = (uint16_t)(rw + __ffs(m) - 1);
     }
     const uint64_t cb = E.cb;
     for (int i = tid; i < min(C::FCH, nlc); i += BT) {  // first feature chunk's accumulators
@@ -1161,19 +1169,18 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
         E.fcmin[i] = 0x7FFFFFFF;
         E.fcmax[i] = -1;
     }
-    if (tid < 32) {  // warp prefix of representative flags over border index (flags are in)
+    // exclusive prefix of the representative flags over border index (flags are in), by one warp
+    // (ballot + popc per 32 entries); in the 512-thread classes a warp without a word does it
+    constexpr int PW = BT == NW ? NWARPS - 1 : NWARPS;
+    if ((tid >> 5) == PW) {
+        const int lane = tid & 31;
         int carry = 0;
         for (int i0 = 0; i0 <= nb; i0 += 32) {
-            const int i = i0 + tid;
-            const int f = (i < nb) ? (E.bflag[i] & 1) : 0;
-            int incl = f;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int n = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (tid >= o) incl += n;
-            }
-            if (i <= nb) E.repx[i] = (uint16_t)(carry + incl - f);
-            carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+            const int i = i0 + lane;
+            const bool f = i < nb && (E.bflag[i] & 1);
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+            if (i <= nb) E.repx[i] = (uint16_t)(carry + __popc(m & ((1u << lane) - 1u)));
+            carry += __popc(m);
         }
     }
     __syncthreads();
