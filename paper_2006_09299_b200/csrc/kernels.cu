@@ -1098,7 +1098,9 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     if (tid == 0) {
         E.ndfold = 0;
         E.cb = (uint64_t)offimg + (uint64_t)tg.b;
-        E.gate = !ws.counters[1] && comps_fit(g, ws);
+        const uint32_t errs = ws.counters[1];
+        const bool fit = comps_fit(g, ws);  // both loads in flight together (no short circuit)
+        E.gate = !errs && fit;
         S.nlc = nlc_h;
         S.nb = nb_h;
         S.nruns = nruns_h;
