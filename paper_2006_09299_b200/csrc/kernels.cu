@@ -456,9 +456,10 @@ __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int
     if (ws.counters[1]) return;
     const uint32_t v8 = g.flip ? 0u : 1u;
     const int32_t tx = blockIdx.x, tid = threadIdx.x;
-    for (int32_t bs = blockIdx.y; bs < g.B * ns; bs += gridDim.y) {
-        const int32_t s = s0 + bs % ns;
-        const int32_t b = bs / ns;
+    // grid (tile column, seam, image): no division by the seam count per block
+    for (int32_t b = blockIdx.z; b < g.B; b += gridDim.z)
+    for (int32_t si = blockIdx.y; si < ns; si += gridDim.y) {
+        const int32_t s = s0 + si;
         const int64_t tu = ((int64_t)b * g.nty + s) * g.ntx + tx, tl = tu + g.ntx;
         const int nbu = (int)ws.tnb[tu], nbd = (int)ws.tnb[tl];
         if (tid < TW / 8)
@@ -1538,8 +1539,7 @@ static int grid_for(int64_t n, int block, int maxgrid) {
 }
 
 void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms) {
-    const int64_t pairs = (int64_t)g.B * ns;
-    const dim3 grid(g.ntx, (unsigned)std::min<int64_t>(pairs, 65535));
+    const dim3 grid(g.ntx, (unsigned)std::min<int64_t>(ns, 65535), (unsigned)std::min<int64_t>(g.B, 65535));
     if (wide_call(g))
         k_seam_h<SEAM_TW><<<grid, SEAM_TW, 0, s>>>(g, ws, s0, ns);
     else
