@@ -793,6 +793,7 @@ rl_ctx* rl_create(int device) {
     if (const char* v = std::getenv("RUNLAB_GPU_KIDS")) c->nkids = std::min(rl_ctx::MAXKIDS, std::max(1, std::atoi(v)));
     if (const char* v = std::getenv("RUNLAB_GPU_HOST_THREADS")) c->host_threads = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("RUNLAB_GPU_CHUNK_PX")) c->chunk_px = std::max(1ll, std::atoll(v));
+    if (const char* v = std::getenv("RUNLAB_GPU_BIG_PX")) c->big_single_px = std::max(1ll, std::atoll(v));
     return c;
 }
 

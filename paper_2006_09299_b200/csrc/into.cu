@@ -354,6 +354,7 @@ int submit_pack(rl_ctx* c, int sb, const uint8_t* pixels, int32_t w, int32_t h, 
         if (cudaMallocHost(&c->h_istage[sb], npx) != cudaSuccess) return set_err(c, RL_ENOMEM, "pinned alloc failed");
         c->h_istage_n[sb] = npx;
     }
+    if (tag < 0) return RL_OK;  // the caller submits the packing itself
     const int64_t rows = (int64_t)h * n;
     const int32_t rowb = (w + 7) / 8;
     const int parts = (int)std::min<int64_t>(std::max<int64_t>(1, rows / 128), 12);
@@ -377,22 +378,52 @@ int into_enqueue(rl_ctx* c, const uint8_t* pixels, int32_t w, int32_t h, int32_t
     const int32_t dfmt = pack_in ? RL_PIXELS_P4 : fmt;
     const size_t npx = (size_t)image_bytes(w, h, dfmt) * n;
     if (!ensure(c->pix, npx)) return set_err(c, RL_ENOMEM, "device allocation failed");
-    const uint8_t* src = pixels;
-    if (pack_in) {
-        if (!prepacked) {
-            if (const int rc = submit_pack(c, c->stage, pixels, w, h, n, pool, SYNC_IN_TAG)) return rc;
-            pool->wait(SYNC_IN_TAG);
-        }
-        src = c->h_istage[c->stage];
-    }
     if (!c->in_stream) {
         if (cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&c->in_done, cudaEventDisableTiming) != cudaSuccess)
             return cuda_fail(c, cudaGetLastError(), "copy stream");
     }
+    const uint8_t* src = pixels;
+    // one large image packed here: in row pieces, each copied as soon as it is packed (the pool
+    // packs the next pieces meanwhile); tags of the kids' input buffers are free in this mode
+    constexpr int NPIECE = 2 * rl_ctx::MAXKIDS;
+    const bool pieces = pack_in && !prepacked && (int64_t)h * n >= 8 * NPIECE;
+    if (pack_in) {
+        if (pieces) {
+            if (const int rc = submit_pack(c, c->stage, pixels, w, h, n, pool, -1)) return rc;  // staging only
+            const int64_t rows = (int64_t)h * n;
+            const int32_t rowb = (w + 7) / 8;
+            uint8_t* dst = c->h_istage[c->stage];
+            for (int k = 0; k < NPIECE; ++k) {
+                const int64_t p0 = rows * k / NPIECE, p1 = rows * (k + 1) / NPIECE;
+                const int parts = 3;  // the pool works on several pieces at once
+                for (int q = 0; q < parts; ++q) {
+                    const int64_t r0 = p0 + (p1 - p0) * q / parts, r1 = p0 + (p1 - p0) * (q + 1) / parts;
+                    pool->submit(in_tag(0, 0) + k,
+                                 [=] { pack_rows_p4(pixels + r0 * w, r1 - r0, w, dst + r0 * rowb, rowb); });
+                }
+            }
+        } else if (!prepacked) {
+            if (const int rc = submit_pack(c, c->stage, pixels, w, h, n, pool, SYNC_IN_TAG)) return rc;
+            pool->wait(SYNC_IN_TAG);
+        }
+        src = c->h_istage[c->stage];
+    }
     tl.hmark(tl.chunk, 3);
     tl.mark(0, c->in_stream);
-    const cudaError_t e = cudaMemcpyAsync(c->pix.p, src, npx, cudaMemcpyHostToDevice, c->in_stream);
+    cudaError_t e = cudaSuccess;
+    if (pieces) {
+        const int64_t rows = (int64_t)h * n;
+        const int32_t rowb = (w + 7) / 8;
+        for (int k = 0; k < NPIECE && e == cudaSuccess; ++k) {
+            const int64_t p0 = rows * k / NPIECE, p1 = rows * (k + 1) / NPIECE;
+            pool->wait(in_tag(0, 0) + k);
+            e = cudaMemcpyAsync(P<uint8_t>(c->pix) + p0 * rowb, src + p0 * rowb, (size_t)(p1 - p0) * rowb,
+                                cudaMemcpyHostToDevice, c->in_stream);
+        }
+    } else {
+        e = cudaMemcpyAsync(c->pix.p, src, npx, cudaMemcpyHostToDevice, c->in_stream);
+    }
     if (e != cudaSuccess) return cuda_fail(c, e, "copy in");
     cudaEventRecord(c->in_done, c->in_stream);
     cudaStreamWaitEvent(c->stream, c->in_done, 0);
@@ -585,11 +616,15 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     // nothing to overlap the host work with: plain copies are faster there (measured: config 3,
     // one 16.7 Mpx image, 7.3 -> 16.0 Gpx/s end to end; config 1, 1.25 -> 2.95).
     const bool multi = nch > 1;
-    const bool packed = multi && ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
+    // ... except a single image so large that its byte-per-pixel copies dominate (config 5: 1 GB
+    // each way over PCIe, 39 of 46 ms): its input is packed to P4 by the host pool before the
+    // copy and its filled image expanded after it (8x fewer bytes on the link)
+    const bool big1 = !multi && P * n >= ctx->big_single_px;
+    const bool packed = (multi || big1) && ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
     const int pack = multi && ctx->packed_recs ? ((out->comps ? 1 : 0) | (out->filled && out->filled_layout == 1 ? 2 : 0)) : 0;
     // u8 input crosses PCIe as P4 bits packed by the host pool one chunk ahead (a single chunk
     // would wait for its packing: plain copy)
-    const bool pack_in = multi && fmt == RL_PIXELS_U8 && ctx->packed_h2d;
+    const bool pack_in = (multi || big1) && fmt == RL_PIXELS_U8 && ctx->packed_h2d;
     const bool staged = packed || pack || pack_in;
     if (staged && !ctx->pool) {
         const int hw = (int)std::thread::hardware_concurrency();
@@ -600,11 +635,16 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     IntoState st;
     tl.begin(ctx->stream, nch);
     if (nch == 1) {
-        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed, pack, ctx->pool, false, false);
+        rc = into_enqueue(ctx, pixels, w, h, n, cfg, out, 0, fmt, packed, pack, ctx->pool, pack_in, false);
         if (!rc) rc = finish(ctx);
+        // the filled image's copy is done with the pipeline (finish), so host threads expand it
+        // while the component tables are still crossing (unless the pipeline re-ran: then
+        // into_post copies it again)
+        const bool early = !rc && packed && !ctx->reran;
+        if (early) expand_filled(ctx, ctx, 0, out, 0);
         if (!rc) rc = into_post(ctx, out, 0, st, ctx->pool, 0);
         if (!rc) rc = into_sync(ctx);
-        if (!rc && packed) expand_filled(ctx, ctx, 0, out, 0);
+        if (!rc && packed && !early) expand_filled(ctx, ctx, 0, out, 0);
         // host tasks of this call end before it returns (after a failed copy only if the
         // stream still completes, i.e. its callbacks run)
         if (staged && (!rc || into_sync(ctx) == RL_OK)) ctx->pool->wait(0);
