@@ -129,7 +129,7 @@ struct rl_ctx {
     // post-fill features of the survivors compacted into `fcomp` (rl_label_into layout 1)
     bool want_compact = false;
     int64_t chunk_px = 32ll << 20;  // rl_label_into: pixels per chunk (env RUNLAB_GPU_CHUNK_PX)
-    int64_t big_single_px = 64ll << 20;  // rl_label_into: one chunk this large crosses PCIe packed (env RUNLAB_GPU_BIG_PX)
+    int64_t big_single_px = 8ll << 20;  // rl_label_into: one chunk this large crosses PCIe packed (env RUNLAB_GPU_BIG_PX; measured: cfg3 16.7 Mpx 12 -> 17 Gpx/s, cfg1 1 Mpx slower)
     // rl_label_into pipelines large batches through these (own workspace and stream each)
     static constexpr int MAXKIDS = 8;
     int nkids = 3;  // env RUNLAB_GPU_KIDS

@@ -617,8 +617,10 @@ int rl_label_into_fmt(rl_ctx* ctx, const uint8_t* pixels, int32_t w, int32_t h, 
     // one 16.7 Mpx image, 7.3 -> 16.0 Gpx/s end to end; config 1, 1.25 -> 2.95).
     const bool multi = nch > 1;
     // ... except a single image so large that its byte-per-pixel copies dominate (config 5: 1 GB
-    // each way over PCIe, 39 of 46 ms): its input is packed to P4 by the host pool before the
-    // copy and its filled image expanded after it (8x fewer bytes on the link)
+    // each way over PCIe, 39 of 46 ms; >= 8 Mpx by default): its input is packed to P4 by the
+    // host pool in row pieces, each copied as soon as it is packed, and its filled image crosses
+    // as P4 and is expanded while the component tables cross (8x fewer bytes on the link:
+    // config 5 46 -> 25.6 ms, config 3 1.38 -> 0.97 ms)
     const bool big1 = !multi && P * n >= ctx->big_single_px;
     const bool packed = (multi || big1) && ctx->packed_d2h && out->filled_image && fmt == RL_PIXELS_U8;
     const int pack = multi && ctx->packed_recs ? ((out->comps ? 1 : 0) | (out->filled && out->filled_layout == 1 ? 2 : 0)) : 0;
