@@ -1057,6 +1057,9 @@ __device__ __forceinline__ int fold_slot(ES& E, uint32_t key) {
 }
 
 // Emits a tile iff it belongs to capacity class C (the class its analyze pass used).
+#ifndef RL_EMIT_TAIL_BARRIER
+#define RL_EMIT_TAIL_BARRIER 0  // 1: the barriers after the last chunk's deferred folds and before the filled image
+#endif
 template <class C>
 __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws& ws, const TileGeom& tg) {
     CclSmem<C>& S = E.c;
@@ -1331,7 +1334,12 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
             acc_atomic_fold_fill(ws.filled + cb + anc, s, (int64_t)E.fsx[k] + s * tg.x0,
                                  (int64_t)(E.fssy[k] >> 14) + s * tg.y0);
         }
-        __syncthreads();
+        // the next chunk clears the accumulators these folds read; after the last chunk nothing
+        // rewrites what they read (the persistent callers synchronise before the next tile)
+        if (!RL_EMIT_TAIL_BARRIER && l0 + C::FCH >= max(nlc, 1)) {
+        } else {
+            __syncthreads();
+        }
         RL_PHASE(tg.t, 22);
     }
     // flush border-keyed folds (the survivors were initialised by k_tops).  The targets are
@@ -1363,7 +1371,9 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     }
     nsurv = __reduce_add_sync(0xFFFFFFFFu, nsurv);
     if ((tid & 31) == 0 && nsurv) atomicAdd(&ws.img_surv[tg.b], (uint32_t)nsurv);
-    __syncthreads();  // the ext-mask atomics are complete
+    // no barrier here: the exterior masks the filled image needs are complete since the first
+    // feature chunk's barrier, and the persistent callers synchronise before the next tile
+    if (RL_EMIT_TAIL_BARRIER) __syncthreads();
     RL_PHASE(tg.t, 23);
 
     // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
