@@ -192,8 +192,10 @@ __device__ __forceinline__ uint32_t valid_mask(const TileGeom& tg, int r, int w)
     return (1u << vc) - 1u;
 }
 
-// Block-wide exclusive scan over BT threads; `wsum` is __shared__ int[BT / 32 + 1].
-template <int BT = NT>
+// Block-wide exclusive scan over BT threads; `wsum` is __shared__ int[BT / 32 + 1].  TRAIL =
+// false drops the closing barrier for callers that do not write `wsum` again before their next
+// barrier.
+template <int BT = NT, bool TRAIL = true>
 __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
     constexpr int NWP = BT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -219,7 +221,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int& total) {
     __syncthreads();
     total = wsum[NWP];
     const int r = wsum[warp] + incl - v;
-    __syncthreads();
+    if (TRAIL) __syncthreads();
     return r;
 }
 

@@ -272,7 +272,11 @@ __device__ __forceinline__ bool tile_runs(CclSmem<C>& S, WordBits& wb) {
         S.st[tid] = wb.st;
     }
     int total;
-    const int rb = block_excl_scan<C::BT>(__popc(wb.st), S.wsum, total);  // contains __syncthreads
+#ifndef RL_SCAN_TRAIL
+#define RL_SCAN_TRAIL 0
+#endif
+    // (the next write to S.wsum is the component scan, many barriers later)
+    const int rb = block_excl_scan<C::BT, RL_SCAN_TRAIL>(__popc(wb.st), S.wsum, total);  // contains __syncthreads
     wb.nruns = total;
     if (total > MR) return false;
     if (!word) return true;
@@ -533,7 +537,7 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
     int nlc, nb;
     {
         int tot;
-        const int pre = block_excl_scan<BT>(
+        const int pre = block_excl_scan<BT, RL_SCAN_TRAIL>(  // S.wsum is not written again in this tile
             tid < nblk ? (__popc(S.rmask[tid]) | (__popc(S.rbmask[tid]) << 16)) : 0, S.wsum, tot);
         if (tid < nblk) {
             S.rpre[tid] = (uint16_t)(pre & 0xFFFF);
