@@ -400,7 +400,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
     record_event(ctx->ev[0], s, use_graph);
     kt();
     launch_analyze(dpix, g, ws, s);
-    launches += 3;
+    launches += direct_call(g) ? 2 : 3;
     record_event(ctx->ev[1], s, use_graph);
     kt();
     launches += enqueue_seams(ctx, g, ws, s);
@@ -420,7 +420,7 @@ int enqueue(rl_ctx* ctx, const uint8_t* dpix, int32_t W, int32_t H, int32_t B, c
         launch_emit(g, ws, s, ctx->seam_stream, ctx->seam_fork, ctx->seam_join);
     else
         launch_emit(g, ws, s);
-    launches += 3 + (g.tpi >= 8192 ? 1 : 0);  // + the shard-table flush (kernels.cu FT_MIN_TILES)
+    launches += (direct_call(g) ? 2 : 3) + (g.tpi >= 8192 ? 1 : 0);  // + the shard-table flush (kernels.cu FT_MIN_TILES)
     kt();
     k_summary<<<(B + 1 + 127) / 128, 128, 0, s>>>(g, ws, P<uint64_t>(ctx->cbase), P<int64_t>(ctx->summ));
     ++launches;

@@ -18,6 +18,7 @@ size_t scan_state_bytes(int64_t n);
 void launch_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t init, void* state, cudaStream_t s,
                  bool zeroed = false);
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s);
+bool direct_call(const Geo& g);  // every tile straight to class M (one analyze and one emit launch less)
 void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaStream_t s, int sms);
 void launch_seam_cols(const Geo& g, const Ws& ws, cudaStream_t s, int sms);
 void launch_resolve(const Geo& g, const Ws& ws, cudaStream_t s, int sms, int64_t nodes_hint);

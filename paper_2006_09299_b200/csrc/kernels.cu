@@ -416,6 +416,19 @@ __global__ void __launch_bounds__(CapM::BT, 4) k_analyze_m(const uint8_t* __rest
     }
 }
 
+// calls with at most one wave of class-M CTAs: every tile goes straight to class M (no class-S
+// attempt and no class-S emit launch: the dense single images' critical path)
+__global__ void __launch_bounds__(CapM::BT, 4) k_analyze_m_direct(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& A = *reinterpret_cast<AnalyzeSmem<CapM>*>(smem_raw);
+    for (uint32_t k = blockIdx.x; k < (uint32_t)g.ntiles; k += gridDim.x) {
+        const TileGeom tg = tile_geom(g, (int32_t)k);
+        if (!analyze_tile<CapM, false>(A, pix, g, ws, tg) && threadIdx.x == 0)
+            ws.ovf2[atomicAdd(&ws.counters[4], 1u)] = (uint32_t)tg.t;
+        __syncthreads();
+    }
+}
+
 // class F over list B (one run per pixel fits)
 __global__ void __launch_bounds__(CapF::BT) k_analyze_full(const uint8_t* __restrict__ pix, Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1451,6 +1464,15 @@ __global__ void __launch_bounds__(CapME::BT, 4) k_emit_m(Geo g, Ws ws) {
     }
 }
 
+__global__ void __launch_bounds__(CapME::BT, 4) k_emit_m_direct(Geo g, Ws ws) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& E = *reinterpret_cast<EmitSmem<CapME>*>(smem_raw);
+    for (uint32_t k = blockIdx.x; k < (uint32_t)g.ntiles; k += gridDim.x) {
+        emit_tile(E, g, ws, tile_geom(g, (int32_t)k));
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(CapFE::BT) k_emit_full(Geo g, Ws ws) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto& E = *reinterpret_cast<EmitSmem<CapFE>*>(smem_raw);
@@ -1527,6 +1549,9 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
 // word phases and barriers).  (env RUNLAB_GPU_WIDE_TILES)
 static int64_t g_wide_tiles = 4096;
 static bool wide_call(const Geo& g) { return (int64_t)g.B * g.tpi <= g_wide_tiles; }
+// calls with at most one wave of class-M CTAs skip the class-S attempt (env RUNLAB_GPU_DIRECT_TILES)
+static int64_t g_direct_tiles = 148 * 4;
+bool direct_call(const Geo& g) { return !g.strip && (int64_t)g.B * g.tpi <= g_direct_tiles; }
 static bool g_cids_blk = true;  // wide calls: one block per tile in k_cids_blk (env RUNLAB_GPU_CIDS_BLK=0: off)
 
 cudaError_t configure_kernels() {
@@ -1536,6 +1561,9 @@ cudaError_t configure_kernels() {
     if (e == cudaSuccess) e = set_smem(k_emit, sizeof(EmitSmem<CapSE>));
     if (e == cudaSuccess) e = set_smem(k_emit_m, sizeof(EmitSmem<CapME>));
     if (e == cudaSuccess) e = set_smem(k_emit_full, sizeof(EmitSmem<CapFE>));
+    if (e == cudaSuccess) e = set_smem(k_analyze_m_direct, sizeof(AnalyzeSmem<CapM>));
+    if (e == cudaSuccess) e = set_smem(k_emit_m_direct, sizeof(EmitSmem<CapME>));
+    if (const char* v = std::getenv("RUNLAB_GPU_DIRECT_TILES")) g_direct_tiles = std::atoll(v);
     if (const char* v = std::getenv("RUNLAB_GPU_WIDE_TILES")) g_wide_tiles = std::atoll(v);
     if (const char* v = std::getenv("RUNLAB_GPU_CIDS_BLK")) g_cids_blk = std::atoi(v) != 0;
     return e;
@@ -1556,6 +1584,12 @@ void launch_seam_rows(const Geo& g, const Ws& ws, int32_t s0, int32_t ns, cudaSt
         k_seam_h<SEAM_T0><<<grid, SEAM_T0, 0, s>>>(g, ws, s0, ns);
 }
 void launch_analyze(const uint8_t* pix, const Geo& g, const Ws& ws, cudaStream_t s) {
+    if (direct_call(g)) {
+        k_analyze_m_direct<<<(unsigned)std::min<int64_t>((int64_t)g.B * g.tpi, 148 * 4), CapM::BT,
+                             sizeof(AnalyzeSmem<CapM>), s>>>(pix, g, ws);
+        k_analyze_full<<<148 * 2, CapF::BT, sizeof(AnalyzeSmem<CapF>), s>>>(pix, g, ws);
+        return;
+    }
     k_analyze<<<dim3(g.ntx, g.ty1 - g.ty0, g.B), NT, sizeof(AnalyzeSmem<CapS>), s>>>(pix, g, ws);
     // deferred heavier tiles: the grids loop over device-side lists (no host sync)
     k_analyze_m<<<148 * 4, CapM::BT, sizeof(AnalyzeSmem<CapM>), s>>>(pix, g, ws);
@@ -1608,6 +1642,13 @@ void launch_emit(const Geo& g, const Ws& ws0, cudaStream_t s, cudaStream_t s2, c
         cudaMemsetAsync(ws.ftsum, 0, (size_t)FT_SHARDS * FT_HS * 24, s);
     } else {
         ws.ftkey = nullptr;
+    }
+    if (direct_call(g)) {  // every tile was analysed in class M (or deferred to F)
+        k_emit_m_direct<<<(unsigned)std::min<int64_t>((int64_t)g.B * g.tpi, 148 * 4), CapME::BT,
+                          sizeof(EmitSmem<CapME>), s>>>(g, ws);
+        k_emit_full<<<148 * 2, CapFE::BT, sizeof(EmitSmem<CapFE>), s>>>(g, ws);
+        if (sharded) k_ftab_flush<<<FT_SHARDS * FT_HS / 256, 256, 0, s>>>(ws);
+        return;
     }
     const cudaStream_t sd = s2 ? s2 : s;
     if (s2) {
