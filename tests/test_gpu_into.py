@@ -213,3 +213,27 @@ def test_into_copy_variants(env):
         assert outs.h2d_bytes == want
     finally:
         lab.close()
+
+
+# one chunk of at least RUNLAB_GPU_BIG_PX pixels (8 Mi by default) crosses PCIe packed: the
+# input packed to P4 in row pieces copied as they are packed, the filled image expanded while
+# the component tables cross
+@pytest.mark.parametrize("shape", [(1, 2048, 4096), (2, 1500, 3000)])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_into_one_large_chunk(labeler, shape, layout):
+    n, h, w = shape
+    h_in = _batch(n, h, w, seed0=31)
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    ref = labeler.label_batch(h_in.numpy(), cfg)
+    for _ in range(2):
+        o, outs = _into(labeler, h_in, cfg, layout, _cap(ref))
+        _check(o, outs, ref, layout)
+        assert outs.h2d_bytes == n * h * ((w + 7) // 8)  # packed input
+
+
+def test_into_one_large_chunk_labels(labeler):
+    h_in = _batch(1, 2048, 4096, seed0=41)
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True, relabel=True)
+    ref = labeler.label_batch(h_in.numpy(), cfg)
+    o, outs = _into(labeler, h_in, cfg, 1, _cap(ref), labels=True)
+    _check(o, outs, ref, 1, labels=True)
