@@ -140,6 +140,110 @@ __device__ __forceinline__ void border_words(AnalyzeSmem<C>& A) {
     warp_flush(kb, vb);
 }
 
+// A tile whose valid pixels all have one value (uniform images, flat regions of any image) is
+// one component: one run per row, run 0 its root, border index 0, touching all four tile edges.
+// Its tables are written directly -- exactly what the general path below writes for it (map,
+// header, perimeter labels, node) -- without the tile CCL's scans and barriers.  xv = the
+// value in 8-connected-value space (pixel ^ flip).  No barrier inside (the caller returns).
+template <int BT>
+__device__ __forceinline__ void uniform_tile(const Geo& g, const Ws& ws, const TileGeom& tg, uint32_t xv) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int th = tg.th, tw = tg.tw;
+    const uint32_t fg = xv ^ (uint32_t)g.flip;
+    const uint16_t lab = (uint16_t)(fg << 15);  // (value << 15) | border index 0
+    if (tid < 32) {
+        // map and node allocations, issued by two lanes so that their latencies overlap
+        const MapLayout ML(th, 1);
+        unsigned long long off = 0;
+        uint32_t base = 0;
+        if (lane == 0) {
+            const unsigned long long need = (unsigned long long)ML.total;
+            off = atomicAdd(ws.rused, need);
+            if (off + need > ws.cap_rstore) atomicOr(ws.counters + 1, ERR_RSTORE_CAP);
+            ws.tmap[tg.t] = off;
+            if (off + need > ws.cap_rstore) off = ~0ull;
+        } else if (lane == 1) {
+            base = atomicAdd(&ws.counters[0], 1u);
+            if ((uint64_t)base + 1 > ws.cap_nodes) atomicOr(&ws.counters[1], ERR_NODE_CAP);
+            ws.tbase[tg.t] = base;
+            ws.tnb[tg.t] = 1u;
+        }
+        off = __shfl_sync(0xFFFFFFFFu, off, 0);
+        base = __shfl_sync(0xFFFFFFFFu, base, 1);
+        if (off != ~0ull) {
+            uint16_t* map = ws.rstore + off;
+            if (lane < th) map[lane] = 0;  // component of each run
+            if (lane == 0) {
+                map[ML.lcrun] = 0;  // first run of the component
+                map[ML.lcb] = 0;    // border index 0
+            }
+            // first run of each word: a row's run starts at its word 0
+            for (int k = lane; k <= NW; k += 32) {
+                const int rr = k / WPR;
+                map[ML.rbase + k] = (uint16_t)(rr >= th ? th : rr + (k % WPR ? 1 : 0));
+            }
+        }
+        if (lane == 0 && (uint64_t)base + 1 <= ws.cap_nodes) {
+            const bool frame = tg.ty == 0 || tg.x0 == 0 || tg.y0 + th == g.H || tg.x0 + tw == g.W;
+            NodeRec rec;
+            rec.tile = (uint32_t)tg.t;
+            rec.fr = 0;
+            rec.fc = 0;
+            rec.ibefore = 0;
+            rec.fg = (uint8_t)fg;
+            rec.pad = 0;
+            rec.leftkind = tg.x0 == 0 ? 2 : 1;
+            rec.left = 0;
+            const uint32_t node = (uint32_t)g.B + base;
+            const uint64_t key = (uint64_t)tg.y0 * (uint64_t)g.W + (uint64_t)tg.x0;
+            const int64_t s = (int64_t)th * tw;
+            Acc f;
+            f.s = s;
+            f.sx = (int64_t)th * (tw * (tw - 1) / 2) + s * tg.x0;
+            f.sy = (int64_t)tw * (th * (th - 1) / 2) + s * tg.y0;
+            f.row_min = tg.y0;
+            f.row_max = tg.y0 + th - 1;
+            f.col_min = tg.x0;
+            f.col_max = tg.x0 + tw - 1;
+            ws.nrec[node] = rec;
+            ws.nkey[node] = key;
+            ws.nmin[node] = key;
+            ws.nacc[node] = f;
+            ws.uf[node] = (!fg && frame) ? (uint32_t)tg.b : node;  // App. A R3
+        }
+    }
+    // tile header: th runs, one component, one border component; row tables
+    uint16_t* hdr = ws.thdr + (int64_t)tg.t * THDR;
+    if (tid == 32) {
+        hdr[0] = (uint16_t)th;
+        hdr[1] = 1;
+        hdr[2] = 1;
+        hdr[3] = 0;
+    }
+    if (tid >= 64 && tid <= 64 + TH) {
+        const int rr = tid - 64;
+        hdr[4 + rr] = (uint16_t)(rr < th ? 0 : 1);
+        hdr[4 + TH + 1 + rr] = (uint16_t)(rr < th ? 0 : 1);
+    }
+    // perimeter labels: top and bottom rows two pixels per 4-B store, then the side columns
+    uint16_t* const perim = ws.perim + (int64_t)tg.t * PERIM;
+    for (int q = tid; q < TW + 2 * TH; q += BT) {
+        if (q < TW) {
+            const bool bot = q >= TW / 2;
+            const int c = 2 * (q & (TW / 2 - 1));
+            uint32_t v = 0xFFFFFFFFu;
+            if (c < tw) v = (c + 1 < tw) ? ((uint32_t)lab | ((uint32_t)lab << 16)) : ((uint32_t)lab | 0xFFFF0000u);
+            reinterpret_cast<uint32_t*>(perim + (bot ? TW : 0))[c >> 1] = v;
+        } else {
+            const int q2 = q - TW;
+            const int pr = q2 >= TH ? q2 - TH : q2;
+            perim[2 * TW + q2] = pr < th ? lab : PERIM_NONE;
+        }
+    }
+    // no interior components in any row
+    if (tid >= 128 && tid < 128 + th) ws.cnt[((int64_t)tg.b * g.H + tg.y0 + (tid - 128)) * g.ntx + tg.tx] = 0u;
+}
+
 // Returns false when the tile exceeds the capacity class C (then nothing but the packed bits and
 // possibly a partial component map -- superseded by the next class's -- was written for it; the
 // caller defers it to the next class).
@@ -156,6 +260,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
     // ---- load 32 pixels (bytes) of this thread's word and pack them to bits (the deferred
     // classes reload the bits the class-S attempt packed)
     const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;
+    uint32_t xw = 0;
     if (word) {
         uint32_t x;
         if (RELOAD) {
@@ -181,6 +286,7 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         }
         S.x[tid] = x;
         S.vm[tid] = vm;
+        xw = x;
     }
     if (tg.tx == 0 && tg.ty == 0 && tid == 0) {
         // exterior node of image b
@@ -193,7 +299,15 @@ __device__ __forceinline__ bool analyze_tile(AnalyzeSmem<C>& A, const uint8_t* _
         ws.nanccid[e] = 0;
         ws.nrep[e] = 0;
     }
-    __syncthreads();
+    // (block reductions return 0/1, not the OR of the values)  words holding a 1 (value space):
+    // none = all 0; all valid words = possibly all 1, checked by a second reduction
+    const int nz = __syncthreads_count(xw != 0u);
+    int uni = nz == 0 ? 1 : 0;  // 1: every valid pixel 0, 2: every valid pixel 1
+    if (nz == tg.th * ((tg.tw + 31) >> 5)) uni = __syncthreads_and(xw == vm) ? 2 : 0;
+    if (uni) {  // one value: the tile is a single border component
+        uniform_tile<BT>(g, ws, tg, (uint32_t)(uni - 1));
+        return true;
+    }
 
     RL_PHASE(tg.t, 1);
     const MapOut mo{ws.rused, ws.rstore, ws.cap_rstore, ws.tmap, ws.counters + 1};
@@ -1069,6 +1183,34 @@ __device__ __forceinline__ int fold_slot(ES& E, uint32_t key) {
     return -1;
 }
 
+// one word of the hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
+__device__ __forceinline__ void emit_filled_word(const Geo& g, const Ws& ws, const TileGeom& tg, int r, int w,
+                                                 uint32_t vm, uint32_t fillbits) {
+    if (vm && g.ofmt == 1) {
+        uint8_t* row = ws.filled_img + tg.b * g.ofbytes + (tg.y0 + r - g.prow0) * (int64_t)g.orowb;
+        p4_store_word(row, g.orowb, (tg.x0 >> 5) + w, fillbits, g.ovec_ok);
+    } else if (vm) {
+        uint8_t* dst = ws.filled_img + tg.b * g.ofbytes + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
+        if (g.ovec_ok && vm == 0xFFFFFFFFu) {
+            uint4 o0, o1;
+            o0.x = nibble_to_bytes(fillbits & 0xF);
+            o0.y = nibble_to_bytes((fillbits >> 4) & 0xF);
+            o0.z = nibble_to_bytes((fillbits >> 8) & 0xF);
+            o0.w = nibble_to_bytes((fillbits >> 12) & 0xF);
+            o1.x = nibble_to_bytes((fillbits >> 16) & 0xF);
+            o1.y = nibble_to_bytes((fillbits >> 20) & 0xF);
+            o1.z = nibble_to_bytes((fillbits >> 24) & 0xF);
+            o1.w = nibble_to_bytes((fillbits >> 28) & 0xF);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            __stcs(d4, o0);
+            __stcs(d4 + 1, o1);
+        } else {
+            const int n = 32 - __clz(vm);
+            for (int j = 0; j < n; ++j) dst[j] = (uint8_t)((fillbits >> j) & 1u);
+        }
+    }
+}
+
 // Emits a tile iff it belongs to capacity class C (the class its analyze pass used).
 #ifndef RL_EMIT_TAIL_BARRIER
 #define RL_EMIT_TAIL_BARRIER 0  // 1: the barriers after the last chunk's deferred folds and before the filled image
@@ -1091,6 +1233,20 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     const int nruns_h = (int)(h01 & 0xFFFFu), nlc_h = (int)(h01 >> 16);
     if (nruns_h > C::MR || nlc_h > C::NLC || nb_h > C::NBC) return false;  // a larger class owns it
     const uint32_t vm = word ? valid_mask(tg, r, w) : 0u;
+    if (nlc_h == 1) {  // a uniform tile (uniform_tile): one border component, no interior records
+        if (ws.counters[1] || !comps_fit(g, ws)) return true;  // capacity overflow: re-run
+        const uint32_t node = (uint32_t)g.B + tb;
+        const uint32_t fl = ws.nrep[node];  // bit 1: the exterior
+        emit_filled_word(g, ws, tg, r, w, vm, (fl & 2u) ? 0u : vm);
+        if (g.label_mode && vm) {
+            const uint2 info = ws.ninfo[node];
+            const uint32_t v = g.label_mode == 2 ? ((fl & 2u) ? 0u : info.y) : info.x;
+            uint32_t* ldst = ws.labels + (int64_t)tg.b * g.P + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
+            const int n = 32 - __clz(vm);
+            for (int j = 0; j < n; ++j) ldst[j] = v;
+        }
+        return true;
+    }
     {
         // bits and run starts (the run positions and word bases come with the stored map)
         const uint32_t x = word ? __ldcs(ws.bits + (int64_t)tg.t * NW + tid) : 0u;
@@ -1390,30 +1546,7 @@ __device__ __forceinline__ bool emit_tile(EmitSmem<C>& E, const Geo& g, const Ws
     RL_PHASE(tg.t, 23);
 
     // ---- hole-filled image (App. A R9): pixel = 0 iff its component is the exterior
-    if (vm && g.ofmt == 1) {
-        uint8_t* row = ws.filled_img + tg.b * g.ofbytes + (tg.y0 + r - g.prow0) * (int64_t)g.orowb;
-        p4_store_word(row, g.orowb, (tg.x0 >> 5) + w, vm & ~E.ext[tid], g.ovec_ok);
-    } else if (vm) {
-        const uint32_t fillbits = vm & ~E.ext[tid];
-        uint8_t* dst = ws.filled_img + tg.b * g.ofbytes + (tg.y0 + r - g.prow0) * g.W + tg.x0 + 32 * w;
-        if (g.ovec_ok && vm == 0xFFFFFFFFu) {
-            uint4 o0, o1;
-            o0.x = nibble_to_bytes(fillbits & 0xF);
-            o0.y = nibble_to_bytes((fillbits >> 4) & 0xF);
-            o0.z = nibble_to_bytes((fillbits >> 8) & 0xF);
-            o0.w = nibble_to_bytes((fillbits >> 12) & 0xF);
-            o1.x = nibble_to_bytes((fillbits >> 16) & 0xF);
-            o1.y = nibble_to_bytes((fillbits >> 20) & 0xF);
-            o1.z = nibble_to_bytes((fillbits >> 24) & 0xF);
-            o1.w = nibble_to_bytes((fillbits >> 28) & 0xF);
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-            __stcs(d4, o0);
-            __stcs(d4 + 1, o1);
-        } else {
-            const int n = 32 - __clz(vm);
-            for (int j = 0; j < n; ++j) dst[j] = (uint8_t)((fillbits >> j) & 1u);
-        }
-    }
+    emit_filled_word(g, ws, tg, r, w, vm, vm & ~E.ext[tid]);
     // ---- optional label image (Alg. 4 relabel, canonical ids), one lane per run
     if (g.label_mode) {
         for (int i = tid; i < nruns; i += BT) {

@@ -376,14 +376,15 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
     const int my0 = incl - nev;  // offset of this lane's first event in the warp's sequence
     // first-contact parents of every word are in place; tiles whose contacts were all first
     // contacts (vertical stacks of equal runs, sparse tiles) skip the union phase
-    // bit 0: some thread has events; bit 1: some warp has more than one queue of them
-    const int evflags = __syncthreads_or((nev ? 1 : 0) | (wtot > C::EVC ? 2 : 0));
-    const int any_events = evflags & 1;
-    // class S with every warp's events in one queue: the warps fill their queues now (before the
-    // pre-flatten barrier) and after it all threads drain all queues together, so a warp with
-    // many events does not hold the others at the next barrier
+    // (a block reduction returns 0/1: whether a warp's events exceed its queue is read from the
+    // queue totals after the pre-flatten barrier)
+    const int any_events = __syncthreads_or(nev);
+    // class S: the warps fill their queues now (before the pre-flatten barrier) and after it all
+    // threads drain all queues together, so a warp with many events does not hold the others at
+    // the next barrier; a warp with more events than its queue holds stores the first EVC only,
+    // and then every warp drains its own queue in rounds instead
     constexpr bool kSharedDrain = C::BT == NW;
-    const bool shared_drain = kSharedDrain && evflags == 1;
+    const bool shared_drain = kSharedDrain && any_events;
     RL_PHASE(tg.t, 14);
     // The first-contact forest links every run to one in the row above, so a vertical stack
     // of runs is a chain as tall as the stack.  It is flattened before the unions so that their
@@ -392,11 +393,17 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
     // already written by another walker, both ancestors, so walks only get shorter.  (Row
     // groups with a barrier between them and pointer-jumping rounds were measured slower.)
     if (shared_drain) {
-        int o = my0;
-        const uint16_t wbase = (uint16_t)(tid << 7);
-        for (uint32_t e = ev; e; e &= e - 1u) S.evq[warp][o++] = (uint16_t)(wbase | (__ffs(e) - 1));
-        for (uint32_t e = d1; e; e &= e - 1u) S.evq[warp][o++] = (uint16_t)(wbase | (1u << 5) | (__ffs(e) - 1));
-        for (uint32_t e = d2; e; e &= e - 1u) S.evq[warp][o++] = (uint16_t)(wbase | (2u << 5) | (__ffs(e) - 1));
+        if (my0 < C::EVC) {
+            int o = my0;
+            const uint16_t wbase = (uint16_t)(tid << 7);
+            auto put = [&](uint32_t code) {
+                if (o < C::EVC) S.evq[warp][o] = (uint16_t)code;
+                ++o;
+            };
+            for (uint32_t e = ev; e; e &= e - 1u) put(wbase | (__ffs(e) - 1));
+            for (uint32_t e = d1; e; e &= e - 1u) put(wbase | (1u << 5) | (__ffs(e) - 1));
+            for (uint32_t e = d2; e; e &= e - 1u) put(wbase | (2u << 5) | (__ffs(e) - 1));
+        }
         if (lane == 0) S.qtot[warp] = wtot;
     }
     {
@@ -445,13 +452,20 @@ __device__ bool ccl_tile(CclSmem<C>& S, const TileGeom& tg, const MapOut& mo, Bo
         }
         sunion(S.par, ra, rb2);
     };
-    if (!any_events) {
-        // nothing to unite
-    } else if (shared_drain) {
-        int qoff[NWARPS + 1];
+    int qoff[NWARPS + 1];
+    bool queues_fit = true;
+    if (shared_drain) {
         qoff[0] = 0;
 #pragma unroll
-        for (int q = 0; q < NWARPS; ++q) qoff[q + 1] = qoff[q] + S.qtot[q];
+        for (int q = 0; q < NWARPS; ++q) {
+            const int n = S.qtot[q];
+            queues_fit &= n <= C::EVC;
+            qoff[q + 1] = qoff[q] + n;
+        }
+    }
+    if (!any_events) {
+        // nothing to unite
+    } else if (shared_drain && queues_fit) {
         for (int k = tid; k < qoff[NWARPS]; k += BT) {
             int q = 0, base = 0;
 #pragma unroll

@@ -51,6 +51,40 @@ def test_multi_tile(labeler, conn, w, h, d, g):
     _check_batch(labeler, img[None], conn, f"{w}x{h} d{d} g{g}")
 
 
+@pytest.mark.parametrize("conn", [0, 1])
+@pytest.mark.parametrize("w,h,d,g", [
+    (1000, 333, 0.5, 64), (777, 129, 0.3, 100), (2048, 256, 0.5, 256), (513, 97, 0.7, 40),
+    (1030, 200, 0.05, 16), (900, 300, 0.8, 120), (256, 32, 1.0, 1), (300, 40, 0.0, 1)])
+def test_flat_regions(labeler, conn, w, h, d, g):
+    """Uniform tiles (one value over the whole tile: the single-component fast path of the
+    analyze and emit passes) next to mixed ones, ragged edge tiles, flat holes filled."""
+    img = O.generate(w, h, d, g, 11 + w + g)
+    _check_batch(labeler, img[None], conn, f"{w}x{h} d{d} g{g}")
+
+
+@pytest.mark.parametrize("conn", [0, 1])
+def test_event_queue_rounds(labeler, conn):
+    """Sparse-class tiles (<= 2048 runs) whose 4-row warps each hold ~254 essential union
+    events -- rows [1010.., 1111.., 0101.., 0000..]: the all-1 row merges the singles above it,
+    the all-0 row the background singles above it -- more than a warp's event queue (192):
+    the shared drain must fall back to per-warp rounds (adjacent warps' queues would collide).
+    One call of 640 tiles, so that the tiles go through the sparse class first (calls of at most
+    one wave of dense-class CTAs go straight to the dense class)."""
+    W, H = 2048, 320
+    x = np.arange(W)
+    imgs = []
+    for bgval in (0, 1):
+        for groups in [(4,), (4, 8, 40, 44), (0, 4, 8, 100, 104, 108), (24, 28, 60, 92, 124), (28, 32, 284)]:
+            img = np.full((H, W), bgval, dtype=np.uint8)
+            for r in groups:
+                img[r] = (x % 2 == 0)
+                img[r + 1] = 1
+                img[r + 2] = (x % 2 == 1)
+                img[r + 3] = 0
+            imgs.append(img)
+    _check_batch(labeler, np.stack(imgs[:8]), conn, "event rounds")
+
+
 def test_batch_mixed(labeler):
     imgs = np.stack([O.generate(520, 96, d, g, 100 + i)
                      for i, (d, g) in enumerate([(0.1, 1), (0.5, 1), (0.9, 2), (0.5, 8), (0.0, 1), (1.0, 1)])])
