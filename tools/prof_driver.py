@@ -32,6 +32,7 @@ def main():
     from paper_2006_09299_b200.runlab import cfg2_cells, generate_device
 
     lab = Labeler(0)
+    lab.set_pipelines(1)  # phase events of one pipeline
     cfg = LabelingConfig(connectivity=Connectivity(args.conn), compute_features=True,
                          compute_euler=True, fill_holes=True)
     S = args.size
