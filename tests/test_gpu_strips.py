@@ -224,3 +224,36 @@ def test_native_strip_rows_and_errors(labelers):
     img = torch.zeros((64, 64), dtype=torch.uint8, device="cuda")
     with pytest.raises(Exception):
         label_strips_native(labelers[:3], [img.data_ptr()] * 3, 64, 64, LabelingConfig())
+
+
+@pytest.mark.parametrize("seed", range(1, 9))
+def test_strips_structured_fuzz(labelers, seed):
+    """Bands of adversarial row patterns (tools/fuzz_struct.py) cut into 2-6 strips at rows that
+    fall inside the bands (events, merge rows and checkerboards across the cuts), against the
+    oracle: every table, the filled image and the label image."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_struct as F
+    rng = np.random.default_rng(100 + seed)
+    W, H = int(rng.choice([2048, 1537, 700])), int(rng.choice([600, 333, 1000]))
+    img = F.image(rng, W, H)
+    conn = int(rng.integers(0, 2))
+    n = int(rng.integers(2, 7))
+    dev = torch.from_numpy(img).cuda()
+    cfg = LabelingConfig(connectivity=conn, compute_features=True, compute_euler=True, fill_holes=True,
+                         relabel=True)
+    got = _run(labelers, dev, W, H, n, cfg)
+    want = O.label_canonical(img, conn, want_labels=True)
+    label = f"seed {seed} {W}x{H} conn {conn} strips {n}"
+    assert got["n_components"] == want.n_components, label
+    assert got["n_fg"] == want.n_fg and got["n_holes"] == want.n_holes and got["euler"] == want.euler, label
+    assert got["n_survivors"] == want.n_survivors, label
+    bad = np.nonzero(got["comps"] != want.comps)[0]
+    assert bad.size == 0, f"{label}: comps differ at {bad[:10]}"
+    np.testing.assert_array_equal(got["top"], want.top, err_msg=label)
+    surv = want.top == np.arange(want.n_components, dtype=np.uint32)
+    assert got["filled"][surv].tobytes() == want.filled[surv].tobytes(), label
+    np.testing.assert_array_equal(got["filled_image"], want.filled_image, err_msg=label)
+    # with hole filling the label image holds post-fill roots (labeling.hpp:231-236)
+    np.testing.assert_array_equal(got["labels"], want.top[want.labels], err_msg=label)
