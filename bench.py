@@ -189,6 +189,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def arm_config(wl: "Workload", world: int) -> dict:
+    """The `config` object of a bench line -- the same for our arm and for --impl reference
+    (the reference arm runs on our arm's config): built from the workload and the rank count
+    alone, rank 0's share standing for the per-GPU figures."""
+    B = len(wl.local_specs(0, world))
+    px = B * wl.W * wl.H
+    return {"workload": wl.desc + ", fg8_bg4, features+Euler+tree+hole fill",
+            "images_per_gpu": B, "pixels_per_gpu": px,
+            "l2": "inputs > L2 (no flush)" if px > 126e6 else "inputs fit L2 (cfg1/cfg3 are launch-bound single images)",
+            "pipelines": PIPELINES,
+            "parallelism": (f"batch sharded by image x{world} (cost-balanced, no data-path "
+                            "collective)" if wl.shard and world > 1
+                            else f"replica per rank x{world}")}
+
+
 # ------------------------------------------------------------------------------ CPU side
 def cpu_threads() -> int:
     try:
@@ -237,10 +252,11 @@ def run_reference_arm(args, wl: Workload, rank: int) -> None:
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpixel/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "higher_is_better": True, "scaling": "strong" if (wl.shard and args.gpus > 1) else "weak",
+        "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (reference generator)",
-        "config": {"workload": wl.desc + ", fg8_bg4",
-                   "path": "label_image(features,euler) + label_image(fill,features,relabel) + binarize_labels"},
+        "config": arm_config(wl, max(1, args.gpus)),
+        "reference_path": "label_image(features,euler) + label_image(fill,features,relabel) + binarize_labels",
         "cpu_baseline": {"value": value, "unit": "Gpixel/s", "cores": threads, "kind": "reference",
                          "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -643,13 +659,7 @@ def main() -> None:
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (reference generator on device)",
-            "config": {"workload": wl.desc + ", fg8_bg4, features+Euler+tree+hole fill",
-                       "images_per_gpu": B, "pixels_per_gpu": px,
-                       "l2": "inputs > L2 (no flush)" if px > 126e6 else "inputs fit L2 (cfg1/cfg3 are launch-bound single images)",
-                       "pipelines": PIPELINES,
-                       "parallelism": (f"batch sharded by image x{world} (cost-balanced, no data-path "
-                                       "collective)" if wl.shard and world > 1
-                                       else f"replica per rank x{world}")},
+            "config": arm_config(wl, world),
             "parity": parity,
             "roofline": {"bound": "hbm", "kernel": dom[0] + " (+ deferred-class launches)", "achieved": dom_gbs,
                          "peak": peak, "unit": "GB/s", "frac": dom_gbs / peak, "traffic": traffic,
