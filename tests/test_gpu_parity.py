@@ -156,3 +156,22 @@ def test_structured_fuzz(labeler, seed):
     import fuzz_struct as F
     imgs, conn = F.batch(seed, big=seed % 3 != 0)
     _check_batch(labeler, imgs, conn, f"fuzz seed {seed}")
+
+
+@pytest.mark.parametrize("seed", range(1, 19))
+def test_shape_fuzz(labeler, seed):
+    """Long thin structures across many seams and tile corners (tools/fuzz_shapes.py: spirals,
+    serpentine combs, concentric rings, diagonal walks, corner pairs, mazes; alone, inverted,
+    salted or XOR-ed), at sizes on and around the tile grid, with and without hole filling."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_shapes as F
+    imgs, conn, relabel, fill = F.batch(seed)
+    cfg = LabelingConfig(connectivity=conn, relabel=relabel, fill_holes=fill, compute_features=True,
+                         compute_euler=True)
+    res = labeler.label_batch(imgs, cfg)
+    for i in range(imgs.shape[0]):
+        ref = O.label_canonical(imgs[i], conn, want_labels=relabel)
+        if relabel and fill:
+            ref.labels = ref.top[ref.labels]
+        compare_image(res.image(i), ref, f"shape fuzz seed {seed} #{i}")
