@@ -580,7 +580,9 @@ __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int
     __shared__ __align__(16) uint16_t rowu[TW], rowd[TW];
     __shared__ uint16_t leftu, leftd;
     static_assert(SEAM_T >= 2 * (TW / 8), "one 16-B load per thread stages both rows");
-    if (ws.counters[1]) return;
+    // the overflow flag is read together with the block's first loads (one round trip less per
+    // block than testing it first); nothing is written before it is tested
+    const uint32_t aborted = ws.counters[1];
     const uint32_t v8 = g.flip ? 0u : 1u;
     const int32_t tx = blockIdx.x, tid = threadIdx.x;
     // grid (tile column, seam, image): no division by the seam count per block
@@ -589,6 +591,8 @@ __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int
         const int32_t s = s0 + si;
         const int64_t tu = ((int64_t)b * g.nty + s) * g.ntx + tx, tl = tu + g.ntx;
         const int nbu = (int)ws.tnb[tu], nbd = (int)ws.tnb[tl];
+        // node bases of the two tiles, for the global links below: loaded now, with the rest
+        const uint32_t bu = (uint32_t)g.B + ws.tbase[tu], bd = (uint32_t)g.B + ws.tbase[tl];
         if (tid < TW / 8)
             reinterpret_cast<uint4*>(rowu)[tid] = reinterpret_cast<const uint4*>(ws.perim + tu * PERIM + TW)[tid];
         else if (tid < TW / 4)
@@ -597,6 +601,7 @@ __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int
             leftu = ws.perim[(tu - 1) * PERIM + TW + TW - 1];
             leftd = ws.perim[(tl - 1) * PERIM + TW - 1];
         }
+        if (aborted) return;
         for (int i = tid; i < nbu + nbd; i += SEAM_T) lp[i] = (uint32_t)i;
         __syncthreads();
         for (int c = tid; c < TW; c += SEAM_T) {
@@ -625,7 +630,6 @@ __global__ void __launch_bounds__(SEAM_T) k_seam_h(Geo g, Ws ws, int32_t s0, int
         }
         __syncthreads();
         // one global link per border component that joined another one here
-        const uint32_t bu = (uint32_t)g.B + ws.tbase[tu], bd = (uint32_t)g.B + ws.tbase[tl];
         for (int i = tid; i < nbu + nbd; i += SEAM_T) {
             uint32_t r = lp[i];
             if (r == (uint32_t)i) continue;
