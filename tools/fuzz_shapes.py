@@ -157,6 +157,15 @@ def image(rng, w: int, h: int) -> np.ndarray:
     return np.ascontiguousarray(img.astype(np.uint8))
 
 
+def large(seed: int):
+    """One image of 4-64 Mpixel: structures spanning thousands of tiles (union chains across the
+    whole seam graph, one component folding features from every tile)."""
+    rng = np.random.default_rng(1_000_000 + seed)
+    w = int(rng.choice([2048, 4096, 4097, 5000, 8192])) + int(rng.choice([0, 0, -1, 1, 37]))
+    h = int(rng.choice([2048, 3000, 4096, 8192])) + int(rng.choice([0, 0, -1, 1, 13]))
+    return image(rng, w, h)[None], int(rng.integers(0, 2)), bool(rng.integers(0, 2)), bool(rng.integers(0, 2))
+
+
 def batch(seed: int):
     rng = np.random.default_rng(seed)
     big = seed % 3 == 0
@@ -170,6 +179,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batches", type=int, default=60)
     ap.add_argument("--start", type=int, default=1)
+    ap.add_argument("--large", action="store_true", help="one 4-64 Mpixel image per seed")
     args = ap.parse_args()
     from oracle import oracle as O
     from paper_2006_09299_b200 import Labeler, LabelingConfig
@@ -178,7 +188,7 @@ def main():
     t0 = time.time()
     bad = n_img = 0
     for seed in range(args.start, args.start + args.batches):
-        imgs, conn, relabel, fill = batch(seed)
+        imgs, conn, relabel, fill = (large if args.large else batch)(seed)
         cfg = LabelingConfig(connectivity=conn, relabel=relabel, fill_holes=fill, compute_features=True,
                              compute_euler=True)
         res = lab.label_batch(imgs, cfg)
