@@ -175,3 +175,20 @@ def test_shape_fuzz(labeler, seed):
         if relabel and fill:
             ref.labels = ref.top[ref.labels]
         compare_image(res.image(i), ref, f"shape fuzz seed {seed} #{i}")
+
+
+@pytest.mark.parametrize("seed", [1, 2, 5])
+def test_shape_fuzz_large(labeler, seed):
+    """One 4-64 Mpixel shape image: structures spanning thousands of tiles (deep union chains
+    over the seam graph, one component folding features from every tile)."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_shapes as F
+    imgs, conn, relabel, fill = F.large(seed)
+    cfg = LabelingConfig(connectivity=conn, relabel=relabel, fill_holes=fill, compute_features=True,
+                         compute_euler=True)
+    res = labeler.label_batch(imgs, cfg)
+    ref = O.label_canonical(imgs[0], conn, want_labels=relabel)
+    if relabel and fill:
+        ref.labels = ref.top[ref.labels]
+    compare_image(res.image(0), ref, f"large shape seed {seed} {imgs.shape}")
