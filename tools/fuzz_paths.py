@@ -54,6 +54,8 @@ def main():
             print("MISMATCH", what, str(e)[:300], flush=True)
 
     for seed in range(args.start, args.start + args.seeds):
+        if (seed - args.start) % 500 == 0 and seed != args.start:
+            print(f"... {seed - args.start} done, {bad} mismatches, {time.time() - t0:.0f} s", flush=True)
         rng = np.random.default_rng(7_000_000 + seed)
         # --- strips
         W = int(rng.choice([255, 256, 257, 700, 1537, 2048, 2300]))

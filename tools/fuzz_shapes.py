@@ -188,6 +188,8 @@ def main():
     t0 = time.time()
     bad = n_img = 0
     for seed in range(args.start, args.start + args.batches):
+        if (seed - args.start) % 500 == 0 and seed != args.start:
+            print(f"... {seed - args.start} done, {bad} mismatches, {time.time() - t0:.0f} s", flush=True)
         imgs, conn, relabel, fill = (large if args.large else batch)(seed)
         cfg = LabelingConfig(connectivity=conn, relabel=relabel, fill_holes=fill, compute_features=True,
                              compute_euler=True)

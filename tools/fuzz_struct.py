@@ -93,6 +93,8 @@ def main():
     t0 = time.time()
     bad = n_img = 0
     for seed in range(args.start, args.start + args.batches):
+        if (seed - args.start) % 500 == 0 and seed != args.start:
+            print(f"... {seed - args.start} done, {bad} mismatches, {time.time() - t0:.0f} s", flush=True)
         imgs, conn = batch(seed, big=seed % 3 != 0)
         cfg = LabelingConfig(connectivity=conn, relabel=True)
         res = lab.label_batch(imgs, cfg)
