@@ -192,3 +192,19 @@ def test_shape_fuzz_large(labeler, seed):
     if relabel and fill:
         ref.labels = ref.top[ref.labels]
     compare_image(res.image(0), ref, f"large shape seed {seed} {imgs.shape}")
+
+
+@pytest.mark.parametrize("seed", range(500000, 500008))
+def test_shape_fuzz_densified_labels(labeler, seed):
+    """Densified label images of shape-fuzz batches, with and without hole filling, against a
+    flood fill of the (hole-filled) image (test_labeling.cpp:301-319)."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_shapes as F
+    imgs, conn, _, fill = F.batch(seed)
+    cfg = LabelingConfig(connectivity=conn, relabel=True, densify_labels=True, fill_holes=fill,
+                         compute_features=True, compute_euler=True)
+    res = labeler.label_batch(imgs, cfg)
+    for i in range(imgs.shape[0]):
+        _, comp, _ = O.flood_label(O.fill_holes(imgs[i], conn) if fill else imgs[i], conn)
+        assert np.array_equal(res.labels[i].astype(np.int32), comp), f"seed {seed} #{i} fill={fill}"

@@ -180,6 +180,9 @@ def main():
     ap.add_argument("--batches", type=int, default=60)
     ap.add_argument("--start", type=int, default=1)
     ap.add_argument("--large", action="store_true", help="one 4-64 Mpixel image per seed")
+    ap.add_argument("--densify", action="store_true",
+                    help="densified label images against a flood fill of the (hole-filled) image "
+                         "(test_labeling.cpp:301-319) instead of the canonical tables")
     args = ap.parse_args()
     from oracle import oracle as O
     from paper_2006_09299_b200 import Labeler, LabelingConfig
@@ -191,6 +194,18 @@ def main():
         if (seed - args.start) % 500 == 0 and seed != args.start:
             print(f"... {seed - args.start} done, {bad} mismatches, {time.time() - t0:.0f} s", flush=True)
         imgs, conn, relabel, fill = (large if args.large else batch)(seed)
+        if args.densify:
+            cfg = LabelingConfig(connectivity=conn, relabel=True, densify_labels=True, fill_holes=fill,
+                                 compute_features=True, compute_euler=True)
+            res = lab.label_batch(imgs, cfg)
+            for i in range(imgs.shape[0]):
+                n_img += 1
+                _, comp, _ = O.flood_label(O.fill_holes(imgs[i], conn) if fill else imgs[i], conn)
+                if not np.array_equal(res.labels[i].astype(np.int32), comp):
+                    bad += 1
+                    print(f"MISMATCH seed={seed} {imgs.shape} conn={conn} fill={fill} image {i}: densified labels "
+                          f"differ at {int((res.labels[i].astype(np.int32) != comp).sum())} pixels", flush=True)
+            continue
         cfg = LabelingConfig(connectivity=conn, relabel=relabel, fill_holes=fill, compute_features=True,
                              compute_euler=True)
         res = lab.label_batch(imgs, cfg)
