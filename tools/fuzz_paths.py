@@ -5,7 +5,9 @@
   multi-context rl_label_strips), every table / filled image / label image against the oracle;
 * rl_label_into: a batch through host buffers in small chunks (compact record slots, escape
   lists, P4 staging of the filled image and of the input), both layouts of the post-fill
-  features, against rl_label of the same batch (itself checked against the oracle).
+  features, against rl_label of the same batch (itself checked against the oracle);
+* filter_components on the device over the first image's tree (random, hole, small-foreground and
+  strided selections) against the oracle's restatement of the reference's filter.
 
   python tools/fuzz_paths.py --seeds 300
 """
@@ -96,6 +98,23 @@ def main():
             o, outs = _into(small, h_in, cfg2, layout, _cap(ref), labels=labels)
             _check(o, outs, ref, layout, labels=labels)
         attempt(f"into seed={seed} {imgs.shape} layout={layout} labels={labels}", into_case)
+
+        # --- filter_components on the device (analysis.hpp:89-125) over the first image's tree
+        def filter_case():
+            from paper_2006_09299_b200.runlab import filter_components
+            comps = ref.image(0)["comps"]
+            nc = comps.shape[0]
+            ids = np.arange(nc)
+            fg = (comps["flags"] & 1).astype(bool)
+            sels = [(rng.random(nc) < float(rng.choice([0.05, 0.3, 0.7, 0.95]))) & (ids > 0),
+                    (~fg) & (ids > 0), fg & (comps["s"] <= int(rng.integers(1, 40))),
+                    (ids % int(rng.integers(2, 5)) == 0) & (ids > 0)]
+            for k, sel in enumerate(sels):
+                got = filter_components(comps, sel)
+                want = O.filter_components(comps, sel)
+                for j, (a, b) in enumerate(zip(got, want)):
+                    assert a.tobytes() == b.tobytes(), f"selection {k} output {j} differs ({nc} components)"
+        attempt(f"filter seed={seed} {imgs.shape}", filter_case)
     print(f"{args.seeds} seeds, {bad} mismatches, {time.time() - t0:.0f} s", flush=True)
     sys.exit(1 if bad else 0)
 
