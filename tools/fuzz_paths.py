@@ -7,7 +7,8 @@
   lists, P4 staging of the filled image and of the input), both layouts of the post-fill
   features, against rl_label of the same batch (itself checked against the oracle);
 * filter_components on the device over the first image's tree (random, hole, small-foreground and
-  strided selections) against the oracle's restatement of the reference's filter.
+  strided selections) against the oracle's restatement of the reference's filter;
+* rl_fill_pbm: a P4 raster in, the hole-filled P4 raster out, against the oracle's filled image.
 
   python tools/fuzz_paths.py --seeds 300
 """
@@ -115,6 +116,17 @@ def main():
                 for j, (a, b) in enumerate(zip(got, want)):
                     assert a.tobytes() == b.tobytes(), f"selection {k} output {j} differs ({nc} components)"
         attempt(f"filter seed={seed} {imgs.shape}", filter_case)
+
+        # --- PBM P4 raster in, hole-filled P4 raster out (`runlab fill`, tools/runlab.cpp:128-137)
+        def pbm_case():
+            from paper_2006_09299_b200.runlab import pack_p4
+            im = imgs[int(rng.integers(0, nb))]
+            hdr = f"P4\n{w2} {h2}\n".encode()
+            got = small.fill_pbm(hdr + pack_p4(im).tobytes(), LabelingConfig(connectivity=conn, fill_holes=True))
+            filled = O.label_canonical(im, conn).filled_image
+            want = O.ref_write_pbm(filled) if O.ref_available() else hdr + pack_p4(filled).tobytes()
+            assert got == want, "filled PBM differs"
+        attempt(f"pbm seed={seed} {w2}x{h2} conn={conn}", pbm_case)
     print(f"{args.seeds} seeds, {bad} mismatches, {time.time() - t0:.0f} s", flush=True)
     sys.exit(1 if bad else 0)
 
