@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--batches", type=int, default=60)
     ap.add_argument("--start", type=int, default=1)
     ap.add_argument("--large", action="store_true", help="one 4-64 Mpixel image per seed")
+    ap.add_argument("--ref", action="store_true",
+                    help="check against the reference itself (oracle/_ref) instead of the C restatement")
     ap.add_argument("--densify", action="store_true",
                     help="densified label images against a flood fill of the (hole-filled) image "
                          "(test_labeling.cpp:301-319) instead of the canonical tables")
@@ -212,7 +214,7 @@ def main():
         for i in range(imgs.shape[0]):
             n_img += 1
             try:
-                want = O.label_canonical(imgs[i], conn, want_labels=relabel)
+                want = (O.ref_label_canonical if args.ref else O.label_canonical)(imgs[i], conn, want_labels=relabel)
                 if relabel and fill:  # the label image of a hole-filling call carries post-fill roots
                     want.labels = want.top[want.labels]
                 compare_image(res.image(i), want, f"seed={seed} {imgs.shape} conn={conn} fill={fill} image {i}")
