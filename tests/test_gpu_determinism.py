@@ -88,3 +88,44 @@ def test_split_pipelines_identical(labeler):
     assert len(set(digests)) == 1
     ref = O.label_canonical(imgs[5].cpu().numpy(), 0)
     compare_image(res.image(5), ref, "split #5")
+
+
+def test_concurrent_contexts_on_host_threads():
+    """One context per host thread (the reference allows distinct images to be
+    labeled concurrently): four threads label different batches at the same time,
+    through rl_label and through rl_label_into, each result bit-exact against the oracle."""
+    import threading
+
+    import torch
+    from oracle import oracle as O
+    from paper_2006_09299_b200 import Labeler, LabelingConfig
+    from tests.parity_util import compare_image
+    from tests.test_gpu_into import _cap, _check, _into
+
+    cfg = LabelingConfig(compute_features=True, compute_euler=True, fill_holes=True)
+    errors: list[str] = []
+
+    def work(k: int):
+        try:
+            lab = Labeler(0)
+            try:
+                for rep in range(3):
+                    imgs = np.stack([O.generate(700 + 13 * k, 300 + 7 * rep, 0.2 + 0.15 * k, 1 + (i + k) % 4,
+                                                1000 * k + 10 * rep + i) for i in range(6)])
+                    res = lab.label_batch(imgs, cfg)
+                    for i in range(imgs.shape[0]):
+                        compare_image(res.image(i), O.label_canonical(imgs[i], 0), f"thread {k} rep {rep} #{i}")
+                    h_in = torch.from_numpy(imgs).pin_memory()
+                    o, outs = _into(lab, h_in, cfg, rep % 2, _cap(res))
+                    _check(o, outs, res, rep % 2)
+            finally:
+                lab.close()
+        except Exception as e:  # noqa: BLE001 -- reported on the main thread
+            errors.append(f"thread {k}: {type(e).__name__}: {e}")
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
